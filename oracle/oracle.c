@@ -1,0 +1,415 @@
+/*
+ * oracle.c -- plain fp64 CPU oracle for the BLSTM training step.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code, header, table or constant with the CUDA path
+ * (paper_1608_00895_b200/csrc), and the CUDA path never calls it.
+ *
+ * What it computes:
+ *   - the LSTM layer of PAPER.md §4.2: "The non-recurrent part of
+ *     the LSTM forward computations are performed in a single matrix
+ *     multiplication for the whole mini-batch"; the recurrence with the gating
+ *     mechanism; back propagation through time, then the gradients "with
+ *     respect to the weights and the inputs".  Here everything is written as the
+ *     plain sequential definition (no blocking, no fusion): the pre-activation
+ *     of every frame is bias + x.W + h.R summed in ascending index order.
+ *   - LSTM variant (paper silent; reading R1 = SPEC S:171/S:193/S:241):
+ *     no peepholes, gate blocks [i | f | g | o] of W[D,4H], R[H,4H], b[4H].
+ *   - index tensor / mask (§5; reading R2): at a masked
+ *     frame the state (h, c) is carried unchanged and the output is 0; the
+ *     backward pass gives dA = 0 there and lets dh, dc pass through (R4).
+ *   - bidirectional stacking (reading A2/A3): Y_l = [fwd | bwd].
+ *   - softmax cross-entropy head, summed over valid frames, no
+ *     scaling of the gradient (§4.3, reading R7).
+ *   - SGD theta' = theta - lr*g (§4.3) and parameter averaging
+ *     theta = (1/N) sum_r theta_r (§4.1).
+ *
+ * Reductions run in ascending index order.  OpenMP (when compiled with
+ * -fopenmp) only splits independent batch rows / output elements, so the
+ * result is bitwise independent of the thread count.
+ *
+ * Pins: tests/test_oracle_pins.py (closed forms, worked examples W1/W2,
+ * torch.nn.LSTM float64 on packed sequences, central finite differences,
+ * direction duality, mask extension, sum semantics, DP algebra).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+static double sigm(double z)
+{
+    /* numerically stable logistic */
+    if (z >= 0.0) return 1.0 / (1.0 + exp(-z));
+    double e = exp(z);
+    return e / (1.0 + e);
+}
+
+int oracle_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/*
+ * One LSTM layer, one direction, forward.
+ *   x [T,B,D], mask [T,B], W [D,4H], R [H,4H], bias [4H], h0/c0 [B,H] or NULL.
+ * Outputs: y [T,B,H] (0 at masked frames), C [T,B,H] (cell state after frame t,
+ * carried at masked frames), hT/cT [B,H] (state after the whole scan, may be NULL),
+ * and the saved state the backward pass needs:
+ *   G [T,B,4H] gate activations (i,f,g,o), Hprev/Cprev [T,B,H] the state before frame t.
+ */
+int ref_lstm_fwd(int T, int B, int D, int H, int dir,
+                 const double *x, const uint8_t *mask,
+                 const double *W, const double *R, const double *bias,
+                 const double *h0, const double *c0,
+                 double *y, double *C, double *hT, double *cT,
+                 double *G, double *Hprev, double *Cprev)
+{
+    if (T < 0 || B < 1 || D < 0 || H < 1 || (dir != 1 && dir != -1)) return -1;
+    const int G4 = 4 * H;
+    double *h = (double *)calloc((size_t)B * H, sizeof(double));
+    double *c = (double *)calloc((size_t)B * H, sizeof(double));
+    if (!h || !c) { free(h); free(c); return -2; }
+    if (h0) memcpy(h, h0, sizeof(double) * B * H);
+    if (c0) memcpy(c, c0, sizeof(double) * B * H);
+
+    for (int s = 0; s < T; ++s) {
+        const int t = dir > 0 ? s : T - 1 - s;
+#pragma omp parallel for schedule(static)
+        for (int b = 0; b < B; ++b) {
+            const size_t fr = (size_t)t * B + b;
+            double *hb = h + (size_t)b * H, *cb = c + (size_t)b * H;
+            memcpy(Hprev + fr * H, hb, sizeof(double) * H);
+            memcpy(Cprev + fr * H, cb, sizeof(double) * H);
+            if (!mask[fr]) {
+                for (int j = 0; j < H; ++j) { y[fr * H + j] = 0.0; C[fr * H + j] = cb[j]; }
+                for (int n = 0; n < G4; ++n) G[fr * G4 + n] = 0.0;
+                continue;
+            }
+            double *a = (double *)malloc(sizeof(double) * G4);
+            for (int n = 0; n < G4; ++n) {
+                double acc = bias[n];
+                for (int d = 0; d < D; ++d) acc += x[fr * D + d] * W[(size_t)d * G4 + n];
+                for (int k = 0; k < H; ++k) acc += hb[k] * R[(size_t)k * G4 + n];
+                a[n] = acc;
+            }
+            for (int j = 0; j < H; ++j) {
+                const double i = sigm(a[j]);
+                const double f = sigm(a[H + j]);
+                const double g = tanh(a[2 * H + j]);
+                const double o = sigm(a[3 * H + j]);
+                const double cn = f * cb[j] + i * g;
+                const double hn = o * tanh(cn);
+                G[fr * G4 + j] = i;
+                G[fr * G4 + H + j] = f;
+                G[fr * G4 + 2 * H + j] = g;
+                G[fr * G4 + 3 * H + j] = o;
+                cb[j] = cn;
+                hb[j] = hn;
+                y[fr * H + j] = hn;
+                C[fr * H + j] = cn;
+            }
+            free(a);
+        }
+    }
+    if (hT) memcpy(hT, h, sizeof(double) * B * H);
+    if (cT) memcpy(cT, c, sizeof(double) * B * H);
+    free(h);
+    free(c);
+    return 0;
+}
+
+/*
+ * Backward through time (the
+ * recurrent part first, then the weight and input gradients).
+ *   dy [T,B,H] (ignored at masked frames), dhT/dcT [B,H] or NULL.
+ * Outputs: dx [T,B,D] overwritten (may be NULL), dW/dR/db accumulated (+=),
+ * dh0/dc0 [B,H] (may be NULL).  dA [T,B,4H] is scratch supplied by the caller
+ * (returned so tests can inspect it).
+ */
+int ref_lstm_bwd(int T, int B, int D, int H, int dir,
+                 const double *x, const uint8_t *mask,
+                 const double *W, const double *R,
+                 const double *C, const double *G, const double *Hprev, const double *Cprev,
+                 const double *dy, const double *dhT, const double *dcT,
+                 double *dx, double *dW, double *dR, double *db,
+                 double *dh0, double *dc0, double *dA)
+{
+    if (T < 0 || B < 1 || D < 0 || H < 1 || (dir != 1 && dir != -1)) return -1;
+    const int G4 = 4 * H;
+    double *dh = (double *)calloc((size_t)B * H, sizeof(double));
+    double *dc = (double *)calloc((size_t)B * H, sizeof(double));
+    if (!dh || !dc) { free(dh); free(dc); return -2; }
+    if (dhT) memcpy(dh, dhT, sizeof(double) * B * H);
+    if (dcT) memcpy(dc, dcT, sizeof(double) * B * H);
+
+    for (int s = T - 1; s >= 0; --s) {
+        const int t = dir > 0 ? s : T - 1 - s;
+#pragma omp parallel for schedule(static)
+        for (int b = 0; b < B; ++b) {
+            const size_t fr = (size_t)t * B + b;
+            double *dab = dA + fr * G4;
+            if (!mask[fr]) {
+                for (int n = 0; n < G4; ++n) dab[n] = 0.0;
+                continue; /* dh, dc pass through unchanged */
+            }
+            double *dhb = dh + (size_t)b * H, *dcb = dc + (size_t)b * H;
+            for (int j = 0; j < H; ++j) {
+                const double i = G[fr * G4 + j];
+                const double f = G[fr * G4 + H + j];
+                const double g = G[fr * G4 + 2 * H + j];
+                const double o = G[fr * G4 + 3 * H + j];
+                const double th = tanh(C[fr * H + j]);
+                const double dH = dhb[j] + dy[fr * H + j];
+                const double dC = dcb[j] + dH * o * (1.0 - th * th);
+                dab[j] = dC * g * i * (1.0 - i);
+                dab[H + j] = dC * Cprev[fr * H + j] * f * (1.0 - f);
+                dab[2 * H + j] = dC * i * (1.0 - g * g);
+                dab[3 * H + j] = dH * th * o * (1.0 - o);
+                dcb[j] = dC * f;
+            }
+            for (int k = 0; k < H; ++k) {
+                double acc = 0.0;
+                for (int n = 0; n < G4; ++n) acc += dab[n] * R[(size_t)k * G4 + n];
+                dhb[k] = acc;
+            }
+        }
+    }
+    const size_t TB = (size_t)T * B;
+    /* dW[d][n] += sum_{t,b} x[t,b,d] dA[t,b,n]  (ascending t, b) */
+#pragma omp parallel for schedule(static)
+    for (int d = 0; d < D; ++d)
+        for (int n = 0; n < G4; ++n) {
+            double acc = 0.0;
+            for (size_t r = 0; r < TB; ++r) acc += x[r * D + d] * dA[r * G4 + n];
+            dW[(size_t)d * G4 + n] += acc;
+        }
+    /* dR[k][n] += sum_{t,b} Hprev[t,b,k] dA[t,b,n] */
+#pragma omp parallel for schedule(static)
+    for (int k = 0; k < H; ++k)
+        for (int n = 0; n < G4; ++n) {
+            double acc = 0.0;
+            for (size_t r = 0; r < TB; ++r) acc += Hprev[r * H + k] * dA[r * G4 + n];
+            dR[(size_t)k * G4 + n] += acc;
+        }
+    for (int n = 0; n < G4; ++n) {
+        double acc = 0.0;
+        for (size_t r = 0; r < TB; ++r) acc += dA[r * G4 + n];
+        db[n] += acc;
+    }
+    /* dx[t,b,d] = sum_n dA[t,b,n] W[d][n] */
+    if (dx) {
+#pragma omp parallel for schedule(static)
+        for (long r = 0; r < (long)TB; ++r)
+            for (int d = 0; d < D; ++d) {
+                double acc = 0.0;
+                for (int n = 0; n < G4; ++n) acc += dA[(size_t)r * G4 + n] * W[(size_t)d * G4 + n];
+                dx[(size_t)r * D + d] = acc;
+            }
+    }
+    if (dh0) memcpy(dh0, dh, sizeof(double) * B * H);
+    if (dc0) memcpy(dc0, dc, sizeof(double) * B * H);
+    free(dh);
+    free(dc);
+    return 0;
+}
+
+/*
+ * Flat parameter layout (interface contract stated in include/blstm.h; the
+ * oracle computes it on its own): for l = 0..L-1, for d in (fwd, bwd):
+ * W [D_l,4H], R [H,4H], b [4H]; then W_out [2H,K], b_out [K] when K > 0.
+ * D_0 = D, D_l = 2H for l >= 1.  Returns the count; fills offs (6L+2 entries).
+ */
+long ref_param_layout(int L, int D, int H, int K, long *offs)
+{
+    long o = 0;
+    for (int l = 0; l < L; ++l) {
+        const long Dl = l == 0 ? D : 2L * H;
+        for (int d = 0; d < 2; ++d) {
+            const int e = 6 * l + 3 * d;
+            if (offs) { offs[e] = o; offs[e + 1] = o + Dl * 4 * H; offs[e + 2] = o + Dl * 4 * H + 4L * H * H; }
+            o += Dl * 4 * H + 4L * H * H + 4L * H;
+        }
+    }
+    if (offs) { offs[6 * L] = o; offs[6 * L + 1] = o + (K > 0 ? 2L * H * K : 0); }
+    if (K > 0) o += 2L * H * K + K;
+    return o;
+}
+
+/*
+ * One BLSTM training step: forward through L
+ * bidirectional layers, softmax-CE head summed over valid frames (or, when
+ * K == 0, the caller's dy_top [T,B,2H] as the gradient of the top output),
+ * backward through time, gradients written to grad (overwritten, flat layout).
+ * Optional outputs: Ys [L,T,B,2H] per-layer outputs, Cs [L,2,T,B,H] cell
+ * states, dX1 [T,B,D] gradient of the input, theta_new = theta - lr*grad.
+ * loss / frame_errors may be NULL.
+ */
+int ref_blstm_step(int L, int D, int H, int K, int T, int B,
+                   const double *theta, const double *x, const uint8_t *mask,
+                   const int32_t *labels, const double *dy_top,
+                   double lr, double *loss, long *frame_errors,
+                   double *grad, double *Ys, double *Cs, double *dX1,
+                   double *theta_new)
+{
+    if (L < 1 || B < 1 || H < 1 || T < 0) return -1;
+    const size_t TB = (size_t)T * B, W2 = 2 * (size_t)H;
+    long *offs = (long *)malloc(sizeof(long) * (6 * L + 2));
+    const long P = ref_param_layout(L, D, H, K, offs);
+    memset(grad, 0, sizeof(double) * P);
+
+    /* per-layer, per-direction saved state */
+    double **Xin = (double **)calloc(L + 1, sizeof(double *));
+    double **sv = (double **)calloc(8 * L, sizeof(double *)); /* y,C,G,Hp,Cp per dir */
+    Xin[0] = (double *)x;
+    for (int l = 0; l < L; ++l) {
+        const int Dl = l == 0 ? D : 2 * H;
+        double *Y = (double *)malloc(sizeof(double) * TB * W2);
+        for (int d = 0; d < 2; ++d) {
+            const int e = 6 * l + 3 * d;
+            double *y = (double *)malloc(sizeof(double) * TB * H);
+            double *C = (double *)malloc(sizeof(double) * TB * H);
+            double *Gs = (double *)malloc(sizeof(double) * TB * 4 * H);
+            double *Hp = (double *)malloc(sizeof(double) * TB * H);
+            double *Cp = (double *)malloc(sizeof(double) * TB * H);
+            ref_lstm_fwd(T, B, Dl, H, d == 0 ? 1 : -1, Xin[l], mask,
+                         theta + offs[e], theta + offs[e + 1], theta + offs[e + 2],
+                         NULL, NULL, y, C, NULL, NULL, Gs, Hp, Cp);
+            for (size_t r = 0; r < TB; ++r)
+                for (int j = 0; j < H; ++j) Y[r * W2 + (size_t)d * H + j] = y[r * H + j];
+            if (Cs) memcpy(Cs + ((size_t)(2 * l + d)) * TB * H, C, sizeof(double) * TB * H);
+            double **p = sv + 8 * l + 4 * d;
+            p[0] = C; p[1] = Gs; p[2] = Hp; p[3] = Cp;
+            free(y);
+        }
+        if (Ys) memcpy(Ys + (size_t)l * TB * W2, Y, sizeof(double) * TB * W2);
+        Xin[l + 1] = Y;
+    }
+
+    /* head (summed, unscaled P:253-254) */
+    double *dY = (double *)calloc(TB * W2, sizeof(double));
+    double lsum = 0.0;
+    long ferr = 0;
+    if (K > 0) {
+        const double *Wo = theta + offs[6 * L], *bo = theta + offs[6 * L + 1];
+        double *gWo = grad + offs[6 * L], *gbo = grad + offs[6 * L + 1];
+        double *dlog = (double *)calloc(TB * (size_t)K, sizeof(double));
+        double *rl = (double *)calloc(TB, sizeof(double));
+        long *re = (long *)calloc(TB, sizeof(long));
+        const double *YL = Xin[L];
+#pragma omp parallel for schedule(static)
+        for (long r = 0; r < (long)TB; ++r) {
+            if (!mask[r]) continue;
+            double *lg = dlog + (size_t)r * K;
+            for (int k = 0; k < K; ++k) {
+                double acc = bo[k];
+                for (size_t j = 0; j < W2; ++j) acc += YL[(size_t)r * W2 + j] * Wo[j * K + k];
+                lg[k] = acc;
+            }
+            int am = 0;
+            double m = lg[0];
+            for (int k = 1; k < K; ++k) if (lg[k] > m) { m = lg[k]; am = k; } /* ties: lowest index */
+            double se = 0.0;
+            for (int k = 0; k < K; ++k) se += exp(lg[k] - m);
+            const double lse = m + log(se);
+            const int lab = labels[r];
+            rl[r] = lse - lg[lab];
+            re[r] = (am != lab);
+            for (int k = 0; k < K; ++k) lg[k] = exp(lg[k] - lse);
+            lg[lab] -= 1.0;
+        }
+        for (size_t r = 0; r < TB; ++r) { lsum += rl[r]; ferr += re[r]; }
+        /* dW_out[j][k] = sum_r Y[r][j] dlog[r][k]; db_out[k] = sum_r dlog[r][k] */
+#pragma omp parallel for schedule(static)
+        for (long j = 0; j < (long)W2; ++j)
+            for (int k = 0; k < K; ++k) {
+                double acc = 0.0;
+                for (size_t r = 0; r < TB; ++r) acc += YL[r * W2 + j] * dlog[r * K + k];
+                gWo[(size_t)j * K + k] += acc;
+            }
+        for (int k = 0; k < K; ++k) {
+            double acc = 0.0;
+            for (size_t r = 0; r < TB; ++r) acc += dlog[r * K + k];
+            gbo[k] += acc;
+        }
+        /* dY[r][j] = sum_k dlog[r][k] W_out[j][k] */
+#pragma omp parallel for schedule(static)
+        for (long r = 0; r < (long)TB; ++r)
+            for (size_t j = 0; j < W2; ++j) {
+                double acc = 0.0;
+                for (int k = 0; k < K; ++k) acc += dlog[(size_t)r * K + k] * Wo[j * K + k];
+                dY[(size_t)r * W2 + j] = acc;
+            }
+        free(dlog); free(rl); free(re);
+    } else {
+        memcpy(dY, dy_top, sizeof(double) * TB * W2);
+    }
+
+    /* backward through the stack, l = L-1 .. 0 */
+    double *dyd = (double *)malloc(sizeof(double) * TB * H);
+    for (int l = L - 1; l >= 0; --l) {
+        const int Dl = l == 0 ? D : 2 * H;
+        double *dXl = (double *)calloc(TB * (size_t)Dl, sizeof(double));
+        double *dxd = (double *)malloc(sizeof(double) * TB * Dl);
+        double *dA = (double *)malloc(sizeof(double) * TB * 4 * H);
+        for (int d = 0; d < 2; ++d) {
+            const int e = 6 * l + 3 * d;
+            double **p = sv + 8 * l + 4 * d;
+            for (size_t r = 0; r < TB; ++r)
+                for (int j = 0; j < H; ++j) dyd[r * H + j] = dY[r * W2 + (size_t)d * H + j];
+            ref_lstm_bwd(T, B, Dl, H, d == 0 ? 1 : -1, Xin[l], mask,
+                         theta + offs[e], theta + offs[e + 1],
+                         p[0], p[1], p[2], p[3], dyd, NULL, NULL,
+                         dxd, grad + offs[e], grad + offs[e + 1], grad + offs[e + 2],
+                         NULL, NULL, dA);
+            for (size_t i = 0; i < TB * (size_t)Dl; ++i) dXl[i] += dxd[i];
+        }
+        free(dxd); free(dA);
+        if (l == 0) {
+            if (dX1) memcpy(dX1, dXl, sizeof(double) * TB * D);
+            free(dXl);
+        } else {
+            free(dY);
+            dY = dXl; /* [T,B,2H] = gradient of Y_{l-1} */
+        }
+    }
+    free(dyd);
+    free(dY);
+    if (loss) *loss = lsum;
+    if (frame_errors) *frame_errors = ferr;
+    if (theta_new)
+        for (long i = 0; i < P; ++i) theta_new[i] = theta[i] - lr * grad[i];
+
+    for (int l = 0; l < L; ++l) {
+        free(Xin[l + 1]);
+        for (int d = 0; d < 2; ++d)
+            for (int q = 0; q < 4; ++q) free(sv[8 * l + 4 * d + q]);
+    }
+    free(Xin); free(sv); free(offs);
+    return 0;
+}
+
+/* SGD (§4.3): theta -= lr * grad, gradients unscaled. */
+void ref_sgd(double *theta, const double *grad, long n, double lr)
+{
+    for (long i = 0; i < n; ++i) theta[i] -= lr * grad[i];
+}
+
+/* Parameter averaging (§4.1): out = (1/N) sum_r theta_r,
+ * thetas laid out [N][n], summed in ascending rank order. */
+void ref_dp_average(int nranks, long n, const double *thetas, double *out)
+{
+    for (long i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int r = 0; r < nranks; ++r) acc += thetas[(size_t)r * n + i];
+        out[i] = acc / nranks;
+    }
+}
