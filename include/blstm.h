@@ -1,0 +1,196 @@
+/*
+ * blstm.h -- C-ABI of libblstm.so, the B200 (sm_100a) fused BLSTM training hot
+ * path of RETURNN (arXiv:1608.00895).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section given), S:n =
+ * SPEC.md line n.  The operation each entry point computes is defined by the
+ * paper passage cited beside it and made exact by DESIGN.md §2 (the readings
+ * R1..R18 of the paper's silent points).
+ *
+ * Conventions for every call:
+ *   - Tensors are row-major and time-major: a sequence tensor is [T, B, F]
+ *     (§5: "time ... as first, the batch index as second and
+ *     the layer output size as third dimension").  Floating tensors are fp32.
+ *   - The mask is the paper's index tensor: uint8 [T, B], 1 = real
+ *     frame, 0 = padding.  Any 0/1 pattern is accepted (nonzero reads as 1).  At
+ *     a masked frame the LSTM state (h, c) is carried unchanged, the output is 0
+ *     and the backward pass emits zero gate gradient (R2/R4).
+ *   - LSTM variant (paper silent, R1): no peepholes, gate blocks
+ *     [i | f | g | o]; W [D, 4H], R [H, 4H], b [4H];
+ *       a = x W + h_{t-1} R + b,  i,f,o = sigmoid, g = tanh,
+ *       c_t = f c_{t-1} + i g,  h_t = o tanh(c_t).
+ *   - Pointers marked DEVICE are CUDA device pointers; streams are cudaStream_t
+ *     passed as void*.  The caller owns every buffer.  The library never
+ *     allocates device memory on the hot path and keeps no pointer after a call
+ *     returns (the dp_comm handle excepted).  Calls are asynchronous on the
+ *     given stream; an error detected by a kernel surfaces as BLSTM_ERR_CUDA on a
+ *     later call.
+ *   - Return 0 (BLSTM_OK) on success, < 0 on error; the text of the last error
+ *     of the calling thread is returned by blstm_last_error().  No exception or
+ *     abort crosses the ABI.  All argument checks happen before any launch.
+ *   - Gradients are SUMS over valid frames (§4.3: "batches
+ *     gradients are not scaled"); parameter gradients accumulate (+=).
+ *   - Arithmetic: fp16 tensor-core operands with round-to-nearest, fp32
+ *     accumulation, fp32 gate math and state (R9/R10).
+ *   - Results are bitwise reproducible for fixed inputs, shapes and device
+ *     (no floating-point atomics).
+ */
+#ifndef BLSTM_H
+#define BLSTM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BLSTM_OK = 0,
+    BLSTM_ERR_ARG = -1,         /* null / out-of-range argument */
+    BLSTM_ERR_SHAPE = -2,       /* inconsistent sizes or strides */
+    BLSTM_ERR_ALIGN = -3,       /* pointer not 16-byte aligned */
+    BLSTM_ERR_WORKSPACE = -4,   /* workspace / reserve too small */
+    BLSTM_ERR_CUDA = -5,        /* CUDA runtime or launch error */
+    BLSTM_ERR_UNSUPPORTED = -6, /* size beyond the kernels' on-chip capacity; never a silent fallback */
+    BLSTM_ERR_NCCL = -7         /* NCCL error */
+} blstm_status;
+
+/* Text of the last error on this thread (valid until the next call on this thread). */
+const char *blstm_last_error(void);
+/* ABI version (major*100 + minor). */
+int blstm_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* One LSTM layer, one direction: PAPER.md §4.2 P:232-236.                   */
+/* ------------------------------------------------------------------------ */
+enum { BLSTM_NO_DX = 4, BLSTM_ACCUM_DX = 2 };
+enum { BLSTM_PREC_FP16 = 0 };
+
+typedef struct {
+    int T, B, D, H;   /* frames, batch, input width, hidden units; T >= 0, B, D, H >= 1 */
+    int direction;    /* +1: scan t = 0..T-1; -1: scan t = T-1..0 (each sequence then starts at its
+                         own last valid frame) */
+    int ldx, ldy;     /* row strides (elements) of x/dx and of y/dy; ldx >= D, ldy >= H.  A BLSTM
+                         direction writes its half of [T,B,2H] with ldy = 2H. */
+    int flags;        /* BLSTM_NO_DX / BLSTM_ACCUM_DX (lstm_bwd only) */
+    int precision;    /* BLSTM_PREC_FP16 */
+} lstm_desc;
+
+/* Scratch bytes for one lstm_fwd / lstm_bwd call. */
+size_t lstm_workspace_bytes(const lstm_desc *d);
+/* Bytes of saved forward state (gate activations, h history); the reserve must
+ * live unchanged from lstm_fwd to the matching lstm_bwd ("reuse memory"). */
+size_t lstm_reserve_bytes(const lstm_desc *d);
+
+/*
+ * Forward: "the non-recurrent part ... in a single matrix
+ * multiplication for the whole mini-batch", then the recurrence with the gating
+ * fused into the recurrent matmul's epilogue.
+ *   x  [T,B,ldx] DEVICE, mask [T,B] DEVICE, W [D,4H], R [H,4H], b [4H] DEVICE
+ *   h0, c0 [B,H] DEVICE or NULL (= 0)
+ *   y  [T,B,ldy] DEVICE out (0 at masked frames), c [T,B,H] DEVICE out (cell state
+ *   after frame t, carried at masked frames), hT, cT [B,H] DEVICE out or NULL
+ *   (state after the whole scan).  reserve: lstm_reserve_bytes, workspace:
+ *   lstm_workspace_bytes, both DEVICE, 256-byte aligned.
+ */
+int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask, const float *W, const float *R,
+             const float *b, const float *h0, const float *c0, float *y, float *c, float *hT, float *cT,
+             void *reserve, void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Backward through time (the recurrent part is back
+ * propagated first, then the weight and input gradients are single matrix
+ * multiplications).  Same x, mask, W, R, h0, c0 and the c / reserve written by
+ * lstm_fwd.  dy [T,B,ldy] (ignored where mask = 0), dhT, dcT [B,H] or NULL.
+ *   dx [T,B,ldx]: overwritten, or += with BLSTM_ACCUM_DX, untouched with BLSTM_NO_DX
+ *   dW [D,4H], dR [H,4H], db [4H]: accumulated (+=)
+ *   dh0, dc0 [B,H] or NULL: gradient w.r.t. h0, c0 (overwritten)
+ */
+int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask, const float *W, const float *R,
+             const float *h0, const float *c0, const float *c, const void *reserve, const float *dy,
+             const float *dhT, const float *dcT, float *dx, float *dW, float *dR, float *db, float *dh0,
+             float *dc0, void *workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Deep bidirectional stack + softmax-CE head: one training step's fwd+BPTT.  */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int L, D, H;  /* layers, input width, units per direction */
+    int K;        /* classes of the softmax-CE head; 0 = no head, dy_top drives BPTT */
+    int T, B;     /* frames, batch (chunks) */
+    int flags;    /* reserved, 0 */
+    int precision;/* BLSTM_PREC_FP16 */
+} blstm_stack_desc;
+
+/*
+ * Flat parameter vector theta (fp32) and its gradient share one layout (the
+ * paper's "image of the current network parameters"):
+ *   for l = 0..L-1, for dir in (forward, backward):  W [D_l,4H], R [H,4H], b [4H]
+ *   then, if K > 0:  W_out [2H,K], b_out [K]
+ * with D_0 = D and D_l = 2H (input of layer l+1 = [y_fwd | y_bwd]).
+ * blstm_param_offsets fills 6L+2 element offsets: offs[6l+3d+{0,1,2}] = W, R, b of
+ * (l, d); offs[6L], offs[6L+1] = W_out, b_out.  Returns the element count.
+ */
+size_t blstm_param_count(const blstm_stack_desc *d);
+size_t blstm_param_offsets(const blstm_stack_desc *d, size_t *offs);
+size_t blstm_stack_workspace_bytes(const blstm_stack_desc *d);
+
+typedef struct dp_comm dp_comm;
+
+/*
+ * One step's forward + BPTT of the stack:
+ *   theta [P] DEVICE; grad [P] DEVICE, accumulated (+=) in theta's layout
+ *   x [T,B,D], mask [T,B], labels [T,B] int32 (K > 0) DEVICE
+ *   dy_top [T,B,2H] DEVICE (K == 0 only), gradient of the top layer's output
+ *   loss_sum: DEVICE double, overwritten with sum over valid frames of
+ *     -log softmax(logits)[label] (K > 0; 0 otherwise)
+ *   frame_errors: DEVICE int32 or NULL, overwritten with #valid frames whose argmax
+ *     (lowest index on ties) differs from the label
+ *   comm: NULL, or a dp_comm: grad is then allreduce-SUMmed over ranks after the
+ *     local accumulation (sync data parallelism, R8)
+ *   workspace: blstm_stack_workspace_bytes DEVICE bytes
+ *   s_main: the stream of the call; s_side: a second stream for work off the
+ *     critical path (may equal s_main or be NULL)
+ */
+int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta, float *grad, const float *x,
+                        const uint8_t *mask, const int32_t *labels, const float *dy_top, double *loss_sum,
+                        int32_t *frame_errors, dp_comm *comm, void *workspace, size_t workspace_bytes,
+                        void *s_main, void *s_side);
+
+/* Forward-only view of the stack for parity checks: Y [L,T,B,2H] and C [L,2,T,B,H]
+ * DEVICE outputs (either may be NULL); same workspace as blstm_stack_fwd_bwd. */
+int blstm_stack_fwd(const blstm_stack_desc *d, const float *theta, const float *x, const uint8_t *mask,
+                    float *Y, float *C, void *workspace, size_t workspace_bytes, void *stream);
+
+/* SGD (§4.3): theta -= lr * grad over n elements (gradients unscaled,
+ * P:253-254); zero_grad != 0 then sets grad = 0.  DEVICE pointers. */
+int sgd_update(float *theta, float *grad, size_t n, float lr, int zero_grad, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Data parallelism over NCCL (§4.1).                      */
+/* ------------------------------------------------------------------------ */
+/* Rank 0 creates the 128-byte NCCL id; the caller broadcasts it (e.g. torch PG). */
+int dp_get_unique_id(unsigned char id[128]);
+/* Create a communicator for this rank on the current CUDA device. */
+int dp_comm_init(int nranks, int rank, const unsigned char id[128], dp_comm **out);
+/* grad <- sum over ranks (in place, fp32): sync mode, one big batch (P:254 unscaled). */
+int dp_allreduce_grads(dp_comm *c, float *grad, size_t n, void *stream);
+/* theta <- (1/N) sum over ranks (in place, fp32): the paper's parameter averaging
+ * "combined into a single set of parameters by averaging". */
+int dp_average_params(dp_comm *c, float *theta, size_t n, void *stream);
+int dp_comm_destroy(dp_comm *c);
+
+/* ------------------------------------------------------------------------ */
+/* Test hook: the tcgen05 GEMM used by every dense contraction of the path.   */
+/* ------------------------------------------------------------------------ */
+/* C[m,n] = alpha * sum_k A(m,k) B(n,k) (+ C[m,n] if beta) (+ bias[n]), A and B fp16
+ * DEVICE (16-byte aligned, ld a multiple of 8), each K-major (element (r,k) at
+ * ptr[r*ld + k], *_mn = 0) or MN-major (at ptr[k*ld + r], *_mn = 1); C fp32. */
+int blstm_gemm_f16(int M, int N, int K, const void *A, long lda, int a_mn, const void *B, long ldb, int b_mn,
+                   float *C, long ldc, float alpha, int beta, const float *bias, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLSTM_H */

@@ -1,0 +1,521 @@
+// api.cu -- the C-ABI of libblstm.so (include/blstm.h): argument validation,
+// workspace / reserve carving and the launch sequence of one layer and of the
+// BLSTM stack's training step.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "blstm.h"
+#include "gemm.h"
+#include "lstm_rec.h"
+#include "ops.h"
+
+using namespace blstm;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local char g_err[512] = "";
+static int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+#define TRY(expr, what)                                                                                   \
+    do {                                                                                                  \
+        int _rc = (expr);                                                                                 \
+        if (_rc != 0) {                                                                                   \
+            cudaError_t _e = cudaGetLastError();                                                          \
+            return fail(BLSTM_ERR_CUDA, "%s failed (rc=%d, cuda: %s)", what, _rc, cudaGetErrorString(_e)); \
+        }                                                                                                 \
+    } while (0)
+
+extern "C" const char *blstm_last_error(void) { return g_err; }
+int blstm_set_error(int code, const char *msg) { return fail(code, "%s", msg); }
+extern "C" int blstm_version(void) { return 100; }
+
+static inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+struct Carve {
+    size_t off = 0;
+    size_t take(size_t bytes) {
+        size_t o = off;
+        off += al256(bytes);
+        return o;
+    }
+};
+static inline int rup(int a, int b) { return (a + b - 1) / b * b; }
+static inline bool al16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+static inline bool al4(const void *p) { return ((uintptr_t)p & 3u) == 0; }
+
+// ---------------------------------------------------------------------------
+// one layer, one direction
+// ---------------------------------------------------------------------------
+struct LayerGeo {
+    int T, B, D, H, Hq, Dp;
+    long TB;
+    RecPlan pl;
+};
+struct FwdWS {
+    size_t x16, w16, rt16, bq, Z, cnt, total;
+};
+struct BwdWS {
+    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, cnt, total;
+};
+struct Reserve {
+    size_t gates, hist, total;
+};
+
+static int layer_geo(const lstm_desc *d, LayerGeo &g) {
+    if (!d) return fail(BLSTM_ERR_ARG, "null lstm_desc");
+    if (d->T < 0 || d->B < 1 || d->D < 1 || d->H < 1)
+        return fail(BLSTM_ERR_SHAPE, "need T>=0, B>=1, D>=1, H>=1 (got T=%d B=%d D=%d H=%d)", d->T, d->B, d->D, d->H);
+    if (d->direction != 1 && d->direction != -1) return fail(BLSTM_ERR_ARG, "direction must be +1 or -1");
+    if (d->ldx < d->D || d->ldy < d->H) return fail(BLSTM_ERR_SHAPE, "need ldx >= D and ldy >= H");
+    if (d->precision != BLSTM_PREC_FP16) return fail(BLSTM_ERR_UNSUPPORTED, "precision %d not supported", d->precision);
+    g.T = d->T; g.B = d->B; g.D = d->D; g.H = d->H;
+    g.TB = (long)d->T * d->B;
+    g.pl = rec_plan(d->T, d->B, d->H, 1, num_sms());
+    g.Hq = g.pl.Hq;
+    g.Dp = rup(d->D, 64);
+    if (!rec_supported(g.pl, d->H))
+        return fail(BLSTM_ERR_UNSUPPORTED, "H=%d B=%d exceeds the recurrence kernels' on-chip capacity (Hq=%d N=%d)",
+                    d->H, d->B, g.pl.Hq, g.pl.N);
+    return 0;
+}
+static FwdWS fwd_ws(const LayerGeo &g) {
+    Carve c;
+    FwdWS w;
+    w.x16 = c.take((size_t)g.TB * g.Dp * 2);
+    w.w16 = c.take((size_t)g.Dp * 4 * g.Hq * 2);
+    w.rt16 = c.take((size_t)4 * g.Hq * g.Hq * 2);
+    w.bq = c.take((size_t)4 * g.Hq * 4);
+    w.Z = c.take((size_t)g.TB * 4 * g.Hq * 4);
+    w.cnt = c.take(256);
+    w.total = c.off;
+    return w;
+}
+static BwdWS bwd_ws(const LayerGeo &g) {
+    Carve c;
+    BwdWS w;
+    w.x16 = c.take((size_t)g.TB * g.Dp * 2);
+    w.w16 = c.take((size_t)g.Dp * 4 * g.Hq * 2);
+    w.rt16 = c.take((size_t)4 * g.Hq * g.Hq * 2);
+    w.dA = c.take((size_t)g.TB * 4 * g.Hq * 2);
+    w.dX = c.take((size_t)g.TB * g.Dp * 4);
+    w.dWT = c.take((size_t)4 * g.Hq * g.Dp * 4);
+    w.dRT = c.take((size_t)4 * g.Hq * g.Hq * 4);
+    w.dbp = c.take((size_t)g.pl.G * 4 * g.Hq * 4);
+    w.P = c.take(rec_P_bytes(g.pl));
+    w.cnt = c.take(256);
+    w.total = c.off;
+    return w;
+}
+static Reserve reserve_of(const LayerGeo &g) {
+    Carve c;
+    Reserve r;
+    r.gates = c.take((size_t)g.TB * 4 * g.Hq * 2);
+    r.hist = c.take((size_t)(g.T + 1) * g.B * g.Hq * 2);
+    r.total = c.off;
+    return r;
+}
+
+extern "C" size_t lstm_workspace_bytes(const lstm_desc *d) {
+    LayerGeo g;
+    if (layer_geo(d, g)) return 0;
+    const size_t a = fwd_ws(g).total, b = bwd_ws(g).total;
+    return a > b ? a : b;
+}
+extern "C" size_t lstm_reserve_bytes(const lstm_desc *d) {
+    LayerGeo g;
+    if (layer_geo(d, g)) return 0;
+    return reserve_of(g).total;
+}
+
+static RecParams base_params(const LayerGeo &g, int ndir, int dir0, const uint8_t *mask) {
+    RecParams p;
+    memset(&p, 0, sizeof(p));
+    p.T = g.T; p.B = g.B; p.H = g.H; p.Hq = g.Hq;
+    p.NC = g.pl.NC; p.G = g.pl.G; p.Bg = g.pl.Bg; p.N = g.pl.N; p.ndir = ndir;
+    p.dir0 = dir0;
+    p.mask = mask;
+    return p;
+}
+
+extern "C" int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask, const float *W, const float *R,
+                        const float *b, const float *h0, const float *c0, float *y, float *c, float *hT, float *cT,
+                        void *reserve, void *workspace, size_t workspace_bytes, void *stream) {
+    LayerGeo g;
+    if (int rc = layer_geo(d, g)) return rc;
+    if (!x || !mask || !W || !R || !b || !y || !c || !reserve || !workspace)
+        return fail(BLSTM_ERR_ARG, "lstm_fwd: null required pointer");
+    if (!al4(x) || !al4(W) || !al4(R) || !al4(b) || !al4(y) || !al4(c)) return fail(BLSTM_ERR_ALIGN, "misaligned fp32 pointer");
+    if (!al16(reserve) || !al16(workspace)) return fail(BLSTM_ERR_ALIGN, "reserve/workspace must be 16-byte aligned");
+    const FwdWS w = fwd_ws(g);
+    const Reserve rv = reserve_of(g);
+    if (workspace_bytes < w.total) return fail(BLSTM_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, w.total);
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *ws = (uint8_t *)workspace, *res = (uint8_t *)reserve;
+    if (g.T == 0) {
+        const size_t bytes = sizeof(float) * g.B * g.H;
+        if (hT) { if (h0) cudaMemcpyAsync(hT, h0, bytes, cudaMemcpyDeviceToDevice, st); else cudaMemsetAsync(hT, 0, bytes, st); }
+        if (cT) { if (c0) cudaMemcpyAsync(cT, c0, bytes, cudaMemcpyDeviceToDevice, st); else cudaMemsetAsync(cT, 0, bytes, st); }
+        return cudaGetLastError() == cudaSuccess ? 0 : fail(BLSTM_ERR_CUDA, "copy failed");
+    }
+    __half *x16 = (__half *)(ws + w.x16), *w16 = (__half *)(ws + w.w16), *rt16 = (__half *)(ws + w.rt16);
+    float *bq = (float *)(ws + w.bq), *Z = (float *)(ws + w.Z);
+    TRY(cast_x_f16(x, d->ldx, g.D, x16, g.Dp, g.TB, st), "cast_x");
+    TRY(pack_w(W, nullptr, g.D, g.H, g.Hq, 1, g.Dp, 0, w16, st), "pack_w");
+    TRY(pack_rt(R, nullptr, g.H, g.Hq, 1, rt16, st), "pack_rt");
+    TRY(pack_bias(b, nullptr, g.H, g.Hq, 1, bq, st), "pack_bias");
+    GemmParams gp{(int)g.TB, 4 * g.Hq, g.Dp, Z, 4L * g.Hq, 1.f, 0, bq, 0, 0};
+    TRY(gemm_f16({x16, g.Dp, 0}, {w16, 4L * g.Hq, 1}, gp, 0, st), "gemm Z");
+    __half *hist = (__half *)(res + rv.hist);
+    TRY(init_hist(hist, h0, g.T, g.B, g.H, g.Hq, 1, d->direction, st), "init_hist");
+    RecParams p = base_params(g, 1, d->direction, mask);
+    p.Z = Z; p.ldz = 4L * g.Hq;
+    p.y = y; p.ldy = d->ldy; p.y_doff = 0;
+    p.C = c; p.ldc = g.H; p.c_doff = 0;
+    p.gates = (__half *)(res + rv.gates); p.ldg = 4L * g.Hq;
+    p.hist = hist;
+    p.c0 = c0; p.h0 = h0; p.hT = hT; p.cT = cT;
+    p.counters = (uint32_t *)(ws + w.cnt);
+    TRY(lstm_rec_fwd(p, rt16, st), "lstm_rec_fwd");
+    return 0;
+}
+
+extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask, const float *W, const float *R,
+                        const float *h0, const float *c0, const float *c, const void *reserve, const float *dy,
+                        const float *dhT, const float *dcT, float *dx, float *dW, float *dR, float *db, float *dh0,
+                        float *dc0, void *workspace, size_t workspace_bytes, void *stream) {
+    (void)h0;  // h0 enters through the saved history (reserve)
+    LayerGeo g;
+    if (int rc = layer_geo(d, g)) return rc;
+    const bool want_dx = !(d->flags & BLSTM_NO_DX);
+    if (!x || !mask || !W || !R || !c || !reserve || !dy || !dW || !dR || !db || !workspace || (want_dx && !dx))
+        return fail(BLSTM_ERR_ARG, "lstm_bwd: null required pointer");
+    if (!al16(reserve) || !al16(workspace)) return fail(BLSTM_ERR_ALIGN, "reserve/workspace must be 16-byte aligned");
+    const BwdWS w = bwd_ws(g);
+    const Reserve rv = reserve_of(g);
+    if (workspace_bytes < w.total) return fail(BLSTM_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, w.total);
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *ws = (uint8_t *)workspace;
+    const uint8_t *res = (const uint8_t *)reserve;
+    if (g.T == 0) {
+        const size_t bytes = sizeof(float) * g.B * g.H;
+        if (dh0) { if (dhT) cudaMemcpyAsync(dh0, dhT, bytes, cudaMemcpyDeviceToDevice, st); else cudaMemsetAsync(dh0, 0, bytes, st); }
+        if (dc0) { if (dcT) cudaMemcpyAsync(dc0, dcT, bytes, cudaMemcpyDeviceToDevice, st); else cudaMemsetAsync(dc0, 0, bytes, st); }
+        return cudaGetLastError() == cudaSuccess ? 0 : fail(BLSTM_ERR_CUDA, "copy failed");
+    }
+    __half *x16 = (__half *)(ws + w.x16), *w16 = (__half *)(ws + w.w16), *rt16 = (__half *)(ws + w.rt16);
+    __half *dA = (__half *)(ws + w.dA);
+    float *dX = (float *)(ws + w.dX), *dWT = (float *)(ws + w.dWT), *dRT = (float *)(ws + w.dRT);
+    float *dbp = (float *)(ws + w.dbp);
+    TRY(cast_x_f16(x, d->ldx, g.D, x16, g.Dp, g.TB, st), "cast_x");
+    TRY(pack_w(W, nullptr, g.D, g.H, g.Hq, 1, g.Dp, 0, w16, st), "pack_w");
+    TRY(pack_rt(R, nullptr, g.H, g.Hq, 1, rt16, st), "pack_rt");
+    RecParams p = base_params(g, 1, d->direction, mask);
+    p.C = const_cast<float *>(c); p.ldc = g.H; p.c_doff = 0;  // read-only in the backward kernel
+    p.gates = (__half *)(res + rv.gates); p.ldg = 4L * g.Hq;
+    p.c0 = c0;
+    p.dy = dy; p.lddy = d->ldy; p.dy_doff = 0;
+    p.dhT = dhT; p.dcT = dcT;
+    p.dA = dA; p.ldda = 4L * g.Hq;
+    p.dbpart = dbp;
+    p.P = (float *)(ws + w.P);
+    p.dh0 = dh0; p.dc0 = dc0;
+    p.counters = (uint32_t *)(ws + w.cnt);
+    TRY(lstm_rec_bwd(p, rt16, st), "lstm_rec_bwd");
+    const float a = 1.f / (float)(1 << DA_SHIFT);
+    if (want_dx) {
+        GemmParams gp{(int)g.TB, g.Dp, 4 * g.Hq, dX, g.Dp, a, 0, nullptr, 0, 0};
+        TRY(gemm_f16({dA, 4L * g.Hq, 0}, {w16, 4L * g.Hq, 0}, gp, 0, st), "gemm dX");
+        TRY(store_dx(dx, d->ldx, dX, g.Dp, g.D, g.TB, (d->flags & BLSTM_ACCUM_DX) ? 1 : 0, st), "store_dx");
+    }
+    {
+        GemmParams gp{4 * g.Hq, g.Dp, (int)g.TB, dWT, g.Dp, a, 0, nullptr, 0, 0};
+        TRY(gemm_f16({dA, 4L * g.Hq, 1}, {x16, g.Dp, 1}, gp, 0, st), "gemm dW");
+    }
+    {
+        const __half *hprev = (const __half *)(res + rv.hist) + (d->direction < 0 ? (long)g.B * g.Hq : 0);
+        GemmParams gp{4 * g.Hq, g.Hq, (int)g.TB, dRT, g.Hq, a, 0, nullptr, 0, 0};
+        TRY(gemm_f16({dA, 4L * g.Hq, 1}, {hprev, g.Hq, 1}, gp, 0, st), "gemm dR");
+    }
+    TRY(scatter_w(dW, g.D, g.H, g.Hq, dWT, g.Dp, 0, 0, st), "scatter dW");
+    TRY(scatter_r(dR, g.H, g.Hq, dRT, st), "scatter dR");
+    TRY(scatter_b(db, g.H, g.Hq, dbp, g.pl.G, 0, st), "scatter db");
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// BLSTM stack
+// ---------------------------------------------------------------------------
+struct StackGeo {
+    int L, D, H, K, T, B, Hq, Dp0, Kp;
+    long TB;
+    RecPlan pl;
+    std::vector<int> Dn, Drows, rowmode;
+};
+struct StackWS {
+    size_t x16, Z, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, total;
+    std::vector<size_t> y16, w16, rt16, bq, gates, C, hist;
+};
+
+static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
+    if (!d) return fail(BLSTM_ERR_ARG, "null blstm_stack_desc");
+    if (d->L < 1 || d->D < 1 || d->H < 1 || d->K < 0 || d->T < 1 || d->B < 1)
+        return fail(BLSTM_ERR_SHAPE, "need L,D,H,T,B >= 1 and K >= 0");
+    if (d->precision != BLSTM_PREC_FP16) return fail(BLSTM_ERR_UNSUPPORTED, "precision %d not supported", d->precision);
+    g.L = d->L; g.D = d->D; g.H = d->H; g.K = d->K; g.T = d->T; g.B = d->B;
+    g.TB = (long)d->T * d->B;
+    g.pl = rec_plan(d->T, d->B, d->H, 2, num_sms());
+    g.Hq = g.pl.Hq;
+    g.Dp0 = rup(d->D, 64);
+    g.Kp = d->K > 0 ? rup(d->K, 64) : 0;
+    if (!rec_supported(g.pl, d->H))
+        return fail(BLSTM_ERR_UNSUPPORTED, "H=%d B=%d exceeds the recurrence kernels' on-chip capacity (Hq=%d N=%d)",
+                    d->H, d->B, g.pl.Hq, g.pl.N);
+    g.Dn.resize(g.L); g.Drows.resize(g.L); g.rowmode.resize(g.L);
+    for (int l = 0; l < g.L; ++l) {
+        g.Dn[l] = l == 0 ? g.Dp0 : 2 * g.Hq;
+        g.Drows[l] = l == 0 ? g.D : 2 * g.H;
+        g.rowmode[l] = l == 0 ? 0 : 1;
+    }
+    return 0;
+}
+static StackWS stack_ws(const StackGeo &g) {
+    Carve c;
+    StackWS w;
+    const long TB = g.TB;
+    const int Hq = g.Hq;
+    int maxDn = 0;
+    for (int v : g.Dn) maxDn = v > maxDn ? v : maxDn;
+    w.x16 = c.take((size_t)TB * g.Dp0 * 2);
+    for (int l = 0; l < g.L; ++l) {
+        w.y16.push_back(c.take((size_t)TB * 2 * Hq * 2));
+        w.w16.push_back(c.take((size_t)g.Dn[l] * 8 * Hq * 2));
+        w.rt16.push_back(c.take((size_t)2 * 4 * Hq * Hq * 2));
+        w.bq.push_back(c.take((size_t)8 * Hq * 4));
+        w.gates.push_back(c.take((size_t)TB * 8 * Hq * 2));
+        w.C.push_back(c.take((size_t)2 * TB * Hq * 4));
+        w.hist.push_back(c.take((size_t)2 * (g.T + 1) * g.B * Hq * 2));
+    }
+    const int zc = 8 * Hq > g.Kp ? 8 * Hq : g.Kp;
+    w.Z = c.take((size_t)TB * zc * 4);
+    w.dA = c.take((size_t)TB * 8 * Hq * 2);
+    w.dY0 = c.take((size_t)TB * 2 * Hq * 4);
+    w.dY1 = c.take((size_t)TB * 2 * Hq * 4);
+    w.dWT = c.take((size_t)8 * Hq * maxDn * 4);
+    w.dRT = c.take((size_t)2 * 4 * Hq * Hq * 4);
+    w.dbp = c.take((size_t)2 * g.pl.G * 4 * Hq * 4);
+    w.P = c.take(rec_P_bytes(g.pl));
+    w.cnt = c.take(256);
+    w.wo16 = c.take((size_t)2 * Hq * (g.Kp ? g.Kp : 64) * 2);
+    w.boq = c.take((size_t)(g.Kp ? g.Kp : 64) * 4);
+    w.dlog16 = c.take((size_t)TB * (g.Kp ? g.Kp : 64) * 2);
+    w.dWoT = c.take((size_t)(g.K ? g.K : 1) * 2 * Hq * 4);
+    w.rowloss = c.take((size_t)TB * 8);
+    w.rowerr = c.take((size_t)TB * 4);
+    w.cs = c.take(colsum_scratch_bytes(TB, g.K ? g.K : 1));
+    w.total = c.off;
+    return w;
+}
+
+static size_t param_layout(const blstm_stack_desc *d, size_t *offs) {
+    size_t o = 0;
+    const size_t H = d->H;
+    for (int l = 0; l < d->L; ++l) {
+        const size_t Dl = l == 0 ? (size_t)d->D : 2 * H;
+        for (int dd = 0; dd < 2; ++dd) {
+            const int e = 6 * l + 3 * dd;
+            if (offs) {
+                offs[e] = o;
+                offs[e + 1] = o + Dl * 4 * H;
+                offs[e + 2] = o + Dl * 4 * H + 4 * H * H;
+            }
+            o += Dl * 4 * H + 4 * H * H + 4 * H;
+        }
+    }
+    if (offs) {
+        offs[6 * d->L] = o;
+        offs[6 * d->L + 1] = o + (d->K > 0 ? 2 * H * d->K : 0);
+    }
+    if (d->K > 0) o += 2 * H * d->K + d->K;
+    return o;
+}
+
+extern "C" size_t blstm_param_count(const blstm_stack_desc *d) {
+    if (!d || d->L < 1 || d->H < 1 || d->D < 1 || d->K < 0) return 0;
+    return param_layout(d, nullptr);
+}
+extern "C" size_t blstm_param_offsets(const blstm_stack_desc *d, size_t *offs) {
+    if (!d || d->L < 1 || d->H < 1 || d->D < 1 || d->K < 0) return 0;
+    return param_layout(d, offs);
+}
+extern "C" size_t blstm_stack_workspace_bytes(const blstm_stack_desc *d) {
+    StackGeo g;
+    if (stack_geo(d, g)) return 0;
+    return stack_ws(g).total;
+}
+
+// forward of the whole stack; Yout [L,T,B,2H] / Cout [L,2,T,B,H] optional (parity view)
+static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const StackWS &w, uint8_t *ws,
+                         const float *theta, const float *x, const uint8_t *mask, float *Yout, float *Cout,
+                         cudaStream_t st) {
+    std::vector<size_t> offs(6 * g.L + 2);
+    param_layout(d, offs.data());
+    const int Hq = g.Hq;
+    __half *x16 = (__half *)(ws + w.x16);
+    TRY(cast_x_f16(x, g.D, g.D, x16, g.Dp0, g.TB, st), "cast_x");
+    for (int l = 0; l < g.L; ++l) {
+        const float *Wf = theta + offs[6 * l], *Rf = theta + offs[6 * l + 1], *bf = theta + offs[6 * l + 2];
+        const float *Wb = theta + offs[6 * l + 3], *Rb = theta + offs[6 * l + 4], *bb = theta + offs[6 * l + 5];
+        TRY(pack_w(Wf, Wb, g.Drows[l], g.H, Hq, 2, g.Dn[l], g.rowmode[l], (__half *)(ws + w.w16[l]), st), "pack_w");
+        TRY(pack_rt(Rf, Rb, g.H, Hq, 2, (__half *)(ws + w.rt16[l]), st), "pack_rt");
+        TRY(pack_bias(bf, bb, g.H, Hq, 2, (float *)(ws + w.bq[l]), st), "pack_bias");
+    }
+    float *Z = (float *)(ws + w.Z);
+    for (int l = 0; l < g.L; ++l) {
+        const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
+        const long lda = l == 0 ? g.Dp0 : 2L * Hq;
+        GemmParams gp{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
+        TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gp, 0, st), "gemm Z");
+        __half *hist = (__half *)(ws + w.hist[l]);
+        TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
+        RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
+        p.Z = Z; p.ldz = 8L * Hq;
+        if (Yout) { p.y = Yout + (size_t)l * g.TB * 2 * g.H; p.ldy = 2L * g.H; p.y_doff = g.H; }
+        p.y16 = (__half *)(ws + w.y16[l]); p.ldy16 = 2L * Hq;
+        if (Cout) { p.C = Cout + (size_t)l * 2 * g.TB * g.H; p.ldc = g.H; p.c_doff = g.TB * g.H; }
+        else { p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq; }
+        p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
+        p.hist = hist;
+        p.counters = (uint32_t *)(ws + w.cnt);
+        TRY(lstm_rec_fwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_fwd");
+    }
+    return 0;
+}
+
+static int check_stack_ptrs(const StackWS &w, const float *theta, const float *x, const uint8_t *mask, void *workspace,
+                            size_t workspace_bytes) {
+    if (!theta || !x || !mask || !workspace) return fail(BLSTM_ERR_ARG, "null required pointer");
+    if (!al16(theta) || !al4(x) || !al16(workspace)) return fail(BLSTM_ERR_ALIGN, "theta/workspace must be 16-byte aligned");
+    if (workspace_bytes < w.total) return fail(BLSTM_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, w.total);
+    return 0;
+}
+
+extern "C" int blstm_stack_fwd(const blstm_stack_desc *d, const float *theta, const float *x, const uint8_t *mask,
+                               float *Y, float *C, void *workspace, size_t workspace_bytes, void *stream) {
+    StackGeo g;
+    if (int rc = stack_geo(d, g)) return rc;
+    const StackWS w = stack_ws(g);
+    if (int rc = check_stack_ptrs(w, theta, x, mask, workspace, workspace_bytes)) return rc;
+    return stack_forward(d, g, w, (uint8_t *)workspace, theta, x, mask, Y, C, (cudaStream_t)stream);
+}
+
+int dp_allreduce_grads_impl(dp_comm *c, float *grad, size_t n, cudaStream_t st);
+
+extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta, float *grad, const float *x,
+                                   const uint8_t *mask, const int32_t *labels, const float *dy_top, double *loss_sum,
+                                   int32_t *frame_errors, dp_comm *comm, void *workspace, size_t workspace_bytes,
+                                   void *s_main, void *s_side) {
+    (void)s_side;
+    StackGeo g;
+    if (int rc = stack_geo(d, g)) return rc;
+    const StackWS w = stack_ws(g);
+    if (int rc = check_stack_ptrs(w, theta, x, mask, workspace, workspace_bytes)) return rc;
+    if (!grad || !loss_sum) return fail(BLSTM_ERR_ARG, "null grad / loss_sum");
+    if (!al16(grad)) return fail(BLSTM_ERR_ALIGN, "grad must be 16-byte aligned");
+    if (g.K > 0 && !labels) return fail(BLSTM_ERR_ARG, "K > 0 needs labels");
+    if (g.K == 0 && !dy_top) return fail(BLSTM_ERR_ARG, "K == 0 needs dy_top");
+    cudaStream_t st = (cudaStream_t)s_main;
+    uint8_t *ws = (uint8_t *)workspace;
+    std::vector<size_t> offs(6 * g.L + 2);
+    param_layout(d, offs.data());
+    if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st)) return rc;
+
+    const int Hq = g.Hq;
+    const float a = 1.f / (float)(1 << DA_SHIFT);
+    float *dY[2] = {(float *)(ws + w.dY0), (float *)(ws + w.dY1)};
+    const __half *ytop = (const __half *)(ws + w.y16[g.L - 1]);
+    if (g.K > 0) {
+        __half *wo16 = (__half *)(ws + w.wo16), *dlog = (__half *)(ws + w.dlog16);
+        float *boq = (float *)(ws + w.boq), *logits = (float *)(ws + w.Z), *dWoT = (float *)(ws + w.dWoT);
+        TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, Hq, g.K, g.Kp, wo16, boq, st), "pack_wout");
+        GemmParams gl{(int)g.TB, g.K, 2 * Hq, logits, g.Kp, 1.f, 0, boq, 0, 0};
+        TRY(gemm_f16({ytop, 2L * Hq, 0}, {wo16, g.Kp, 1}, gl, 0, st), "gemm logits");
+        TRY(ce_head(logits, g.Kp, g.K, g.Kp, mask, labels, (float)(1 << DA_SHIFT), dlog, (double *)(ws + w.rowloss),
+                    (int32_t *)(ws + w.rowerr), g.TB, st), "ce_head");
+        TRY(reduce_loss((double *)(ws + w.rowloss), (int32_t *)(ws + w.rowerr), g.TB, loss_sum, frame_errors, st),
+            "reduce_loss");
+        GemmParams gd{(int)g.TB, 2 * Hq, g.Kp, dY[0], 2L * Hq, a, 0, nullptr, 0, 0};
+        TRY(gemm_f16({dlog, g.Kp, 0}, {wo16, g.Kp, 0}, gd, 0, st), "gemm dY_top");
+        GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
+        TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, 0, st), "gemm dW_out");
+        TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, st), "scatter dW_out");
+        TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), st), "db_out");
+    } else {
+        TRY(pad_halves(dy_top, g.H, Hq, g.TB, dY[0], st), "pad dy_top");
+        if (cudaMemsetAsync(loss_sum, 0, sizeof(double), st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
+        if (frame_errors && cudaMemsetAsync(frame_errors, 0, sizeof(int32_t), st) != cudaSuccess)
+            return fail(BLSTM_ERR_CUDA, "memset");
+    }
+
+    __half *dA = (__half *)(ws + w.dA);
+    float *dWT = (float *)(ws + w.dWT), *dRT = (float *)(ws + w.dRT), *dbp = (float *)(ws + w.dbp);
+    int cur = 0;
+    for (int l = g.L - 1; l >= 0; --l) {
+        RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
+        p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq;
+        p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
+        p.dy = dY[cur]; p.lddy = 2L * Hq; p.dy_doff = Hq;
+        p.dA = dA; p.ldda = 8L * Hq;
+        p.dbpart = dbp;
+        p.P = (float *)(ws + w.P);
+        p.counters = (uint32_t *)(ws + w.cnt);
+        TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
+        const __half *w16 = (const __half *)(ws + w.w16[l]);
+        if (l > 0) {
+            GemmParams gx{(int)g.TB, g.Dn[l], 8 * Hq, dY[1 - cur], 2L * Hq, a, 0, nullptr, 0, 0};
+            TRY(gemm_f16({dA, 8L * Hq, 0}, {w16, 8L * Hq, 0}, gx, 0, st), "gemm dX");
+        }
+        const __half *X = l == 0 ? (const __half *)(ws + w.x16) : (const __half *)(ws + w.y16[l - 1]);
+        GemmParams gw{8 * Hq, g.Dn[l], (int)g.TB, dWT, g.Dn[l], a, 0, nullptr, 0, 0};
+        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, 0, st), "gemm dW");
+        const __half *hist = (const __half *)(ws + w.hist[l]);
+        for (int dd = 0; dd < 2; ++dd) {
+            const __half *hprev = hist + ((long)dd * (g.T + 1) + dd) * g.B * Hq;
+            GemmParams gr{4 * Hq, Hq, (int)g.TB, dRT + (size_t)dd * 4 * Hq * Hq, Hq, a, 0, nullptr, 0, 0};
+            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, 0, st), "gemm dR");
+        }
+        for (int dd = 0; dd < 2; ++dd) {
+            const int e = 6 * l + 3 * dd;
+            TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], st), "scatter dW");
+            TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, st), "scatter dR");
+            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.pl.G, dd, st), "scatter db");
+        }
+        cur = 1 - cur;
+    }
+    if (comm) {
+        if (int rc = dp_allreduce_grads_impl(comm, grad, param_layout(d, nullptr), st)) return rc;
+    }
+    return 0;
+}
+
+extern "C" int sgd_update(float *theta, float *grad, size_t n, float lr, int zero_grad, void *stream) {
+    if (!theta || !grad) return fail(BLSTM_ERR_ARG, "null theta / grad");
+    if (!al16(theta) || !al16(grad)) return fail(BLSTM_ERR_ALIGN, "theta/grad must be 16-byte aligned");
+    TRY(sgd(theta, grad, (long)n, lr, zero_grad, (cudaStream_t)stream), "sgd");
+    return 0;
+}
+
+extern "C" int blstm_gemm_f16(int M, int N, int K, const void *A, long lda, int a_mn, const void *B, long ldb,
+                              int b_mn, float *C, long ldc, float alpha, int beta, const float *bias, void *stream) {
+    if (!A || !B || !C || M < 0 || N < 0 || K < 1) return fail(BLSTM_ERR_ARG, "blstm_gemm_f16: bad argument");
+    if (!al16(A) || !al16(B) || (lda & 7) || (ldb & 7)) return fail(BLSTM_ERR_ALIGN, "A/B must be 16-byte aligned, ld % 8 == 0");
+    GemmParams gp{M, N, K, C, ldc, alpha, beta, bias, 0, 0};
+    TRY(gemm_f16({A, lda, a_mn}, {B, ldb, b_mn}, gp, 0, (cudaStream_t)stream), "gemm");
+    return 0;
+}

@@ -1,0 +1,286 @@
+// gemm.cu -- TMA-fed tcgen05 GEMM for the dense contractions of the path:
+//   a1  Z  = X W + b            (§4.2, "a single matrix multiplication
+//                                 for the whole mini-batch of sequences")
+//   a4  logits = Y W_out + b_out, dY = dlogits W_out^T, dW_out = Y^T dlogits
+//   a6  dX = dA W^T, dW = X^T dA, dR = Hprev^T dA  ("after the recurrent part is
+//                                 back propagated through time")
+//
+//   C[m, n] = alpha * sum_k A(m, k) * B(n, k)  (+ C[m, n] if beta)  (+ bias[n])
+//
+// A and B are fp16, each either K-major (element (r, k) at ptr[r*ld + k]) or MN-major
+// (element (r, k) at ptr[k*ld + r]); C is fp32 row-major.  fp32 accumulation in TMEM.
+//
+// Structure (persistent, one CTA per SM, 6 warps):
+//   warp 0      TMA producer (one elected lane), STAGES-deep smem ring, 128B swizzle
+//   warp 1      TMEM allocator + MMA issuer (one lane), tcgen05.mma M=128 N=BN K=16
+//   warps 2..5  epilogue: tcgen05.ld -> alpha/bias/beta -> fp32 global stores
+//   Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the
+//   MMAs of tile i+1.
+#include "common.cuh"
+#include "gemm.h"
+
+namespace blstm {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_THREADS = 192;
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int STAGES = BN >= 256 ? 4 : 6;
+    static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
+    static constexpr int B_BYTES = BN * GEMM_BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int TMEM_COLS = 2 * BN;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_f16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    GemmParams p) {
+    using Cfg = GemmCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t *empty = full + Cfg::STAGES;
+    uint64_t *tfull = empty + Cfg::STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+
+    const int warp = warp_id();
+    const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
+    const int num_n = (p.N + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+    const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+
+    if (warp == 0 && lane_id() == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < Cfg::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m0 = (tile % num_m) * GEMM_BM;
+                const int n0 = (tile / num_m) * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
+                    uint8_t *sb = sa + Cfg::A_BYTES;
+                    mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+                    const int k0 = kb * GEMM_BK;
+                    if (!p.a_mn) {
+                        tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+                    } else {
+                        tma_load_2d(sa, &tmA, &full[stage], m0, k0);
+                        tma_load_2d(sa + 8192, &tmA, &full[stage], m0 + 64, k0);
+                    }
+                    if (!p.b_mn) {
+                        tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+                    }
+                    if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t idesc = idesc_f16(GEMM_BM, BN, p.a_mn, p.b_mn);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+                    const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
+                        const uint64_t ad = p.a_mn ? sdesc_sw128(sa + kk * 2048, 8192, 1024)
+                                                   : sdesc_sw128(sa + kk * 32, 16, 1024);
+                        const uint64_t bd = p.b_mn ? sdesc_sw128(sb + kk * 2048, 8192, 1024)
+                                                   : sdesc_sw128(sb + kk * 32, 16, 1024);
+                        mma_f16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (kb == num_kb - 1) mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+                if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+            }
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    } else {
+        // ---------------- epilogue (warps 2..5) ----------------
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row_in_tile = q * 32 + lane_id();
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int m0 = (tile % num_m) * GEMM_BM;
+            const int n0 = (tile / num_m) * BN;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int m = m0 + row_in_tile;
+            float *crow = p.C + (size_t)m * p.ldc;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 16) {
+                float v[16];
+                tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+                tmem_ld_wait();
+                const int n = n0 + c;
+                if (m < p.M && n < p.N) {
+                    if (n + 16 <= p.N && (p.ldc & 3) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) {
+                            float4 o = make_float4(v[j] * p.alpha, v[j + 1] * p.alpha, v[j + 2] * p.alpha,
+                                                   v[j + 3] * p.alpha);
+                            if (p.bias) {
+                                o.x += p.bias[n + j]; o.y += p.bias[n + j + 1];
+                                o.z += p.bias[n + j + 2]; o.w += p.bias[n + j + 3];
+                            }
+                            float4 *dst = reinterpret_cast<float4 *>(crow + n + j);
+                            if (p.beta) {
+                                const float4 old = *dst;
+                                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+                            }
+                            *dst = o;
+                        }
+                    } else {
+                        for (int j = 0; j < 16 && n + j < p.N; ++j) {
+                            float o = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
+                            if (p.beta) o += crow[n + j];
+                            crow[n + j] = o;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)ptr;
+    }
+    return fn;
+}
+
+// 2-D fp16 tensor map over a row-major [outer, inner] array with row stride ld
+// (elements), box {64 inner, box_outer}, 128B swizzle, OOB reads as zero.
+int make_tmap_f16(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                  uint32_t box_outer) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return -1;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld * 2};
+    cuuint32_t box[2] = {64, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+static int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+template <int BN>
+static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, const GemmParams &p, int max_ctas,
+                               cudaStream_t st) {
+    using Cfg = GemmCfg<BN>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_f16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
+    int grid = tiles < max_ctas ? tiles : max_ctas;
+    if (grid < 1) grid = 1;
+    gemm_f16_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, p);
+    return cudaGetLastError();
+}
+
+// C = alpha * op(A) op(B)^T (+C) (+bias).  Returns 0 / negative error.
+int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, int max_ctas, cudaStream_t st) {
+    GemmParams p = pin;
+    p.a_mn = A.mn_major;
+    p.b_mn = B.mn_major;
+    if (p.M <= 0 || p.N <= 0) return 0;
+    if (p.K <= 0) return -3;  // callers never ask for an empty contraction
+    const int BN = p.N > 128 ? 256 : 128;
+    CUtensorMap ta, tb;
+    int rc;
+    if (!A.mn_major) rc = make_tmap_f16(&ta, A.ptr, p.K, p.M, A.ld, GEMM_BM);
+    else rc = make_tmap_f16(&ta, A.ptr, p.M, p.K, A.ld, GEMM_BK);
+    if (rc) return rc;
+    if (!B.mn_major) rc = make_tmap_f16(&tb, B.ptr, p.K, p.N, B.ld, BN);
+    else rc = make_tmap_f16(&tb, B.ptr, p.N, p.K, B.ld, GEMM_BK);
+    if (rc) return rc;
+    if (max_ctas <= 0) max_ctas = num_sms();
+    cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, p, max_ctas, st) : launch_gemm<128>(ta, tb, p, max_ctas, st);
+    return e == cudaSuccess ? 0 : -5;
+}
+
+}  // namespace blstm

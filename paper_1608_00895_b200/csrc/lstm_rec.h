@@ -1,0 +1,58 @@
+// lstm_rec.h -- internal interface of the persistent recurrence kernels (lstm_rec.cu).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace blstm {
+
+constexpr int REC_UNITS = 32;   // hidden units per CTA -> 128 gate rows = one tcgen05 M tile
+constexpr int DA_SHIFT = 10;    // dA is scaled by 2^10 before its fp16 cast
+
+// Kernel-private layouts:
+//   Hq = round_up(H, 128); gate column of (unit j, gate gamma in i,f,g,o) = 4*j + gamma
+//   ("gate-interleaved"), direction d adds d*4*Hq.
+struct RecPlan {
+    int Hq, NC;     // padded units, CTAs per (direction, batch group) = Hq / 32
+    int G, Bg, N;   // batch groups, rows per group, MMA N (= round_up(Bg, 16))
+    int ndir;
+};
+
+struct RecParams {
+    int T, B, H, Hq, NC, G, Bg, N, ndir;
+    int dir0;                    // direction (+1/-1) of direction index 0; index 1 is always -1
+    const uint8_t *mask;         // [T, B]
+    // forward
+    const float *Z;              // [T*B, ldz], direction d at column d*4Hq
+    long ldz;
+    float *y;                    // [T*B, ldy] (+ d*y_doff), j < H; nullable
+    long ldy, y_doff;
+    __half *y16;                 // [T*B, ldy16] (+ d*Hq), all j < Hq; nullable
+    long ldy16;
+    float *C;                    // cell state after frame t: [T*B, ldc] (+ d*c_doff), j < H
+    long ldc, c_doff;
+    __half *gates;               // [T*B, ldg] (+ d*4Hq) saved activations
+    long ldg;
+    __half *hist;                // [ndir][T+1][B][Hq]: h before frame t at slot t + (dir<0)
+    const float *c0, *h0;        // [B, H] (+ d*B*H) or nullptr
+    float *hT, *cT;              // [B, H] (+ d*B*H) or nullptr
+    // backward
+    const float *dy;             // [T*B, lddy] (+ d*dy_doff), j < H
+    long lddy, dy_doff;
+    const float *dhT, *dcT;      // [B, H] or nullptr
+    __half *dA;                  // [T*B, ldda] (+ d*4Hq), scaled by 2^DA_SHIFT
+    long ldda;
+    float *dbpart;               // [ndir][G][4Hq] partial bias gradient (unscaled)
+    float *P;                    // [2][ndir][G][NC][Hq][N] partial dh exchange
+    float *dh0, *dc0;            // [B, H] (+ d*B*H) or nullptr
+    uint32_t *counters;          // [ndir][G], zeroed before each launch
+};
+
+RecPlan rec_plan(int T, int B, int H, int ndir, int num_sms);
+bool rec_supported(const RecPlan &pl, int H);
+size_t rec_P_bytes(const RecPlan &pl);
+// RT16: [ndir][4Hq][Hq] fp16 (row = gate column 4j+gamma, col = k)
+int lstm_rec_fwd(const RecParams &p, const __half *RT16, cudaStream_t st);
+int lstm_rec_bwd(const RecParams &p, const __half *RT16, cudaStream_t st);
+
+}  // namespace blstm

@@ -1,0 +1,364 @@
+// ops.cu -- HBM-bound helper kernels of the path: operand packing (fp32 master
+// parameters -> fp16 tensor-core operands in the kernel-private gate-interleaved
+// layout), the softmax-CE head (§3.2, summed over valid frames,
+// P:253-254), deterministic reductions, gradient scatter-add back to the flat
+// theta layout, and SGD (§4.3).  All grid-stride, coalesced on the
+// large side of each mapping.
+#include "common.cuh"
+#include "ops.h"
+
+namespace blstm {
+
+static int grid_for(long n, int block = 256, int cap = 148 * 16) {
+    long g = (n + block - 1) / block;
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+// --- x [rows, ldx] fp32 -> X16 [rows, Dp] fp16 (zero pad) ---------------------------------
+__global__ void cast_x_kernel(const float *__restrict__ x, long ldx, int D, __half *__restrict__ x16, int Dp,
+                              long rows) {
+    const long n = rows * Dp;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long r = i / Dp;
+        const int k = (int)(i - r * Dp);
+        x16[i] = __float2half_rn(k < D ? x[r * ldx + k] : 0.f);
+    }
+}
+int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, cudaStream_t st) {
+    cast_x_kernel<<<grid_for(rows * Dp), 256, 0, st>>>(x, ldx, D, x16, Dp, rows);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// internal input row r of layer input -> source row of W (or -1 for padding)
+DEVI int src_row(int r, int Drows, int H, int Hq, int rowmode) {
+    if (rowmode == 0) return r < Drows ? r : -1;
+    const int half = r / Hq, jj = r - half * Hq;
+    return (half < 2 && jj < H) ? half * H + jj : -1;
+}
+
+// --- W_d [Drows, 4H] -> W16 [Dn, ndir*4Hq] with column 4j+gamma (+ d*4Hq) ------------------
+__global__ void pack_w_kernel(const float *__restrict__ W0, const float *__restrict__ W1, int Drows, int H, int Hq,
+                              int ndir, int Dn, int rowmode, __half *__restrict__ W16) {
+    const int cols = ndir * 4 * Hq;
+    const long n = (long)Dn * cols;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cols), col = (int)(i - (long)r * cols);
+        const int d = col / (4 * Hq), qq = col - d * 4 * Hq, j = qq >> 2, gam = qq & 3;
+        const int sr = src_row(r, Drows, H, Hq, rowmode);
+        const float *W = d == 0 ? W0 : W1;
+        float v = 0.f;
+        if (sr >= 0 && j < H) v = W[(long)sr * 4 * H + gam * H + j];
+        W16[i] = __float2half_rn(v);
+    }
+}
+int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir, int Dn, int rowmode, __half *W16,
+           cudaStream_t st) {
+    pack_w_kernel<<<grid_for((long)Dn * ndir * 4 * Hq), 256, 0, st>>>(W0, W1, Drows, H, Hq, ndir, Dn, rowmode, W16);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- R_d [H, 4H] -> RT16 [ndir][4Hq][Hq]: row 4j+gamma, col k --------------------------------
+__global__ void pack_rt_kernel(const float *__restrict__ R0, const float *__restrict__ R1, int H, int Hq, int ndir,
+                               __half *__restrict__ RT16) {
+    const long n = (long)ndir * 4 * Hq * Hq;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long row = i / Hq;
+        const int k = (int)(i - row * Hq);
+        const int d = (int)(row / (4 * Hq)), qq = (int)(row - (long)d * 4 * Hq), j = qq >> 2, gam = qq & 3;
+        const float *R = d == 0 ? R0 : R1;
+        const float v = (j < H && k < H) ? R[(long)k * 4 * H + gam * H + j] : 0.f;
+        RT16[i] = __float2half_rn(v);
+    }
+}
+int pack_rt(const float *R0, const float *R1, int H, int Hq, int ndir, __half *RT16, cudaStream_t st) {
+    pack_rt_kernel<<<grid_for((long)ndir * 4 * Hq * Hq), 256, 0, st>>>(R0, R1, H, Hq, ndir, RT16);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+__global__ void pack_bias_kernel(const float *__restrict__ b0, const float *__restrict__ b1, int H, int Hq, int ndir,
+                                 float *__restrict__ bq) {
+    const int n = ndir * 4 * Hq;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int d = i / (4 * Hq), qq = i - d * 4 * Hq, j = qq >> 2, gam = qq & 3;
+        const float *b = d == 0 ? b0 : b1;
+        bq[i] = j < H ? b[gam * H + j] : 0.f;
+    }
+}
+int pack_bias(const float *b0, const float *b1, int H, int Hq, int ndir, float *bq, cudaStream_t st) {
+    pack_bias_kernel<<<grid_for(ndir * 4 * Hq), 256, 0, st>>>(b0, b1, H, Hq, ndir, bq);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- head weights: W_out [2H, K] -> Wo16 [2Hq, Kp] (rows = padded [fwd | bwd] halves) --------
+__global__ void pack_wout_kernel(const float *__restrict__ Wo, const float *__restrict__ bo, int H, int Hq, int K,
+                                 int Kp, __half *__restrict__ Wo16, float *__restrict__ boq) {
+    const long n = (long)2 * Hq * Kp;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / Kp), k = (int)(i - (long)r * Kp);
+        const int sr = src_row(r, 2 * H, H, Hq, 1);
+        Wo16[i] = __float2half_rn((sr >= 0 && k < K) ? Wo[(long)sr * K + k] : 0.f);
+        if (r == 0) boq[k] = k < K ? bo[k] : 0.f;
+    }
+}
+int pack_wout(const float *Wo, const float *bo, int H, int Hq, int K, int Kp, __half *Wo16, float *boq,
+              cudaStream_t st) {
+    pack_wout_kernel<<<grid_for((long)2 * Hq * Kp), 256, 0, st>>>(Wo, bo, H, Hq, K, Kp, Wo16, boq);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- initial history slot (h0 or 0) for each direction -------------------------------------
+__global__ void init_hist_kernel(__half *__restrict__ hist, const float *__restrict__ h0, int T, int B, int H,
+                                 int Hq, int ndir, int dir0) {
+    const long n = (long)ndir * B * Hq;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int d = (int)(i / ((long)B * Hq));
+        const long rem = i - (long)d * B * Hq;
+        const int b = (int)(rem / Hq), j = (int)(rem - (long)b * Hq);
+        const int dir = d == 0 ? dir0 : -1;
+        const int slot = dir > 0 ? 0 : T;
+        const float v = (h0 && j < H) ? h0[(long)d * B * H + (long)b * H + j] : 0.f;
+        hist[(((long)d * (T + 1) + slot) * B + b) * Hq + j] = __float2half_rn(v);
+    }
+}
+int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int ndir, int dir0, cudaStream_t st) {
+    init_hist_kernel<<<grid_for((long)ndir * B * Hq), 256, 0, st>>>(hist, h0, T, B, H, Hq, ndir, dir0);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- softmax cross-entropy over one frame per CTA ------------------------------------------
+// logits [rows, ldl] fp32 (K valid columns); writes dlog16 [rows, Kp] = 2^shift (softmax - onehot)
+// at valid frames (0 elsewhere), rowloss (double) and rowerr (argmax != label, lowest index on ties).
+constexpr int CE_THREADS = 256;
+__global__ void __launch_bounds__(CE_THREADS) ce_head_kernel(const float *__restrict__ logits, long ldl, int K, int Kp,
+                                                             const uint8_t *__restrict__ mask,
+                                                             const int32_t *__restrict__ labels, float scale,
+                                                             __half *__restrict__ dlog16, double *__restrict__ rowloss,
+                                                             int32_t *__restrict__ rowerr) {
+    const long r = blockIdx.x;
+    __half *drow = dlog16 + r * Kp;
+    if (!mask[r]) {
+        for (int k = threadIdx.x; k < Kp; k += CE_THREADS) drow[k] = __float2half_rn(0.f);
+        if (threadIdx.x == 0) { rowloss[r] = 0.0; rowerr[r] = 0; }
+        return;
+    }
+    const float *lrow = logits + r * ldl;
+    __shared__ float s_v[CE_THREADS / 32];
+    __shared__ int s_i[CE_THREADS / 32];
+    __shared__ float s_sum[CE_THREADS / 32];
+    // max + argmax (ties: lowest index)
+    float mv = -INFINITY;
+    int mi = 0x7fffffff;
+    for (int k = threadIdx.x; k < K; k += CE_THREADS) {
+        const float v = lrow[k];
+        if (v > mv || (v == mv && k < mi)) { mv = v; mi = k; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, mv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
+        if (ov > mv || (ov == mv && oi < mi)) { mv = ov; mi = oi; }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { s_v[w] = mv; s_i[w] = mi; }
+    __syncthreads();
+    mv = s_v[0];
+    mi = s_i[0];
+    for (int i = 1; i < CE_THREADS / 32; ++i)
+        if (s_v[i] > mv || (s_v[i] == mv && s_i[i] < mi)) { mv = s_v[i]; mi = s_i[i]; }
+    // sum exp
+    float se = 0.f;
+    for (int k = threadIdx.x; k < K; k += CE_THREADS) se += expf(lrow[k] - mv);
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    if ((threadIdx.x & 31) == 0) s_sum[w] = se;
+    __syncthreads();
+    se = 0.f;
+    for (int i = 0; i < CE_THREADS / 32; ++i) se += s_sum[i];
+    const float lse = mv + logf(se);
+    const int lab = labels[r];
+    for (int k = threadIdx.x; k < Kp; k += CE_THREADS) {
+        float v = 0.f;
+        if (k < K) v = expf(lrow[k] - lse) - (k == lab ? 1.f : 0.f);
+        drow[k] = __float2half_rn(v * scale);
+    }
+    if (threadIdx.x == 0) {
+        rowloss[r] = (double)lse - (double)lrow[lab];
+        rowerr[r] = mi != lab;
+    }
+}
+int ce_head(const float *logits, long ldl, int K, int Kp, const uint8_t *mask, const int32_t *labels, float scale,
+            __half *dlog16, double *rowloss, int32_t *rowerr, long rows, cudaStream_t st) {
+    if (rows <= 0) return 0;
+    ce_head_kernel<<<(unsigned)rows, CE_THREADS, 0, st>>>(logits, ldl, K, Kp, mask, labels, scale, dlog16, rowloss,
+                                                          rowerr);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- deterministic loss / error reduction (one CTA, fixed order) ---------------------------
+__global__ void __launch_bounds__(1024) reduce_loss_kernel(const double *__restrict__ rowloss,
+                                                           const int32_t *__restrict__ rowerr, long rows,
+                                                           double *__restrict__ loss, int32_t *__restrict__ ferr) {
+    __shared__ double sl[1024];
+    __shared__ long se[1024];
+    double a = 0.0;
+    long e = 0;
+    for (long r = threadIdx.x; r < rows; r += 1024) { a += rowloss[r]; e += rowerr[r]; }
+    sl[threadIdx.x] = a;
+    se[threadIdx.x] = e;
+    __syncthreads();
+    for (int s = 512; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) { sl[threadIdx.x] += sl[threadIdx.x + s]; se[threadIdx.x] += se[threadIdx.x + s]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *loss = sl[0];
+        if (ferr) *ferr = (int32_t)se[0];
+    }
+}
+int reduce_loss(const double *rowloss, const int32_t *rowerr, long rows, double *loss, int32_t *ferr,
+                cudaStream_t st) {
+    reduce_loss_kernel<<<1, 1024, 0, st>>>(rowloss, rowerr, rows, loss, ferr);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- column sums of an fp16 matrix, two deterministic passes: out[k] += alpha * sum_r src[r,k] ----
+constexpr int CS_ROWS = 256;
+__global__ void colsum_pass1(const __half *__restrict__ src, long rows, int cols, long ld, float *__restrict__ part) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const long r0 = (long)blockIdx.y * CS_ROWS;
+    if (k >= cols) return;
+    float a = 0.f;
+    const long r1 = r0 + CS_ROWS < rows ? r0 + CS_ROWS : rows;
+    for (long r = r0; r < r1; ++r) a += __half2float(src[r * ld + k]);
+    part[(long)blockIdx.y * cols + k] = a;
+}
+__global__ void colsum_pass2(const float *__restrict__ part, int nchunks, int cols, float alpha,
+                             float *__restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= cols) return;
+    float a = 0.f;
+    for (int c = 0; c < nchunks; ++c) a += part[(long)c * cols + k];
+    out[k] += alpha * a;
+}
+size_t colsum_scratch_bytes(long rows, int cols) { return (size_t)((rows + CS_ROWS - 1) / CS_ROWS) * cols * 4; }
+int colsum_f16_add(const __half *src, long rows, int cols, long ld, float alpha, float *out, float *scratch,
+                   cudaStream_t st) {
+    const int nch = (int)((rows + CS_ROWS - 1) / CS_ROWS);
+    if (nch == 0) return 0;
+    dim3 g1((cols + 127) / 128, nch);
+    colsum_pass1<<<g1, 128, 0, st>>>(src, rows, cols, ld, scratch);
+    colsum_pass2<<<(cols + 127) / 128, 128, 0, st>>>(scratch, nch, cols, alpha, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- gradient scatter-add from kernel-private layouts to the flat theta layout ---------------
+// gW [Drows, 4H] += dWT[(d*4Hq + 4j+gamma) * ldw + r(src_row)]
+__global__ void scatter_w_kernel(float *__restrict__ gW, int Drows, int H, int Hq, const float *__restrict__ dWT,
+                                 long ldw, int d, int rowmode) {
+    const long n = (long)Drows * 4 * H;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int sr = (int)(i / (4 * H)), col = (int)(i - (long)sr * 4 * H);
+        const int gam = col / H, j = col - gam * H;
+        const int r = rowmode == 0 ? sr : (sr / H) * Hq + (sr % H);
+        gW[i] += dWT[((long)d * 4 * Hq + 4 * j + gam) * ldw + r];
+    }
+}
+int scatter_w(float *gW, int Drows, int H, int Hq, const float *dWT, long ldw, int d, int rowmode, cudaStream_t st) {
+    scatter_w_kernel<<<grid_for((long)Drows * 4 * H), 256, 0, st>>>(gW, Drows, H, Hq, dWT, ldw, d, rowmode);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+// gR [H, 4H] += dRT[(4j+gamma) * Hq + k]
+__global__ void scatter_r_kernel(float *__restrict__ gR, int H, int Hq, const float *__restrict__ dRT) {
+    const long n = (long)H * 4 * H;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int k = (int)(i / (4 * H)), col = (int)(i - (long)k * 4 * H);
+        const int gam = col / H, j = col - gam * H;
+        gR[i] += dRT[(long)(4 * j + gam) * Hq + k];
+    }
+}
+int scatter_r(float *gR, int H, int Hq, const float *dRT, cudaStream_t st) {
+    scatter_r_kernel<<<grid_for((long)H * 4 * H), 256, 0, st>>>(gR, H, Hq, dRT);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+// gb [4H] += sum_g dbpart[(d*G + g)*4Hq + 4j+gamma]
+__global__ void scatter_b_kernel(float *__restrict__ gb, int H, int Hq, const float *__restrict__ dbpart, int G,
+                                 int d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 4 * H; i += gridDim.x * blockDim.x) {
+        const int gam = i / H, j = i - gam * H;
+        float a = 0.f;
+        for (int g = 0; g < G; ++g) a += dbpart[((long)d * G + g) * 4 * Hq + 4 * j + gam];
+        gb[i] += a;
+    }
+}
+int scatter_b(float *gb, int H, int Hq, const float *dbpart, int G, int d, cudaStream_t st) {
+    scatter_b_kernel<<<grid_for(4 * H), 256, 0, st>>>(gb, H, Hq, dbpart, G, d);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+// gWo [2H, K] += dWoT[k * ldw + r(src)]
+__global__ void scatter_wout_kernel(float *__restrict__ gWo, int H, int Hq, int K, const float *__restrict__ dWoT,
+                                    long ldw) {
+    const long n = (long)2 * H * K;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int sr = (int)(i / K), k = (int)(i - (long)sr * K);
+        const int r = (sr / H) * Hq + (sr % H);
+        gWo[i] += dWoT[(long)k * ldw + r];
+    }
+}
+int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, cudaStream_t st) {
+    scatter_wout_kernel<<<grid_for((long)2 * H * K), 256, 0, st>>>(gWo, H, Hq, K, dWoT, ldw);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- dy_top [rows, 2H] -> dY [rows, 2Hq] (padded halves) ------------------------------------
+__global__ void pad_halves_kernel(const float *__restrict__ src, int H, int Hq, long rows, float *__restrict__ dst) {
+    const long n = rows * 2 * Hq;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long r = i / (2 * Hq);
+        const int c = (int)(i - r * 2 * Hq), half = c / Hq, j = c - half * Hq;
+        dst[i] = j < H ? src[r * 2 * H + half * H + j] : 0.f;
+    }
+}
+int pad_halves(const float *src, int H, int Hq, long rows, float *dst, cudaStream_t st) {
+    pad_halves_kernel<<<grid_for(rows * 2 * Hq), 256, 0, st>>>(src, H, Hq, rows, dst);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- dx [rows, ldx] (=|+=) dX [rows, ldX] for k < D ------------------------------------------
+__global__ void store_dx_kernel(float *__restrict__ dx, long ldx, const float *__restrict__ dX, long ldX, int D,
+                                long rows, int accum) {
+    const long n = rows * D;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long r = i / D;
+        const int k = (int)(i - r * D);
+        const float v = dX[r * ldX + k];
+        if (accum) dx[r * ldx + k] += v;
+        else dx[r * ldx + k] = v;
+    }
+}
+int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, int accum, cudaStream_t st) {
+    store_dx_kernel<<<grid_for(rows * D), 256, 0, st>>>(dx, ldx, dX, ldX, D, rows, accum);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- SGD (§4.3): theta -= lr * grad; optional grad = 0 ------------------------------
+__global__ void sgd_kernel(float *__restrict__ th, float *__restrict__ gr, long n, float lr, int zero) {
+    const long n4 = n >> 2;
+    float4 *t4 = reinterpret_cast<float4 *>(th);
+    float4 *g4 = reinterpret_cast<float4 *>(gr);
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+        float4 t = t4[i];
+        const float4 g = g4[i];
+        t.x -= lr * g.x; t.y -= lr * g.y; t.z -= lr * g.z; t.w -= lr * g.w;
+        t4[i] = t;
+        if (zero) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (long i = (n4 << 2) + blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        th[i] -= lr * gr[i];
+        if (zero) gr[i] = 0.f;
+    }
+}
+int sgd(float *theta, float *grad, long n, float lr, int zero, cudaStream_t st) {
+    sgd_kernel<<<grid_for(n / 4 + 1, 256, 148 * 8), 256, 0, st>>>(theta, grad, n, lr, zero);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+}  // namespace blstm

@@ -1,0 +1,35 @@
+// ops.h -- internal interface of the helper kernels (ops.cu).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace blstm {
+
+int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, cudaStream_t st);
+// rowmode 0: input rows are W rows (rows >= Drows are padding); 1: input rows are the padded
+// [fwd (Hq) | bwd (Hq)] halves of the layer below (row half*Hq + jj <-> W row half*H + jj).
+int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir, int Dn, int rowmode, __half *W16,
+           cudaStream_t st);
+int pack_rt(const float *R0, const float *R1, int H, int Hq, int ndir, __half *RT16, cudaStream_t st);
+int pack_bias(const float *b0, const float *b1, int H, int Hq, int ndir, float *bq, cudaStream_t st);
+int pack_wout(const float *Wo, const float *bo, int H, int Hq, int K, int Kp, __half *Wo16, float *boq,
+              cudaStream_t st);
+int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int ndir, int dir0, cudaStream_t st);
+int ce_head(const float *logits, long ldl, int K, int Kp, const uint8_t *mask, const int32_t *labels, float scale,
+            __half *dlog16, double *rowloss, int32_t *rowerr, long rows, cudaStream_t st);
+int reduce_loss(const double *rowloss, const int32_t *rowerr, long rows, double *loss, int32_t *ferr,
+                cudaStream_t st);
+size_t colsum_scratch_bytes(long rows, int cols);
+int colsum_f16_add(const __half *src, long rows, int cols, long ld, float alpha, float *out, float *scratch,
+                   cudaStream_t st);
+int scatter_w(float *gW, int Drows, int H, int Hq, const float *dWT, long ldw, int d, int rowmode, cudaStream_t st);
+int scatter_r(float *gR, int H, int Hq, const float *dRT, cudaStream_t st);
+int scatter_b(float *gb, int H, int Hq, const float *dbpart, int G, int d, cudaStream_t st);
+int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, cudaStream_t st);
+int pad_halves(const float *src, int H, int Hq, long rows, float *dst, cudaStream_t st);
+int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, int accum, cudaStream_t st);
+int sgd(float *theta, float *grad, long n, float lr, int zero, cudaStream_t st);
+
+}  // namespace blstm

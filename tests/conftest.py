@@ -16,3 +16,10 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_libraries():
+    """Build (no-op when up to date) the CUDA library and the C oracle once per session."""
+    import __graft_entry__
+    __graft_entry__.build()
