@@ -1,0 +1,346 @@
+"""Benchmark: BLSTM training frames/sec (fwd + BPTT + SGD) on N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl cuda|reference]
+
+One step = one full pass of the hot path over one
+batch: the 5-layer 500-unit BLSTM + 1501-class CE head training step of
+BASELINE.json configs[2] (81 chunks x 250 frames per GPU, §6 shape),
+synthetic speech-shaped data (paper_1608_00895_b200/synth.py).  For N > 1 the
+driver launches one process per GPU with torchrun; each rank trains on its own
+batch (data seed 1000 + rank) and gradients are summed over NVLink with NCCL
+every step (sync mode; --dp-mode avg --avg-k K for the paper's averaging).
+
+Prints ONE JSON line (rank 0).  value = valid frames processed by all ranks /
+max-over-ranks device time of exactly K steps (CUDA events, barrier + sync on
+both sides).  The per-step working set (~2.3 GB) exceeds the 126 MB L2, so no
+extra L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_1608_00895_b200 import synth  # noqa: E402
+from paper_1608_00895_b200.train import DPSchedule, rank_env  # noqa: E402
+
+METRIC = "BLSTM train frames/sec (fwd+BPTT) at 1/2/4/8 B200; % of roofline"
+UNIT = "frames/s"
+
+
+def workload_desc(cfg, world):
+    return {
+        "workload": (f"{cfg.name}: {cfg.L}-layer BLSTM {cfg.H} units/direction, {cfg.D}-dim input, "
+                     f"{cfg.K}-class softmax-CE, {cfg.B} chunks x {cfg.T} frames per GPU, fwd+BPTT+SGD"),
+        "L": cfg.L, "H": cfg.H, "D": cfg.D, "K": cfg.K, "T": cfg.T, "B_per_gpu": cfg.B,
+        "global_batch": cfg.B * world, "parallelism": f"dp{world}",
+        "l2": "no flush: per-step working set ~2.3 GB > 126 MB L2",
+    }
+
+
+# ----------------------------------------------------------------------------
+# algorithmic work
+# ----------------------------------------------------------------------------
+def alg_flops_per_frame(cfg):
+    H, K = cfg.H, cfg.K
+    f = 0
+    for l in range(cfg.L):
+        Dl = cfg.D if l == 0 else 2 * H
+        f += 2 * (8 * Dl * H + 8 * Dl * H + 8 * H * H)   # Z, dW, dR per direction
+        f += 2 * (8 * H * H + 8 * H * H)                 # recurrent fwd + bwd MMAs
+        if l > 0:
+            f += 2 * 8 * Dl * H                          # dX
+    f += 12 * H * K                                      # logits, dY, dW_out
+    return f
+
+
+def kernel_roofline(cat, total_ms, launches, cfg, V, peaks):
+    """achieved / peak of the dominant kernel category (per launch, algorithmic units)."""
+    H = cfg.H
+    if cat in (0, 1):          # recurrence: one launch per layer, both directions
+        flops = 2 * V * 8 * H * H
+        bytes_ = 2 * V * 40 * H
+    else:                      # GEMMs: all dense contractions of the step
+        flops = V * (alg_flops_per_frame(cfg) - cfg.L * 2 * 16 * H * H)
+        bytes_ = None
+    per_launch_s = total_ms / max(launches, 1) / 1e3
+    if cat == 2:
+        per_flops = flops / max(launches, 1)
+        a = per_flops / per_launch_s / 1e12
+        return {"bound": "tensor", "achieved": a, "peak": peaks["tf"], "unit": "TFLOP/s", "frac": a / peaks["tf"]}
+    a_tf = flops / per_launch_s / 1e12
+    a_gb = bytes_ / per_launch_s / 1e9
+    f_tf, f_gb = a_tf / peaks["tf"], a_gb / peaks["gbs"]
+    if f_gb >= f_tf:
+        return {"bound": "hbm", "achieved": a_gb, "peak": peaks["gbs"], "unit": "GB/s", "frac": f_gb,
+                "alt": {"bound": "tensor", "achieved": a_tf, "peak": peaks["tf"], "unit": "TFLOP/s", "frac": f_tf}}
+    return {"bound": "tensor", "achieved": a_tf, "peak": peaks["tf"], "unit": "TFLOP/s", "frac": f_tf,
+            "alt": {"bound": "hbm", "achieved": a_gb, "peak": peaks["gbs"], "unit": "GB/s", "frac": f_gb}}
+
+
+def measured_peaks():
+    p = {"gbs": 6549.8, "tf": 1378.5, "source": "MEASURED_PEAKS.json (hbm_gbs, bf16_tflops_sustained)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        p["gbs"] = float(j["hbm_gbs"])
+        p["tf"] = float(j.get("bf16_tflops_sustained", j["bf16_tflops"]))
+    except Exception:
+        p = {"gbs": 6650.0, "tf": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+    p["note"] = "fp16 dense peak taken = bf16 measured peak (nominal ratio 1)"
+    return p
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max((float(r[2]) for r in rows if r[2].replace(".", "").isdigit()), default=None)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------
+# the oracle, timed on the host cores (cpu_baseline / --impl reference)
+# ----------------------------------------------------------------------------
+def time_oracle(cfg, budget_s: float, rank: int = 0):
+    """frames/s of the fp64 oracle on a bounded sample (b chunks) of the same workload."""
+    import oracle
+    _, params, batch = synth.make_workload(cfg, rank)
+    theta = oracle.pack_params(params, cfg.L, cfg.D, cfg.H, cfg.K)
+
+    def run(b, T):
+        x = np.ascontiguousarray(batch.x[:T, :b])
+        m = np.ascontiguousarray(batch.mask[:T, :b])
+        lab = np.ascontiguousarray(batch.labels[:T, :b]) if cfg.K > 0 else None
+        dy = np.ascontiguousarray(batch.dy_top[:T, :b]) if cfg.K == 0 else None
+        t0 = time.perf_counter()
+        oracle.blstm_step(theta, x, m, cfg.L, cfg.H, cfg.K, labels=lab, dy_top=dy, lr=1e-5)
+        return time.perf_counter() - t0, int(m.sum())
+
+    cores = oracle.num_threads()
+    b = min(cfg.B, cores)                      # one chunk per host thread
+    dt, _ = run(b, 8)                          # calibration: cost per frame-step
+    T = int(np.clip(budget_s / max(dt / 8, 1e-6), 8, cfg.T))
+    dt, fr = run(b, T)
+    return {"value": fr / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"one training step (fwd+BPTT+SGD, fp64) of {cfg.name} restricted to {b} of its "
+                      f"{cfg.B} chunks and their first {T} of {cfg.T} frames ({fr} valid frames) in "
+                      f"{dt:.1f} s; OpenMP over batch rows / output rows"}
+
+
+def run_reference(args, cfg):
+    rank, _, world = rank_env()
+    if rank != 0:
+        return
+    budget = max(2.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        time_oracle(cfg, budget)
+    vals = [time_oracle(cfg, budget) for _ in range(args.steps)]
+    v = statistics.median(r["value"] for r in vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_desc(cfg, world),
+            "cpu_baseline": dict(vals[-1], value=v),
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# the CUDA path
+# ----------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--dp-mode", default="sync", choices=["sync", "avg"])
+    ap.add_argument("--avg-k", type=int, default=3)
+    ap.add_argument("--lr", type=float, default=1e-5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1608_00895_b200 import blstm
+    from paper_1608_00895_b200.train import StackTrainer, dp_comm_from_torch
+
+    rank, local, world = rank_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = dp_comm_from_torch(rank, world)
+    cfg, params, batch = synth.make_workload(cfg, rank)
+    tr = StackTrainer(cfg, params, batch, dev, lr=args.lr, comm=comm, world=world,
+                      sched=DPSchedule(args.dp_mode, args.avg_k if args.dp_mode == "avg" else 1))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def sum_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t.item()
+
+    for _ in range(args.warmup):
+        tr.step()
+    barrier()
+
+    # ---------------- device-resident timed region ----------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    n0 = blstm.blstm_launch_count()
+    blstm.blstm_profile_enable(True)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        tr.step()
+    e1.record(st)
+    barrier()
+    t_local = e0.elapsed_time(e1) / 1e3
+    launches = blstm.blstm_launch_count() - n0
+    prof = {c: blstm.blstm_profile_read(c) for c in (blstm.PROF_REC_FWD, blstm.PROF_REC_BWD, blstm.PROF_GEMM)}
+    blstm.blstm_profile_enable(False)
+    clk = clocks.stop()
+    t_max = max_over_ranks(t_local)
+    frames = sum_over_ranks(tr.valid_frames * args.steps)
+    value = frames / t_max
+
+    # ---------------- end to end: host buffers, H2D + D2H inside the timed region ----------------
+    ek = args.e2e_steps or args.steps
+    hx = torch.tensor(batch.x).pin_memory()
+    hm = torch.tensor(batch.mask).pin_memory()
+    hl = torch.tensor(batch.labels).pin_memory() if cfg.K > 0 else None
+    hloss = torch.zeros(1, dtype=torch.float64).pin_memory()
+    h2d = hx.numel() * 4 + hm.numel() + (hl.numel() * 4 if hl is not None else 0)
+    barrier()
+    e0.record(st)
+    for _ in range(ek):
+        tr.x.copy_(hx, non_blocking=True)
+        tr.mask.copy_(hm, non_blocking=True)
+        if hl is not None:
+            tr.labels.copy_(hl, non_blocking=True)
+        tr.step()
+        hloss.copy_(tr.loss, non_blocking=True)
+    e1.record(st)
+    barrier()
+    t_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    e2e_value = sum_over_ranks(tr.valid_frames * ek) / t_e2e
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = measured_peaks()
+    cats = {0: "lstm_rec_fwd", 1: "lstm_rec_bwd", 2: "gemm_f16 (all GEMMs)"}
+    dom = max(prof, key=lambda c: prof[c][0])
+    roof = kernel_roofline(dom, prof[dom][0], prof[dom][1], cfg, tr.valid_frames, peaks)
+    roof.update({"kernel": cats[dom], "traffic": None,
+                 "launch_ms": prof[dom][0] / max(prof[dom][1], 1),
+                 "share_of_step": prof[dom][0] / (t_local * 1e3),
+                 "peak_source": peaks["source"], "peak_note": peaks["note"]})
+    step_ms = t_max / args.steps * 1e3
+    V = tr.valid_frames
+    t_tc = V * alg_flops_per_frame(cfg) / (peaks["tf"] * 1e12) * 1e3
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16 MMA operands / f32 accumulate+state", "data": "synthetic",
+        "config": dict(workload_desc(cfg, world), valid_frames_per_gpu=V, dp_mode=args.dp_mode,
+                       **({"avg_k": args.avg_k} if args.dp_mode == "avg" else {})),
+        "roofline": roof,
+        "kernel_ms_per_step": {cats[c]: prof[c][0] / args.steps for c in prof},
+        "step_tensor_bound_ms": t_tc,
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8},
+        "clocks": clk,
+        "tflops_achieved": V * world * alg_flops_per_frame(cfg) * args.steps / t_max / 1e12,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = time_oracle(cfg, 15.0)
+        except Exception as e:  # the oracle is a reported baseline, never the product path
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -190,6 +190,18 @@ int dp_comm_destroy(dp_comm *c);
 int blstm_gemm_f16(int M, int N, int K, const void *A, long lda, int a_mn, const void *B, long ldb, int b_mn,
                    float *C, long ldc, float alpha, int beta, const float *bias, void *stream);
 
+/* ------------------------------------------------------------------------ */
+/* Measurement hooks (bench.py).                                              */
+/* ------------------------------------------------------------------------ */
+/* Number of kernels this library has launched since it was loaded. */
+long blstm_launch_count(void);
+/* on != 0: from now on bracket every launch of the categories below with CUDA
+ * events on the launching stream (records are reset); on == 0: stop. */
+int blstm_profile_enable(int on);
+/* cat: 0 forward recurrence, 1 BPTT recurrence, 2 GEMM.  Synchronizes the
+ * recorded events; returns the summed device time (ms) and launch count. */
+int blstm_profile_read(int cat, double *total_ms, long *launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,12 +94,19 @@ int ref_lstm_fwd(int T, int B, int D, int H, int dir,
                 for (int n = 0; n < G4; ++n) G[fr * G4 + n] = 0.0;
                 continue;
             }
+            /* a[n] = bias[n] + sum_d x[d] W[d][n] + sum_k h[k] R[k][n], each a[n] summed in
+             * ascending d then k (rows of W and R traversed contiguously) */
             double *a = (double *)malloc(sizeof(double) * G4);
-            for (int n = 0; n < G4; ++n) {
-                double acc = bias[n];
-                for (int d = 0; d < D; ++d) acc += x[fr * D + d] * W[(size_t)d * G4 + n];
-                for (int k = 0; k < H; ++k) acc += hb[k] * R[(size_t)k * G4 + n];
-                a[n] = acc;
+            for (int n = 0; n < G4; ++n) a[n] = bias[n];
+            for (int d = 0; d < D; ++d) {
+                const double xd = x[fr * D + d];
+                const double *Wd = W + (size_t)d * G4;
+                for (int n = 0; n < G4; ++n) a[n] += xd * Wd[n];
+            }
+            for (int k = 0; k < H; ++k) {
+                const double hk = hb[k];
+                const double *Rk = R + (size_t)k * G4;
+                for (int n = 0; n < G4; ++n) a[n] += hk * Rk[n];
             }
             for (int j = 0; j < H; ++j) {
                 const double i = sigm(a[j]);
@@ -184,26 +191,37 @@ int ref_lstm_bwd(int T, int B, int D, int H, int dir,
         }
     }
     const size_t TB = (size_t)T * B;
-    /* dW[d][n] += sum_{t,b} x[t,b,d] dA[t,b,n]  (ascending t, b) */
+    /* dW[d][n] += sum_{t,b} x[t,b,d] dA[t,b,n]  (each element summed over rows r = t*B+b in
+     * ascending order into a zeroed accumulator, then added) */
 #pragma omp parallel for schedule(static)
-    for (int d = 0; d < D; ++d)
-        for (int n = 0; n < G4; ++n) {
-            double acc = 0.0;
-            for (size_t r = 0; r < TB; ++r) acc += x[r * D + d] * dA[r * G4 + n];
-            dW[(size_t)d * G4 + n] += acc;
+    for (int d = 0; d < D; ++d) {
+        double *acc = (double *)calloc(G4, sizeof(double));
+        for (size_t r = 0; r < TB; ++r) {
+            const double xd = x[r * D + d];
+            const double *dar = dA + r * G4;
+            for (int n = 0; n < G4; ++n) acc[n] += xd * dar[n];
         }
+        for (int n = 0; n < G4; ++n) dW[(size_t)d * G4 + n] += acc[n];
+        free(acc);
+    }
     /* dR[k][n] += sum_{t,b} Hprev[t,b,k] dA[t,b,n] */
 #pragma omp parallel for schedule(static)
-    for (int k = 0; k < H; ++k)
-        for (int n = 0; n < G4; ++n) {
-            double acc = 0.0;
-            for (size_t r = 0; r < TB; ++r) acc += Hprev[r * H + k] * dA[r * G4 + n];
-            dR[(size_t)k * G4 + n] += acc;
+    for (int k = 0; k < H; ++k) {
+        double *acc = (double *)calloc(G4, sizeof(double));
+        for (size_t r = 0; r < TB; ++r) {
+            const double hk = Hprev[r * H + k];
+            const double *dar = dA + r * G4;
+            for (int n = 0; n < G4; ++n) acc[n] += hk * dar[n];
         }
-    for (int n = 0; n < G4; ++n) {
-        double acc = 0.0;
-        for (size_t r = 0; r < TB; ++r) acc += dA[r * G4 + n];
-        db[n] += acc;
+        for (int n = 0; n < G4; ++n) dR[(size_t)k * G4 + n] += acc[n];
+        free(acc);
+    }
+    {
+        double *acc = (double *)calloc(G4, sizeof(double));
+        for (size_t r = 0; r < TB; ++r)
+            for (int n = 0; n < G4; ++n) acc[n] += dA[r * G4 + n];
+        for (int n = 0; n < G4; ++n) db[n] += acc[n];
+        free(acc);
     }
     /* dx[t,b,d] = sum_n dA[t,b,n] W[d][n] */
     if (dx) {
@@ -308,11 +326,13 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
 #pragma omp parallel for schedule(static)
         for (long r = 0; r < (long)TB; ++r) {
             if (!mask[r]) continue;
+            /* logits[k] = b_out[k] + sum_j Y[r][j] W_out[j][k], ascending j */
             double *lg = dlog + (size_t)r * K;
-            for (int k = 0; k < K; ++k) {
-                double acc = bo[k];
-                for (size_t j = 0; j < W2; ++j) acc += YL[(size_t)r * W2 + j] * Wo[j * K + k];
-                lg[k] = acc;
+            for (int k = 0; k < K; ++k) lg[k] = bo[k];
+            for (size_t j = 0; j < W2; ++j) {
+                const double yj = YL[(size_t)r * W2 + j];
+                const double *Woj = Wo + j * K;
+                for (int k = 0; k < K; ++k) lg[k] += yj * Woj[k];
             }
             int am = 0;
             double m = lg[0];
@@ -329,16 +349,22 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
         for (size_t r = 0; r < TB; ++r) { lsum += rl[r]; ferr += re[r]; }
         /* dW_out[j][k] = sum_r Y[r][j] dlog[r][k]; db_out[k] = sum_r dlog[r][k] */
 #pragma omp parallel for schedule(static)
-        for (long j = 0; j < (long)W2; ++j)
-            for (int k = 0; k < K; ++k) {
-                double acc = 0.0;
-                for (size_t r = 0; r < TB; ++r) acc += YL[r * W2 + j] * dlog[r * K + k];
-                gWo[(size_t)j * K + k] += acc;
+        for (long j = 0; j < (long)W2; ++j) {
+            double *acc = (double *)calloc(K, sizeof(double));
+            for (size_t r = 0; r < TB; ++r) {
+                const double yrj = YL[r * W2 + j];
+                const double *dl = dlog + r * K;
+                for (int k = 0; k < K; ++k) acc[k] += yrj * dl[k];
             }
-        for (int k = 0; k < K; ++k) {
-            double acc = 0.0;
-            for (size_t r = 0; r < TB; ++r) acc += dlog[r * K + k];
-            gbo[k] += acc;
+            for (int k = 0; k < K; ++k) gWo[(size_t)j * K + k] += acc[k];
+            free(acc);
+        }
+        {
+            double *acc = (double *)calloc(K, sizeof(double));
+            for (size_t r = 0; r < TB; ++r)
+                for (int k = 0; k < K; ++k) acc[k] += dlog[r * K + k];
+            for (int k = 0; k < K; ++k) gbo[k] += acc[k];
+            free(acc);
         }
         /* dY[r][j] = sum_k dlog[r][k] W_out[j][k] */
 #pragma omp parallel for schedule(static)

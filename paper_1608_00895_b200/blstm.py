@@ -63,7 +63,28 @@ _SIGS = {
     "dp_comm_destroy": (_i, [_vp]),
     "blstm_gemm_f16": (_i, [_i, _i, _i, _vp, ctypes.c_long, _i, _vp, ctypes.c_long, _i, _vp, ctypes.c_long,
                             ctypes.c_float, _i, _vp, _vp]),
+    "blstm_launch_count": (ctypes.c_long, []),
+    "blstm_profile_enable": (_i, [_i]),
+    "blstm_profile_read": (_i, [_i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_long)]),
 }
+
+PROF_REC_FWD, PROF_REC_BWD, PROF_GEMM = 0, 1, 2
+
+
+def blstm_launch_count() -> int:
+    return int(lib().blstm_launch_count())
+
+
+def blstm_profile_enable(on: bool):
+    _check("blstm_profile_enable", lib().blstm_profile_enable(int(on)))
+
+
+def blstm_profile_read(cat: int):
+    """(total device ms, launches) of one launch category since profiling was enabled."""
+    ms = ctypes.c_double(0.0)
+    n = ctypes.c_long(0)
+    _check("blstm_profile_read", lib().blstm_profile_read(cat, ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value
 EXPORTS = tuple(_SIGS)
 
 

@@ -18,6 +18,7 @@
 //   MMAs of tile i+1.
 #include "common.cuh"
 #include "gemm.h"
+#include "prof.h"
 
 namespace blstm {
 
@@ -258,7 +259,9 @@ static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, con
     const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
     int grid = tiles < max_ctas ? tiles : max_ctas;
     if (grid < 1) grid = 1;
+    ProfScope ps(PROF_GEMM, st);
     gemm_f16_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, p);
+    note_launch();
     return cudaGetLastError();
 }
 

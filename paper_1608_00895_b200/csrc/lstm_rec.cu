@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "gemm.h"
 #include "lstm_rec.h"
+#include "prof.h"
 
 namespace blstm {
 
@@ -501,6 +502,8 @@ int lstm_rec_fwd(const RecParams &p, const __half *RT16, cudaStream_t st) {
     const size_t smem = fwd_smem(pl);
     cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * p.ndir * p.G, st);
     if (e != cudaSuccess) return -5;
+    ProfScope ps(PROF_REC_FWD, st);
+    note_launch();
     switch (p.N / 16) {
         case 1: e = launch_coop(lstm_rec_fwd_kernel<1>, grid, smem, st, tmR, tmH, p); break;
         case 2: e = launch_coop(lstm_rec_fwd_kernel<2>, grid, smem, st, tmR, tmH, p); break;
@@ -519,6 +522,8 @@ int lstm_rec_bwd(const RecParams &p, const __half *RT16, cudaStream_t st) {
     const size_t smem = bwd_smem(pl);
     cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * p.ndir * p.G, st);
     if (e != cudaSuccess) return -5;
+    ProfScope ps(PROF_REC_BWD, st);
+    note_launch();
     switch (p.N / 16) {
         case 1: e = launch_coop(lstm_rec_bwd_kernel<1>, grid, smem, st, tmR, p); break;
         case 2: e = launch_coop(lstm_rec_bwd_kernel<2>, grid, smem, st, tmR, p); break;

@@ -6,6 +6,7 @@
 // large side of each mapping.
 #include "common.cuh"
 #include "ops.h"
+#include "prof.h"
 
 namespace blstm {
 
@@ -27,6 +28,7 @@ __global__ void cast_x_kernel(const float *__restrict__ x, long ldx, int D, __ha
 }
 int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, cudaStream_t st) {
     cast_x_kernel<<<grid_for(rows * Dp), 256, 0, st>>>(x, ldx, D, x16, Dp, rows);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -55,6 +57,7 @@ __global__ void pack_w_kernel(const float *__restrict__ W0, const float *__restr
 int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir, int Dn, int rowmode, __half *W16,
            cudaStream_t st) {
     pack_w_kernel<<<grid_for((long)Dn * ndir * 4 * Hq), 256, 0, st>>>(W0, W1, Drows, H, Hq, ndir, Dn, rowmode, W16);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -73,6 +76,7 @@ __global__ void pack_rt_kernel(const float *__restrict__ R0, const float *__rest
 }
 int pack_rt(const float *R0, const float *R1, int H, int Hq, int ndir, __half *RT16, cudaStream_t st) {
     pack_rt_kernel<<<grid_for((long)ndir * 4 * Hq * Hq), 256, 0, st>>>(R0, R1, H, Hq, ndir, RT16);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -87,6 +91,7 @@ __global__ void pack_bias_kernel(const float *__restrict__ b0, const float *__re
 }
 int pack_bias(const float *b0, const float *b1, int H, int Hq, int ndir, float *bq, cudaStream_t st) {
     pack_bias_kernel<<<grid_for(ndir * 4 * Hq), 256, 0, st>>>(b0, b1, H, Hq, ndir, bq);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -104,6 +109,7 @@ __global__ void pack_wout_kernel(const float *__restrict__ Wo, const float *__re
 int pack_wout(const float *Wo, const float *bo, int H, int Hq, int K, int Kp, __half *Wo16, float *boq,
               cudaStream_t st) {
     pack_wout_kernel<<<grid_for((long)2 * Hq * Kp), 256, 0, st>>>(Wo, bo, H, Hq, K, Kp, Wo16, boq);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -123,6 +129,7 @@ __global__ void init_hist_kernel(__half *__restrict__ hist, const float *__restr
 }
 int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int ndir, int dir0, cudaStream_t st) {
     init_hist_kernel<<<grid_for((long)ndir * B * Hq), 256, 0, st>>>(hist, h0, T, B, H, Hq, ndir, dir0);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -190,6 +197,7 @@ int ce_head(const float *logits, long ldl, int K, int Kp, const uint8_t *mask, c
     if (rows <= 0) return 0;
     ce_head_kernel<<<(unsigned)rows, CE_THREADS, 0, st>>>(logits, ldl, K, Kp, mask, labels, scale, dlog16, rowloss,
                                                           rowerr);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -217,6 +225,7 @@ __global__ void __launch_bounds__(1024) reduce_loss_kernel(const double *__restr
 int reduce_loss(const double *rowloss, const int32_t *rowerr, long rows, double *loss, int32_t *ferr,
                 cudaStream_t st) {
     reduce_loss_kernel<<<1, 1024, 0, st>>>(rowloss, rowerr, rows, loss, ferr);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -247,6 +256,7 @@ int colsum_f16_add(const __half *src, long rows, int cols, long ld, float alpha,
     dim3 g1((cols + 127) / 128, nch);
     colsum_pass1<<<g1, 128, 0, st>>>(src, rows, cols, ld, scratch);
     colsum_pass2<<<(cols + 127) / 128, 128, 0, st>>>(scratch, nch, cols, alpha, out);
+    note_launch(2);
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -264,6 +274,7 @@ __global__ void scatter_w_kernel(float *__restrict__ gW, int Drows, int H, int H
 }
 int scatter_w(float *gW, int Drows, int H, int Hq, const float *dWT, long ldw, int d, int rowmode, cudaStream_t st) {
     scatter_w_kernel<<<grid_for((long)Drows * 4 * H), 256, 0, st>>>(gW, Drows, H, Hq, dWT, ldw, d, rowmode);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 // gR [H, 4H] += dRT[(4j+gamma) * Hq + k]
@@ -277,6 +288,7 @@ __global__ void scatter_r_kernel(float *__restrict__ gR, int H, int Hq, const fl
 }
 int scatter_r(float *gR, int H, int Hq, const float *dRT, cudaStream_t st) {
     scatter_r_kernel<<<grid_for((long)H * 4 * H), 256, 0, st>>>(gR, H, Hq, dRT);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 // gb [4H] += sum_g dbpart[(d*G + g)*4Hq + 4j+gamma]
@@ -291,6 +303,7 @@ __global__ void scatter_b_kernel(float *__restrict__ gb, int H, int Hq, const fl
 }
 int scatter_b(float *gb, int H, int Hq, const float *dbpart, int G, int d, cudaStream_t st) {
     scatter_b_kernel<<<grid_for(4 * H), 256, 0, st>>>(gb, H, Hq, dbpart, G, d);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 // gWo [2H, K] += dWoT[k * ldw + r(src)]
@@ -305,6 +318,7 @@ __global__ void scatter_wout_kernel(float *__restrict__ gWo, int H, int Hq, int 
 }
 int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, cudaStream_t st) {
     scatter_wout_kernel<<<grid_for((long)2 * H * K), 256, 0, st>>>(gWo, H, Hq, K, dWoT, ldw);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -319,6 +333,7 @@ __global__ void pad_halves_kernel(const float *__restrict__ src, int H, int Hq, 
 }
 int pad_halves(const float *src, int H, int Hq, long rows, float *dst, cudaStream_t st) {
     pad_halves_kernel<<<grid_for(rows * 2 * Hq), 256, 0, st>>>(src, H, Hq, rows, dst);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -336,6 +351,7 @@ __global__ void store_dx_kernel(float *__restrict__ dx, long ldx, const float *_
 }
 int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, int accum, cudaStream_t st) {
     store_dx_kernel<<<grid_for(rows * D), 256, 0, st>>>(dx, ldx, dX, ldX, D, rows, accum);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
@@ -358,6 +374,7 @@ __global__ void sgd_kernel(float *__restrict__ th, float *__restrict__ gr, long 
 }
 int sgd(float *theta, float *grad, long n, float lr, int zero, cudaStream_t st) {
     sgd_kernel<<<grid_for(n / 4 + 1, 256, 148 * 8), 256, 0, st>>>(theta, grad, n, lr, zero);
+    note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 

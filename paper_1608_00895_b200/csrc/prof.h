@@ -1,0 +1,21 @@
+// prof.h -- internal launch counting / event timing (prof.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace blstm {
+
+enum { PROF_REC_FWD = 0, PROF_REC_BWD = 1, PROF_GEMM = 2, PROF_OTHER = 3 };
+
+void note_launch(int n = 1);
+int prof_begin(int cat, cudaStream_t st);
+void prof_end(int idx, cudaStream_t st);
+
+// RAII bracket of one launch
+struct ProfScope {
+    int idx;
+    cudaStream_t st;
+    ProfScope(int cat, cudaStream_t s) : idx(prof_begin(cat, s)), st(s) {}
+    ~ProfScope() { prof_end(idx, st); }
+};
+
+}  // namespace blstm

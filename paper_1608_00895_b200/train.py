@@ -1,0 +1,188 @@
+"""Host-side driver of the training step: device buffers, one step
+(fwd + BPTT + update) through the C-ABI, and the data-parallel schedule.
+
+Data parallelism follows PAPER.md §4.1: one process per GPU, each
+with its own batches ("a user specified number of batches is assigned to each
+device") and a full parameter image.  Two exchange modes
+(R8):
+  sync    : gradients are summed over ranks every step (one big batch; the
+            paper's unscaled-gradient convention P:253-254), then SGD
+  avg(K)  : each rank makes K local SGD updates, then the parameters are
+            averaged (K=3 in fig:mgpu P:223-224)
+The schedule logic is backend-agnostic (``Collective``): NCCL through the C-ABI
+on GPUs, or torch.distributed (gloo) for the CPU tests of the N>1 path.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+
+def rank_env():
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    return rank, local, world
+
+
+# ----------------------------------------------------------------------------
+# DP schedule (backend-agnostic)
+# ----------------------------------------------------------------------------
+class Collective:
+    """In-place fp32 collectives over all ranks."""
+
+    def sum_(self, t):  # pragma: no cover - interface
+        raise NotImplementedError
+
+    def mean_(self, t):  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+class TorchCollective(Collective):
+    """torch.distributed collectives (gloo on CPU in the tests)."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def sum_(self, t):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    def mean_(self, t):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            t /= self.world
+
+
+class NcclCollective(Collective):
+    """The library's dp_* entry points (NCCL over NVLink)."""
+
+    def __init__(self, comm, world: int):
+        self.comm, self.world = comm, world
+
+    def sum_(self, t):
+        from . import blstm
+        if self.world > 1:
+            blstm.dp_allreduce_grads(self.comm, t)
+
+    def mean_(self, t):
+        from . import blstm
+        if self.world > 1:
+            blstm.dp_average_params(self.comm, t)
+
+
+@dataclass
+class DPSchedule:
+    mode: str = "sync"   # "sync" | "avg"
+    K: int = 1           # averaging interval (avg mode)
+
+    def __post_init__(self):
+        assert self.mode in ("sync", "avg") and self.K >= 1
+
+    def grads_summed(self) -> bool:
+        return self.mode == "sync"
+
+    def average_after(self, step_index: int) -> bool:
+        """True when parameters are averaged after local step `step_index` (0-based)."""
+        return self.mode == "avg" and (step_index + 1) % self.K == 0
+
+
+def dp_step(theta, grad, compute_grad: Callable[[object, object], None], update: Callable[[object, object], None],
+            coll: Collective, sched: DPSchedule, step_index: int):
+    """One data-parallel training step on this rank.
+
+    compute_grad(theta, grad) accumulates the local gradient into a zeroed grad;
+    update(theta, grad) applies SGD and zeroes grad.
+    """
+    compute_grad(theta, grad)
+    if sched.grads_summed():
+        coll.sum_(grad)
+    update(theta, grad)
+    if sched.average_after(step_index):
+        coll.mean_(theta)
+
+
+# ----------------------------------------------------------------------------
+# CUDA stack runner
+# ----------------------------------------------------------------------------
+def theta_from_params(params, desc) -> np.ndarray:
+    """Flatten synth.StackParams into the library's flat theta layout (fp32)."""
+    from . import blstm
+    n, offs = blstm.blstm_param_offsets(desc)
+    th = np.zeros(n, np.float32)
+    for l, (f, bw) in enumerate(params.layers):
+        for d, p in enumerate((f, bw)):
+            e = 6 * l + 3 * d
+            for q, a in enumerate((p.W, p.R, p.b)):
+                th[offs[e + q]: offs[e + q] + a.size] = a.ravel()
+    if desc.K > 0:
+        th[offs[6 * desc.L]: offs[6 * desc.L] + params.W_out.size] = params.W_out.ravel()
+        th[offs[6 * desc.L + 1]: offs[6 * desc.L + 1] + desc.K] = params.b_out
+    return th
+
+
+class StackTrainer:
+    """Device-resident training of one rank: theta, grad, workspace and a batch."""
+
+    def __init__(self, cfg, params, batch, device, lr: float = 1e-5, comm=None, world: int = 1,
+                 sched: Optional[DPSchedule] = None):
+        import torch
+        from . import blstm
+        self.torch, self.blstm = torch, blstm
+        self.cfg, self.dev, self.lr, self.world = cfg, device, lr, world
+        self.desc = blstm.stack_desc(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B)
+        self.theta = torch.tensor(theta_from_params(params, self.desc), device=device)
+        self.grad = torch.zeros_like(self.theta)
+        self.ws = torch.empty(blstm.blstm_stack_workspace_bytes(self.desc), dtype=torch.uint8, device=device)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=device)
+        self.ferr = torch.zeros(1, dtype=torch.int32, device=device)
+        self.comm = comm
+        self.sched = sched or DPSchedule()
+        self.coll = NcclCollective(comm, world) if comm is not None else None
+        self.set_batch(batch)
+        self.steps_done = 0
+
+    def set_batch(self, batch):
+        t = self.torch
+        self.x = t.tensor(batch.x, device=self.dev)
+        self.mask = t.tensor(batch.mask, device=self.dev)
+        self.labels = t.tensor(batch.labels, device=self.dev) if self.cfg.K > 0 else None
+        self.dy_top = t.tensor(batch.dy_top, device=self.dev) if self.cfg.K == 0 else None
+        self.valid_frames = int(batch.mask.sum())
+
+    def _grad(self, theta, grad):
+        # sync mode: the library allreduce-sums grad right after the local accumulation
+        comm = self.comm if (self.comm is not None and self.sched.grads_summed()) else None
+        self.blstm.blstm_stack_fwd_bwd(self.desc, theta, grad, self.x, self.mask, self.labels, self.dy_top,
+                                       self.loss, self.ferr, comm, self.ws)
+
+    def _update(self, theta, grad):
+        self.blstm.sgd_update(theta, grad, self.lr, zero_grad=True)
+
+    def step(self):
+        class _NoSum(Collective):  # the sum already happened inside blstm_stack_fwd_bwd
+            def __init__(s, inner): s.inner = inner
+            def sum_(s, t): pass
+            def mean_(s, t):
+                if s.inner is not None:
+                    s.inner.mean_(t)
+        dp_step(self.theta, self.grad, self._grad, self._update, _NoSum(self.coll), self.sched, self.steps_done)
+        self.steps_done += 1
+
+
+def dp_comm_from_torch(rank: int, world: int):
+    """NCCL communicator of the library, its id broadcast over the torch process group."""
+    import torch
+    import torch.distributed as dist
+    from . import blstm
+    if world == 1:
+        return None
+    uid = blstm.dp_get_unique_id() if rank == 0 else bytes(128)
+    t = torch.tensor(list(uid), dtype=torch.uint8, device=f"cuda:{torch.cuda.current_device()}")
+    dist.broadcast(t, src=0)
+    return blstm.dp_comm_init(world, rank, bytes(t.cpu().tolist()))

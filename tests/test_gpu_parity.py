@@ -28,8 +28,14 @@ def test_gemm_tcgen05_matches_torch(a_mn, b_mn, M, N, K):
     ref = A.float() @ Bm.float().T
     bias = torch.randn(N, generator=g)
     ref_b = 0.5 * ref + bias
-    Ad = (A.T.contiguous() if a_mn else A).to(dev())
-    Bd = (Bm.T.contiguous() if b_mn else Bm).to(dev())
+    def padded(X):  # row stride a multiple of 8 elements (TMA: 16-byte strides)
+        r, c = X.shape
+        buf = torch.zeros(r, (c + 7) // 8 * 8, dtype=X.dtype)
+        buf[:, :c] = X
+        return buf.to(dev())[:, :c]
+
+    Ad = padded(A.T.contiguous() if a_mn else A)
+    Bd = padded(Bm.T.contiguous() if b_mn else Bm)
     C = torch.zeros(M, N, device=dev())
     blstm.blstm_gemm_f16(Ad, a_mn, Bd, b_mn, C, M, N, K, alpha=0.5, bias=bias.to(dev()))
     torch.cuda.synchronize()
