@@ -171,6 +171,7 @@ extern "C" int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     TRY(pack_rt(R, nullptr, g.H, g.Hq, 1, rt16, st), "pack_rt");
     TRY(pack_bias(b, nullptr, g.H, g.Hq, 1, bq, st), "pack_bias");
     GemmParams gp{(int)g.TB, 4 * g.Hq, g.Dp, Z, 4L * g.Hq, 1.f, 0, bq, 0, 0};
+    gp.remapB = g.B;  // Z time-major transposed [T][4Hq][B] for the recurrence
     TRY(gemm_f16({x16, g.Dp, 0}, {w16, 4L * g.Hq, 1}, gp, 0, st), "gemm Z");
     __half *hist = (__half *)(res + rv.hist);
     TRY(init_hist(hist, h0, g.T, g.B, g.H, g.Hq, 1, d->direction, st), "init_hist");
@@ -381,6 +382,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
         const long lda = l == 0 ? g.Dp0 : 2L * Hq;
         GemmParams gp{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
+        gp.remapB = g.B;  // Z time-major transposed [T][8Hq][B] for the recurrence
         TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gp, 0, st), "gemm Z");
         __half *hist = (__half *)(ws + w.hist[l]);
         TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");

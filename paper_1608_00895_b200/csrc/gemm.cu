@@ -159,7 +159,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
                 tmem_ld_wait();
                 const int n = n0 + c;
-                if (m < p.M && n < p.N) {
+                if (m < p.M && n < p.N && p.remapB) {
+                    // time-major transposed output: row m = t*B + b -> C[(t*ldc + col)*B + b]
+                    const long t = m / p.remapB, b = m - t * p.remapB;
+                    float *base = p.C + (size_t)t * p.ldc * p.remapB + b;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (n + j < p.N) {
+                            float o = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
+                            float *dst = base + (size_t)(n + j) * p.remapB;
+                            if (p.beta) o += *dst;
+                            *dst = o;
+                        }
+                } else if (m < p.M && n < p.N) {
                     if (n + 16 <= p.N && (p.ldc & 3) == 0) {
 #pragma unroll
                         for (int j = 0; j < 16; j += 4) {
@@ -177,11 +189,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                             *dst = o;
                         }
                     } else {
-                        for (int j = 0; j < 16 && n + j < p.N; ++j) {
-                            float o = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
-                            if (p.beta) o += crow[n + j];
-                            crow[n + j] = o;
-                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (n + j < p.N) {
+                                float o = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
+                                if (p.beta) o += crow[n + j];
+                                crow[n + j] = o;
+                            }
                     }
                 }
             }

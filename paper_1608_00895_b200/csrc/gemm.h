@@ -19,6 +19,8 @@ struct GemmParams {
     int beta;           // 1: C += result
     const float *bias;  // [N] or nullptr
     int a_mn, b_mn;     // filled by gemm_f16
+    long remapB = 0;    // > 0: rows are frames m = t*remapB + b and C is written time-major
+                        // transposed, C[(t*ldc + n)*remapB + b] (ldc = number of columns)
 };
 
 int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &p, int max_ctas, cudaStream_t st);

@@ -6,7 +6,9 @@
 // Decomposition: CTA (d, g, c) owns hidden units [32c, 32c+32) of
 // direction d for batch group g.  Its 128 gate rows of R^T (gate-interleaved, row 4*jl+gamma)
 // stay resident in shared memory for the whole sequence as the tcgen05 A operand.
-// Per step:
+// 16 warps: warp w reads TMEM lane quarter q = w%4 (8 units x 4 gates) for the batch
+// columns of block cb = w/4 (N/4 columns), so the per-step epilogue is spread over 4 warps
+// per scheduler.  Per step:
 //   forward : D[128 x N] = R^T_slice[128 x Hq] . h_{t-1}^T  (h from the group's history buffer,
 //             TMA-loaded after the group barrier), + Z_t, gates, cell update, mask in registers,
 //             h_t published to the history buffer, group barrier (gpu-scope counter).
@@ -21,10 +23,37 @@
 
 namespace blstm {
 
+constexpr int REC_THREADS = 512;
+
 static DEVI uint8_t *align1024(uint8_t *p) { return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023); }
 
 static __host__ __device__ constexpr uint32_t tmem_cols_for(int cols) {
     return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+}
+
+// 32 lanes x NC columns of TMEM -> registers (thread i: lane base+i)
+template <int NC>
+DEVI void tmem_ld(uint32_t taddr, float (&v)[NC]) {
+    uint32_t r[NC];
+    if constexpr (NC == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                     : "r"(taddr));
+    } else if constexpr (NC == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                       "=r"(r[7])
+                     : "r"(taddr));
+    } else {
+        static_assert(NC == 16, "tmem_ld: 4, 8 or 16 columns");
+        float t[16];
+        tmem_ld16(taddr, t);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(t[i]);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < NC; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // 4x4 transpose inside each group of 4 lanes: lane gam holds a[k] = gate gam at batch column
@@ -44,11 +73,14 @@ DEVI void xpose4(const float (&a)[4], float (&b)[4], int gam) {
     }
 }
 
-// activation of gate row gam: tanh for g (gam == 2, via 2*sigmoid(2x)-1), sigmoid otherwise;
-// one code path for all lanes (no divergence).
+// Gate nonlinearities in fp32 with the hardware exp2 (relative error ~1e-7, far inside the
+// fp16-operand budget; R9): sigmoid(z) = 1/(1+e^-z), tanh(z) = 2 sigmoid(2z) - 1.
+DEVI float sigm_f(float z) { return __fdividef(1.f, 1.f + __expf(-z)); }
+DEVI float tanh_f(float z) { return 2.f * sigm_f(2.f * z) - 1.f; }
+// activation of gate row gam (tanh for g, sigmoid otherwise) without lane divergence
 DEVI float gate_act(float pre, int gam) {
     const bool is_g = gam == 2;
-    const float s = sigmoidf_acc(is_g ? 2.f * pre : pre);
+    const float s = sigm_f(is_g ? 2.f * pre : pre);
     return is_g ? 2.f * s - 1.f : s;
 }
 
@@ -56,11 +88,12 @@ DEVI float gate_act(float pre, int gam) {
 // forward
 // ---------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(REC_THREADS, 1)
     lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmH,
                         RecParams p) {
-    constexpr int N = 16 * NT;
-    constexpr int NM = N / 4;
+    constexpr int N = 16 * NT;   // MMA N = padded batch columns of the group
+    constexpr int NQ = N / 4;    // columns handled by one warp
+    constexpr int NMQ = NQ / 4;  // columns owned (cell state) by one thread
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     const int Hq = p.Hq, KB = Hq / 64;
@@ -73,13 +106,16 @@ __global__ void __launch_bounds__(128, 1)
     const int g = (blockIdx.x / p.NC) % p.G;
     const int d = blockIdx.x / (p.NC * p.G);
     const int dir = d == 0 ? p.dir0 : -1;
-    const int q = warp_id(), l = lane_id();
+    const int w = warp_id(), q = w & 3, cb = w >> 2, l = lane_id();
     const int jl = 8 * q + (l >> 2), gam = l & 3;
     const int j = c * REC_UNITS + jl;
     const bool unit_ok = j < p.H;
-    const long zcol = (long)d * 4 * Hq + 4 * j + gam;
-    const int b0 = g * p.Bg;
-    const int B = p.B, T = p.T;
+    const int B = p.B, T = p.T, H = p.H;
+    const long NROW = (long)p.ndir * 4 * Hq;
+    const long zrow = (long)d * 4 * Hq + 4 * j + gam;
+    const int b0 = g * p.Bg;        // first batch row of the group
+    const int nq0 = cb * NQ;        // first column of this warp
+    const int bq0 = b0 + nq0;       // its first batch row
     uint32_t *counter = p.counters + d * p.G + g;
     constexpr uint32_t TCOLS = tmem_cols_for(N);
 
@@ -88,7 +124,7 @@ __global__ void __launch_bounds__(128, 1)
         mbar_init(&bars[1], 1);
         fence_mbar_init();
     }
-    if (q == 0) {
+    if (w == 0) {
         tmem_alloc(tslot, TCOLS);
         tmem_relinquish();
     }
@@ -98,11 +134,11 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t tmem = *tslot;
     const uint32_t idesc = idesc_f16(128, N, 0, 0);
 
-    // valid batch columns of this group (bit n)
-    uint64_t colmask = 0;
+    // valid columns of this warp (bit i <-> column nq0 + i)
+    uint32_t cm = 0;
 #pragma unroll
-    for (int n = 0; n < N; ++n)
-        if (n < p.Bg && b0 + n < B) colmask |= 1ull << n;
+    for (int i = 0; i < NQ; ++i)
+        if (nq0 + i < p.Bg && bq0 + i < B) cm |= 1u << i;
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmR);
@@ -113,20 +149,20 @@ __global__ void __launch_bounds__(128, 1)
     }
     uint32_t tma_phase = 1, mma_phase = 0;
 
-    float c_st[NM], h_st[NM];
+    float c_st[NMQ], h_st[NMQ];
 #pragma unroll
-    for (int m = 0; m < NM; ++m) {
-        const int n = 4 * m + gam, b = b0 + n;
-        const bool ok = ((colmask >> n) & 1) && unit_ok;
-        c_st[m] = (ok && p.c0) ? p.c0[(long)d * B * p.H + (long)b * p.H + j] : 0.f;
-        h_st[m] = (ok && p.h0) ? p.h0[(long)d * B * p.H + (long)b * p.H + j] : 0.f;
+    for (int m = 0; m < NMQ; ++m) {
+        const int i = 4 * m + gam, b = bq0 + i;
+        const bool ok = ((cm >> i) & 1) && unit_ok;
+        c_st[m] = (ok && p.c0) ? p.c0[(long)d * B * H + (long)b * H + j] : 0.f;
+        h_st[m] = (ok && p.h0) ? p.h0[(long)d * B * H + (long)b * H + j] : 0.f;
     }
 
-    float zv[N];
+    float zv[NQ];
     auto prefetch_z = [&](int t) {
+        const float *zp = p.Z + ((long)t * NROW + zrow) * B + bq0;
 #pragma unroll
-        for (int n = 0; n < N; ++n)
-            zv[n] = ((colmask >> n) & 1) ? __ldg(p.Z + (long)(t * B + b0 + n) * p.ldz + zcol) : 0.f;
+        for (int i = 0; i < NQ; ++i) zv[i] = ((cm >> i) & 1) ? __ldg(zp + i) : 0.f;
     };
     if (T > 0) prefetch_z(dir > 0 ? 0 : T - 1);
 
@@ -150,76 +186,66 @@ __global__ void __launch_bounds__(128, 1)
             mma_commit(&bars[1]);
         }
         tma_phase ^= 1;
-        // frame-valid bits of this step (lane n holds mask of column n)
-        uint64_t frm = 0;
-        {
-            const int n0 = l, n1 = l + 32;
-            const bool v0 = n0 < N && ((colmask >> n0) & 1) && p.mask[(long)t * B + b0 + n0];
-            const bool v1 = n1 < N && ((colmask >> n1) & 1) && p.mask[(long)t * B + b0 + n1];
-            frm = (uint64_t)__ballot_sync(0xffffffffu, v0) | ((uint64_t)__ballot_sync(0xffffffffu, v1) << 32);
-        }
+        // frame-valid bits of this warp's columns (lane i reads the mask of column i)
+        const uint32_t frm =
+            __ballot_sync(0xffffffffu, l < NQ && ((cm >> l) & 1) && p.mask[(long)t * B + bq0 + l]);
         const int wslot = t + (dir > 0 ? 1 : 0);
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
 
-        float act[N];
+        float act[NQ];
+        {
+            float v[NQ];
+            tmem_ld<NQ>(tmem + ((uint32_t)(32 * q) << 16) + nq0, v);
 #pragma unroll
-        for (int ch = 0; ch < NT; ++ch) {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + 16 * ch, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) act[16 * ch + i] = gate_act(v[i] + zv[16 * ch + i], gam);
+            for (int i = 0; i < NQ; ++i) act[i] = gate_act(v[i] + zv[i], gam);
         }
         tc_fence_before();
-        // save activations (the BPTT kernel's "reserve"), coalesced along gate rows
+        // saved activations for BPTT, time-major [t][gate row][b]: contiguous per thread
+        {
+            __half *gp = p.gates + ((long)t * NROW + zrow) * B + bq0;
 #pragma unroll
-        for (int n = 0; n < N; ++n)
-            if ((colmask >> n) & 1) {
-                const bool fm = ((frm >> n) & 1) && unit_ok;
-                p.gates[(long)(t * B + b0 + n) * p.ldg + zcol] = __float2half_rn(fm ? act[n] : 0.f);
-            }
+            for (int i = 0; i < NQ; ++i)
+                if ((cm >> i) & 1) gp[i] = __float2half_rn((((frm >> i) & 1) && unit_ok) ? act[i] : 0.f);
+        }
 #pragma unroll
-        for (int m = 0; m < NM; ++m) {
+        for (int m = 0; m < NMQ; ++m) {
             float a4[4] = {act[4 * m], act[4 * m + 1], act[4 * m + 2], act[4 * m + 3]};
             float gv[4];
-            xpose4(a4, gv, gam);  // gv = (i, f, g, o) of unit j at column n = 4m + gam
-            const int n = 4 * m + gam;
-            const bool fm = ((frm >> n) & 1) && unit_ok;
+            xpose4(a4, gv, gam);  // gv = (i, f, g, o) of unit j at column 4m + gam
+            const int i = 4 * m + gam;
+            const bool fm = ((frm >> i) & 1) && unit_ok;
             if (fm) {
                 const float cn = gv[1] * c_st[m] + gv[0] * gv[2];
                 c_st[m] = cn;
-                h_st[m] = gv[3] * tanhf(cn);
+                h_st[m] = gv[3] * tanh_f(cn);
             }
-            if ((colmask >> n) & 1) {
-                const long row = (long)t * B + b0 + n;
+            if ((cm >> i) & 1) {
+                const long row = (long)t * B + bq0 + i;
                 if (unit_ok) {
                     if (p.y) p.y[row * p.ldy + d * p.y_doff + j] = fm ? h_st[m] : 0.f;
                     p.C[row * p.ldc + d * p.c_doff + j] = c_st[m];
                 }
                 if (p.y16) p.y16[row * p.ldy16 + (long)d * Hq + j] = __float2half_rn(fm ? h_st[m] : 0.f);
-                p.hist[(((long)d * (T + 1) + wslot) * B + b0 + n) * Hq + j] = __float2half_rn(h_st[m]);
+                p.hist[(((long)d * (T + 1) + wslot) * B + bq0 + i) * Hq + j] = __float2half_rn(h_st[m]);
             }
         }
         if (s + 1 < T) prefetch_z(dir > 0 ? t + 1 : t - 1);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            red_release_gpu_add(counter, 1u);
-        }
+        if (threadIdx.x == 0) red_release_gpu_add(counter, 1u);
     }
 #pragma unroll
-    for (int m = 0; m < NM; ++m) {
-        const int n = 4 * m + gam, b = b0 + n;
-        if (((colmask >> n) & 1) && unit_ok) {
-            if (p.hT) p.hT[(long)d * B * p.H + (long)b * p.H + j] = h_st[m];
-            if (p.cT) p.cT[(long)d * B * p.H + (long)b * p.H + j] = c_st[m];
+    for (int m = 0; m < NMQ; ++m) {
+        const int i = 4 * m + gam, b = bq0 + i;
+        if (((cm >> i) & 1) && unit_ok) {
+            if (p.hT) p.hT[(long)d * B * H + (long)b * H + j] = h_st[m];
+            if (p.cT) p.cT[(long)d * B * H + (long)b * H + j] = c_st[m];
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (q == 0) {
+    if (w == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, TCOLS);
     }
@@ -229,10 +255,11 @@ __global__ void __launch_bounds__(128, 1)
 // backward through time
 // ---------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(REC_THREADS, 1)
     lstm_rec_bwd_kernel(const __grid_constant__ CUtensorMap tmR, RecParams p) {
     constexpr int N = 16 * NT;
-    constexpr int NM = N / 4;
+    constexpr int NQ = N / 4;
+    constexpr int NMQ = NQ / 4;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     const int Hq = p.Hq, KB = Hq / 64, MT = Hq / 128;
@@ -245,13 +272,16 @@ __global__ void __launch_bounds__(128, 1)
     const int g = (blockIdx.x / p.NC) % p.G;
     const int d = blockIdx.x / (p.NC * p.G);
     const int dir = d == 0 ? p.dir0 : -1;
-    const int q = warp_id(), l = lane_id();
+    const int w = warp_id(), q = w & 3, cb = w >> 2, l = lane_id();
     const int jl = 8 * q + (l >> 2), gam = l & 3;
     const int j = c * REC_UNITS + jl;
     const bool unit_ok = j < p.H;
-    const long gcol = (long)d * 4 * Hq + 4 * j + gam;
-    const int b0 = g * p.Bg;
     const int B = p.B, T = p.T, H = p.H, NC = p.NC;
+    const long NROW = (long)p.ndir * 4 * Hq;
+    const long grow = (long)d * 4 * Hq + 4 * j + gam;
+    const int b0 = g * p.Bg;
+    const int nq0 = cb * NQ;
+    const int bq0 = b0 + nq0;
     uint32_t *counter = p.counters + d * p.G + g;
     const uint32_t TCOLS = tmem_cols_for(MT * N);
     const float inv_scale = 1.f / (float)(1 << DA_SHIFT);
@@ -262,7 +292,7 @@ __global__ void __launch_bounds__(128, 1)
         mbar_init(&bars[1], 1);
         fence_mbar_init();
     }
-    if (q == 0) {
+    if (w == 0) {
         tmem_alloc(tslot, TCOLS);
         tmem_relinquish();
     }
@@ -272,10 +302,10 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t tmem = *tslot;
     const uint32_t idesc = idesc_f16(128, N, 1, 0);
 
-    uint64_t colmask = 0;
+    uint32_t cm = 0;
 #pragma unroll
-    for (int n = 0; n < N; ++n)
-        if (n < p.Bg && b0 + n < B) colmask |= 1ull << n;
+    for (int i = 0; i < NQ; ++i)
+        if (nq0 + i < p.Bg && bq0 + i < B) cm |= 1u << i;
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmR);
@@ -285,23 +315,23 @@ __global__ void __launch_bounds__(128, 1)
     }
     __syncthreads();
 
-    float dh[NM], dc[NM], dbp[4] = {0.f, 0.f, 0.f, 0.f};
-    uint32_t pfm = 0;  // bit m: the frame processed in the previous step was valid for column 4m+gam
+    float dh[NMQ], dc[NMQ], dbp[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t pfm = 0;  // bit m: the previous step's frame was valid for owned column 4m+gam
 #pragma unroll
-    for (int m = 0; m < NM; ++m) {
-        const int n = 4 * m + gam, b = b0 + n;
-        const bool ok = ((colmask >> n) & 1) && unit_ok;
+    for (int m = 0; m < NMQ; ++m) {
+        const int i = 4 * m + gam, b = bq0 + i;
+        const bool ok = ((cm >> i) & 1) && unit_ok;
         dh[m] = (ok && p.dhT) ? p.dhT[(long)d * B * H + (long)b * H + j] : 0.f;
         dc[m] = (ok && p.dcT) ? p.dcT[(long)d * B * H + (long)b * H + j] : 0.f;
     }
     const size_t pstride_buf = (size_t)p.ndir * p.G * NC * Hq * N;
     auto gather = [&](int buf) {
-        const float *Pb = p.P + buf * pstride_buf + (((size_t)d * p.G + g) * NC) * Hq * N;
+        const float *Pb = p.P + buf * pstride_buf + (((size_t)d * p.G + g) * NC) * Hq * N + (size_t)j * N + nq0;
 #pragma unroll
-        for (int m = 0; m < NM; ++m) {
+        for (int m = 0; m < NMQ; ++m) {
             if ((pfm >> m) & 1) {
                 float acc = 0.f;
-                for (int cc = 0; cc < NC; ++cc) acc += Pb[((size_t)cc * Hq + j) * N + 4 * m + gam];
+                for (int cc = 0; cc < NC; ++cc) acc += Pb[(size_t)cc * Hq * N + 4 * m + gam];
                 dh[m] = acc * inv_scale;
             }
         }
@@ -313,30 +343,27 @@ __global__ void __launch_bounds__(128, 1)
         const int t = dir > 0 ? s : T - 1 - s;
         const int k_done = T - 1 - s;
         // ---- this step's saved state (independent of the recurrence: issue first) ----
-        float graw[N];
+        float graw[NQ];
+        {
+            const __half *gp = p.gates + ((long)t * NROW + grow) * B + bq0;
 #pragma unroll
-        for (int n = 0; n < N; ++n)
-            graw[n] = ((colmask >> n) & 1) ? __half2float(p.gates[(long)(t * B + b0 + n) * p.ldg + gcol]) : 0.f;
-        float ct[NM], cp[NM], dyv[NM];
+            for (int i = 0; i < NQ; ++i) graw[i] = ((cm >> i) & 1) ? __half2float(gp[i]) : 0.f;
+        }
+        float ct[NMQ], cp[NMQ], dyv[NMQ];
         const int tp = t - dir;
 #pragma unroll
-        for (int m = 0; m < NM; ++m) {
-            const int n = 4 * m + gam, b = b0 + n;
-            const bool ok = ((colmask >> n) & 1) && unit_ok;
+        for (int m = 0; m < NMQ; ++m) {
+            const int i = 4 * m + gam, b = bq0 + i;
+            const bool ok = ((cm >> i) & 1) && unit_ok;
             const long row = (long)t * B + b;
             ct[m] = ok ? p.C[row * p.ldc + d * p.c_doff + j] : 0.f;
             if (ok && tp >= 0 && tp < T) cp[m] = p.C[((long)tp * B + b) * p.ldc + d * p.c_doff + j];
             else cp[m] = (ok && p.c0) ? p.c0[(long)d * B * H + (long)b * H + j] : 0.f;
             dyv[m] = ok ? p.dy[row * p.lddy + d * p.dy_doff + j] : 0.f;
         }
-        uint64_t frm = 0;
-        {
-            const int n0 = l, n1 = l + 32;
-            const bool v0 = n0 < N && ((colmask >> n0) & 1) && p.mask[(long)t * B + b0 + n0];
-            const bool v1 = n1 < N && ((colmask >> n1) & 1) && p.mask[(long)t * B + b0 + n1];
-            frm = (uint64_t)__ballot_sync(0xffffffffu, v0) | ((uint64_t)__ballot_sync(0xffffffffu, v1) << 32);
-        }
-        // ---- dh_{t} from the previous step's partials ----
+        const uint32_t frm =
+            __ballot_sync(0xffffffffu, l < NQ && ((cm >> l) & 1) && p.mask[(long)t * B + bq0 + l]);
+        // ---- dh_t from the previous step's partials ----
         if (k_done > 0) {
             if (threadIdx.x == 0) spin_until_geq(counter, (uint32_t)(NC * k_done));
             __syncthreads();
@@ -345,21 +372,21 @@ __global__ void __launch_bounds__(128, 1)
         // ---- gate gradients ----
         pfm = 0;
 #pragma unroll
-        for (int m = 0; m < NM; ++m) {
+        for (int m = 0; m < NMQ; ++m) {
             float a4[4] = {graw[4 * m], graw[4 * m + 1], graw[4 * m + 2], graw[4 * m + 3]};
             float gv[4];
             xpose4(a4, gv, gam);
-            const int n = 4 * m + gam;
-            const bool fm = ((frm >> n) & 1) && unit_ok;
+            const int i = 4 * m + gam, n = nq0 + i;
+            const bool fm = ((frm >> i) & 1) && unit_ok;
             float da0 = 0.f, da1 = 0.f, da2 = 0.f, da3 = 0.f;
             if (fm) {
-                const float i = gv[0], f = gv[1], gg = gv[2], o = gv[3];
-                const float th = tanhf(ct[m]);
+                const float ig = gv[0], f = gv[1], gg = gv[2], o = gv[3];
+                const float th = tanh_f(ct[m]);
                 const float dH = dh[m] + dyv[m];
                 const float dC = dc[m] + dH * o * (1.f - th * th);
-                da0 = dC * gg * i * (1.f - i);
+                da0 = dC * gg * ig * (1.f - ig);
                 da1 = dC * cp[m] * f * (1.f - f);
-                da2 = dC * i * (1.f - gg * gg);
+                da2 = dC * ig * (1.f - gg * gg);
                 da3 = dH * th * o * (1.f - o);
                 dc[m] = dC * f;
                 dbp[0] += da0; dbp[1] += da1; dbp[2] += da2; dbp[3] += da3;
@@ -371,8 +398,8 @@ __global__ void __launch_bounds__(128, 1)
             pk.x = *reinterpret_cast<uint32_t *>(&lo);
             pk.y = *reinterpret_cast<uint32_t *>(&hi);
             *reinterpret_cast<uint2 *>(dAs + sw128_offset(n, 4 * jl, N)) = pk;
-            if ((colmask >> n) & 1)
-                *reinterpret_cast<uint2 *>(p.dA + ((long)t * B + b0 + n) * p.ldda + (long)d * 4 * Hq + 4 * j) = pk;
+            if ((cm >> i) & 1)
+                *reinterpret_cast<uint2 *>(p.dA + ((long)t * B + bq0 + i) * p.ldda + (long)d * 4 * Hq + 4 * j) = pk;
         }
         fence_async_smem();
         tc_fence_before();
@@ -389,25 +416,18 @@ __global__ void __launch_bounds__(128, 1)
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
-        float *Pw = p.P + (size_t)(k_done & 1) * pstride_buf + ((((size_t)d * p.G + g) * NC + c) * Hq) * N;
+        float *Pw = p.P + (size_t)(k_done & 1) * pstride_buf + ((((size_t)d * p.G + g) * NC + c) * Hq) * N + nq0;
         for (int mt = 0; mt < MT; ++mt) {
             const int k = 128 * mt + 32 * q + l;
+            float v[NQ];
+            tmem_ld<NQ>(tmem + ((uint32_t)(32 * q) << 16) + mt * N + nq0, v);
+            float4 *dst = reinterpret_cast<float4 *>(Pw + (size_t)k * N);
 #pragma unroll
-            for (int ch = 0; ch < NT; ++ch) {
-                float v[16];
-                tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + mt * N + 16 * ch, v);
-                tmem_ld_wait();
-                float4 *dst = reinterpret_cast<float4 *>(Pw + (size_t)k * N + 16 * ch);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
+            for (int i = 0; i < NQ / 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
         tc_fence_before();
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            red_release_gpu_add(counter, 1u);
-        }
+        if (threadIdx.x == 0) red_release_gpu_add(counter, 1u);
     }
     if (T > 0) {
         if (threadIdx.x == 0) spin_until_geq(counter, (uint32_t)(NC * T));
@@ -415,23 +435,31 @@ __global__ void __launch_bounds__(128, 1)
         gather((T - 1) & 1);
     }
 #pragma unroll
-    for (int m = 0; m < NM; ++m) {
-        const int n = 4 * m + gam, b = b0 + n;
-        if (((colmask >> n) & 1) && unit_ok) {
+    for (int m = 0; m < NMQ; ++m) {
+        const int i = 4 * m + gam, b = bq0 + i;
+        if (((cm >> i) & 1) && unit_ok) {
             if (p.dh0) p.dh0[(long)d * B * H + (long)b * H + j] = dh[m];
             if (p.dc0) p.dc0[(long)d * B * H + (long)b * H + j] = dc[m];
         }
     }
-    // bias gradient: sum over this thread's columns, then over the 4 lanes of the unit
+    // bias gradient: sum over the thread's columns, the 4 lanes of the unit, then the 4 column
+    // blocks (fixed order through shared memory)
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         dbp[k] += __shfl_xor_sync(0xffffffffu, dbp[k], 1);
         dbp[k] += __shfl_xor_sync(0xffffffffu, dbp[k], 2);
     }
-    p.dbpart[((long)d * p.G + g) * 4 * Hq + 4 * j + gam] = sel4(dbp, gam);
+    float *dbs = reinterpret_cast<float *>(dAs);  // [4 cb][128 rows]
+    __syncthreads();
+    dbs[cb * 128 + 4 * jl + gam] = sel4(dbp, gam);
+    __syncthreads();
+    if (cb == 0) {
+        const int r = 4 * jl + gam;
+        p.dbpart[((long)d * p.G + g) * 4 * Hq + 4 * j + gam] = ((dbs[r] + dbs[128 + r]) + dbs[256 + r]) + dbs[384 + r];
+    }
     tc_fence_before();
     __syncthreads();
-    if (q == 0) {
+    if (w == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, TCOLS);
     }
@@ -441,8 +469,10 @@ __global__ void __launch_bounds__(128, 1)
 // host side
 // ---------------------------------------------------------------------------
 static int round_up(int a, int b) { return (a + b - 1) / b * b; }
+static int mma_n(int Bg) { return Bg <= 16 ? 16 : Bg <= 32 ? 32 : round_up(Bg, 64); }
 
 RecPlan rec_plan(int T, int B, int H, int ndir, int sms) {
+    (void)T;
     RecPlan pl{};
     pl.Hq = round_up(H, 128);
     pl.NC = pl.Hq / REC_UNITS;
@@ -450,13 +480,12 @@ RecPlan rec_plan(int T, int B, int H, int ndir, int sms) {
     int bestG = 1, bestN = 1 << 30;
     for (int G = 1; G <= B; ++G) {
         if (ndir * G * pl.NC > sms) break;
-        const int Bg = (B + G - 1) / G;
-        const int N = round_up(Bg, 16);
+        const int N = mma_n((B + G - 1) / G);
         if (N < bestN) { bestN = N; bestG = G; }
     }
     pl.G = bestG;
     pl.Bg = (B + bestG - 1) / bestG;
-    pl.N = round_up(pl.Bg, 16);
+    pl.N = mma_n(pl.Bg);
     return pl;
 }
 
@@ -464,7 +493,7 @@ static size_t fwd_smem(const RecPlan &pl) { return (size_t)pl.Hq / 64 * (16384 +
 static size_t bwd_smem(const RecPlan &pl) { return (size_t)pl.Hq / 64 * 16384 + 2 * pl.N * 128 + 1024 + 64; }
 
 bool rec_supported(const RecPlan &pl, int H) {
-    if (H < 1 || pl.N > 64 || pl.N < 16) return false;
+    if (H < 1 || (pl.N != 16 && pl.N != 32 && pl.N != 64)) return false;
     if (fwd_smem(pl) > 227 * 1024 || bwd_smem(pl) > 227 * 1024) return false;
     if (pl.ndir * pl.G * pl.NC > num_sms()) return false;
     if (pl.Hq / 128 * pl.N > 512) return false;
@@ -481,7 +510,7 @@ static cudaError_t launch_coop(Kern kern, int grid, size_t smem, cudaStream_t st
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(REC_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -504,11 +533,10 @@ int lstm_rec_fwd(const RecParams &p, const __half *RT16, cudaStream_t st) {
     if (e != cudaSuccess) return -5;
     ProfScope ps(PROF_REC_FWD, st);
     note_launch();
-    switch (p.N / 16) {
-        case 1: e = launch_coop(lstm_rec_fwd_kernel<1>, grid, smem, st, tmR, tmH, p); break;
-        case 2: e = launch_coop(lstm_rec_fwd_kernel<2>, grid, smem, st, tmR, tmH, p); break;
-        case 3: e = launch_coop(lstm_rec_fwd_kernel<3>, grid, smem, st, tmR, tmH, p); break;
-        case 4: e = launch_coop(lstm_rec_fwd_kernel<4>, grid, smem, st, tmR, tmH, p); break;
+    switch (p.N) {
+        case 16: e = launch_coop(lstm_rec_fwd_kernel<1>, grid, smem, st, tmR, tmH, p); break;
+        case 32: e = launch_coop(lstm_rec_fwd_kernel<2>, grid, smem, st, tmR, tmH, p); break;
+        case 64: e = launch_coop(lstm_rec_fwd_kernel<4>, grid, smem, st, tmR, tmH, p); break;
         default: return -6;
     }
     return e == cudaSuccess ? 0 : -5;
@@ -524,11 +552,10 @@ int lstm_rec_bwd(const RecParams &p, const __half *RT16, cudaStream_t st) {
     if (e != cudaSuccess) return -5;
     ProfScope ps(PROF_REC_BWD, st);
     note_launch();
-    switch (p.N / 16) {
-        case 1: e = launch_coop(lstm_rec_bwd_kernel<1>, grid, smem, st, tmR, p); break;
-        case 2: e = launch_coop(lstm_rec_bwd_kernel<2>, grid, smem, st, tmR, p); break;
-        case 3: e = launch_coop(lstm_rec_bwd_kernel<3>, grid, smem, st, tmR, p); break;
-        case 4: e = launch_coop(lstm_rec_bwd_kernel<4>, grid, smem, st, tmR, p); break;
+    switch (p.N) {
+        case 16: e = launch_coop(lstm_rec_bwd_kernel<1>, grid, smem, st, tmR, p); break;
+        case 32: e = launch_coop(lstm_rec_bwd_kernel<2>, grid, smem, st, tmR, p); break;
+        case 64: e = launch_coop(lstm_rec_bwd_kernel<4>, grid, smem, st, tmR, p); break;
         default: return -6;
     }
     return e == cudaSuccess ? 0 : -5;

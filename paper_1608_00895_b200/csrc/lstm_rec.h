@@ -23,16 +23,16 @@ struct RecParams {
     int dir0;                    // direction (+1/-1) of direction index 0; index 1 is always -1
     const uint8_t *mask;         // [T, B]
     // forward
-    const float *Z;              // [T*B, ldz], direction d at column d*4Hq
-    long ldz;
+    const float *Z;              // time-major transposed [T][ndir*4Hq][B] (gate row d*4Hq + 4j+gamma)
+    long ldz;                    // unused (kept for ABI stability of the struct)
     float *y;                    // [T*B, ldy] (+ d*y_doff), j < H; nullable
     long ldy, y_doff;
     __half *y16;                 // [T*B, ldy16] (+ d*Hq), all j < Hq; nullable
     long ldy16;
     float *C;                    // cell state after frame t: [T*B, ldc] (+ d*c_doff), j < H
     long ldc, c_doff;
-    __half *gates;               // [T*B, ldg] (+ d*4Hq) saved activations
-    long ldg;
+    __half *gates;               // saved activations, [T][ndir*4Hq][B] like Z
+    long ldg;                    // unused
     __half *hist;                // [ndir][T+1][B][Hq]: h before frame t at slot t + (dir<0)
     const float *c0, *h0;        // [B, H] (+ d*B*H) or nullptr
     float *hT, *cT;              // [B, H] (+ d*B*H) or nullptr
