@@ -201,6 +201,10 @@ int blstm_profile_enable(int on);
 /* cat: 0 forward recurrence, 1 BPTT recurrence, 2 GEMM.  Synchronizes the
  * recorded events; returns the summed device time (ms) and launch count. */
 int blstm_profile_read(int cat, double *total_ms, long *launches);
+/* Debug: record per-step phase timestamps (globaltimer ns, 8 per step, CTA 0 / thread 0)
+ * of the following forward / BPTT recurrence launches into DEVICE buffers of 8*T
+ * uint64 each; NULL disables. */
+int blstm_debug_set_trace(void *fwd, void *bwd);
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,7 @@ _SIGS = {
     "blstm_launch_count": (ctypes.c_long, []),
     "blstm_profile_enable": (_i, [_i]),
     "blstm_profile_read": (_i, [_i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_long)]),
+    "blstm_debug_set_trace": (_i, [_vp, _vp]),
 }
 
 PROF_REC_FWD, PROF_REC_BWD, PROF_GEMM = 0, 1, 2
@@ -233,3 +234,8 @@ def blstm_gemm_f16(A, a_mn: int, B, b_mn: int, C, M: int, N: int, K: int, alpha:
     _check("blstm_gemm_f16", lib().blstm_gemm_f16(M, N, K, _p(A), A.stride(0), a_mn, _p(B), B.stride(0), b_mn,
                                                   _p(C), C.stride(0), float(alpha), int(beta), _p(bias),
                                                   _stream(stream)))
+
+
+def blstm_debug_set_trace(fwd=None, bwd=None):
+    """Debug: per-step phase timestamps of the next recurrence launches (uint64 [T, 8] tensors)."""
+    _check("blstm_debug_set_trace", lib().blstm_debug_set_trace(_p(fwd), _p(bwd)))

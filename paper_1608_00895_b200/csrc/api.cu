@@ -50,6 +50,12 @@ static inline int rup(int a, int b) { return (a + b - 1) / b * b; }
 static inline bool al16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 static inline bool al4(const void *p) { return ((uintptr_t)p & 3u) == 0; }
 
+// the Z GEMM writes its output in the recurrence kernels' CTA-native layout (lstm_rec.h)
+static void set_native(GemmParams &gp, const RecPlan &pl, int B) {
+    gp.natB = B; gp.natBg = pl.Bg; gp.natG = pl.G; gp.natNQ = pl.N / 4; gp.natNC = pl.NC;
+    gp.natHq4 = 4 * pl.Hq; gp.natNdir = pl.ndir;
+}
+
 // ---------------------------------------------------------------------------
 // one layer, one direction
 // ---------------------------------------------------------------------------
@@ -92,7 +98,7 @@ static FwdWS fwd_ws(const LayerGeo &g) {
     w.w16 = c.take((size_t)g.Dp * 4 * g.Hq * 2);
     w.rt16 = c.take((size_t)4 * g.Hq * g.Hq * 2);
     w.bq = c.take((size_t)4 * g.Hq * 4);
-    w.Z = c.take((size_t)g.TB * 4 * g.Hq * 4);
+    w.Z = c.take(rec_native_elems(g.pl, g.T) * 4);
     w.cnt = c.take(256);
     w.total = c.off;
     return w;
@@ -116,7 +122,7 @@ static BwdWS bwd_ws(const LayerGeo &g) {
 static Reserve reserve_of(const LayerGeo &g) {
     Carve c;
     Reserve r;
-    r.gates = c.take((size_t)g.TB * 4 * g.Hq * 2);
+    r.gates = c.take(rec_native_elems(g.pl, g.T) * 2);
     r.hist = c.take((size_t)(g.T + 1) * g.B * g.Hq * 2);
     r.total = c.off;
     return r;
@@ -171,7 +177,7 @@ extern "C" int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     TRY(pack_rt(R, nullptr, g.H, g.Hq, 1, rt16, st), "pack_rt");
     TRY(pack_bias(b, nullptr, g.H, g.Hq, 1, bq, st), "pack_bias");
     GemmParams gp{(int)g.TB, 4 * g.Hq, g.Dp, Z, 4L * g.Hq, 1.f, 0, bq, 0, 0};
-    gp.remapB = g.B;  // Z time-major transposed [T][4Hq][B] for the recurrence
+    set_native(gp, g.pl, g.B);  // Z in the recurrence kernels' CTA-native layout
     TRY(gemm_f16({x16, g.Dp, 0}, {w16, 4L * g.Hq, 1}, gp, 0, st), "gemm Z");
     __half *hist = (__half *)(res + rv.hist);
     TRY(init_hist(hist, h0, g.T, g.B, g.H, g.Hq, 1, d->direction, st), "init_hist");
@@ -299,12 +305,12 @@ static StackWS stack_ws(const StackGeo &g) {
         w.w16.push_back(c.take((size_t)g.Dn[l] * 8 * Hq * 2));
         w.rt16.push_back(c.take((size_t)2 * 4 * Hq * Hq * 2));
         w.bq.push_back(c.take((size_t)8 * Hq * 4));
-        w.gates.push_back(c.take((size_t)TB * 8 * Hq * 2));
+        w.gates.push_back(c.take(rec_native_elems(g.pl, g.T) * 2));
         w.C.push_back(c.take((size_t)2 * TB * Hq * 4));
         w.hist.push_back(c.take((size_t)2 * (g.T + 1) * g.B * Hq * 2));
     }
-    const int zc = 8 * Hq > g.Kp ? 8 * Hq : g.Kp;
-    w.Z = c.take((size_t)TB * zc * 4);
+    const size_t zn = rec_native_elems(g.pl, g.T), zl = (size_t)TB * g.Kp;  // Z, or logits [TB, Kp]
+    w.Z = c.take((zn > zl ? zn : zl) * 4);
     w.dA = c.take((size_t)TB * 8 * Hq * 2);
     w.dY0 = c.take((size_t)TB * 2 * Hq * 4);
     w.dY1 = c.take((size_t)TB * 2 * Hq * 4);
@@ -382,7 +388,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
         const long lda = l == 0 ? g.Dp0 : 2L * Hq;
         GemmParams gp{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
-        gp.remapB = g.B;  // Z time-major transposed [T][8Hq][B] for the recurrence
+        set_native(gp, g.pl, g.B);  // Z in the recurrence kernels' CTA-native layout
         TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gp, 0, st), "gemm Z");
         __half *hist = (__half *)(ws + w.hist[l]);
         TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
@@ -519,5 +525,12 @@ extern "C" int blstm_gemm_f16(int M, int N, int K, const void *A, long lda, int 
     if (!al16(A) || !al16(B) || (lda & 7) || (ldb & 7)) return fail(BLSTM_ERR_ALIGN, "A/B must be 16-byte aligned, ld % 8 == 0");
     GemmParams gp{M, N, K, C, ldc, alpha, beta, bias, 0, 0};
     TRY(gemm_f16({A, lda, a_mn}, {B, ldb, b_mn}, gp, 0, (cudaStream_t)stream), "gemm");
+    return 0;
+}
+
+// debug hook: per-step phase timestamps of the next recurrence launches (8 u64 per step,
+// CTA 0 thread 0), nullptr to disable
+extern "C" int blstm_debug_set_trace(void *fwd, void *bwd) {
+    rec_set_trace((unsigned long long *)fwd, (unsigned long long *)bwd);
     return 0;
 }

@@ -19,7 +19,8 @@ def nccl_dir():
     raise RuntimeError("nccl headers not found (expected site-packages/nvidia/nccl)")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True adds -DBLSTM_TRACE (per-step phase timestamps, scripts/trace_rec.py)."""
     srcs = [os.path.join(HERE, s) for s in SOURCES]
     deps = srcs + [os.path.join(HERE, h) for h in os.listdir(HERE) if h.endswith((".h", ".cuh"))]
     deps.append(os.path.join(ROOT, "include", "blstm.h"))
@@ -34,6 +35,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
            "-Xlinker", "-rpath=" + os.path.join(nd, "lib"),
            "-o", tmp] + srcs
+    if trace:
+        cmd.insert(1, "-DBLSTM_TRACE")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
@@ -42,4 +45,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -159,7 +159,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
                 tmem_ld_wait();
                 const int n = n0 + c;
-                if (m < p.M && n < p.N && p.remapB) {
+                if (m < p.M && n < p.N && p.natB) {
+                    // CTA-native layout of the recurrence (see lstm_rec.h): the 16 columns stay in
+                    // one 128-row block of one CTA, consecutive columns are NQ floats apart
+                    const long t = m / p.natB, b = m - t * p.natB;
+                    const int g = (int)(b / p.natBg), nn = (int)(b - (long)g * p.natBg);
+                    const int cb = nn / p.natNQ, i = nn - cb * p.natNQ;
+                    const long blk = 512L * p.natNQ;
+                    const long rm = ((t * p.natNdir * p.natG + g) * p.natNC) * blk + (long)cb * 128 * p.natNQ + i;
+                    const int d = n / p.natHq4, rr = n - d * p.natHq4;
+                    const long cn = ((long)d * p.natG * p.natNC + (rr >> 7)) * blk + (long)(rr & 127) * p.natNQ;
+                    float *base = p.C + rm + cn;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (n + j < p.N) base[(long)j * p.natNQ] = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
+                } else if (m < p.M && n < p.N && p.remapB) {
                     // time-major transposed output: row m = t*B + b -> C[(t*ldc + col)*B + b]
                     const long t = m / p.remapB, b = m - t * p.remapB;
                     float *base = p.C + (size_t)t * p.ldc * p.remapB + b;

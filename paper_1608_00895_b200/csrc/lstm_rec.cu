@@ -111,8 +111,6 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const int j = c * REC_UNITS + jl;
     const bool unit_ok = j < p.H;
     const int B = p.B, T = p.T, H = p.H;
-    const long NROW = (long)p.ndir * 4 * Hq;
-    const long zrow = (long)d * 4 * Hq + 4 * j + gam;
     const int b0 = g * p.Bg;        // first batch row of the group
     const int nq0 = cb * NQ;        // first column of this warp
     const int bq0 = b0 + nq0;       // its first batch row
@@ -158,25 +156,42 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         h_st[m] = (ok && p.h0) ? p.h0[(long)d * B * H + (long)b * H + j] : 0.f;
     }
 
+    // CTA-native layout of Z and of the saved gates: this thread's NQ values of step t are
+    // contiguous, and the warp's 32 x NQ values form one contiguous block
+    const long nat_step = (long)p.ndir * p.G * p.NC * 512 * NQ;
+    const long nat_off = (((long)d * p.G + g) * p.NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
     float zv[NQ];
     auto prefetch_z = [&](int t) {
-        const float *zp = p.Z + ((long)t * NROW + zrow) * B + bq0;
+        const float4 *zp = reinterpret_cast<const float4 *>(p.Z + t * nat_step + nat_off);
 #pragma unroll
-        for (int i = 0; i < NQ; ++i) zv[i] = ((cm >> i) & 1) ? __ldg(zp + i) : 0.f;
+        for (int i = 0; i < NQ / 4; ++i) {
+            const float4 v = __ldg(zp + i);
+            zv[4 * i] = v.x; zv[4 * i + 1] = v.y; zv[4 * i + 2] = v.z; zv[4 * i + 3] = v.w;
+        }
     };
     if (T > 0) prefetch_z(dir > 0 ? 0 : T - 1);
 
     const uint32_t rs_addr = smem_u32(Rs), hs_addr = smem_u32(Hs);
+#ifdef BLSTM_TRACE
+    unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
+#define TRACE(k) \
+    if (trace) trace[(size_t)s * 8 + (k)] = globaltimer_ns()
+#else
+#define TRACE(k)
+#endif
     for (int s = 0; s < T; ++s) {
         const int t = dir > 0 ? s : T - 1 - s;
+        TRACE(0);
         if (threadIdx.x == 0) {
             if (s > 0) spin_until_geq(counter, (uint32_t)(p.NC * s));
+            TRACE(1);
             fence_async_global();
             const int rslot = t + (dir < 0 ? 1 : 0);
             const int row0 = (d * (T + 1) + rslot) * B + b0;
             mbar_arrive_expect_tx(&bars[0], KB * N * 128);
             for (int kb = 0; kb < KB; ++kb) tma_load_2d(Hs + kb * N * 128, &tmH, &bars[0], kb * 64, row0);
             mbar_wait(&bars[0], tma_phase);
+            TRACE(2);
             tc_fence_after();
             for (int kb = 0; kb < KB; ++kb)
 #pragma unroll
@@ -193,6 +208,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
+        TRACE(3);
 
         float act[NQ];
         {
@@ -202,13 +218,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             for (int i = 0; i < NQ; ++i) act[i] = gate_act(v[i] + zv[i], gam);
         }
         tc_fence_before();
-        // saved activations for BPTT, time-major [t][gate row][b]: contiguous per thread
-        {
-            __half *gp = p.gates + ((long)t * NROW + zrow) * B + bq0;
-#pragma unroll
-            for (int i = 0; i < NQ; ++i)
-                if ((cm >> i) & 1) gp[i] = __float2half_rn((((frm >> i) & 1) && unit_ok) ? act[i] : 0.f);
-        }
+        uint32_t fmq = 0;  // bit m: owned column 4m+gam is a valid frame
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
             float a4[4] = {act[4 * m], act[4 * m + 1], act[4 * m + 2], act[4 * m + 3]};
@@ -220,20 +230,51 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
                 const float cn = gv[1] * c_st[m] + gv[0] * gv[2];
                 c_st[m] = cn;
                 h_st[m] = gv[3] * tanh_f(cn);
+                fmq |= 1u << m;
             }
-            if ((cm >> i) & 1) {
+            // h_t to the history buffer first: the only store the group barrier publishes
+            if ((cm >> i) & 1)
+                p.hist[(((long)d * (T + 1) + wslot) * B + bq0 + i) * Hq + j] = __float2half_rn(h_st[m]);
+        }
+        TRACE(4);
+        __syncthreads();
+        TRACE(5);
+        if (threadIdx.x == 0) red_release_gpu_add(counter, 1u);
+        TRACE(6);
+        // off the critical path: saved activations (CTA-native, one vector store), c, y, y16
+        {
+            uint32_t hv[NQ / 2];
+#pragma unroll
+            for (int i = 0; i < NQ; i += 2) {
+                const float a0 = (((frm >> i) & 1) && unit_ok) ? act[i] : 0.f;
+                const float a1 = (((frm >> (i + 1)) & 1) && unit_ok) ? act[i + 1] : 0.f;
+                __half2 h2 = __floats2half2_rn(a0, a1);
+                hv[i / 2] = *reinterpret_cast<uint32_t *>(&h2);
+            }
+            __half *gp = p.gates + t * nat_step + nat_off;
+            if constexpr (NQ == 4) {
+                *reinterpret_cast<uint2 *>(gp) = make_uint2(hv[0], hv[1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < NQ / 8; ++i)
+                    reinterpret_cast<uint4 *>(gp)[i] = make_uint4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < NMQ; ++m) {
+            const int i = 4 * m + gam;
+            if (((cm >> i) & 1)) {
+                const bool fm = (fmq >> m) & 1;
                 const long row = (long)t * B + bq0 + i;
                 if (unit_ok) {
                     if (p.y) p.y[row * p.ldy + d * p.y_doff + j] = fm ? h_st[m] : 0.f;
                     p.C[row * p.ldc + d * p.c_doff + j] = c_st[m];
                 }
                 if (p.y16) p.y16[row * p.ldy16 + (long)d * Hq + j] = __float2half_rn(fm ? h_st[m] : 0.f);
-                p.hist[(((long)d * (T + 1) + wslot) * B + bq0 + i) * Hq + j] = __float2half_rn(h_st[m]);
             }
         }
         if (s + 1 < T) prefetch_z(dir > 0 ? t + 1 : t - 1);
-        __syncthreads();
-        if (threadIdx.x == 0) red_release_gpu_add(counter, 1u);
+        TRACE(7);
     }
 #pragma unroll
     for (int m = 0; m < NMQ; ++m) {
@@ -277,8 +318,6 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const int j = c * REC_UNITS + jl;
     const bool unit_ok = j < p.H;
     const int B = p.B, T = p.T, H = p.H, NC = p.NC;
-    const long NROW = (long)p.ndir * 4 * Hq;
-    const long grow = (long)d * 4 * Hq + 4 * j + gam;
     const int b0 = g * p.Bg;
     const int nq0 = cb * NQ;
     const int bq0 = b0 + nq0;
@@ -324,30 +363,56 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         dh[m] = (ok && p.dhT) ? p.dhT[(long)d * B * H + (long)b * H + j] : 0.f;
         dc[m] = (ok && p.dcT) ? p.dcT[(long)d * B * H + (long)b * H + j] : 0.f;
     }
-    const size_t pstride_buf = (size_t)p.ndir * p.G * NC * Hq * N;
+    // P (partial dh) exchange in a CTA-native layout [buf][d][g][c_src][mt][cb][128][NQ]: the
+    // writer's warp stores one contiguous block per M tile; the reader sums its units' rows
+    const size_t p_src = (size_t)MT * 512 * NQ;             // one source CTA
+    const size_t pstride_buf = (size_t)p.ndir * p.G * NC * p_src;
+    const size_t p_grp = (((size_t)d * p.G + g) * NC) * p_src;
     auto gather = [&](int buf) {
-        const float *Pb = p.P + buf * pstride_buf + (((size_t)d * p.G + g) * NC) * Hq * N + (size_t)j * N + nq0;
+        const float *Pb = p.P + buf * pstride_buf + p_grp + (size_t)(j >> 7) * 512 * NQ +
+                          ((size_t)cb * 128 + (j & 127)) * NQ;
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
             if ((pfm >> m) & 1) {
                 float acc = 0.f;
-                for (int cc = 0; cc < NC; ++cc) acc += Pb[(size_t)cc * Hq * N + 4 * m + gam];
+                for (int cc = 0; cc < NC; ++cc) acc += Pb[(size_t)cc * p_src + 4 * m + gam];
                 dh[m] = acc * inv_scale;
             }
         }
     };
+    const long nat_step = (long)p.ndir * p.G * NC * 512 * NQ;
+    const long nat_off = (((long)d * p.G + g) * NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
 
     uint32_t mma_phase = 0;
     const uint32_t rs_addr = smem_u32(Rs), das_addr = smem_u32(dAs);
+#ifdef BLSTM_TRACE
+    unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
+#endif
     for (int s = T - 1; s >= 0; --s) {
         const int t = dir > 0 ? s : T - 1 - s;
         const int k_done = T - 1 - s;
+        TRACE(0);
         // ---- this step's saved state (independent of the recurrence: issue first) ----
         float graw[NQ];
         {
-            const __half *gp = p.gates + ((long)t * NROW + grow) * B + bq0;
+            const __half *gp = p.gates + t * nat_step + nat_off;
+            uint32_t hv[NQ / 2];
+            if constexpr (NQ == 4) {
+                const uint2 u = *reinterpret_cast<const uint2 *>(gp);
+                hv[0] = u.x; hv[1] = u.y;
+            } else {
 #pragma unroll
-            for (int i = 0; i < NQ; ++i) graw[i] = ((cm >> i) & 1) ? __half2float(gp[i]) : 0.f;
+                for (int i = 0; i < NQ / 8; ++i) {
+                    const uint4 u = reinterpret_cast<const uint4 *>(gp)[i];
+                    hv[4 * i] = u.x; hv[4 * i + 1] = u.y; hv[4 * i + 2] = u.z; hv[4 * i + 3] = u.w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NQ; i += 2) {
+                const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&hv[i / 2]));
+                graw[i] = f2.x;
+                graw[i + 1] = f2.y;
+            }
         }
         float ct[NMQ], cp[NMQ], dyv[NMQ];
         const int tp = t - dir;
@@ -364,13 +429,17 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         const uint32_t frm =
             __ballot_sync(0xffffffffu, l < NQ && ((cm >> l) & 1) && p.mask[(long)t * B + bq0 + l]);
         // ---- dh_t from the previous step's partials ----
+        TRACE(1);
         if (k_done > 0) {
             if (threadIdx.x == 0) spin_until_geq(counter, (uint32_t)(NC * k_done));
+            TRACE(2);
             __syncthreads();
             gather((k_done - 1) & 1);
         }
+        TRACE(3);
         // ---- gate gradients ----
         pfm = 0;
+        uint2 pks[NMQ];
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
             float a4[4] = {graw[4 * m], graw[4 * m + 1], graw[4 * m + 2], graw[4 * m + 3]};
@@ -398,13 +467,14 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             pk.x = *reinterpret_cast<uint32_t *>(&lo);
             pk.y = *reinterpret_cast<uint32_t *>(&hi);
             *reinterpret_cast<uint2 *>(dAs + sw128_offset(n, 4 * jl, N)) = pk;
-            if ((cm >> i) & 1)
-                *reinterpret_cast<uint2 *>(p.dA + ((long)t * B + bq0 + i) * p.ldda + (long)d * 4 * Hq + 4 * j) = pk;
+            pks[m] = pk;
         }
         fence_async_smem();
         tc_fence_before();
+        TRACE(4);
         __syncthreads();
         if (threadIdx.x == 0) {
+            TRACE(5);
             tc_fence_after();
             for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -413,22 +483,32 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
                                sdesc_sw128(das_addr + (kk >> 2) * N * 128 + (kk & 3) * 32, 16, 1024), idesc, kk != 0);
             mma_commit(&bars[1]);
         }
+        // while the MMA runs: dA of this step to global memory for the weight / input GEMMs
+#pragma unroll
+        for (int m = 0; m < NMQ; ++m) {
+            const int i = 4 * m + gam;
+            if ((cm >> i) & 1)
+                *reinterpret_cast<uint2 *>(p.dA + ((long)t * B + bq0 + i) * p.ldda + (long)d * 4 * Hq + 4 * j) = pks[m];
+        }
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
-        float *Pw = p.P + (size_t)(k_done & 1) * pstride_buf + ((((size_t)d * p.G + g) * NC + c) * Hq) * N + nq0;
+        TRACE(6);
+        float *Pw = p.P + (size_t)(k_done & 1) * pstride_buf + p_grp + (size_t)c * p_src +
+                    ((size_t)cb * 128 + 32 * q + l) * NQ;
         for (int mt = 0; mt < MT; ++mt) {
-            const int k = 128 * mt + 32 * q + l;
             float v[NQ];
             tmem_ld<NQ>(tmem + ((uint32_t)(32 * q) << 16) + mt * N + nq0, v);
-            float4 *dst = reinterpret_cast<float4 *>(Pw + (size_t)k * N);
+            float4 *dst = reinterpret_cast<float4 *>(Pw + (size_t)mt * 512 * NQ);
 #pragma unroll
             for (int i = 0; i < NQ / 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
         tc_fence_before();
         __syncthreads();
         if (threadIdx.x == 0) red_release_gpu_add(counter, 1u);
+        TRACE(7);
     }
+#undef TRACE
     if (T > 0) {
         if (threadIdx.x == 0) spin_until_geq(counter, (uint32_t)(NC * T));
         __syncthreads();
@@ -521,7 +601,15 @@ static cudaError_t launch_coop(Kern kern, int grid, size_t smem, cudaStream_t st
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-int lstm_rec_fwd(const RecParams &p, const __half *RT16, cudaStream_t st) {
+static unsigned long long *g_trace_fwd = nullptr, *g_trace_bwd = nullptr;
+void rec_set_trace(unsigned long long *fwd, unsigned long long *bwd) {
+    g_trace_fwd = fwd;
+    g_trace_bwd = bwd;
+}
+
+int lstm_rec_fwd(const RecParams &p_in, const __half *RT16, cudaStream_t st) {
+    RecParams p = p_in;
+    if (g_trace_fwd) p.trace = g_trace_fwd;
     if (p.T == 0) return 0;
     CUtensorMap tmR, tmH;
     if (make_tmap_f16(&tmR, RT16, p.Hq, (uint64_t)p.ndir * 4 * p.Hq, p.Hq, 128)) return -2;
@@ -542,7 +630,9 @@ int lstm_rec_fwd(const RecParams &p, const __half *RT16, cudaStream_t st) {
     return e == cudaSuccess ? 0 : -5;
 }
 
-int lstm_rec_bwd(const RecParams &p, const __half *RT16, cudaStream_t st) {
+int lstm_rec_bwd(const RecParams &p_in, const __half *RT16, cudaStream_t st) {
+    RecParams p = p_in;
+    if (g_trace_bwd) p.trace = g_trace_bwd;
     CUtensorMap tmR;
     if (make_tmap_f16(&tmR, RT16, p.Hq, (uint64_t)p.ndir * 4 * p.Hq, p.Hq, 128)) return -2;
     RecPlan pl{p.Hq, p.NC, p.G, p.Bg, p.N, p.ndir};

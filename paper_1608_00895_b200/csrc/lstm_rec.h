@@ -46,8 +46,20 @@ struct RecParams {
     float *P;                    // [2][ndir][G][NC][Hq][N] partial dh exchange
     float *dh0, *dc0;            // [B, H] (+ d*B*H) or nullptr
     uint32_t *counters;          // [ndir][G], zeroed before each launch
+    unsigned long long *trace;   // debug: per-step phase timestamps of CTA 0 / thread 0, or nullptr
 };
 
+// debug hook: per-step phase timestamps (globaltimer ns, 8 per step) of the next launches
+void rec_set_trace(unsigned long long *fwd, unsigned long long *bwd);
+
+// CTA-native layout of Z and of the saved gate activations (one time step = one block per
+// (direction, batch group, CTA)): element (t, d, g, c, column block cb, gate row r, i) at
+//   ((((t*ndir + d)*G + g)*NC + c)*4 + cb)*128*NQ + r*NQ + i,   NQ = N/4,
+// for batch row b = g*Bg + cb*NQ + i and gate column d*4Hq + 128c + r.  Each thread of the
+// recurrence kernels reads/writes NQ contiguous values; each warp one contiguous block.
+inline size_t rec_native_elems(const RecPlan &pl, int T) {
+    return (size_t)T * pl.ndir * 4 * pl.Hq * pl.G * pl.N;
+}
 RecPlan rec_plan(int T, int B, int H, int ndir, int num_sms);
 bool rec_supported(const RecPlan &pl, int H);
 size_t rec_P_bytes(const RecPlan &pl);
