@@ -70,6 +70,58 @@ DEVI void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------------
+// thread-block clusters / distributed shared memory
+// ---------------------------------------------------------------------------
+DEVI uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+DEVI void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address -> shared::cluster address of the same offset in CTA `rank`
+DEVI uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+// bulk copy local smem -> (possibly remote) smem, completing tx bytes on the destination's mbarrier
+DEVI void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes, uint32_t mbar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst_cluster),
+        "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
+        : "memory");
+}
+DEVI void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+DEVI void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// 16-byte store into a (possibly remote) CTA's shared memory, completing tx bytes on its mbarrier
+DEVI void st_async_v4u(uint32_t dst_cluster, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t mbar_cluster) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+            dst_cluster),
+        "r"(a), "r"(b), "r"(c), "r"(d), "r"(mbar_cluster)
+        : "memory");
+}
+DEVI void st_async_v2u(uint32_t dst_cluster, uint32_t a, uint32_t b, uint32_t mbar_cluster) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(
+                     dst_cluster),
+                 "r"(a), "r"(b), "r"(mbar_cluster)
+                 : "memory");
+}
+DEVI void st_async_v4(uint32_t dst_cluster, float a, float b, float c, float d, uint32_t mbar_cluster) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+            dst_cluster),
+        "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar_cluster)
+        : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // proxy fences
 // ---------------------------------------------------------------------------
 // generic-proxy writes to shared memory -> visible to the async proxy (tcgen05.mma, TMA store)
@@ -167,6 +219,18 @@ DEVI uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes
     d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
     d |= (uint64_t)1 << 46;  // version
     d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+
+// Shared-memory matrix descriptor without swizzle (K-major "interleave" layout): core matrices
+// of 8 rows x 16 B stored contiguously (128 B); SBO = byte distance between 8-row groups,
+// LBO = byte distance between the two 8-element K halves of one 16-element MMA step.
+DEVI uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // version; layout type 0 = SWIZZLE_NONE
     return d;
 }
 

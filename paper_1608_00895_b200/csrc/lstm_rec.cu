@@ -3,19 +3,21 @@
 // ("custom CUDA kernels for the LSTM gating mechanism"), the cell update and
 // the mask, one launch for the whole sequence (no launch per time step).
 //
-// Decomposition: CTA (d, g, c) owns hidden units [32c, 32c+32) of
-// direction d for batch group g.  Its 128 gate rows of R^T (gate-interleaved, row 4*jl+gamma)
-// stay resident in shared memory for the whole sequence as the tcgen05 A operand.
-// 16 warps: warp w reads TMEM lane quarter q = w%4 (8 units x 4 gates) for the batch
-// columns of block cb = w/4 (N/4 columns), so the per-step epilogue is spread over 4 warps
-// per scheduler.  Per step:
-//   forward : D[128 x N] = R^T_slice[128 x Hq] . h_{t-1}^T  (h from the group's history buffer,
-//             TMA-loaded after the group barrier), + Z_t, gates, cell update, mask in registers,
-//             h_t published to the history buffer, group barrier (gpu-scope counter).
-//   backward: dA_t for the CTA's 128 gate columns (fp16, scaled), partial
-//             P_c[Hq x N] = R[:, cols_c] . dA_t^T on tcgen05 (same smem tile read MN-major),
-//             P published, group barrier, each CTA sums the NC partials of its own units
-//             (fixed order -> deterministic) to get dh_{t-1}.
+// Decomposition: one thread-block cluster of NC = Hq/32 CTAs per
+// (direction d, batch group g); cluster rank c owns hidden units [32c, 32c+32).  The CTA's
+// slice of the recurrent weights stays resident in TMEM for the whole sequence as the
+// tcgen05 A operand (forward: R^T rows of its 128 gate columns; BPTT: R rows, all Hq units x
+// its 128 gate columns).  16 warps: warp w reads TMEM lane quarter q = w%4 (8 units x 4 gates)
+// for the batch columns of block cb = w/4 (N/4 columns).
+// Per step, all exchange is on chip, through distributed shared memory and mbarriers:
+//   forward : D[128 x N] = R^T_slice . h_{t-1}^T (B operand = the cluster's h, double-buffered
+//             in smem), + Z_t, gates, cell update, mask in registers; the CTA's h_t slice is
+//             staged in smem and bulk-copied into every peer's next B buffer (complete_tx on
+//             the peer's mbarrier).
+//   backward: dA_t for the CTA's 128 gate columns (fp16, scaled) -> smem B operand;
+//             P_c[Hq x N] = R[:, cols_c] . dA_t^T; each warp st.async's the 32 rows owned by
+//             peer c' straight from registers into c''s slot for source c; every CTA sums its
+//             NC slots in fixed order (deterministic) -> dh_{t-1} of its units.
 #include "common.cuh"
 #include "gemm.h"
 #include "lstm_rec.h"
@@ -26,10 +28,6 @@ namespace blstm {
 constexpr int REC_THREADS = 512;
 
 static DEVI uint8_t *align1024(uint8_t *p) { return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023); }
-
-static __host__ __device__ constexpr uint32_t tmem_cols_for(int cols) {
-    return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
-}
 
 // 32 lanes x NC columns of TMEM -> registers (thread i: lane base+i)
 template <int NC>
@@ -54,6 +52,34 @@ DEVI void tmem_ld(uint32_t taddr, float (&v)[NC]) {
     tmem_ld_wait();
 #pragma unroll
     for (int i = 0; i < NC; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 32 lanes x NC columns, issued without waiting (pair with tmem_wait_regs on the same registers)
+template <int NC>
+DEVI void tmem_ld_nowait(uint32_t taddr, uint32_t (&r)[NC]) {
+    if constexpr (NC == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                     : "r"(taddr));
+    } else if constexpr (NC == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                       "=r"(r[7])
+                     : "r"(taddr));
+    } else {
+        static_assert(NC == 16, "tmem_ld_nowait: 4, 8 or 16 columns");
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+    }
+}
+// after tcgen05.wait::ld: "redefine" the loaded registers so no consumer is scheduled before the wait
+template <int NC>
+DEVI void pin_regs(uint32_t (&r)[NC]) {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) asm volatile("" : "+r"(r[i]));
 }
 
 // 4x4 transpose inside each group of 4 lanes: lane gam holds a[k] = gate gam at batch column
@@ -84,27 +110,46 @@ DEVI float gate_act(float pre, int gam) {
     return is_g ? 2.f * s - 1.f : s;
 }
 
+#ifdef BLSTM_TRACE
+#define TRACE(k) \
+    if (trace) trace[(size_t)s * 8 + (k)] = globaltimer_ns()
+#else
+#define TRACE(k)
+#endif
+
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
+// smem: [region0: R^T slice (TMA, start only) | aliased later by hbuf[2] + stg[2]] [barriers]
+//   hbuf[b]: B operand [N x Hq] fp16, no-swizzle K-major: element (n, k) at ((k/8)*N + n)*16 + (k%8)*2,
+//            so CTA c's units [32c, 32c+32) are one contiguous 64N-byte block
+//   stg[b] : this CTA's h slice in that block format
+static __host__ __device__ size_t fwd_region0(int Hq, int N) {
+    const size_t rs = (size_t)Hq / 64 * 16384, hb = 2 * (size_t)Hq * N * 2 + 2 * 64 * (size_t)N;
+    return rs > hb ? rs : hb;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(REC_THREADS, 1)
-    lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmH,
-                        RecParams p) {
+    lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmR, RecParams p) {
     constexpr int N = 16 * NT;   // MMA N = padded batch columns of the group
     constexpr int NQ = N / 4;    // columns handled by one warp
     constexpr int NMQ = NQ / 4;  // columns owned (cell state) by one thread
+    constexpr uint32_t SG = 64 * N;  // bytes of one CTA's h slice
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    const int Hq = p.Hq, KB = Hq / 64;
+    const int Hq = p.Hq, KB = Hq / 64, NC = p.NC;
+    const uint32_t HB = (uint32_t)Hq * N * 2;
     uint8_t *Rs = smem;
-    uint8_t *Hs = smem + KB * 16384;
-    uint64_t *bars = (uint64_t *)(Hs + KB * N * 128);
-    uint32_t *tslot = (uint32_t *)(bars + 2);
+    uint8_t *hbuf = smem;            // aliases Rs after the TMEM load
+    uint8_t *stg = smem + 2 * HB;
+    uint64_t *bars = (uint64_t *)(smem + fwd_region0(Hq, N));  // [0] tma, [1] mma, [2..3] full[b]
+    uint32_t *tslot = (uint32_t *)(bars + 4);
 
-    const int c = blockIdx.x % p.NC;
-    const int g = (blockIdx.x / p.NC) % p.G;
-    const int d = blockIdx.x / (p.NC * p.G);
+    const int c = (int)cluster_ctarank();
+    const int grp = blockIdx.x / NC;  // cluster index = d*G + g
+    const int g = grp % p.G;
+    const int d = grp / p.G;
     const int dir = d == 0 ? p.dir0 : -1;
     const int w = warp_id(), q = w & 3, cb = w >> 2, l = lane_id();
     const int jl = 8 * q + (l >> 2), gam = l & 3;
@@ -114,12 +159,18 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const int b0 = g * p.Bg;        // first batch row of the group
     const int nq0 = cb * NQ;        // first column of this warp
     const int bq0 = b0 + nq0;       // its first batch row
-    uint32_t *counter = p.counters + d * p.G + g;
-    constexpr uint32_t TCOLS = tmem_cols_for(N);
+    constexpr uint32_t TCOLS = 512;
+    // TMEM: columns [0, Hq/2) hold the CTA's R^T slice (A operand, 128 lanes = gate rows, two
+    // fp16 of K per 32-bit column); from column Hq/2, four K-split accumulators D_w[128 x N]
+    // (the tiny N=16..64 MMAs are issue-bound, so warps 0..3 issue a quarter of K each).
+    const uint32_t DCOL = Hq / 2;
+    constexpr int NISSUE = 4;
 
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        mbar_init(&bars[1], NISSUE);
+        mbar_init(&bars[2], 1);
+        mbar_init(&bars[3], 1);
         fence_mbar_init();
     }
     if (w == 0) {
@@ -140,12 +191,49 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmR);
-        tma_prefetch_desc(&tmH);
         mbar_arrive_expect_tx(&bars[0], KB * 16384);
         for (int kb = 0; kb < KB; ++kb) tma_load_2d(Rs + kb * 16384, &tmR, &bars[0], kb * 64, d * 4 * Hq + c * 128);
-        mbar_wait(&bars[0], 0);
     }
-    uint32_t tma_phase = 1, mma_phase = 0;
+    mbar_wait(&bars[0], 0);
+    // R^T slice: shared memory (SW128 K-major) -> registers -> TMEM, once per launch.
+    // Warp (q, cb) writes lanes 32q.. and columns [cb*Hq/8, (cb+1)*Hq/8).
+    {
+        const int r = 32 * q + l;
+        const int cw = Hq / 8;
+        for (int col = cb * cw; col < (cb + 1) * cw; col += 16) {
+            uint32_t v[16];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int kc = col / 4 + u;  // 8 K-elements = 4 columns
+                const uint4 x = *reinterpret_cast<const uint4 *>(Rs + (kc >> 3) * 16384 + r * 128 +
+                                                                  (((kc & 7) ^ (r & 7)) << 4));
+                v[4 * u] = x.x; v[4 * u + 1] = x.y; v[4 * u + 2] = x.z; v[4 * u + 3] = x.w;
+            }
+            tmem_st16(tmem + ((uint32_t)(32 * q) << 16) + col, v);
+        }
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    // h_{-1} = h0 (or 0) into hbuf[0], all Hq units of the group's N columns
+    for (int e = threadIdx.x; e < N * Hq / 2; e += REC_THREADS) {
+        const int n = e / (Hq / 2), k = 2 * (e - n * (Hq / 2)), b = b0 + n;
+        float v0 = 0.f, v1 = 0.f;
+        if (p.h0 && n < p.Bg && b < B) {
+            const float *hp = p.h0 + (long)d * B * H + (long)b * H;
+            if (k < H) v0 = hp[k];
+            if (k + 1 < H) v1 = hp[k + 1];
+        }
+        __half2 h2 = __floats2half2_rn(v0, v1);
+        *reinterpret_cast<__half2 *>(hbuf + ((k >> 3) * N + n) * 16 + (k & 7) * 2) = h2;
+    }
+    fence_async_smem();
+    if (threadIdx.x == 0) {
+        if (T > 1) mbar_arrive_expect_tx(&bars[3], NC * SG);  // h_0 from the cluster -> step 1
+        if (T > 2) mbar_arrive_expect_tx(&bars[2], NC * SG);  // h_1 -> step 2
+    }
+    cluster_sync();  // every CTA done with its R staging before peers write into hbuf / stg
 
     float c_st[NMQ], h_st[NMQ];
 #pragma unroll
@@ -156,10 +244,10 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         h_st[m] = (ok && p.h0) ? p.h0[(long)d * B * H + (long)b * H + j] : 0.f;
     }
 
-    // CTA-native layout of Z and of the saved gates: this thread's NQ values of step t are
-    // contiguous, and the warp's 32 x NQ values form one contiguous block
-    const long nat_step = (long)p.ndir * p.G * p.NC * 512 * NQ;
-    const long nat_off = (((long)d * p.G + g) * p.NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
+    // CTA-native layout of Z and of the saved gates (lstm_rec.h): this thread's NQ values of step t
+    // are contiguous, and the warp's 32 x NQ values form one contiguous block
+    const long nat_step = (long)p.ndir * p.G * NC * 512 * NQ;
+    const long nat_off = (((long)d * p.G + g) * NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
     float zv[NQ];
     auto prefetch_z = [&](int t) {
         const float4 *zp = reinterpret_cast<const float4 *>(p.Z + t * nat_step + nat_off);
@@ -171,36 +259,29 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     };
     if (T > 0) prefetch_z(dir > 0 ? 0 : T - 1);
 
-    const uint32_t rs_addr = smem_u32(Rs), hs_addr = smem_u32(Hs);
+    const uint32_t hbuf_addr = smem_u32(hbuf), stg_addr = smem_u32(stg);
+    const uint32_t full_addr = smem_u32(&bars[2]);
+    uint32_t fph = 0, mma_phase = 0;  // fph bit b: phase parity of full[b]
 #ifdef BLSTM_TRACE
     unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
-#define TRACE(k) \
-    if (trace) trace[(size_t)s * 8 + (k)] = globaltimer_ns()
-#else
-#define TRACE(k)
 #endif
     for (int s = 0; s < T; ++s) {
         const int t = dir > 0 ? s : T - 1 - s;
+        const int b = s & 1;
         TRACE(0);
-        if (threadIdx.x == 0) {
-            if (s > 0) spin_until_geq(counter, (uint32_t)(p.NC * s));
+        if (l == 0 && w < NISSUE) {
+            if (s > 0) mbar_wait(&bars[2 + b], (fph >> b) & 1);  // the cluster's h_{s-1} landed in hbuf[b]
             TRACE(1);
-            fence_async_global();
-            const int rslot = t + (dir < 0 ? 1 : 0);
-            const int row0 = (d * (T + 1) + rslot) * B + b0;
-            mbar_arrive_expect_tx(&bars[0], KB * N * 128);
-            for (int kb = 0; kb < KB; ++kb) tma_load_2d(Hs + kb * N * 128, &tmH, &bars[0], kb * 64, row0);
-            mbar_wait(&bars[0], tma_phase);
-            TRACE(2);
             tc_fence_after();
-            for (int kb = 0; kb < KB; ++kb)
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    mma_f16_ss(tmem, sdesc_sw128(rs_addr + kb * 16384 + kk * 32, 16, 1024),
-                               sdesc_sw128(hs_addr + kb * N * 128 + kk * 32, 16, 1024), idesc, (kb | kk) != 0);
+            const uint32_t hb = hbuf_addr + b * HB;
+            const int ks0 = w * (Hq / 16 / NISSUE), ks1 = ks0 + Hq / 16 / NISSUE;
+            for (int ks = ks0; ks < ks1; ++ks)
+                mma_f16_ts(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * N, 16 * N, 128), idesc,
+                           ks != ks0);
             mma_commit(&bars[1]);
+            TRACE(2);
         }
-        tma_phase ^= 1;
+        if (s > 0) fph ^= 1u << b;
         // frame-valid bits of this warp's columns (lane i reads the mask of column i)
         const uint32_t frm =
             __ballot_sync(0xffffffffu, l < NQ && ((cm >> l) & 1) && p.mask[(long)t * B + bq0 + l]);
@@ -212,13 +293,25 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 
         float act[NQ];
         {
-            float v[NQ];
-            tmem_ld<NQ>(tmem + ((uint32_t)(32 * q) << 16) + nq0, v);
+            uint32_t v0[NQ], v1[NQ], v2[NQ], v3[NQ];
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + DCOL + nq0;
+            tmem_ld_nowait<NQ>(ta, v0);
+            tmem_ld_nowait<NQ>(ta + N, v1);
+            tmem_ld_nowait<NQ>(ta + 2 * N, v2);
+            tmem_ld_nowait<NQ>(ta + 3 * N, v3);
+            tmem_ld_wait();
+            pin_regs<NQ>(v0);
+            pin_regs<NQ>(v1);
+            pin_regs<NQ>(v2);
+            pin_regs<NQ>(v3);
 #pragma unroll
-            for (int i = 0; i < NQ; ++i) act[i] = gate_act(v[i] + zv[i], gam);
+            for (int i = 0; i < NQ; ++i)
+                act[i] = gate_act(((__uint_as_float(v0[i]) + __uint_as_float(v1[i])) +
+                                   (__uint_as_float(v2[i]) + __uint_as_float(v3[i]))) + zv[i], gam);
         }
         tc_fence_before();
         uint32_t fmq = 0;  // bit m: owned column 4m+gam is a valid frame
+        uint8_t *sg = stg + b * SG;
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
             float a4[4] = {act[4 * m], act[4 * m + 1], act[4 * m + 2], act[4 * m + 3]};
@@ -232,16 +325,21 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
                 h_st[m] = gv[3] * tanh_f(cn);
                 fmq |= 1u << m;
             }
-            // h_t to the history buffer first: the only store the group barrier publishes
-            if ((cm >> i) & 1)
-                p.hist[(((long)d * (T + 1) + wslot) * B + bq0 + i) * Hq + j] = __float2half_rn(h_st[m]);
+            // staged slice in the B-operand block format: unit jl -> k chunk q, byte (jl%8)*2
+            *reinterpret_cast<__half *>(sg + (q * N + nq0 + i) * 16 + (jl & 7) * 2) = __float2half_rn(h_st[m]);
         }
-        TRACE(4);
+        fence_async_smem();
         __syncthreads();
+        TRACE(4);
+        if (l == 0 && w < NC && s + 1 < T) {
+            // h_s of this CTA -> hbuf[b^1] (block c) of CTA w of the cluster (16 warps send in parallel)
+            bulk_s2c(mapa_shared(hbuf_addr + (b ^ 1) * HB + c * SG, w), stg_addr + b * SG, SG,
+                     mapa_shared(full_addr + 8 * (b ^ 1), w));
+            bulk_commit();
+        }
+        if (threadIdx.x == 0 && s > 0 && s + 2 < T) mbar_arrive_expect_tx(&bars[2 + b], NC * SG);  // full[b]: step s+2
         TRACE(5);
-        if (threadIdx.x == 0) red_release_gpu_add(counter, 1u);
-        TRACE(6);
-        // off the critical path: saved activations (CTA-native, one vector store), c, y, y16
+        // off the critical path: history (for the dR GEMM), saved activations, c, y, y16
         {
             uint32_t hv[NQ / 2];
 #pragma unroll
@@ -271,10 +369,14 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
                     p.C[row * p.ldc + d * p.c_doff + j] = c_st[m];
                 }
                 if (p.y16) p.y16[row * p.ldy16 + (long)d * Hq + j] = __float2half_rn(fm ? h_st[m] : 0.f);
+                p.hist[(((long)d * (T + 1) + wslot) * B + bq0 + i) * Hq + j] = __float2half_rn(h_st[m]);
             }
         }
         if (s + 1 < T) prefetch_z(dir > 0 ? t + 1 : t - 1);
-        TRACE(7);
+        // the bulk copies of stg[b] have read it before stg[b] is rewritten at step s+2 (ordered
+        // by step s+1's __syncthreads)
+        if (l == 0 && w < NC) bulk_wait_read<0>();
+        TRACE(6);
     }
 #pragma unroll
     for (int m = 0; m < NMQ; ++m) {
@@ -286,6 +388,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();
     if (w == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, TCOLS);
@@ -295,40 +398,62 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 // ---------------------------------------------------------------------------
 // backward through time
 // ---------------------------------------------------------------------------
+// smem: [region0: R^T slice (TMA, start only) | aliased later by the P slots] [dAs] [barriers]
+//   slots[b][src][32 rows][N + 8] fp16: partial dh (x 2^DA_SHIFT x P_SCALE) of this CTA's 32
+//   units from CTA src (row pitch padded by 16 B so the owner's gather is conflict-free)
+constexpr float P_SCALE = 1.f / 16.f;  // keeps the fp16 partials far from overflow
+//   stg[b][owner][32 rows][N + 8] fp16: this CTA's partial rows per owner, bulk-copied as one block
+static __host__ __device__ size_t bwd_region0(int Hq, int N, int NC) {
+    const size_t rs = (size_t)Hq / 64 * 16384, sl = 4 * (size_t)NC * 32 * (N + 8) * 2;
+    return rs > sl ? rs : sl;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(REC_THREADS, 1)
     lstm_rec_bwd_kernel(const __grid_constant__ CUtensorMap tmR, RecParams p) {
     constexpr int N = 16 * NT;
     constexpr int NQ = N / 4;
     constexpr int NMQ = NQ / 4;
+    constexpr int PITCH = N + 8;  // halves per slot row
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    const int Hq = p.Hq, KB = Hq / 64, MT = Hq / 128;
+    const int Hq = p.Hq, KB = Hq / 64, MT = Hq / 128, NC = p.NC;
+    const uint32_t SLOTB = (uint32_t)NC * 32 * PITCH * 2;  // bytes of one slot buffer
+    const uint32_t SLOT_TX = SLOTB;                        // bytes arriving per buffer (NC blocks)
+    const uint32_t BLK = 32 * PITCH * 2;                   // one (owner, source) block
     uint8_t *Rs = smem;
-    uint8_t *dAs = smem + KB * 16384;  // [2][N][128 B] K-major SW128
-    uint64_t *bars = (uint64_t *)(dAs + 2 * N * 128);
-    uint32_t *tslot = (uint32_t *)(bars + 2);
+    __half *slots = reinterpret_cast<__half *>(smem);  // aliases Rs after the TMEM load
+    __half *stgp = slots + 2 * (size_t)NC * 32 * PITCH;
+    uint8_t *dAs = smem + bwd_region0(Hq, N, NC);      // [2][N][128 B] K-major SW128
+    uint64_t *bars = (uint64_t *)(dAs + 2 * N * 128);   // [0] tma, [1] mma, [2..3] slots full[b]
+    uint32_t *tslot = (uint32_t *)(bars + 4);
 
-    const int c = blockIdx.x % p.NC;
-    const int g = (blockIdx.x / p.NC) % p.G;
-    const int d = blockIdx.x / (p.NC * p.G);
+    const int c = (int)cluster_ctarank();
+    const int grp = blockIdx.x / NC;
+    const int g = grp % p.G;
+    const int d = grp / p.G;
     const int dir = d == 0 ? p.dir0 : -1;
     const int w = warp_id(), q = w & 3, cb = w >> 2, l = lane_id();
     const int jl = 8 * q + (l >> 2), gam = l & 3;
     const int j = c * REC_UNITS + jl;
     const bool unit_ok = j < p.H;
-    const int B = p.B, T = p.T, H = p.H, NC = p.NC;
+    const int B = p.B, T = p.T, H = p.H;
     const int b0 = g * p.Bg;
     const int nq0 = cb * NQ;
     const int bq0 = b0 + nq0;
-    uint32_t *counter = p.counters + d * p.G + g;
-    const uint32_t TCOLS = tmem_cols_for(MT * N);
-    const float inv_scale = 1.f / (float)(1 << DA_SHIFT);
+    constexpr uint32_t TCOLS = 512;
+    // TMEM: M tile mt of A = R[128mt.., cols_c] (lanes = hidden unit k, two fp16 gate columns per
+    // 32-bit column) at columns [64mt, 64mt+64); accumulators D_mt[128 x N] from column Hq/2.
+    // Warp mt issues the MMAs of tile mt (the tiny MMAs are issue-bound).
+    const uint32_t DCOL = Hq / 2;
+    const float inv_scale = 1.f / ((float)(1 << DA_SHIFT) * P_SCALE);
     const float scale = (float)(1 << DA_SHIFT);
 
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        mbar_init(&bars[1], MT);
+        mbar_init(&bars[2], 1);
+        mbar_init(&bars[3], 1);
         fence_mbar_init();
     }
     if (w == 0) {
@@ -339,7 +464,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    const uint32_t idesc = idesc_f16(128, N, 1, 0);
+    const uint32_t idesc = idesc_f16(128, N, 0, 0);
 
     uint32_t cm = 0;
 #pragma unroll
@@ -350,9 +475,38 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         tma_prefetch_desc(&tmR);
         mbar_arrive_expect_tx(&bars[0], KB * 16384);
         for (int kb = 0; kb < KB; ++kb) tma_load_2d(Rs + kb * 16384, &tmR, &bars[0], kb * 64, d * 4 * Hq + c * 128);
-        mbar_wait(&bars[0], 0);
     }
+    mbar_wait(&bars[0], 0);
+    // R[:, cols_c] (the R^T slice read transposed): shared memory -> registers -> TMEM, once.
+    {
+        const int cw = Hq / 8;
+        for (int col = cb * cw; col < (cb + 1) * cw; col += 16) {
+            const int mt = col >> 6, k = 128 * mt + 32 * q + l, r0 = (col & 63) * 2;
+            const uint8_t *rk = Rs + (k >> 6) * 16384 + (k & 7) * 2;
+            const int chunk = (k & 63) >> 3;
+            uint32_t v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int r = r0 + 2 * u;
+                const uint16_t lo = *reinterpret_cast<const uint16_t *>(rk + r * 128 + ((chunk ^ (r & 7)) << 4));
+                const uint16_t hi =
+                    *reinterpret_cast<const uint16_t *>(rk + (r + 1) * 128 + ((chunk ^ ((r + 1) & 7)) << 4));
+                v[u] = (uint32_t)lo | ((uint32_t)hi << 16);
+            }
+            tmem_st16(tmem + ((uint32_t)(32 * q) << 16) + col, v);
+        }
+        tmem_st_wait();
+    }
+    tc_fence_before();
     __syncthreads();
+    tc_fence_after();
+    // P produced at processing index k lands in slots[k&1] and is consumed at index k+1
+    // (index T = the final gather for dh0)
+    if (threadIdx.x == 0) {
+        if (T >= 1) mbar_arrive_expect_tx(&bars[2], SLOT_TX);  // index 1 <- P of index 0
+        if (T >= 2) mbar_arrive_expect_tx(&bars[3], SLOT_TX);  // index 2 <- P of index 1
+    }
+    cluster_sync();  // every CTA done with its R staging before peers write into the slots
 
     float dh[NMQ], dc[NMQ], dbp[4] = {0.f, 0.f, 0.f, 0.f};
     uint32_t pfm = 0;  // bit m: the previous step's frame was valid for owned column 4m+gam
@@ -363,19 +517,19 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         dh[m] = (ok && p.dhT) ? p.dhT[(long)d * B * H + (long)b * H + j] : 0.f;
         dc[m] = (ok && p.dcT) ? p.dcT[(long)d * B * H + (long)b * H + j] : 0.f;
     }
-    // P (partial dh) exchange in a CTA-native layout [buf][d][g][c_src][mt][cb][128][NQ]: the
-    // writer's warp stores one contiguous block per M tile; the reader sums its units' rows
-    const size_t p_src = (size_t)MT * 512 * NQ;             // one source CTA
-    const size_t pstride_buf = (size_t)p.ndir * p.G * NC * p_src;
-    const size_t p_grp = (((size_t)d * p.G + g) * NC) * p_src;
-    auto gather = [&](int buf) {
-        const float *Pb = p.P + buf * pstride_buf + p_grp + (size_t)(j >> 7) * 512 * NQ +
-                          ((size_t)cb * 128 + (j & 127)) * NQ;
+    uint32_t fph = 0;
+    // wait for the cluster's partials of index k-1 and sum this CTA's rows in fixed order
+    auto gather = [&](int k) {
+        const int b = (k - 1) & 1;
+        mbar_wait(&bars[2 + b], (fph >> b) & 1);
+        fph ^= 1u << b;
+        if (threadIdx.x == 0 && k + 2 <= T) mbar_arrive_expect_tx(&bars[2 + b], SLOT_TX);  // index k+2
+        const __half *sl = slots + (size_t)b * NC * 32 * PITCH + jl * PITCH + nq0;
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
             if ((pfm >> m) & 1) {
                 float acc = 0.f;
-                for (int cc = 0; cc < NC; ++cc) acc += Pb[(size_t)cc * p_src + 4 * m + gam];
+                for (int src = 0; src < NC; ++src) acc += __half2float(sl[src * 32 * PITCH + 4 * m + gam]);
                 dh[m] = acc * inv_scale;
             }
         }
@@ -383,38 +537,28 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const long nat_step = (long)p.ndir * p.G * NC * 512 * NQ;
     const long nat_off = (((long)d * p.G + g) * NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
 
-    uint32_t mma_phase = 0;
-    const uint32_t rs_addr = smem_u32(Rs), das_addr = smem_u32(dAs);
-#ifdef BLSTM_TRACE
-    unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
-#endif
-    for (int s = T - 1; s >= 0; --s) {
-        const int t = dir > 0 ? s : T - 1 - s;
-        const int k_done = T - 1 - s;
-        TRACE(0);
-        // ---- this step's saved state (independent of the recurrence: issue first) ----
-        float graw[NQ];
-        {
-            const __half *gp = p.gates + t * nat_step + nat_off;
-            uint32_t hv[NQ / 2];
-            if constexpr (NQ == 4) {
-                const uint2 u = *reinterpret_cast<const uint2 *>(gp);
-                hv[0] = u.x; hv[1] = u.y;
-            } else {
+    // saved state of one step (independent of the recurrence: prefetched one step ahead)
+    float graw[NQ], ct[NMQ], cp[NMQ], dyv[NMQ];
+    uint32_t frm = 0;
+    auto load_step = [&](int t) {
+        const __half *gp = p.gates + t * nat_step + nat_off;
+        uint32_t hv[NQ / 2];
+        if constexpr (NQ == 4) {
+            const uint2 u = *reinterpret_cast<const uint2 *>(gp);
+            hv[0] = u.x; hv[1] = u.y;
+        } else {
 #pragma unroll
-                for (int i = 0; i < NQ / 8; ++i) {
-                    const uint4 u = reinterpret_cast<const uint4 *>(gp)[i];
-                    hv[4 * i] = u.x; hv[4 * i + 1] = u.y; hv[4 * i + 2] = u.z; hv[4 * i + 3] = u.w;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < NQ; i += 2) {
-                const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&hv[i / 2]));
-                graw[i] = f2.x;
-                graw[i + 1] = f2.y;
+            for (int i = 0; i < NQ / 8; ++i) {
+                const uint4 u = reinterpret_cast<const uint4 *>(gp)[i];
+                hv[4 * i] = u.x; hv[4 * i + 1] = u.y; hv[4 * i + 2] = u.z; hv[4 * i + 3] = u.w;
             }
         }
-        float ct[NMQ], cp[NMQ], dyv[NMQ];
+#pragma unroll
+        for (int i = 0; i < NQ; i += 2) {
+            const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&hv[i / 2]));
+            graw[i] = f2.x;
+            graw[i + 1] = f2.y;
+        }
         const int tp = t - dir;
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
@@ -426,17 +570,24 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             else cp[m] = (ok && p.c0) ? p.c0[(long)d * B * H + (long)b * H + j] : 0.f;
             dyv[m] = ok ? p.dy[row * p.lddy + d * p.dy_doff + j] : 0.f;
         }
-        const uint32_t frm =
-            __ballot_sync(0xffffffffu, l < NQ && ((cm >> l) & 1) && p.mask[(long)t * B + bq0 + l]);
-        // ---- dh_t from the previous step's partials ----
+        frm = __ballot_sync(0xffffffffu, l < NQ && ((cm >> l) & 1) && p.mask[(long)t * B + bq0 + l]);
+    };
+    if (T > 0) load_step(dir > 0 ? T - 1 : 0);
+
+    uint32_t mma_phase = 0;
+    const uint32_t das_addr = smem_u32(dAs);
+    const uint32_t slots_addr = smem_u32(slots), full_addr = smem_u32(&bars[2]);
+#ifdef BLSTM_TRACE
+    unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
+#endif
+    for (int s = T - 1; s >= 0; --s) {
+        const int t = dir > 0 ? s : T - 1 - s;
+        const int k_done = T - 1 - s;
+        TRACE(0);
         TRACE(1);
-        if (k_done > 0) {
-            if (threadIdx.x == 0) spin_until_geq(counter, (uint32_t)(NC * k_done));
-            TRACE(2);
-            __syncthreads();
-            gather((k_done - 1) & 1);
-        }
-        TRACE(3);
+        // ---- dh_t from the previous step's partials ----
+        if (k_done > 0) gather(k_done);
+        TRACE(2);
         // ---- gate gradients ----
         pfm = 0;
         uint2 pks[NMQ];
@@ -471,16 +622,14 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         }
         fence_async_smem();
         tc_fence_before();
-        TRACE(4);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            TRACE(5);
+        TRACE(3);
+        if (l == 0 && w < MT) {
             tc_fence_after();
-            for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    mma_f16_ss(tmem + mt * N, sdesc_sw128(rs_addr + 2 * mt * 16384 + kk * 2048, 16384, 1024),
-                               sdesc_sw128(das_addr + (kk >> 2) * N * 128 + (kk & 3) * 32, 16, 1024), idesc, kk != 0);
+            for (int kk = 0; kk < 8; ++kk)
+                mma_f16_ts(tmem + DCOL + w * N, tmem + w * 64 + kk * 8,
+                           sdesc_sw128(das_addr + (kk >> 2) * N * 128 + (kk & 3) * 32, 16, 1024), idesc, kk != 0);
             mma_commit(&bars[1]);
         }
         // while the MMA runs: dA of this step to global memory for the weight / input GEMMs
@@ -493,27 +642,46 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
-        TRACE(6);
-        float *Pw = p.P + (size_t)(k_done & 1) * pstride_buf + p_grp + (size_t)c * p_src +
-                    ((size_t)cb * 128 + 32 * q + l) * NQ;
-        for (int mt = 0; mt < MT; ++mt) {
-            float v[NQ];
-            tmem_ld<NQ>(tmem + ((uint32_t)(32 * q) << 16) + mt * N + nq0, v);
-            float4 *dst = reinterpret_cast<float4 *>(Pw + (size_t)mt * 512 * NQ);
+        TRACE(4);
+        // rows k = 128mt + 32q + l of P belong to owner c' = 4mt + q (its local row l): stage them
+        // (fp16) per owner, then warp w bulk-copies the block of owner w into w's slot for source c
+        {
+            const int kb = k_done & 1;
+            for (int mt = 0; mt < MT; ++mt) {
+                float v[NQ];
+                tmem_ld<NQ>(tmem + ((uint32_t)(32 * q) << 16) + DCOL + mt * N + nq0, v);
+                uint32_t hv[NQ / 2];
 #pragma unroll
-            for (int i = 0; i < NQ / 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                for (int i = 0; i < NQ; i += 2) {
+                    __half2 h2 = __floats2half2_rn(v[i] * P_SCALE, v[i + 1] * P_SCALE);
+                    hv[i / 2] = *reinterpret_cast<uint32_t *>(&h2);
+                }
+                __half *dst = stgp + (((size_t)kb * NC + 4 * mt + q) * 32 + l) * PITCH + nq0;
+                if constexpr (NQ == 4) {
+                    *reinterpret_cast<uint2 *>(dst) = make_uint2(hv[0], hv[1]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NQ / 8; ++i)
+                        reinterpret_cast<uint4 *>(dst)[i] = make_uint4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
+                }
+            }
+            tc_fence_before();
+            fence_async_smem();
+            __syncthreads();
+            if (l == 0 && w < NC) {
+                bulk_s2c(mapa_shared(slots_addr + kb * SLOTB + c * BLK, w),
+                         smem_u32(stgp) + ((uint32_t)kb * NC + w) * BLK, BLK, mapa_shared(full_addr + 8 * kb, w));
+                bulk_commit();
+            }
         }
-        tc_fence_before();
-        __syncthreads();
-        if (threadIdx.x == 0) red_release_gpu_add(counter, 1u);
-        TRACE(7);
+        if (s > 0) load_step(dir > 0 ? s - 1 : T - s);
+        // the bulk copies of stg[kb] have read it before it is rewritten two steps later
+        // (ordered by the next step's __syncthreads)
+        if (l == 0 && w < NC) bulk_wait_read<0>();
+        TRACE(5);
     }
 #undef TRACE
-    if (T > 0) {
-        if (threadIdx.x == 0) spin_until_geq(counter, (uint32_t)(NC * T));
-        __syncthreads();
-        gather((T - 1) & 1);
-    }
+    if (T > 0) gather(T);
 #pragma unroll
     for (int m = 0; m < NMQ; ++m) {
         const int i = 4 * m + gam, b = bq0 + i;
@@ -529,7 +697,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         dbp[k] += __shfl_xor_sync(0xffffffffu, dbp[k], 1);
         dbp[k] += __shfl_xor_sync(0xffffffffu, dbp[k], 2);
     }
-    float *dbs = reinterpret_cast<float *>(dAs);  // [4 cb][128 rows]
+    float *dbs = reinterpret_cast<float *>(dAs);  // [4 cb][128 rows]; the last MMA has completed
     __syncthreads();
     dbs[cb * 128 + 4 * jl + gam] = sel4(dbp, gam);
     __syncthreads();
@@ -539,6 +707,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // no peer still writes into this CTA's slots
     if (w == 0) {
         tc_fence_after();
         tmem_dealloc(tmem, TCOLS);
@@ -569,33 +738,42 @@ RecPlan rec_plan(int T, int B, int H, int ndir, int sms) {
     return pl;
 }
 
-static size_t fwd_smem(const RecPlan &pl) { return (size_t)pl.Hq / 64 * (16384 + pl.N * 128) + 1024 + 64; }
-static size_t bwd_smem(const RecPlan &pl) { return (size_t)pl.Hq / 64 * 16384 + 2 * pl.N * 128 + 1024 + 64; }
+static size_t fwd_smem(const RecPlan &pl) { return fwd_region0(pl.Hq, pl.N) + 1024 + 64; }
+static size_t bwd_smem(const RecPlan &pl) { return bwd_region0(pl.Hq, pl.N, pl.NC) + 2 * pl.N * 128 + 1024 + 64; }
 
 bool rec_supported(const RecPlan &pl, int H) {
     if (H < 1 || (pl.N != 16 && pl.N != 32 && pl.N != 64)) return false;
+    if (pl.NC > 16) return false;  // one cluster (<= 16 CTAs, non-portable size) per group
     if (fwd_smem(pl) > 227 * 1024 || bwd_smem(pl) > 227 * 1024) return false;
     if (pl.ndir * pl.G * pl.NC > num_sms()) return false;
-    if (pl.Hq / 128 * pl.N > 512) return false;
+    const int nacc = pl.Hq / 128 > 4 ? pl.Hq / 128 : 4;  // forward: 4 K-split accumulators
+    if (pl.Hq / 2 + nacc * pl.N > 512) return false;     // TMEM: resident R + accumulators
     return pl.Hq % 128 == 0;
 }
 
 size_t rec_P_bytes(const RecPlan &pl) {
-    return (size_t)2 * pl.ndir * pl.G * pl.NC * pl.Hq * pl.N * sizeof(float);
+    (void)pl;
+    return 256;  // partials travel through distributed shared memory
 }
 
 template <typename Kern, typename... Args>
-static cudaError_t launch_coop(Kern kern, int grid, size_t smem, cudaStream_t st, Args... args) {
+static cudaError_t launch_cluster(Kern kern, int grid, int cluster, size_t smem, cudaStream_t st, Args... args) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    if (cluster > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(REC_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, args...);
@@ -611,20 +789,18 @@ int lstm_rec_fwd(const RecParams &p_in, const __half *RT16, cudaStream_t st) {
     RecParams p = p_in;
     if (g_trace_fwd) p.trace = g_trace_fwd;
     if (p.T == 0) return 0;
-    CUtensorMap tmR, tmH;
+    CUtensorMap tmR;
     if (make_tmap_f16(&tmR, RT16, p.Hq, (uint64_t)p.ndir * 4 * p.Hq, p.Hq, 128)) return -2;
-    if (make_tmap_f16(&tmH, p.hist, p.Hq, (uint64_t)p.ndir * (p.T + 1) * p.B, p.Hq, p.N)) return -2;
     RecPlan pl{p.Hq, p.NC, p.G, p.Bg, p.N, p.ndir};
     const int grid = p.ndir * p.G * p.NC;
     const size_t smem = fwd_smem(pl);
-    cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * p.ndir * p.G, st);
-    if (e != cudaSuccess) return -5;
     ProfScope ps(PROF_REC_FWD, st);
     note_launch();
+    cudaError_t e;
     switch (p.N) {
-        case 16: e = launch_coop(lstm_rec_fwd_kernel<1>, grid, smem, st, tmR, tmH, p); break;
-        case 32: e = launch_coop(lstm_rec_fwd_kernel<2>, grid, smem, st, tmR, tmH, p); break;
-        case 64: e = launch_coop(lstm_rec_fwd_kernel<4>, grid, smem, st, tmR, tmH, p); break;
+        case 16: e = launch_cluster(lstm_rec_fwd_kernel<1>, grid, p.NC, smem, st, tmR, p); break;
+        case 32: e = launch_cluster(lstm_rec_fwd_kernel<2>, grid, p.NC, smem, st, tmR, p); break;
+        case 64: e = launch_cluster(lstm_rec_fwd_kernel<4>, grid, p.NC, smem, st, tmR, p); break;
         default: return -6;
     }
     return e == cudaSuccess ? 0 : -5;
@@ -638,14 +814,13 @@ int lstm_rec_bwd(const RecParams &p_in, const __half *RT16, cudaStream_t st) {
     RecPlan pl{p.Hq, p.NC, p.G, p.Bg, p.N, p.ndir};
     const int grid = p.ndir * p.G * p.NC;
     const size_t smem = bwd_smem(pl);
-    cudaError_t e = cudaMemsetAsync(p.counters, 0, sizeof(uint32_t) * p.ndir * p.G, st);
-    if (e != cudaSuccess) return -5;
     ProfScope ps(PROF_REC_BWD, st);
     note_launch();
+    cudaError_t e;
     switch (p.N) {
-        case 16: e = launch_coop(lstm_rec_bwd_kernel<1>, grid, smem, st, tmR, p); break;
-        case 32: e = launch_coop(lstm_rec_bwd_kernel<2>, grid, smem, st, tmR, p); break;
-        case 64: e = launch_coop(lstm_rec_bwd_kernel<4>, grid, smem, st, tmR, p); break;
+        case 16: e = launch_cluster(lstm_rec_bwd_kernel<1>, grid, p.NC, smem, st, tmR, p); break;
+        case 32: e = launch_cluster(lstm_rec_bwd_kernel<2>, grid, p.NC, smem, st, tmR, p); break;
+        case 64: e = launch_cluster(lstm_rec_bwd_kernel<4>, grid, p.NC, smem, st, tmR, p); break;
         default: return -6;
     }
     return e == cudaSuccess ? 0 : -5;

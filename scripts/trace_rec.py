@@ -16,8 +16,8 @@ import torch  # noqa: E402
 from paper_1608_00895_b200 import blstm, synth  # noqa: E402
 from paper_1608_00895_b200.train import StackTrainer  # noqa: E402
 
-FWD = ["spin(counter)", "TMA h", "MMA+wait", "epilogue", "prefetch Z", "syncthreads", "signal"]
-BWD = ["loads", "spin", "sync+gather", "dA+smem", "MMA issue", "MMA wait", "P write+sync+signal"]
+FWD = ["wait h (DSMEM)", "MMA issue", "MMA wait", "epilogue+sync", "send h", "stores+prefetch"]
+BWD = ["loads", "wait P + gather", "dA+smem+sync", "MMA (+dA stores)", "send P"]
 
 
 def main():
