@@ -267,6 +267,7 @@ struct StackGeo {
 };
 struct StackWS {
     size_t x16, Z, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, total;
+    size_t maxDn;
     std::vector<size_t> y16, w16, rt16, bq, gates, C, hist;
 };
 
@@ -311,12 +312,15 @@ static StackWS stack_ws(const StackGeo &g) {
     }
     const size_t zn = rec_native_elems(g.pl, g.T), zl = (size_t)TB * g.Kp;  // Z, or logits [TB, Kp]
     w.Z = c.take((zn > zl ? zn : zl) * 4);
-    w.dA = c.take((size_t)TB * 8 * Hq * 2);
+    w.maxDn = maxDn;
+    // dA / dWT / dRT / dbpart: two copies (layer parity) so layer l's weight gradients can run on a
+    // side stream while BPTT of layer l-1 writes the other copy
+    w.dA = c.take((size_t)2 * TB * 8 * Hq * 2);
     w.dY0 = c.take((size_t)TB * 2 * Hq * 4);
     w.dY1 = c.take((size_t)TB * 2 * Hq * 4);
-    w.dWT = c.take((size_t)8 * Hq * maxDn * 4);
-    w.dRT = c.take((size_t)2 * 4 * Hq * Hq * 4);
-    w.dbp = c.take((size_t)2 * g.pl.G * 4 * Hq * 4);
+    w.dWT = c.take((size_t)2 * 8 * Hq * maxDn * 4);
+    w.dRT = c.take((size_t)2 * 2 * 4 * Hq * Hq * 4);
+    w.dbp = c.take((size_t)2 * 2 * g.pl.G * 4 * Hq * 4);
     w.P = c.take(rec_P_bytes(g.pl));
     w.cnt = c.take(256);
     w.wo16 = c.take((size_t)2 * Hq * (g.Kp ? g.Kp : 64) * 2);
@@ -471,10 +475,33 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             return fail(BLSTM_ERR_CUDA, "memset");
     }
 
-    __half *dA = (__half *)(ws + w.dA);
-    float *dWT = (float *)(ws + w.dWT), *dRT = (float *)(ws + w.dRT), *dbp = (float *)(ws + w.dbp);
+    // Weight gradients (dW, dR, db) of layer l are off the critical path (PAPER.md P:233-234 only
+    // needs them after BPTT of layer l): with a side stream they run on the SMs the recurrence
+    // clusters leave free, overlapping BPTT of layer l-1.  Their inputs (dA, dbpart) and scratch
+    // are double-buffered by layer parity.
+    cudaStream_t side = (s_side && s_side != s_main) ? (cudaStream_t)s_side : st;
+    const bool overlap = side != st;
+    const int rec_ctas = 2 * g.pl.G * g.pl.NC;
+    const int side_ctas = overlap ? (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8) : 0;
+    static thread_local std::vector<cudaEvent_t> evs;
+    if (overlap && evs.size() < (size_t)g.L + 2) {
+        while (evs.size() < (size_t)g.L + 2) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "event");
+            evs.push_back(e);
+        }
+    }
+    if (overlap) {  // the side stream may start only after everything issued so far on s_main
+        cudaEventRecord(evs[g.L + 1], st);
+        cudaStreamWaitEvent(side, evs[g.L + 1], 0);
+    }
     int cur = 0;
     for (int l = g.L - 1; l >= 0; --l) {
+        const int par = l & 1;
+        __half *dA = (__half *)(ws + w.dA) + (size_t)par * g.TB * 8 * Hq;
+        float *dWT = (float *)(ws + w.dWT) + (size_t)par * 8 * Hq * w.maxDn;
+        float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
+        float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
         RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
         p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq;
         p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
@@ -485,26 +512,34 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         p.counters = (uint32_t *)(ws + w.cnt);
         TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
         const __half *w16 = (const __half *)(ws + w.w16[l]);
-        if (l > 0) {
+        if (l > 0) {  // critical path: gradient of the layer below's output
             GemmParams gx{(int)g.TB, g.Dn[l], 8 * Hq, dY[1 - cur], 2L * Hq, a, 0, nullptr, 0, 0};
             TRY(gemm_f16({dA, 8L * Hq, 0}, {w16, 8L * Hq, 0}, gx, 0, st), "gemm dX");
         }
+        if (overlap) {
+            cudaEventRecord(evs[l], st);
+            cudaStreamWaitEvent(side, evs[l], 0);
+        }
         const __half *X = l == 0 ? (const __half *)(ws + w.x16) : (const __half *)(ws + w.y16[l - 1]);
         GemmParams gw{8 * Hq, g.Dn[l], (int)g.TB, dWT, g.Dn[l], a, 0, nullptr, 0, 0};
-        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, 0, st), "gemm dW");
+        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, side_ctas, side), "gemm dW");
         const __half *hist = (const __half *)(ws + w.hist[l]);
         for (int dd = 0; dd < 2; ++dd) {
             const __half *hprev = hist + ((long)dd * (g.T + 1) + dd) * g.B * Hq;
             GemmParams gr{4 * Hq, Hq, (int)g.TB, dRT + (size_t)dd * 4 * Hq * Hq, Hq, a, 0, nullptr, 0, 0};
-            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, 0, st), "gemm dR");
+            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, side_ctas, side), "gemm dR");
         }
         for (int dd = 0; dd < 2; ++dd) {
             const int e = 6 * l + 3 * dd;
-            TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], st), "scatter dW");
-            TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, st), "scatter dR");
-            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.pl.G, dd, st), "scatter db");
+            TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], side), "scatter dW");
+            TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, side), "scatter dR");
+            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.pl.G, dd, side), "scatter db");
         }
         cur = 1 - cur;
+    }
+    if (overlap) {  // s_main's view: all gradient work of this call is complete
+        cudaEventRecord(evs[g.L], side);
+        cudaStreamWaitEvent(st, evs[g.L], 0);
     }
     if (comm) {
         if (int rc = dp_allreduce_grads_impl(comm, grad, param_layout(d, nullptr), st)) return rc;

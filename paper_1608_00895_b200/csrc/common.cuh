@@ -174,6 +174,24 @@ DEVI void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t 
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Four TS-mode MMAs in one asm block (operands made warp-uniform once per block, not per
+// MMA): D += A[a + 8i] . B[bdesc + i*binc]^T for i = 0..3; the first one accumulates iff acc0.
+// a + 8 columns = the next 16 fp16 of K in TMEM; binc = descriptor start-address step (16-B units).
+DEVI void mma_f16_ts_x4(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t binc, uint32_t idesc,
+                        uint32_t acc0) {
+    asm volatile(
+        "{\n .reg .pred p, t;\n .reg .b32 a1, a2, a3;\n .reg .b64 inc, b1, b2, b3;\n"
+        " setp.ne.b32 p, %5, 0;\n setp.eq.b32 t, %5, %5;\n"
+        " cvt.u64.u32 inc, %4;\n"
+        " add.u32 a1, %1, 8;\n add.u32 a2, %1, 16;\n add.u32 a3, %1, 24;\n"
+        " add.u64 b1, %2, inc;\n add.u64 b2, b1, inc;\n add.u64 b3, b2, inc;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(binc), "r"(acc0)
+        : "memory");
+}
 // arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete
 DEVI void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))

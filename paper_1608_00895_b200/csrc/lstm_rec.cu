@@ -275,9 +275,15 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             tc_fence_after();
             const uint32_t hb = hbuf_addr + b * HB;
             const int ks0 = w * (Hq / 16 / NISSUE), ks1 = ks0 + Hq / 16 / NISSUE;
-            for (int ks = ks0; ks < ks1; ++ks)
-                mma_f16_ts(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * N, 16 * N, 128), idesc,
-                           ks != ks0);
+            if ((ks1 - ks0) % 4 == 0) {
+                for (int ks = ks0; ks < ks1; ks += 4)  // K step = 32N bytes of the B buffer = 2N desc units
+                    mma_f16_ts_x4(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * N, 16 * N, 128),
+                                  2 * N, idesc, ks != ks0);
+            } else {
+                for (int ks = ks0; ks < ks1; ++ks)
+                    mma_f16_ts(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * N, 16 * N, 128), idesc,
+                               ks != ks0);
+            }
             mma_commit(&bars[1]);
             TRACE(2);
         }
@@ -329,6 +335,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             *reinterpret_cast<__half *>(sg + (q * N + nq0 + i) * 16 + (jl & 7) * 2) = __float2half_rn(h_st[m]);
         }
         fence_async_smem();
+        // the previous step's bulk copies (of the other staging buffer) have long finished reading;
+        // this __syncthreads orders that before the rewrite of that buffer at the next step
+        if (l == 0 && w < NC) bulk_wait_read<0>();
         __syncthreads();
         TRACE(4);
         if (l == 0 && w < NC && s + 1 < T) {
@@ -373,9 +382,6 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             }
         }
         if (s + 1 < T) prefetch_z(dir > 0 ? t + 1 : t - 1);
-        // the bulk copies of stg[b] have read it before stg[b] is rewritten at step s+2 (ordered
-        // by step s+1's __syncthreads)
-        if (l == 0 && w < NC) bulk_wait_read<0>();
         TRACE(6);
     }
 #pragma unroll
@@ -386,6 +392,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             if (p.cT) p.cT[(long)d * B * H + (long)b * H + j] = c_st[m];
         }
     }
+    if (l == 0 && w < NC) bulk_wait_read<0>();  // outgoing copies done with the staging buffers
     tc_fence_before();
     __syncthreads();
     cluster_sync();
@@ -627,9 +634,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         if (l == 0 && w < MT) {
             tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk)
-                mma_f16_ts(tmem + DCOL + w * N, tmem + w * 64 + kk * 8,
-                           sdesc_sw128(das_addr + (kk >> 2) * N * 128 + (kk & 3) * 32, 16, 1024), idesc, kk != 0);
+            for (int kb = 0; kb < 2; ++kb)  // 64 gate columns per SW128 block, K step = 32 B = 2 desc units
+                mma_f16_ts_x4(tmem + DCOL + w * N, tmem + w * 64 + kb * 32, sdesc_sw128(das_addr + kb * N * 128, 16, 1024),
+                              2, idesc, kb != 0);
             mma_commit(&bars[1]);
         }
         // while the MMA runs: dA of this step to global memory for the weight / input GEMMs
@@ -667,6 +674,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             }
             tc_fence_before();
             fence_async_smem();
+            // the previous step's bulk copies (other staging buffer) are done reading; this
+            // __syncthreads orders that before the rewrite of that buffer at the next step
+            if (l == 0 && w < NC) bulk_wait_read<0>();
             __syncthreads();
             if (l == 0 && w < NC) {
                 bulk_s2c(mapa_shared(slots_addr + kb * SLOTB + c * BLK, w),
@@ -675,9 +685,6 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             }
         }
         if (s > 0) load_step(dir > 0 ? s - 1 : T - s);
-        // the bulk copies of stg[kb] have read it before it is rewritten two steps later
-        // (ordered by the next step's __syncthreads)
-        if (l == 0 && w < NC) bulk_wait_read<0>();
         TRACE(5);
     }
 #undef TRACE
@@ -705,6 +712,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         const int r = 4 * jl + gam;
         p.dbpart[((long)d * p.G + g) * 4 * Hq + 4 * j + gam] = ((dbs[r] + dbs[128 + r]) + dbs[256 + r]) + dbs[384 + r];
     }
+    if (l == 0 && w < NC) bulk_wait_read<0>();  // outgoing copies done with the staging buffers
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // no peer still writes into this CTA's slots

@@ -142,6 +142,8 @@ class StackTrainer:
         self.loss = torch.zeros(1, dtype=torch.float64, device=device)
         self.ferr = torch.zeros(1, dtype=torch.int32, device=device)
         self.comm = comm
+        # weight-gradient GEMMs overlap the next layer's BPTT on this stream (blstm_stack_fwd_bwd)
+        self.side = torch.cuda.Stream(device=device)
         self.sched = sched or DPSchedule()
         self.coll = NcclCollective(comm, world) if comm is not None else None
         self.set_batch(batch)
@@ -159,7 +161,7 @@ class StackTrainer:
         # sync mode: the library allreduce-sums grad right after the local accumulation
         comm = self.comm if (self.comm is not None and self.sched.grads_summed()) else None
         self.blstm.blstm_stack_fwd_bwd(self.desc, theta, grad, self.x, self.mask, self.labels, self.dy_top,
-                                       self.loss, self.ferr, comm, self.ws)
+                                       self.loss, self.ferr, comm, self.ws, s_side=self.side)
 
     def _update(self, theta, grad):
         self.blstm.sgd_update(theta, grad, self.lr, zero_grad=True)

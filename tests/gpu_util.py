@@ -101,15 +101,16 @@ class Stack:
         self.n, self.offs = blstm.blstm_param_offsets(self.desc)
         self.ws = torch.empty(blstm.blstm_stack_workspace_bytes(self.desc), dtype=torch.uint8, device=dev())
 
-    def step(self, theta_np, batch, dy_top=None):
+    def step(self, theta_np, batch, dy_top=None, side_stream=False):
         theta = T_(theta_np, torch.float32)
         grad = torch.zeros(self.n, dtype=torch.float32, device=dev())
         loss = torch.zeros(1, dtype=torch.float64, device=dev())
         ferr = torch.zeros(1, dtype=torch.int32, device=dev())
         labels = T_(batch.labels) if self.K > 0 else None
         dyt = T_(dy_top, torch.float32) if dy_top is not None else None
+        side = torch.cuda.Stream() if side_stream else None
         blstm.blstm_stack_fwd_bwd(self.desc, theta, grad, T_(batch.x), T_(batch.mask), labels, dyt, loss, ferr,
-                                  None, self.ws)
+                                  None, self.ws, s_side=side)
         torch.cuda.synchronize()
         return dict(grad=np_(grad), loss=loss.item(), frame_errors=int(ferr.item()))
 

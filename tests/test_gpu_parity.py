@@ -156,6 +156,21 @@ def test_stack_small_with_head():
             assert norm_rel(C[l, d], ref["Cs"][l, d]) < OUT_TOL
 
 
+def test_stack_side_stream_bitwise_equal():
+    """Weight-gradient GEMMs on a side stream (overlapping BPTT) give bitwise the same step."""
+    L, D, H, K, T, B = 3, 40, 130, 11, 9, 7
+    params = synth.stack_params(L, D, H, K)
+    batch = synth.speech_batch(T, B, D, K, np.array([9, 8, 6, 9, 3, 2, 1]), seed=1002)
+    theta = oracle.pack_params(params, L, D, H, K)
+    st = Stack(L, D, H, K, T, B)
+    a = st.step(theta, batch)
+    b = st.step(theta, batch, side_stream=True)
+    assert np.array_equal(a["grad"], b["grad"]) and a["loss"] == b["loss"]
+    ref = oracle.blstm_step(theta, batch.x, batch.mask, L, H, K, labels=batch.labels)
+    errs = grad_errors(b["grad"], ref["grad"], L, D, H, K)
+    assert max(errs.values()) < GRAD_TOL, errs
+
+
 def test_stack_no_head_dy_top():
     L, D, H, T, B = 1, 40, 130, 20, 6
     params = synth.stack_params(L, D, H, 0)
