@@ -107,6 +107,23 @@ def dp_step(theta, grad, compute_grad: Callable[[object, object], None], update:
         coll.mean_(theta)
 
 
+def reduce_over_ranks(value: float, op: str, world: int, device=None) -> float:
+    """max / sum of a scalar over all ranks (the bench's max-over-ranks time, total frames)."""
+    if world == 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def rank_data_seed(rank: int) -> int:
+    """Each rank trains on its own batches: data seed 1000 + rank."""
+    from .synth import DATA_SEED_BASE
+    return DATA_SEED_BASE + rank
+
+
 # ----------------------------------------------------------------------------
 # CUDA stack runner
 # ----------------------------------------------------------------------------
