@@ -32,7 +32,7 @@ struct GemmCfg {
     static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
     static constexpr int B_BYTES = BN * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 2 * BN * 4 /*bias*/;
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -146,9 +146,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int row_in_tile = q * 32 + lane_id();
         int acc = 0;
         uint32_t acc_phase = 0;
+        float *sbias = reinterpret_cast<float *>(tmem_slot + 4);  // [2][BN], one per accumulator
+        const int et = threadIdx.x - 64;                           // 0..127 over the epilogue warps
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int m0 = (tile % num_m) * GEMM_BM;
             const int n0 = (tile / num_m) * BN;
+            // this tile's bias slice -> shared memory while the MMAs run (a global load per
+            // element in the store loop stalled the epilogue on L2 latency)
+            for (int k = et; k < BN; k += 128)
+                sbias[acc * BN + k] = (p.bias && n0 + k < p.N) ? p.bias[n0 + k] : 0.f;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const float *bs = sbias + acc * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int m = m0 + row_in_tile;
@@ -159,6 +167,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
                 tmem_ld_wait();
                 const int n = n0 + c;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = v[j] * p.alpha + bs[c + j];
                 if (m < p.M && n < p.N && p.natB) {
                     // CTA-native layout of the recurrence (see lstm_rec.h): the 16 columns stay in
                     // one 128-row block of one CTA, consecutive columns are NQ floats apart
@@ -172,29 +182,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     float *base = p.C + rm + cn;
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
-                        if (n + j < p.N) base[(long)j * p.natNQ] = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
-                } else if (m < p.M && n < p.N && p.remapB) {
-                    // time-major transposed output: row m = t*B + b -> C[(t*ldc + col)*B + b]
-                    const long t = m / p.remapB, b = m - t * p.remapB;
-                    float *base = p.C + (size_t)t * p.ldc * p.remapB + b;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (n + j < p.N) {
-                            float o = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
-                            float *dst = base + (size_t)(n + j) * p.remapB;
-                            if (p.beta) o += *dst;
-                            *dst = o;
-                        }
+                        if (n + j < p.N) base[(long)j * p.natNQ] = v[j];
                 } else if (m < p.M && n < p.N) {
                     if (n + 16 <= p.N && (p.ldc & 3) == 0) {
 #pragma unroll
                         for (int j = 0; j < 16; j += 4) {
-                            float4 o = make_float4(v[j] * p.alpha, v[j + 1] * p.alpha, v[j + 2] * p.alpha,
-                                                   v[j + 3] * p.alpha);
-                            if (p.bias) {
-                                o.x += p.bias[n + j]; o.y += p.bias[n + j + 1];
-                                o.z += p.bias[n + j + 2]; o.w += p.bias[n + j + 3];
-                            }
+                            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                             float4 *dst = reinterpret_cast<float4 *>(crow + n + j);
                             if (p.beta) {
                                 const float4 old = *dst;
@@ -205,11 +198,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     } else {
 #pragma unroll
                         for (int j = 0; j < 16; ++j)
-                            if (n + j < p.N) {
-                                float o = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
-                                if (p.beta) o += crow[n + j];
-                                crow[n + j] = o;
-                            }
+                            if (n + j < p.N) crow[n + j] = p.beta ? crow[n + j] + v[j] : v[j];
                     }
                 }
             }

@@ -19,8 +19,6 @@ struct GemmParams {
     int beta;           // 1: C += result
     const float *bias;  // [N] or nullptr
     int a_mn, b_mn;     // filled by gemm_f16
-    long remapB = 0;    // > 0: rows are frames m = t*remapB + b and C is written time-major
-                        // transposed, C[(t*ldc + n)*remapB + b] (ldc = number of columns)
     // > 0: C is written in the recurrence kernels' CTA-native layout (lstm_rec.h, rec_native_index)
     int natB = 0, natBg = 0, natG = 0, natNQ = 0, natNC = 0, natHq4 = 0, natNdir = 0;
 };
