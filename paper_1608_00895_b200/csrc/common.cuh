@@ -174,6 +174,33 @@ DEVI void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t 
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-collective issue: the whole (converged) warp executes these and one elected lane issues.
+// With warp-uniform operands ptxas keeps them in uniform registers (UIADD3 + UTCHMMA, no
+// per-MMA ELECT / R2UR waterfall as when a single divergent thread issues).
+DEVI void mma_f16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+DEVI void mma_f16_ss_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+DEVI void mma_commit_w(uint64_t *bar) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+// a warp-uniform copy of v (lane 0's), so the compiler may keep it in a uniform register
+DEVI int warp_uniform(int v) { return __shfl_sync(0xffffffffu, v, 0); }
+
 // Four TS-mode MMAs in one asm block (operands made warp-uniform once per block, not per
 // MMA): D += A[a + 8i] . B[bdesc + i*binc]^T for i = 0..3; the first one accumulates iff acc0.
 // a + 8 columns = the next 16 fp16 of K in TMEM; binc = descriptor start-address step (16-B units).

@@ -10,10 +10,11 @@
 // A and B are fp16, each either K-major (element (r, k) at ptr[r*ld + k]) or MN-major
 // (element (r, k) at ptr[k*ld + r]); C is fp32 row-major.  fp32 accumulation in TMEM.
 //
-// Structure (persistent, one CTA per SM, 6 warps):
+// Structure (persistent, one CTA per SM, 10 warps):
 //   warp 0      TMA producer (one elected lane), STAGES-deep smem ring, 128B swizzle
 //   warp 1      TMEM allocator + MMA issuer (one lane), tcgen05.mma M=128 N=BN K=16
-//   warps 2..5  epilogue: tcgen05.ld -> alpha/bias/beta -> fp32 global stores
+//   warps 2..9  epilogue (two per TMEM lane quarter, each half of the columns):
+//               tcgen05.ld -> alpha/bias (bias staged in smem)/beta -> fp32 global stores
 //   Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the
 //   MMAs of tile i+1.
 #include "common.cuh"
@@ -24,7 +25,8 @@ namespace blstm {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 192;
+constexpr int GEMM_EPI_WARPS = 8;  // two per TMEM lane quarter, each half of the tile's columns
+constexpr int GEMM_THREADS = 64 + 32 * GEMM_EPI_WARPS;
 
 template <int BN>
 struct GemmCfg {
@@ -64,7 +66,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], GEMM_EPI_WARPS);
         }
         fence_mbar_init();
     }
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         const uint32_t idesc = idesc_f16(GEMM_BM, BN, p.a_mn, p.b_mn);
+        const int a_mn = warp_uniform(p.a_mn), b_mn = warp_uniform(p.b_mn);
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -121,19 +124,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
-                if (elect_one()) {
+                {  // warp-collective issue (one elected lane), operands warp-uniform
                     const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
                     const uint32_t sb = sa + Cfg::A_BYTES;
 #pragma unroll
                     for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
-                        const uint64_t ad = p.a_mn ? sdesc_sw128(sa + kk * 2048, 8192, 1024)
-                                                   : sdesc_sw128(sa + kk * 32, 16, 1024);
-                        const uint64_t bd = p.b_mn ? sdesc_sw128(sb + kk * 2048, 8192, 1024)
-                                                   : sdesc_sw128(sb + kk * 32, 16, 1024);
-                        mma_f16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                        const uint64_t ad = a_mn ? sdesc_sw128(sa + kk * 2048, 8192, 1024)
+                                                 : sdesc_sw128(sa + kk * 32, 16, 1024);
+                        const uint64_t bd = b_mn ? sdesc_sw128(sb + kk * 2048, 8192, 1024)
+                                                 : sdesc_sw128(sb + kk * 32, 16, 1024);
+                        mma_f16_ss_w(d_tmem, ad, bd, idesc, (kb | kk) != 0);
                     }
-                    mma_commit(&empty[stage]);
-                    if (kb == num_kb - 1) mma_commit(&tfull[acc]);
+                    mma_commit_w(&empty[stage]);
+                    if (kb == num_kb - 1) mma_commit_w(&tfull[acc]);
                 }
                 __syncwarp();
                 if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
@@ -141,28 +144,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     } else {
-        // ---------------- epilogue (warps 2..5) ----------------
+        // ---------------- epilogue (warps 2..9) ----------------
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int row_in_tile = q * 32 + lane_id();
         int acc = 0;
         uint32_t acc_phase = 0;
         float *sbias = reinterpret_cast<float *>(tmem_slot + 4);  // [2][BN], one per accumulator
-        const int et = threadIdx.x - 64;                           // 0..127 over the epilogue warps
+        const int et = threadIdx.x - 64;                           // 0..255 over the epilogue warps
+        const int chalf = (warp - 2) / 4;                          // column half of this warp
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             const int m0 = (tile % num_m) * GEMM_BM;
             const int n0 = (tile / num_m) * BN;
             // this tile's bias slice -> shared memory while the MMAs run (a global load per
             // element in the store loop stalled the epilogue on L2 latency)
-            for (int k = et; k < BN; k += 128)
+            for (int k = et; k < BN; k += 32 * GEMM_EPI_WARPS)
                 sbias[acc * BN + k] = (p.bias && n0 + k < p.N) ? p.bias[n0 + k] : 0.f;
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * GEMM_EPI_WARPS) : "memory");
             const float *bs = sbias + acc * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int m = m0 + row_in_tile;
             float *crow = p.C + (size_t)m * p.ldc;
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 16) {
+            for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 16) {
                 float v[16];
                 tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
                 tmem_ld_wait();

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const int g = grp % p.G;
     const int d = grp / p.G;
     const int dir = d == 0 ? p.dir0 : -1;
-    const int w = warp_id(), q = w & 3, cb = w >> 2, l = lane_id();
+    const int w = warp_uniform(warp_id()), q = w & 3, cb = w >> 2, l = lane_id();
     const int jl = 8 * q + (l >> 2), gam = l & 3;
     const int j = c * REC_UNITS + jl;
     const bool unit_ok = j < p.H;
@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const long nat_step = (long)p.ndir * p.G * NC * 512 * NQ;
     const long nat_off = (((long)d * p.G + g) * NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
     float zv[NQ];
+    uint32_t mraw = 0;  // mask byte of column l (lane l < NQ) of the prefetched step
     auto prefetch_z = [&](int t) {
         const float4 *zp = reinterpret_cast<const float4 *>(p.Z + t * nat_step + nat_off);
 #pragma unroll
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             const float4 v = __ldg(zp + i);
             zv[4 * i] = v.x; zv[4 * i + 1] = v.y; zv[4 * i + 2] = v.z; zv[4 * i + 3] = v.w;
         }
+        mraw = (l < NQ && ((cm >> l) & 1)) ? p.mask[(long)t * B + bq0 + l] : 0;
     };
     if (T > 0) prefetch_z(dir > 0 ? 0 : T - 1);
 
@@ -265,39 +267,71 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 #ifdef BLSTM_TRACE
     unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
 #endif
+    // HBM stores of a step (saved activations in CTA-native layout, c, y, y16, h history): off the
+    // critical path, so they are issued at the start of the NEXT step, behind its MMA issue
+    float act[NQ];
+    auto store_step = [&](int t, uint32_t frm, uint32_t fmq) {
+        {
+            uint32_t hv[NQ / 2];
+#pragma unroll
+            for (int i = 0; i < NQ; i += 2) {
+                const float a0 = (((frm >> i) & 1) && unit_ok) ? act[i] : 0.f;
+                const float a1 = (((frm >> (i + 1)) & 1) && unit_ok) ? act[i + 1] : 0.f;
+                __half2 h2 = __floats2half2_rn(a0, a1);
+                hv[i / 2] = *reinterpret_cast<uint32_t *>(&h2);
+            }
+            __half *gp = p.gates + t * nat_step + nat_off;
+            if constexpr (NQ == 4) {
+                *reinterpret_cast<uint2 *>(gp) = make_uint2(hv[0], hv[1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < NQ / 8; ++i)
+                    reinterpret_cast<uint4 *>(gp)[i] = make_uint4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
+            }
+        }
+        const int wslot = t + (dir > 0 ? 1 : 0);
+#pragma unroll
+        for (int m = 0; m < NMQ; ++m) {
+            const int i = 4 * m + gam;
+            if (((cm >> i) & 1)) {
+                const bool fm = (fmq >> m) & 1;
+                const long row = (long)t * B + bq0 + i;
+                if (unit_ok) {
+                    if (p.y) p.y[row * p.ldy + d * p.y_doff + j] = fm ? h_st[m] : 0.f;
+                    p.C[row * p.ldc + d * p.c_doff + j] = c_st[m];
+                }
+                if (p.y16) p.y16[row * p.ldy16 + (long)d * Hq + j] = __float2half_rn(fm ? h_st[m] : 0.f);
+                p.hist[(((long)d * (T + 1) + wslot) * B + bq0 + i) * Hq + j] = __float2half_rn(h_st[m]);
+            }
+        }
+    };
+    int t_prev = 0;
+    uint32_t frm_prev = 0, fmq_prev = 0;
     for (int s = 0; s < T; ++s) {
         const int t = dir > 0 ? s : T - 1 - s;
         const int b = s & 1;
         TRACE(0);
-        if (l == 0 && w < NISSUE) {
+        if (w < NISSUE) {  // warp-collective issue (one elected lane), operands warp-uniform
             if (s > 0) mbar_wait(&bars[2 + b], (fph >> b) & 1);  // the cluster's h_{s-1} landed in hbuf[b]
             TRACE(1);
             tc_fence_after();
             const uint32_t hb = hbuf_addr + b * HB;
             const int ks0 = w * (Hq / 16 / NISSUE), ks1 = ks0 + Hq / 16 / NISSUE;
-            if ((ks1 - ks0) % 4 == 0) {
-                for (int ks = ks0; ks < ks1; ks += 4)  // K step = 32N bytes of the B buffer = 2N desc units
-                    mma_f16_ts_x4(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * N, 16 * N, 128),
-                                  2 * N, idesc, ks != ks0);
-            } else {
-                for (int ks = ks0; ks < ks1; ++ks)
-                    mma_f16_ts(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * N, 16 * N, 128), idesc,
-                               ks != ks0);
-            }
-            mma_commit(&bars[1]);
+            for (int ks = ks0; ks < ks1; ++ks)  // K step = 32N bytes of the B buffer
+                mma_f16_ts_w(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * N, 16 * N, 128), idesc,
+                             ks != ks0);
+            mma_commit_w(&bars[1]);
             TRACE(2);
         }
         if (s > 0) fph ^= 1u << b;
-        // frame-valid bits of this warp's columns (lane i reads the mask of column i)
-        const uint32_t frm =
-            __ballot_sync(0xffffffffu, l < NQ && ((cm >> l) & 1) && p.mask[(long)t * B + bq0 + l]);
-        const int wslot = t + (dir > 0 ? 1 : 0);
+        if (s > 0) store_step(t_prev, frm_prev, fmq_prev);
+        // frame-valid bits of this warp's columns (lane i holds the prefetched mask of column i)
+        const uint32_t frm = __ballot_sync(0xffffffffu, mraw != 0);
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
         TRACE(3);
 
-        float act[NQ];
         {
             uint32_t v0[NQ], v1[NQ], v2[NQ], v3[NQ];
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + DCOL + nq0;
@@ -348,42 +382,13 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         }
         if (threadIdx.x == 0 && s > 0 && s + 2 < T) mbar_arrive_expect_tx(&bars[2 + b], NC * SG);  // full[b]: step s+2
         TRACE(5);
-        // off the critical path: history (for the dR GEMM), saved activations, c, y, y16
-        {
-            uint32_t hv[NQ / 2];
-#pragma unroll
-            for (int i = 0; i < NQ; i += 2) {
-                const float a0 = (((frm >> i) & 1) && unit_ok) ? act[i] : 0.f;
-                const float a1 = (((frm >> (i + 1)) & 1) && unit_ok) ? act[i + 1] : 0.f;
-                __half2 h2 = __floats2half2_rn(a0, a1);
-                hv[i / 2] = *reinterpret_cast<uint32_t *>(&h2);
-            }
-            __half *gp = p.gates + t * nat_step + nat_off;
-            if constexpr (NQ == 4) {
-                *reinterpret_cast<uint2 *>(gp) = make_uint2(hv[0], hv[1]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < NQ / 8; ++i)
-                    reinterpret_cast<uint4 *>(gp)[i] = make_uint4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
-            }
-        }
-#pragma unroll
-        for (int m = 0; m < NMQ; ++m) {
-            const int i = 4 * m + gam;
-            if (((cm >> i) & 1)) {
-                const bool fm = (fmq >> m) & 1;
-                const long row = (long)t * B + bq0 + i;
-                if (unit_ok) {
-                    if (p.y) p.y[row * p.ldy + d * p.y_doff + j] = fm ? h_st[m] : 0.f;
-                    p.C[row * p.ldc + d * p.c_doff + j] = c_st[m];
-                }
-                if (p.y16) p.y16[row * p.ldy16 + (long)d * Hq + j] = __float2half_rn(fm ? h_st[m] : 0.f);
-                p.hist[(((long)d * (T + 1) + wslot) * B + bq0 + i) * Hq + j] = __float2half_rn(h_st[m]);
-            }
-        }
+        t_prev = t;
+        frm_prev = frm;
+        fmq_prev = fmq;
         if (s + 1 < T) prefetch_z(dir > 0 ? t + 1 : t - 1);
         TRACE(6);
     }
+    if (T > 0) store_step(t_prev, frm_prev, fmq_prev);
 #pragma unroll
     for (int m = 0; m < NMQ; ++m) {
         const int i = 4 * m + gam, b = bq0 + i;
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const int g = grp % p.G;
     const int d = grp / p.G;
     const int dir = d == 0 ? p.dir0 : -1;
-    const int w = warp_id(), q = w & 3, cb = w >> 2, l = lane_id();
+    const int w = warp_uniform(warp_id()), q = w & 3, cb = w >> 2, l = lane_id();
     const int jl = 8 * q + (l >> 2), gam = l & 3;
     const int j = c * REC_UNITS + jl;
     const bool unit_ok = j < p.H;
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 
     // saved state of one step (independent of the recurrence: prefetched one step ahead)
     float graw[NQ], ct[NMQ], cp[NMQ], dyv[NMQ];
-    uint32_t frm = 0;
+    uint32_t mraw = 0;  // mask byte of column l (lane l < NQ) of the prefetched step
     auto load_step = [&](int t) {
         const __half *gp = p.gates + t * nat_step + nat_off;
         uint32_t hv[NQ / 2];
@@ -577,7 +582,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             else cp[m] = (ok && p.c0) ? p.c0[(long)d * B * H + (long)b * H + j] : 0.f;
             dyv[m] = ok ? p.dy[row * p.lddy + d * p.dy_doff + j] : 0.f;
         }
-        frm = __ballot_sync(0xffffffffu, l < NQ && ((cm >> l) & 1) && p.mask[(long)t * B + bq0 + l]);
+        mraw = (l < NQ && ((cm >> l) & 1)) ? p.mask[(long)t * B + bq0 + l] : 0;  // ballot at use
     };
     if (T > 0) load_step(dir > 0 ? T - 1 : 0);
 
@@ -596,6 +601,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         if (k_done > 0) gather(k_done);
         TRACE(2);
         // ---- gate gradients ----
+        const uint32_t frm = __ballot_sync(0xffffffffu, mraw != 0);
         pfm = 0;
         uint2 pks[NMQ];
 #pragma unroll
@@ -631,13 +637,13 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         tc_fence_before();
         __syncthreads();
         TRACE(3);
-        if (l == 0 && w < MT) {
+        if (w < MT) {  // warp-collective issue of M tile w (one elected lane), operands warp-uniform
             tc_fence_after();
 #pragma unroll
-            for (int kb = 0; kb < 2; ++kb)  // 64 gate columns per SW128 block, K step = 32 B = 2 desc units
-                mma_f16_ts_x4(tmem + DCOL + w * N, tmem + w * 64 + kb * 32, sdesc_sw128(das_addr + kb * N * 128, 16, 1024),
-                              2, idesc, kb != 0);
-            mma_commit(&bars[1]);
+            for (int kk = 0; kk < 8; ++kk)  // 64 gate columns per SW128 block, K step = 32 B
+                mma_f16_ts_w(tmem + DCOL + w * N, tmem + w * 64 + kk * 8,
+                             sdesc_sw128(das_addr + (kk >> 2) * N * 128 + (kk & 3) * 32, 16, 1024), idesc, kk != 0);
+            mma_commit_w(&bars[1]);
         }
         // while the MMA runs: dA of this step to global memory for the weight / input GEMMs
 #pragma unroll
@@ -654,13 +660,22 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         // (fp16) per owner, then warp w bulk-copies the block of owner w into w's slot for source c
         {
             const int kb = k_done & 1;
-            for (int mt = 0; mt < MT; ++mt) {
-                float v[NQ];
-                tmem_ld<NQ>(tmem + ((uint32_t)(32 * q) << 16) + DCOL + mt * N + nq0, v);
+            constexpr int MTMAX = 4;  // Hq <= 512
+            uint32_t v[MTMAX][NQ];
+#pragma unroll
+            for (int mt = 0; mt < MTMAX; ++mt)
+                if (mt < MT) tmem_ld_nowait<NQ>(tmem + ((uint32_t)(32 * q) << 16) + DCOL + mt * N + nq0, v[mt]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int mt = 0; mt < MTMAX; ++mt) pin_regs<NQ>(v[mt]);
+#pragma unroll
+            for (int mt = 0; mt < MTMAX; ++mt) {
+                if (mt >= MT) break;
                 uint32_t hv[NQ / 2];
 #pragma unroll
                 for (int i = 0; i < NQ; i += 2) {
-                    __half2 h2 = __floats2half2_rn(v[i] * P_SCALE, v[i + 1] * P_SCALE);
+                    __half2 h2 = __floats2half2_rn(__uint_as_float(v[mt][i]) * P_SCALE,
+                                                   __uint_as_float(v[mt][i + 1]) * P_SCALE);
                     hv[i / 2] = *reinterpret_cast<uint32_t *>(&h2);
                 }
                 __half *dst = stgp + (((size_t)kb * NC + 4 * mt + q) * 32 + l) * PITCH + nq0;
@@ -674,10 +689,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             }
             tc_fence_before();
             fence_async_smem();
+            TRACE(6);
             // the previous step's bulk copies (other staging buffer) are done reading; this
             // __syncthreads orders that before the rewrite of that buffer at the next step
             if (l == 0 && w < NC) bulk_wait_read<0>();
             __syncthreads();
+            TRACE(7);
             if (l == 0 && w < NC) {
                 bulk_s2c(mapa_shared(slots_addr + kb * SLOTB + c * BLK, w),
                          smem_u32(stgp) + ((uint32_t)kb * NC + w) * BLK, BLK, mapa_shared(full_addr + 8 * kb, w));

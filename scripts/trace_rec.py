@@ -48,6 +48,8 @@ def main():
     for k, name in enumerate(BWD):
         d = bb[:, k + 1] - bb[:, k]
         print(f"  {name:16s} {np.median(d[1:]):8.0f} ns")
+    print("  backward send split: staging", np.median((bb[:, 6] - bb[:, 4])[1:]),
+          "sync", np.median((bb[:, 7] - bb[:, 6])[1:]), "copies+loads", np.median((bb[:, 5] - bb[:, 7])[1:]))
 
 
 if __name__ == "__main__":
