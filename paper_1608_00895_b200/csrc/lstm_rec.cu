@@ -161,9 +161,11 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const int bq0 = b0 + nq0;       // its first batch row
     constexpr uint32_t TCOLS = 512;
     // TMEM: columns [0, Hq/2) hold the CTA's R^T slice (A operand, 128 lanes = gate rows, two
-    // fp16 of K per 32-bit column); from column Hq/2, four K-split accumulators D_w[128 x N]
-    // (the tiny N=16..64 MMAs are issue-bound, so warps 0..3 issue a quarter of K each).
+    // fp16 of K per 32-bit column); from column Hq/2, NISSUE K-split accumulators D_w[128 x N]
+    // (warps 0..NISSUE-1 each issue a 1/NISSUE share of K).
     const uint32_t DCOL = Hq / 2;
+    // four issuing warps: even with warp-collective uniform-register issue one warp sustains only
+    // ~1 MMA per ~45 cycles (measured: 32 MMAs 0.77 us from one warp vs 0.26 us from four)
     constexpr int NISSUE = 4;
 
     if (threadIdx.x == 0) {
@@ -333,21 +335,20 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         TRACE(3);
 
         {
-            uint32_t v0[NQ], v1[NQ], v2[NQ], v3[NQ];
+            uint32_t v[NISSUE][NQ];
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + DCOL + nq0;
-            tmem_ld_nowait<NQ>(ta, v0);
-            tmem_ld_nowait<NQ>(ta + N, v1);
-            tmem_ld_nowait<NQ>(ta + 2 * N, v2);
-            tmem_ld_nowait<NQ>(ta + 3 * N, v3);
-            tmem_ld_wait();
-            pin_regs<NQ>(v0);
-            pin_regs<NQ>(v1);
-            pin_regs<NQ>(v2);
-            pin_regs<NQ>(v3);
 #pragma unroll
-            for (int i = 0; i < NQ; ++i)
-                act[i] = gate_act(((__uint_as_float(v0[i]) + __uint_as_float(v1[i])) +
-                                   (__uint_as_float(v2[i]) + __uint_as_float(v3[i]))) + zv[i], gam);
+            for (int k4 = 0; k4 < NISSUE; ++k4) tmem_ld_nowait<NQ>(ta + k4 * N, v[k4]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k4 = 0; k4 < NISSUE; ++k4) pin_regs<NQ>(v[k4]);
+#pragma unroll
+            for (int i = 0; i < NQ; ++i) {
+                float pre = __uint_as_float(v[0][i]);
+#pragma unroll
+                for (int k4 = 1; k4 < NISSUE; ++k4) pre += __uint_as_float(v[k4][i]);
+                act[i] = gate_act(pre + zv[i], gam);
+            }
         }
         tc_fence_before();
         uint32_t fmq = 0;  // bit m: owned column 4m+gam is a valid frame
