@@ -201,9 +201,9 @@ int blstm_profile_enable(int on);
 /* cat: 0 forward recurrence, 1 BPTT recurrence, 2 GEMM.  Synchronizes the
  * recorded events; returns the summed device time (ms) and launch count. */
 int blstm_profile_read(int cat, double *total_ms, long *launches);
-/* Debug: record per-step phase timestamps (globaltimer ns, 8 per step, CTA 0 / thread 0)
- * of the following forward / BPTT recurrence launches into DEVICE buffers of 8*T
- * uint64 each; NULL disables. */
+/* Debug: record per-step phase timestamps (SM clock64 cycles, 16 slots per step, CTA 0 /
+ * thread 0) of the following forward / BPTT recurrence launches into DEVICE buffers of
+ * 16*T uint64 each; NULL disables.  Only a library built with -DBLSTM_TRACE writes them. */
 int blstm_debug_set_trace(void *fwd, void *bwd);
 
 #ifdef __cplusplus

@@ -237,5 +237,5 @@ def blstm_gemm_f16(A, a_mn: int, B, b_mn: int, C, M: int, N: int, K: int, alpha:
 
 
 def blstm_debug_set_trace(fwd=None, bwd=None):
-    """Debug: per-step phase timestamps of the next recurrence launches (uint64 [T, 8] tensors)."""
+    """Debug: per-step phase timestamps of the next recurrence launches (uint64 [T, 16] tensors)."""
     _check("blstm_debug_set_trace", lib().blstm_debug_set_trace(_p(fwd), _p(bwd)))

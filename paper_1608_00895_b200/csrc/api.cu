@@ -483,9 +483,11 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     const bool overlap = side != st;
     const int rec_ctas = 2 * g.pl.G * g.pl.NC;
     const int side_ctas = overlap ? (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8) : 0;
+    // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
+    // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused)
     static thread_local std::vector<cudaEvent_t> evs;
-    if (overlap && evs.size() < (size_t)g.L + 2) {
-        while (evs.size() < (size_t)g.L + 2) {
+    if (overlap && evs.size() < 2 * (size_t)g.L + 2) {
+        while (evs.size() < 2 * (size_t)g.L + 2) {
             cudaEvent_t e;
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "event");
             evs.push_back(e);
@@ -502,6 +504,8 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         float *dWT = (float *)(ws + w.dWT) + (size_t)par * 8 * Hq * w.maxDn;
         float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
         float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
+        // layer l+2 used the same parity buffers: its side-stream GEMMs must be done reading them
+        if (overlap && l + 2 < g.L) cudaStreamWaitEvent(st, evs[g.L + 2 + l + 2], 0);
         RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
         p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq;
         p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
@@ -535,6 +539,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, side), "scatter dR");
             TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.pl.G, dd, side), "scatter db");
         }
+        if (overlap) cudaEventRecord(evs[g.L + 2 + l], side);
         cur = 1 - cur;
     }
     if (overlap) {  // s_main's view: all gradient work of this call is complete

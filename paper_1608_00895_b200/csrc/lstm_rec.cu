@@ -27,7 +27,9 @@ namespace blstm {
 
 constexpr int REC_THREADS = 512;
 
-static DEVI uint8_t *align1024(uint8_t *p) { return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023); }
+// pointer arithmetic on the shared array (not an integer round trip) keeps the shared address
+// space visible to the compiler, so accesses through the result compile to LDS/STS
+static DEVI uint8_t *align1024(uint8_t *p) { return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u); }
 
 // 32 lanes x NC columns of TMEM -> registers (thread i: lane base+i)
 template <int NC>
@@ -83,20 +85,25 @@ DEVI void pin_regs(uint32_t (&r)[NC]) {
 }
 
 // 4x4 transpose inside each group of 4 lanes: lane gam holds a[k] = gate gam at batch column
-// 4m+k; afterwards b[k] = gate k at batch column 4m+gam.
-DEVI float sel4(const float (&a)[4], int i) { return i == 0 ? a[0] : i == 1 ? a[1] : i == 2 ? a[2] : a[3]; }
+// 4m+k; afterwards b[k] = gate k at batch column 4m+gam.  Two butterfly stages (lane bit 0 /
+// element bit 0, then lane bit 1 / element bit 1), selects only: a lane-dependent array index
+// would compile to divergent branch trees.
+DEVI float sel4(const float (&a)[4], int i) {
+    const float lo = (i & 1) ? a[1] : a[0], hi = (i & 1) ? a[3] : a[2];
+    return (i & 2) ? hi : lo;
+}
 DEVI void xpose4(const float (&a)[4], float (&b)[4], int gam) {
-    b[0] = b[1] = b[2] = b[3] = 0.f;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int k = gam ^ r;
-        const float send = sel4(a, k);
-        const float recv = r == 0 ? send : __shfl_xor_sync(0xffffffffu, send, r);
-        if (k == 0) b[0] = recv;
-        if (k == 1) b[1] = recv;
-        if (k == 2) b[2] = recv;
-        if (k == 3) b[3] = recv;
-    }
+    const bool o1 = gam & 1, o2 = gam & 2;
+    float v0 = a[0], v1 = a[1], v2 = a[2], v3 = a[3];
+    float s0 = __shfl_xor_sync(0xffffffffu, o1 ? v0 : v1, 1);
+    float s1 = __shfl_xor_sync(0xffffffffu, o1 ? v2 : v3, 1);
+    v0 = o1 ? s0 : v0; v1 = o1 ? v1 : s0;
+    v2 = o1 ? s1 : v2; v3 = o1 ? v3 : s1;
+    s0 = __shfl_xor_sync(0xffffffffu, o2 ? v0 : v2, 2);
+    s1 = __shfl_xor_sync(0xffffffffu, o2 ? v1 : v3, 2);
+    v0 = o2 ? s0 : v0; v2 = o2 ? v2 : s0;
+    v1 = o2 ? s1 : v1; v3 = o2 ? v3 : s1;
+    b[0] = v0; b[1] = v1; b[2] = v2; b[3] = v3;
 }
 
 // Gate nonlinearities in fp32 with the hardware exp2 (relative error ~1e-7, far inside the
@@ -112,7 +119,7 @@ DEVI float gate_act(float pre, int gam) {
 
 #ifdef BLSTM_TRACE
 #define TRACE(k) \
-    if (trace) trace[(size_t)s * 8 + (k)] = globaltimer_ns()
+    if (trace) trace[(size_t)s * 16 + (k)] = (unsigned long long)clock64()
 #else
 #define TRACE(k)
 #endif
@@ -342,6 +349,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             tmem_ld_wait();
 #pragma unroll
             for (int k4 = 0; k4 < NISSUE; ++k4) pin_regs<NQ>(v[k4]);
+            TRACE(8);
 #pragma unroll
             for (int i = 0; i < NQ; ++i) {
                 float pre = __uint_as_float(v[0][i]);
@@ -350,6 +358,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
                 act[i] = gate_act(pre + zv[i], gam);
             }
         }
+        TRACE(9);
         tc_fence_before();
         uint32_t fmq = 0;  // bit m: owned column 4m+gam is a valid frame
         uint8_t *sg = stg + b * SG;
@@ -360,16 +369,19 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             xpose4(a4, gv, gam);  // gv = (i, f, g, o) of unit j at column 4m + gam
             const int i = 4 * m + gam;
             const bool fm = ((frm >> i) & 1) && unit_ok;
-            if (fm) {
-                const float cn = gv[1] * c_st[m] + gv[0] * gv[2];
-                c_st[m] = cn;
-                h_st[m] = gv[3] * tanh_f(cn);
-                fmq |= 1u << m;
-            }
+            // computed for every lane, kept by select (no divergent branch; padded columns may
+            // hold garbage, which the select discards)
+            const float cn = gv[1] * c_st[m] + gv[0] * gv[2];
+            const float hn = gv[3] * tanh_f(cn);
+            c_st[m] = fm ? cn : c_st[m];
+            h_st[m] = fm ? hn : h_st[m];
+            fmq |= (uint32_t)fm << m;
             // staged slice in the B-operand block format: unit jl -> k chunk q, byte (jl%8)*2
             *reinterpret_cast<__half *>(sg + (q * N + nq0 + i) * 16 + (jl & 7) * 2) = __float2half_rn(h_st[m]);
         }
+        TRACE(10);
         fence_async_smem();
+        TRACE(7);
         // the previous step's bulk copies (of the other staging buffer) have long finished reading;
         // this __syncthreads orders that before the rewrite of that buffer at the next step
         if (l == 0 && w < NC) bulk_wait_read<0>();
@@ -604,6 +616,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         // ---- gate gradients ----
         const uint32_t frm = __ballot_sync(0xffffffffu, mraw != 0);
         pfm = 0;
+        TRACE(8);
         uint2 pks[NMQ];
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
@@ -612,20 +625,18 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             xpose4(a4, gv, gam);
             const int i = 4 * m + gam, n = nq0 + i;
             const bool fm = ((frm >> i) & 1) && unit_ok;
-            float da0 = 0.f, da1 = 0.f, da2 = 0.f, da3 = 0.f;
-            if (fm) {
-                const float ig = gv[0], f = gv[1], gg = gv[2], o = gv[3];
-                const float th = tanh_f(ct[m]);
-                const float dH = dh[m] + dyv[m];
-                const float dC = dc[m] + dH * o * (1.f - th * th);
-                da0 = dC * gg * ig * (1.f - ig);
-                da1 = dC * cp[m] * f * (1.f - f);
-                da2 = dC * ig * (1.f - gg * gg);
-                da3 = dH * th * o * (1.f - o);
-                dc[m] = dC * f;
-                dbp[0] += da0; dbp[1] += da1; dbp[2] += da2; dbp[3] += da3;
-                pfm |= 1u << m;
-            }
+            // computed for every lane, kept by select (no divergent branch)
+            const float ig = gv[0], f = gv[1], gg = gv[2], o = gv[3];
+            const float th = tanh_f(ct[m]);
+            const float dH = dh[m] + dyv[m];
+            const float dC = dc[m] + dH * o * (1.f - th * th);
+            const float da0 = fm ? dC * gg * ig * (1.f - ig) : 0.f;
+            const float da1 = fm ? dC * cp[m] * f * (1.f - f) : 0.f;
+            const float da2 = fm ? dC * ig * (1.f - gg * gg) : 0.f;
+            const float da3 = fm ? dH * th * o * (1.f - o) : 0.f;
+            dc[m] = fm ? dC * f : dc[m];
+            dbp[0] += da0; dbp[1] += da1; dbp[2] += da2; dbp[3] += da3;
+            pfm |= (uint32_t)fm << m;
             __half2 lo = __floats2half2_rn(da0 * scale, da1 * scale);
             __half2 hi = __floats2half2_rn(da2 * scale, da3 * scale);
             uint2 pk;
@@ -634,6 +645,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             *reinterpret_cast<uint2 *>(dAs + sw128_offset(n, 4 * jl, N)) = pk;
             pks[m] = pk;
         }
+        TRACE(9);
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
@@ -653,6 +665,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             if ((cm >> i) & 1)
                 *reinterpret_cast<uint2 *>(p.dA + ((long)t * B + bq0 + i) * p.ldda + (long)d * 4 * Hq + 4 * j) = pks[m];
         }
+        TRACE(10);
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
@@ -669,6 +682,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             tmem_ld_wait();
 #pragma unroll
             for (int mt = 0; mt < MTMAX; ++mt) pin_regs<NQ>(v[mt]);
+            TRACE(11);
 #pragma unroll
             for (int mt = 0; mt < MTMAX; ++mt) {
                 if (mt >= MT) break;

@@ -1,7 +1,10 @@
 """Per-step phase timing of the persistent recurrence kernels (debug trace hook).
 
-Runs training steps of a config (default C3) with the library's trace hook on and
-prints the median duration of each phase of one time step (CTA 0, thread 0).
+Runs training steps of a config (default C3) with the library's trace hook on (library built
+with `python paper_1608_00895_b200/csrc/build.py --trace --force`) and prints the median
+duration of each phase of one time step of CTA 0 / thread 0, from the SM cycle counter
+(clock64), converted to ns at the SM clock given by --mhz.  Trace slot k of step s is written
+at the point marked TRACE(k) in lstm_rec.cu.
 """
 import argparse
 import os
@@ -16,40 +19,47 @@ import torch  # noqa: E402
 from paper_1608_00895_b200 import blstm, synth  # noqa: E402
 from paper_1608_00895_b200.train import StackTrainer  # noqa: E402
 
-FWD = ["wait h (DSMEM)", "MMA issue", "MMA wait", "epilogue+sync", "send h", "stores+prefetch"]
-BWD = ["loads", "wait P + gather", "dA+smem+sync", "MMA (+dA stores)", "send P"]
+SLOTS = 16
+# (slot sequence in program order, label of the phase ending at that slot)
+FWD = [(0, None), (1, "wait h (DSMEM full)"), (2, "MMA issue"), (3, "stores + MMA wait"),
+       (8, "TMEM ld"), (9, "gate activations"), (10, "cell update + staging"), (7, "proxy fence"),
+       (4, "bulk_wait + __syncthreads"), (5, "send h + arm"), (6, "Z prefetch")]
+BWD = [(0, None), (2, "wait P + gather"), (8, "ballot"), (9, "dA math + smem"),
+       (3, "fences + __syncthreads"), (10, "MMA issue + dA stores"), (4, "MMA wait"),
+       (11, "TMEM ld"), (6, "P staging"), (7, "bulk_wait + __syncthreads"), (5, "send P + loads")]
+
+
+def report(name, tr, seq):
+    step = np.diff(tr[:, 0])
+    print(f"{name}: median step {np.median(step):.0f} ns")
+    for (a, _), (b, label) in zip(seq[:-1], seq[1:]):
+        d = tr[1:, b] - tr[1:, a]
+        print(f"  {label:28s} {np.median(d):8.0f} ns")
+    last = seq[-1][0]
+    d = tr[1:, 0] - tr[:-1, last]
+    print(f"  {'(to next step)':28s} {np.median(d):8.0f} ns")
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--mhz", type=float, default=1965.0)
     args = ap.parse_args()
     cfg, params, batch = synth.make_workload(synth.CONFIGS[args.config])
     dev = torch.device("cuda:0")
     tr = StackTrainer(cfg, params, batch, dev)
     tr.step()
-    tf = torch.zeros((cfg.T, 8), dtype=torch.int64, device=dev)
-    tb = torch.zeros((cfg.T, 8), dtype=torch.int64, device=dev)
+    tf = torch.zeros((cfg.T, SLOTS), dtype=torch.int64, device=dev)
+    tb = torch.zeros((cfg.T, SLOTS), dtype=torch.int64, device=dev)
     blstm.blstm_debug_set_trace(tf, tb)
     tr.step()
     torch.cuda.synchronize()
     blstm.blstm_debug_set_trace(None, None)
-    f = tf.cpu().numpy().astype(np.float64)
-    b = tb.cpu().numpy().astype(np.float64)
-    step_f = np.diff(f[:, 0])
-    print(f"forward: median step {np.median(step_f):.0f} ns")
-    for k, name in enumerate(FWD):
-        d = f[:, k + 1] - f[:, k]
-        print(f"  {name:16s} {np.median(d[1:]):8.0f} ns")
+    f = tf.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
+    b = tb.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
+    report("forward", f, FWD)
     # backward rows are indexed by s descending; use processing order
-    bb = b[::-1]
-    step_b = np.diff(bb[:, 0])
-    print(f"backward: median step {np.median(step_b):.0f} ns")
-    for k, name in enumerate(BWD):
-        d = bb[:, k + 1] - bb[:, k]
-        print(f"  {name:16s} {np.median(d[1:]):8.0f} ns")
-    print("  backward send split: staging", np.median((bb[:, 6] - bb[:, 4])[1:]),
-          "sync", np.median((bb[:, 7] - bb[:, 6])[1:]), "copies+loads", np.median((bb[:, 5] - bb[:, 7])[1:]))
+    report("backward", b[::-1], BWD)
 
 
 if __name__ == "__main__":
