@@ -65,10 +65,10 @@ struct LayerGeo {
     RecPlan pl;
 };
 struct FwdWS {
-    size_t x16, w16, rt16, bq, Z, cnt, total;
+    size_t x16, w16, rt16, bq, Z, maskN, cnt, total;
 };
 struct BwdWS {
-    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, cnt, total;
+    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cnt, total;
 };
 struct Reserve {
     size_t gates, hist, total;
@@ -99,6 +99,7 @@ static FwdWS fwd_ws(const LayerGeo &g) {
     w.rt16 = c.take((size_t)4 * g.Hq * g.Hq * 2);
     w.bq = c.take((size_t)4 * g.Hq * 4);
     w.Z = c.take(rec_native_elems(g.pl, g.T) * 4);
+    w.maskN = c.take(rec_mask_bytes(g.pl, g.T));
     w.cnt = c.take(256);
     w.total = c.off;
     return w;
@@ -115,6 +116,7 @@ static BwdWS bwd_ws(const LayerGeo &g) {
     w.dRT = c.take((size_t)4 * g.Hq * g.Hq * 4);
     w.dbp = c.take((size_t)g.pl.G * 4 * g.Hq * 4);
     w.P = c.take(rec_P_bytes(g.pl));
+    w.maskN = c.take(rec_mask_bytes(g.pl, g.T));
     w.cnt = c.take(256);
     w.total = c.off;
     return w;
@@ -181,7 +183,10 @@ extern "C" int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     TRY(gemm_f16({x16, g.Dp, 0}, {w16, 4L * g.Hq, 1}, gp, 0, st), "gemm Z");
     __half *hist = (__half *)(res + rv.hist);
     TRY(init_hist(hist, h0, g.T, g.B, g.H, g.Hq, 1, d->direction, st), "init_hist");
+    uint8_t *maskN = ws + w.maskN;
+    TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
     RecParams p = base_params(g, 1, d->direction, mask);
+    p.maskN = maskN;
     p.Z = Z; p.ldz = 4L * g.Hq;
     p.y = y; p.ldy = d->ldy; p.y_doff = 0;
     p.C = c; p.ldc = g.H; p.c_doff = 0;
@@ -223,7 +228,10 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     TRY(cast_x_f16(x, d->ldx, g.D, x16, g.Dp, g.TB, st), "cast_x");
     TRY(pack_w(W, nullptr, g.D, g.H, g.Hq, 1, g.Dp, 0, w16, st), "pack_w");
     TRY(pack_rt(R, nullptr, g.H, g.Hq, 1, rt16, st), "pack_rt");
+    uint8_t *maskN = ws + w.maskN;
+    TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
     RecParams p = base_params(g, 1, d->direction, mask);
+    p.maskN = maskN;
     p.C = const_cast<float *>(c); p.ldc = g.H; p.c_doff = 0;  // read-only in the backward kernel
     p.gates = (__half *)(res + rv.gates); p.ldg = 4L * g.Hq;
     p.c0 = c0;
@@ -266,7 +274,7 @@ struct StackGeo {
     std::vector<int> Dn, Drows, rowmode;
 };
 struct StackWS {
-    size_t x16, Z, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, total;
+    size_t x16, Z, maskN, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, total;
     size_t maxDn;
     std::vector<size_t> y16, w16, rt16, bq, gates, C, hist;
 };
@@ -312,6 +320,7 @@ static StackWS stack_ws(const StackGeo &g) {
     }
     const size_t zn = rec_native_elems(g.pl, g.T), zl = (size_t)TB * g.Kp;  // Z, or logits [TB, Kp]
     w.Z = c.take((zn > zl ? zn : zl) * 4);
+    w.maskN = c.take(rec_mask_bytes(g.pl, g.T));
     w.maxDn = maxDn;
     // dA / dWT / dRT / dbpart: two copies (layer parity) so layer l's weight gradients can run on a
     // side stream while BPTT of layer l-1 writes the other copy
@@ -388,6 +397,8 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         TRY(pack_bias(bf, bb, g.H, Hq, 2, (float *)(ws + w.bq[l]), st), "pack_bias");
     }
     float *Z = (float *)(ws + w.Z);
+    uint8_t *maskN = ws + w.maskN;  // shared by every layer, forward and BPTT
+    TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
     for (int l = 0; l < g.L; ++l) {
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
         const long lda = l == 0 ? g.Dp0 : 2L * Hq;
@@ -397,6 +408,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         __half *hist = (__half *)(ws + w.hist[l]);
         TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
         RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
+        p.maskN = maskN;
         p.Z = Z; p.ldz = 8L * Hq;
         if (Yout) { p.y = Yout + (size_t)l * g.TB * 2 * g.H; p.ldy = 2L * g.H; p.y_doff = g.H; }
         p.y16 = (__half *)(ws + w.y16[l]); p.ldy16 = 2L * Hq;
@@ -507,6 +519,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         // layer l+2 used the same parity buffers: its side-stream GEMMs must be done reading them
         if (overlap && l + 2 < g.L) cudaStreamWaitEvent(st, evs[g.L + 2 + l + 2], 0);
         RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
+        p.maskN = (const uint8_t *)(ws + w.maskN);  // packed by stack_forward
         p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq;
         p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
         p.dy = dY[cur]; p.lddy = 2L * Hq; p.dy_doff = Hq;

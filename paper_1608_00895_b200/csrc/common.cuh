@@ -94,6 +94,39 @@ DEVI void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes, uint3
         "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
         : "memory");
 }
+// bulk copy global -> this CTA's smem (16-byte aligned, size % 16 == 0), completing tx bytes on bar
+DEVI void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// per-thread asynchronous copies global -> own smem through the LSU (not the bulk-copy engine);
+// completion is per thread (cp.async.commit_group / wait_group), no register scoreboard involved
+DEVI void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+DEVI void cp_async8(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+DEVI void cp_async4(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+// 4-byte copy reading src_bytes (0 or 4) bytes; the rest of the destination is zero-filled
+DEVI void cp_async4_zfill(uint32_t dst, const void *src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+template <int BYTES>
+DEVI void cp_async(uint32_t dst, const void *src) {
+    static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16, "cp.async size");
+    if constexpr (BYTES == 16) cp_async16(dst, src);
+    else if constexpr (BYTES == 8) cp_async8(dst, src);
+    else cp_async4(dst, src);
+}
+DEVI void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+DEVI void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 DEVI void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 DEVI void bulk_wait_read() {

@@ -450,7 +450,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     __half *slots = reinterpret_cast<__half *>(smem);  // aliases Rs after the TMEM load
     __half *stgp = slots + 2 * (size_t)NC * 32 * PITCH;
     uint8_t *dAs = smem + bwd_region0(Hq, N, NC);      // [2][N][128 B] K-major SW128
-    uint64_t *bars = (uint64_t *)(dAs + 2 * N * 128);   // [0] tma, [1] mma, [2..3] slots full[b]
+    // per-step inputs, ring of 2 (bwd_in_bytes): each thread cp.async's exactly the values it reads
+    // (gates [512 thr][NQ] fp16, then c_t, c_{t-dir}, dy as [NMQ][512 thr] fp32, then [16 warps][16] mask
+    // bytes), one step ahead, so no global load latency sits on the recurrence's critical path
+    constexpr uint32_t IN_G = 512 * NQ * 2, IN_F = NMQ * 512 * 4, IN_SLOT = IN_G + 3 * IN_F + 256;
+    uint8_t *inr = dAs + 2 * N * 128;
+    uint64_t *bars = (uint64_t *)(inr + 2 * IN_SLOT);   // [0] tma, [1] mma, [2..3] slots full[b]
     uint32_t *tslot = (uint32_t *)(bars + 4);
 
     const int c = (int)cluster_ctarank();
@@ -562,27 +567,17 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const long nat_step = (long)p.ndir * p.G * NC * 512 * NQ;
     const long nat_off = (((long)d * p.G + g) * NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
 
-    // saved state of one step (independent of the recurrence: prefetched one step ahead)
-    float graw[NQ], ct[NMQ], cp[NMQ], dyv[NMQ];
-    uint32_t mraw = 0;  // mask byte of column l (lane l < NQ) of the prefetched step
-    auto load_step = [&](int t) {
-        const __half *gp = p.gates + t * nat_step + nat_off;
-        uint32_t hv[NQ / 2];
-        if constexpr (NQ == 4) {
-            const uint2 u = *reinterpret_cast<const uint2 *>(gp);
-            hv[0] = u.x; hv[1] = u.y;
+    // saved state of one step (independent of the recurrence): cp.async'd one step ahead into ring
+    // slot sl, read back by the same thread (the mask bytes by its warp)
+    const int tid = threadIdx.x;
+    const uint32_t in_addr = smem_u32(inr);
+    auto load_step = [&](int t, int sl) {
+        const uint32_t base = in_addr + sl * IN_SLOT;
+        if constexpr (NQ * 2 <= 16) {
+            cp_async<NQ * 2>(base + tid * NQ * 2, p.gates + t * nat_step + nat_off);
         } else {
 #pragma unroll
-            for (int i = 0; i < NQ / 8; ++i) {
-                const uint4 u = reinterpret_cast<const uint4 *>(gp)[i];
-                hv[4 * i] = u.x; hv[4 * i + 1] = u.y; hv[4 * i + 2] = u.z; hv[4 * i + 3] = u.w;
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < NQ; i += 2) {
-            const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&hv[i / 2]));
-            graw[i] = f2.x;
-            graw[i + 1] = f2.y;
+            for (int i = 0; i < NQ / 8; ++i) cp_async16(base + tid * NQ * 2 + 16 * i, p.gates + t * nat_step + nat_off + 8 * i);
         }
         const int tp = t - dir;
 #pragma unroll
@@ -590,14 +585,21 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             const int i = 4 * m + gam, b = bq0 + i;
             const bool ok = ((cm >> i) & 1) && unit_ok;
             const long row = (long)t * B + b;
-            ct[m] = ok ? p.C[row * p.ldc + d * p.c_doff + j] : 0.f;
-            if (ok && tp >= 0 && tp < T) cp[m] = p.C[((long)tp * B + b) * p.ldc + d * p.c_doff + j];
-            else cp[m] = (ok && p.c0) ? p.c0[(long)d * B * H + (long)b * H + j] : 0.f;
-            dyv[m] = ok ? p.dy[row * p.lddy + d * p.dy_doff + j] : 0.f;
+            const uint32_t o = (uint32_t)(m * 512 + tid) * 4;
+            cp_async4_zfill(base + IN_G + o, ok ? p.C + row * p.ldc + d * p.c_doff + j : p.C, ok ? 4 : 0);
+            if (tp >= 0 && tp < T)
+                cp_async4_zfill(base + IN_G + IN_F + o, ok ? p.C + ((long)tp * B + b) * p.ldc + d * p.c_doff + j : p.C,
+                                ok ? 4 : 0);
+            else
+                cp_async4_zfill(base + IN_G + IN_F + o, (ok && p.c0) ? p.c0 + (long)d * B * H + (long)b * H + j : p.C,
+                                (ok && p.c0) ? 4 : 0);
+            cp_async4_zfill(base + IN_G + 2 * IN_F + o, ok ? p.dy + row * p.lddy + d * p.dy_doff + j : p.dy, ok ? 4 : 0);
         }
-        mraw = (l < NQ && ((cm >> l) & 1)) ? p.mask[(long)t * B + bq0 + l] : 0;  // ballot at use
+        if (l == 0) cp_async<NQ>(base + IN_G + 3 * IN_F + w * 16, p.maskN + ((long)t * p.G + g) * N + nq0);
+        cp_async_commit();
     };
-    if (T > 0) load_step(dir > 0 ? T - 1 : 0);
+    if (T > 0) load_step(dir > 0 ? T - 1 : 0, 0);
+    float graw[NQ], ct[NMQ], cp[NMQ], dyv[NMQ];
 
     uint32_t mma_phase = 0;
     const uint32_t das_addr = smem_u32(dAs);
@@ -613,6 +615,28 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         // ---- dh_t from the previous step's partials ----
         if (k_done > 0) gather(k_done);
         TRACE(2);
+        // ---- this step's saved state (landed during the gather) ----
+        cp_async_wait<0>();
+        __syncwarp();  // lane 0 copied the warp's mask bytes
+        uint32_t mraw;
+        {
+            const uint8_t *in = inr + (k_done & 1) * IN_SLOT;
+            const __half2 *gh = reinterpret_cast<const __half2 *>(in + tid * NQ * 2);
+#pragma unroll
+            for (int i = 0; i < NQ; i += 2) {
+                const float2 f2 = __half22float2(gh[i / 2]);
+                graw[i] = f2.x;
+                graw[i + 1] = f2.y;
+            }
+            const float *fin = reinterpret_cast<const float *>(in + IN_G);
+#pragma unroll
+            for (int m = 0; m < NMQ; ++m) {
+                ct[m] = fin[m * 512 + tid];
+                cp[m] = fin[NMQ * 512 + m * 512 + tid];
+                dyv[m] = fin[2 * NMQ * 512 + m * 512 + tid];
+            }
+            mraw = l < NQ ? in[IN_G + 3 * IN_F + w * 16 + l] : 0;
+        }
         // ---- gate gradients ----
         const uint32_t frm = __ballot_sync(0xffffffffu, mraw != 0);
         pfm = 0;
@@ -716,7 +740,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
                 bulk_commit();
             }
         }
-        if (s > 0) load_step(dir > 0 ? s - 1 : T - s);
+        if (s > 0) load_step(dir > 0 ? s - 1 : T - s, (k_done + 1) & 1);
         TRACE(5);
     }
 #undef TRACE
@@ -779,7 +803,11 @@ RecPlan rec_plan(int T, int B, int H, int ndir, int sms) {
 }
 
 static size_t fwd_smem(const RecPlan &pl) { return fwd_region0(pl.Hq, pl.N) + 1024 + 64; }
-static size_t bwd_smem(const RecPlan &pl) { return bwd_region0(pl.Hq, pl.N, pl.NC) + 2 * pl.N * 128 + 1024 + 64; }
+// per-step input ring of the BPTT kernel (2 slots; see IN_SLOT there)
+static size_t bwd_in_bytes(int N) { return 2 * ((size_t)512 * (N / 4) * 2 + 3 * (size_t)(N / 16) * 512 * 4 + 256); }
+static size_t bwd_smem(const RecPlan &pl) {
+    return bwd_region0(pl.Hq, pl.N, pl.NC) + 2 * pl.N * 128 + bwd_in_bytes(pl.N) + 1024 + 64;
+}
 
 bool rec_supported(const RecPlan &pl, int H) {
     if (H < 1 || (pl.N != 16 && pl.N != 32 && pl.N != 64)) return false;

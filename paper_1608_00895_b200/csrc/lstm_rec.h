@@ -22,6 +22,7 @@ struct RecParams {
     int T, B, H, Hq, NC, G, Bg, N, ndir;
     int dir0;                    // direction (+1/-1) of direction index 0; index 1 is always -1
     const uint8_t *mask;         // [T, B]
+    const uint8_t *maskN;        // [T][G][N] mask rows per batch group (pack_mask)
     // forward
     const float *Z;              // time-major transposed [T][ndir*4Hq][B] (gate row d*4Hq + 4j+gamma)
     long ldz;                    // unused (kept for ABI stability of the struct)
@@ -57,6 +58,7 @@ void rec_set_trace(unsigned long long *fwd, unsigned long long *bwd);
 //   ((((t*ndir + d)*G + g)*NC + c)*4 + cb)*128*NQ + r*NQ + i,   NQ = N/4,
 // for batch row b = g*Bg + cb*NQ + i and gate column d*4Hq + 128c + r.  Each thread of the
 // recurrence kernels reads/writes NQ contiguous values; each warp one contiguous block.
+inline size_t rec_mask_bytes(const RecPlan &pl, int T) { return (size_t)T * pl.G * pl.N; }
 inline size_t rec_native_elems(const RecPlan &pl, int T) {
     return (size_t)T * pl.ndir * 4 * pl.Hq * pl.G * pl.N;
 }

@@ -323,6 +323,24 @@ int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, 
 }
 
 // --- dy_top [rows, 2H] -> dY [rows, 2Hq] (padded halves) ------------------------------------
+__global__ void pack_mask_kernel(const uint8_t *__restrict__ mask, int T, int B, int G, int Bg, int N,
+                                 uint8_t *__restrict__ maskN) {
+    const long n = (long)T * G * N;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long tg = i / N;
+        const int c = (int)(i - tg * N), g = (int)(tg % G);
+        const long t = tg / G;
+        const int b = g * Bg + c;
+        maskN[i] = (c < Bg && b < B) ? mask[t * B + b] : 0;
+    }
+}
+int pack_mask(const uint8_t *mask, int T, int B, int G, int Bg, int N, uint8_t *maskN, cudaStream_t st) {
+    if (T == 0) return 0;
+    pack_mask_kernel<<<grid_for((long)T * G * N), 256, 0, st>>>(mask, T, B, G, Bg, N, maskN);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 __global__ void pad_halves_kernel(const float *__restrict__ src, int H, int Hq, long rows, float *__restrict__ dst) {
     const long n = rows * 2 * Hq;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {

@@ -28,6 +28,9 @@ int scatter_w(float *gW, int Drows, int H, int Hq, const float *dWT, long ldw, i
 int scatter_r(float *gR, int H, int Hq, const float *dRT, cudaStream_t st);
 int scatter_b(float *gb, int H, int Hq, const float *dbpart, int G, int d, cudaStream_t st);
 int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, cudaStream_t st);
+// recurrence kernels' mask rows: maskN[(t*G + g)*N + n] = mask[t*B + g*Bg + n] for n < Bg,
+// g*Bg + n < B, else 0 (one N-byte row per step and batch group, bulk-copyable)
+int pack_mask(const uint8_t *mask, int T, int B, int G, int Bg, int N, uint8_t *maskN, cudaStream_t st);
 int pad_halves(const float *src, int H, int Hq, long rows, float *dst, cudaStream_t st);
 int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, int accum, cudaStream_t st);
 int sgd(float *theta, float *grad, long n, float lr, int zero, cudaStream_t st);
