@@ -423,14 +423,24 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 // ---------------------------------------------------------------------------
 // backward through time
 // ---------------------------------------------------------------------------
-// smem: [region0: R^T slice (TMA, start only) | aliased later by the P slots] [dAs] [barriers]
-//   slots[b][src][32 rows][N + 8] fp16: partial dh (x 2^DA_SHIFT x P_SCALE) of this CTA's 32
-//   units from CTA src (row pitch padded by 16 B so the owner's gather is conflict-free)
+// smem: [region0: R^T slice (TMA, start only) | aliased later by the P slots] [dAs] [in ring] [barriers]
+//   slots[b][src][32 rows][N] fp16: partial dh (x 2^DA_SHIFT x P_SCALE) of this CTA's 32 units
+//   from CTA src, 16-byte chunks swizzled by row (pswz) so the owner's gather is conflict-free
 constexpr float P_SCALE = 1.f / 16.f;  // keeps the fp16 partials far from overflow
-//   stg[b][owner][32 rows][N + 8] fp16: this CTA's partial rows per owner, bulk-copied as one block
+//   stg[b][owner][32 rows][N] fp16: this CTA's partial rows per owner (same swizzle), bulk-copied
+//   as one block
 static __host__ __device__ size_t bwd_region0(int Hq, int N, int NC) {
-    const size_t rs = (size_t)Hq / 64 * 16384, sl = 4 * (size_t)NC * 32 * (N + 8) * 2;
+    const size_t rs = (size_t)Hq / 64 * 16384, sl = 4 * (size_t)NC * 32 * N * 2;
     return rs > sl ? rs : sl;
+}
+// byte offset of element (row r, column n) in a P block [32 rows][N] fp16: the 16-byte chunk index
+// is XORed with a row function, so the gather's warp access (8 rows x 4 adjacent columns) hits 8
+// distinct 4-bank groups
+template <int N>
+DEVI uint32_t pswz(int r, int n) {
+    constexpr int RB = 2 * N, CH = RB / 16, RPL = 128 / RB > 1 ? 128 / RB : 1;
+    const int f = (r / RPL) % CH;
+    return (uint32_t)(r * RB + ((((2 * n) >> 4) ^ f) << 4) + ((2 * n) & 15));
 }
 
 template <int NT>
@@ -439,16 +449,15 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     constexpr int N = 16 * NT;
     constexpr int NQ = N / 4;
     constexpr int NMQ = NQ / 4;
-    constexpr int PITCH = N + 8;  // halves per slot row
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     const int Hq = p.Hq, KB = Hq / 64, MT = Hq / 128, NC = p.NC;
-    const uint32_t SLOTB = (uint32_t)NC * 32 * PITCH * 2;  // bytes of one slot buffer
+    constexpr uint32_t BLK = 32 * N * 2;                   // one (owner, source) block
+    const uint32_t SLOTB = (uint32_t)NC * BLK;             // bytes of one slot buffer
     const uint32_t SLOT_TX = SLOTB;                        // bytes arriving per buffer (NC blocks)
-    const uint32_t BLK = 32 * PITCH * 2;                   // one (owner, source) block
     uint8_t *Rs = smem;
-    __half *slots = reinterpret_cast<__half *>(smem);  // aliases Rs after the TMEM load
-    __half *stgp = slots + 2 * (size_t)NC * 32 * PITCH;
+    uint8_t *slots = smem;             // [2][NC][BLK], aliases Rs after the TMEM load
+    uint8_t *stgp = smem + 2 * SLOTB;  // [2][NC][BLK]
     uint8_t *dAs = smem + bwd_region0(Hq, N, NC);      // [2][N][128 B] K-major SW128
     // per-step inputs, ring of 2 (bwd_in_bytes): each thread cp.async's exactly the values it reads
     // (gates [512 thr][NQ] fp16, then c_t, c_{t-dir}, dy as [NMQ][512 thr] fp32, then [16 warps][16] mask
@@ -554,12 +563,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         mbar_wait(&bars[2 + b], (fph >> b) & 1);
         fph ^= 1u << b;
         if (threadIdx.x == 0 && k + 2 <= T) mbar_arrive_expect_tx(&bars[2 + b], SLOT_TX);  // index k+2
-        const __half *sl = slots + (size_t)b * NC * 32 * PITCH + jl * PITCH + nq0;
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
             if ((pfm >> m) & 1) {
+                const uint8_t *sl = slots + b * SLOTB + pswz<N>(jl, nq0 + 4 * m + gam);
                 float acc = 0.f;
-                for (int src = 0; src < NC; ++src) acc += __half2float(sl[src * 32 * PITCH + 4 * m + gam]);
+                for (int src = 0; src < NC; ++src) acc += __half2float(*reinterpret_cast<const __half *>(sl + src * BLK));
                 dh[m] = acc * inv_scale;
             }
         }
@@ -717,13 +726,14 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
                                                    __uint_as_float(v[mt][i + 1]) * P_SCALE);
                     hv[i / 2] = *reinterpret_cast<uint32_t *>(&h2);
                 }
-                __half *dst = stgp + (((size_t)kb * NC + 4 * mt + q) * 32 + l) * PITCH + nq0;
+                uint8_t *blk = stgp + ((uint32_t)kb * NC + 4 * mt + q) * BLK;
                 if constexpr (NQ == 4) {
-                    *reinterpret_cast<uint2 *>(dst) = make_uint2(hv[0], hv[1]);
+                    *reinterpret_cast<uint2 *>(blk + pswz<N>(l, nq0)) = make_uint2(hv[0], hv[1]);
                 } else {
 #pragma unroll
                     for (int i = 0; i < NQ / 8; ++i)
-                        reinterpret_cast<uint4 *>(dst)[i] = make_uint4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
+                        *reinterpret_cast<uint4 *>(blk + pswz<N>(l, nq0 + 8 * i)) =
+                            make_uint4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
                 }
             }
             tc_fence_before();
