@@ -10,6 +10,7 @@
 #include "gemm.h"
 #include "lstm_rec.h"
 #include "ops.h"
+#include "prof.h"
 
 using namespace blstm;
 
@@ -274,7 +275,7 @@ struct StackGeo {
     std::vector<int> Dn, Drows, rowmode;
 };
 struct StackWS {
-    size_t x16, Z, maskN, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, total;
+    size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, total;
     size_t maxDn;
     std::vector<size_t> y16, w16, rt16, bq, gates, C, hist;
 };
@@ -301,6 +302,10 @@ static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
     }
     return 0;
 }
+// Z GEMM -> recurrence completion counters: [L][2 directions][M-tiles]
+static size_t zflag_words(const StackGeo &g) {
+    return (size_t)g.L * 2 * ((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS);
+}
 static StackWS stack_ws(const StackGeo &g) {
     Carve c;
     StackWS w;
@@ -321,6 +326,7 @@ static StackWS stack_ws(const StackGeo &g) {
     const size_t zn = rec_native_elems(g.pl, g.T), zl = (size_t)TB * g.Kp;  // Z, or logits [TB, Kp]
     w.Z = c.take((zn > zl ? zn : zl) * 4);
     w.maskN = c.take(rec_mask_bytes(g.pl, g.T));
+    w.zflags = c.take(zflag_words(g) * 4);
     w.maxDn = maxDn;
     // dA / dWT / dRT / dbpart: two copies (layer parity) so layer l's weight gradients can run on a
     // side stream while BPTT of layer l-1 writes the other copy
@@ -380,7 +386,7 @@ extern "C" size_t blstm_stack_workspace_bytes(const blstm_stack_desc *d) {
     return stack_ws(g).total;
 }
 
-// forward of the whole stack; Yout [L,T,B,2H] / Cout [L,2,T,B,H] optional (parity view)
+// forward of the whole stack; Yout [L,T,B,2H] / Cout [L,2,T,B,H] optional (parity view).
 static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const StackWS &w, uint8_t *ws,
                          const float *theta, const float *x, const uint8_t *mask, float *Yout, float *Cout,
                          cudaStream_t st) {
@@ -399,25 +405,49 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     float *Z = (float *)(ws + w.Z);
     uint8_t *maskN = ws + w.maskN;  // shared by every layer, forward and BPTT
     TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
+    const int num_m = (int)((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS);
+    uint32_t *zflags = (uint32_t *)(ws + w.zflags);
+    if (cudaMemsetAsync(zflags, 0, zflag_words(g) * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset zflags");
+    // Overlap: layer l's recurrence is launched first and, once all its CTAs are resident, triggers
+    // the Z GEMM as a programmatic dependent launch on the SMs its clusters leave free; the
+    // recurrence waits per M-tile on the GEMM's completion counters.  Only when every GEMM CTA can
+    // be co-resident with the clusters (one CTA per SM each): a GEMM CTA waiting for an SM would
+    // deadlock the spinning recurrence.  Otherwise the GEMM simply runs first.
+    const int side_ctas = num_sms() - 2 * g.pl.G * g.pl.NC;
+    const bool overlap = side_ctas >= 8;
+    if (overlap && gemm_prepare()) return fail(BLSTM_ERR_CUDA, "gemm_prepare");
     for (int l = 0; l < g.L; ++l) {
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
         const long lda = l == 0 ? g.Dp0 : 2L * Hq;
         GemmParams gp{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
         set_native(gp, g.pl, g.B);  // Z in the recurrence kernels' CTA-native layout
-        TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gp, 0, st), "gemm Z");
+        gp.flags = zflags + (size_t)l * 2 * num_m;
+        gp.flag_desc = 2;  // direction 1 (backward) reads time steps in descending order
+        gp.pdl = overlap;
+        if (!overlap) TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gp, 0, st), "gemm Z");
         __half *hist = (__half *)(ws + w.hist[l]);
         TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
         RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
         p.maskN = maskN;
         p.Z = Z; p.ldz = 8L * Hq;
+        p.zflags = gp.flags; p.zflag_target = 4 * Hq / gemm_bn(8 * Hq); p.zflag_nm = num_m;
         if (Yout) { p.y = Yout + (size_t)l * g.TB * 2 * g.H; p.ldy = 2L * g.H; p.y_doff = g.H; }
         p.y16 = (__half *)(ws + w.y16[l]); p.ldy16 = 2L * Hq;
         if (Cout) { p.C = Cout + (size_t)l * 2 * g.TB * g.H; p.ldc = g.H; p.c_doff = g.TB * g.H; }
         else { p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq; }
         p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
         p.hist = hist;
-        p.counters = (uint32_t *)(ws + w.cnt);
-        TRY(lstm_rec_fwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_fwd");
+        p.counters = (uint32_t *)(ws + w.cnt);        if (overlap) {  // the pair is timed as one forward-recurrence scope (prof_suspend)
+            ProfScope ps(PROF_REC_FWD, st);
+            prof_suspend(1);
+            const int rc1 = lstm_rec_fwd(p, (const __half *)(ws + w.rt16[l]), st);
+            const int rc2 = rc1 ? 0 : gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gp, side_ctas, st);
+            prof_suspend(0);
+            TRY(rc1, "lstm_rec_fwd");
+            TRY(rc2, "gemm Z");
+        } else {
+            TRY(lstm_rec_fwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_fwd");
+        }
     }
     return 0;
 }

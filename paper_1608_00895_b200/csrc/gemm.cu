@@ -38,6 +38,22 @@ struct GemmCfg {
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
+// tile index -> (M-tile, N-tile).  Default: M fastest (consecutive CTAs share the B tile).  With
+// completion flags: round r visits, per direction d, all N-tiles of that direction at M-tile r
+// (ascending) or num_m-1-r (descending), so Z becomes complete in the order the recurrence reads it.
+template <int BN>
+DEVI void tile_coords(int tile, int num_m, const GemmParams &p, int &mt, int &nt) {
+    if (!p.flags) {
+        mt = tile % num_m;
+        nt = tile / num_m;
+        return;
+    }
+    const int ntd = p.natHq4 / BN, per = p.natNdir * ntd;
+    const int r = tile / per, w = tile - r * per, d = w / ntd;
+    mt = ((p.flag_desc >> d) & 1) ? num_m - 1 - r : r;
+    nt = w;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_f16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -85,8 +101,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int m0 = (tile % num_m) * GEMM_BM;
-                const int n0 = (tile / num_m) * BN;
+                int mt, nt;
+                tile_coords<BN>(tile, num_m, p, mt, nt);
+                const int m0 = mt * GEMM_BM, n0 = nt * BN;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
@@ -153,8 +170,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int et = threadIdx.x - 64;                           // 0..255 over the epilogue warps
         const int chalf = (warp - 2) / 4;                          // column half of this warp
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int m0 = (tile % num_m) * GEMM_BM;
-            const int n0 = (tile / num_m) * BN;
+            int mt, nt;
+            tile_coords<BN>(tile, num_m, p, mt, nt);
+            const int m0 = mt * GEMM_BM, n0 = nt * BN;
             // this tile's bias slice -> shared memory while the MMAs run (a global load per
             // element in the store loop stalled the epilogue on L2 latency)
             for (int k = et; k < BN; k += 32 * GEMM_EPI_WARPS)
@@ -206,6 +224,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     }
                 }
             }
+            if (p.flags) {  // publish the tile to the concurrently running recurrence
+                asm volatile("bar.sync 2, %0;" ::"n"(32 * GEMM_EPI_WARPS) : "memory");
+                if (et == 0) {
+                    __threadfence();
+                    red_release_gpu_add(p.flags + (n0 / p.natHq4) * num_m + mt, 1);
+                }
+            }
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&tempty[acc]);
@@ -217,6 +242,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
     }
+    // programmatic dependent launch: complete only after the primary grid (the recurrence this GEMM
+    // feeds) has, so later work in the stream keeps plain stream order.  All tiles are published
+    // before this point, hence no cycle.
+    if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -267,23 +296,48 @@ int num_sms() {
 }
 
 template <int BN>
+static cudaError_t gemm_setup() {
+    static bool done = false;
+    if (!done) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_f16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             GemmCfg<BN>::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        cudaFuncAttributes a;
+        e = cudaFuncGetAttributes(&a, gemm_f16_kernel<BN>);  // forces the (lazy) module load
+        if (e != cudaSuccess) return e;
+        done = true;
+    }
+    return cudaSuccess;
+}
+int gemm_prepare() {
+    return (gemm_setup<128>() == cudaSuccess && gemm_setup<256>() == cudaSuccess) ? 0 : -5;
+}
+
+template <int BN>
 static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, const GemmParams &p, int max_ctas,
                                cudaStream_t st) {
     using Cfg = GemmCfg<BN>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_f16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg::SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    if (cudaError_t e = gemm_setup<BN>()) return e;
     const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
     int grid = tiles < max_ctas ? tiles : max_ctas;
     if (grid < 1) grid = 1;
     ProfScope ps(PROF_GEMM, st);
-    gemm_f16_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, p);
     note_launch();
-    return cudaGetLastError();
+    if (!p.pdl) {
+        gemm_f16_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, p);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_f16_kernel<BN>, ta, tb, p);
 }
 
 // C = alpha * op(A) op(B)^T (+C) (+bias).  Returns 0 / negative error.
@@ -293,7 +347,7 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
     p.b_mn = B.mn_major;
     if (p.M <= 0 || p.N <= 0) return 0;
     if (p.K <= 0) return -3;  // callers never ask for an empty contraction
-    const int BN = p.N > 128 ? 256 : 128;
+    const int BN = gemm_bn(p.N);
     CUtensorMap ta, tb;
     int rc;
     if (!A.mn_major) rc = make_tmap_f16(&ta, A.ptr, p.K, p.M, A.ld, GEMM_BM);

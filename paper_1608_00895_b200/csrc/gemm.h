@@ -21,9 +21,25 @@ struct GemmParams {
     int a_mn, b_mn;     // filled by gemm_f16
     // > 0: C is written in the recurrence kernels' CTA-native layout (lstm_rec.h, rec_native_index)
     int natB = 0, natBg = 0, natG = 0, natNQ = 0, natNC = 0, natHq4 = 0, natNdir = 0;
+    // != nullptr (CTA-native mode only): the Z GEMM feeds a recurrence running concurrently on other
+    // SMs.  Tiles are then visited M-tile by M-tile in each direction's time order (bit d of
+    // flag_desc: direction d consumes time steps in descending order) and, after a tile's stores,
+    // the epilogue adds 1 (release, gpu scope) to flags[d * ceil(M/128) + m_tile]; a (direction,
+    // M-tile) is complete when its counter reaches natHq4 / gemm_bn(N).
+    uint32_t *flags = nullptr;
+    int flag_desc = 0;
+    // launch as a programmatic dependent of the previous kernel in the stream (which triggers it
+    // once all its CTAs are resident: lstm_rec_fwd), so the GEMM runs beside it on the free SMs
+    int pdl = 0;
 };
 
+constexpr int GEMM_BM_ROWS = 128;           // M tile
+inline int gemm_bn(int N) { return N > 128 ? 256 : 128; }  // N tile chosen by gemm_f16
+
 int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &p, int max_ctas, cudaStream_t st);
+// load + configure the GEMM kernels now: with lazy module loading the first launch of a kernel
+// synchronizes the context, which must not happen while a recurrence waits on that GEMM (pdl)
+int gemm_prepare();
 int make_tmap_f16(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                   uint32_t box_outer);
 int num_sms();

@@ -153,6 +153,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     uint64_t *bars = (uint64_t *)(smem + fwd_region0(Hq, N));  // [0] tma, [1] mma, [2..3] full[b]
     uint32_t *tslot = (uint32_t *)(bars + 4);
 
+    // this CTA is resident: a programmatically dependent launch (the concurrent Z GEMM, gemm.h pdl)
+    // may start on the SMs left free once every CTA of this grid got here
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int c = (int)cluster_ctarank();
     const int grp = blockIdx.x / NC;  // cluster index = d*G + g
     const int g = grp % p.G;
@@ -242,6 +245,24 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         if (T > 1) mbar_arrive_expect_tx(&bars[3], NC * SG);  // h_0 from the cluster -> step 1
         if (T > 2) mbar_arrive_expect_tx(&bars[2], NC * SG);  // h_1 -> step 2
     }
+    // Z of step t2 may still be in flight from the concurrent Z GEMM (p.zflags): one thread (lane 0
+    // of the first non-issuing warp) verifies the M-tiles holding frames t2*B .. t2*B+B-1 in this
+    // direction's time order, advancing a frontier; the CTA barrier that follows publishes it to
+    // the threads that then load Z (acquire -> bar.sync -> ld.global.cg)
+    constexpr int ZPOLL = 32 * NISSUE;
+    const uint32_t *zf = p.zflags ? p.zflags + (size_t)d * p.zflag_nm : nullptr;
+    int zfront = dir > 0 ? 0 : p.zflag_nm - 1;  // next M-tile to verify (polling thread only)
+    auto z_tile_of = [&](int t2) {  // last M-tile (in time order) that step t2 needs
+        return dir > 0 ? (int)(((long)t2 * B + B - 1) / GEMM_BM_ROWS) : (int)(((long)t2 * B) / GEMM_BM_ROWS);
+    };
+    auto z_wait = [&](int t2) {
+        const int need = z_tile_of(t2);
+        while (dir > 0 ? zfront <= need : zfront >= need) {
+            spin_until_geq(zf + zfront, (uint32_t)p.zflag_target);
+            zfront += dir;
+        }
+    };
+    if (zf && threadIdx.x == ZPOLL && T > 0) z_wait(dir > 0 ? 0 : T - 1);
     cluster_sync();  // every CTA done with its R staging before peers write into hbuf / stg
 
     float c_st[NMQ], h_st[NMQ];
@@ -263,7 +284,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         const float4 *zp = reinterpret_cast<const float4 *>(p.Z + t * nat_step + nat_off);
 #pragma unroll
         for (int i = 0; i < NQ / 4; ++i) {
-            const float4 v = __ldg(zp + i);
+            const float4 v = __ldcg(zp + i);  // L2-coherent: Z may have been written during this kernel
             zv[4 * i] = v.x; zv[4 * i + 1] = v.y; zv[4 * i + 2] = v.z; zv[4 * i + 3] = v.w;
         }
         mraw = (l < NQ && ((cm >> l) & 1)) ? p.mask[(long)t * B + bq0 + l] : 0;
@@ -320,6 +341,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         const int t = dir > 0 ? s : T - 1 - s;
         const int b = s & 1;
         TRACE(0);
+        // the next step's Z: issue the acquire load of the frontier M-tile now, check it before this
+        // step's __syncthreads (its latency hides behind the step)
+        const bool zcheck = zf && threadIdx.x == ZPOLL && s + 1 < T &&
+                            (dir > 0 ? zfront <= z_tile_of(t + 1) : zfront >= z_tile_of(t - 1));
+        uint32_t zseen = 0;
+        if (zcheck) zseen = ld_acquire_gpu(zf + zfront);
         if (w < NISSUE) {  // warp-collective issue (one elected lane), operands warp-uniform
             if (s > 0) mbar_wait(&bars[2 + b], (fph >> b) & 1);  // the cluster's h_{s-1} landed in hbuf[b]
             TRACE(1);
@@ -382,6 +409,11 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         TRACE(10);
         fence_async_smem();
         TRACE(7);
+        if (zcheck) {
+            if (zseen < (uint32_t)p.zflag_target) spin_until_geq(zf + zfront, (uint32_t)p.zflag_target);
+            zfront += dir;
+            z_wait(dir > 0 ? t + 1 : t - 1);  // rare: the step spans a further M-tile
+        }
         // the previous step's bulk copies (of the other staging buffer) have long finished reading;
         // this __syncthreads orders that before the rewrite of that buffer at the next step
         if (l == 0 && w < NC) bulk_wait_read<0>();

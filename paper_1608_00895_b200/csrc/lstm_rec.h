@@ -26,6 +26,10 @@ struct RecParams {
     // forward
     const float *Z;              // time-major transposed [T][ndir*4Hq][B] (gate row d*4Hq + 4j+gamma)
     long ldz;                    // unused (kept for ABI stability of the struct)
+    // != nullptr: Z is still being written by a concurrent GEMM (GemmParams::flags); step t may be
+    // read once zflags[d*zflag_nm + m] >= zflag_target for every 128-row M-tile m holding its frames
+    const uint32_t *zflags;
+    int zflag_target, zflag_nm;
     float *y;                    // [T*B, ldy] (+ d*y_doff), j < H; nullable
     long ldy, y_doff;
     __half *y16;                 // [T*B, ldy16] (+ d*Hq), all j < Hq; nullable

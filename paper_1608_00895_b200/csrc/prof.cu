@@ -17,6 +17,9 @@ struct ProfRec {
 static std::vector<ProfRec> g_recs;   // recorded launches since enable
 static std::vector<cudaEvent_t> g_pool;
 static size_t g_pool_used = 0;
+static int g_suspend = 0;
+
+void prof_suspend(int on) { g_suspend += on ? 1 : -1; }
 
 void note_launch(int n) { g_launches += n; }
 
@@ -30,7 +33,7 @@ static cudaEvent_t pool_event() {
 }
 
 int prof_begin(int cat, cudaStream_t st) {
-    if (!g_prof_on) return -1;
+    if (!g_prof_on || g_suspend > 0) return -1;
     ProfRec r{cat, pool_event(), pool_event()};
     if (!r.e0 || !r.e1) return -1;
     cudaEventRecord(r.e0, st);

@@ -10,6 +10,10 @@ void note_launch(int n = 1);
 int prof_begin(int cat, cudaStream_t st);
 void prof_end(int idx, cudaStream_t st);
 
+// while > 0, prof_begin records nothing (a launch pair timed as one scope: an event between a
+// primary kernel and its programmatic dependent would serialize them)
+void prof_suspend(int on);
+
 // RAII bracket of one launch
 struct ProfScope {
     int idx;

@@ -4,6 +4,8 @@
 // mbarrier, double-buffered), exactly the forward kernel's h exchange.  Reports ns per round.
 //   modes: 0 = one thread issues all 16 copies, 1 = lane 0 of 16 warps issues one each,
 //          2 = st.async.v4 from registers by all threads (no staging)
+//          3 = half the peers by bulk copy (mode 1), the other half by st.async (mode 2): tests
+//              whether the bulk-copy engine and the LSU st.async path add bandwidth
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o dsmem_bench dsmem_bench.cu
 #include <cstdio>
 #include <cstdint>
@@ -56,15 +58,19 @@ __global__ void __cluster_dims__(16, 1, 1) __launch_bounds__(512, 1) kern(int ro
             }
         } else if (mode == 1) {
             if (l == 0 && w < NC) { bulk(mapa(dst, w), smem_u32(stg), bytes, mapa(mb, w)); asm volatile("cp.async.bulk.commit_group;"); }
-        } else {
+        } else if (mode == 2) {
             // each thread stores 16 B pieces of the slice to every peer
             for (int i = threadIdx.x * 16; i < bytes; i += 512 * 16)
                 for (int r = 0; r < NC; ++r) stas(mapa(dst + i, r), s, c, i, 0, mapa(mb, r));
+        } else {
+            if (l == 0 && w < NC / 2) { bulk(mapa(dst, w), smem_u32(stg), bytes, mapa(mb, w)); asm volatile("cp.async.bulk.commit_group;"); }
+            for (int i = threadIdx.x * 16; i < bytes; i += 512 * 16)
+                for (int r = NC / 2; r < NC; ++r) stas(mapa(dst + i, r), s, c, i, 0, mapa(mb, r));
         }
         mwait(&full[b], (ph >> b) & 1);
         ph ^= 1u << b;
         if (threadIdx.x == 0 && s + 2 < rounds) mexpect(&full[b], NC * bytes);
-        if (mode < 2 && threadIdx.x < 32 * NC && l == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (mode != 2 && threadIdx.x < 32 * NC && l == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
     }
     long long t1 = clock64();
@@ -79,8 +85,8 @@ int main() {
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     const int rounds = 2000;
-    for (int mode = 0; mode < 3; ++mode)
-        for (int bytes : {1024, 2048, 4096, 8192}) {
+    for (int mode = 0; mode < 4; ++mode)
+        for (int bytes : {1024, 2048, 4096}) {
             const size_t smem = 2 * 16 * bytes + bytes + 64;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             for (int clusters : {1, 6}) {
