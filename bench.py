@@ -89,6 +89,27 @@ def kernel_roofline(cat, total_ms, launches, cfg, V, peaks):
             "alt": {"bound": "hbm", "achieved": a_gb, "peak": peaks["gbs"], "unit": "GB/s", "frac": f_gb}}
 
 
+def ncu_traffic(kernel_prefix):
+    """DRAM bytes (read + write) per launch of a kernel, from the newest committed ncu summary
+    (profiles/r*_ncu_v*.json, one `ncu --set full` capture; scripts/ncu_summarize.py), or None."""
+    import glob
+    import re
+    files = glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_v*.json"))
+    key = lambda f: tuple(int(x) for x in re.findall(r"r(\d+)_ncu_v(\d+)", os.path.basename(f))[0])  # noqa: E731
+    for f in sorted(files, key=key, reverse=True):
+        try:
+            with open(f) as fh:
+                caps = json.load(fh).get("full_captures", {})
+        except Exception:
+            continue
+        for rep, ks in caps.items():
+            for k in ks:
+                if k["kernel"].startswith(kernel_prefix) and k.get("dram_read_unit") == "Mbyte":
+                    return {"bytes": (k["dram_read"] + k["dram_write"]) * 1e6,
+                            "source": f"{os.path.relpath(f, ROOT)} ({os.path.basename(rep)}, {k['kernel']})"}
+    return None
+
+
 def measured_peaks():
     p = {"gbs": 6549.8, "tf": 1378.5, "source": "MEASURED_PEAKS.json (hbm_gbs, bf16_tflops_sustained)"}
     try:
@@ -311,7 +332,12 @@ def main():
     cats = {0: "lstm_rec_fwd", 1: "lstm_rec_bwd", 2: "gemm_f16 (all GEMMs)"}
     dom = max(prof, key=lambda c: prof[c][0])
     roof = kernel_roofline(dom, prof[dom][0], prof[dom][1], cfg, tr.valid_frames, peaks)
-    roof.update({"kernel": cats[dom], "traffic": None,
+    tr_ncu = ncu_traffic({0: "lstm_rec_fwd_kernel", 1: "lstm_rec_bwd_kernel"}.get(dom, "-"))
+    roof.update({"kernel": cats[dom], "traffic": tr_ncu["bytes"] if tr_ncu else None,
+                 "traffic_unit": "bytes/launch (dram read + write)",
+                 "traffic_source": tr_ncu["source"] if tr_ncu else None,
+                 "algorithmic_bytes_per_launch": (roof["achieved"] * 1e9 * prof[dom][0] / max(prof[dom][1], 1) / 1e3
+                                                  if roof["unit"] == "GB/s" else None),
                  "launch_ms": prof[dom][0] / max(prof[dom][1], 1),
                  "share_of_step": prof[dom][0] / (t_local * 1e3),
                  "peak_source": peaks["source"], "peak_note": peaks["note"]})

@@ -3,6 +3,7 @@
 // BLSTM stack's training step.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -413,8 +414,11 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     // recurrence waits per M-tile on the GEMM's completion counters.  Only when every GEMM CTA can
     // be co-resident with the clusters (one CTA per SM each): a GEMM CTA waiting for an SM would
     // deadlock the spinning recurrence.  Otherwise the GEMM simply runs first.
+    // BLSTM_OVERLAP=0 disables it: profilers that serialize or replay kernels one at a time (ncu)
+    // would otherwise leave the recurrence waiting for a GEMM that cannot run beside it.
     const int side_ctas = num_sms() - 2 * g.pl.G * g.pl.NC;
-    const bool overlap = side_ctas >= 8;
+    static const bool overlap_env = !(getenv("BLSTM_OVERLAP") && atoi(getenv("BLSTM_OVERLAP")) == 0);
+    const bool overlap = overlap_env && side_ctas >= 8;
     if (overlap && gemm_prepare()) return fail(BLSTM_ERR_CUDA, "gemm_prepare");
     for (int l = 0; l < g.L; ++l) {
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
