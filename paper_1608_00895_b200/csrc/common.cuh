@@ -231,6 +231,63 @@ DEVI void mma_commit_w(uint64_t *bar) {
             smem_u32(bar))
         : "memory");
 }
+// ---- CTA pairs (cta_group::2): cluster ranks 2p and 2p+1, on the two SMs of a TPC ----------------
+// Verified on B200 by scripts/pair_test.cu: alloc/relinquish/dealloc are executed by one warp in
+// EACH CTA of the pair; an MMA issued by the even CTA computes M = 256 rows, A (TMEM, TS mode)
+// supplying rows 128r.. from CTA r's TMEM, B split by N (CTA r holds columns [rN/2, (r+1)N/2)
+// at the same smem offset), and CTA r's TMEM receives its 128 rows x all N columns of D.
+DEVI void tmem_alloc2(uint32_t *dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+}
+DEVI void tmem_relinquish2() { asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory"); }
+DEVI void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+DEVI void mma_f16_ts2_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive (once) on the mbarrier at this smem offset in every CTA of cta_mask when the pair MMAs
+// issued so far by this thread complete
+DEVI void mma_commit2_w(uint64_t *bar, uint16_t cta_mask) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "h"(cta_mask)
+        : "memory");
+}
+// arrive on an mbarrier of another CTA of the cluster.  Relaxed: a release would first wait for
+// this thread's earlier global stores to become visible (measured ~0.9 us on the recurrence's
+// critical path); the data announced here was written by bulk copies whose completion this thread
+// has just observed on its own mbarrier.
+DEVI void mbar_remote_arrive(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+DEVI bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// wait for a phase completed by a remote (cluster-scope) arrive
+DEVI void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    if (mbar_try_wait_cluster(a, parity)) return;
+    const uint64_t t0 = globaltimer_ns();
+    while (!mbar_try_wait_cluster(a, parity)) {
+        if (globaltimer_ns() - t0 > SPIN_TIMEOUT_NS) __trap();
+    }
+}
+
 // a warp-uniform copy of v (lane 0's), so the compiler may keep it in a uniform register
 DEVI int warp_uniform(int v) { return __shfl_sync(0xffffffffu, v, 0); }
 

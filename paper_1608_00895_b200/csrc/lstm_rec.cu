@@ -127,12 +127,17 @@ DEVI float gate_act(float pre, int gam) {
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
-// smem: [region0: R^T slice (TMA, start only) | aliased later by hbuf[2] + stg[2]] [barriers]
-//   hbuf[b]: B operand [N x Hq] fp16, no-swizzle K-major: element (n, k) at ((k/8)*N + n)*16 + (k%8)*2,
-//            so CTA c's units [32c, 32c+32) are one contiguous 64N-byte block
-//   stg[b] : this CTA's h slice in that block format
+// CTA pairs: cluster ranks (2p, 2p+1) run each step's MMA as one cta_group::2 MMA (M = 256: the
+// pair's 2 x 128 gate rows), issued by the even CTA.  The B operand h_{t-1}^T is split by batch
+// column: CTA 2p holds columns [0, N/2), CTA 2p+1 columns [N/2, N).  Every CTA therefore receives
+// and sends half the bytes of a full all-gather (the DSMEM port, ~18 B/clk/SM, bounds the step).
+// smem: [region0: R^T slice (TMA, start only) | aliased later by hbuf[2] + stg[2][2]] [barriers]
+//   hbuf[b]: this CTA's half of the B operand [N/2 x Hq] fp16, no-swizzle K-major: element (n', k)
+//            at ((k/8)*N/2 + n')*16 + (k%8)*2, so CTA c's units [32c, 32c+32) are one contiguous
+//            32N-byte block
+//   stg[b][h]: this CTA's h slice, column half h, in that block format (sent to the CTAs of parity h)
 static __host__ __device__ size_t fwd_region0(int Hq, int N) {
-    const size_t rs = (size_t)Hq / 64 * 16384, hb = 2 * (size_t)Hq * N * 2 + 2 * 64 * (size_t)N;
+    const size_t rs = (size_t)Hq / 64 * 16384, hb = (size_t)Hq * N * 2 + 2 * 64 * (size_t)N;
     return rs > hb ? rs : hb;
 }
 
@@ -142,21 +147,26 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     constexpr int N = 16 * NT;   // MMA N = padded batch columns of the group
     constexpr int NQ = N / 4;    // columns handled by one warp
     constexpr int NMQ = NQ / 4;  // columns owned (cell state) by one thread
-    constexpr uint32_t SG = 64 * N;  // bytes of one CTA's h slice
+    constexpr int NH = N / 2;          // B-operand columns held by each CTA of a pair
+    constexpr uint32_t SGh = 64 * NH;  // bytes of one column half of a CTA's h slice
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     const int Hq = p.Hq, KB = Hq / 64, NC = p.NC;
-    const uint32_t HB = (uint32_t)Hq * N * 2;
+    const uint32_t HB = (uint32_t)Hq * NH * 2;
     uint8_t *Rs = smem;
     uint8_t *hbuf = smem;            // aliases Rs after the TMEM load
-    uint8_t *stg = smem + 2 * HB;
-    uint64_t *bars = (uint64_t *)(smem + fwd_region0(Hq, N));  // [0] tma, [1] mma, [2..3] full[b]
-    uint32_t *tslot = (uint32_t *)(bars + 4);
+    uint8_t *stg = smem + 2 * HB;    // [2 b][2 halves][SGh]
+    // [0] tma, [1] mma (arrived by the pair's commits), [2..3] full[b] (own half of h landed),
+    // [4..5] pfull[b] (even CTA: the odd CTA's half landed)
+    uint64_t *bars = (uint64_t *)(smem + fwd_region0(Hq, N));
+    uint32_t *tslot = (uint32_t *)(bars + 6);
 
     // this CTA is resident: a programmatically dependent launch (the concurrent Z GEMM, gemm.h pdl)
     // may start on the SMs left free once every CTA of this grid got here
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int c = (int)cluster_ctarank();
+    const int pr = c & 1;                                   // 0: issues the pair's MMAs
+    const uint16_t pair_mask = (uint16_t)(3u << (c & ~1));  // both CTAs of the pair
     const int grp = blockIdx.x / NC;  // cluster index = d*G + g
     const int g = grp % p.G;
     const int d = grp / p.G;
@@ -183,17 +193,19 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         mbar_init(&bars[1], NISSUE);
         mbar_init(&bars[2], 1);
         mbar_init(&bars[3], 1);
+        mbar_init(&bars[4], 1);
+        mbar_init(&bars[5], 1);
         fence_mbar_init();
     }
-    if (w == 0) {
-        tmem_alloc(tslot, TCOLS);
-        tmem_relinquish();
+    if (w == 0) {  // one warp of each CTA of the pair
+        tmem_alloc2(tslot, TCOLS);
+        tmem_relinquish2();
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    const uint32_t idesc = idesc_f16(128, N, 0, 0);
+    const uint32_t idesc = idesc_f16(256, N, 0, 0);
 
     // valid columns of this warp (bit i <-> column nq0 + i)
     uint32_t cm = 0;
@@ -228,9 +240,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    // h_{-1} = h0 (or 0) into hbuf[0], all Hq units of the group's N columns
-    for (int e = threadIdx.x; e < N * Hq / 2; e += REC_THREADS) {
-        const int n = e / (Hq / 2), k = 2 * (e - n * (Hq / 2)), b = b0 + n;
+    // h_{-1} = h0 (or 0) into hbuf[0]: all Hq units of this CTA's column half
+    for (int e = threadIdx.x; e < NH * Hq / 2; e += REC_THREADS) {
+        const int nn = e / (Hq / 2), k = 2 * (e - nn * (Hq / 2)), n = pr * NH + nn, b = b0 + n;
         float v0 = 0.f, v1 = 0.f;
         if (p.h0 && n < p.Bg && b < B) {
             const float *hp = p.h0 + (long)d * B * H + (long)b * H;
@@ -238,12 +250,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             if (k + 1 < H) v1 = hp[k + 1];
         }
         __half2 h2 = __floats2half2_rn(v0, v1);
-        *reinterpret_cast<__half2 *>(hbuf + ((k >> 3) * N + n) * 16 + (k & 7) * 2) = h2;
+        *reinterpret_cast<__half2 *>(hbuf + ((k >> 3) * NH + nn) * 16 + (k & 7) * 2) = h2;
     }
     fence_async_smem();
     if (threadIdx.x == 0) {
-        if (T > 1) mbar_arrive_expect_tx(&bars[3], NC * SG);  // h_0 from the cluster -> step 1
-        if (T > 2) mbar_arrive_expect_tx(&bars[2], NC * SG);  // h_1 -> step 2
+        if (T > 1) mbar_arrive_expect_tx(&bars[3], NC * SGh);  // h_0 from the cluster -> step 1
+        if (T > 2) mbar_arrive_expect_tx(&bars[2], NC * SGh);  // h_1 -> step 2
     }
     // Z of step t2 may still be in flight from the concurrent Z GEMM (p.zflags): one thread (lane 0
     // of the first non-issuing warp) verifies the M-tiles holding frames t2*B .. t2*B+B-1 in this
@@ -347,17 +359,25 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
                             (dir > 0 ? zfront <= z_tile_of(t + 1) : zfront >= z_tile_of(t - 1));
         uint32_t zseen = 0;
         if (zcheck) zseen = ld_acquire_gpu(zf + zfront);
-        if (w < NISSUE) {  // warp-collective issue (one elected lane), operands warp-uniform
-            if (s > 0) mbar_wait(&bars[2 + b], (fph >> b) & 1);  // the cluster's h_{s-1} landed in hbuf[b]
+        if (pr == 0 && w < NISSUE) {  // warp-collective issue of the pair MMA (one elected lane)
+            if (s > 0) {  // h_{s-1}: this CTA's half and the odd CTA's half have landed
+                mbar_wait(&bars[2 + b], (fph >> b) & 1);
+                TRACE(11);
+                mbar_wait_cluster(&bars[4 + b], (fph >> b) & 1);
+            }
             TRACE(1);
             tc_fence_after();
             const uint32_t hb = hbuf_addr + b * HB;
             const int ks0 = w * (Hq / 16 / NISSUE), ks1 = ks0 + Hq / 16 / NISSUE;
-            for (int ks = ks0; ks < ks1; ++ks)  // K step = 32N bytes of the B buffer
-                mma_f16_ts_w(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * N, 16 * N, 128), idesc,
-                             ks != ks0);
-            mma_commit_w(&bars[1]);
+            for (int ks = ks0; ks < ks1; ++ks)  // K step = 16N bytes of the half B buffer
+                mma_f16_ts2_w(tmem + DCOL + w * N, tmem + ks * 8, sdesc_noswz(hb + ks * 32 * NH, 16 * NH, 128), idesc,
+                              ks != ks0);
+            mma_commit2_w(&bars[1], pair_mask);
             TRACE(2);
+        } else if (pr == 1 && threadIdx.x == 0 && s > 0) {
+            // odd CTA: its half of h_{s-1} landed -> tell the even CTA, which reads it in the MMA
+            mbar_wait(&bars[2 + b], (fph >> b) & 1);
+            mbar_remote_arrive(mapa_shared(smem_u32(&bars[4 + b]), c ^ 1));
         }
         if (s > 0) fph ^= 1u << b;
         if (s > 0) store_step(t_prev, frm_prev, fmq_prev);
@@ -388,7 +408,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         TRACE(9);
         tc_fence_before();
         uint32_t fmq = 0;  // bit m: owned column 4m+gam is a valid frame
-        uint8_t *sg = stg + b * SG;
+        // this warp's columns lie in one column half (NQ divides N/2)
+        const int hh = nq0 / NH;
+        uint8_t *sg = stg + (b * 2 + hh) * SGh;
 #pragma unroll
         for (int m = 0; m < NMQ; ++m) {
             float a4[4] = {act[4 * m], act[4 * m + 1], act[4 * m + 2], act[4 * m + 3]};
@@ -404,7 +426,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             h_st[m] = fm ? hn : h_st[m];
             fmq |= (uint32_t)fm << m;
             // staged slice in the B-operand block format: unit jl -> k chunk q, byte (jl%8)*2
-            *reinterpret_cast<__half *>(sg + (q * N + nq0 + i) * 16 + (jl & 7) * 2) = __float2half_rn(h_st[m]);
+            *reinterpret_cast<__half *>(sg + (q * NH + nq0 - hh * NH + i) * 16 + (jl & 7) * 2) = __float2half_rn(h_st[m]);
         }
         TRACE(10);
         fence_async_smem();
@@ -420,12 +442,13 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         __syncthreads();
         TRACE(4);
         if (l == 0 && w < NC && s + 1 < T) {
-            // h_s of this CTA -> hbuf[b^1] (block c) of CTA w of the cluster (16 warps send in parallel)
-            bulk_s2c(mapa_shared(hbuf_addr + (b ^ 1) * HB + c * SG, w), stg_addr + b * SG, SG,
+            // h_s of this CTA, the column half CTA w holds -> hbuf[b^1] (block c) of CTA w
+            // (16 warps send in parallel)
+            bulk_s2c(mapa_shared(hbuf_addr + (b ^ 1) * HB + c * SGh, w), stg_addr + (b * 2 + (w & 1)) * SGh, SGh,
                      mapa_shared(full_addr + 8 * (b ^ 1), w));
             bulk_commit();
         }
-        if (threadIdx.x == 0 && s > 0 && s + 2 < T) mbar_arrive_expect_tx(&bars[2 + b], NC * SG);  // full[b]: step s+2
+        if (threadIdx.x == 0 && s > 0 && s + 2 < T) mbar_arrive_expect_tx(&bars[2 + b], NC * SGh);  // full[b]: step s+2
         TRACE(5);
         t_prev = t;
         frm_prev = frm;
@@ -445,10 +468,10 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     if (l == 0 && w < NC) bulk_wait_read<0>();  // outgoing copies done with the staging buffers
     tc_fence_before();
     __syncthreads();
-    cluster_sync();
+    cluster_sync();  // both CTAs of every pair are done (the pair MMAs wrote both TMEMs)
     if (w == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem, TCOLS);
+        tmem_dealloc2(tmem, TCOLS);
     }
 }
 
