@@ -70,7 +70,7 @@ struct FwdWS {
     size_t x16, w16, rt16, bq, Z, maskN, cnt, total;
 };
 struct BwdWS {
-    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cnt, total;
+    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cpk, dypk, cnt, total;
 };
 struct Reserve {
     size_t gates, hist, total;
@@ -119,6 +119,10 @@ static BwdWS bwd_ws(const LayerGeo &g) {
     w.dbp = c.take((size_t)g.pl.G * 4 * g.Hq * 4);
     w.P = c.take(rec_P_bytes(g.pl));
     w.maskN = c.take(rec_mask_bytes(g.pl, g.T));
+    // c and dy repacked with a 16-byte row pitch when the caller's is not (the BPTT kernel reads
+    // them by TMA)
+    w.cpk = c.take((size_t)g.TB * g.Hq * 4);
+    w.dypk = c.take((size_t)g.TB * g.Hq * 4);
     w.cnt = c.take(256);
     w.total = c.off;
     return w;
@@ -235,9 +239,19 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     RecParams p = base_params(g, 1, d->direction, mask);
     p.maskN = maskN;
     p.C = const_cast<float *>(c); p.ldc = g.H; p.c_doff = 0;  // read-only in the backward kernel
+    if (((uintptr_t)c & 15) || (g.H & 3)) {  // TMA rows need a 16-byte pitch
+        float *cpk = (float *)(ws + w.cpk);
+        TRY(copy_rows(c, g.H, g.TB, g.H, cpk, g.Hq, st), "copy c");
+        p.C = cpk; p.ldc = g.Hq;
+    }
     p.gates = (__half *)(res + rv.gates); p.ldg = 4L * g.Hq;
     p.c0 = c0;
     p.dy = dy; p.lddy = d->ldy; p.dy_doff = 0;
+    if (((uintptr_t)dy & 15) || (d->ldy & 3)) {
+        float *dypk = (float *)(ws + w.dypk);
+        TRY(copy_rows(dy, d->ldy, g.TB, g.H, dypk, g.Hq, st), "copy dy");
+        p.dy = dypk; p.lddy = g.Hq;
+    }
     p.dhT = dhT; p.dcT = dcT;
     p.dA = dA; p.ldda = 4L * g.Hq;
     p.dbpart = dbp;

@@ -284,6 +284,24 @@ int make_tmap_f16(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t ou
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+// 2-D fp32 tensor map over a row-major [outer, inner] array with row stride ld (elements),
+// box {32 inner (128 B), box_outer}, 128B swizzle, OOB reads as zero.  Needs ld*4 % 16 == 0 and
+// a 16-byte aligned base.
+int make_tmap_f32_rows(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                       uint32_t box_outer) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return -1;
+    if (((uintptr_t)ptr & 15) || ((ld * 4) & 15)) return -3;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld * 4};
+    cuuint32_t box[2] = {32, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 static int g_num_sms = 0;
 int num_sms() {
     if (!g_num_sms) {

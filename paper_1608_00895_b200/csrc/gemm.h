@@ -42,6 +42,8 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &p, in
 int gemm_prepare();
 int make_tmap_f16(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                   uint32_t box_outer);
+int make_tmap_f32_rows(CUtensorMap *map, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                       uint32_t box_outer);
 int num_sms();
 
 }  // namespace blstm

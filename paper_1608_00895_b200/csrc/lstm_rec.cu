@@ -478,14 +478,24 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 // ---------------------------------------------------------------------------
 // backward through time
 // ---------------------------------------------------------------------------
-// smem: [region0: R^T slice (TMA, start only) | aliased later by the P slots] [dAs] [in ring] [barriers]
-//   slots[b][src][32 rows][N] fp16: partial dh (x 2^DA_SHIFT x P_SCALE) of this CTA's 32 units
-//   from CTA src, 16-byte chunks swizzled by row (pswz) so the owner's gather is conflict-free
+// CTA pairs (cluster ranks 2p, 2p+1; see the forward): the pair owns the 256 gate columns of its
+// 64 units.  Per step it computes P_p[Hq x N] = R[:, cols_p] . dA_p^T as cta_group::2 MMAs with
+// K = those 256 columns and M = 256-unit tiles, CTA r of the pair holding unit rows
+// 256mt + 128r + [0, 128) of tile mt (in TMEM, A operand) and batch columns [rN/2, (r+1)N/2) of
+// dA (smem, B operand).  Each CTA computes dA for its own 128 gate columns and all N batch columns
+// and st.async's the half its partner holds (4 KB at N=32).  P rows are partial sums over the
+// pair's 256 gate columns, so every owner gathers NC/2 partials (not NC) and every CTA sends NC/2
+// blocks: half the DSMEM bytes of a per-CTA decomposition.
+// smem: [region0: R slices (TMA, start only) | aliased later by slots[2] + stg[2]] [dAs] [in ring]
+//       [barriers]
+//   slots[b][src pair][32 rows][N] fp16: partial dh (x 2^DA_SHIFT x P_SCALE) of this CTA's 32
+//   units from source pair src, 16-byte chunks swizzled by row (pswz): conflict-free gather
 constexpr float P_SCALE = 1.f / 16.f;  // keeps the fp16 partials far from overflow
-//   stg[b][owner][32 rows][N] fp16: this CTA's partial rows per owner (same swizzle), bulk-copied
-//   as one block
+//   stg[b][block][32 rows][N] fp16: this CTA's partial rows per destination owner (same swizzle)
+//   dAs[4 x 64-column blocks][N/2 rows][128 B] fp16, K-major SW128: the pair's 256 gate columns
+//   (the even CTA's first) for this CTA's batch-column half
 static __host__ __device__ size_t bwd_region0(int Hq, int N, int NC) {
-    const size_t rs = (size_t)Hq / 64 * 16384, sl = 4 * (size_t)NC * 32 * N * 2;
+    const size_t rs = (size_t)Hq / 64 * 16384, sl = 2 * (size_t)NC * 32 * N * 2;
     return rs > sl ? rs : sl;
 }
 // byte offset of element (row r, column n) in a P block [32 rows][N] fp16: the 16-byte chunk index
@@ -498,31 +508,46 @@ DEVI uint32_t pswz(int r, int n) {
     return (uint32_t)(r * RB + ((((2 * n) >> 4) ^ f) << 4) + ((2 * n) & 15));
 }
 
-template <int NT>
+template <int NT, int MT2>
 __global__ void __launch_bounds__(REC_THREADS, 1)
-    lstm_rec_bwd_kernel(const __grid_constant__ CUtensorMap tmR, RecParams p) {
+    lstm_rec_bwd_kernel(const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmC,
+                        const __grid_constant__ CUtensorMap tmDY, RecParams p) {
     constexpr int N = 16 * NT;
+    constexpr int NH = N / 2;  // batch columns of the B operand held by each CTA of a pair
     constexpr int NQ = N / 4;
     constexpr int NMQ = NQ / 4;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
-    const int Hq = p.Hq, KB = Hq / 64, MT = Hq / 128, NC = p.NC;
-    constexpr uint32_t BLK = 32 * N * 2;                   // one (owner, source) block
-    const uint32_t SLOTB = (uint32_t)NC * BLK;             // bytes of one slot buffer
-    const uint32_t SLOT_TX = SLOTB;                        // bytes arriving per buffer (NC blocks)
+    const int Hq = p.Hq, NC = p.NC;
+    // MT2 = Hq / 256 pair M tiles (256 units); KP K parts per tile: 4 issuing warps, one
+    // accumulator each
+    constexpr int KP = 4 / MT2;
+    const int NSRC = NC / 2;       // source pairs = P blocks per slot buffer = blocks sent per CTA
+    constexpr uint32_t BLK = 32 * N * 2;  // one (owner, source) block
+    const uint32_t SLOTB = (uint32_t)NSRC * BLK;
+    const uint32_t SLOT_TX = SLOTB;
+    constexpr uint32_t DA_TX = 128 * NH * 2;  // dA bytes the partner sends per step
     uint8_t *Rs = smem;
-    uint8_t *slots = smem;             // [2][NC][BLK], aliases Rs after the TMEM load
-    uint8_t *stgp = smem + 2 * SLOTB;  // [2][NC][BLK]
-    uint8_t *dAs = smem + bwd_region0(Hq, N, NC);      // [2][N][128 B] K-major SW128
-    // per-step inputs, ring of 2 (bwd_in_bytes): each thread cp.async's exactly the values it reads
-    // (gates [512 thr][NQ] fp16, then c_t, c_{t-dir}, dy as [NMQ][512 thr] fp32, then [16 warps][16] mask
-    // bytes), one step ahead, so no global load latency sits on the recurrence's critical path
-    constexpr uint32_t IN_G = 512 * NQ * 2, IN_F = NMQ * 512 * 4, IN_SLOT = IN_G + 3 * IN_F + 256;
-    uint8_t *inr = dAs + 2 * N * 128;
-    uint64_t *bars = (uint64_t *)(inr + 2 * IN_SLOT);   // [0] tma, [1] mma, [2..3] slots full[b]
-    uint32_t *tslot = (uint32_t *)(bars + 4);
+    uint8_t *slots = smem;               // [2][NSRC][BLK], aliases Rs after the TMEM load
+    uint8_t *stgp = smem + 2 * SLOTB;    // [2][NSRC][BLK]
+    uint8_t *dAs = smem + bwd_region0(Hq, N, NC);  // [4][NH][128 B]
+    // per-step inputs, loaded by one thread with bulk / TMA copies one step ahead (bwd_in_bytes); a
+    // per-thread cp.async of these scattered values cost ~0.7 us of issue per step:
+    //   inr[2]: dy tile [N rows][32 units] fp32 (TMA, SW128), the CTA's gate block (512 x NQ fp16,
+    //           CTA-native), the mask row (N bytes); slot k&1 for processing index k
+    //   cring[3]: c tile [N rows][32 units] fp32 (TMA, SW128); slot k%3 holds c(t_k), so step k reads
+    //           c_t from slot k%3 and c_{t-dir} = c(t_{k+1}) from slot (k+1)%3: one c tile per step
+    constexpr uint32_t TILE = N * 128, IN_G = 512 * NQ * 2, IN_SLOT = TILE + IN_G + 1024;
+    uint8_t *inr = dAs + 4 * NH * 128;
+    uint8_t *cring = inr + 2 * IN_SLOT;
+    // [0] tma, [1] mma (pair commits), [2..3] slots full[b], [4] dfull (partner's dA half landed),
+    // [5] dpair (even CTA: the odd CTA's B operand is complete), [6..7] inb[slot] (inputs landed)
+    uint64_t *bars = (uint64_t *)(cring + 3 * TILE);
+    uint32_t *tslot = (uint32_t *)(bars + 8);
 
     const int c = (int)cluster_ctarank();
+    const int pr = c & 1;
+    const uint16_t pair_mask = (uint16_t)(3u << (c & ~1));
     const int grp = blockIdx.x / NC;
     const int g = grp % p.G;
     const int d = grp / p.G;
@@ -536,56 +561,68 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const int nq0 = cb * NQ;
     const int bq0 = b0 + nq0;
     constexpr uint32_t TCOLS = 512;
-    // TMEM: M tile mt of A = R[128mt.., cols_c] (lanes = hidden unit k, two fp16 gate columns per
-    // 32-bit column) at columns [64mt, 64mt+64); accumulators D_mt[128 x N] from column Hq/2.
-    // Warp mt issues the MMAs of tile mt (the tiny MMAs are issue-bound).
+    // TMEM: pair tile mt of A at columns [128mt, 128mt+128): lanes = this CTA's units 256mt+128pr+lane,
+    // two fp16 gate columns (pair K order) per 32-bit column.  Accumulators D_w[128 x N] at
+    // Hq/2 + w*N: warp w issues tile w / KP, K part w % KP.
     const uint32_t DCOL = Hq / 2;
     const float inv_scale = 1.f / ((float)(1 << DA_SHIFT) * P_SCALE);
     const float scale = (float)(1 << DA_SHIFT);
 
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], MT);
+        mbar_init(&bars[1], 4);
         mbar_init(&bars[2], 1);
         mbar_init(&bars[3], 1);
+        mbar_init(&bars[4], 1);
+        mbar_init(&bars[5], 1);
+        mbar_init(&bars[6], 1);
+        mbar_init(&bars[7], 1);
         fence_mbar_init();
     }
-    if (w == 0) {
-        tmem_alloc(tslot, TCOLS);
-        tmem_relinquish();
+    if (w == 0) {  // one warp of each CTA of the pair
+        tmem_alloc2(tslot, TCOLS);
+        tmem_relinquish2();
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    const uint32_t idesc = idesc_f16(128, N, 0, 0);
+    const uint32_t idesc = idesc_f16(256, N, 0, 0);
 
     uint32_t cm = 0;
 #pragma unroll
     for (int i = 0; i < NQ; ++i)
         if (nq0 + i < p.Bg && bq0 + i < B) cm |= 1u << i;
 
+    // R^T rows of both slices of the pair (gate columns), unit columns of this CTA's rows:
+    // box (si, mt, h) = slice si (0: even CTA), units 256mt + 128pr + 64h .. +64
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmR);
-        mbar_arrive_expect_tx(&bars[0], KB * 16384);
-        for (int kb = 0; kb < KB; ++kb) tma_load_2d(Rs + kb * 16384, &tmR, &bars[0], kb * 64, d * 4 * Hq + c * 128);
+        mbar_arrive_expect_tx(&bars[0], (uint32_t)(2 * MT2 * 2) * 16384);
+        for (int si = 0; si < 2; ++si)
+            for (int mt = 0; mt < MT2; ++mt)
+                for (int h = 0; h < 2; ++h)
+                    tma_load_2d(Rs + ((si * MT2 + mt) * 2 + h) * 16384, &tmR, &bars[0], 256 * mt + 128 * pr + 64 * h,
+                                d * 4 * Hq + ((c & ~1) + si) * 128);
     }
     mbar_wait(&bars[0], 0);
-    // R[:, cols_c] (the R^T slice read transposed): shared memory -> registers -> TMEM, once.
+    // -> TMEM: lane u = unit 256mt + 128pr + u, column 128mt + kk/2 holds gate columns kk, kk+1 of
+    // the pair (kk < 128: the even CTA's slice)
     {
+        const int u = 32 * q + l;
         const int cw = Hq / 8;
         for (int col = cb * cw; col < (cb + 1) * cw; col += 16) {
-            const int mt = col >> 6, k = 128 * mt + 32 * q + l, r0 = (col & 63) * 2;
-            const uint8_t *rk = Rs + (k >> 6) * 16384 + (k & 7) * 2;
-            const int chunk = (k & 63) >> 3;
+            const int mt = col >> 7, kk0 = (col & 127) * 2, si = kk0 >> 7, r0 = kk0 & 127;
+            const uint8_t *rk = Rs + ((si * MT2 + mt) * 2 + (u >> 6)) * 16384 + (u & 7) * 2;
+            const int chunk = (u & 63) >> 3;
             uint32_t v[16];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int r = r0 + 2 * u;
+            for (int uu = 0; uu < 16; ++uu) {
+                const int r = r0 + 2 * uu;
                 const uint16_t lo = *reinterpret_cast<const uint16_t *>(rk + r * 128 + ((chunk ^ (r & 7)) << 4));
                 const uint16_t hi =
                     *reinterpret_cast<const uint16_t *>(rk + (r + 1) * 128 + ((chunk ^ ((r + 1) & 7)) << 4));
-                v[u] = (uint32_t)lo | ((uint32_t)hi << 16);
+                v[uu] = (uint32_t)lo | ((uint32_t)hi << 16);
             }
             tmem_st16(tmem + ((uint32_t)(32 * q) << 16) + col, v);
         }
@@ -599,6 +636,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     if (threadIdx.x == 0) {
         if (T >= 1) mbar_arrive_expect_tx(&bars[2], SLOT_TX);  // index 1 <- P of index 0
         if (T >= 2) mbar_arrive_expect_tx(&bars[3], SLOT_TX);  // index 2 <- P of index 1
+        if (T >= 1) mbar_arrive_expect_tx(&bars[4], DA_TX);    // the partner's dA of index 0
     }
     cluster_sync();  // every CTA done with its R staging before peers write into the slots
 
@@ -623,51 +661,55 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             if ((pfm >> m) & 1) {
                 const uint8_t *sl = slots + b * SLOTB + pswz<N>(jl, nq0 + 4 * m + gam);
                 float acc = 0.f;
-                for (int src = 0; src < NC; ++src) acc += __half2float(*reinterpret_cast<const __half *>(sl + src * BLK));
+                for (int src = 0; src < NSRC; ++src)
+                    acc += __half2float(*reinterpret_cast<const __half *>(sl + src * BLK));
                 dh[m] = acc * inv_scale;
             }
         }
     };
     const long nat_step = (long)p.ndir * p.G * NC * 512 * NQ;
-    const long nat_off = (((long)d * p.G + g) * NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
 
-    // saved state of one step (independent of the recurrence): cp.async'd one step ahead into ring
-    // slot sl, read back by the same thread (the mask bytes by its warp)
+    // saved state of one step (independent of the recurrence), one step ahead: thread 0 issues the
+    // copies for processing index k into ring slot k&1, and c(t_{k+1}) into cring[(k+1)%3]
     const int tid = threadIdx.x;
-    const uint32_t in_addr = smem_u32(inr);
-    auto load_step = [&](int t, int sl) {
-        const uint32_t base = in_addr + sl * IN_SLOT;
-        if constexpr (NQ * 2 <= 16) {
-            cp_async<NQ * 2>(base + tid * NQ * 2, p.gates + t * nat_step + nat_off);
-        } else {
-#pragma unroll
-            for (int i = 0; i < NQ / 8; ++i) cp_async16(base + tid * NQ * 2 + 16 * i, p.gates + t * nat_step + nat_off + 8 * i);
-        }
-        const int tp = t - dir;
-#pragma unroll
-        for (int m = 0; m < NMQ; ++m) {
-            const int i = 4 * m + gam, b = bq0 + i;
-            const bool ok = ((cm >> i) & 1) && unit_ok;
-            const long row = (long)t * B + b;
-            const uint32_t o = (uint32_t)(m * 512 + tid) * 4;
-            cp_async4_zfill(base + IN_G + o, ok ? p.C + row * p.ldc + d * p.c_doff + j : p.C, ok ? 4 : 0);
-            if (tp >= 0 && tp < T)
-                cp_async4_zfill(base + IN_G + IN_F + o, ok ? p.C + ((long)tp * B + b) * p.ldc + d * p.c_doff + j : p.C,
-                                ok ? 4 : 0);
-            else
-                cp_async4_zfill(base + IN_G + IN_F + o, (ok && p.c0) ? p.c0 + (long)d * B * H + (long)b * H + j : p.C,
-                                (ok && p.c0) ? 4 : 0);
-            cp_async4_zfill(base + IN_G + 2 * IN_F + o, ok ? p.dy + row * p.lddy + d * p.dy_doff + j : p.dy, ok ? 4 : 0);
-        }
-        if (l == 0) cp_async<NQ>(base + IN_G + 3 * IN_F + w * 16, p.maskN + ((long)t * p.G + g) * N + nq0);
-        cp_async_commit();
+    const long nat_cta = (((long)d * p.G + g) * NC + c) * 512 * NQ;
+    const int crows = p.ldc ? (int)(p.c_doff / p.ldc) : 0;  // rows per direction of the C array
+    auto t_of = [&](int k) { return dir > 0 ? T - 1 - k : k; };
+    auto issue_in = [&](int k, bool with_c0) {
+        const int tk = t_of(k), sl = k & 1;
+        uint8_t *slot = inr + sl * IN_SLOT;
+        const bool cnext = k + 1 < T;
+        mbar_arrive_expect_tx(&bars[6 + sl], TILE + IN_G + N + (cnext ? TILE : 0) + (with_c0 ? TILE : 0));
+        tma_load_2d(slot, &tmDY, &bars[6 + sl], d * (int)p.dy_doff + 32 * c, tk * B + b0);
+        bulk_g2s(smem_u32(slot + TILE), p.gates + tk * nat_step + nat_cta, IN_G, &bars[6 + sl]);
+        bulk_g2s(smem_u32(slot + TILE + IN_G), p.maskN + ((long)tk * p.G + g) * N, N, &bars[6 + sl]);
+        if (with_c0) tma_load_2d(cring + (k % 3) * TILE, &tmC, &bars[6 + sl], 32 * c, d * crows + tk * B + b0);
+        if (cnext) tma_load_2d(cring + ((k + 1) % 3) * TILE, &tmC, &bars[6 + sl], 32 * c, d * crows + t_of(k + 1) * B + b0);
     };
-    if (T > 0) load_step(dir > 0 ? T - 1 : 0, 0);
+    if (threadIdx.x == 0 && T > 0) {
+        tma_prefetch_desc(&tmC);
+        tma_prefetch_desc(&tmDY);
+        issue_in(0, true);
+    }
+    // element (row n, unit jl) of a [N rows][32 fp32] SW128 tile
+    auto tile_f32 = [&](const uint8_t *tile, int n) {
+        return *reinterpret_cast<const float *>(tile + n * 128 + ((((jl >> 2) ^ n) & 7) << 4) + (jl & 3) * 4);
+    };
+    // c before the sequence (for the last processed frame): c0 or 0
+    float c0v[NMQ];
+#pragma unroll
+    for (int m = 0; m < NMQ; ++m) {
+        const int i = 4 * m + gam, b = bq0 + i;
+        c0v[m] = (((cm >> i) & 1) && unit_ok && p.c0) ? p.c0[(long)d * B * H + (long)b * H + j] : 0.f;
+    }
     float graw[NQ], ct[NMQ], cp[NMQ], dyv[NMQ];
 
     uint32_t mma_phase = 0;
     const uint32_t das_addr = smem_u32(dAs);
     const uint32_t slots_addr = smem_u32(slots), full_addr = smem_u32(&bars[2]);
+    const uint32_t das_peer = mapa_shared(das_addr, c ^ 1), dfull_peer = mapa_shared(smem_u32(&bars[4]), c ^ 1);
+    // this warp's batch columns lie in one column half (NQ divides N/2): local or the partner's
+    const int hh = nq0 / NH;
 #ifdef BLSTM_TRACE
     unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
 #endif
@@ -675,31 +717,33 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         const int t = dir > 0 ? s : T - 1 - s;
         const int k_done = T - 1 - s;
         TRACE(0);
+        // the next step's inputs: its ring slots were last read one step ago
+        if (threadIdx.x == 0 && k_done + 1 < T) issue_in(k_done + 1, false);
         TRACE(1);
         // ---- dh_t from the previous step's partials ----
         if (k_done > 0) gather(k_done);
         TRACE(2);
-        // ---- this step's saved state (landed during the gather) ----
-        cp_async_wait<0>();
-        __syncwarp();  // lane 0 copied the warp's mask bytes
+        // ---- this step's saved state (issued one step ago) ----
+        mbar_wait(&bars[6 + (k_done & 1)], (k_done >> 1) & 1);
         uint32_t mraw;
         {
             const uint8_t *in = inr + (k_done & 1) * IN_SLOT;
-            const __half2 *gh = reinterpret_cast<const __half2 *>(in + tid * NQ * 2);
+            const __half2 *gh = reinterpret_cast<const __half2 *>(in + TILE + tid * NQ * 2);
 #pragma unroll
             for (int i = 0; i < NQ; i += 2) {
                 const float2 f2 = __half22float2(gh[i / 2]);
                 graw[i] = f2.x;
                 graw[i + 1] = f2.y;
             }
-            const float *fin = reinterpret_cast<const float *>(in + IN_G);
+            const uint8_t *ctile = cring + (k_done % 3) * TILE, *ptile = cring + ((k_done + 1) % 3) * TILE;
 #pragma unroll
             for (int m = 0; m < NMQ; ++m) {
-                ct[m] = fin[m * 512 + tid];
-                cp[m] = fin[NMQ * 512 + m * 512 + tid];
-                dyv[m] = fin[2 * NMQ * 512 + m * 512 + tid];
+                const int n = nq0 + 4 * m + gam;
+                ct[m] = tile_f32(ctile, n);
+                cp[m] = k_done + 1 < T ? tile_f32(ptile, n) : c0v[m];
+                dyv[m] = tile_f32(in, n);
             }
-            mraw = l < NQ ? in[IN_G + 3 * IN_F + w * 16 + l] : 0;
+            mraw = l < NQ ? in[TILE + IN_G + nq0 + l] : 0;
         }
         // ---- gate gradients ----
         const uint32_t frm = __ballot_sync(0xffffffffu, mraw != 0);
@@ -730,7 +774,10 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             uint2 pk;
             pk.x = *reinterpret_cast<uint32_t *>(&lo);
             pk.y = *reinterpret_cast<uint32_t *>(&hi);
-            *reinterpret_cast<uint2 *>(dAs + sw128_offset(n, 4 * jl, N)) = pk;
+            // B operand position: row n - hh*NH of the CTA holding half hh, pair K column 128pr + 4jl
+            const uint32_t off = sw128_offset(n - hh * NH, 128 * pr + 4 * jl, NH);
+            if (hh == pr) *reinterpret_cast<uint2 *>(dAs + off) = pk;
+            else st_async_v2u(das_peer + off, pk.x, pk.y, dfull_peer);
             pks[m] = pk;
         }
         TRACE(9);
@@ -738,13 +785,24 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         tc_fence_before();
         __syncthreads();
         TRACE(3);
-        if (w < MT) {  // warp-collective issue of M tile w (one elected lane), operands warp-uniform
+        if (pr == 0 && w < 4) {  // even CTA: warp-collective issue of tile w / KP, K part w % KP
+            // the partner's dA half has landed here, and the partner's own B operand is complete
+            mbar_wait_cluster(&bars[4], k_done & 1);
+            mbar_wait_cluster(&bars[5], k_done & 1);
+            if (threadIdx.x == 0 && k_done + 1 < T) mbar_arrive_expect_tx(&bars[4], DA_TX);
             tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk)  // 64 gate columns per SW128 block, K step = 32 B
-                mma_f16_ts_w(tmem + DCOL + w * N, tmem + w * 64 + kk * 8,
-                             sdesc_sw128(das_addr + (kk >> 2) * N * 128 + (kk & 3) * 32, 16, 1024), idesc, kk != 0);
-            mma_commit_w(&bars[1]);
+            const int mt = w / KP, kp = w % KP, kpn = 16 / KP;  // K steps of 16 per part
+#pragma unroll 1
+            for (int ks = kp * kpn; ks < (kp + 1) * kpn; ++ks)  // 64 gate columns per SW128 block
+                mma_f16_ts2_w(tmem + DCOL + w * N, tmem + 128 * mt + ks * 8,
+                              sdesc_sw128(das_addr + (ks >> 2) * NH * 128 + (ks & 3) * 32, 16, 1024), idesc,
+                              ks != kp * kpn);
+            mma_commit2_w(&bars[1], pair_mask);
+        } else if (pr == 1 && threadIdx.x == 0) {
+            // odd CTA: the even CTA's dA half landed and this CTA's own part is written -> relay
+            mbar_wait_cluster(&bars[4], k_done & 1);
+            if (k_done + 1 < T) mbar_arrive_expect_tx(&bars[4], DA_TX);
+            mbar_remote_arrive(mapa_shared(smem_u32(&bars[5]), c ^ 1));
         }
         // while the MMA runs: dA of this step to global memory for the weight / input GEMMs
 #pragma unroll
@@ -758,30 +816,35 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         mma_phase ^= 1;
         tc_fence_after();
         TRACE(4);
-        // rows k = 128mt + 32q + l of P belong to owner c' = 4mt + q (its local row l): stage them
-        // (fp16) per owner, then warp w bulk-copies the block of owner w into w's slot for source c
+        // rows of tile mt, lane quarter q = units 256mt + 128pr + 32q + l belong to owner
+        // c' = 8mt + 4pr + q (its local row l): stage P = sum of the tile's K parts (fp16) per owner,
+        // then warp w (< NSRC) bulk-copies block w into its owner's slot for this pair
         {
             const int kb = k_done & 1;
-            constexpr int MTMAX = 4;  // Hq <= 512
-            uint32_t v[MTMAX][NQ];
+            constexpr int NACC = 4;
+            uint32_t v[NACC][NQ];
 #pragma unroll
-            for (int mt = 0; mt < MTMAX; ++mt)
-                if (mt < MT) tmem_ld_nowait<NQ>(tmem + ((uint32_t)(32 * q) << 16) + DCOL + mt * N + nq0, v[mt]);
+            for (int a = 0; a < NACC; ++a) tmem_ld_nowait<NQ>(tmem + ((uint32_t)(32 * q) << 16) + DCOL + a * N + nq0, v[a]);
             tmem_ld_wait();
 #pragma unroll
-            for (int mt = 0; mt < MTMAX; ++mt) pin_regs<NQ>(v[mt]);
+            for (int a = 0; a < NACC; ++a) pin_regs<NQ>(v[a]);
             TRACE(11);
 #pragma unroll
-            for (int mt = 0; mt < MTMAX; ++mt) {
-                if (mt >= MT) break;
+            for (int mt = 0; mt < MT2; ++mt) {
                 uint32_t hv[NQ / 2];
 #pragma unroll
                 for (int i = 0; i < NQ; i += 2) {
-                    __half2 h2 = __floats2half2_rn(__uint_as_float(v[mt][i]) * P_SCALE,
-                                                   __uint_as_float(v[mt][i + 1]) * P_SCALE);
+                    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+                    for (int a = 0; a < NACC; ++a)
+                        if (a / KP == mt) {
+                            s0 += __uint_as_float(v[a][i]);
+                            s1 += __uint_as_float(v[a][i + 1]);
+                        }
+                    __half2 h2 = __floats2half2_rn(s0 * P_SCALE, s1 * P_SCALE);
                     hv[i / 2] = *reinterpret_cast<uint32_t *>(&h2);
                 }
-                uint8_t *blk = stgp + ((uint32_t)kb * NC + 4 * mt + q) * BLK;
+                uint8_t *blk = stgp + ((uint32_t)kb * NSRC + 4 * mt + q) * BLK;
                 if constexpr (NQ == 4) {
                     *reinterpret_cast<uint2 *>(blk + pswz<N>(l, nq0)) = make_uint2(hv[0], hv[1]);
                 } else {
@@ -796,16 +859,16 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             TRACE(6);
             // the previous step's bulk copies (other staging buffer) are done reading; this
             // __syncthreads orders that before the rewrite of that buffer at the next step
-            if (l == 0 && w < NC) bulk_wait_read<0>();
+            if (l == 0 && w < NSRC) bulk_wait_read<0>();
             __syncthreads();
             TRACE(7);
-            if (l == 0 && w < NC) {
-                bulk_s2c(mapa_shared(slots_addr + kb * SLOTB + c * BLK, w),
-                         smem_u32(stgp) + ((uint32_t)kb * NC + w) * BLK, BLK, mapa_shared(full_addr + 8 * kb, w));
+            if (l == 0 && w < NSRC) {
+                const int owner = 8 * (w >> 2) + 4 * pr + (w & 3);
+                bulk_s2c(mapa_shared(slots_addr + kb * SLOTB + (c >> 1) * BLK, owner),
+                         smem_u32(stgp) + ((uint32_t)kb * NSRC + w) * BLK, BLK, mapa_shared(full_addr + 8 * kb, owner));
                 bulk_commit();
             }
         }
-        if (s > 0) load_step(dir > 0 ? s - 1 : T - s, (k_done + 1) & 1);
         TRACE(5);
     }
 #undef TRACE
@@ -825,21 +888,21 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         dbp[k] += __shfl_xor_sync(0xffffffffu, dbp[k], 1);
         dbp[k] += __shfl_xor_sync(0xffffffffu, dbp[k], 2);
     }
-    float *dbs = reinterpret_cast<float *>(dAs);  // [4 cb][128 rows]; the last MMA has completed
-    __syncthreads();
+    float *dbs = reinterpret_cast<float *>(dAs);  // [4 cb][128 rows] (2 KB <= dAs); the last MMA is done
+    cluster_sync();  // the partner's last st.async into dAs (and its MMA reads) are complete
     dbs[cb * 128 + 4 * jl + gam] = sel4(dbp, gam);
     __syncthreads();
     if (cb == 0) {
         const int r = 4 * jl + gam;
         p.dbpart[((long)d * p.G + g) * 4 * Hq + 4 * j + gam] = ((dbs[r] + dbs[128 + r]) + dbs[256 + r]) + dbs[384 + r];
     }
-    if (l == 0 && w < NC) bulk_wait_read<0>();  // outgoing copies done with the staging buffers
+    if (l == 0 && w < NSRC) bulk_wait_read<0>();  // outgoing copies done with the staging buffers
     tc_fence_before();
     __syncthreads();
-    cluster_sync();  // no peer still writes into this CTA's slots
+    cluster_sync();  // no peer still writes into this CTA's slots; both CTAs of the pair are done
     if (w == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem, TCOLS);
+        tmem_dealloc2(tmem, TCOLS);
     }
 }
 
@@ -852,7 +915,7 @@ static int mma_n(int Bg) { return Bg <= 16 ? 16 : Bg <= 32 ? 32 : round_up(Bg, 6
 RecPlan rec_plan(int T, int B, int H, int ndir, int sms) {
     (void)T;
     RecPlan pl{};
-    pl.Hq = round_up(H, 128);
+    pl.Hq = round_up(H, 256);  // BPTT pair tiles are 256 units (two CTAs x 128)
     pl.NC = pl.Hq / REC_UNITS;
     pl.ndir = ndir;
     int bestG = 1, bestN = 1 << 30;
@@ -868,8 +931,8 @@ RecPlan rec_plan(int T, int B, int H, int ndir, int sms) {
 }
 
 static size_t fwd_smem(const RecPlan &pl) { return fwd_region0(pl.Hq, pl.N) + 1024 + 64; }
-// per-step input ring of the BPTT kernel (2 slots; see IN_SLOT there)
-static size_t bwd_in_bytes(int N) { return 2 * ((size_t)512 * (N / 4) * 2 + 3 * (size_t)(N / 16) * 512 * 4 + 256); }
+// per-step input rings of the BPTT kernel (see IN_SLOT / cring there)
+static size_t bwd_in_bytes(int N) { return 2 * ((size_t)N * 128 + 512 * (N / 4) * 2 + 1024) + 3 * (size_t)N * 128; }
 static size_t bwd_smem(const RecPlan &pl) {
     return bwd_region0(pl.Hq, pl.N, pl.NC) + 2 * pl.N * 128 + bwd_in_bytes(pl.N) + 1024 + 64;
 }
@@ -879,9 +942,8 @@ bool rec_supported(const RecPlan &pl, int H) {
     if (pl.NC > 16) return false;  // one cluster (<= 16 CTAs, non-portable size) per group
     if (fwd_smem(pl) > 227 * 1024 || bwd_smem(pl) > 227 * 1024) return false;
     if (pl.ndir * pl.G * pl.NC > num_sms()) return false;
-    const int nacc = pl.Hq / 128 > 4 ? pl.Hq / 128 : 4;  // forward: 4 K-split accumulators
-    if (pl.Hq / 2 + nacc * pl.N > 512) return false;     // TMEM: resident R + accumulators
-    return pl.Hq % 128 == 0;
+    if (pl.Hq / 2 + 4 * pl.N > 512) return false;  // TMEM: resident R + 4 accumulators (both kernels)
+    return pl.Hq == 256 || pl.Hq == 512;  // one cluster of <= 16 CTAs; BPTT tiles of 256 units
 }
 
 size_t rec_P_bytes(const RecPlan &pl) {
@@ -942,20 +1004,26 @@ int lstm_rec_fwd(const RecParams &p_in, const __half *RT16, cudaStream_t st) {
 int lstm_rec_bwd(const RecParams &p_in, const __half *RT16, cudaStream_t st) {
     RecParams p = p_in;
     if (g_trace_bwd) p.trace = g_trace_bwd;
-    CUtensorMap tmR;
+    if (p.T == 0) return 0;
+    CUtensorMap tmR, tmC, tmDY;
     if (make_tmap_f16(&tmR, RT16, p.Hq, (uint64_t)p.ndir * 4 * p.Hq, p.Hq, 128)) return -2;
+    // c and dy tiles [N rows][32 units] by TMA: C rows = ndir blocks of c_doff/ldc rows (or T*B)
+    const uint64_t crows = p.c_doff ? (uint64_t)(p.ndir - 1) * (p.c_doff / p.ldc) + (uint64_t)p.T * p.B
+                                    : (uint64_t)p.T * p.B;
+    if (make_tmap_f32_rows(&tmC, p.C, p.ldc, crows, p.ldc, p.N)) return -3;
+    if (make_tmap_f32_rows(&tmDY, p.dy, p.lddy, (uint64_t)p.T * p.B, p.lddy, p.N)) return -3;
     RecPlan pl{p.Hq, p.NC, p.G, p.Bg, p.N, p.ndir};
     const int grid = p.ndir * p.G * p.NC;
     const size_t smem = bwd_smem(pl);
     ProfScope ps(PROF_REC_BWD, st);
     note_launch();
     cudaError_t e;
-    switch (p.N) {
-        case 16: e = launch_cluster(lstm_rec_bwd_kernel<1>, grid, p.NC, smem, st, tmR, p); break;
-        case 32: e = launch_cluster(lstm_rec_bwd_kernel<2>, grid, p.NC, smem, st, tmR, p); break;
-        case 64: e = launch_cluster(lstm_rec_bwd_kernel<4>, grid, p.NC, smem, st, tmR, p); break;
-        default: return -6;
-    }
+#define BWD_CASE(n, mt2)                                                                                  \
+    if (p.N == 16 * (n) && p.Hq == 256 * (mt2)) {                                                         \
+        e = launch_cluster(lstm_rec_bwd_kernel<n, mt2>, grid, p.NC, smem, st, tmR, tmC, tmDY, p);         \
+    } else
+    BWD_CASE(1, 1) BWD_CASE(2, 1) BWD_CASE(4, 1) BWD_CASE(1, 2) BWD_CASE(2, 2) BWD_CASE(4, 2) { return -6; }
+#undef BWD_CASE
     return e == cudaSuccess ? 0 : -5;
 }
 

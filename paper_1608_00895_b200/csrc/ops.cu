@@ -341,6 +341,22 @@ int pack_mask(const uint8_t *mask, int T, int B, int G, int Bg, int N, uint8_t *
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
+__global__ void copy_rows_kernel(const float *__restrict__ src, long lds, long rows, int cols,
+                                 float *__restrict__ dst, long ldd) {
+    const long n = rows * cols;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long r = i / cols;
+        const int j = (int)(i - r * cols);
+        dst[r * ldd + j] = src[r * lds + j];
+    }
+}
+int copy_rows(const float *src, long lds, long rows, int cols, float *dst, long ldd, cudaStream_t st) {
+    if (rows * cols == 0) return 0;
+    copy_rows_kernel<<<grid_for(rows * cols), 256, 0, st>>>(src, lds, rows, cols, dst, ldd);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 __global__ void pad_halves_kernel(const float *__restrict__ src, int H, int Hq, long rows, float *__restrict__ dst) {
     const long n = rows * 2 * Hq;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {

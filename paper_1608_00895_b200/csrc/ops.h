@@ -31,6 +31,8 @@ int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, 
 // recurrence kernels' mask rows: maskN[(t*G + g)*N + n] = mask[t*B + g*Bg + n] for n < Bg,
 // g*Bg + n < B, else 0 (one N-byte row per step and batch group, bulk-copyable)
 int pack_mask(const uint8_t *mask, int T, int B, int G, int Bg, int N, uint8_t *maskN, cudaStream_t st);
+// dst[r*ldd + j] = src[r*lds + j] for j < cols (a row-strided copy into an aligned buffer)
+int copy_rows(const float *src, long lds, long rows, int cols, float *dst, long ldd, cudaStream_t st);
 int pad_halves(const float *src, int H, int Hq, long rows, float *dst, cudaStream_t st);
 int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, int accum, cudaStream_t st);
 int sgd(float *theta, float *grad, long n, float lr, int zero, cudaStream_t st);
