@@ -127,6 +127,8 @@ template <int N>
 DEVI void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+// order this thread's (acquired) view of global memory before its later async-proxy reads of it
+DEVI void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 DEVI void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 DEVI void bulk_wait_read() {

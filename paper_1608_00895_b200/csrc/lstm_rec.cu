@@ -136,8 +136,11 @@ DEVI float gate_act(float pre, int gam) {
 //            at ((k/8)*N/2 + n')*16 + (k%8)*2, so CTA c's units [32c, 32c+32) are one contiguous
 //            32N-byte block
 //   stg[b][h]: this CTA's h slice, column half h, in that block format (sent to the CTAs of parity h)
+//   zin[2]: the CTA's Z block of a step (CTA-native, 512N bytes) + its mask row (N bytes, padded
+//           to 128), bulk-copied by one thread one step ahead (per-thread loads cost ~0.27 us/step)
 static __host__ __device__ size_t fwd_region0(int Hq, int N) {
-    const size_t rs = (size_t)Hq / 64 * 16384, hb = (size_t)Hq * N * 2 + 2 * 64 * (size_t)N;
+    const size_t rs = (size_t)Hq / 64 * 16384,
+                 hb = (size_t)Hq * N * 2 + 2 * 64 * (size_t)N + 2 * (512 * (size_t)N + 128);
     return rs > hb ? rs : hb;
 }
 
@@ -156,10 +159,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     uint8_t *Rs = smem;
     uint8_t *hbuf = smem;            // aliases Rs after the TMEM load
     uint8_t *stg = smem + 2 * HB;    // [2 b][2 halves][SGh]
+    constexpr uint32_t ZB = 512 * N, ZSLOT = ZB + 128;  // Z block + mask row
+    uint8_t *zin = stg + 4 * SGh;    // [2][ZSLOT]
     // [0] tma, [1] mma (arrived by the pair's commits), [2..3] full[b] (own half of h landed),
-    // [4..5] pfull[b] (even CTA: the odd CTA's half landed)
+    // [4..5] pfull[b] (even CTA: the odd CTA's half landed), [6..7] zfull[slot] (Z + mask landed)
     uint64_t *bars = (uint64_t *)(smem + fwd_region0(Hq, N));
-    uint32_t *tslot = (uint32_t *)(bars + 6);
+    uint32_t *tslot = (uint32_t *)(bars + 8);
 
     // this CTA is resident: a programmatically dependent launch (the concurrent Z GEMM, gemm.h pdl)
     // may start on the SMs left free once every CTA of this grid got here
@@ -195,6 +200,8 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         mbar_init(&bars[3], 1);
         mbar_init(&bars[4], 1);
         mbar_init(&bars[5], 1);
+        mbar_init(&bars[6], 1);
+        mbar_init(&bars[7], 1);
         fence_mbar_init();
     }
     if (w == 0) {  // one warp of each CTA of the pair
@@ -274,7 +281,10 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             zfront += dir;
         }
     };
-    if (zf && threadIdx.x == ZPOLL && T > 0) z_wait(dir > 0 ? 0 : T - 1);
+    if (zf && threadIdx.x == ZPOLL && T > 0) {
+        z_wait(dir > 0 ? 0 : T - 1);
+        if (T > 1) z_wait(dir > 0 ? 1 : T - 2);
+    }
     cluster_sync();  // every CTA done with its R staging before peers write into hbuf / stg
 
     float c_st[NMQ], h_st[NMQ];
@@ -289,19 +299,21 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     // CTA-native layout of Z and of the saved gates (lstm_rec.h): this thread's NQ values of step t
     // are contiguous, and the warp's 32 x NQ values form one contiguous block
     const long nat_step = (long)p.ndir * p.G * NC * 512 * NQ;
-    const long nat_off = (((long)d * p.G + g) * NC + c) * 512 * NQ + ((long)cb * 128 + 32 * q + l) * NQ;
-    float zv[NQ];
-    uint32_t mraw = 0;  // mask byte of column l (lane l < NQ) of the prefetched step
-    auto prefetch_z = [&](int t) {
-        const float4 *zp = reinterpret_cast<const float4 *>(p.Z + t * nat_step + nat_off);
-#pragma unroll
-        for (int i = 0; i < NQ / 4; ++i) {
-            const float4 v = __ldcg(zp + i);  // L2-coherent: Z may have been written during this kernel
-            zv[4 * i] = v.x; zv[4 * i + 1] = v.y; zv[4 * i + 2] = v.z; zv[4 * i + 3] = v.w;
-        }
-        mraw = (l < NQ && ((cm >> l) & 1)) ? p.mask[(long)t * B + bq0 + l] : 0;
+    const long nat_cta = (((long)d * p.G + g) * NC + c) * 512 * NQ;
+    const long nat_off = nat_cta + ((long)cb * 128 + 32 * q + l) * NQ;
+    // step s2's Z block + mask row -> zin[s2 & 1] (thread 0); the slot was last read at step s2-2.
+    // The bulk copy engine serves these behind this CTA's h sends of the previous step.
+    auto issue_z = [&](int s2) {
+        const int t2 = dir > 0 ? s2 : T - 1 - s2, sl = s2 & 1;
+        mbar_arrive_expect_tx(&bars[6 + sl], ZB + N);
+        bulk_g2s(smem_u32(zin + sl * ZSLOT), p.Z + t2 * nat_step + nat_cta, ZB, &bars[6 + sl]);
+        bulk_g2s(smem_u32(zin + sl * ZSLOT + ZB), p.maskN + ((long)t2 * p.G + g) * N, N, &bars[6 + sl]);
     };
-    if (T > 0) prefetch_z(dir > 0 ? 0 : T - 1);
+    if (threadIdx.x == ZPOLL && T > 0) {  // verified ready above (zf)
+        fence_proxy_async_global();
+        issue_z(0);
+        if (T > 1) issue_z(1);
+    }
 
     const uint32_t hbuf_addr = smem_u32(hbuf), stg_addr = smem_u32(stg);
     const uint32_t full_addr = smem_u32(&bars[2]);
@@ -353,10 +365,15 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         const int t = dir > 0 ? s : T - 1 - s;
         const int b = s & 1;
         TRACE(0);
-        // the next step's Z: issue the acquire load of the frontier M-tile now, check it before this
+        // Z of step s+1 (verified during step s-1) -> its ring slot, last read at step s-1
+        if (threadIdx.x == ZPOLL && s >= 1 && s + 1 < T) {
+            fence_proxy_async_global();  // generic writes acquired from the GEMM -> bulk-copy reads
+            issue_z(s + 1);
+        }
+        // Z of step s+2: issue the acquire load of the frontier M-tile now, check it before this
         // step's __syncthreads (its latency hides behind the step)
-        const bool zcheck = zf && threadIdx.x == ZPOLL && s + 1 < T &&
-                            (dir > 0 ? zfront <= z_tile_of(t + 1) : zfront >= z_tile_of(t - 1));
+        const bool zcheck = zf && threadIdx.x == ZPOLL && s + 2 < T &&
+                            (dir > 0 ? zfront <= z_tile_of(t + 2) : zfront >= z_tile_of(t - 2));
         uint32_t zseen = 0;
         if (zcheck) zseen = ld_acquire_gpu(zf + zfront);
         if (pr == 0 && w < NISSUE) {  // warp-collective issue of the pair MMA (one elected lane)
@@ -381,8 +398,11 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         }
         if (s > 0) fph ^= 1u << b;
         if (s > 0) store_step(t_prev, frm_prev, fmq_prev);
-        // frame-valid bits of this warp's columns (lane i holds the prefetched mask of column i)
-        const uint32_t frm = __ballot_sync(0xffffffffu, mraw != 0);
+        // this step's Z block and mask row (issued two steps ahead)
+        mbar_wait(&bars[6 + b], (s >> 1) & 1);
+        const uint8_t *zs = zin + b * ZSLOT;
+        // frame-valid bits of this warp's columns (lane i reads the mask byte of column i)
+        const uint32_t frm = __ballot_sync(0xffffffffu, l < NQ && zs[ZB + nq0 + l] != 0);
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
@@ -390,6 +410,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 
         {
             uint32_t v[NISSUE][NQ];
+            float zv[NQ];
+#pragma unroll
+            for (int i = 0; i < NQ / 4; ++i) {
+                const float4 z4 = reinterpret_cast<const float4 *>(zs)[((cb * 128 + 32 * q + l) * NQ) / 4 + i];
+                zv[4 * i] = z4.x; zv[4 * i + 1] = z4.y; zv[4 * i + 2] = z4.z; zv[4 * i + 3] = z4.w;
+            }
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + DCOL + nq0;
 #pragma unroll
             for (int k4 = 0; k4 < NISSUE; ++k4) tmem_ld_nowait<NQ>(ta + k4 * N, v[k4]);
@@ -434,7 +460,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         if (zcheck) {
             if (zseen < (uint32_t)p.zflag_target) spin_until_geq(zf + zfront, (uint32_t)p.zflag_target);
             zfront += dir;
-            z_wait(dir > 0 ? t + 1 : t - 1);  // rare: the step spans a further M-tile
+            z_wait(dir > 0 ? t + 2 : t - 2);  // rare: the step spans a further M-tile
         }
         // the previous step's bulk copies (of the other staging buffer) have long finished reading;
         // this __syncthreads orders that before the rewrite of that buffer at the next step
@@ -453,7 +479,6 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         t_prev = t;
         frm_prev = frm;
         fmq_prev = fmq;
-        if (s + 1 < T) prefetch_z(dir > 0 ? t + 1 : t - 1);
         TRACE(6);
     }
     if (T > 0) store_step(t_prev, frm_prev, fmq_prev);
