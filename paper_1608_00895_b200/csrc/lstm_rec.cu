@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     };
     const long nat_step = (long)p.ndir * p.G * NC * 512 * NQ;
 
-    // saved state of one step (independent of the recurrence), one step ahead: thread 0 issues the
+    // saved state of one step (independent of the recurrence), one step ahead: one thread issues the
     // copies for processing index k into ring slot k&1, and c(t_{k+1}) into cring[(k+1)%3]
     const int tid = threadIdx.x;
     const long nat_cta = (((long)d * p.G + g) * NC + c) * 512 * NQ;
@@ -711,7 +711,8 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         if (with_c0) tma_load_2d(cring + (k % 3) * TILE, &tmC, &bars[6 + sl], 32 * c, d * crows + tk * B + b0);
         if (cnext) tma_load_2d(cring + ((k + 1) % 3) * TILE, &tmC, &bars[6 + sl], 32 * c, d * crows + t_of(k + 1) * B + b0);
     };
-    if (threadIdx.x == 0 && T > 0) {
+    constexpr int IN_THREAD = 128;  // lane 0 of warp 4: not an MMA-issuing warp
+    if (threadIdx.x == IN_THREAD && T > 0) {
         tma_prefetch_desc(&tmC);
         tma_prefetch_desc(&tmDY);
         issue_in(0, true);
@@ -743,7 +744,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         const int k_done = T - 1 - s;
         TRACE(0);
         // the next step's inputs: its ring slots were last read one step ago
-        if (threadIdx.x == 0 && k_done + 1 < T) issue_in(k_done + 1, false);
+        if (threadIdx.x == IN_THREAD && k_done + 1 < T) issue_in(k_done + 1, false);
         TRACE(1);
         // ---- dh_t from the previous step's partials ----
         if (k_done > 0) gather(k_done);
