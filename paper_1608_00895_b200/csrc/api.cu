@@ -512,29 +512,6 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     const float a = 1.f / (float)(1 << DA_SHIFT);
     float *dY[2] = {(float *)(ws + w.dY0), (float *)(ws + w.dY1)};
     const __half *ytop = (const __half *)(ws + w.y16[g.L - 1]);
-    if (g.K > 0) {
-        __half *wo16 = (__half *)(ws + w.wo16), *dlog = (__half *)(ws + w.dlog16);
-        float *boq = (float *)(ws + w.boq), *logits = (float *)(ws + w.Z), *dWoT = (float *)(ws + w.dWoT);
-        TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, Hq, g.K, g.Kp, wo16, boq, st), "pack_wout");
-        GemmParams gl{(int)g.TB, g.K, 2 * Hq, logits, g.Kp, 1.f, 0, boq, 0, 0};
-        TRY(gemm_f16({ytop, 2L * Hq, 0}, {wo16, g.Kp, 1}, gl, 0, st), "gemm logits");
-        TRY(ce_head(logits, g.Kp, g.K, g.Kp, mask, labels, (float)(1 << DA_SHIFT), dlog, (double *)(ws + w.rowloss),
-                    (int32_t *)(ws + w.rowerr), g.TB, st), "ce_head");
-        TRY(reduce_loss((double *)(ws + w.rowloss), (int32_t *)(ws + w.rowerr), g.TB, loss_sum, frame_errors, st),
-            "reduce_loss");
-        GemmParams gd{(int)g.TB, 2 * Hq, g.Kp, dY[0], 2L * Hq, a, 0, nullptr, 0, 0};
-        TRY(gemm_f16({dlog, g.Kp, 0}, {wo16, g.Kp, 0}, gd, 0, st), "gemm dY_top");
-        GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
-        TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, 0, st), "gemm dW_out");
-        TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, st), "scatter dW_out");
-        TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), st), "db_out");
-    } else {
-        TRY(pad_halves(dy_top, g.H, Hq, g.TB, dY[0], st), "pad dy_top");
-        if (cudaMemsetAsync(loss_sum, 0, sizeof(double), st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
-        if (frame_errors && cudaMemsetAsync(frame_errors, 0, sizeof(int32_t), st) != cudaSuccess)
-            return fail(BLSTM_ERR_CUDA, "memset");
-    }
-
     // Weight gradients (dW, dR, db) of layer l are off the critical path (PAPER.md P:233-234 only
     // needs them after BPTT of layer l): with a side stream they run on the SMs the recurrence
     // clusters leave free, overlapping BPTT of layer l-1.  Their inputs (dA, dbpart) and scratch
@@ -553,10 +530,38 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             evs.push_back(e);
         }
     }
-    if (overlap) {  // the side stream may start only after everything issued so far on s_main
+    if (overlap && g.K == 0) {  // the side stream may start only after everything issued so far on s_main
         cudaEventRecord(evs[g.L + 1], st);
         cudaStreamWaitEvent(side, evs[g.L + 1], 0);
     }
+    if (g.K > 0) {
+        __half *wo16 = (__half *)(ws + w.wo16), *dlog = (__half *)(ws + w.dlog16);
+        float *boq = (float *)(ws + w.boq), *logits = (float *)(ws + w.Z), *dWoT = (float *)(ws + w.dWoT);
+        TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, Hq, g.K, g.Kp, wo16, boq, st), "pack_wout");
+        GemmParams gl{(int)g.TB, g.K, 2 * Hq, logits, g.Kp, 1.f, 0, boq, 0, 0};
+        TRY(gemm_f16({ytop, 2L * Hq, 0}, {wo16, g.Kp, 1}, gl, 0, st), "gemm logits");
+        TRY(ce_head(logits, g.Kp, g.K, g.Kp, mask, labels, (float)(1 << DA_SHIFT), dlog, (double *)(ws + w.rowloss),
+                    (int32_t *)(ws + w.rowerr), g.TB, st), "ce_head");
+        TRY(reduce_loss((double *)(ws + w.rowloss), (int32_t *)(ws + w.rowerr), g.TB, loss_sum, frame_errors, st),
+            "reduce_loss");
+        GemmParams gd{(int)g.TB, 2 * Hq, g.Kp, dY[0], 2L * Hq, a, 0, nullptr, 0, 0};
+        TRY(gemm_f16({dlog, g.Kp, 0}, {wo16, g.Kp, 0}, gd, 0, st), "gemm dY_top");
+        // the head's parameter gradients are off the critical path too: side stream
+        if (overlap) {
+            cudaEventRecord(evs[g.L + 1], st);
+            cudaStreamWaitEvent(side, evs[g.L + 1], 0);
+        }
+        GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
+        TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
+        TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
+        TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
+    } else {
+        TRY(pad_halves(dy_top, g.H, Hq, g.TB, dY[0], st), "pad dy_top");
+        if (cudaMemsetAsync(loss_sum, 0, sizeof(double), st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
+        if (frame_errors && cudaMemsetAsync(frame_errors, 0, sizeof(int32_t), st) != cudaSuccess)
+            return fail(BLSTM_ERR_CUDA, "memset");
+    }
+
     int cur = 0;
     for (int l = g.L - 1; l >= 0; --l) {
         const int par = l & 1;

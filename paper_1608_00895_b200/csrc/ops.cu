@@ -40,42 +40,60 @@ DEVI int src_row(int r, int Drows, int H, int Hq, int rowmode) {
 }
 
 // --- W_d [Drows, 4H] -> W16 [Dn, ndir*4Hq] with column 4j+gamma (+ d*4Hq) ------------------
+// one thread per (row, direction, unit j): the four gate reads are each coalesced across the warp
+// (consecutive j), the four fp16 results one 8-byte store
 __global__ void pack_w_kernel(const float *__restrict__ W0, const float *__restrict__ W1, int Drows, int H, int Hq,
                               int ndir, int Dn, int rowmode, __half *__restrict__ W16) {
-    const int cols = ndir * 4 * Hq;
-    const long n = (long)Dn * cols;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const int r = (int)(i / cols), col = (int)(i - (long)r * cols);
-        const int d = col / (4 * Hq), qq = col - d * 4 * Hq, j = qq >> 2, gam = qq & 3;
-        const int sr = src_row(r, Drows, H, Hq, rowmode);
-        const float *W = d == 0 ? W0 : W1;
-        float v = 0.f;
-        if (sr >= 0 && j < H) v = W[(long)sr * 4 * H + gam * H + j];
-        W16[i] = __float2half_rn(v);
+    const int r = blockIdx.y, d = blockIdx.z;
+    const int sr = src_row(r, Drows, H, Hq, rowmode);
+    const float *W = d == 0 ? W0 : W1;
+    __half *out = W16 + (long)r * ndir * 4 * Hq + (long)d * 4 * Hq;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < Hq; j += gridDim.x * blockDim.x) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (sr >= 0 && j < H) {
+#pragma unroll
+            for (int gam = 0; gam < 4; ++gam) v[gam] = W[(long)sr * 4 * H + gam * H + j];
+        }
+        __half2 lo = __floats2half2_rn(v[0], v[1]), hi = __floats2half2_rn(v[2], v[3]);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t *>(&lo);
+        pk.y = *reinterpret_cast<uint32_t *>(&hi);
+        *reinterpret_cast<uint2 *>(out + 4 * j) = pk;
     }
 }
 int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir, int Dn, int rowmode, __half *W16,
            cudaStream_t st) {
-    pack_w_kernel<<<grid_for((long)Dn * ndir * 4 * Hq), 256, 0, st>>>(W0, W1, Drows, H, Hq, ndir, Dn, rowmode, W16);
+    dim3 grid((Hq + 255) / 256, Dn, ndir);
+    pack_w_kernel<<<grid, 256, 0, st>>>(W0, W1, Drows, H, Hq, ndir, Dn, rowmode, W16);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
 // --- R_d [H, 4H] -> RT16 [ndir][4Hq][Hq]: row 4j+gamma, col k --------------------------------
-__global__ void pack_rt_kernel(const float *__restrict__ R0, const float *__restrict__ R1, int H, int Hq, int ndir,
-                               __half *__restrict__ RT16) {
-    const long n = (long)ndir * 4 * Hq * Hq;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const long row = i / Hq;
-        const int k = (int)(i - row * Hq);
-        const int d = (int)(row / (4 * Hq)), qq = (int)(row - (long)d * 4 * Hq), j = qq >> 2, gam = qq & 3;
-        const float *R = d == 0 ? R0 : R1;
-        const float v = (j < H && k < H) ? R[(long)k * 4 * H + gam * H + j] : 0.f;
-        RT16[i] = __float2half_rn(v);
+// a transpose: 32 k x 32 j tiles through shared memory, reads coalesced along j (R's rows) and
+// writes coalesced along k (RT16's rows)
+__global__ void __launch_bounds__(256) pack_rt_kernel(const float *__restrict__ R0, const float *__restrict__ R1, int H,
+                                                      int Hq, int ndir, __half *__restrict__ RT16) {
+    __shared__ float tile[4][32][33];
+    const int k0 = blockIdx.x * 32, j0 = blockIdx.y * 32, d = blockIdx.z;
+    const float *R = d == 0 ? R0 : R1;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int kk = ty; kk < 32; kk += 8) {
+        const int k = k0 + kk, j = j0 + tx;
+#pragma unroll
+        for (int gam = 0; gam < 4; ++gam)
+            tile[gam][kk][tx] = (k < H && j < H) ? R[(long)k * 4 * H + gam * H + j] : 0.f;
+    }
+    __syncthreads();
+    // output rows 4j + gam for j in the tile (128 rows), 32 k each
+    for (int rr = ty; rr < 128; rr += 8) {
+        const int jj = rr >> 2, gam = rr & 3;
+        RT16[((long)d * 4 * Hq + 4 * (j0 + jj) + gam) * Hq + k0 + tx] = __float2half_rn(tile[gam][tx][jj]);
     }
 }
 int pack_rt(const float *R0, const float *R1, int H, int Hq, int ndir, __half *RT16, cudaStream_t st) {
-    pack_rt_kernel<<<grid_for((long)ndir * 4 * Hq * Hq), 256, 0, st>>>(R0, R1, H, Hq, ndir, RT16);
+    dim3 grid(Hq / 32, Hq / 32, ndir);
+    pack_rt_kernel<<<grid, 256, 0, st>>>(R0, R1, H, Hq, ndir, RT16);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
