@@ -66,11 +66,14 @@ struct LayerGeo {
     long TB;
     RecPlan pl;
 };
+// split-K scratch of the weight-gradient GEMMs (GemmParams::splitk_ws): 32 MB
+constexpr long GSK_ELEMS = 8L << 20;
+
 struct FwdWS {
     size_t x16, w16, rt16, bq, Z, maskN, cnt, total;
 };
 struct BwdWS {
-    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cpk, dypk, cnt, total;
+    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cpk, dypk, gsk, cnt, total;
 };
 struct Reserve {
     size_t gates, hist, total;
@@ -123,6 +126,7 @@ static BwdWS bwd_ws(const LayerGeo &g) {
     // them by TMA)
     w.cpk = c.take((size_t)g.TB * g.Hq * 4);
     w.dypk = c.take((size_t)g.TB * g.Hq * 4);
+    w.gsk = c.take((size_t)GSK_ELEMS * 4);
     w.cnt = c.take(256);
     w.total = c.off;
     return w;
@@ -267,11 +271,13 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     }
     {
         GemmParams gp{4 * g.Hq, g.Dp, (int)g.TB, dWT, g.Dp, a, 0, nullptr, 0, 0};
+        gp.splitk_ws = (float *)(ws + w.gsk); gp.splitk_elems = GSK_ELEMS;
         TRY(gemm_f16({dA, 4L * g.Hq, 1}, {x16, g.Dp, 1}, gp, 0, st), "gemm dW");
     }
     {
         const __half *hprev = (const __half *)(res + rv.hist) + (d->direction < 0 ? (long)g.B * g.Hq : 0);
         GemmParams gp{4 * g.Hq, g.Hq, (int)g.TB, dRT, g.Hq, a, 0, nullptr, 0, 0};
+        gp.splitk_ws = (float *)(ws + w.gsk); gp.splitk_elems = GSK_ELEMS;
         TRY(gemm_f16({dA, 4L * g.Hq, 1}, {hprev, g.Hq, 1}, gp, 0, st), "gemm dR");
     }
     TRY(scatter_w(dW, g.D, g.H, g.Hq, dWT, g.Dp, 0, 0, st), "scatter dW");
@@ -290,7 +296,8 @@ struct StackGeo {
     std::vector<int> Dn, Drows, rowmode;
 };
 struct StackWS {
-    size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, total;
+    size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, gsk,
+        total;
     size_t maxDn;
     std::vector<size_t> y16, w16, rt16, bq, gates, C, hist;
 };
@@ -360,6 +367,7 @@ static StackWS stack_ws(const StackGeo &g) {
     w.rowloss = c.take((size_t)TB * 8);
     w.rowerr = c.take((size_t)TB * 4);
     w.cs = c.take(colsum_scratch_bytes(TB, g.K ? g.K : 1));
+    w.gsk = c.take((size_t)GSK_ELEMS * 4);
     w.total = c.off;
     return w;
 }
@@ -552,6 +560,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             cudaStreamWaitEvent(side, evs[g.L + 1], 0);
         }
         GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
+        gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
         TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
         TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
         TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
@@ -591,13 +600,17 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             cudaStreamWaitEvent(side, evs[l], 0);
         }
         const __half *X = l == 0 ? (const __half *)(ws + w.x16) : (const __half *)(ws + w.y16[l - 1]);
+        // the last layer's weight gradients run after all BPTT work: every SM is free then
+        const int wctas = l == 0 ? 0 : side_ctas;
         GemmParams gw{8 * Hq, g.Dn[l], (int)g.TB, dWT, g.Dn[l], a, 0, nullptr, 0, 0};
-        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, side_ctas, side), "gemm dW");
+        gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
+        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, wctas, side), "gemm dW");
         const __half *hist = (const __half *)(ws + w.hist[l]);
         for (int dd = 0; dd < 2; ++dd) {
             const __half *hprev = hist + ((long)dd * (g.T + 1) + dd) * g.B * Hq;
             GemmParams gr{4 * Hq, Hq, (int)g.TB, dRT + (size_t)dd * 4 * Hq * Hq, Hq, a, 0, nullptr, 0, 0};
-            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, side_ctas, side), "gemm dR");
+            gr.splitk_ws = (float *)(ws + w.gsk); gr.splitk_elems = GSK_ELEMS;
+            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, wctas, side), "gemm dR");
         }
         for (int dd = 0; dd < 2; ++dd) {
             const int e = 6 * l + 3 * dd;

@@ -72,6 +72,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int num_n = (p.N + BN - 1) / BN;
     const int num_tiles = num_m * num_n;
     const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+    // split-K: work item = (split, tile); split s covers k-blocks [s*kbs, min(num_kb, (s+1)*kbs))
+    const int kbs = (num_kb + p.ksplit - 1) / p.ksplit;
+    const int num_items = num_tiles * p.ksplit;
 
     if (warp == 0 && lane_id() == 0) {
         tma_prefetch_desc(&tmA);
@@ -100,11 +103,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
+                const int split = item / num_tiles, tile = item - split * num_tiles;
                 int mt, nt;
                 tile_coords<BN>(tile, num_m, p, mt, nt);
                 const int m0 = mt * GEMM_BM, n0 = nt * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                const int kb1 = min(num_kb, (split + 1) * kbs);
+                for (int kb = split * kbs; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
                     uint8_t *sb = sa + Cfg::A_BYTES;
@@ -134,11 +139,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
+            const int split = item / num_tiles;
+            const int kb0 = split * kbs, kb1 = min(num_kb, (split + 1) * kbs);
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < num_kb; ++kb) {
+            for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 {  // warp-collective issue (one elected lane), operands warp-uniform
@@ -150,10 +157,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                                                  : sdesc_sw128(sa + kk * 32, 16, 1024);
                         const uint64_t bd = b_mn ? sdesc_sw128(sb + kk * 2048, 8192, 1024)
                                                  : sdesc_sw128(sb + kk * 32, 16, 1024);
-                        mma_f16_ss_w(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                        mma_f16_ss_w(d_tmem, ad, bd, idesc, (kb != kb0) | (kk != 0));
                     }
                     mma_commit_w(&empty[stage]);
-                    if (kb == num_kb - 1) mma_commit_w(&tfull[acc]);
+                    if (kb == kb1 - 1) mma_commit_w(&tfull[acc]);
                 }
                 __syncwarp();
                 if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
@@ -169,10 +176,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float *sbias = reinterpret_cast<float *>(tmem_slot + 4);  // [2][BN], one per accumulator
         const int et = threadIdx.x - 64;                           // 0..255 over the epilogue warps
         const int chalf = (warp - 2) / 4;                          // column half of this warp
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
+            const int split = item / num_tiles, tile = item - split * num_tiles;
             int mt, nt;
             tile_coords<BN>(tile, num_m, p, mt, nt);
             const int m0 = mt * GEMM_BM, n0 = nt * BN;
+            float *Cbase = p.C + split * p.split_stride;
             // this tile's bias slice -> shared memory while the MMAs run (a global load per
             // element in the store loop stalled the epilogue on L2 latency)
             for (int k = et; k < BN; k += 32 * GEMM_EPI_WARPS)
@@ -182,7 +191,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int m = m0 + row_in_tile;
-            float *crow = p.C + (size_t)m * p.ldc;
+            float *crow = Cbase + (size_t)m * p.ldc;
 #pragma unroll 1
             for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 16) {
                 float v[16];
@@ -336,7 +345,7 @@ static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, con
                                cudaStream_t st) {
     using Cfg = GemmCfg<BN>;
     if (cudaError_t e = gemm_setup<BN>()) return e;
-    const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
+    const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN) * p.ksplit;
     int grid = tiles < max_ctas ? tiles : max_ctas;
     if (grid < 1) grid = 1;
     ProfScope ps(PROF_GEMM, st);
@@ -358,6 +367,21 @@ static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, con
     return cudaLaunchKernelEx(&cfg, gemm_f16_kernel<BN>, ta, tb, p);
 }
 
+// split-K reduction: C = alpha * sum_s part[s] (+C) (+bias), in fixed order
+__global__ void splitk_reduce_kernel(const float *__restrict__ part, int S, long stride, int M, int N, float *C,
+                                     long ldc, float alpha, int beta, const float *__restrict__ bias) {
+    const long n = (long)M * N;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long m = i / N;
+        const int c = (int)(i - m * N);
+        float acc = 0.f;
+        for (int s = 0; s < S; ++s) acc += part[s * stride + i];
+        float v = acc * alpha + (bias ? bias[c] : 0.f);
+        float *dst = C + m * ldc + c;
+        *dst = beta ? *dst + v : v;
+    }
+}
+
 // C = alpha * op(A) op(B)^T (+C) (+bias).  Returns 0 / negative error.
 int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, int max_ctas, cudaStream_t st) {
     GemmParams p = pin;
@@ -375,8 +399,34 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
     else rc = make_tmap_f16(&tb, B.ptr, p.N, p.K, B.ld, GEMM_BK);
     if (rc) return rc;
     if (max_ctas <= 0) max_ctas = num_sms();
-    cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, p, max_ctas, st) : launch_gemm<128>(ta, tb, p, max_ctas, st);
-    return e == cudaSuccess ? 0 : -5;
+    // split K when the output tiles leave at least half of the allowed CTAs idle
+    const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
+    const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+    int S = 1;
+    if (p.splitk_ws && !p.natB && !p.flags && tiles * 2 <= max_ctas && num_kb >= 32) {
+        S = max_ctas / tiles;
+        if (S > num_kb / 16) S = num_kb / 16;  // >= 16 k-blocks per split
+        if (S > 8) S = 8;
+        while (S > 1 && (long)S * p.M * p.N > p.splitk_elems) --S;
+        if (S > 1) S = (num_kb + (num_kb + S - 1) / S - 1) / ((num_kb + S - 1) / S);  // no empty split
+    }
+    GemmParams q = p;
+    if (S > 1) {
+        q.C = p.splitk_ws; q.ldc = p.N; q.alpha = 1.f; q.beta = 0; q.bias = nullptr;
+        q.ksplit = S; q.split_stride = (long)p.M * p.N;
+    }
+    cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, q, max_ctas, st) : launch_gemm<128>(ta, tb, q, max_ctas, st);
+    if (e != cudaSuccess) return -5;
+    if (S > 1) {
+        const long n = (long)p.M * p.N;
+        long g = (n + 255) / 256;
+        if (g > 148 * 8) g = 148 * 8;
+        splitk_reduce_kernel<<<(int)g, 256, 0, st>>>(p.splitk_ws, S, (long)p.M * p.N, p.M, p.N, p.C, p.ldc, p.alpha,
+                                                    p.beta, p.bias);
+        note_launch();
+        if (cudaGetLastError() != cudaSuccess) return -5;
+    }
+    return 0;
 }
 
 }  // namespace blstm

@@ -31,6 +31,13 @@ struct GemmParams {
     // launch as a programmatic dependent of the previous kernel in the stream (which triggers it
     // once all its CTAs are resident: lstm_rec_fwd), so the GEMM runs beside it on the free SMs
     int pdl = 0;
+    // != nullptr: split-K scratch (fp32, splitk_elems floats).  GEMMs with few output tiles and a long
+    // K (the weight gradients, K = T*B) split K over idle SMs; partial tiles land in the scratch and
+    // a fixed-order reduction writes C (deterministic).
+    float *splitk_ws = nullptr;
+    long splitk_elems = 0;
+    int ksplit = 1;          // set by gemm_f16
+    long split_stride = 0;   // set by gemm_f16: C offset of split s (elements)
 };
 
 constexpr int GEMM_BM_ROWS = 128;           // M tile
