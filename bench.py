@@ -65,20 +65,29 @@ def alg_flops_per_frame(cfg):
     return f
 
 
-def kernel_roofline(cat, total_ms, launches, cfg, V, peaks):
-    """achieved / peak of the dominant kernel category (per launch, algorithmic units)."""
+def z_flops_per_frame(cfg):
+    """the input projections (a1): 2 directions x 8*D_l*H per layer"""
+    return sum(2 * 8 * (cfg.D if l == 0 else 2 * cfg.H) * cfg.H for l in range(cfg.L))
+
+
+def kernel_roofline(cat, total_ms, launches, cfg, V, peaks, steps):
+    """achieved / peak of the dominant kernel category, in algorithmic units per launch.
+
+    Recurrence (cat 0/1): one launch per layer (both directions): 2*V*8H^2 FLOPs and 2*V*40H
+    bytes.  GEMMs (cat 2): all dense contractions of a step over all GEMM
+    launches of the step; with the Z GEMM overlapped beside the forward recurrence (DESIGN.md
+    5.4) its time is inside the lstm_rec_fwd scope, so its FLOPs are excluded here."""
     H = cfg.H
-    if cat in (0, 1):          # recurrence: one launch per layer, both directions
-        flops = 2 * V * 8 * H * H
-        bytes_ = 2 * V * 40 * H
-    else:                      # GEMMs: all dense contractions of the step
-        flops = V * (alg_flops_per_frame(cfg) - cfg.L * 2 * 16 * H * H)
-        bytes_ = None
     per_launch_s = total_ms / max(launches, 1) / 1e3
     if cat == 2:
-        per_flops = flops / max(launches, 1)
-        a = per_flops / per_launch_s / 1e12
-        return {"bound": "tensor", "achieved": a, "peak": peaks["tf"], "unit": "TFLOP/s", "frac": a / peaks["tf"]}
+        fl = alg_flops_per_frame(cfg) - cfg.L * 2 * 16 * H * H
+        if os.environ.get("BLSTM_OVERLAP", "1") != "0":
+            fl -= z_flops_per_frame(cfg)
+        a = V * fl * steps / (total_ms / 1e3) / 1e12
+        return {"bound": "tensor", "achieved": a, "peak": peaks["tf"], "unit": "TFLOP/s", "frac": a / peaks["tf"],
+                "note": "aggregate over the step's GEMM launches (several shapes)"}
+    flops = 2 * V * 8 * H * H
+    bytes_ = 2 * V * 40 * H
     a_tf = flops / per_launch_s / 1e12
     a_gb = bytes_ / per_launch_s / 1e9
     f_tf, f_gb = a_tf / peaks["tf"], a_gb / peaks["gbs"]
@@ -331,7 +340,7 @@ def main():
     peaks = measured_peaks()
     cats = {0: "lstm_rec_fwd", 1: "lstm_rec_bwd", 2: "gemm_f16 (all GEMMs)"}
     dom = max(prof, key=lambda c: prof[c][0])
-    roof = kernel_roofline(dom, prof[dom][0], prof[dom][1], cfg, tr.valid_frames, peaks)
+    roof = kernel_roofline(dom, prof[dom][0], prof[dom][1], cfg, tr.valid_frames, peaks, args.steps)
     tr_ncu = ncu_traffic({0: "lstm_rec_fwd_kernel", 1: "lstm_rec_bwd_kernel"}.get(dom, "-"))
     roof.update({"kernel": cats[dom], "traffic": tr_ncu["bytes"] if tr_ncu else None,
                  "traffic_unit": "bytes/launch (dram read + write)",
@@ -352,6 +361,8 @@ def main():
                        **({"avg_k": args.avg_k} if args.dp_mode == "avg" else {})),
         "roofline": roof,
         "kernel_ms_per_step": {cats[c]: prof[c][0] / args.steps for c in prof},
+        "roofline_by_kernel": {cats[c]: kernel_roofline(c, prof[c][0], prof[c][1], cfg, tr.valid_frames, peaks, args.steps)
+                               for c in prof},
         "step_tensor_bound_ms": t_tc,
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8},
