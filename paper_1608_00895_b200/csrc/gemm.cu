@@ -38,14 +38,17 @@ struct GemmCfg {
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
-// tile index -> (M-tile, N-tile).  Default: M fastest (consecutive CTAs share the B tile).  With
-// completion flags: round r visits, per direction d, all N-tiles of that direction at M-tile r
-// (ascending) or num_m-1-r (descending), so Z becomes complete in the order the recurrence reads it.
+// tile index -> (M-tile, N-tile).  Default: N fastest, so the N-tiles of one M block run on
+// neighbouring CTAs at about the same time and the (large) A operand streams from HBM once while
+// the (small) B operand stays in L2; M-fastest re-read A once per N-tile (the dX GEMM read 4x its
+// 166 MB A from DRAM).  With completion flags: round r visits, per direction d, all N-tiles of
+// that direction at M-tile r (ascending) or num_m-1-r (descending), so Z becomes complete in the
+// order the recurrence reads it.
 template <int BN>
-DEVI void tile_coords(int tile, int num_m, const GemmParams &p, int &mt, int &nt) {
+DEVI void tile_coords(int tile, int num_m, int num_n, const GemmParams &p, int &mt, int &nt) {
     if (!p.flags) {
-        mt = tile % num_m;
-        nt = tile / num_m;
+        mt = tile / num_n;
+        nt = tile - mt * num_n;
         return;
     }
     const int ntd = p.natHq4 / BN, per = p.natNdir * ntd;
@@ -106,7 +109,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
                 const int split = item / num_tiles, tile = item - split * num_tiles;
                 int mt, nt;
-                tile_coords<BN>(tile, num_m, p, mt, nt);
+                tile_coords<BN>(tile, num_m, num_n, p, mt, nt);
                 const int m0 = mt * GEMM_BM, n0 = nt * BN;
                 const int kb1 = min(num_kb, (split + 1) * kbs);
                 for (int kb = split * kbs; kb < kb1; ++kb) {
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
             const int split = item / num_tiles, tile = item - split * num_tiles;
             int mt, nt;
-            tile_coords<BN>(tile, num_m, p, mt, nt);
+            tile_coords<BN>(tile, num_m, num_n, p, mt, nt);
             const int m0 = mt * GEMM_BM, n0 = nt * BN;
             float *Cbase = p.C + split * p.split_stride;
             // this tile's bias slice -> shared memory while the MMAs run (a global load per
