@@ -34,7 +34,8 @@ struct GemmCfg {
     static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
     static constexpr int B_BYTES = BN * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 2 * BN * 4 /*bias*/;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 2 * BN * 4 /*bias*/ +
+                                      GEMM_EPI_WARPS * 2048 /*store staging*/;
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -179,6 +180,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float *sbias = reinterpret_cast<float *>(tmem_slot + 4);  // [2][BN], one per accumulator
         const int et = threadIdx.x - 64;                           // 0..255 over the epilogue warps
         const int chalf = (warp - 2) / 4;                          // column half of this warp
+        // row-major stores go through a per-warp [32 rows][16 cols] staging tile (float4 index
+        // XOR-swizzled by row) so each store instruction writes 8 rows x 64 contiguous bytes; direct
+        // per-lane row stores touched 32 rows x 16 B (half sectors), which bound the output-heavy GEMMs
+        float4 *stg4 = reinterpret_cast<float4 *>(sbias + 2 * BN) + (warp - 2) * 128;
+        const int lane = lane_id();
         for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
             const int split = item / num_tiles, tile = item - split * num_tiles;
             int mt, nt;
@@ -203,7 +209,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const int n = n0 + c;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = v[j] * p.alpha + bs[c + j];
-                if (m < p.M && n < p.N && p.natB) {
+                if (p.natB) {
+                    if (m >= p.M || n >= p.N) continue;
                     // CTA-native layout of the recurrence (see lstm_rec.h): the 16 columns stay in
                     // one 128-row block of one CTA, consecutive columns are NQ floats apart
                     const long t = m / p.natB, b = m - t * p.natB;
@@ -217,6 +224,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         if (n + j < p.N) base[(long)j * p.natNQ] = v[j];
+                } else if ((p.ldc & 3) == 0 && ((uintptr_t)Cbase & 15) == 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        stg4[lane * 4 + (k ^ (lane & 3))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int it = 0; it < 4; ++it) {
+                        const int r = 8 * it + (lane >> 2), k = lane & 3;
+                        float4 o = stg4[r * 4 + (k ^ (r & 3))];
+                        const int mm = m0 + 32 * q + r, nn = n + 4 * k;
+                        if (mm < p.M && nn < p.N) {
+                            float *dst = Cbase + (size_t)mm * p.ldc + nn;
+                            if (nn + 4 <= p.N) {
+                                if (p.beta) {
+                                    const float4 old = *reinterpret_cast<const float4 *>(dst);
+                                    o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+                                }
+                                *reinterpret_cast<float4 *>(dst) = o;
+                            } else {
+                                const float ov[4] = {o.x, o.y, o.z, o.w};
+                                for (int e = 0; e < p.N - nn; ++e) dst[e] = p.beta ? dst[e] + ov[e] : ov[e];
+                            }
+                        }
+                    }
+                    __syncwarp();
                 } else if (m < p.M && n < p.N) {
                     if (n + 16 <= p.N && (p.ldc & 3) == 0) {
 #pragma unroll
