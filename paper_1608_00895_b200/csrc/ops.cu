@@ -154,58 +154,54 @@ int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int nd
 // --- softmax cross-entropy over one frame per CTA ------------------------------------------
 // logits [rows, ldl] fp32 (K valid columns); writes dlog16 [rows, Kp] = 2^shift (softmax - onehot)
 // at valid frames (0 elsewhere), rowloss (double) and rowerr (argmax != label, lowest index on ties).
-constexpr int CE_THREADS = 256;
+constexpr int CE_THREADS = 256;  // 8 warps, one frame (row) per warp
+// one warp per frame: coalesced 128-byte reads of the logits row (re-reads hit L1), warp-shuffle
+// max / argmax (ties: lowest index) and sum, 16-byte fp16 stores of dlogits.  Per row:
+//   loss = lse - logit[label],  err = argmax != label,  dlog = (softmax - onehot) * scale
 __global__ void __launch_bounds__(CE_THREADS) ce_head_kernel(const float *__restrict__ logits, long ldl, int K, int Kp,
                                                              const uint8_t *__restrict__ mask,
                                                              const int32_t *__restrict__ labels, float scale,
                                                              __half *__restrict__ dlog16, double *__restrict__ rowloss,
-                                                             int32_t *__restrict__ rowerr) {
-    const long r = blockIdx.x;
+                                                             int32_t *__restrict__ rowerr, long rows) {
+    const long r = (long)blockIdx.x * (CE_THREADS / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
     __half *drow = dlog16 + r * Kp;
     if (!mask[r]) {
-        for (int k = threadIdx.x; k < Kp; k += CE_THREADS) drow[k] = __float2half_rn(0.f);
-        if (threadIdx.x == 0) { rowloss[r] = 0.0; rowerr[r] = 0; }
+        for (int k = lane * 8; k < Kp; k += 256) *reinterpret_cast<uint4 *>(drow + k) = make_uint4(0, 0, 0, 0);
+        if (lane == 0) { rowloss[r] = 0.0; rowerr[r] = 0; }
         return;
     }
     const float *lrow = logits + r * ldl;
-    __shared__ float s_v[CE_THREADS / 32];
-    __shared__ int s_i[CE_THREADS / 32];
-    __shared__ float s_sum[CE_THREADS / 32];
-    // max + argmax (ties: lowest index)
     float mv = -INFINITY;
     int mi = 0x7fffffff;
-    for (int k = threadIdx.x; k < K; k += CE_THREADS) {
+    for (int k = lane; k < K; k += 32) {
         const float v = lrow[k];
-        if (v > mv || (v == mv && k < mi)) { mv = v; mi = k; }
+        if (v > mv) { mv = v; mi = k; }  // k ascends per lane: the first max is the lowest index
     }
     for (int o = 16; o > 0; o >>= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, mv, o);
         const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
         if (ov > mv || (ov == mv && oi < mi)) { mv = ov; mi = oi; }
     }
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) { s_v[w] = mv; s_i[w] = mi; }
-    __syncthreads();
-    mv = s_v[0];
-    mi = s_i[0];
-    for (int i = 1; i < CE_THREADS / 32; ++i)
-        if (s_v[i] > mv || (s_v[i] == mv && s_i[i] < mi)) { mv = s_v[i]; mi = s_i[i]; }
-    // sum exp
     float se = 0.f;
-    for (int k = threadIdx.x; k < K; k += CE_THREADS) se += expf(lrow[k] - mv);
+    for (int k = lane; k < K; k += 32) se += expf(lrow[k] - mv);
     for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-    if ((threadIdx.x & 31) == 0) s_sum[w] = se;
-    __syncthreads();
-    se = 0.f;
-    for (int i = 0; i < CE_THREADS / 32; ++i) se += s_sum[i];
     const float lse = mv + logf(se);
     const int lab = labels[r];
-    for (int k = threadIdx.x; k < Kp; k += CE_THREADS) {
-        float v = 0.f;
-        if (k < K) v = expf(lrow[k] - lse) - (k == lab ? 1.f : 0.f);
-        drow[k] = __float2half_rn(v * scale);
+    for (int k0 = lane * 8; k0 < Kp; k0 += 256) {
+        uint32_t hv[4];
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+            float v0 = 0.f, v1 = 0.f;
+            if (k0 + u < K) v0 = expf(lrow[k0 + u] - lse) - (k0 + u == lab ? 1.f : 0.f);
+            if (k0 + u + 1 < K) v1 = expf(lrow[k0 + u + 1] - lse) - (k0 + u + 1 == lab ? 1.f : 0.f);
+            __half2 h2 = __floats2half2_rn(v0 * scale, v1 * scale);
+            hv[u / 2] = *reinterpret_cast<uint32_t *>(&h2);
+        }
+        *reinterpret_cast<uint4 *>(drow + k0) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
         rowloss[r] = (double)lse - (double)lrow[lab];
         rowerr[r] = mi != lab;
     }
@@ -213,8 +209,9 @@ __global__ void __launch_bounds__(CE_THREADS) ce_head_kernel(const float *__rest
 int ce_head(const float *logits, long ldl, int K, int Kp, const uint8_t *mask, const int32_t *labels, float scale,
             __half *dlog16, double *rowloss, int32_t *rowerr, long rows, cudaStream_t st) {
     if (rows <= 0) return 0;
-    ce_head_kernel<<<(unsigned)rows, CE_THREADS, 0, st>>>(logits, ldl, K, Kp, mask, labels, scale, dlog16, rowloss,
-                                                          rowerr);
+    const long blocks = (rows + CE_THREADS / 32 - 1) / (CE_THREADS / 32);
+    ce_head_kernel<<<(unsigned)blocks, CE_THREADS, 0, st>>>(logits, ldl, K, Kp, mask, labels, scale, dlog16, rowloss,
+                                                            rowerr, rows);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
