@@ -37,6 +37,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
            "-o", tmp] + srcs
     if trace:
         cmd.insert(1, "-DBLSTM_TRACE")
+        if os.environ.get("BLSTM_TRACE_CTA"):  # trace another CTA than 0 (e.g. 1: an odd pair CTA)
+            cmd.insert(1, "-DBLSTM_TRACE_CTA=" + str(int(os.environ["BLSTM_TRACE_CTA"])))
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

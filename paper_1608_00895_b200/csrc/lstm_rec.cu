@@ -117,6 +117,9 @@ DEVI float gate_act(float pre, int gam) {
     return is_g ? 2.f * s - 1.f : s;
 }
 
+#ifndef BLSTM_TRACE_CTA
+#define BLSTM_TRACE_CTA 0  // the CTA whose thread 0 records the trace (build.py: BLSTM_TRACE_CTA env)
+#endif
 #ifdef BLSTM_TRACE
 #define TRACE(k) \
     if (trace) trace[(size_t)s * 16 + (k)] = (unsigned long long)clock64()
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     const uint32_t full_addr = smem_u32(&bars[2]);
     uint32_t fph = 0, mma_phase = 0;  // fph bit b: phase parity of full[b]
 #ifdef BLSTM_TRACE
-    unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
+    unsigned long long *trace = (blockIdx.x == BLSTM_TRACE_CTA && threadIdx.x == 0) ? p.trace : nullptr;
 #endif
     // HBM stores of a step (saved activations in CTA-native layout, c, y, y16, h history): off the
     // critical path, so they are issued at the start of the NEXT step, behind its MMA issue
@@ -394,7 +397,10 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         } else if (pr == 1 && threadIdx.x == 0 && s > 0) {
             // odd CTA: its half of h_{s-1} landed -> tell the even CTA, which reads it in the MMA
             mbar_wait(&bars[2 + b], (fph >> b) & 1);
+            TRACE(11);
             mbar_remote_arrive(mapa_shared(smem_u32(&bars[4 + b]), c ^ 1));
+            TRACE(1);
+            TRACE(2);
         }
         if (s > 0) fph ^= 1u << b;
         if (s > 0) store_step(t_prev, frm_prev, fmq_prev);
@@ -737,7 +743,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     // this warp's batch columns lie in one column half (NQ divides N/2): local or the partner's
     const int hh = nq0 / NH;
 #ifdef BLSTM_TRACE
-    unsigned long long *trace = (blockIdx.x == 0 && threadIdx.x == 0) ? p.trace : nullptr;
+    unsigned long long *trace = (blockIdx.x == BLSTM_TRACE_CTA && threadIdx.x == 0) ? p.trace : nullptr;
 #endif
     for (int s = T - 1; s >= 0; --s) {
         const int t = dir > 0 ? s : T - 1 - s;
