@@ -80,6 +80,7 @@ def test_layer_c1(direction, state):
     (9, 37, 16, 33, 2),     # batch padded to the MMA N granularity, several groups
     (40, 3, 40, 500, 3),    # the paper-sized layer width
     (25, 64, 8, 64, 4),
+    (3, 300, 10, 300, 5),   # one direction, G = 9 groups of 34: MMA N = 64; ldy_pad makes c / dy repacked
 ])
 @pytest.mark.parametrize("direction", [1, -1])
 def test_layer_random_shapes(T, B, D, H, seed, direction):
@@ -154,6 +155,28 @@ def test_stack_small_with_head():
         assert norm_rel(Y[l], ref["Ys"][l]) < OUT_TOL
         for d in range(2):
             assert norm_rel(C[l, d], ref["Cs"][l, d]) < OUT_TOL
+
+
+@pytest.mark.parametrize("H,B", [(64, 300),    # Hq = 256 (one BPTT pair tile), G = 9 groups of 34 -> MMA N = 64
+                                 (300, 140)])  # Hq = 512 (two pair tiles), G = 4 groups of 35 -> N = 64
+def test_stack_wide_groups_n64(H, B):
+    """The N = 64 instantiations of both recurrence kernels (4 K-split accumulators x 64 columns next
+    to the resident R in TMEM) and their native layouts, through a full training step."""
+    L, D, K, T = 1, 12, 7, 4
+    params = synth.stack_params(L, D, H, K)
+    lengths = np.array([T - (i % 3) for i in range(B)])
+    batch = synth.speech_batch(T, B, D, K, lengths, seed=1003)
+    theta = oracle.pack_params(params, L, D, H, K)
+    st = Stack(L, D, H, K, T, B)
+    got = st.step(theta, batch, side_stream=True)
+    ref = oracle.blstm_step(theta, batch.x, batch.mask, L, H, K, labels=batch.labels, want_states=True)
+    assert abs(got["loss"] - ref["loss"]) / abs(ref["loss"]) < OUT_TOL
+    errs = grad_errors(got["grad"], ref["grad"], L, D, H, K)
+    assert max(errs.values()) < GRAD_TOL, errs
+    Y, C = st.forward(theta, batch)
+    assert norm_rel(Y[0], ref["Ys"][0]) < OUT_TOL
+    for d in range(2):
+        assert norm_rel(C[0, d], ref["Cs"][0, d]) < OUT_TOL
 
 
 def test_stack_side_stream_bitwise_equal():
