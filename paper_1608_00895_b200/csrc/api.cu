@@ -544,7 +544,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     }
     if (g.K > 0) {
         __half *wo16 = (__half *)(ws + w.wo16), *dlog = (__half *)(ws + w.dlog16);
-        float *boq = (float *)(ws + w.boq), *logits = (float *)(ws + w.Z), *dWoT = (float *)(ws + w.dWoT);
+        float *boq = (float *)(ws + w.boq), *logits = (float *)(ws + w.Z);
         TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, Hq, g.K, g.Kp, wo16, boq, st), "pack_wout");
         GemmParams gl{(int)g.TB, g.K, 2 * Hq, logits, g.Kp, 1.f, 0, boq, 0, 0};
         TRY(gemm_f16({ytop, 2L * Hq, 0}, {wo16, g.Kp, 1}, gl, 0, st), "gemm logits");
@@ -554,16 +554,8 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             "reduce_loss");
         GemmParams gd{(int)g.TB, 2 * Hq, g.Kp, dY[0], 2L * Hq, a, 0, nullptr, 0, 0};
         TRY(gemm_f16({dlog, g.Kp, 0}, {wo16, g.Kp, 0}, gd, 0, st), "gemm dY_top");
-        // the head's parameter gradients are off the critical path too: side stream
-        if (overlap) {
-            cudaEventRecord(evs[g.L + 1], st);
-            cudaStreamWaitEvent(side, evs[g.L + 1], 0);
-        }
-        GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
-        gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
-        TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
-        TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
-        TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
+        // the head's parameter gradients are off the critical path too: side stream (side_head)
+        if (overlap) cudaEventRecord(evs[g.L + 1], st);
     } else {
         TRY(pad_halves(dy_top, g.H, Hq, g.TB, dY[0], st), "pad dy_top");
         if (cudaMemsetAsync(loss_sum, 0, sizeof(double), st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
@@ -571,34 +563,28 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             return fail(BLSTM_ERR_CUDA, "memset");
     }
 
-    int cur = 0;
-    for (int l = g.L - 1; l >= 0; --l) {
+    // Side-stream work is enqueued (host order) after the BPTT launch it overlaps: both become ready
+    // when the same main-stream kernel completes, and side GEMM CTAs dispatched first would spread
+    // over the GPCs and keep the recurrence clusters out until they finish.
+    auto side_head = [&]() -> int {  // dW_out, db_out of the head
+        if (g.K == 0) return 0;
+        __half *dlog = (__half *)(ws + w.dlog16);
+        float *dWoT = (float *)(ws + w.dWoT);
+        if (overlap) cudaStreamWaitEvent(side, evs[g.L + 1], 0);
+        GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
+        gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
+        TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
+        TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
+        TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
+        return 0;
+    };
+    auto side_layer = [&](int l) -> int {  // dW, dR, db of layer l (inputs: dA / dbpart of its parity)
         const int par = l & 1;
-        __half *dA = (__half *)(ws + w.dA) + (size_t)par * g.TB * 8 * Hq;
+        const __half *dA = (__half *)(ws + w.dA) + (size_t)par * g.TB * 8 * Hq;
         float *dWT = (float *)(ws + w.dWT) + (size_t)par * 8 * Hq * w.maxDn;
         float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
-        float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
-        // layer l+2 used the same parity buffers: its side-stream GEMMs must be done reading them
-        if (overlap && l + 2 < g.L) cudaStreamWaitEvent(st, evs[g.L + 2 + l + 2], 0);
-        RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
-        p.maskN = (const uint8_t *)(ws + w.maskN);  // packed by stack_forward
-        p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq;
-        p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
-        p.dy = dY[cur]; p.lddy = 2L * Hq; p.dy_doff = Hq;
-        p.dA = dA; p.ldda = 8L * Hq;
-        p.dbpart = dbp;
-        p.P = (float *)(ws + w.P);
-        p.counters = (uint32_t *)(ws + w.cnt);
-        TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
-        const __half *w16 = (const __half *)(ws + w.w16[l]);
-        if (l > 0) {  // critical path: gradient of the layer below's output
-            GemmParams gx{(int)g.TB, g.Dn[l], 8 * Hq, dY[1 - cur], 2L * Hq, a, 0, nullptr, 0, 0};
-            TRY(gemm_f16({dA, 8L * Hq, 0}, {w16, 8L * Hq, 0}, gx, 0, st), "gemm dX");
-        }
-        if (overlap) {
-            cudaEventRecord(evs[l], st);
-            cudaStreamWaitEvent(side, evs[l], 0);
-        }
+        const float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
+        if (overlap) cudaStreamWaitEvent(side, evs[l], 0);
         const __half *X = l == 0 ? (const __half *)(ws + w.x16) : (const __half *)(ws + w.y16[l - 1]);
         // the last layer's weight gradients run after all BPTT work: every SM is free then
         const int wctas = l == 0 ? 0 : side_ctas;
@@ -619,8 +605,36 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.pl.G, dd, side), "scatter db");
         }
         if (overlap) cudaEventRecord(evs[g.L + 2 + l], side);
+        return 0;
+    };
+    int cur = 0;
+    for (int l = g.L - 1; l >= 0; --l) {
+        const int par = l & 1;
+        __half *dA = (__half *)(ws + w.dA) + (size_t)par * g.TB * 8 * Hq;
+        float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
+        // layer l+2 used the same parity buffers: its side-stream GEMMs must be done reading them
+        if (overlap && l + 2 < g.L) cudaStreamWaitEvent(st, evs[g.L + 2 + l + 2], 0);
+        RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
+        p.maskN = (const uint8_t *)(ws + w.maskN);  // packed by stack_forward
+        p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq;
+        p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
+        p.dy = dY[cur]; p.lddy = 2L * Hq; p.dy_doff = Hq;
+        p.dA = dA; p.ldda = 8L * Hq;
+        p.dbpart = dbp;
+        p.P = (float *)(ws + w.P);
+        p.counters = (uint32_t *)(ws + w.cnt);
+        TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
+        // the gradient work this BPTT overlaps, enqueued after it
+        if (int rc = (l == g.L - 1) ? side_head() : side_layer(l + 1)) return rc;
+        const __half *w16 = (const __half *)(ws + w.w16[l]);
+        if (l > 0) {  // critical path: gradient of the layer below's output
+            GemmParams gx{(int)g.TB, g.Dn[l], 8 * Hq, dY[1 - cur], 2L * Hq, a, 0, nullptr, 0, 0};
+            TRY(gemm_f16({dA, 8L * Hq, 0}, {w16, 8L * Hq, 0}, gx, 0, st), "gemm dX");
+        }
+        if (overlap) cudaEventRecord(evs[l], st);
         cur = 1 - cur;
     }
+    if (int rc = side_layer(0)) return rc;
     if (overlap) {  // s_main's view: all gradient work of this call is complete
         cudaEventRecord(evs[g.L], side);
         cudaStreamWaitEvent(st, evs[g.L], 0);
