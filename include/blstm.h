@@ -147,8 +147,10 @@ typedef struct dp_comm dp_comm;
  *     -log softmax(logits)[label] (K > 0; 0 otherwise)
  *   frame_errors: DEVICE int32 or NULL, overwritten with #valid frames whose argmax
  *     (lowest index on ties) differs from the label
- *   comm: NULL, or a dp_comm: grad is then allreduce-SUMmed over ranks after the
- *     local accumulation (sync data parallelism, R8)
+ *   comm: NULL, or a dp_comm: grad is then allreduce-SUMmed over ranks (sync data
+ *     parallelism, R8), one bucket per layer (and one for the head) as soon as
+ *     that bucket is accumulated, on s_side: the exchange overlaps the BPTT of the layers
+ *     below.  Every rank must make the same calls in the same order.
  *   workspace: blstm_stack_workspace_bytes DEVICE bytes
  *   s_main: the stream of the call; s_side: a second stream for work off the
  *     critical path (may equal s_main or be NULL)

@@ -513,7 +513,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     cudaStream_t st = (cudaStream_t)s_main;
     uint8_t *ws = (uint8_t *)workspace;
     std::vector<size_t> offs(6 * g.L + 2);
-    param_layout(d, offs.data());
+    const size_t nparam = param_layout(d, offs.data());
     if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st)) return rc;
 
     const int Hq = g.Hq;
@@ -576,6 +576,9 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
         TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
         TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
+        if (comm) {  // sync-mode exchange of this bucket (the head), overlapping the BPTT below
+            if (int rc = dp_allreduce_grads_impl(comm, grad + offs[6 * g.L], nparam - offs[6 * g.L], side)) return rc;
+        }
         return 0;
     };
     auto side_layer = [&](int l) -> int {  // dW, dR, db of layer l (inputs: dA / dbpart of its parity)
@@ -603,6 +606,10 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], side), "scatter dW");
             TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, side), "scatter dR");
             TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.pl.G, dd, side), "scatter db");
+        }
+        if (comm) {  // sync-mode exchange of layer l's bucket (§4.1), overlapping BPTT
+            const size_t end = l + 1 < g.L ? offs[6 * (l + 1)] : offs[6 * g.L];
+            if (int rc = dp_allreduce_grads_impl(comm, grad + offs[6 * l], end - offs[6 * l], side)) return rc;
         }
         if (overlap) cudaEventRecord(evs[g.L + 2 + l], side);
         return 0;
@@ -638,9 +645,6 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     if (overlap) {  // s_main's view: all gradient work of this call is complete
         cudaEventRecord(evs[g.L], side);
         cudaStreamWaitEvent(st, evs[g.L], 0);
-    }
-    if (comm) {
-        if (int rc = dp_allreduce_grads_impl(comm, grad, param_layout(d, nullptr), st)) return rc;
     }
     return 0;
 }
