@@ -524,7 +524,9 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     // needs them after BPTT of layer l): with a side stream they run on the SMs the recurrence
     // clusters leave free, overlapping BPTT of layer l-1.  Their inputs (dA, dbpart) and scratch
     // are double-buffered by layer parity.
-    cudaStream_t side = (s_side && s_side != s_main) ? (cudaStream_t)s_side : st;
+    // BLSTM_NO_SIDE=1: run the off-critical-path work on s_main too (experiments)
+    static const bool no_side = getenv("BLSTM_NO_SIDE") && atoi(getenv("BLSTM_NO_SIDE")) != 0;
+    cudaStream_t side = (s_side && s_side != s_main && !no_side) ? (cudaStream_t)s_side : st;
     const bool overlap = side != st;
     const int rec_ctas = 2 * g.pl.G * g.pl.NC;
     const int side_ctas = overlap ? (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8) : 0;

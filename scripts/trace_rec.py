@@ -31,10 +31,11 @@ BWD = [(0, None), (1, "issue next-step loads"), (2, "wait P + gather"), (8, "wai
 
 def report(name, tr, seq):
     step = np.diff(tr[:, 0])
-    print(f"{name}: median step {np.median(step):.0f} ns")
+    print(f"{name}: median step {np.median(step):.0f} ns, mean {np.mean(step):.0f}, p90 {np.percentile(step, 90):.0f}, "
+          f"max {np.max(step):.0f}, total {np.sum(step) / 1e3:.1f} us")
     for (a, _), (b, label) in zip(seq[:-1], seq[1:]):
         d = tr[1:, b] - tr[1:, a]
-        print(f"  {label:28s} {np.median(d):8.0f} ns")
+        print(f"  {label:28s} {np.median(d):8.0f} ns  (mean {np.mean(d):6.0f})")
     last = seq[-1][0]
     d = tr[1:, 0] - tr[:-1, last]
     print(f"  {'(to next step)':28s} {np.median(d):8.0f} ns")
