@@ -60,12 +60,17 @@ DEVI uint64_t globaltimer_ns() {
 }
 // Watchdog for every spin: a synchronisation bug traps (kernel error) instead of hanging the GPU.
 constexpr uint64_t SPIN_TIMEOUT_NS = 20ull * 1000 * 1000 * 1000;
+// (the timer is read every 256 polls only: each read is an issue slot on the critical path)
 DEVI void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait(a, parity)) return;
-    const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try_wait(a, parity)) {
-        if (globaltimer_ns() - t0 > SPIN_TIMEOUT_NS) __trap();
+    uint64_t t0 = 0;
+    for (uint32_t n = 1; !mbar_try_wait(a, parity); ++n) {
+        if ((n & 255) == 0) {
+            const uint64_t t = globaltimer_ns();
+            if (!t0) t0 = t;
+            else if (t - t0 > SPIN_TIMEOUT_NS) __trap();
+        }
     }
 }
 
@@ -284,9 +289,13 @@ DEVI bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
 DEVI void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait_cluster(a, parity)) return;
-    const uint64_t t0 = globaltimer_ns();
-    while (!mbar_try_wait_cluster(a, parity)) {
-        if (globaltimer_ns() - t0 > SPIN_TIMEOUT_NS) __trap();
+    uint64_t t0 = 0;
+    for (uint32_t n = 1; !mbar_try_wait_cluster(a, parity); ++n) {
+        if ((n & 255) == 0) {
+            const uint64_t t = globaltimer_ns();
+            if (!t0) t0 = t;
+            else if (t - t0 > SPIN_TIMEOUT_NS) __trap();
+        }
     }
 }
 
