@@ -174,6 +174,26 @@ def sgd(theta, grad, lr: float):
     return theta
 
 
+OPT_RULES = {"sgd": 0, "momentum": 1, "nesterov": 2, "adagrad": 3, "adadelta": 4, "adam": 5}
+
+
+def opt_update(rule, theta, grad, s0=None, s1=None, *, lr, mu=0.9, rho=0.95, beta1=0.9, beta2=0.999, eps=1e-8,
+               l2=0.0, max_norm=0.0, step=1, is_bias=None, zero_grad=False):
+    """One update of oracle.c ref_opt_update (fp64); returns (theta, grad, s0, s1) as new arrays."""
+    theta = np.array(theta, dtype=np.float64, copy=True)
+    grad = np.array(grad, dtype=np.float64, copy=True)
+    n = theta.size
+    s0 = np.zeros(n) if s0 is None else np.array(s0, dtype=np.float64, copy=True)
+    s1 = np.zeros(n) if s1 is None else np.array(s1, dtype=np.float64, copy=True)
+    ib = None if is_bias is None else np.ascontiguousarray(is_bias, dtype=np.uint8)
+    lib().ref_opt_update(ctypes.c_int(OPT_RULES[rule] if isinstance(rule, str) else rule), ctypes.c_double(lr),
+                         ctypes.c_double(mu), ctypes.c_double(rho), ctypes.c_double(beta1), ctypes.c_double(beta2),
+                         ctypes.c_double(eps), ctypes.c_double(l2), ctypes.c_double(max_norm), ctypes.c_long(step),
+                         ctypes.c_long(n), _d(theta), _d(grad), _d(s0), _d(s1),
+                         None if ib is None else ib.ctypes.data_as(_u8p), ctypes.c_int(int(zero_grad)))
+    return theta, grad, s0, s1
+
+
 def dp_average(thetas):
     th = np.ascontiguousarray(np.stack([np.asarray(t, np.float64) for t in thetas]))
     out = np.zeros(th.shape[1])

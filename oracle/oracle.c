@@ -22,8 +22,10 @@
  *   - bidirectional stacking (reading A2/A3): Y_l = [fwd | bwd].
  *   - softmax cross-entropy head, summed over valid frames, no
  *     scaling of the gradient (§4.3, reading R7).
- *   - SGD theta' = theta - lr*g (§4.3) and parameter averaging
- *     theta = (1/N) sum_r theta_r (§4.1).
+ *   - SGD theta' = theta - lr*g (§4.3), the other update rules of §4.3 (momentum,
+ *     simplified Nesterov, Adagrad, Adadelta, Adam, L2 penalty, norm constraint:
+ *     ref_opt_update) and parameter averaging theta = (1/N) sum_r theta_r
+ *     (§4.1).
  *
  * Reductions run in ascending index order.  OpenMP (when compiled with
  * -fopenmp) only splits independent batch rows / output elements, so the
@@ -427,6 +429,66 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
 void ref_sgd(double *theta, const double *grad, long n, double lr)
 {
     for (long i = 0; i < n; ++i) theta[i] -= lr * grad[i];
+}
+
+/* Update rules of PAPER.md §4.3: "Adagrad, Adadelta and Adam", "the classical momentum
+ * term and also the simplified Nesterov accelerated gradient"; "penalizing large L2 norms of the
+ * weight matrices" and the "norm constraints".  The paper gives no formulas; these
+ * are the standard definitions of the cited works as SPEC S:391/S:398 restates them (DESIGN.md
+ * reading R19), one update of n parameters:
+ *   conditioning, in this order: g += 2*l2*theta on weight-matrix entries (is_bias == 0);
+ *     then, if max_norm > 0 and ||g||_2 > max_norm, g *= max_norm / ||g||_2;
+ *   rule 0 sgd      theta -= lr*g
+ *   rule 1 momentum v = mu*v - lr*g; theta += v                               (s0 = v)
+ *   rule 2 nesterov v = mu*v - lr*g; theta += mu*v - lr*g  (simplified form)  (s0 = v)
+ *   rule 3 adagrad  a += g^2; theta -= lr*g / (sqrt(a) + eps)                  (s0 = a)
+ *   rule 4 adadelta Eg = rho*Eg + (1-rho)*g^2; u = g*sqrt(Ed + eps)/sqrt(Eg + eps);
+ *                   Ed = rho*Ed + (1-rho)*u^2; theta -= lr*u                   (s0 = Eg, s1 = Ed)
+ *   rule 5 adam     m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g^2;
+ *                   theta -= lr * (m/(1-b1^t)) / (sqrt(v/(1-b2^t)) + eps)      (s0 = m, s1 = v)
+ *   zero_grad: g = 0 afterwards (the gradient buffer, not the conditioned copy).
+ * is_bias may be NULL (every entry is a weight). */
+void ref_opt_update(int rule, double lr, double mu, double rho, double b1, double b2, double eps, double l2,
+                    double max_norm, long step, long n, double *theta, double *grad, double *s0, double *s1,
+                    const uint8_t *is_bias, int zero_grad)
+{
+    double *g = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    for (long i = 0; i < n; ++i) {
+        g[i] = grad[i];
+        if (l2 > 0.0 && !(is_bias && is_bias[i])) g[i] += 2.0 * l2 * theta[i];
+    }
+    if (max_norm > 0.0) {
+        double ss = 0.0;
+        for (long i = 0; i < n; ++i) ss += g[i] * g[i];
+        const double norm = sqrt(ss);
+        if (norm > max_norm)
+            for (long i = 0; i < n; ++i) g[i] *= max_norm / norm;
+    }
+    for (long i = 0; i < n; ++i) {
+        const double gi = g[i];
+        switch (rule) {
+        case 0: theta[i] -= lr * gi; break;
+        case 1: s0[i] = mu * s0[i] - lr * gi; theta[i] += s0[i]; break;
+        case 2: s0[i] = mu * s0[i] - lr * gi; theta[i] += mu * s0[i] - lr * gi; break;
+        case 3: s0[i] += gi * gi; theta[i] -= lr * gi / (sqrt(s0[i]) + eps); break;
+        case 4: {
+            s0[i] = rho * s0[i] + (1.0 - rho) * gi * gi;
+            const double u = gi * sqrt(s1[i] + eps) / sqrt(s0[i] + eps);
+            s1[i] = rho * s1[i] + (1.0 - rho) * u * u;
+            theta[i] -= lr * u;
+            break;
+        }
+        case 5: {
+            s0[i] = b1 * s0[i] + (1.0 - b1) * gi;
+            s1[i] = b2 * s1[i] + (1.0 - b2) * gi * gi;
+            const double mh = s0[i] / (1.0 - pow(b1, (double)step)), vh = s1[i] / (1.0 - pow(b2, (double)step));
+            theta[i] -= lr * mh / (sqrt(vh) + eps);
+            break;
+        }
+        }
+        if (zero_grad) grad[i] = 0.0;
+    }
+    free(g);
 }
 
 /* Parameter averaging (§4.1): out = (1/N) sum_r theta_r,
