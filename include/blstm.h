@@ -169,6 +169,52 @@ int blstm_stack_fwd(const blstm_stack_desc *d, const float *theta, const float *
  * P:253-254); zero_grad != 0 then sets grad = 0.  DEVICE pointers. */
 int sgd_update(float *theta, float *grad, size_t n, float lr, int zero_grad, void *stream);
 
+/*
+ * Update rules (§4.3: "Adagrad, Adadelta and Adam ... the classical
+ * momentum term and also the simplified Nesterov accelerated gradient ... norm constraints
+ * ... penalizing large L2 norms of the weight matrices"; formulas as restated in DESIGN.md
+ * R19).  One step over the flat vector theta[n] with gradient grad[n] (unscaled):
+ *   g = grad + 2*l2*theta on weight entries (l2 > 0; bias entries are not penalised)
+ *   g *= max_norm / ||g||_2 when max_norm > 0 and ||g||_2 exceeds it (global norm constraint)
+ *   SGD       theta -= lr*g
+ *   MOMENTUM  v = mu*v - lr*g;  theta += v
+ *   NESTEROV  v = mu*v - lr*g;  theta += mu*v - lr*g
+ *   ADAGRAD   a += g^2;  theta -= lr*g/(sqrt(a) + eps)
+ *   ADADELTA  Eg = rho*Eg + (1-rho)g^2;  u = g*sqrt(Eu+eps)/sqrt(Eg+eps);  Eu = rho*Eu + (1-rho)u^2;
+ *             theta -= lr*u
+ *   ADAM      m = b1*m + (1-b1)g;  v = b2*v + (1-b2)g^2;
+ *             theta -= lr*(m/(1-b1^step)) / (sqrt(v/(1-b2^step)) + eps)
+ * then grad = 0 if zero_grad.  Arithmetic fp32 (norm sum fp64, reproducible bit for bit).
+ */
+enum { BLSTM_OPT_SGD = 0, BLSTM_OPT_MOMENTUM = 1, BLSTM_OPT_NESTEROV = 2, BLSTM_OPT_ADAGRAD = 3,
+       BLSTM_OPT_ADADELTA = 4, BLSTM_OPT_ADAM = 5 };
+typedef struct {
+    int rule;       /* BLSTM_OPT_* */
+    double lr, mu, rho, beta1, beta2, eps;
+    double l2;       /* L2 penalty factor on weight entries, 0 = off */
+    double max_norm; /* global gradient norm constraint, 0 = off */
+    long step;       /* 1-based count of this update (Adam's bias correction) */
+} blstm_opt_params;
+/* Hyper-parameters are fp64 at the boundary: 1-beta2, 1-rho etc. are formed in fp64 on the
+ * host (1 - 0.999f would carry a 1.3e-5 relative error into every second moment). */
+/* Floats of optimizer state for n parameters: 0 (SGD), n4 (MOMENTUM, NESTEROV: v; ADAGRAD: a),
+ * 2*n4 (ADADELTA: Eg then Eu; ADAM: m then v), n4 = n rounded up to a multiple of 4: the
+ * second slot starts at state + n4.  The caller zero-fills it before the first step. */
+size_t blstm_opt_state_floats(int rule, size_t n);
+/* DEVICE workspace bytes blstm_opt_update needs (the norm pass's fp64 partials). */
+size_t blstm_opt_workspace_bytes(size_t n);
+/*
+ * theta, grad [n], state [blstm_opt_state_floats] (NULL if 0), workspace: DEVICE, 16-byte
+ * aligned, owned by the caller; updated in place on `stream` (asynchronous).
+ * layout: NULL = every entry is a weight; else n must equal blstm_param_count(layout) and the
+ * b / b_out ranges of its layout are the bias entries (L <= 31).
+ * Errors (nothing launched): BLSTM_ERR_ARG (null pointer, unknown rule, step < 1 for ADAM,
+ * n mismatch), BLSTM_ERR_ALIGN, BLSTM_ERR_WORKSPACE, BLSTM_ERR_UNSUPPORTED (L > 31).
+ */
+int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_desc *layout, float *theta, float *grad,
+                     float *state, size_t n, int zero_grad, void *workspace, size_t workspace_bytes,
+                     void *stream);
+
 /* ------------------------------------------------------------------------ */
 /* Data parallelism over NCCL (§4.1).                      */
 /* ------------------------------------------------------------------------ */

@@ -39,6 +39,15 @@ class StackDesc(ctypes.Structure):
                 ("precision", ctypes.c_int)]
 
 
+class OptParams(ctypes.Structure):
+    _fields_ = [("rule", ctypes.c_int), ("lr", ctypes.c_double), ("mu", ctypes.c_double), ("rho", ctypes.c_double),
+                ("beta1", ctypes.c_double), ("beta2", ctypes.c_double), ("eps", ctypes.c_double),
+                ("l2", ctypes.c_double), ("max_norm", ctypes.c_double), ("step", ctypes.c_long)]
+
+
+# update rules (include/blstm.h BLSTM_OPT_*)
+OPT_RULES = {"sgd": 0, "momentum": 1, "nesterov": 2, "adagrad": 3, "adadelta": 4, "adam": 5}
+
 _vp = ctypes.c_void_p
 _sz = ctypes.c_size_t
 _i = ctypes.c_int
@@ -56,6 +65,10 @@ _SIGS = {
     "blstm_stack_fwd_bwd": (_i, [ctypes.POINTER(StackDesc)] + [_vp] * 10 + [_sz, _vp, _vp]),
     "blstm_stack_fwd": (_i, [ctypes.POINTER(StackDesc)] + [_vp] * 6 + [_sz, _vp]),
     "sgd_update": (_i, [_vp, _vp, _sz, ctypes.c_float, _i, _vp]),
+    "blstm_opt_state_floats": (_sz, [_i, _sz]),
+    "blstm_opt_workspace_bytes": (_sz, [_sz]),
+    "blstm_opt_update": (_i, [ctypes.POINTER(OptParams), ctypes.POINTER(StackDesc), _vp, _vp, _vp, _sz, _i, _vp,
+                              _sz, _vp]),
     "dp_get_unique_id": (_i, [ctypes.c_char_p]),
     "dp_comm_init": (_i, [_i, _i, ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "dp_allreduce_grads": (_i, [_vp, _vp, _sz, _vp]),
@@ -202,6 +215,28 @@ def blstm_stack_fwd(desc, theta, x, mask, Y, C, workspace, stream=None):
 def sgd_update(theta, grad, lr: float, zero_grad: bool = False, stream=None):
     _check("sgd_update", lib().sgd_update(_p(theta), _p(grad), theta.numel(), float(lr), int(zero_grad),
                                           _stream(stream)))
+
+
+def opt_params(rule, lr, mu=0.9, rho=0.95, beta1=0.9, beta2=0.999, eps=1e-8, l2=0.0, max_norm=0.0,
+               step=1) -> OptParams:
+    r = OPT_RULES[rule] if isinstance(rule, str) else int(rule)
+    return OptParams(r, lr, mu, rho, beta1, beta2, eps, l2, max_norm, step)
+
+
+def blstm_opt_state_floats(rule, n: int) -> int:
+    return int(lib().blstm_opt_state_floats(OPT_RULES[rule] if isinstance(rule, str) else int(rule), n))
+
+
+def blstm_opt_workspace_bytes(n: int) -> int:
+    return int(lib().blstm_opt_workspace_bytes(n))
+
+
+def blstm_opt_update(params: OptParams, layout, theta, grad, state, zero_grad: bool, workspace, stream=None):
+    """One update-rule step in place (theta, grad, state: fp32 DEVICE; layout: StackDesc or None)."""
+    _check("blstm_opt_update", lib().blstm_opt_update(
+        ctypes.byref(params), ctypes.byref(layout) if layout is not None else None, _p(theta), _p(grad),
+        _p(state), theta.numel(), int(zero_grad), _p(workspace),
+        workspace.numel() * workspace.element_size() if workspace is not None else 0, _stream(stream)))
 
 
 def dp_get_unique_id() -> bytes:

@@ -11,6 +11,7 @@
 #include "gemm.h"
 #include "lstm_rec.h"
 #include "ops.h"
+#include "optim.h"
 #include "prof.h"
 
 using namespace blstm;
@@ -655,6 +656,72 @@ extern "C" int sgd_update(float *theta, float *grad, size_t n, float lr, int zer
     if (!theta || !grad) return fail(BLSTM_ERR_ARG, "null theta / grad");
     if (!al16(theta) || !al16(grad)) return fail(BLSTM_ERR_ALIGN, "theta/grad must be 16-byte aligned");
     TRY(sgd(theta, grad, (long)n, lr, zero_grad, (cudaStream_t)stream), "sgd");
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// update rules (§4.3; optim.cu)
+// ---------------------------------------------------------------------------
+static inline size_t rup4(size_t n) { return (n + 3) & ~(size_t)3; }
+extern "C" size_t blstm_opt_state_floats(int rule, size_t n) {
+    switch (rule) {
+    case BLSTM_OPT_SGD: return 0;
+    case BLSTM_OPT_MOMENTUM: case BLSTM_OPT_NESTEROV: case BLSTM_OPT_ADAGRAD: return rup4(n);
+    case BLSTM_OPT_ADADELTA: case BLSTM_OPT_ADAM: return 2 * rup4(n);
+    default: return 0;
+    }
+}
+extern "C" size_t blstm_opt_workspace_bytes(size_t) { return sizeof(double) * (size_t)opt_norm_partials(); }
+
+extern "C" int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_desc *layout, float *theta, float *grad,
+                                float *state, size_t n, int zero_grad, void *workspace, size_t workspace_bytes,
+                                void *stream) {
+    if (!p || !theta || !grad) return fail(BLSTM_ERR_ARG, "blstm_opt_update: null params / theta / grad");
+    if (p->rule < BLSTM_OPT_SGD || p->rule > BLSTM_OPT_ADAM) return fail(BLSTM_ERR_ARG, "unknown rule %d", p->rule);
+    if (p->rule == BLSTM_OPT_ADAM && p->step < 1) return fail(BLSTM_ERR_ARG, "ADAM needs step >= 1");
+    const size_t ns = blstm_opt_state_floats(p->rule, n);
+    if (ns && !state) return fail(BLSTM_ERR_ARG, "rule %d needs %zu floats of state", p->rule, ns);
+    if (!al16(theta) || !al16(grad) || (ns && !al16(state)))
+        return fail(BLSTM_ERR_ALIGN, "theta / grad / state must be 16-byte aligned");
+    if (p->max_norm > 0.0) {
+        if (!workspace || !al16(workspace)) return fail(BLSTM_ERR_ALIGN, "norm constraint needs an aligned workspace");
+        if (workspace_bytes < blstm_opt_workspace_bytes(n))
+            return fail(BLSTM_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, blstm_opt_workspace_bytes(n));
+    }
+    OptBiasTable tab;
+    tab.nb = 0;
+    for (int k = 0; k < OPT_MAX_BOUNDS; ++k) tab.bnd[k] = 0x7fffffffffffffffL;
+    if (layout) {
+        if (layout->L > 31) return fail(BLSTM_ERR_UNSUPPORTED, "layout with L=%d > 31", layout->L);
+        const size_t np = blstm_param_count(layout);
+        if (np == 0 || np != n) return fail(BLSTM_ERR_ARG, "n=%zu != blstm_param_count(layout)=%zu", n, np);
+        std::vector<size_t> offs(6 * layout->L + 2);
+        param_layout(layout, offs.data());
+        const long h4 = 4L * layout->H;
+        for (int l = 0; l < layout->L; ++l)
+            for (int dd = 0; dd < 2; ++dd) {
+                const long b0 = (long)offs[6 * l + 3 * dd + 2];
+                tab.bnd[tab.nb++] = b0;
+                tab.bnd[tab.nb++] = b0 + h4;
+            }
+        if (layout->K > 0) {
+            tab.bnd[tab.nb++] = (long)offs[6 * layout->L + 1];
+            tab.bnd[tab.nb++] = (long)offs[6 * layout->L + 1] + layout->K;
+        }
+    }
+    const size_t n4 = rup4(n);
+    float *s0 = ns ? state : nullptr;
+    float *s1 = ns > n4 ? state + n4 : nullptr;
+    OptArgs a{(float)p->lr, (float)p->mu, (float)p->rho, (float)p->beta1, (float)p->beta2, (float)p->eps,
+              (float)p->l2, (float)p->max_norm, (float)(1.0 - p->rho), (float)(1.0 - p->beta1),
+              (float)(1.0 - p->beta2), 1.f, 1.f};
+    if (p->rule == BLSTM_OPT_ADAM) {
+        a.c1 = (float)(1.0 / (1.0 - pow(p->beta1, (double)p->step)));
+        a.c2 = (float)(1.0 / (1.0 - pow(p->beta2, (double)p->step)));
+    }
+    if (n == 0) return 0;
+    TRY(opt_update(p->rule, theta, grad, s0, s1, (long)n, a, p->max_norm, tab, (double *)workspace, zero_grad,
+                   (cudaStream_t)stream), "opt_update");
     return 0;
 }
 

@@ -147,7 +147,9 @@ class StackTrainer:
     """Device-resident training of one rank: theta, grad, workspace and a batch."""
 
     def __init__(self, cfg, params, batch, device, lr: float = 1e-5, comm=None, world: int = 1,
-                 sched: Optional[DPSchedule] = None):
+                 sched: Optional[DPSchedule] = None, opt: Optional[dict] = None):
+        """opt: None = plain SGD (sgd_update); else the update rule of blstm_opt_update, e.g.
+        {"rule": "adam", "lr": 1e-3, "l2": 1e-4, "max_norm": 10.0} (§4.3)."""
         import torch
         from . import blstm
         self.torch, self.blstm = torch, blstm
@@ -165,6 +167,13 @@ class StackTrainer:
         self.coll = NcclCollective(comm, world) if comm is not None else None
         self.set_batch(batch)
         self.steps_done = 0
+        self.opt = dict(opt) if opt is not None else None
+        if self.opt is not None:
+            ns = blstm.blstm_opt_state_floats(self.opt["rule"], self.theta.numel())
+            self.opt_state = torch.zeros(max(ns, 4), dtype=torch.float32, device=device) if ns else None
+            self.opt_ws = torch.empty(blstm.blstm_opt_workspace_bytes(self.theta.numel()), dtype=torch.uint8,
+                                      device=device)
+            self.opt_steps = 0
 
     def set_batch(self, batch):
         t = self.torch
@@ -181,7 +190,12 @@ class StackTrainer:
                                        self.loss, self.ferr, comm, self.ws, s_side=self.side)
 
     def _update(self, theta, grad):
-        self.blstm.sgd_update(theta, grad, self.lr, zero_grad=True)
+        if self.opt is None:
+            self.blstm.sgd_update(theta, grad, self.lr, zero_grad=True)
+            return
+        self.opt_steps += 1
+        P = self.blstm.opt_params(step=self.opt_steps, **self.opt)
+        self.blstm.blstm_opt_update(P, self.desc, theta, grad, self.opt_state, True, self.opt_ws)
 
     def step(self):
         class _NoSum(Collective):  # the sum already happened inside blstm_stack_fwd_bwd

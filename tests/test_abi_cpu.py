@@ -24,7 +24,8 @@ def _declared_functions():
 def test_header_declares_expected_boundary():
     names = _declared_functions()
     for n in ("lstm_fwd", "lstm_bwd", "blstm_stack_fwd_bwd", "dp_average_params", "dp_allreduce_grads",
-              "sgd_update", "blstm_param_offsets", "lstm_workspace_bytes", "lstm_reserve_bytes"):
+              "sgd_update", "blstm_param_offsets", "lstm_workspace_bytes", "lstm_reserve_bytes",
+              "blstm_opt_update", "blstm_opt_state_floats", "blstm_opt_workspace_bytes"):
         assert n in names, n
 
 
@@ -61,3 +62,37 @@ def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
     monkeypatch.setattr(blstm, "_lib", None)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         blstm.lib()
+
+
+def test_opt_state_sizes():
+    for n in (0, 1, 4, 5, 1001):
+        n4 = (n + 3) // 4 * 4
+        assert blstm.blstm_opt_state_floats("sgd", n) == 0
+        for r in ("momentum", "nesterov", "adagrad"):
+            assert blstm.blstm_opt_state_floats(r, n) == n4
+        for r in ("adadelta", "adam"):
+            assert blstm.blstm_opt_state_floats(r, n) == 2 * n4
+    assert blstm.blstm_opt_workspace_bytes(10) >= 8
+
+
+def test_opt_update_rejects_bad_arguments():
+    """Host-side validation of blstm_opt_update returns an error code before any launch."""
+    import ctypes
+    L = blstm.lib()
+    fake = ctypes.c_void_p(1 << 20)  # aligned, never dereferenced (validation fails first)
+    P = blstm.opt_params("adam", 0.1, step=0)
+    assert L.blstm_opt_update(ctypes.byref(P), None, fake, fake, fake, 16, 0, None, 0, None) != 0
+    assert "step" in blstm.last_error()
+    P = blstm.opt_params(9, 0.1)
+    assert L.blstm_opt_update(ctypes.byref(P), None, fake, fake, fake, 16, 0, None, 0, None) != 0
+    P = blstm.opt_params("momentum", 0.1)
+    assert L.blstm_opt_update(ctypes.byref(P), None, fake, fake, None, 16, 0, None, 0, None) != 0  # no state
+    assert L.blstm_opt_update(ctypes.byref(P), None, ctypes.c_void_p((1 << 20) + 4), fake, fake, 16, 0, None, 0,
+                              None) != 0  # misaligned theta
+    P = blstm.opt_params("sgd", 0.1, max_norm=1.0)
+    assert L.blstm_opt_update(ctypes.byref(P), None, fake, fake, None, 16, 0, None, 0, None) != 0  # no workspace
+    d = blstm.stack_desc(2, 3, 5, 7, 4, 2)
+    P = blstm.opt_params("sgd", 0.1)
+    n = blstm.blstm_param_count(d)
+    assert L.blstm_opt_update(ctypes.byref(P), ctypes.byref(d), fake, fake, None, n + 1, 0, None, 0, None) != 0
+    assert L.blstm_opt_update(ctypes.byref(P), None, fake, fake, None, 0, 0, None, 0, None) == 0  # n = 0: no-op
