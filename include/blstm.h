@@ -243,12 +243,19 @@ int blstm_gemm_f16(int M, int N, int K, const void *A, long lda, int a_mn, const
 /* ------------------------------------------------------------------------ */
 /* Number of kernels this library has launched since it was loaded. */
 long blstm_launch_count(void);
-/* on != 0: from now on bracket every launch of the categories below with CUDA
- * events on the launching stream (records are reset); on == 0: stop. */
+/* on = 1: from now on bracket every launch of the categories below with CUDA events on the
+ * launching stream (records are reset); on = 2: also the helper kernels (category 3, for
+ * blstm_profile_timeline; adds two events per helper launch); on == 0: stop. */
 int blstm_profile_enable(int on);
 /* cat: 0 forward recurrence, 1 BPTT recurrence, 2 GEMM.  Synchronizes the
  * recorded events; returns the summed device time (ms) and launch count. */
 int blstm_profile_read(int cat, double *total_ms, long *launches);
+/* Timeline of the launches recorded since blstm_profile_enable(1) (synchronizes them):
+ * 7 doubles per launch into host `rec` (at most max_recs launches): category (0-2 as above,
+ * 3 = helper kernels), stream index (order of first appearance), start and end (ms, relative
+ * to the first recorded start), and the launch shape (GEMM: M, N, K; else 0).  Returns the
+ * number of launches written, < 0 on error. */
+int blstm_profile_timeline(double *rec, int max_recs);
 /* Debug: record per-step phase timestamps (SM clock64 cycles, 16 slots per step, CTA 0 /
  * thread 0) of the following forward / BPTT recurrence launches into DEVICE buffers of
  * 16*T uint64 each; NULL disables.  Only a library built with -DBLSTM_TRACE writes them. */

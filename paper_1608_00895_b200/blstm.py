@@ -79,6 +79,7 @@ _SIGS = {
     "blstm_launch_count": (ctypes.c_long, []),
     "blstm_profile_enable": (_i, [_i]),
     "blstm_profile_read": (_i, [_i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_long)]),
+    "blstm_profile_timeline": (_i, [ctypes.POINTER(ctypes.c_double), _i]),
     "blstm_debug_set_trace": (_i, [_vp, _vp]),
 }
 
@@ -89,7 +90,8 @@ def blstm_launch_count() -> int:
     return int(lib().blstm_launch_count())
 
 
-def blstm_profile_enable(on: bool):
+def blstm_profile_enable(on):
+    """on: False/0 off, True/1 recurrence + GEMM launches, 2 also helper kernels (timeline)."""
     _check("blstm_profile_enable", lib().blstm_profile_enable(int(on)))
 
 
@@ -99,6 +101,17 @@ def blstm_profile_read(cat: int):
     n = ctypes.c_long(0)
     _check("blstm_profile_read", lib().blstm_profile_read(cat, ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
+
+
+def blstm_profile_timeline(max_recs: int = 4096):
+    """[(cat, stream, t0_ms, t1_ms, a, b, c)] of the launches recorded since profiling was enabled."""
+    buf = (ctypes.c_double * (7 * max_recs))()
+    n = lib().blstm_profile_timeline(buf, max_recs)
+    if n < 0:
+        raise BlstmError("blstm_profile_timeline", n, last_error())
+    return [tuple(buf[7 * i + k] for k in range(7)) for i in range(n)]
+
+
 EXPORTS = tuple(_SIGS)
 
 

@@ -326,8 +326,9 @@ static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
     return 0;
 }
 // Z GEMM -> recurrence completion counters: [L][2 directions][M-tiles]
+// Z GEMM completion counters [L][2][M tiles], then one BPTT "CTAs started" counter per layer
 static size_t zflag_words(const StackGeo &g) {
-    return (size_t)g.L * 2 * ((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS);
+    return (size_t)g.L * 2 * ((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS) + g.L;
 }
 static StackWS stack_ws(const StackGeo &g) {
     Carve c;
@@ -530,6 +531,19 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     cudaStream_t side = (s_side && s_side != s_main && !no_side) ? (cudaStream_t)s_side : st;
     const bool overlap = side != st;
     const int rec_ctas = 2 * g.pl.G * g.pl.NC;
+    // per-layer BPTT start counters (zeroed with the Z flags by stack_forward)
+    uint32_t *bstarted = (uint32_t *)(ws + w.zflags) + (zflag_words(g) - g.L);
+    // Side-stream work that overlaps BPTT(l) must not take SMs before BPTT(l)'s clusters are all
+    // placed: GEMM CTAs dispatched first spread over every GPC, no GPC keeps 16 free SMs and the
+    // BPTT waits for the whole GEMM (measured: 0.98 instead of 0.63 ms per layer).  Both become
+    // ready when the same main-stream kernel completes, so the order is a race; a one-CTA kernel
+    // on the side stream waits for BPTT(l)'s CTAs to check in first.
+    static const bool no_guard = getenv("BLSTM_NO_GUARD") && atoi(getenv("BLSTM_NO_GUARD")) != 0;  // A/B
+    auto side_guard = [&](int l) -> int {
+        if (!overlap || no_guard) return 0;
+        TRY(wait_count(bstarted + l, (uint32_t)rec_ctas, side), "wait_count");
+        return 0;
+    };
     const int side_ctas = overlap ? (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8) : 0;
     // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused)
@@ -574,6 +588,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         __half *dlog = (__half *)(ws + w.dlog16);
         float *dWoT = (float *)(ws + w.dWoT);
         if (overlap) cudaStreamWaitEvent(side, evs[g.L + 1], 0);
+        if (int rc = side_guard(g.L - 1)) return rc;
         GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
         gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
         TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
@@ -591,6 +606,8 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
         const float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
         if (overlap) cudaStreamWaitEvent(side, evs[l], 0);
+        if (l > 0)  // overlaps BPTT(l-1)
+            if (int rc = side_guard(l - 1)) return rc;
         const __half *X = l == 0 ? (const __half *)(ws + w.x16) : (const __half *)(ws + w.y16[l - 1]);
         // the last layer's weight gradients run after all BPTT work: every SM is free then
         const int wctas = l == 0 ? 0 : side_ctas;
@@ -633,6 +650,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         p.dbpart = dbp;
         p.P = (float *)(ws + w.P);
         p.counters = (uint32_t *)(ws + w.cnt);
+        p.started = overlap ? bstarted + l : nullptr;
         TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
         // the gradient work this BPTT overlaps, enqueued after it
         if (int rc = (l == g.L - 1) ? side_head() : side_layer(l + 1)) return rc;

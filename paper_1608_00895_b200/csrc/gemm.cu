@@ -383,7 +383,7 @@ static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, con
     const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN) * p.ksplit;
     int grid = tiles < max_ctas ? tiles : max_ctas;
     if (grid < 1) grid = 1;
-    ProfScope ps(PROF_GEMM, st);
+    ProfScope ps(PROF_GEMM, st, p.M, p.N, p.K);
     note_launch();
     if (!p.pdl) {
         gemm_f16_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, p);

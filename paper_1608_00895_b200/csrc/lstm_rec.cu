@@ -547,6 +547,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     constexpr int NH = N / 2;  // batch columns of the B operand held by each CTA of a pair
     constexpr int NQ = N / 4;
     constexpr int NMQ = NQ / 4;
+    if (p.started && threadIdx.x == 0) atomicAdd(p.started, 1u);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     const int Hq = p.Hq, NC = p.NC;

@@ -51,6 +51,9 @@ struct RecParams {
     float *P;                    // [2][ndir][G][NC][Hq][N] partial dh exchange
     float *dh0, *dc0;            // [B, H] (+ d*B*H) or nullptr
     uint32_t *counters;          // [ndir][G], zeroed before each launch
+    // != nullptr (BPTT): each CTA adds 1 at entry, so a side-stream kernel can hold back work
+    // that would otherwise take SMs before every recurrence cluster is placed (wait_count)
+    uint32_t *started;
     unsigned long long *trace;   // debug: per-step phase timestamps of CTA 0 / thread 0, or nullptr
 };
 

@@ -27,6 +27,7 @@ __global__ void cast_x_kernel(const float *__restrict__ x, long ldx, int D, __ha
     }
 }
 int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     cast_x_kernel<<<grid_for(rows * Dp), 256, 0, st>>>(x, ldx, D, x16, Dp, rows);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -63,6 +64,7 @@ __global__ void pack_w_kernel(const float *__restrict__ W0, const float *__restr
 }
 int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir, int Dn, int rowmode, __half *W16,
            cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     dim3 grid((Hq + 255) / 256, Dn, ndir);
     pack_w_kernel<<<grid, 256, 0, st>>>(W0, W1, Drows, H, Hq, ndir, Dn, rowmode, W16);
     note_launch();
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(256) pack_rt_kernel(const float *__restrict__ 
     }
 }
 int pack_rt(const float *R0, const float *R1, int H, int Hq, int ndir, __half *RT16, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     dim3 grid(Hq / 32, Hq / 32, ndir);
     pack_rt_kernel<<<grid, 256, 0, st>>>(R0, R1, H, Hq, ndir, RT16);
     note_launch();
@@ -108,6 +111,7 @@ __global__ void pack_bias_kernel(const float *__restrict__ b0, const float *__re
     }
 }
 int pack_bias(const float *b0, const float *b1, int H, int Hq, int ndir, float *bq, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     pack_bias_kernel<<<grid_for(ndir * 4 * Hq), 256, 0, st>>>(b0, b1, H, Hq, ndir, bq);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -126,6 +130,7 @@ __global__ void pack_wout_kernel(const float *__restrict__ Wo, const float *__re
 }
 int pack_wout(const float *Wo, const float *bo, int H, int Hq, int K, int Kp, __half *Wo16, float *boq,
               cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     pack_wout_kernel<<<grid_for((long)2 * Hq * Kp), 256, 0, st>>>(Wo, bo, H, Hq, K, Kp, Wo16, boq);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -146,6 +151,7 @@ __global__ void init_hist_kernel(__half *__restrict__ hist, const float *__restr
     }
 }
 int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int ndir, int dir0, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     init_hist_kernel<<<grid_for((long)ndir * B * Hq), 256, 0, st>>>(hist, h0, T, B, H, Hq, ndir, dir0);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -208,6 +214,7 @@ __global__ void __launch_bounds__(CE_THREADS) ce_head_kernel(const float *__rest
 }
 int ce_head(const float *logits, long ldl, int K, int Kp, const uint8_t *mask, const int32_t *labels, float scale,
             __half *dlog16, double *rowloss, int32_t *rowerr, long rows, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     if (rows <= 0) return 0;
     const long blocks = (rows + CE_THREADS / 32 - 1) / (CE_THREADS / 32);
     ce_head_kernel<<<(unsigned)blocks, CE_THREADS, 0, st>>>(logits, ldl, K, Kp, mask, labels, scale, dlog16, rowloss,
@@ -239,6 +246,7 @@ __global__ void __launch_bounds__(1024) reduce_loss_kernel(const double *__restr
 }
 int reduce_loss(const double *rowloss, const int32_t *rowerr, long rows, double *loss, int32_t *ferr,
                 cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     reduce_loss_kernel<<<1, 1024, 0, st>>>(rowloss, rowerr, rows, loss, ferr);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -266,6 +274,7 @@ __global__ void colsum_pass2(const float *__restrict__ part, int nchunks, int co
 size_t colsum_scratch_bytes(long rows, int cols) { return (size_t)((rows + CS_ROWS - 1) / CS_ROWS) * cols * 4; }
 int colsum_f16_add(const __half *src, long rows, int cols, long ld, float alpha, float *out, float *scratch,
                    cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     const int nch = (int)((rows + CS_ROWS - 1) / CS_ROWS);
     if (nch == 0) return 0;
     dim3 g1((cols + 127) / 128, nch);
@@ -288,6 +297,7 @@ __global__ void scatter_w_kernel(float *__restrict__ gW, int Drows, int H, int H
     }
 }
 int scatter_w(float *gW, int Drows, int H, int Hq, const float *dWT, long ldw, int d, int rowmode, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     scatter_w_kernel<<<grid_for((long)Drows * 4 * H), 256, 0, st>>>(gW, Drows, H, Hq, dWT, ldw, d, rowmode);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -302,6 +312,7 @@ __global__ void scatter_r_kernel(float *__restrict__ gR, int H, int Hq, const fl
     }
 }
 int scatter_r(float *gR, int H, int Hq, const float *dRT, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     scatter_r_kernel<<<grid_for((long)H * 4 * H), 256, 0, st>>>(gR, H, Hq, dRT);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -317,6 +328,7 @@ __global__ void scatter_b_kernel(float *__restrict__ gb, int H, int Hq, const fl
     }
 }
 int scatter_b(float *gb, int H, int Hq, const float *dbpart, int G, int d, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     scatter_b_kernel<<<grid_for(4 * H), 256, 0, st>>>(gb, H, Hq, dbpart, G, d);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -332,6 +344,7 @@ __global__ void scatter_wout_kernel(float *__restrict__ gWo, int H, int Hq, int 
     }
 }
 int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     scatter_wout_kernel<<<grid_for((long)2 * H * K), 256, 0, st>>>(gWo, H, Hq, K, dWoT, ldw);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -350,6 +363,7 @@ __global__ void pack_mask_kernel(const uint8_t *__restrict__ mask, int T, int B,
     }
 }
 int pack_mask(const uint8_t *mask, int T, int B, int G, int Bg, int N, uint8_t *maskN, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     if (T == 0) return 0;
     pack_mask_kernel<<<grid_for((long)T * G * N), 256, 0, st>>>(mask, T, B, G, Bg, N, maskN);
     note_launch();
@@ -366,6 +380,7 @@ __global__ void copy_rows_kernel(const float *__restrict__ src, long lds, long r
     }
 }
 int copy_rows(const float *src, long lds, long rows, int cols, float *dst, long ldd, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     if (rows * cols == 0) return 0;
     copy_rows_kernel<<<grid_for(rows * cols), 256, 0, st>>>(src, lds, rows, cols, dst, ldd);
     note_launch();
@@ -381,6 +396,7 @@ __global__ void pad_halves_kernel(const float *__restrict__ src, int H, int Hq, 
     }
 }
 int pad_halves(const float *src, int H, int Hq, long rows, float *dst, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     pad_halves_kernel<<<grid_for(rows * 2 * Hq), 256, 0, st>>>(src, H, Hq, rows, dst);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -399,7 +415,23 @@ __global__ void store_dx_kernel(float *__restrict__ dx, long ldx, const float *_
     }
 }
 int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, int accum, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     store_dx_kernel<<<grid_for(rows * D), 256, 0, st>>>(dx, ldx, dX, ldX, D, rows, accum);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- placement guard: hold a stream until *flag >= target (or timeout_ns passed) -------------
+__global__ void wait_count_kernel(const uint32_t *flag, uint32_t target, unsigned long long timeout_ns) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_gpu(flag) < target) {
+        if (globaltimer_ns() - t0 > timeout_ns) break;  // never a deadlock: only placement is at stake
+        __nanosleep(200);
+    }
+}
+int wait_count(const uint32_t *flag, uint32_t target, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
+    wait_count_kernel<<<1, 32, 0, st>>>(flag, target, 2000000ull);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
@@ -422,6 +454,7 @@ __global__ void sgd_kernel(float *__restrict__ th, float *__restrict__ gr, long 
     }
 }
 int sgd(float *theta, float *grad, long n, float lr, int zero, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
     sgd_kernel<<<grid_for(n / 4 + 1, 256, 148 * 8), 256, 0, st>>>(theta, grad, n, lr, zero);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;

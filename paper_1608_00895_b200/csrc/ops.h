@@ -35,6 +35,9 @@ int pack_mask(const uint8_t *mask, int T, int B, int G, int Bg, int N, uint8_t *
 int copy_rows(const float *src, long lds, long rows, int cols, float *dst, long ldd, cudaStream_t st);
 int pad_halves(const float *src, int H, int Hq, long rows, float *dst, cudaStream_t st);
 int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, int accum, cudaStream_t st);
+// one-thread kernel: returns once *flag >= target (acquire) or after 2 ms (placement guard of
+// side-stream work behind a recurrence launch)
+int wait_count(const uint32_t *flag, uint32_t target, cudaStream_t st);
 int sgd(float *theta, float *grad, long n, float lr, int zero, cudaStream_t st);
 
 }  // namespace blstm

@@ -9,10 +9,12 @@
 namespace blstm {
 
 static long g_launches = 0;
-static bool g_prof_on = false;
+static int g_prof_on = 0;  // 0 off, 1 categories 0-2, 2 also helper kernels (timeline)
 struct ProfRec {
     int cat;
     cudaEvent_t e0, e1;
+    cudaStream_t st;
+    int a, b, c;
 };
 static std::vector<ProfRec> g_recs;   // recorded launches since enable
 static std::vector<cudaEvent_t> g_pool;
@@ -32,9 +34,9 @@ static cudaEvent_t pool_event() {
     return g_pool[g_pool_used++];
 }
 
-int prof_begin(int cat, cudaStream_t st) {
-    if (!g_prof_on || g_suspend > 0) return -1;
-    ProfRec r{cat, pool_event(), pool_event()};
+int prof_begin(int cat, cudaStream_t st, int a, int b, int c) {
+    if (!g_prof_on || g_suspend > 0 || (cat == PROF_OTHER && g_prof_on < 2)) return -1;
+    ProfRec r{cat, pool_event(), pool_event(), st, a, b, c};
     if (!r.e0 || !r.e1) return -1;
     cudaEventRecord(r.e0, st);
     g_recs.push_back(r);
@@ -52,7 +54,7 @@ using namespace blstm;
 extern "C" long blstm_launch_count(void) { return g_launches; }
 
 extern "C" int blstm_profile_enable(int on) {
-    g_prof_on = on != 0;
+    g_prof_on = on < 0 ? 0 : on;
     g_recs.clear();
     g_pool_used = 0;
     return 0;
@@ -72,4 +74,24 @@ extern "C" int blstm_profile_read(int cat, double *total_ms, long *launches) {
     if (total_ms) *total_ms = tot;
     if (launches) *launches = n;
     return 0;
+}
+
+extern "C" int blstm_profile_timeline(double *rec, int max_recs) {
+    if (g_recs.empty()) return 0;
+    std::vector<cudaStream_t> streams;
+    int n = 0;
+    for (const ProfRec &r : g_recs) {
+        if (n >= max_recs) break;
+        if (cudaEventSynchronize(r.e1) != cudaSuccess) return BLSTM_ERR_CUDA;
+        float t0 = 0.f, t1 = 0.f;
+        if (cudaEventElapsedTime(&t0, g_recs[0].e0, r.e0) != cudaSuccess) return BLSTM_ERR_CUDA;
+        if (cudaEventElapsedTime(&t1, g_recs[0].e0, r.e1) != cudaSuccess) return BLSTM_ERR_CUDA;
+        int si = 0;
+        while (si < (int)streams.size() && streams[si] != r.st) ++si;
+        if (si == (int)streams.size()) streams.push_back(r.st);
+        double *o = rec + 7L * n;
+        o[0] = r.cat; o[1] = si; o[2] = t0; o[3] = t1; o[4] = r.a; o[5] = r.b; o[6] = r.c;
+        ++n;
+    }
+    return n;
 }
