@@ -35,6 +35,8 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
            "-Xlinker", "-rpath=" + os.path.join(nd, "lib"),
            "-o", tmp] + srcs
+    for f in os.environ.get("BLSTM_NVCC_EXTRA", "").split():  # experiment builds (e.g. -DBLSTM_WAIT_HINT_NS=0)
+        cmd.insert(1, f)
     if trace:
         cmd.insert(1, "-DBLSTM_TRACE")
         if os.environ.get("BLSTM_TRACE_CTA"):  # trace another CTA than 0 (e.g. 1: an odd pair CTA)

@@ -58,12 +58,33 @@ DEVI uint64_t globaltimer_ns() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+// try_wait with a suspend-time hint: a thread whose phase is not complete is parked by the
+// hardware until the phase completes (or the hint expires) instead of re-polling; a polling warp
+// takes issue slots from the warps of its sub-partition that do the step's work (measured: the
+// MMA-completion wait alone was ~70 instructions per warp per step of the forward recurrence)
+#ifndef BLSTM_WAIT_HINT_NS
+#define BLSTM_WAIT_HINT_NS 10000000u
+#endif
+DEVI bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "r"(BLSTM_WAIT_HINT_NS)
+        : "memory");
+    return ok != 0;
+}
 // Watchdog for every spin: a synchronisation bug traps (kernel error) instead of hanging the GPU.
 constexpr uint64_t SPIN_TIMEOUT_NS = 20ull * 1000 * 1000 * 1000;
-// (the timer is read every 256 polls only: each read is an issue slot on the critical path)
 DEVI void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait(a, parity)) return;
+#if BLSTM_WAIT_HINT_NS
+    const uint64_t t0 = globaltimer_ns();
+    while (!mbar_try_wait_sleep(a, parity))
+        if (globaltimer_ns() - t0 > SPIN_TIMEOUT_NS) __trap();
+#else
+    // (the timer is read every 256 polls only: each read is an issue slot on the critical path)
     uint64_t t0 = 0;
     for (uint32_t n = 1; !mbar_try_wait(a, parity); ++n) {
         if ((n & 255) == 0) {
@@ -72,6 +93,7 @@ DEVI void mbar_wait(uint64_t *bar, uint32_t parity) {
             else if (t - t0 > SPIN_TIMEOUT_NS) __trap();
         }
     }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -285,10 +307,24 @@ DEVI bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+DEVI bool mbar_try_wait_cluster_sleep(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "r"(BLSTM_WAIT_HINT_NS)
+        : "memory");
+    return ok != 0;
+}
 // wait for a phase completed by a remote (cluster-scope) arrive
 DEVI void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait_cluster(a, parity)) return;
+#if BLSTM_WAIT_HINT_NS
+    const uint64_t t0 = globaltimer_ns();
+    while (!mbar_try_wait_cluster_sleep(a, parity))
+        if (globaltimer_ns() - t0 > SPIN_TIMEOUT_NS) __trap();
+#else
     uint64_t t0 = 0;
     for (uint32_t n = 1; !mbar_try_wait_cluster(a, parity); ++n) {
         if ((n & 255) == 0) {
@@ -297,6 +333,7 @@ DEVI void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
             else if (t - t0 > SPIN_TIMEOUT_NS) __trap();
         }
     }
+#endif
 }
 
 // a warp-uniform copy of v (lane 0's), so the compiler may keep it in a uniform register

@@ -404,11 +404,13 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         }
         if (s > 0) fph ^= 1u << b;
         if (s > 0) store_step(t_prev, frm_prev, fmq_prev);
+        TRACE(12);
         // this step's Z block and mask row (issued two steps ahead)
         mbar_wait(&bars[6 + b], (s >> 1) & 1);
         const uint8_t *zs = zin + b * ZSLOT;
         // frame-valid bits of this warp's columns (lane i reads the mask byte of column i)
         const uint32_t frm = __ballot_sync(0xffffffffu, l < NQ && zs[ZB + nq0 + l] != 0);
+        TRACE(13);
         mbar_wait(&bars[1], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();

@@ -21,7 +21,8 @@ from paper_1608_00895_b200.train import StackTrainer  # noqa: E402
 
 SLOTS = 16
 # (slot sequence in program order, label of the phase ending at that slot)
-FWD = [(0, None), (11, "wait own half of h"), (1, "wait partner relay"), (2, "MMA issue"), (3, "stores + MMA wait"),
+FWD = [(0, None), (11, "wait own half of h"), (1, "wait partner relay"), (2, "MMA issue"), (12, "prev-step HBM stores"),
+       (13, "Z wait + mask ballot"), (3, "MMA wait"),
        (8, "TMEM ld"), (9, "gate activations"), (10, "cell update + staging"), (7, "proxy fence"),
        (4, "bulk_wait + __syncthreads"), (5, "send h + arm"), (6, "Z prefetch")]
 BWD = [(0, None), (1, "issue next-step loads"), (2, "wait P + gather"), (8, "wait inputs + smem reads"), (9, "dA math + smem"),
