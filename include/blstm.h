@@ -228,6 +228,15 @@ int dp_allreduce_grads(dp_comm *c, float *grad, size_t n, void *stream);
  * "combined into a single set of parameters by averaging". */
 int dp_average_params(dp_comm *c, float *theta, size_t n, void *stream);
 int dp_comm_destroy(dp_comm *c);
+/*
+ * N replicas resident on ONE device (a single-GPU simulation of N workers, SURVEY.md §8(f)
+ * NEXT-1): x_r <- scale * sum_{q<n} x_q for every r < n, summed in replica order 0..n-1 in
+ * fp32, so all replicas receive identical bits.  scale = 1/n is the paper's parameter
+ * averaging; scale = 1 is the sync-mode gradient sum (R8).
+ *   ptrs: HOST array of n DEVICE pointers (16-byte aligned, pairwise distinct), 1 <= n <= 16
+ *   len: elements per replica.  Errors: BLSTM_ERR_ARG, BLSTM_ERR_ALIGN.
+ */
+int blstm_reduce_replicas(float *const *ptrs, int n, size_t len, float scale, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* Test hook: the tcgen05 GEMM used by every dense contraction of the path.   */

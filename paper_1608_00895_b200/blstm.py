@@ -74,6 +74,7 @@ _SIGS = {
     "dp_allreduce_grads": (_i, [_vp, _vp, _sz, _vp]),
     "dp_average_params": (_i, [_vp, _vp, _sz, _vp]),
     "dp_comm_destroy": (_i, [_vp]),
+    "blstm_reduce_replicas": (_i, [ctypes.POINTER(ctypes.c_void_p), _i, _sz, ctypes.c_float, _vp]),
     "blstm_gemm_f16": (_i, [_i, _i, _i, _vp, ctypes.c_long, _i, _vp, ctypes.c_long, _i, _vp, ctypes.c_long,
                             ctypes.c_float, _i, _vp, _vp]),
     "blstm_launch_count": (ctypes.c_long, []),
@@ -270,6 +271,13 @@ def dp_allreduce_grads(comm, grad, stream=None):
 
 def dp_average_params(comm, theta, stream=None):
     _check("dp_average_params", lib().dp_average_params(comm, _p(theta), theta.numel(), _stream(stream)))
+
+
+def blstm_reduce_replicas(tensors, scale: float, stream=None):
+    """x_r <- scale * sum_q x_q for every tensor (all the same length, one device)."""
+    arr = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+    _check("blstm_reduce_replicas", lib().blstm_reduce_replicas(arr, len(tensors), tensors[0].numel(), float(scale),
+                                                                  _stream(stream)))
 
 
 def dp_comm_destroy(comm):

@@ -743,6 +743,21 @@ extern "C" int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_des
     return 0;
 }
 
+extern "C" int blstm_reduce_replicas(float *const *ptrs, int n, size_t len, float scale, void *stream) {
+    if (!ptrs || n < 1 || n > MAX_REPLICAS) return fail(BLSTM_ERR_ARG, "need 1 <= n <= %d replicas", MAX_REPLICAS);
+    ReplicaPtrs rp{};
+    for (int r = 0; r < n; ++r) {
+        if (!ptrs[r]) return fail(BLSTM_ERR_ARG, "null replica pointer %d", r);
+        if (!al16(ptrs[r])) return fail(BLSTM_ERR_ALIGN, "replica %d not 16-byte aligned", r);
+        for (int q = 0; q < r; ++q)
+            if (ptrs[q] == ptrs[r]) return fail(BLSTM_ERR_ARG, "replicas %d and %d alias", q, r);
+        rp.p[r] = ptrs[r];
+    }
+    if (len == 0) return 0;
+    TRY(reduce_replicas(rp, n, (long)len, scale, (cudaStream_t)stream), "reduce_replicas");
+    return 0;
+}
+
 extern "C" int blstm_gemm_f16(int M, int N, int K, const void *A, long lda, int a_mn, const void *B, long ldb,
                               int b_mn, float *C, long ldc, float alpha, int beta, const float *bias, void *stream) {
     if (!A || !B || !C || M < 0 || N < 0 || K < 1) return fail(BLSTM_ERR_ARG, "blstm_gemm_f16: bad argument");

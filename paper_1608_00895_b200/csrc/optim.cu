@@ -238,6 +238,39 @@ int grid_for_tiles(long n4) {
 
 int opt_norm_partials() { return 148 * 8; }
 
+// --- replicas on one device: x_r <- scale * sum_q x_q for every r (§4.1 P:209-211:
+// "combined into a single set of parameters by averaging"; scale = 1/n).  Summed in fixed
+// replica order 0..n-1 in fp32, so every replica receives the same bits.
+__global__ void __launch_bounds__(OPT_THREADS) reduce_replicas_kernel(const __grid_constant__ ReplicaPtrs rp, int n,
+                                                                      long len, float scale) {
+    const long n4 = len >> 2;
+    const long stride = (long)gridDim.x * OPT_THREADS;
+    for (long q = blockIdx.x * (long)OPT_THREADS + threadIdx.x; q < n4; q += stride) {
+        float4 acc = ld4(rp.p[0], q);
+        for (int r = 1; r < n; ++r) {
+            const float4 v = ld4(rp.p[r], q);
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        acc.x *= scale; acc.y *= scale; acc.z *= scale; acc.w *= scale;
+        for (int r = 0; r < n; ++r) st4(rp.p[r], q, acc);
+    }
+    for (long i = (n4 << 2) + blockIdx.x * (long)OPT_THREADS + threadIdx.x; i < len; i += stride) {
+        float acc = rp.p[0][i];
+        for (int r = 1; r < n; ++r) acc += rp.p[r][i];
+        acc *= scale;
+        for (int r = 0; r < n; ++r) rp.p[r][i] = acc;
+    }
+}
+
+int reduce_replicas(const ReplicaPtrs &rp, int n, long len, float scale, cudaStream_t st) {
+    const long n4 = len >> 2;
+    long grid = (n4 + OPT_THREADS - 1) / OPT_THREADS;
+    grid = grid < 1 ? 1 : (grid > 148L * 8 ? 148L * 8 : grid);
+    reduce_replicas_kernel<<<(int)grid, OPT_THREADS, 0, st>>>(rp, n, len, scale);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 int opt_update(int rule, float *theta, float *grad, float *s0, float *s1, long n, const OptArgs &a,
                double max_norm, const OptBiasTable &tab, double *partial, int zero, cudaStream_t st) {
     int npartial = 0;

@@ -26,4 +26,12 @@ int opt_norm_partials();
 int opt_update(int rule, float *theta, float *grad, float *s0, float *s1, long n, const OptArgs &a,
                double max_norm, const OptBiasTable &tab, double *partial, int zero, cudaStream_t st);
 
+constexpr int MAX_REPLICAS = 16;
+struct ReplicaPtrs {
+    float *p[MAX_REPLICAS];
+};
+// x_r <- scale * sum_{q<n} x_q for r < n (fixed order; every replica gets identical bits);
+// pointers 16-byte aligned
+int reduce_replicas(const ReplicaPtrs &rp, int n, long len, float scale, cudaStream_t st);
+
 }  // namespace blstm

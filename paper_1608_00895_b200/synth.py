@@ -222,3 +222,35 @@ def random_small_case(seed: int, T: int, B: int, D: int, H: int,
     dcT = g.standard_normal((B, H)).astype(np.float32)
     return dict(x=x, mask=mask, W=W, R=R, b=b, h0=h0, c0=c0, dy=dy, dhT=dhT,
                 dcT=dcT, lengths=lengths)
+
+
+# ----------------------------------------------------------------------------
+# NEXT-1: a synthetic labelling task with a learnable answer, for the
+# convergence study of the paper's K-step parameter averaging (§4.1).
+# ----------------------------------------------------------------------------
+ECHO_SYMBOLS = 10   # input alphabet 1..V
+ECHO_DELAY = 3      # label at frame t = input symbol at frame t - k ("delayed echo, k=3")
+
+
+def echo_batch(T: int, B: int, D: int, seed: int, V: int = ECHO_SYMBOLS, delay: int = ECHO_DELAY,
+               min_len: Optional[int] = None) -> Batch:
+    """Delayed echo: symbol s_t ~ U{1..V} per frame, x_t = one-hot(s_t) in dims 0..V-1 plus
+    N(0, 0.1^2) noise in the other D-V dims; label_t = s_{t-delay} (0 = "blank" for t < delay);
+    K = V + 1 classes.  Variable lengths U{min_len..T} (one sequence of length T), trailing
+    padding (x = 0, label 0)."""
+    assert D > V
+    g = rng(seed)
+    lo = min_len if min_len is not None else max(delay + 1, T // 2)
+    lengths = g.integers(lo, T + 1, size=B).astype(np.int32)
+    lengths[g.integers(0, B)] = T
+    mask = mask_from_lengths(T, lengths)
+    s = g.integers(1, V + 1, size=(T, B)).astype(np.int32)
+    x = np.zeros((T, B, D), np.float32)
+    x[..., V:] = (0.1 * g.standard_normal((T, B, D - V))).astype(np.float32)
+    tt, bb = np.meshgrid(np.arange(T), np.arange(B), indexing="ij")
+    x[tt, bb, s - 1] = 1.0
+    labels = np.zeros((T, B), np.int32)
+    labels[delay:] = s[:-delay]
+    x[mask == 0] = 0.0
+    labels[mask == 0] = 0
+    return Batch(x=x, mask=mask, labels=labels, lengths=lengths)

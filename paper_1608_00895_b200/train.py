@@ -219,3 +219,67 @@ def dp_comm_from_torch(rank: int, world: int):
     t = torch.tensor(list(uid), dtype=torch.uint8, device=f"cuda:{torch.cuda.current_device()}")
     dist.broadcast(t, src=0)
     return blstm.dp_comm_init(world, rank, bytes(t.cpu().tolist()))
+
+
+# ----------------------------------------------------------------------------
+# N workers simulated on one GPU
+# ----------------------------------------------------------------------------
+class SimulatedDP:
+    """N data-parallel workers on ONE device: the same schedule as dp_step, with the exchange
+    done by blstm_reduce_replicas over the workers' device buffers instead of NCCL.
+
+    sync   : every step the N local gradients are summed (R8: one big batch, unscaled), then
+             every worker applies the same update (the replicas stay identical);
+    avg(K) : every worker applies its own update each step; after every K-th step the
+             parameters are averaged, theta_r <- (1/N) sum_q theta_q.
+    Each worker trains on its own batches: batches[r] is worker r's list, cycled.
+    """
+
+    def __init__(self, cfg, params, batches, device, sched: DPSchedule, lr: float, opt: Optional[dict] = None):
+        from . import blstm
+        self.blstm, self.sched, self.N = blstm, sched, len(batches)
+        self.batches = batches
+        self.workers = [StackTrainer(cfg, params, b[0], device, lr=lr, opt=opt) for b in batches]
+        self.steps_done = 0
+
+    def step(self):
+        k = self.steps_done
+        for r, w in enumerate(self.workers):
+            bl = self.batches[r]
+            if len(bl) > 1:
+                w.set_batch(bl[k % len(bl)])
+        if self.sched.grads_summed():
+            for w in self.workers:
+                w._grad(w.theta, w.grad)
+            if self.N > 1:
+                self.blstm.blstm_reduce_replicas([w.grad for w in self.workers], 1.0)
+            for w in self.workers:
+                w._update(w.theta, w.grad)
+        else:
+            for w in self.workers:
+                w._grad(w.theta, w.grad)
+                w._update(w.theta, w.grad)
+            if self.N > 1 and self.sched.average_after(k):
+                self.blstm.blstm_reduce_replicas([w.theta for w in self.workers], 1.0 / self.N)
+        self.steps_done += 1
+
+    def consensus(self):
+        """theta of the model the workers agree on: every replica after an averaging step (or in
+        sync mode); otherwise worker 0's."""
+        return self.workers[0].theta
+
+
+class Evaluator:
+    """Loss and frame errors of a parameter vector on a fixed batch (forward + head through
+    blstm_stack_fwd_bwd into a scratch gradient)."""
+
+    def __init__(self, cfg, params, batch, device):
+        self.tr = StackTrainer(cfg, params, batch, device)
+
+    def __call__(self, theta):
+        t = self.tr
+        t.theta.copy_(theta)
+        t.grad.zero_()
+        t._grad(t.theta, t.grad)
+        t.torch.cuda.synchronize()
+        return float(t.loss.item()), int(t.ferr.item()), t.valid_frames
