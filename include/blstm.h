@@ -165,6 +165,19 @@ int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta, float *gr
 int blstm_stack_fwd(const blstm_stack_desc *d, const float *theta, const float *x, const uint8_t *mask,
                     float *Y, float *C, void *workspace, size_t workspace_bytes, void *stream);
 
+/*
+ * Chunked batches from a device-resident corpus (§4: sequences chunked
+ * into "(possibly overlapping) segments of constant length").  Column b of the
+ * batch is the chunk of clen[b] frames starting at corpus frame cstart[b]:
+ *   frames [F, D] fp32, frame_labels [F] int32 or NULL: the corpus (sequences concatenated)
+ *   cstart [B] int64, clen [B] int32 (0 <= clen <= T; 0 = empty column): DEVICE
+ *   x [T, B, D] fp32, mask [T, B] uint8, labels [T, B] int32 or NULL: DEVICE outputs,
+ *   x = 0 / mask = 0 / label = 0 at t >= clen[b].  Bit-exact copies (no arithmetic).
+ * Errors: BLSTM_ERR_ARG.  Frame indices are not range-checked (the caller's table).
+ */
+int blstm_gather_chunks(const float *frames, const int32_t *frame_labels, int D, const int64_t *cstart,
+                        const int32_t *clen, int B, int T, float *x, uint8_t *mask, int32_t *labels, void *stream);
+
 /* SGD (§4.3): theta -= lr * grad over n elements (gradients unscaled,
  * P:253-254); zero_grad != 0 then sets grad = 0.  DEVICE pointers. */
 int sgd_update(float *theta, float *grad, size_t n, float lr, int zero_grad, void *stream);

@@ -135,8 +135,14 @@ def unpack(theta: np.ndarray, L: int, D: int, H: int, K: int):
     return out
 
 
+def dropout_keep(seed: int, site: int, i: int, p: float) -> bool:
+    """oracle.c ref_dropout_keep: the counter-based keep decision of input dropout (R20)."""
+    return bool(lib().ref_dropout_keep(ctypes.c_uint32(seed), site, ctypes.c_uint64(i), ctypes.c_double(p)))
+
+
 def blstm_step(theta, x, mask, L: int, H: int, K: int, labels=None, dy_top=None,
-               lr: float = 0.0, want_states: bool = False, want_dx: bool = False):
+               lr: float = 0.0, want_states: bool = False, want_dx: bool = False,
+               dropout: float = 0.0, seed: int = 0):
     """One training step of the L-layer BLSTM (+ CE head when K > 0).
 
     Returns dict loss, frame_errors, grad (flat), theta_new, and optionally
@@ -158,10 +164,10 @@ def blstm_step(theta, x, mask, L: int, H: int, K: int, labels=None, dy_top=None,
     if K > 0:
         labels = np.ascontiguousarray(labels, dtype=np.int32)
         lab = labels.ctypes.data_as(_i32p)
-    rc = lib().ref_blstm_step(L, D, H, K, T, B, _d(theta), _d(x), mask.ctypes.data_as(_u8p),
-                              lab, _d(dy_top), ctypes.c_double(lr), ctypes.byref(loss),
-                              ctypes.byref(ferr), _d(grad), _d(Ys), _d(Cs), _d(dX1),
-                              _d(theta_new))
+    rc = lib().ref_blstm_step_ex(L, D, H, K, T, B, _d(theta), _d(x), mask.ctypes.data_as(_u8p),
+                                 lab, _d(dy_top), ctypes.c_double(lr), ctypes.byref(loss),
+                                 ctypes.byref(ferr), _d(grad), _d(Ys), _d(Cs), _d(dX1),
+                                 _d(theta_new), ctypes.c_double(dropout), ctypes.c_uint32(seed))
     assert rc == 0, rc
     return dict(loss=loss.value, frame_errors=ferr.value, grad=grad, theta_new=theta_new,
                 Ys=Ys, Cs=Cs, dX1=dX1)

@@ -273,14 +273,50 @@ long ref_param_layout(int L, int D, int H, int K, long *offs)
  * states, dX1 [T,B,D] gradient of the input, theta_new = theta - lr*grad.
  * loss / frame_errors may be NULL.
  */
-int ref_blstm_step(int L, int D, int H, int K, int T, int B,
-                   const double *theta, const double *x, const uint8_t *mask,
-                   const int32_t *labels, const double *dy_top,
-                   double lr, double *loss, long *frame_errors,
-                   double *grad, double *Ys, double *Cs, double *dX1,
-                   double *theta_new)
+/*
+ * Input dropout (§4.3: "dropout on the layer inputs of any layer"; DESIGN.md
+ * reading R20).  The input of layer l (l = 0: x; l >= 1: Y_{l-1} = [y_f | y_b]) and, with a head,
+ * the head's input Y_{L-1} (site L) are replaced by X~ = X * keep / (1 - p); X~ feeds the layer
+ * (so dW = X~^T dA) and the gradient reaching X is dX = dX~ * keep / (1 - p).  keep of element
+ * (row r = t*B + b, feature j) of site s is the counter-based draw
+ *     h = mix(seed + 0x9E3779B9 * (s + 1));  h = mix(h ^ lo32(i));  h = mix(h ^ hi32(i)),
+ *     i = r * D_s + j,  keep  <=>  h >= floor(p * 2^32),
+ * mix = the "lowbias32" integer finalizer.  Padded frames are dropped or kept alike: their
+ * inputs are 0 and their gradients 0.
+ */
+static uint32_t mix32(uint32_t x)
 {
-    if (L < 1 || B < 1 || H < 1 || T < 0) return -1;
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return x;
+}
+int ref_dropout_keep(uint32_t seed, int site, uint64_t i, double p)
+{
+    uint32_t h = mix32(seed + 0x9E3779B9u * (uint32_t)(site + 1));
+    h = mix32(h ^ (uint32_t)i);
+    h = mix32(h ^ (uint32_t)(i >> 32));
+    const uint32_t thr = (uint32_t)floor(p * 4294967296.0);
+    return h >= thr;
+}
+/* X~ = X * keep / (1-p) over rows x Dl (site s) */
+static void ref_dropout_apply(double *X, size_t rows, int Dl, int site, double p, uint32_t seed)
+{
+    const double sc = 1.0 / (1.0 - p);
+    for (size_t r = 0; r < rows; ++r)
+        for (int j = 0; j < Dl; ++j) {
+            const size_t i = r * (size_t)Dl + j;
+            X[i] = ref_dropout_keep(seed, site, i, p) ? X[i] * sc : 0.0;
+        }
+}
+
+int ref_blstm_step_ex(int L, int D, int H, int K, int T, int B,
+                      const double *theta, const double *x, const uint8_t *mask,
+                      const int32_t *labels, const double *dy_top,
+                      double lr, double *loss, long *frame_errors,
+                      double *grad, double *Ys, double *Cs, double *dX1,
+                      double *theta_new, double p_drop, uint32_t seed)
+{
+    if (L < 1 || B < 1 || H < 1 || T < 0 || p_drop < 0.0 || p_drop >= 1.0) return -1;
+    const int drop = p_drop > 0.0;
     const size_t TB = (size_t)T * B, W2 = 2 * (size_t)H;
     long *offs = (long *)malloc(sizeof(long) * (6 * L + 2));
     const long P = ref_param_layout(L, D, H, K, offs);
@@ -288,10 +324,18 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
 
     /* per-layer, per-direction saved state */
     double **Xin = (double **)calloc(L + 1, sizeof(double *));
+    double **Xd = (double **)calloc(L + 1, sizeof(double *)); /* the inputs the layers see */
     double **sv = (double **)calloc(8 * L, sizeof(double *)); /* y,C,G,Hp,Cp per dir */
     Xin[0] = (double *)x;
     for (int l = 0; l < L; ++l) {
         const int Dl = l == 0 ? D : 2 * H;
+        if (drop) {
+            Xd[l] = (double *)malloc(sizeof(double) * TB * Dl);
+            memcpy(Xd[l], Xin[l], sizeof(double) * TB * Dl);
+            ref_dropout_apply(Xd[l], TB, Dl, l, p_drop, seed);
+        } else {
+            Xd[l] = Xin[l];
+        }
         double *Y = (double *)malloc(sizeof(double) * TB * W2);
         for (int d = 0; d < 2; ++d) {
             const int e = 6 * l + 3 * d;
@@ -300,7 +344,7 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
             double *Gs = (double *)malloc(sizeof(double) * TB * 4 * H);
             double *Hp = (double *)malloc(sizeof(double) * TB * H);
             double *Cp = (double *)malloc(sizeof(double) * TB * H);
-            ref_lstm_fwd(T, B, Dl, H, d == 0 ? 1 : -1, Xin[l], mask,
+            ref_lstm_fwd(T, B, Dl, H, d == 0 ? 1 : -1, Xd[l], mask,
                          theta + offs[e], theta + offs[e + 1], theta + offs[e + 2],
                          NULL, NULL, y, C, NULL, NULL, Gs, Hp, Cp);
             for (size_t r = 0; r < TB; ++r)
@@ -324,7 +368,14 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
         double *dlog = (double *)calloc(TB * (size_t)K, sizeof(double));
         double *rl = (double *)calloc(TB, sizeof(double));
         long *re = (long *)calloc(TB, sizeof(long));
-        const double *YL = Xin[L];
+        if (drop) {
+            Xd[L] = (double *)malloc(sizeof(double) * TB * W2);
+            memcpy(Xd[L], Xin[L], sizeof(double) * TB * W2);
+            ref_dropout_apply(Xd[L], TB, (int)W2, L, p_drop, seed);
+        } else {
+            Xd[L] = Xin[L];
+        }
+        const double *YL = Xd[L];
 #pragma omp parallel for schedule(static)
         for (long r = 0; r < (long)TB; ++r) {
             if (!mask[r]) continue;
@@ -377,6 +428,7 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
                 dY[(size_t)r * W2 + j] = acc;
             }
         free(dlog); free(rl); free(re);
+        if (drop) ref_dropout_apply(dY, TB, (int)W2, L, p_drop, seed); /* dY_{L-1} = dY~ * keep/(1-p) */
     } else {
         memcpy(dY, dy_top, sizeof(double) * TB * W2);
     }
@@ -393,7 +445,7 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
             double **p = sv + 8 * l + 4 * d;
             for (size_t r = 0; r < TB; ++r)
                 for (int j = 0; j < H; ++j) dyd[r * H + j] = dY[r * W2 + (size_t)d * H + j];
-            ref_lstm_bwd(T, B, Dl, H, d == 0 ? 1 : -1, Xin[l], mask,
+            ref_lstm_bwd(T, B, Dl, H, d == 0 ? 1 : -1, Xd[l], mask,
                          theta + offs[e], theta + offs[e + 1],
                          p[0], p[1], p[2], p[3], dyd, NULL, NULL,
                          dxd, grad + offs[e], grad + offs[e + 1], grad + offs[e + 2],
@@ -401,6 +453,7 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
             for (size_t i = 0; i < TB * (size_t)Dl; ++i) dXl[i] += dxd[i];
         }
         free(dxd); free(dA);
+        if (drop) ref_dropout_apply(dXl, TB, Dl, l, p_drop, seed); /* gradient of the undropped input */
         if (l == 0) {
             if (dX1) memcpy(dX1, dXl, sizeof(double) * TB * D);
             free(dXl);
@@ -416,13 +469,26 @@ int ref_blstm_step(int L, int D, int H, int K, int T, int B,
     if (theta_new)
         for (long i = 0; i < P; ++i) theta_new[i] = theta[i] - lr * grad[i];
 
+    for (int l = 0; l <= L; ++l)
+        if (drop && Xd[l]) free(Xd[l]);
     for (int l = 0; l < L; ++l) {
         free(Xin[l + 1]);
         for (int d = 0; d < 2; ++d)
             for (int q = 0; q < 4; ++q) free(sv[8 * l + 4 * d + q]);
     }
-    free(Xin); free(sv); free(offs);
+    free(Xin); free(Xd); free(sv); free(offs);
     return 0;
+}
+
+int ref_blstm_step(int L, int D, int H, int K, int T, int B,
+                   const double *theta, const double *x, const uint8_t *mask,
+                   const int32_t *labels, const double *dy_top,
+                   double lr, double *loss, long *frame_errors,
+                   double *grad, double *Ys, double *Cs, double *dX1,
+                   double *theta_new)
+{
+    return ref_blstm_step_ex(L, D, H, K, T, B, theta, x, mask, labels, dy_top, lr, loss, frame_errors, grad, Ys,
+                             Cs, dX1, theta_new, 0.0, 0u);
 }
 
 /* SGD (§4.3): theta -= lr * grad, gradients unscaled. */

@@ -74,6 +74,7 @@ _SIGS = {
     "dp_allreduce_grads": (_i, [_vp, _vp, _sz, _vp]),
     "dp_average_params": (_i, [_vp, _vp, _sz, _vp]),
     "dp_comm_destroy": (_i, [_vp]),
+    "blstm_gather_chunks": (_i, [_vp, _vp, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
     "blstm_reduce_replicas": (_i, [ctypes.POINTER(ctypes.c_void_p), _i, _sz, ctypes.c_float, _vp]),
     "blstm_gemm_f16": (_i, [_i, _i, _i, _vp, ctypes.c_long, _i, _vp, ctypes.c_long, _i, _vp, ctypes.c_long,
                             ctypes.c_float, _i, _vp, _vp]),
@@ -271,6 +272,12 @@ def dp_allreduce_grads(comm, grad, stream=None):
 
 def dp_average_params(comm, theta, stream=None):
     _check("dp_average_params", lib().dp_average_params(comm, _p(theta), theta.numel(), _stream(stream)))
+
+
+def blstm_gather_chunks(frames, frame_labels, D: int, cstart, clen, B: int, T: int, x, mask, labels=None,
+                        stream=None):
+    _check("blstm_gather_chunks", lib().blstm_gather_chunks(_p(frames), _p(frame_labels), D, _p(cstart), _p(clen), B,
+                                                            T, _p(x), _p(mask), _p(labels), _stream(stream)))
 
 
 def blstm_reduce_replicas(tensors, scale: float, stream=None):

@@ -743,6 +743,17 @@ extern "C" int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_des
     return 0;
 }
 
+extern "C" int blstm_gather_chunks(const float *frames, const int32_t *frame_labels, int D, const int64_t *cstart,
+                                   const int32_t *clen, int B, int T, float *x, uint8_t *mask, int32_t *labels,
+                                   void *stream) {
+    if (!frames || !cstart || !clen || !x || !mask || D < 1 || B < 1 || T < 0)
+        return fail(BLSTM_ERR_ARG, "blstm_gather_chunks: bad argument");
+    if ((long)T * B * D == 0) return 0;
+    TRY(gather_chunks(frames, frame_labels, D, cstart, clen, B, T, x, mask, labels, (cudaStream_t)stream),
+        "gather_chunks");
+    return 0;
+}
+
 extern "C" int blstm_reduce_replicas(float *const *ptrs, int n, size_t len, float scale, void *stream) {
     if (!ptrs || n < 1 || n > MAX_REPLICAS) return fail(BLSTM_ERR_ARG, "need 1 <= n <= %d replicas", MAX_REPLICAS);
     ReplicaPtrs rp{};

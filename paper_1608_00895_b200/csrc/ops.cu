@@ -421,6 +421,35 @@ int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, i
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
+// --- chunk gather (NEXT-4): batch tensors from a device-resident corpus -----------------------
+// one thread per (t, b, d): x[t][b][d] = frames[(start_b + t) * D + d] for t < len_b, else 0
+__global__ void gather_chunks_kernel(const float *__restrict__ frames, const int32_t *__restrict__ flab, int D,
+                                     const int64_t *__restrict__ cstart, const int32_t *__restrict__ clen, int B,
+                                     int T, float *__restrict__ x, uint8_t *__restrict__ mask,
+                                     int32_t *__restrict__ labels) {
+    const long total = (long)T * B * D;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+        const int d = (int)(e % D);
+        const long tb = e / D;
+        const int b = (int)(tb % B), t = (int)(tb / B);
+        const bool ok = t < clen[b];
+        const long f = cstart[b] + t;
+        x[e] = ok ? frames[f * D + d] : 0.f;
+        if (d == 0) {
+            mask[tb] = ok ? 1 : 0;
+            if (labels) labels[tb] = (ok && flab) ? flab[f] : 0;
+        }
+    }
+}
+int gather_chunks(const float *frames, const int32_t *flab, int D, const int64_t *cstart, const int32_t *clen, int B,
+                  int T, float *x, uint8_t *mask, int32_t *labels, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
+    gather_chunks_kernel<<<grid_for((long)T * B * D), 256, 0, st>>>(frames, flab, D, cstart, clen, B, T, x, mask,
+                                                                    labels);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 // --- placement guard: hold a stream until *flag >= target (or timeout_ns passed) -------------
 __global__ void wait_count_kernel(const uint32_t *flag, uint32_t target, unsigned long long timeout_ns) {
     const uint64_t t0 = globaltimer_ns();

@@ -38,6 +38,8 @@ int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, i
 // one-thread kernel: returns once *flag >= target (acquire) or after 2 ms (placement guard of
 // side-stream work behind a recurrence launch)
 int wait_count(const uint32_t *flag, uint32_t target, cudaStream_t st);
+int gather_chunks(const float *frames, const int32_t *flab, int D, const int64_t *cstart, const int32_t *clen, int B,
+                  int T, float *x, uint8_t *mask, int32_t *labels, cudaStream_t st);
 int sgd(float *theta, float *grad, long n, float lr, int zero, cudaStream_t st);
 
 }  // namespace blstm
