@@ -121,6 +121,13 @@ typedef struct {
     int T, B;     /* frames, batch (chunks) */
     int flags;    /* reserved, 0 */
     int precision;/* BLSTM_PREC_FP16 */
+    /* Input dropout of blstm_stack_fwd_bwd ("dropout on the layer inputs of any
+     * layer"; R20): 0 <= dropout < 1 is the drop probability of every element of every
+     * layer's input and of the head's input; dropout_seed selects the masks (a counter-based draw
+     * of (seed, site, element), reproducible; pass a new seed per step).  0 = off.
+     * blstm_stack_fwd (inference) never drops. */
+    float dropout;
+    uint32_t dropout_seed;
 } blstm_stack_desc;
 
 /*

@@ -36,7 +36,7 @@ class LstmDesc(ctypes.Structure):
 class StackDesc(ctypes.Structure):
     _fields_ = [("L", ctypes.c_int), ("D", ctypes.c_int), ("H", ctypes.c_int), ("K", ctypes.c_int),
                 ("T", ctypes.c_int), ("B", ctypes.c_int), ("flags", ctypes.c_int),
-                ("precision", ctypes.c_int)]
+                ("precision", ctypes.c_int), ("dropout", ctypes.c_float), ("dropout_seed", ctypes.c_uint32)]
 
 
 class OptParams(ctypes.Structure):
@@ -163,8 +163,8 @@ def lstm_desc(T, B, D, H, direction=1, ldx=None, ldy=None, flags=0, precision=BL
     return LstmDesc(T, B, D, H, direction, ldx or D, ldy or H, flags, precision)
 
 
-def stack_desc(L, D, H, K, T, B, flags=0, precision=BLSTM_PREC_FP16) -> StackDesc:
-    return StackDesc(L, D, H, K, T, B, flags, precision)
+def stack_desc(L, D, H, K, T, B, flags=0, precision=BLSTM_PREC_FP16, dropout=0.0, dropout_seed=0) -> StackDesc:
+    return StackDesc(L, D, H, K, T, B, flags, precision, dropout, dropout_seed)
 
 
 def lstm_workspace_bytes(desc: LstmDesc) -> int:

@@ -295,6 +295,7 @@ struct StackGeo {
     long TB;
     RecPlan pl;
     std::vector<int> Dn, Drows, rowmode;
+    Dropout dr;  // input dropout of the training step (R20); dr.on == 0: off
 };
 struct StackWS {
     size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, gsk,
@@ -317,6 +318,11 @@ static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
     if (!rec_supported(g.pl, d->H))
         return fail(BLSTM_ERR_UNSUPPORTED, "H=%d B=%d exceeds the recurrence kernels' on-chip capacity (Hq=%d N=%d)",
                     d->H, d->B, g.pl.Hq, g.pl.N);
+    if (!(d->dropout >= 0.f && d->dropout < 1.f)) return fail(BLSTM_ERR_ARG, "dropout must be in [0, 1)");
+    g.dr.on = d->dropout > 0.f;
+    g.dr.thr = (uint32_t)floor((double)d->dropout * 4294967296.0);
+    g.dr.seed = d->dropout_seed;
+    g.dr.scale = (float)(1.0 / (1.0 - (double)d->dropout));
     g.Dn.resize(g.L); g.Drows.resize(g.L); g.rowmode.resize(g.L);
     for (int l = 0; l < g.L; ++l) {
         g.Dn[l] = l == 0 ? g.Dp0 : 2 * g.Hq;
@@ -412,14 +418,16 @@ extern "C" size_t blstm_stack_workspace_bytes(const blstm_stack_desc *d) {
 }
 
 // forward of the whole stack; Yout [L,T,B,2H] / Cout [L,2,T,B,H] optional (parity view).
+// train: apply the input dropout of g.dr (sites 0..L-1 on the layer inputs, site L on the head's)
 static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const StackWS &w, uint8_t *ws,
                          const float *theta, const float *x, const uint8_t *mask, float *Yout, float *Cout,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool train = false) {
+    const bool drop = train && g.dr.on;
     std::vector<size_t> offs(6 * g.L + 2);
     param_layout(d, offs.data());
     const int Hq = g.Hq;
     __half *x16 = (__half *)(ws + w.x16);
-    TRY(cast_x_f16(x, g.D, g.D, x16, g.Dp0, g.TB, st), "cast_x");
+    TRY(cast_x_f16(x, g.D, g.D, x16, g.Dp0, g.TB, st, drop ? g.dr : Dropout{0, 0, 0, 1.f}), "cast_x");
     for (int l = 0; l < g.L; ++l) {
         const float *Wf = theta + offs[6 * l], *Rf = theta + offs[6 * l + 1], *bf = theta + offs[6 * l + 2];
         const float *Wb = theta + offs[6 * l + 3], *Rb = theta + offs[6 * l + 4], *bb = theta + offs[6 * l + 5];
@@ -445,6 +453,8 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     const bool overlap = overlap_env && side_ctas >= 8;
     if (overlap && gemm_prepare()) return fail(BLSTM_ERR_CUDA, "gemm_prepare");
     for (int l = 0; l < g.L; ++l) {
+        if (drop && l > 0)  // layer l's input = layer l-1's output, dropped in place (site l)
+            TRY(dropout_f16((__half *)(ws + w.y16[l - 1]), g.TB, g.H, Hq, l, g.dr, st), "dropout");
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
         const long lda = l == 0 ? g.Dp0 : 2L * Hq;
         GemmParams gp{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
@@ -516,7 +526,9 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     uint8_t *ws = (uint8_t *)workspace;
     std::vector<size_t> offs(6 * g.L + 2);
     const size_t nparam = param_layout(d, offs.data());
-    if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st)) return rc;
+    if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st, true)) return rc;
+    if (g.dr.on && g.K > 0)  // the head's input (site L)
+        TRY(dropout_f16((__half *)(ws + w.y16[g.L - 1]), g.TB, g.H, g.Hq, g.L, g.dr, st), "dropout");
 
     const int Hq = g.Hq;
     const float a = 1.f / (float)(1 << DA_SHIFT);
@@ -571,6 +583,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             "reduce_loss");
         GemmParams gd{(int)g.TB, 2 * Hq, g.Kp, dY[0], 2L * Hq, a, 0, nullptr, 0, 0};
         TRY(gemm_f16({dlog, g.Kp, 0}, {wo16, g.Kp, 0}, gd, 0, st), "gemm dY_top");
+        if (g.dr.on) TRY(dropout_f32(dY[0], g.TB, g.H, Hq, g.L, g.dr, st), "dropout dY_top");
         // the head's parameter gradients are off the critical path too: side stream (side_head)
         if (overlap) cudaEventRecord(evs[g.L + 1], st);
     } else {
@@ -658,6 +671,8 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         if (l > 0) {  // critical path: gradient of the layer below's output
             GemmParams gx{(int)g.TB, g.Dn[l], 8 * Hq, dY[1 - cur], 2L * Hq, a, 0, nullptr, 0, 0};
             TRY(gemm_f16({dA, 8L * Hq, 0}, {w16, 8L * Hq, 0}, gx, 0, st), "gemm dX");
+            // gradient of the undropped output of layer l-1 (site l)
+            if (g.dr.on) TRY(dropout_f32(dY[1 - cur], g.TB, g.H, Hq, l, g.dr, st), "dropout dX");
         }
         if (overlap) cudaEventRecord(evs[l], st);
         cur = 1 - cur;

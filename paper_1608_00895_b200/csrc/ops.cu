@@ -16,19 +16,59 @@ static int grid_for(long n, int block = 256, int cap = 148 * 16) {
     return g < 1 ? 1 : (int)g;
 }
 
-// --- x [rows, ldx] fp32 -> X16 [rows, Dp] fp16 (zero pad) ---------------------------------
+// --- input dropout draw (R20): lowbias32 finalizer over (seed, site, element) --------
+DEVI uint32_t mix32(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return x;
+}
+DEVI bool drop_keep(uint32_t seed, int site, unsigned long long i, uint32_t thr) {
+    uint32_t h = mix32(seed + 0x9E3779B9u * (uint32_t)(site + 1));
+    h = mix32(h ^ (uint32_t)i);
+    h = mix32(h ^ (uint32_t)(i >> 32));
+    return h >= thr;
+}
+
+// --- x [rows, ldx] fp32 -> X16 [rows, Dp] fp16 (zero pad; site-0 dropout when dr.on) ---------
 __global__ void cast_x_kernel(const float *__restrict__ x, long ldx, int D, __half *__restrict__ x16, int Dp,
-                              long rows) {
+                              long rows, Dropout dr) {
     const long n = rows * Dp;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
         const long r = i / Dp;
         const int k = (int)(i - r * Dp);
-        x16[i] = __float2half_rn(k < D ? x[r * ldx + k] : 0.f);
+        float v = k < D ? x[r * ldx + k] : 0.f;
+        if (dr.on && k < D) v = drop_keep(dr.seed, 0, (unsigned long long)r * D + k, dr.thr) ? v * dr.scale : 0.f;
+        x16[i] = __float2half_rn(v);
     }
 }
-int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, cudaStream_t st) {
+int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, cudaStream_t st, const Dropout &dr) {
     ProfScope ps_(PROF_OTHER, st);
-    cast_x_kernel<<<grid_for(rows * Dp), 256, 0, st>>>(x, ldx, D, x16, Dp, rows);
+    cast_x_kernel<<<grid_for(rows * Dp), 256, 0, st>>>(x, ldx, D, x16, Dp, rows, dr);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+// --- in-place dropout of a layer output (next layer's input) / its gradient -------------------
+template <typename V>
+__global__ void dropout_kernel(V *__restrict__ y, long rows, int H, int Hq, int site, Dropout dr) {
+    const long n = rows * 2 * H;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const long r = i / (2 * H);
+        const int f = (int)(i - r * 2 * H), dd = f >= H, u = f - dd * H;
+        V *p = y + r * 2 * Hq + dd * Hq + u;
+        const bool keep = drop_keep(dr.seed, site, (unsigned long long)i, dr.thr);
+        if constexpr (sizeof(V) == 2) *p = keep ? __float2half_rn(__half2float(*p) * dr.scale) : __float2half_rn(0.f);
+        else *p = keep ? *p * dr.scale : 0.f;
+    }
+}
+int dropout_f16(__half *y, long rows, int H, int Hq, int site, const Dropout &dr, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
+    dropout_kernel<__half><<<grid_for(rows * 2 * H), 256, 0, st>>>(y, rows, H, Hq, site, dr);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+int dropout_f32(float *y, long rows, int H, int Hq, int site, const Dropout &dr, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
+    dropout_kernel<float><<<grid_for(rows * 2 * H), 256, 0, st>>>(y, rows, H, Hq, site, dr);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }

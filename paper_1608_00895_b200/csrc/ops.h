@@ -7,7 +7,19 @@
 
 namespace blstm {
 
-int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, cudaStream_t st);
+// Input dropout (R20): element (row r, logical feature j) of site s is kept iff the
+// counter-based draw h(seed, s, r * width + j) >= thr; kept elements are scaled by `scale`.
+struct Dropout {
+    int on;
+    uint32_t thr, seed;
+    float scale;
+};
+int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, cudaStream_t st,
+               const Dropout &dr = Dropout{0, 0, 0, 1.f});
+// in place on a [rows, 2Hq] layer output (fp16) or input gradient (fp32): logical feature
+// d*H + u of column d*Hq + u (u < H), site `site`, width 2H
+int dropout_f16(__half *y, long rows, int H, int Hq, int site, const Dropout &dr, cudaStream_t st);
+int dropout_f32(float *y, long rows, int H, int Hq, int site, const Dropout &dr, cudaStream_t st);
 // rowmode 0: input rows are W rows (rows >= Drows are padding); 1: input rows are the padded
 // [fwd (Hq) | bwd (Hq)] halves of the layer below (row half*Hq + jj <-> W row half*H + jj).
 int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir, int Dn, int rowmode, __half *W16,

@@ -95,9 +95,9 @@ def compare_layer(got, ref, label=""):
 class Stack:
     """Device buffers + one call of blstm_stack_fwd_bwd / blstm_stack_fwd."""
 
-    def __init__(self, L, D, H, K, T, B):
+    def __init__(self, L, D, H, K, T, B, dropout=0.0, seed=0):
         self.L, self.D, self.H, self.K, self.T, self.B = L, D, H, K, T, B
-        self.desc = blstm.stack_desc(L, D, H, K, T, B)
+        self.desc = blstm.stack_desc(L, D, H, K, T, B, dropout=dropout, dropout_seed=seed)
         self.n, self.offs = blstm.blstm_param_offsets(self.desc)
         self.ws = torch.empty(blstm.blstm_stack_workspace_bytes(self.desc), dtype=torch.uint8, device=dev())
 
