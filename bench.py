@@ -244,6 +244,7 @@ def main():
     ap.add_argument("--avg-k", type=int, default=3)
     ap.add_argument("--lr", type=float, default=1e-5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dropout", type=float, default=0.0, help="input dropout of every layer (NEXT-4); 0 = off")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -264,7 +265,8 @@ def main():
     comm = dp_comm_from_torch(rank, world)
     cfg, params, batch = synth.make_workload(cfg, rank)
     tr = StackTrainer(cfg, params, batch, dev, lr=args.lr, comm=comm, world=world,
-                      sched=DPSchedule(args.dp_mode, args.avg_k if args.dp_mode == "avg" else 1))
+                      sched=DPSchedule(args.dp_mode, args.avg_k if args.dp_mode == "avg" else 1),
+                      dropout=args.dropout, dropout_seed=7 + 1000 * rank)
 
     def barrier():
         torch.cuda.synchronize()
@@ -358,7 +360,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f16 MMA operands / f32 accumulate+state", "data": "synthetic",
         "config": dict(workload_desc(cfg, world), valid_frames_per_gpu=V, dp_mode=args.dp_mode,
-                       **({"avg_k": args.avg_k} if args.dp_mode == "avg" else {})),
+                       **({"avg_k": args.avg_k} if args.dp_mode == "avg" else {}),
+                       **({"input_dropout": args.dropout} if args.dropout > 0 else {})),
         "roofline": roof,
         "kernel_ms_per_step": {cats[c]: prof[c][0] / args.steps for c in prof},
         "roofline_by_kernel": {cats[c]: kernel_roofline(c, prof[c][0], prof[c][1], cfg, tr.valid_frames, peaks, args.steps)

@@ -48,27 +48,56 @@ int cast_x_f16(const float *x, long ldx, int D, __half *x16, int Dp, long rows, 
 }
 
 // --- in-place dropout of a layer output (next layer's input) / its gradient -------------------
+// element keep draw with the (seed, site) part precomputed: h0 = mix32(seed + 0x9E3779B9 (site+1))
+DEVI bool drop_keep_h0(uint32_t h0, unsigned long long i, uint32_t thr) {
+    uint32_t h = mix32(h0 ^ (uint32_t)i);
+    h = mix32(h ^ (uint32_t)(i >> 32));
+    return h >= thr;
+}
+// VEC elements (16 bytes) per thread per iteration over the padded row [2Hq]; physical column
+// c holds logical feature c (c < H) or H + c - Hq (Hq <= c < Hq + H); padding columns are 0 and
+// stay 0 either way.  Blocks stride over rows: no integer division.
 template <typename V>
-__global__ void dropout_kernel(V *__restrict__ y, long rows, int H, int Hq, int site, Dropout dr) {
-    const long n = rows * 2 * H;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const long r = i / (2 * H);
-        const int f = (int)(i - r * 2 * H), dd = f >= H, u = f - dd * H;
-        V *p = y + r * 2 * Hq + dd * Hq + u;
-        const bool keep = drop_keep(dr.seed, site, (unsigned long long)i, dr.thr);
-        if constexpr (sizeof(V) == 2) *p = keep ? __float2half_rn(__half2float(*p) * dr.scale) : __float2half_rn(0.f);
-        else *p = keep ? *p * dr.scale : 0.f;
+__global__ void dropout_kernel(V *__restrict__ y, long rows, int H, int Hq, int site, Dropout dr, int lg_nv) {
+    constexpr int VEC = 16 / sizeof(V);
+    const uint32_t h0 = mix32(dr.seed + 0x9E3779B9u * (uint32_t)(site + 1));
+    const long total = rows << lg_nv;  // 16-byte vectors; a row holds 2^lg_nv of them (Hq = 2^k)
+    const int W = 2 * H;
+    uint4 *y4 = reinterpret_cast<uint4 *>(y);
+    for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < total; q += (long)gridDim.x * blockDim.x) {
+        const long r = q >> lg_nv;
+        const int v = (int)(q & ((1 << lg_nv) - 1));
+        uint4 pk = y4[q];
+        V *e = reinterpret_cast<V *>(&pk);
+        const unsigned long long base = (unsigned long long)r * W;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            const int c = v * VEC + k, dd = c >= Hq, u = c - dd * Hq;
+            const bool keep = u < H && drop_keep_h0(h0, base + dd * H + u, dr.thr);
+            if constexpr (sizeof(V) == 2) e[k] = keep ? __float2half_rn(__half2float(e[k]) * dr.scale) : __float2half_rn(0.f);
+            else e[k] = keep ? e[k] * dr.scale : 0.f;
+        }
+        y4[q] = pk;
     }
+}
+static int lg2(int v) {
+    int k = 0;
+    while ((1 << k) < v) ++k;
+    return (1 << k) == v ? k : -1;
 }
 int dropout_f16(__half *y, long rows, int H, int Hq, int site, const Dropout &dr, cudaStream_t st) {
     ProfScope ps_(PROF_OTHER, st);
-    dropout_kernel<__half><<<grid_for(rows * 2 * H), 256, 0, st>>>(y, rows, H, Hq, site, dr);
+    const int lg = lg2(2 * Hq / 8);
+    if (lg < 0) return -1;  // Hq is a power of two (rec_supported)
+    dropout_kernel<__half><<<grid_for(rows << lg, 256, 148 * 8), 256, 0, st>>>(y, rows, H, Hq, site, dr, lg);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 int dropout_f32(float *y, long rows, int H, int Hq, int site, const Dropout &dr, cudaStream_t st) {
     ProfScope ps_(PROF_OTHER, st);
-    dropout_kernel<float><<<grid_for(rows * 2 * H), 256, 0, st>>>(y, rows, H, Hq, site, dr);
+    const int lg = lg2(2 * Hq / 4);
+    if (lg < 0) return -1;
+    dropout_kernel<float><<<grid_for(rows << lg, 256, 148 * 8), 256, 0, st>>>(y, rows, H, Hq, site, dr, lg);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
@@ -462,20 +491,28 @@ int store_dx(float *dx, long ldx, const float *dX, long ldX, int D, long rows, i
 }
 
 // --- chunk gather (NEXT-4): batch tensors from a device-resident corpus -----------------------
-// one thread per (t, b, d): x[t][b][d] = frames[(start_b + t) * D + d] for t < len_b, else 0
+// one warp per batch row (t, b): lanes copy the row's D features (float4 when D % 4 == 0);
+// x = 0, mask = 0, label = 0 past the chunk's valid length
 __global__ void gather_chunks_kernel(const float *__restrict__ frames, const int32_t *__restrict__ flab, int D,
                                      const int64_t *__restrict__ cstart, const int32_t *__restrict__ clen, int B,
                                      int T, float *__restrict__ x, uint8_t *__restrict__ mask,
                                      int32_t *__restrict__ labels) {
-    const long total = (long)T * B * D;
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
-        const int d = (int)(e % D);
-        const long tb = e / D;
-        const int b = (int)(tb % B), t = (int)(tb / B);
+    const int lane = threadIdx.x & 31;
+    const long rows = (long)T * B;
+    const long nw = (long)gridDim.x * (blockDim.x >> 5);
+    for (long tb = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); tb < rows; tb += nw) {
+        const int t = (int)(tb / B), b = (int)(tb - (long)t * B);
         const bool ok = t < clen[b];
         const long f = cstart[b] + t;
-        x[e] = ok ? frames[f * D + d] : 0.f;
-        if (d == 0) {
+        float *xo = x + tb * D;
+        if ((D & 3) == 0) {
+            const float4 *src = reinterpret_cast<const float4 *>(frames + f * D);
+            float4 *dst = reinterpret_cast<float4 *>(xo);
+            for (int k = lane; k < D / 4; k += 32) dst[k] = ok ? src[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            for (int k = lane; k < D; k += 32) xo[k] = ok ? frames[f * D + k] : 0.f;
+        }
+        if (lane == 0) {
             mask[tb] = ok ? 1 : 0;
             if (labels) labels[tb] = (ok && flab) ? flab[f] : 0;
         }
@@ -484,8 +521,8 @@ __global__ void gather_chunks_kernel(const float *__restrict__ frames, const int
 int gather_chunks(const float *frames, const int32_t *flab, int D, const int64_t *cstart, const int32_t *clen, int B,
                   int T, float *x, uint8_t *mask, int32_t *labels, cudaStream_t st) {
     ProfScope ps_(PROF_OTHER, st);
-    gather_chunks_kernel<<<grid_for((long)T * B * D), 256, 0, st>>>(frames, flab, D, cstart, clen, B, T, x, mask,
-                                                                    labels);
+    gather_chunks_kernel<<<grid_for((long)T * B * 32, 256, 148 * 8), 256, 0, st>>>(frames, flab, D, cstart, clen, B, T,
+                                                                                  x, mask, labels);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }

@@ -87,3 +87,24 @@ class DeviceCorpus:
         st = t.tensor(start, device=self.device)
         nl = t.tensor(n, device=self.device)
         blstm.blstm_gather_chunks(self.frames, self.labels, self.D, st, nl, B, T, x, mask, labels, stream)
+
+    def plan_epoch(self, batches: List[List[Chunk]], B: int, T: int):
+        """Upload the chunk tables of a whole epoch once (int64 starts / int32 lengths [n, B]);
+        gather_planned(k, ...) then moves no host data per step."""
+        t = self.torch
+        n = len(batches)
+        start = np.zeros((n, B), np.int64)
+        ln = np.zeros((n, B), np.int32)
+        for k, batch in enumerate(batches):
+            for b, c in enumerate(batch):
+                if c.valid_len > T:
+                    raise ValueError("chunk longer than T")
+                start[k, b] = self.offset[c.seq] + c.start
+                ln[k, b] = c.valid_len
+        self.plan = (t.tensor(start, device=self.device), t.tensor(ln, device=self.device), B, T)
+        return n
+
+    def gather_planned(self, k: int, x, mask, labels=None, stream=None):
+        from . import blstm
+        start, ln, B, T = self.plan
+        blstm.blstm_gather_chunks(self.frames, self.labels, self.D, start[k], ln[k], B, T, x, mask, labels, stream)

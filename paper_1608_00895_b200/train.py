@@ -147,14 +147,18 @@ class StackTrainer:
     """Device-resident training of one rank: theta, grad, workspace and a batch."""
 
     def __init__(self, cfg, params, batch, device, lr: float = 1e-5, comm=None, world: int = 1,
-                 sched: Optional[DPSchedule] = None, opt: Optional[dict] = None):
+                 sched: Optional[DPSchedule] = None, opt: Optional[dict] = None, dropout: float = 0.0,
+                 dropout_seed: int = 0):
         """opt: None = plain SGD (sgd_update); else the update rule of blstm_opt_update, e.g.
         {"rule": "adam", "lr": 1e-3, "l2": 1e-4, "max_norm": 10.0} (§4.3)."""
         import torch
         from . import blstm
         self.torch, self.blstm = torch, blstm
         self.cfg, self.dev, self.lr, self.world = cfg, device, lr, world
-        self.desc = blstm.stack_desc(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B)
+        # input dropout (PAPER.md P:255): a fresh mask seed per step (dropout_seed + step index)
+        self.dropout, self.dropout_seed = dropout, dropout_seed
+        self.desc = blstm.stack_desc(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B, dropout=dropout,
+                                     dropout_seed=dropout_seed)
         self.theta = torch.tensor(theta_from_params(params, self.desc), device=device)
         self.grad = torch.zeros_like(self.theta)
         self.ws = torch.empty(blstm.blstm_stack_workspace_bytes(self.desc), dtype=torch.uint8, device=device)
@@ -184,6 +188,8 @@ class StackTrainer:
         self.valid_frames = int(batch.mask.sum())
 
     def _grad(self, theta, grad):
+        if self.dropout > 0:
+            self.desc.dropout_seed = (self.dropout_seed + self.steps_done) & 0xFFFFFFFF
         # sync mode: the library allreduce-sums grad right after the local accumulation
         comm = self.comm if (self.comm is not None and self.sched.grads_summed()) else None
         self.blstm.blstm_stack_fwd_bwd(self.desc, theta, grad, self.x, self.mask, self.labels, self.dy_top,

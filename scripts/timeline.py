@@ -23,10 +23,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--dropout", type=float, default=0.0)
     args = ap.parse_args()
     cfg, params, batch = synth.make_workload(synth.CONFIGS[args.config])
     dev = torch.device("cuda:0")
-    tr = StackTrainer(cfg, params, batch, dev)
+    tr = StackTrainer(cfg, params, batch, dev, dropout=args.dropout)
     for _ in range(args.warmup):
         tr.step()
     torch.cuda.synchronize()

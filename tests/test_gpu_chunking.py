@@ -38,3 +38,21 @@ def test_gather_bit_exact(C, S, D):
         assert np.array_equal(x.cpu().numpy(), rx)
         assert np.array_equal(m.cpu().numpy(), rm)
         assert np.array_equal(lab.cpu().numpy(), rl)
+
+
+def test_planned_epoch_equals_per_batch_gather():
+    dev = torch.device("cuda:0")
+    g = np.random.default_rng(5)
+    lengths = g.integers(1, 600, size=9)
+    xs = [g.normal(size=(L, 8)).astype(np.float32) for L in lengths]
+    corpus = data.DeviceCorpus(xs, None, dev)
+    batches = data.make_batches(data.chunk_sequences(lengths, 250, 100), 4, seed=1)
+    corpus.plan_epoch(batches, 4, 250)
+    for k, batch in enumerate(batches):
+        a = torch.empty((250, 4, 8), device=dev)
+        am = torch.empty((250, 4), dtype=torch.uint8, device=dev)
+        b = torch.empty_like(a)
+        bm = torch.empty_like(am)
+        corpus.gather(batch, 250, a, am)
+        corpus.gather_planned(k, b, bm)
+        assert torch.equal(a, b) and torch.equal(am, bm)
