@@ -13,6 +13,7 @@
 #include "ops.h"
 #include "optim.h"
 #include "prof.h"
+#include "rec_step.h"
 
 using namespace blstm;
 
@@ -296,10 +297,13 @@ struct StackGeo {
     RecPlan pl;
     std::vector<int> Dn, Drows, rowmode;
     Dropout dr;  // input dropout of the training step (R20); dr.on == 0: off
+    // beyond the persistent kernels' on-chip capacity (e.g. H = 1024): step-launched recurrence
+    // (rec_step.h); BLSTM_FORCE_STEP=1 selects it for any size (tests)
+    bool step = false;
 };
 struct StackWS {
     size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, gsk,
-        total;
+        stepF, stepB, cs2, total;
     size_t maxDn;
     std::vector<size_t> y16, w16, rt16, bq, gates, C, hist;
 };
@@ -315,9 +319,10 @@ static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
     g.Hq = g.pl.Hq;
     g.Dp0 = rup(d->D, 64);
     g.Kp = d->K > 0 ? rup(d->K, 64) : 0;
-    if (!rec_supported(g.pl, d->H))
-        return fail(BLSTM_ERR_UNSUPPORTED, "H=%d B=%d exceeds the recurrence kernels' on-chip capacity (Hq=%d N=%d)",
-                    d->H, d->B, g.pl.Hq, g.pl.N);
+    const bool force_step = getenv("BLSTM_FORCE_STEP") && atoi(getenv("BLSTM_FORCE_STEP")) != 0;
+    g.step = force_step || !rec_supported(g.pl, d->H);
+    if (g.step && (g.Hq % 256 != 0 || (long)g.B * 4 * g.Hq * 2 > GSK_ELEMS))
+        return fail(BLSTM_ERR_UNSUPPORTED, "H=%d B=%d: no recurrence path for this size", d->H, d->B);
     if (!(d->dropout >= 0.f && d->dropout < 1.f)) return fail(BLSTM_ERR_ARG, "dropout must be in [0, 1)");
     g.dr.on = d->dropout > 0.f;
     g.dr.thr = (uint32_t)floor((double)d->dropout * 4294967296.0);
@@ -349,11 +354,12 @@ static StackWS stack_ws(const StackGeo &g) {
         w.w16.push_back(c.take((size_t)g.Dn[l] * 8 * Hq * 2));
         w.rt16.push_back(c.take((size_t)2 * 4 * Hq * Hq * 2));
         w.bq.push_back(c.take((size_t)8 * Hq * 4));
-        w.gates.push_back(c.take(rec_native_elems(g.pl, g.T) * 2));
+        const size_t ge = g.step ? (size_t)TB * 8 * Hq : rec_native_elems(g.pl, g.T);
+        w.gates.push_back(c.take(ge * 2));
         w.C.push_back(c.take((size_t)2 * TB * Hq * 4));
         w.hist.push_back(c.take((size_t)2 * (g.T + 1) * g.B * Hq * 2));
     }
-    const size_t zn = rec_native_elems(g.pl, g.T), zl = (size_t)TB * g.Kp;  // Z, or logits [TB, Kp]
+    const size_t zn = g.step ? (size_t)TB * 8 * Hq : rec_native_elems(g.pl, g.T), zl = (size_t)TB * g.Kp;  // Z / logits
     w.Z = c.take((zn > zl ? zn : zl) * 4);
     w.maskN = c.take(rec_mask_bytes(g.pl, g.T));
     w.zflags = c.take(zflag_words(g) * 4);
@@ -376,6 +382,10 @@ static StackWS stack_ws(const StackGeo &g) {
     w.rowerr = c.take((size_t)TB * 4);
     w.cs = c.take(colsum_scratch_bytes(TB, g.K ? g.K : 1));
     w.gsk = c.take((size_t)GSK_ELEMS * 4);
+    // step mode: per-step scratch and the column-sum scratch of db (dbpart from dA)
+    w.stepF = c.take(g.step ? rec_step_fwd_scratch_bytes(g.B, Hq) : 0);
+    w.stepB = c.take(g.step ? rec_step_bwd_scratch_bytes(g.B, Hq) : 0);
+    w.cs2 = c.take(g.step ? colsum_scratch_bytes(TB, 8 * Hq) : 0);
     w.total = c.off;
     return w;
 }
@@ -437,7 +447,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     }
     float *Z = (float *)(ws + w.Z);
     uint8_t *maskN = ws + w.maskN;  // shared by every layer, forward and BPTT
-    TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
+    if (!g.step) TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
     const int num_m = (int)((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS);
     uint32_t *zflags = (uint32_t *)(ws + w.zflags);
     if (cudaMemsetAsync(zflags, 0, zflag_words(g) * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset zflags");
@@ -450,13 +460,31 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     // would otherwise leave the recurrence waiting for a GEMM that cannot run beside it.
     const int side_ctas = num_sms() - 2 * g.pl.G * g.pl.NC;
     static const bool overlap_env = !(getenv("BLSTM_OVERLAP") && atoi(getenv("BLSTM_OVERLAP")) == 0);
-    const bool overlap = overlap_env && side_ctas >= 8;
+    const bool overlap = overlap_env && side_ctas >= 8 && !g.step;
     if (overlap && gemm_prepare()) return fail(BLSTM_ERR_CUDA, "gemm_prepare");
     for (int l = 0; l < g.L; ++l) {
         if (drop && l > 0)  // layer l's input = layer l-1's output, dropped in place (site l)
             TRY(dropout_f16((__half *)(ws + w.y16[l - 1]), g.TB, g.H, Hq, l, g.dr, st), "dropout");
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
         const long lda = l == 0 ? g.Dp0 : 2L * Hq;
+        if (g.step) {  // row-major Z, then one launch pair per time step (rec_step.h)
+            GemmParams gz{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
+            TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gz, 0, st), "gemm Z");
+            __half *hist = (__half *)(ws + w.hist[l]);
+            TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
+            RecStepFwd q{};
+            q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = Hq;
+            q.Z = Z; q.mask = mask; q.RT16 = (const __half *)(ws + w.rt16[l]);
+            q.P = (float *)(ws + w.stepF);
+            if (Cout) { q.C = Cout + (size_t)l * 2 * g.TB * g.H; q.ldc = g.H; q.c_doff = g.TB * g.H; }
+            else { q.C = (float *)(ws + w.C[l]); q.ldc = Hq; q.c_doff = g.TB * Hq; }
+            if (Yout) { q.y = Yout + (size_t)l * g.TB * 2 * g.H; q.ldy = 2L * g.H; q.y_doff = g.H; }
+            q.y16 = (__half *)(ws + w.y16[l]);
+            q.gates = (__half *)(ws + w.gates[l]);
+            q.hist = hist;
+            TRY(rec_step_fwd(q, st), "rec_step_fwd");
+            continue;
+        }
         GemmParams gp{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
         set_native(gp, g.pl, g.B);  // Z in the recurrence kernels' CTA-native layout
         gp.flags = zflags + (size_t)l * 2 * num_m;
@@ -552,7 +580,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     // on the side stream waits for BPTT(l)'s CTAs to check in first.
     static const bool no_guard = getenv("BLSTM_NO_GUARD") && atoi(getenv("BLSTM_NO_GUARD")) != 0;  // A/B
     auto side_guard = [&](int l) -> int {
-        if (!overlap || no_guard) return 0;
+        if (!overlap || no_guard || g.step) return 0;  // (step mode: no persistent BPTT to place)
         TRY(wait_count(bstarted + l, (uint32_t)rec_ctas, side), "wait_count");
         return 0;
     };
@@ -638,7 +666,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             const int e = 6 * l + 3 * dd;
             TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], side), "scatter dW");
             TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, side), "scatter dR");
-            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.pl.G, dd, side), "scatter db");
+            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.step ? 1 : g.pl.G, dd, side), "scatter db");
         }
         if (comm) {  // sync-mode exchange of layer l's bucket (§4.1), overlapping BPTT
             const size_t end = l + 1 < g.L ? offs[6 * (l + 1)] : offs[6 * g.L];
@@ -664,7 +692,24 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         p.P = (float *)(ws + w.P);
         p.counters = (uint32_t *)(ws + w.cnt);
         p.started = overlap ? bstarted + l : nullptr;
-        TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
+        if (g.step) {  // one launch group per time step (rec_step.h); db = column sums of dA
+            RecStepBwd q{};
+            q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = Hq;
+            q.mask = mask; q.RT16 = (const __half *)(ws + w.rt16[l]);
+            q.C = p.C; q.ldc = p.ldc; q.c_doff = p.c_doff;
+            q.gates = p.gates;
+            q.dy = p.dy; q.lddy = p.lddy; q.dy_doff = p.dy_doff;
+            q.dA = dA;
+            float *sb = (float *)(ws + w.stepB);
+            q.dhR = sb; q.dhc = sb + 2L * g.B * Hq; q.dcc = sb + 4L * g.B * Hq;
+            q.splitk_ws = (float *)(ws + w.gsk); q.splitk_elems = GSK_ELEMS;
+            TRY(rec_step_bwd(q, st), "rec_step_bwd");
+            if (cudaMemsetAsync(dbp, 0, (size_t)8 * Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
+            TRY(colsum_f16_add(dA, g.TB, 8 * Hq, 8L * Hq, 1.f / (float)(1 << DA_SHIFT), dbp, (float *)(ws + w.cs2), st),
+                "db colsum");
+        } else {
+            TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
+        }
         // the gradient work this BPTT overlaps, enqueued after it
         if (int rc = (l == g.L - 1) ? side_head() : side_layer(l + 1)) return rc;
         const __half *w16 = (const __half *)(ws + w.w16[l]);

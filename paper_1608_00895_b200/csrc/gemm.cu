@@ -371,7 +371,11 @@ static cudaError_t gemm_setup() {
     }
     return cudaSuccess;
 }
+__global__ void splitk_reduce_kernel(const float *__restrict__ part, int S, long stride, int M, int N, float *C,
+                                     long ldc, float alpha, int beta, const float *__restrict__ bias);
 int gemm_prepare() {
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, splitk_reduce_kernel) != cudaSuccess) return -5;
     return (gemm_setup<128>() == cudaSuccess && gemm_setup<256>() == cudaSuccess) ? 0 : -5;
 }
 
@@ -424,7 +428,7 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
     p.b_mn = B.mn_major;
     if (p.M <= 0 || p.N <= 0) return 0;
     if (p.K <= 0) return -3;  // callers never ask for an empty contraction
-    const int BN = gemm_bn(p.N);
+    const int BN = p.bn == 128 ? 128 : gemm_bn(p.N);
     CUtensorMap ta, tb;
     int rc;
     if (!A.mn_major) rc = make_tmap_f16(&ta, A.ptr, p.K, p.M, A.ld, GEMM_BM);

@@ -38,6 +38,7 @@ struct GemmParams {
     long splitk_elems = 0;
     int ksplit = 1;          // set by gemm_f16
     long split_stride = 0;   // set by gemm_f16: C offset of split s (elements)
+    int bn = 0;              // N tile: 0 = gemm_bn(N); 128 forces the narrow tile (more CTAs for small M)
 };
 
 constexpr int GEMM_BM_ROWS = 128;           // M tile

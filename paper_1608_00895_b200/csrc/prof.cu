@@ -24,6 +24,7 @@ static int g_suspend = 0;
 void prof_suspend(int on) { g_suspend += on ? 1 : -1; }
 
 void note_launch(int n) { g_launches += n; }
+long launch_count() { return g_launches; }
 
 static cudaEvent_t pool_event() {
     if (g_pool_used == g_pool.size()) {

@@ -7,6 +7,7 @@ namespace blstm {
 enum { PROF_REC_FWD = 0, PROF_REC_BWD = 1, PROF_GEMM = 2, PROF_OTHER = 3 };
 
 void note_launch(int n = 1);
+long launch_count();
 // a, b, c: launch shape recorded for the timeline (GEMM: M, N, K)
 int prof_begin(int cat, cudaStream_t st, int a = 0, int b = 0, int c = 0);
 void prof_end(int idx, cudaStream_t st);

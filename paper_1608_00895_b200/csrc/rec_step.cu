@@ -1,0 +1,257 @@
+// rec_step.cu -- step-launched recurrence (rec_step.h).
+//
+// Forward step s (both directions; direction d processes frame t_d = s or T-1-s):
+//   P_d = h_{t-1,d} R_d^T            tcgen05 GEMM, M = B, N = 4Hq, K = Hq (A = the h history slot)
+//   a = P_d + Z[t_d]; i, f, o = sigma(a); g = tanh(a); c = f c_prev + i g; h = o tanh(c);
+//   masked frame: state carried, outputs 0 (R2).
+// BPTT step s (reverse order per direction):
+//   dH = dh_in + dy_t; dc~ = dc + dH o (1 - tanh^2 c); dA = [dc~ g i(1-i), dc~ c_prev f(1-f),
+//   dc~ i (1-g^2), dH tanh(c) o(1-o)]; dc <- dc~ f; masked: dA = 0, dh and dc pass through (R4);
+//   dh_in of the next step = dA_t R_d (GEMM, M = B, N = Hq, K = 4Hq, split-K), or the carried dh
+//   where frame t was masked.
+#include "common.cuh"
+#include "gemm.h"
+#include "lstm_rec.h"
+#include "prof.h"
+#include "rec_step.h"
+
+#include <map>
+#include <vector>
+
+namespace blstm {
+
+namespace {
+
+DEVI float sg(float z) { return __fdividef(1.f, 1.f + __expf(-z)); }
+DEVI float th(float z) { return 2.f * sg(2.f * z) - 1.f; }
+
+// thread per (d, b, u), u < Hq
+__global__ void step_fwd_gate_kernel(RecStepFwd p, int s) {
+    const int Hq = p.Hq, B = p.B, T = p.T;
+    const long n = 2L * B * Hq;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int u = (int)(e % Hq);
+        const long db = e / Hq;
+        const int b = (int)(db % B), d = (int)(db / B);
+        const int dir = d == 0 ? 1 : -1;
+        const int t = d == 0 ? s : T - 1 - s;
+        const long r = (long)t * B + b;
+        const bool valid = p.mask[r] != 0 && u < p.H;
+        const int slot_prev = t + (dir < 0), slot_next = slot_prev + dir;
+        const __half *hp = p.hist + (((long)d * (T + 1) + slot_prev) * B + b) * Hq + u;
+        __half *hn = p.hist + (((long)d * (T + 1) + slot_next) * B + b) * Hq + u;
+        const float c_prev = s == 0 ? 0.f : p.C[d * p.c_doff + (r - (long)dir * B) * p.ldc + u];
+        float c = c_prev, h = __half2float(*hp);
+        float4 act = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+            const float4 z = reinterpret_cast<const float4 *>(p.Z + r * 8 * Hq + (long)d * 4 * Hq)[u];
+            float4 a = z;
+            if (s > 0) {
+                const float4 q = reinterpret_cast<const float4 *>(p.P + ((long)d * B + b) * 4 * Hq)[u];
+                a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
+            }
+            act = make_float4(sg(a.x), sg(a.y), th(a.z), sg(a.w));
+            c = act.y * c_prev + act.x * act.z;
+            h = act.w * th(c);
+        }
+        if (u < p.H) p.C[d * p.c_doff + r * p.ldc + u] = c;
+        *hn = valid ? __float2half_rn(h) : *hp;
+        if (p.y && u < p.H) p.y[r * p.ldy + d * p.y_doff + u] = valid ? h : 0.f;
+        if (p.y16) p.y16[r * 2 * Hq + (long)d * Hq + u] = __float2half_rn(valid ? h : 0.f);
+        __half2 *gp = reinterpret_cast<__half2 *>(p.gates + r * 8 * Hq + (long)d * 4 * Hq + 4 * u);
+        gp[0] = __floats2half2_rn(act.x, act.y);
+        gp[1] = __floats2half2_rn(act.z, act.w);
+    }
+}
+
+__global__ void step_bwd_gate_kernel(RecStepBwd p, int s) {
+    const int Hq = p.Hq, B = p.B, T = p.T;
+    const float scale = (float)(1 << DA_SHIFT);
+    const long n = 2L * B * Hq;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int u = (int)(e % Hq);
+        const long db = e / Hq;
+        const int b = (int)(db % B), d = (int)(db / B);
+        const int dir = d == 0 ? 1 : -1;
+        const int t = d == 0 ? T - 1 - s : s;       // this step's frame (reverse of the forward scan)
+        const long r = (long)t * B + b;
+        const long sidx = db * Hq + u;               // [2][B][Hq] state index
+        const bool valid = p.mask[r] != 0 && u < p.H;
+        float dh_in = 0.f, dc = 0.f;
+        if (s > 0) {
+            const long rp = r + (long)dir * B;       // the frame processed at step s-1
+            dh_in = p.mask[rp] ? p.dhR[sidx] : p.dhc[sidx];
+            dc = p.dcc[sidx];
+        }
+        __half2 *dap = reinterpret_cast<__half2 *>(p.dA + r * 8 * Hq + (long)d * 4 * Hq + 4 * u);
+        if (!valid) {
+            dap[0] = __floats2half2_rn(0.f, 0.f);
+            dap[1] = __floats2half2_rn(0.f, 0.f);
+            p.dhc[sidx] = dh_in;                     // pass through; dc unchanged
+            if (s == 0) p.dcc[sidx] = 0.f;
+            continue;
+        }
+        const __half2 *gp = reinterpret_cast<const __half2 *>(p.gates + r * 8 * Hq + (long)d * 4 * Hq + 4 * u);
+        const float2 g01 = __half22float2(gp[0]), g23 = __half22float2(gp[1]);
+        const float gi = g01.x, gf = g01.y, gg = g23.x, go = g23.y;
+        const float c = p.C[d * p.c_doff + r * p.ldc + u];
+        const int tp = t - dir;                      // the frame before t in the forward scan
+        const float c_prev = (tp >= 0 && tp < T) ? p.C[d * p.c_doff + ((long)tp * B + b) * p.ldc + u] : 0.f;
+        const float dH = dh_in + p.dy[r * p.lddy + d * p.dy_doff + u];
+        const float tc = th(c);
+        const float dct = dc + dH * go * (1.f - tc * tc);
+        const float da_i = dct * gg * gi * (1.f - gi);
+        const float da_f = dct * c_prev * gf * (1.f - gf);
+        const float da_g = dct * gi * (1.f - gg * gg);
+        const float da_o = dH * tc * go * (1.f - go);
+        dap[0] = __floats2half2_rn(da_i * scale, da_f * scale);
+        dap[1] = __floats2half2_rn(da_g * scale, da_o * scale);
+        p.dcc[sidx] = dct * gf;
+    }
+}
+
+int grid_of(long n) {
+    long g = (n + 255) / 256;
+    return (int)(g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g));
+}
+
+}  // namespace
+
+size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * B * 4 * Hq * 4; }
+size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)3 * 2 * B * Hq * 4; }
+
+// ---------------------------------------------------------------------------------------------
+// The T-step loop of a layer is captured once into a CUDA graph (keyed by every pointer and size
+// it bakes in) and replayed: a loop of ~3T small launches is otherwise bound by the host's launch
+// rate.  Inside the graph the two directions' per-step GEMMs are parallel branches.
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+struct GraphEntry {
+    cudaGraphExec_t exec;
+    long launches;
+};
+std::map<std::vector<uint64_t>, GraphEntry> g_graphs;
+cudaStream_t g_side = nullptr, g_cap = nullptr;  // capture streams (never the caller's: it may be legacy)
+cudaEvent_t g_fork = nullptr, g_join = nullptr;
+
+int side_init() {
+    if (g_side) return 0;
+    if (cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking) != cudaSuccess) return -5;
+    if (cudaStreamCreateWithFlags(&g_cap, cudaStreamNonBlocking) != cudaSuccess) return -5;
+    if (cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess) return -5;
+    if (cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming) != cudaSuccess) return -5;
+    return 0;
+}
+
+// fork: work on g_side may start once everything issued so far on st has; join: st waits for g_side
+void fork_side(cudaStream_t st) {
+    cudaEventRecord(g_fork, st);
+    cudaStreamWaitEvent(g_side, g_fork, 0);
+}
+void join_side(cudaStream_t st) {
+    cudaEventRecord(g_join, g_side);
+    cudaStreamWaitEvent(st, g_join, 0);
+}
+
+template <typename Body>
+int run_graph(const std::vector<uint64_t> &key, int cat, cudaStream_t st, Body body) {
+    auto it = g_graphs.find(key);
+    if (it == g_graphs.end()) {
+        // load every kernel the body launches first: a lazy module load synchronizes the context,
+        // which a capturing stream does not allow
+        if (gemm_prepare() || side_init()) return -5;
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, step_fwd_gate_kernel) != cudaSuccess) return -5;
+        if (cudaFuncGetAttributes(&fa, step_bwd_gate_kernel) != cudaSuccess) return -5;
+        const long n0 = launch_count();
+        // recorded on a stream of our own (capture is not allowed on the legacy default stream);
+        // the graph is then launched on the caller's stream
+        if (cudaStreamBeginCapture(g_cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return -5;
+        prof_suspend(1);
+        const int rc = body(g_cap);
+        prof_suspend(0);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(g_cap, &graph);
+        const long nl = launch_count() - n0;
+        note_launch((int)-nl);  // counted when the graph runs, not when it is recorded
+        if (rc || e != cudaSuccess || !graph) {
+            if (graph) cudaGraphDestroy(graph);
+            return -5;
+        }
+        GraphEntry en{nullptr, nl};
+        const cudaError_t ei = cudaGraphInstantiate(&en.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ei != cudaSuccess) return -5;
+        it = g_graphs.emplace(key, en).first;
+    }
+    ProfScope ps(cat, st);
+    if (cudaGraphLaunch(it->second.exec, st) != cudaSuccess) return -5;
+    note_launch((int)it->second.launches);
+    return 0;
+}
+
+uint64_t u64(const void *p) { return (uint64_t)(uintptr_t)p; }
+
+}  // namespace
+
+int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
+    const int Hq = p.Hq, B = p.B, T = p.T;
+    const std::vector<uint64_t> key{1, (uint64_t)T, (uint64_t)B, (uint64_t)p.H, (uint64_t)Hq, u64(p.Z), u64(p.mask),
+                                    u64(p.RT16), u64(p.P), u64(p.C), (uint64_t)p.ldc, (uint64_t)p.c_doff, u64(p.y),
+                                    (uint64_t)p.ldy, (uint64_t)p.y_doff, u64(p.y16), u64(p.gates), u64(p.hist)};
+    return run_graph(key, PROF_REC_FWD, st, [&](cudaStream_t s0) -> int {
+        for (int s = 0; s < T; ++s) {
+            if (s > 0) {
+                fork_side(s0);
+                for (int d = 0; d < 2; ++d) {
+                    const int dir = d == 0 ? 1 : -1;
+                    const int t = d == 0 ? s : T - 1 - s;
+                    const __half *hprev = p.hist + ((long)d * (T + 1) + t + (dir < 0)) * B * Hq;
+                    GemmParams g{B, 4 * Hq, Hq, p.P + (size_t)d * B * 4 * Hq, 4L * Hq, 1.f, 0, nullptr, 0, 0};
+                    g.bn = 128;
+                    if (gemm_f16({hprev, Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 0}, g, 0, d ? g_side : s0))
+                        return -5;
+                }
+                join_side(s0);
+            }
+            step_fwd_gate_kernel<<<grid_of(2L * B * Hq), 256, 0, s0>>>(p, s);
+            note_launch();
+            if (cudaGetLastError() != cudaSuccess) return -5;
+        }
+        return 0;
+    });
+}
+
+int rec_step_bwd(const RecStepBwd &p, cudaStream_t st) {
+    const int Hq = p.Hq, B = p.B, T = p.T;
+    const float alpha = 1.f / (float)(1 << DA_SHIFT);
+    const std::vector<uint64_t> key{2, (uint64_t)T, (uint64_t)B, (uint64_t)p.H, (uint64_t)Hq, u64(p.mask), u64(p.RT16),
+                                    u64(p.C), (uint64_t)p.ldc, (uint64_t)p.c_doff, u64(p.gates), u64(p.dy),
+                                    (uint64_t)p.lddy, (uint64_t)p.dy_doff, u64(p.dA), u64(p.dhR), u64(p.dhc),
+                                    u64(p.dcc), u64(p.splitk_ws), (uint64_t)p.splitk_elems};
+    return run_graph(key, PROF_REC_BWD, st, [&](cudaStream_t s0) -> int {
+        for (int s = 0; s < T; ++s) {
+            step_bwd_gate_kernel<<<grid_of(2L * B * Hq), 256, 0, s0>>>(p, s);
+            note_launch();
+            if (cudaGetLastError() != cudaSuccess) return -5;
+            if (s + 1 == T) break;
+            fork_side(s0);
+            for (int d = 0; d < 2; ++d) {
+                const int t = d == 0 ? T - 1 - s : s;
+                const __half *dA = p.dA + ((size_t)t * B) * 8 * Hq + (size_t)d * 4 * Hq;
+                GemmParams g{B, Hq, 4 * Hq, p.dhR + (size_t)d * B * Hq, (long)Hq, alpha, 0, nullptr, 0, 0};
+                g.bn = 128;
+                // each direction its own half of the split-K scratch (the branches run concurrently)
+                g.splitk_ws = p.splitk_ws + (size_t)d * (p.splitk_elems / 2);
+                g.splitk_elems = p.splitk_elems / 2;
+                if (gemm_f16({dA, 8L * Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 1}, g, 0, d ? g_side : s0))
+                    return -5;
+            }
+            join_side(s0);
+        }
+        return 0;
+    });
+}
+
+}  // namespace blstm

@@ -1,0 +1,51 @@
+// rec_step.h -- step-launched recurrence for layers beyond the persistent kernels' on-chip
+// capacity (rec_supported false, e.g. BASELINE C5: H = 1024).  DESIGN.md §5.7.
+//
+// Same operation as lstm_rec_fwd / lstm_rec_bwd (§4.2, readings R1-R4), same
+// HBM layouts for everything the rest of the step reads (h history, cell states, dA), but each
+// time step is launched: per step and direction one tcgen05 GEMM (h_{t-1} R^T, or dA_t R) with R
+// streamed from L2, plus one fused gate / cell-update kernel for both directions.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace blstm {
+
+struct RecStepFwd {
+    int T, B, H, Hq;
+    const float *Z;          // [T*B][8Hq] row-major, column d*4Hq + 4u + gamma, bias included
+    const uint8_t *mask;     // [T*B]
+    const __half *RT16;      // [2][4Hq][Hq] (R^T per direction, gate-interleaved rows)
+    float *P;                // [2][B][4Hq] scratch: this step's h_{t-1} R^T
+    float *C;                // cell state after frame t: C[d*c_doff + r*ldc + u]
+    long ldc, c_doff;
+    float *y;                // [T*B][ldy] (+ d*y_doff), u < H; nullable
+    long ldy, y_doff;
+    __half *y16;             // [T*B][2Hq] (+ d*Hq); nullable
+    __half *gates;           // [T*B][8Hq] fp16 activations (i, f, g, o at 4u + gamma)
+    __half *hist;            // [2][T+1][B][Hq]: h before frame t at slot t + (dir < 0); slot 0 / T = h0
+};
+
+struct RecStepBwd {
+    int T, B, H, Hq;
+    const uint8_t *mask;
+    const __half *RT16;      // [2][4Hq][Hq]
+    const float *C;          // as written by the forward (ldc = Hq, c_doff = T*B*Hq)
+    long ldc, c_doff;
+    const __half *gates;     // [T*B][8Hq]
+    const float *dy;         // [T*B][lddy] (+ d*dy_doff), u < H
+    long lddy, dy_doff;
+    __half *dA;              // [T*B][8Hq], scaled by 2^DA_SHIFT
+    float *dhR;              // [2][B][Hq] scratch: dA_t R of the previous step
+    float *dhc, *dcc;        // [2][B][Hq] carried dh (masked frames) and dc
+    float *splitk_ws;        // split-K scratch of the per-step GEMM
+    long splitk_elems;
+};
+
+size_t rec_step_fwd_scratch_bytes(int B, int Hq);
+size_t rec_step_bwd_scratch_bytes(int B, int Hq);
+int rec_step_fwd(const RecStepFwd &p, cudaStream_t st);
+int rec_step_bwd(const RecStepBwd &p, cudaStream_t st);
+
+}  // namespace blstm

@@ -1,0 +1,80 @@
+"""The step-launched recurrence (rec_step.cu), the path for layers beyond the
+persistent kernels' on-chip capacity: BASELINE C5's H = 1024 against the oracle, and the same
+path forced at small sizes (BLSTM_FORCE_STEP=1) against the oracle and the persistent path."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from paper_1608_00895_b200 import synth  # noqa: E402
+from tests.gpu_util import GRAD_TOL, OUT_TOL, Stack, grad_errors, norm_rel  # noqa: E402
+
+
+@pytest.fixture
+def force_step():
+    os.environ["BLSTM_FORCE_STEP"] = "1"
+    yield
+    del os.environ["BLSTM_FORCE_STEP"]
+
+
+def _check(L, D, H, K, T, lengths, side_stream=True, dropout=0.0):
+    B = len(lengths)
+    params = synth.stack_params(L, D, H, K)
+    batch = synth.speech_batch(T, B, D, K, np.array(lengths), seed=1004)
+    theta = oracle.pack_params(params, L, D, H, K)
+    st = Stack(L, D, H, K, T, B, dropout=dropout, seed=5)
+    got = st.step(theta, batch, side_stream=side_stream)
+    ref = oracle.blstm_step(theta, batch.x, batch.mask, L, H, K, labels=batch.labels, want_states=True,
+                            dropout=dropout, seed=5)
+    assert abs(got["loss"] - ref["loss"]) / abs(ref["loss"]) < OUT_TOL
+    errs = grad_errors(got["grad"], ref["grad"], L, D, H, K)
+    assert max(errs.values()) < GRAD_TOL, errs
+    if dropout == 0.0:
+        Y, C = st.forward(theta, batch)
+        for l in range(L):
+            assert norm_rel(Y[l], ref["Ys"][l]) < OUT_TOL
+            for d in range(2):
+                assert norm_rel(C[l, d], ref["Cs"][l, d]) < OUT_TOL
+    return got
+
+
+def test_h1024_matches_oracle():
+    """C5's width (H = 1024 > the persistent kernels' capacity): selected automatically."""
+    _check(L=2, D=40, H=1024, K=17, T=6, lengths=[6, 5, 3, 6, 1])
+
+
+def test_h1024_wide_batch():
+    _check(L=1, D=40, H=1024, K=9, T=4, lengths=[4 - (i % 3) for i in range(130)])
+
+
+@pytest.mark.parametrize("H", [64, 300])
+def test_forced_step_small(force_step, H):
+    _check(L=3, D=40, H=H, K=11, T=9, lengths=[9, 8, 6, 9, 3, 2, 1])
+
+
+def test_forced_step_with_dropout(force_step):
+    _check(L=2, D=40, H=130, K=11, T=7, lengths=[7, 5, 3, 7], dropout=0.25)
+
+
+def test_forced_step_close_to_persistent():
+    L, D, H, K, T = 2, 40, 130, 11, 9
+    lengths = [9, 8, 6, 9, 3, 2, 1]
+    params = synth.stack_params(L, D, H, K)
+    batch = synth.speech_batch(T, len(lengths), D, K, np.array(lengths), seed=1004)
+    theta = oracle.pack_params(params, L, D, H, K)
+    a = Stack(L, D, H, K, T, len(lengths)).step(theta, batch, side_stream=True)
+    os.environ["BLSTM_FORCE_STEP"] = "1"
+    try:
+        b = Stack(L, D, H, K, T, len(lengths)).step(theta, batch, side_stream=True)
+    finally:
+        del os.environ["BLSTM_FORCE_STEP"]
+    assert abs(a["loss"] - b["loss"]) / abs(a["loss"]) < 1e-4
+    errs = grad_errors(a["grad"], b["grad"], L, D, H, K)
+    assert max(errs.values()) < GRAD_TOL, errs
