@@ -205,3 +205,68 @@ def dp_average(thetas):
     out = np.zeros(th.shape[1])
     lib().ref_dp_average(th.shape[0], ctypes.c_long(th.shape[1]), _d(th), _d(out))
     return out
+
+
+# ----------------------------------------------------------------------------
+# MDLSTM (§4.2; R21)
+# ----------------------------------------------------------------------------
+MD_FLIPS = ((False, False), (True, False), (False, True), (True, True))  # identity, flip-u, flip-v, both
+
+
+def mdlstm_fwd(x, mask, W, Ru, Rv, b, stable: bool):
+    """One direction in raster order (oracle.c ref_mdlstm_fwd): x [U,V,B,D], mask [U,V,B]."""
+    x = _f64(x)
+    U, V, B, D = x.shape
+    H = Ru.shape[0]
+    mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    h = np.zeros((U, V, B, H)); c = np.zeros((U, V, B, H)); act = np.zeros((U, V, B, 5 * H))
+    rc = lib().ref_mdlstm_fwd(U, V, B, D, H, int(stable), _d(x), mask.ctypes.data_as(_u8p), _d(_f64(W)),
+                              _d(_f64(Ru)), _d(_f64(Rv)), _d(_f64(b)), _d(h), _d(c), _d(act))
+    assert rc == 0
+    return dict(h=h, c=c, act=act)
+
+
+def mdlstm_bwd(x, mask, W, Ru, Rv, fwd, dh, stable: bool):
+    x = _f64(x)
+    U, V, B, D = x.shape
+    H = Ru.shape[0]
+    mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    dx = np.zeros_like(x)
+    dW = np.zeros((D, 5 * H)); dRu = np.zeros((H, 5 * H)); dRv = np.zeros((H, 5 * H)); db = np.zeros(5 * H)
+    rc = lib().ref_mdlstm_bwd(U, V, B, D, H, int(stable), _d(x), mask.ctypes.data_as(_u8p), _d(_f64(W)),
+                              _d(_f64(Ru)), _d(_f64(Rv)), _d(fwd["h"]), _d(fwd["c"]), _d(fwd["act"]),
+                              _d(_f64(dh)), _d(dx), _d(dW), _d(dRu), _d(dRv), _d(db))
+    assert rc == 0
+    return dict(dx=dx, dW=dW, dRu=dRu, dRv=dRv, db=db)
+
+
+def _flip(a, fu, fv):
+    if fu:
+        a = a[::-1]
+    if fv:
+        a = a[:, ::-1]
+    return np.ascontiguousarray(a)
+
+
+def mdlstm_multidir(x, mask, params, stable: bool):
+    """Four directions: direction k runs on the grid flipped by MD_FLIPS[k], its
+    output is flipped back; y [U,V,B,4H] = [y_0 | y_1 | y_2 | y_3].  params: 4 x (W, Ru, Rv, b)."""
+    outs, fwds = [], []
+    for (fu, fv), (W, Ru, Rv, b) in zip(MD_FLIPS, params):
+        f = mdlstm_fwd(_flip(_f64(x), fu, fv), _flip(mask, fu, fv), W, Ru, Rv, b, stable)
+        fwds.append(f)
+        outs.append(_flip(f["h"], fu, fv))
+    return np.concatenate(outs, axis=3), fwds
+
+
+def mdlstm_multidir_bwd(x, mask, params, fwds, dy, stable: bool):
+    """Gradients of sum(y * dy): dx (summed over the directions) and per-direction (dW, dRu, dRv, db)."""
+    H = params[0][1].shape[0]
+    dx = np.zeros(np.shape(x))
+    grads = []
+    for k, ((fu, fv), (W, Ru, Rv, b)) in enumerate(zip(MD_FLIPS, params)):
+        g = mdlstm_bwd(_flip(_f64(x), fu, fv), _flip(mask, fu, fv), W, Ru, Rv, fwds[k],
+                       _flip(_f64(dy)[..., k * H:(k + 1) * H], fu, fv), stable)
+        dx += _flip(g["dx"], fu, fv)
+        grads.append((g["dW"], g["dRu"], g["dRv"], g["db"]))
+    return dx, grads

@@ -567,3 +567,155 @@ void ref_dp_average(int nranks, long n, const double *thetas, double *out)
         out[i] = acc / nranks;
     }
 }
+
+/*
+ * MDLSTM, one direction (§4.2: 2-D LSTM whose cell at (u,v) depends on the
+ * predecessor states (u-1,v) and (u,v-1); SPEC S:256-306 fixes the equations, R21).
+ * Plain raster order (u outer, v inner) -- the CPU scheme P:241-242 describes; the GPU path uses
+ * the anti-diagonal wavefront instead.
+ *   x [U][V][B][D], mask [U][V][B] (1 = pixel of the image), W [D][5H], Ru, Rv [H][5H], b [5H].
+ *   a = x W + h(u-1,v) Ru + h(u,v-1) Rv + b   (out-of-grid predecessors: h = c = 0)
+ *   stable = 0, blocks [i, fu, fv, g, o]: c = s(fu) c(u-1,v) + s(fv) c(u,v-1) + s(i) tanh(g)
+ *   stable = 1, blocks [i, f, g, o, l]:   c = s(f) (s(l) c(u-1,v) + (1-s(l)) c(u,v-1)) + s(i) tanh(g)
+ *   h = s(o) tanh(c).  Masked cell: h = 0, c = c(u-1,v) if u > 0, else c(u,v-1) if v > 0, else 0.
+ * Outputs h, c [U][V][B][H] and act [U][V][B][5H] (gate activations: sigmoid of each block,
+ * tanh of the g block; 0 at masked cells).
+ */
+static double *mdl_at(double *a, int U, int V, int B, int n, int u, int v, int b)
+{
+    (void)U;
+    return a + (((size_t)u * V + v) * B + b) * n;
+}
+int ref_mdlstm_fwd(int U, int V, int B, int D, int H, int stable, const double *x, const uint8_t *mask,
+                   const double *W, const double *Ru, const double *Rv, const double *bias,
+                   double *h, double *c, double *act)
+{
+    if (U < 1 || V < 1 || B < 1 || D < 1 || H < 1) return -1;
+    const int G = 5 * H;
+    const int gg = stable ? 2 : 3;  /* index of the tanh block */
+    double *a = (double *)malloc(sizeof(double) * G);
+    for (int u = 0; u < U; ++u)
+        for (int v = 0; v < V; ++v)
+            for (int b = 0; b < B; ++b) {
+                double *hc = mdl_at(h, U, V, B, H, u, v, b), *cc = mdl_at(c, U, V, B, H, u, v, b);
+                double *ac = mdl_at(act, U, V, B, G, u, v, b);
+                const double *hu = u > 0 ? mdl_at(h, U, V, B, H, u - 1, v, b) : NULL;
+                const double *hv = v > 0 ? mdl_at(h, U, V, B, H, u, v - 1, b) : NULL;
+                const double *cu = u > 0 ? mdl_at(c, U, V, B, H, u - 1, v, b) : NULL;
+                const double *cv = v > 0 ? mdl_at(c, U, V, B, H, u, v - 1, b) : NULL;
+                if (!mask[((size_t)u * V + v) * B + b]) {
+                    for (int j = 0; j < H; ++j) { hc[j] = 0.0; cc[j] = cu ? cu[j] : (cv ? cv[j] : 0.0); }
+                    for (int n = 0; n < G; ++n) ac[n] = 0.0;
+                    continue;
+                }
+                const double *xc = x + (((size_t)u * V + v) * B + b) * D;
+                for (int n = 0; n < G; ++n) a[n] = bias[n];
+                for (int k = 0; k < D; ++k) for (int n = 0; n < G; ++n) a[n] += xc[k] * W[(size_t)k * G + n];
+                if (hu) for (int k = 0; k < H; ++k) for (int n = 0; n < G; ++n) a[n] += hu[k] * Ru[(size_t)k * G + n];
+                if (hv) for (int k = 0; k < H; ++k) for (int n = 0; n < G; ++n) a[n] += hv[k] * Rv[(size_t)k * G + n];
+                for (int n = 0; n < G; ++n) ac[n] = (n / H == gg) ? tanh(a[n]) : sigm(a[n]);
+                for (int j = 0; j < H; ++j) {
+                    const double cuj = cu ? cu[j] : 0.0, cvj = cv ? cv[j] : 0.0;
+                    double cn;
+                    if (!stable) {
+                        cn = ac[H + j] * cuj + ac[2 * H + j] * cvj + ac[j] * ac[3 * H + j];
+                    } else {
+                        const double lam = ac[4 * H + j];
+                        cn = ac[H + j] * (lam * cuj + (1.0 - lam) * cvj) + ac[j] * ac[2 * H + j];
+                    }
+                    cc[j] = cn;
+                    hc[j] = ac[(stable ? 3 : 4) * H + j] * tanh(cn);
+                }
+            }
+    free(a);
+    return 0;
+}
+
+/*
+ * Backward of ref_mdlstm_fwd (reverse raster order), from the saved h, c, act and the output
+ * gradient dh_out [U][V][B][H]:  dx [U][V][B][D] (overwritten), dW, dRu, dRv, db (accumulated).
+ * A masked cell passes its dc to the predecessor its c was carried from; its dh is dropped.
+ */
+int ref_mdlstm_bwd(int U, int V, int B, int D, int H, int stable, const double *x, const uint8_t *mask,
+                   const double *W, const double *Ru, const double *Rv, const double *h, const double *c,
+                   const double *act, const double *dh_out, double *dx, double *dW, double *dRu, double *dRv,
+                   double *db)
+{
+    if (U < 1 || V < 1 || B < 1 || D < 1 || H < 1) return -1;
+    const int G = 5 * H;
+    const size_t NC = (size_t)U * V * B;
+    double *dh = (double *)calloc(NC * H, sizeof(double)), *dc = (double *)calloc(NC * H, sizeof(double));
+    double *da = (double *)malloc(sizeof(double) * G);
+    memcpy(dh, dh_out, sizeof(double) * NC * H);
+    for (int u = U - 1; u >= 0; --u)
+        for (int v = V - 1; v >= 0; --v)
+            for (int b = 0; b < B; ++b) {
+                const size_t cell = ((size_t)u * V + v) * B + b;
+                double *dhc = dh + cell * H, *dcc = dc + cell * H;
+                double *dhu = u > 0 ? dh + (cell - (size_t)V * B) * H : NULL;
+                double *dhv = v > 0 ? dh + (cell - B) * H : NULL;
+                double *dcu = u > 0 ? dc + (cell - (size_t)V * B) * H : NULL;
+                double *dcv = v > 0 ? dc + (cell - B) * H : NULL;
+                double *dxc = dx + cell * D;
+                for (int k = 0; k < D; ++k) dxc[k] = 0.0;
+                if (!mask[cell]) {
+                    for (int j = 0; j < H; ++j) {
+                        if (dcu) dcu[j] += dcc[j];
+                        else if (dcv) dcv[j] += dcc[j];
+                    }
+                    continue;
+                }
+                const double *ac = act + cell * G, *cc = c + cell * H;
+                const double *cu = u > 0 ? c + (cell - (size_t)V * B) * H : NULL;
+                const double *cv = v > 0 ? c + (cell - B) * H : NULL;
+                for (int j = 0; j < H; ++j) {
+                    const double cuj = cu ? cu[j] : 0.0, cvj = cv ? cv[j] : 0.0;
+                    const double tc = tanh(cc[j]);
+                    const int oi = (stable ? 3 : 4) * H + j;
+                    const double o = ac[oi];
+                    const double dct = dcc[j] + dhc[j] * o * (1.0 - tc * tc);
+                    da[oi] = dhc[j] * tc * o * (1.0 - o);
+                    const double ig = ac[j];
+                    if (!stable) {
+                        const double fu = ac[H + j], fv = ac[2 * H + j], g = ac[3 * H + j];
+                        da[j] = dct * g * ig * (1.0 - ig);
+                        da[H + j] = dct * cuj * fu * (1.0 - fu);
+                        da[2 * H + j] = dct * cvj * fv * (1.0 - fv);
+                        da[3 * H + j] = dct * ig * (1.0 - g * g);
+                        if (dcu) dcu[j] += dct * fu;
+                        if (dcv) dcv[j] += dct * fv;
+                    } else {
+                        const double f = ac[H + j], g = ac[2 * H + j], lam = ac[4 * H + j];
+                        const double m = lam * cuj + (1.0 - lam) * cvj;
+                        da[j] = dct * g * ig * (1.0 - ig);
+                        da[H + j] = dct * m * f * (1.0 - f);
+                        da[2 * H + j] = dct * ig * (1.0 - g * g);
+                        da[4 * H + j] = dct * f * (cuj - cvj) * lam * (1.0 - lam);
+                        if (dcu) dcu[j] += dct * f * lam;
+                        if (dcv) dcv[j] += dct * f * (1.0 - lam);
+                    }
+                }
+                const double *xc = x + cell * D;
+                const double *hu = u > 0 ? h + (cell - (size_t)V * B) * H : NULL;
+                const double *hv = v > 0 ? h + (cell - B) * H : NULL;
+                for (int n = 0; n < G; ++n) db[n] += da[n];
+                for (int k = 0; k < D; ++k) {
+                    double acc = 0.0;
+                    for (int n = 0; n < G; ++n) { dW[(size_t)k * G + n] += xc[k] * da[n]; acc += da[n] * W[(size_t)k * G + n]; }
+                    dxc[k] = acc;
+                }
+                for (int k = 0; k < H; ++k) {
+                    double au = 0.0, av = 0.0;
+                    for (int n = 0; n < G; ++n) {
+                        if (hu) dRu[(size_t)k * G + n] += hu[k] * da[n];
+                        if (hv) dRv[(size_t)k * G + n] += hv[k] * da[n];
+                        au += da[n] * Ru[(size_t)k * G + n];
+                        av += da[n] * Rv[(size_t)k * G + n];
+                    }
+                    if (dhu) dhu[k] += au;
+                    if (dhv) dhv[k] += av;
+                }
+            }
+    free(dh); free(dc); free(da);
+    return 0;
+}
