@@ -259,6 +259,38 @@ int dp_comm_destroy(dp_comm *c);
 int blstm_reduce_replicas(float *const *ptrs, int n, size_t len, float scale, void *stream);
 
 /* ------------------------------------------------------------------------ */
+/* Multi-directional 2-D LSTM layer (NEXT-2): PAPER.md §4.2 P:238-245.        */
+/* ------------------------------------------------------------------------ */
+/*
+ * A grid x [U, V, B, D] (rows u, columns v, B images) is scanned by four 2-D LSTMs, one per
+ * corner: direction k runs on the grid flipped by (k & 1: flip u, k & 2: flip v) and its output
+ * is flipped back; y [U, V, B, 4H] = [y_0 | y_1 | y_2 | y_3].  In a direction's
+ * frame (R21):
+ *   a = x W + h(u-1,v) Ru + h(u,v-1) Rv + b        (missing predecessors: h = c = 0)
+ *   stable = 0, gate blocks [i, fu, fv, g, o]:  c = s(fu) c(u-1,v) + s(fv) c(u,v-1) + s(i) tanh(g)
+ *   stable = 1, gate blocks [i, f, g, o, l]:    c = s(f) (s(l) c(u-1,v) + (1-s(l)) c(u,v-1)) + s(i) tanh(g)
+ *   h = s(o) tanh(c);  mask [U, V, B] = 0: h = 0, c carried from (u-1,v), else (u,v-1), else 0.
+ * Cells on one anti-diagonal are independent ("activations for all positions on a common
+ * diagonal can be computed at the same time"): one launch per diagonal for all four
+ * directions and all images.
+ * theta / grad: per direction k: W [D, 5H], Ru [H, 5H], Rv [H, 5H], b [5H] (fp32, DEVICE).
+ */
+typedef struct {
+    int U, V, B, D, H;
+    int stable;
+} mdlstm_desc;
+size_t mdlstm_param_count(const mdlstm_desc *d);
+size_t mdlstm_workspace_bytes(const mdlstm_desc *d);
+/* saved forward state (kept unchanged from mdlstm_fwd to the matching mdlstm_bwd) */
+size_t mdlstm_reserve_bytes(const mdlstm_desc *d);
+/* x [U,V,B,D], mask [U,V,B] uint8, y [U,V,B,4H] out; DEVICE, 16-byte aligned buffers. */
+int mdlstm_fwd(const mdlstm_desc *d, const float *theta, const float *x, const uint8_t *mask, float *y,
+               void *reserve, void *workspace, size_t workspace_bytes, void *stream);
+/* Gradients of sum(y * dy): dx [U,V,B,D] overwritten (NULL: not computed), grad += (theta's layout). */
+int mdlstm_bwd(const mdlstm_desc *d, const float *theta, const float *x, const uint8_t *mask, const void *reserve,
+               const float *dy, float *dx, float *grad, void *workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------ */
 /* Test hook: the tcgen05 GEMM used by every dense contraction of the path.   */
 /* ------------------------------------------------------------------------ */
 /* C[m,n] = alpha * sum_k A(m,k) B(n,k) (+ C[m,n] if beta) (+ bias[n]), A and B fp16

@@ -48,6 +48,11 @@ class OptParams(ctypes.Structure):
 # update rules (include/blstm.h BLSTM_OPT_*)
 OPT_RULES = {"sgd": 0, "momentum": 1, "nesterov": 2, "adagrad": 3, "adadelta": 4, "adam": 5}
 
+class MdDesc(ctypes.Structure):
+    _fields_ = [("U", ctypes.c_int), ("V", ctypes.c_int), ("B", ctypes.c_int), ("D", ctypes.c_int),
+                ("H", ctypes.c_int), ("stable", ctypes.c_int)]
+
+
 _vp = ctypes.c_void_p
 _sz = ctypes.c_size_t
 _i = ctypes.c_int
@@ -74,6 +79,11 @@ _SIGS = {
     "dp_allreduce_grads": (_i, [_vp, _vp, _sz, _vp]),
     "dp_average_params": (_i, [_vp, _vp, _sz, _vp]),
     "dp_comm_destroy": (_i, [_vp]),
+    "mdlstm_param_count": (_sz, [ctypes.POINTER(MdDesc)]),
+    "mdlstm_workspace_bytes": (_sz, [ctypes.POINTER(MdDesc)]),
+    "mdlstm_reserve_bytes": (_sz, [ctypes.POINTER(MdDesc)]),
+    "mdlstm_fwd": (_i, [ctypes.POINTER(MdDesc)] + [_vp] * 6 + [_sz, _vp]),
+    "mdlstm_bwd": (_i, [ctypes.POINTER(MdDesc)] + [_vp] * 8 + [_sz, _vp]),
     "blstm_gather_chunks": (_i, [_vp, _vp, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp]),
     "blstm_reduce_replicas": (_i, [ctypes.POINTER(ctypes.c_void_p), _i, _sz, ctypes.c_float, _vp]),
     "blstm_gemm_f16": (_i, [_i, _i, _i, _vp, ctypes.c_long, _i, _vp, ctypes.c_long, _i, _vp, ctypes.c_long,
@@ -272,6 +282,32 @@ def dp_allreduce_grads(comm, grad, stream=None):
 
 def dp_average_params(comm, theta, stream=None):
     _check("dp_average_params", lib().dp_average_params(comm, _p(theta), theta.numel(), _stream(stream)))
+
+
+def mdlstm_desc(U, V, B, D, H, stable=False) -> MdDesc:
+    return MdDesc(U, V, B, D, H, int(stable))
+
+
+def mdlstm_sizes(desc: MdDesc):
+    """(parameter count, workspace bytes, reserve bytes)."""
+    L = lib()
+    n, w, r = L.mdlstm_param_count(ctypes.byref(desc)), L.mdlstm_workspace_bytes(ctypes.byref(desc)), \
+        L.mdlstm_reserve_bytes(ctypes.byref(desc))
+    if n == 0:
+        raise BlstmError("mdlstm_param_count", -1, last_error())
+    return int(n), int(w), int(r)
+
+
+def mdlstm_fwd(desc, theta, x, mask, y, reserve, workspace, stream=None):
+    _check("mdlstm_fwd", lib().mdlstm_fwd(ctypes.byref(desc), _p(theta), _p(x), _p(mask), _p(y), _p(reserve),
+                                          _p(workspace), workspace.numel() * workspace.element_size(),
+                                          _stream(stream)))
+
+
+def mdlstm_bwd(desc, theta, x, mask, reserve, dy, dx, grad, workspace, stream=None):
+    _check("mdlstm_bwd", lib().mdlstm_bwd(ctypes.byref(desc), _p(theta), _p(x), _p(mask), _p(reserve), _p(dy), _p(dx),
+                                          _p(grad), _p(workspace), workspace.numel() * workspace.element_size(),
+                                          _stream(stream)))
 
 
 def blstm_gather_chunks(frames, frame_labels, D: int, cstart, clen, B: int, T: int, x, mask, labels=None,

@@ -13,6 +13,7 @@
 #include "ops.h"
 #include "optim.h"
 #include "prof.h"
+#include "mdlstm.h"
 #include "rec_step.h"
 
 using namespace blstm;
@@ -800,6 +801,55 @@ extern "C" int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_des
     if (n == 0) return 0;
     TRY(opt_update(p->rule, theta, grad, s0, s1, (long)n, a, p->max_norm, tab, (double *)workspace, zero_grad,
                    (cudaStream_t)stream), "opt_update");
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// MDLSTM (NEXT-2; mdlstm.cu)
+// ---------------------------------------------------------------------------
+static int md_check(const mdlstm_desc *d, MdGeo &g) {
+    if (!d) return fail(BLSTM_ERR_ARG, "null mdlstm_desc");
+    if (d->U < 1 || d->V < 1 || d->B < 1 || d->D < 1 || d->H < 1)
+        return fail(BLSTM_ERR_SHAPE, "need U, V, B, D, H >= 1");
+    if (d->H > 256) return fail(BLSTM_ERR_UNSUPPORTED, "mdlstm: H=%d > 256", d->H);
+    g = md_geo(d->U, d->V, d->B, d->D, d->H, d->stable ? 1 : 0);
+    if (g.cells * 20L * g.Hp > 0x7fffffffL) return fail(BLSTM_ERR_UNSUPPORTED, "mdlstm: grid too large");
+    return 0;
+}
+extern "C" size_t mdlstm_param_count(const mdlstm_desc *d) {
+    MdGeo g;
+    return md_check(d, g) ? 0 : md_param_count(g);
+}
+extern "C" size_t mdlstm_workspace_bytes(const mdlstm_desc *d) {
+    MdGeo g;
+    return md_check(d, g) ? 0 : md_ws(g).total;
+}
+extern "C" size_t mdlstm_reserve_bytes(const mdlstm_desc *d) {
+    MdGeo g;
+    return md_check(d, g) ? 0 : md_ws(g).rtotal;
+}
+extern "C" int mdlstm_fwd(const mdlstm_desc *d, const float *theta, const float *x, const uint8_t *mask, float *y,
+                          void *reserve, void *workspace, size_t workspace_bytes, void *stream) {
+    MdGeo g;
+    if (int rc = md_check(d, g)) return rc;
+    if (!theta || !x || !mask || !y || !reserve || !workspace) return fail(BLSTM_ERR_ARG, "mdlstm_fwd: null pointer");
+    if (!al16(reserve) || !al16(workspace) || !al4(theta) || !al4(x) || !al4(y))
+        return fail(BLSTM_ERR_ALIGN, "mdlstm_fwd: misaligned buffer");
+    if (workspace_bytes < md_ws(g).total) return fail(BLSTM_ERR_WORKSPACE, "workspace %zu < %zu", workspace_bytes, md_ws(g).total);
+    TRY(md_forward(g, theta, x, mask, y, (uint8_t *)workspace, (uint8_t *)reserve, (cudaStream_t)stream), "mdlstm fwd");
+    return 0;
+}
+extern "C" int mdlstm_bwd(const mdlstm_desc *d, const float *theta, const float *x, const uint8_t *mask,
+                          const void *reserve, const float *dy, float *dx, float *grad, void *workspace,
+                          size_t workspace_bytes, void *stream) {
+    MdGeo g;
+    if (int rc = md_check(d, g)) return rc;
+    if (!theta || !x || !mask || !reserve || !dy || !grad || !workspace)
+        return fail(BLSTM_ERR_ARG, "mdlstm_bwd: null pointer");
+    if (!al16(reserve) || !al16(workspace)) return fail(BLSTM_ERR_ALIGN, "mdlstm_bwd: misaligned buffer");
+    if (workspace_bytes < md_ws(g).total) return fail(BLSTM_ERR_WORKSPACE, "workspace %zu < %zu", workspace_bytes, md_ws(g).total);
+    TRY(md_backward(g, theta, x, mask, dy, dx, grad, (uint8_t *)workspace, (uint8_t *)reserve, (cudaStream_t)stream),
+        "mdlstm bwd");
     return 0;
 }
 

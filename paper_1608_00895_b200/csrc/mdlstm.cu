@@ -1,0 +1,420 @@
+// mdlstm.cu -- multi-directional 2-D LSTM layer (§4.2: "the activations for all
+// positions on a common diagonal can be computed at the same time ... we process multiple images
+// and also the four directions ... simultaneously", R21).
+//
+// Direction k = 0..3 runs on the grid flipped by (fu, fv) = (k & 1, k >> 1) (identity, flip-u,
+// flip-v, both); its state lives in its own frame (u', v').  Per call:
+//   Z = X W_all + b_all                 one tcgen05 GEMM for every cell and all four directions
+//   for d = 0 .. U+V-2:                 one fused launch per anti-diagonal, all directions, images
+//     a = Z + h(u'-1,v') Ru + h(u',v'-1) Rv;  gates, cell (two-forget or stable), mask
+// Backward: the reverse wavefront (dh from the successors' dA through R^T, dc from the successors),
+// then dX = dA W_all^T, dW^T = dA^T X, dRu^T / dRv^T = dA^T H_pred (tcgen05 GEMMs; the predecessor
+// pairing is a fixed row shift of a zero-bordered [(U+1) x (V+1) x B] grid), db = column sums.
+#include "common.cuh"
+#include "gemm.h"
+#include "lstm_rec.h"
+#include "mdlstm.h"
+#include "ops.h"
+#include "prof.h"
+
+namespace blstm {
+
+namespace {
+
+DEVI float msg(float z) { return __fdividef(1.f, 1.f + __expf(-z)); }
+DEVI float mth(float z) { return 2.f * msg(2.f * z) - 1.f; }
+
+inline size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+int rup(int a, int b) { return (a + b - 1) / b * b; }
+int grid1(long n) {
+    long g = (n + 255) / 256;
+    return (int)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+}
+
+struct MdK {  // kernel arguments
+    int U, V, B, D, H, Hp, stable;
+    long P1;                 // parameters per direction
+    const float *theta;
+    const float *z;          // [cells][20Hp]
+    const uint8_t *mask;     // [cells]
+    float *y;                // [cells][4H]
+    float *hf;               // [4][U][V][B][H] fp32 h (forward state)
+    float *act, *c;          // [4][U][V][B][5H], [4][U][V][B][H]
+    __half *h16;             // [4][prow][Hp]
+    // backward
+    const float *dy;         // [cells][4H]
+    const float *rt;         // [4][2][5H][H]  Ru^T, Rv^T
+    float *daf;              // [4][U][V][B][5H]
+    float *dcu, *dcv;        // [4][U][V][B][H]: dc this cell passes to its u- / v-predecessor
+    __half *da16;            // [4][prow][5Hp]
+    __half *dap;             // [cells][20Hp]
+};
+
+DEVI void diag_cell(const MdK &a, int d, long e, int &k, int &up, int &vp, int &b, int &j, long &cp, long &ck) {
+    const int U = a.U, V = a.V, B = a.B, H = a.H;
+    const int u0 = d - V + 1 > 0 ? d - V + 1 : 0;
+    const int u1 = d < U - 1 ? d : U - 1;
+    const int nd = u1 - u0 + 1;
+    j = (int)(e % H);
+    long r = e / H;
+    b = (int)(r % B); r /= B;
+    const int i = (int)(r % nd);
+    k = (int)(r / nd);
+    up = u0 + i; vp = d - up;
+    const int u = (k & 1) ? U - 1 - up : up, v = (k & 2) ? V - 1 - vp : vp;
+    cp = ((long)u * V + v) * B + b;
+    ck = (((long)k * U + up) * V + vp) * B + b;
+}
+__host__ DEVI long diag_threads(int U, int V, int B, int H, int d) {
+    const int u0 = d - V + 1 > 0 ? d - V + 1 : 0;
+    const int u1 = d < U - 1 ? d : U - 1;
+    return 4L * (u1 - u0 + 1) * B * H;
+}
+DEVI long slot(const MdK &a, int up, int vp, int b) { return ((long)(up + 1) * (a.V + 1) + vp + 1) * a.B + b; }
+
+__global__ void md_fwd_diag_kernel(MdK a, int d) {
+    const long n = diag_threads(a.U, a.V, a.B, a.H, d);
+    const int H = a.H, G = 5 * H, Hp = a.Hp;
+    const long VB = (long)a.V * a.B;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        int k, up, vp, b, j;
+        long cp, ck;
+        diag_cell(a, d, e, k, up, vp, b, j, cp, ck);
+        const float *hu = up > 0 ? a.hf + (ck - VB) * H : nullptr;
+        const float *hv = vp > 0 ? a.hf + (ck - a.B) * H : nullptr;
+        const float cu = up > 0 ? a.c[(ck - VB) * H + j] : 0.f;
+        const float cv = vp > 0 ? a.c[(ck - a.B) * H + j] : 0.f;
+        float *ac = a.act + ck * G;
+        float h = 0.f, cn;
+        if (!a.mask[cp]) {
+            cn = up > 0 ? cu : cv;  // carried (0 when neither predecessor exists)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) ac[q * H + j] = 0.f;
+        } else {
+            const float *Ru = a.theta + k * a.P1 + (long)a.D * G, *Rv = Ru + (long)H * G;
+            const float *zc = a.z + cp * 20 * Hp + (long)k * 5 * Hp;
+            float g5[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) g5[q] = zc[q * Hp + j];
+            if (hu)
+                for (int m = 0; m < H; ++m) {
+                    const float hm = hu[m];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) g5[q] = fmaf(hm, __ldg(Ru + (long)m * G + q * H + j), g5[q]);
+                }
+            if (hv)
+                for (int m = 0; m < H; ++m) {
+                    const float hm = hv[m];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) g5[q] = fmaf(hm, __ldg(Rv + (long)m * G + q * H + j), g5[q]);
+                }
+            if (!a.stable) {  // [i, fu, fv, g, o]
+                const float gi = msg(g5[0]), fu = msg(g5[1]), fv = msg(g5[2]), gg = mth(g5[3]), go = msg(g5[4]);
+                cn = fu * cu + fv * cv + gi * gg;
+                h = go * mth(cn);
+                ac[j] = gi; ac[H + j] = fu; ac[2 * H + j] = fv; ac[3 * H + j] = gg; ac[4 * H + j] = go;
+            } else {          // [i, f, g, o, lambda]
+                const float gi = msg(g5[0]), f = msg(g5[1]), gg = mth(g5[2]), go = msg(g5[3]), lam = msg(g5[4]);
+                cn = f * (lam * cu + (1.f - lam) * cv) + gi * gg;
+                h = go * mth(cn);
+                ac[j] = gi; ac[H + j] = f; ac[2 * H + j] = gg; ac[3 * H + j] = go; ac[4 * H + j] = lam;
+            }
+        }
+        a.c[ck * H + j] = cn;
+        a.hf[ck * H + j] = h;
+        const long prow = (long)(a.U + 1) * (a.V + 1) * a.B;
+        a.h16[((long)k * prow + slot(a, up, vp, b)) * Hp + j] = __float2half_rn(h);
+        a.y[cp * 4 * H + (long)k * H + j] = h;
+    }
+}
+
+__global__ void md_bwd_diag_kernel(MdK a, int d) {
+    const long n = diag_threads(a.U, a.V, a.B, a.H, d);
+    const int H = a.H, G = 5 * H, Hp = a.Hp;
+    const long VB = (long)a.V * a.B;
+    const long prow = (long)(a.U + 1) * (a.V + 1) * a.B;
+    const float scale = (float)(1 << DA_SHIFT);
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        int k, up, vp, b, j;
+        long cp, ck;
+        diag_cell(a, d, e, k, up, vp, b, j, cp, ck);
+        const bool su = up + 1 < a.U, sv = vp + 1 < a.V;
+        float dc = (su ? a.dcu[(ck + VB) * H + j] : 0.f) + (sv ? a.dcv[(ck + a.B) * H + j] : 0.f);
+        float *df = a.daf + ck * G;
+        __half *d16 = a.da16 + ((long)k * prow + slot(a, up, vp, b)) * 5 * Hp;
+        __half *dp = a.dap + cp * 20 * Hp + (long)k * 5 * Hp;
+        if (!a.mask[cp]) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                df[q * H + j] = 0.f;
+                d16[q * Hp + j] = __float2half_rn(0.f);
+                dp[q * Hp + j] = __float2half_rn(0.f);
+            }
+            a.dcu[ck * H + j] = up > 0 ? dc : 0.f;  // the carried c came from the u-predecessor ...
+            a.dcv[ck * H + j] = (up == 0 && vp > 0) ? dc : 0.f;  // ... else from the v-predecessor
+            continue;
+        }
+        float dh = a.dy[cp * 4 * H + (long)k * H + j];
+        const float *RuT = a.rt + (long)k * 2 * G * H, *RvT = RuT + (long)G * H;
+        if (su) {
+            const float *ds = a.daf + (ck + VB) * G;
+            for (int q = 0; q < G; ++q) dh = fmaf(ds[q], __ldg(RuT + (long)q * H + j), dh);
+        }
+        if (sv) {
+            const float *ds = a.daf + (ck + a.B) * G;
+            for (int q = 0; q < G; ++q) dh = fmaf(ds[q], __ldg(RvT + (long)q * H + j), dh);
+        }
+        const float *ac = a.act + ck * G;
+        const float c = a.c[ck * H + j];
+        const float cu = up > 0 ? a.c[(ck - VB) * H + j] : 0.f;
+        const float cv = vp > 0 ? a.c[(ck - a.B) * H + j] : 0.f;
+        const float tc = mth(c);
+        float da[5];
+        if (!a.stable) {
+            const float gi = ac[j], fu = ac[H + j], fv = ac[2 * H + j], gg = ac[3 * H + j], go = ac[4 * H + j];
+            const float dct = dc + dh * go * (1.f - tc * tc);
+            da[0] = dct * gg * gi * (1.f - gi);
+            da[1] = dct * cu * fu * (1.f - fu);
+            da[2] = dct * cv * fv * (1.f - fv);
+            da[3] = dct * gi * (1.f - gg * gg);
+            da[4] = dh * tc * go * (1.f - go);
+            a.dcu[ck * H + j] = dct * fu;
+            a.dcv[ck * H + j] = dct * fv;
+        } else {
+            const float gi = ac[j], f = ac[H + j], gg = ac[2 * H + j], go = ac[3 * H + j], lam = ac[4 * H + j];
+            const float dct = dc + dh * go * (1.f - tc * tc);
+            const float m = lam * cu + (1.f - lam) * cv;
+            da[0] = dct * gg * gi * (1.f - gi);
+            da[1] = dct * m * f * (1.f - f);
+            da[2] = dct * gi * (1.f - gg * gg);
+            da[3] = dh * tc * go * (1.f - go);
+            da[4] = dct * f * (cu - cv) * lam * (1.f - lam);
+            a.dcu[ck * H + j] = dct * f * lam;
+            a.dcv[ck * H + j] = dct * f * (1.f - lam);
+        }
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            df[q * H + j] = da[q];
+            const __half s = __float2half_rn(da[q] * scale);
+            d16[q * Hp + j] = s;
+            dp[q * Hp + j] = s;
+        }
+    }
+}
+
+// W16 [20Hp][Dp]: row k*5Hp + q*Hp + j <- W_k[f][q*H + j] as hi + lo fp16 parts (w16lo may be
+// null); bq [20Hp] <- b_k
+__global__ void md_pack_kernel(const float *theta, long P1, int D, int H, int Hp, int Dp, __half *w16, __half *w16lo,
+                               float *bq) {
+    const long n = 20L * Hp * Dp;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int f = (int)(e % Dp);
+        const int row = (int)(e / Dp), k = row / (5 * Hp), q = (row / Hp) % 5, j = row % Hp;
+        const bool ok = j < H;
+        const float v = (ok && f < D) ? theta[k * P1 + (long)f * 5 * H + q * H + j] : 0.f;
+        const __half hi = __float2half_rn(v);
+        w16[e] = hi;
+        if (w16lo) w16lo[e] = __float2half_rn(v - __half2float(hi));
+        if (f == 0) bq[row] = ok ? theta[k * P1 + (long)D * 5 * H + 2L * H * 5 * H + q * H + j] : 0.f;
+    }
+}
+// x [cells][D] -> hi / lo fp16 parts [cells][Dp] (zero padded)
+__global__ void md_split_x_kernel(const float *x, int D, int Dp, long cells, __half *hi, __half *lo) {
+    const long n = cells * Dp;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const long r = e / Dp;
+        const int f = (int)(e - r * Dp);
+        const float v = f < D ? x[r * D + f] : 0.f;
+        const __half h = __float2half_rn(v);
+        hi[e] = h;
+        lo[e] = __float2half_rn(v - __half2float(h));
+    }
+}
+// rt [4][2][5H][H] <- Ru_k^T, Rv_k^T
+__global__ void md_pack_rt_kernel(const float *theta, long P1, int D, int H, float *rt) {
+    const int G = 5 * H;
+    const long n = 8L * G * H;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int j = (int)(e % H);
+        const long r = e / H;
+        const int q = (int)(r % G), w = (int)((r / G) % 2), k = (int)(r / (2L * G));
+        rt[e] = theta[k * P1 + (long)D * G + (long)w * H * G + (long)j * G + q];
+    }
+}
+// grad W_k[f][q*H + j] += gW[k*5Hp + q*Hp + j][f]; Ru, Rv from gR [4][2][5Hp][Hp]; b from gb [20Hp]
+__global__ void md_scatter_kernel(float *grad, long P1, int D, int H, int Hp, int Dp, const float *gW, const float *gR,
+                                  const float *gb) {
+    const int G = 5 * H;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < 4 * P1; e += (long)gridDim.x * blockDim.x) {
+        const int k = (int)(e / P1);
+        long o = e - k * P1;
+        float v;
+        if (o < (long)D * G) {
+            const int f = (int)(o / G), n = (int)(o % G), q = n / H, j = n % H;
+            v = gW[((long)k * 5 * Hp + q * Hp + j) * Dp + f];
+        } else if (o < (long)D * G + 2L * H * G) {
+            o -= (long)D * G;
+            const int w = (int)(o / ((long)H * G));
+            const long oo = o - (long)w * H * G;
+            const int m = (int)(oo / G), n = (int)(oo % G), q = n / H, j = n % H;
+            v = gR[(((long)k * 2 + w) * 5 * Hp + q * Hp + j) * Hp + m];
+        } else {
+            const int n = (int)(o - (long)D * G - 2L * H * G), q = n / H, j = n % H;
+            v = gb[(long)k * 5 * Hp + q * Hp + j];
+        }
+        grad[e] += v;
+    }
+}
+
+}  // namespace
+
+MdGeo md_geo(int U, int V, int B, int D, int H, int stable) {
+    MdGeo g;
+    g.U = U; g.V = V; g.B = B; g.D = D; g.H = H; g.stable = stable;
+    g.Hp = rup(H, 16);
+    g.Dp = rup(D, 64);
+    g.cells = (long)U * V * B;
+    g.prow = (long)(U + 1) * (V + 1) * B;
+    return g;
+}
+size_t md_param_count(const MdGeo &g) { return 4 * ((size_t)g.D * 5 * g.H + 2 * (size_t)g.H * 5 * g.H + 5 * g.H); }
+
+MdWS md_ws(const MdGeo &g) {
+    MdWS w{};
+    size_t o = 0;
+    auto take = [&](size_t b) { size_t r = o; o += al(b); return r; };
+    const size_t cells = g.cells, st = 4 * cells;  // direction-frame elements per unit
+    w.x16 = take(cells * g.Dp * 2);
+    w.x16lo = take(cells * g.Dp * 2);
+    w.w16 = take((size_t)20 * g.Hp * g.Dp * 2);
+    w.w16lo = take((size_t)20 * g.Hp * g.Dp * 2);
+    w.z = take(cells * 20 * g.Hp * 4);
+    w.hf = take(st * g.H * 4);
+    w.gb = take((size_t)20 * g.Hp * 4);  // bias vector in the forward, db in the backward
+    w.dap = take(cells * 20 * g.Hp * 2);
+    w.rt = take((size_t)8 * 5 * g.H * g.H * 4);
+    w.dcu = take(st * g.H * 4);
+    w.dcv = take(st * g.H * 4);
+    w.daf = take(st * 5 * g.H * 4);
+    w.gW = take((size_t)20 * g.Hp * g.Dp * 4);
+    w.gR = take((size_t)8 * 5 * g.Hp * g.Hp * 4);
+    w.cs = take(colsum_scratch_bytes(cells, 20 * g.Hp));
+    w.gsk = take((size_t)(8L << 20) * 4);
+    w.da16 = take((size_t)4 * g.prow * 5 * g.Hp * 2);
+    w.dxs = take(cells * g.Dp * 4);
+    w.total = o;
+    size_t r = 0;
+    auto rtake = [&](size_t b) { size_t q = r; r += al(b); return q; };
+    w.act = rtake(st * 5 * g.H * 4);
+    w.c = rtake(st * g.H * 4);
+    w.h16 = rtake((size_t)4 * g.prow * g.Hp * 2);
+    w.rtotal = r;
+    return w;
+}
+
+static MdK md_args(const MdGeo &g, const float *theta, const uint8_t *mask, uint8_t *ws, uint8_t *res) {
+    const MdWS w = md_ws(g);
+    MdK a{};
+    a.U = g.U; a.V = g.V; a.B = g.B; a.D = g.D; a.H = g.H; a.Hp = g.Hp; a.stable = g.stable;
+    a.P1 = (long)(md_param_count(g) / 4);
+    a.theta = theta; a.mask = mask;
+    a.z = (const float *)(ws + w.z);
+    a.hf = (float *)(ws + w.hf);
+    a.act = (float *)(res + w.act); a.c = (float *)(res + w.c); a.h16 = (__half *)(res + w.h16);
+    a.rt = (const float *)(ws + w.rt);
+    a.daf = (float *)(ws + w.daf); a.dcu = (float *)(ws + w.dcu); a.dcv = (float *)(ws + w.dcv);
+    a.da16 = (__half *)(ws + w.da16); a.dap = (__half *)(ws + w.dap);
+    return a;
+}
+
+int md_forward(const MdGeo &g, const float *theta, const float *x, const uint8_t *mask, float *y, uint8_t *ws,
+               uint8_t *res, cudaStream_t st) {
+    const MdWS w = md_ws(g);
+    MdK a = md_args(g, theta, mask, ws, res);
+    a.y = y;
+    __half *x16 = (__half *)(ws + w.x16), *w16 = (__half *)(ws + w.w16);
+    __half *x16lo = (__half *)(ws + w.x16lo), *w16lo = (__half *)(ws + w.w16lo);
+    float *bq = (float *)(ws + w.gb);
+    {
+        ProfScope ps(PROF_OTHER, st);
+        md_pack_kernel<<<grid1(20L * g.Hp * g.Dp), 256, 0, st>>>(theta, a.P1, g.D, g.H, g.Hp, g.Dp, w16, w16lo, bq);
+        md_split_x_kernel<<<grid1(g.cells * g.Dp), 256, 0, st>>>(x, g.D, g.Dp, g.cells, x16, x16lo);
+        note_launch(2);
+    }
+    if (cudaMemsetAsync(res + w.h16, 0, (size_t)4 * g.prow * g.Hp * 2, st) != cudaSuccess) return -5;
+    // Z = x W + b in split precision: x_hi W_hi + x_hi W_lo + x_lo W_hi (fp16 tensor-core operands,
+    // fp32 accumulate; operand error ~2^-22 instead of 2^-11: the 2-D recurrence compounds the input
+    // error along paths of up to U+V cells)
+    GemmParams gz{(int)g.cells, 20 * g.Hp, g.Dp, (float *)(ws + w.z), 20L * g.Hp, 1.f, 0, bq, 0, 0};
+    if (gemm_f16({x16, g.Dp, 0}, {w16, g.Dp, 0}, gz, 0, st)) return -5;
+    GemmParams gz2 = gz;
+    gz2.beta = 1; gz2.bias = nullptr;
+    if (gemm_f16({x16, g.Dp, 0}, {w16lo, g.Dp, 0}, gz2, 0, st)) return -5;
+    if (gemm_f16({x16lo, g.Dp, 0}, {w16, g.Dp, 0}, gz2, 0, st)) return -5;
+    for (int d = 0; d < g.U + g.V - 1; ++d) {
+        ProfScope ps(PROF_REC_FWD, st);
+        md_fwd_diag_kernel<<<grid1(diag_threads(g.U, g.V, g.B, g.H, d)), 256, 0, st>>>(a, d);
+        note_launch();
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+int md_backward(const MdGeo &g, const float *theta, const float *x, const uint8_t *mask, const float *dy, float *dx,
+                float *grad, uint8_t *ws, uint8_t *res, cudaStream_t st) {
+    const MdWS w = md_ws(g);
+    MdK a = md_args(g, theta, mask, ws, res);
+    a.dy = dy;
+    const float alpha = 1.f / (float)(1 << DA_SHIFT);
+    __half *x16 = (__half *)(ws + w.x16), *w16 = (__half *)(ws + w.w16);
+    {
+        ProfScope ps(PROF_OTHER, st);
+        md_pack_kernel<<<grid1(20L * g.Hp * g.Dp), 256, 0, st>>>(theta, a.P1, g.D, g.H, g.Hp, g.Dp, w16, nullptr,
+                                                                 (float *)(ws + w.gb));
+        md_pack_rt_kernel<<<grid1(8L * 5 * g.H * g.H), 256, 0, st>>>(theta, a.P1, g.D, g.H, (float *)(ws + w.rt));
+        note_launch(2);
+    }
+    if (cast_x_f16(x, g.D, g.D, x16, g.Dp, g.cells, st)) return -5;
+    if (cudaMemsetAsync(ws + w.da16, 0, (size_t)4 * g.prow * 5 * g.Hp * 2, st) != cudaSuccess) return -5;
+    if (cudaMemsetAsync(ws + w.dap, 0, (size_t)g.cells * 20 * g.Hp * 2, st) != cudaSuccess) return -5;
+    for (int d = g.U + g.V - 2; d >= 0; --d) {
+        ProfScope ps(PROF_REC_BWD, st);
+        md_bwd_diag_kernel<<<grid1(diag_threads(g.U, g.V, g.B, g.H, d)), 256, 0, st>>>(a, d);
+        note_launch();
+    }
+    if (cudaGetLastError() != cudaSuccess) return -5;
+    const __half *dap = (const __half *)(ws + w.dap);
+    float *gsk = (float *)(ws + w.gsk);
+    if (dx) {  // dX = dA W_all^T (the four directions sum in the contraction)
+        GemmParams gx{(int)g.cells, g.Dp, 20 * g.Hp, (float *)(ws + w.dxs), (long)g.Dp, alpha, 0, nullptr, 0, 0};
+        if (gemm_f16({dap, 20L * g.Hp, 0}, {w16, g.Dp, 1}, gx, 0, st)) return -5;
+        if (store_dx(dx, g.D, (const float *)(ws + w.dxs), g.Dp, g.D, g.cells, 0, st)) return -5;
+    }
+    {   // dW_all^T [20Hp, Dp] = dA^T X
+        GemmParams gw{20 * g.Hp, g.Dp, (int)g.cells, (float *)(ws + w.gW), (long)g.Dp, alpha, 0, nullptr, 0, 0};
+        gw.splitk_ws = gsk; gw.splitk_elems = 8L << 20;
+        if (gemm_f16({dap, 20L * g.Hp, 1}, {x16, g.Dp, 1}, gw, 0, st)) return -5;
+    }
+    const __half *da16 = (const __half *)(ws + w.da16), *h16 = (const __half *)(res + w.h16);
+    for (int k = 0; k < 4; ++k)
+        for (int wv = 0; wv < 2; ++wv) {  // dRu (shift one u-row of the padded grid) / dRv (one v-step)
+            const long shift = wv == 0 ? (long)(g.V + 1) * g.B : (long)g.B;
+            const __half *A = da16 + ((long)k * g.prow + shift) * 5 * g.Hp;
+            const __half *Hb = h16 + (long)k * g.prow * g.Hp;
+            GemmParams gr{5 * g.Hp, g.Hp, (int)(g.prow - shift), (float *)(ws + w.gR) + (size_t)(k * 2 + wv) * 5 * g.Hp * g.Hp,
+                          (long)g.Hp, alpha, 0, nullptr, 0, 0};
+            gr.splitk_ws = gsk; gr.splitk_elems = 8L << 20;
+            if (gemm_f16({A, 5L * g.Hp, 1}, {Hb, g.Hp, 1}, gr, 0, st)) return -5;
+        }
+    if (cudaMemsetAsync(ws + w.gb, 0, (size_t)20 * g.Hp * 4, st) != cudaSuccess) return -5;
+    if (colsum_f16_add(dap, g.cells, 20 * g.Hp, 20L * g.Hp, alpha, (float *)(ws + w.gb), (float *)(ws + w.cs), st))
+        return -5;
+    {
+        ProfScope ps(PROF_OTHER, st);
+        md_scatter_kernel<<<grid1(4 * a.P1), 256, 0, st>>>(grad, a.P1, g.D, g.H, g.Hp, g.Dp, (const float *)(ws + w.gW),
+                                                           (const float *)(ws + w.gR), (const float *)(ws + w.gb));
+        note_launch();
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+}  // namespace blstm
