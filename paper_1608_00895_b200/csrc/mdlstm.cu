@@ -50,144 +50,236 @@ struct MdK {  // kernel arguments
     __half *dap;             // [cells][20Hp]
 };
 
-DEVI void diag_cell(const MdK &a, int d, long e, int &k, int &up, int &vp, int &b, int &j, long &cp, long &ck) {
-    const int U = a.U, V = a.V, B = a.B, H = a.H;
-    const int u0 = d - V + 1 > 0 ? d - V + 1 : 0;
-    const int u1 = d < U - 1 ? d : U - 1;
-    const int nd = u1 - u0 + 1;
-    j = (int)(e % H);
-    long r = e / H;
-    b = (int)(r % B); r /= B;
-    const int i = (int)(r % nd);
-    k = (int)(r / nd);
-    up = u0 + i; vp = d - up;
-    const int u = (k & 1) ? U - 1 - up : up, v = (k & 2) ? V - 1 - vp : vp;
-    cp = ((long)u * V + v) * B + b;
-    ck = (((long)k * U + up) * V + vp) * B + b;
+// Tile decomposition of one anti-diagonal: block = (direction k, 32-unit tile, group of 32 rows),
+// row = (cell on the diagonal, image); warp w of the block owns rows w, w+8, w+16, w+24 of its group
+// (warp-uniform), lane = unit.  The recurrent weights of the unit tile are staged in shared memory
+// 32 rows of K at a time; the predecessor states are warp-broadcast loads.
+constexpr int MT_J = 32, MT_RL = 8, MT_RPT = 2, MT_ROWS = MT_RL * MT_RPT, MT_MC = 32;
+constexpr int MT_MCF = 16;  // K chunk of the forward (5 gates x 2 predecessors of R per chunk row)
+
+struct MdRow {
+    long cp, ck;
+    int up, vp;
+    bool live, on;  // row exists on this diagonal; its pixel is in the image
+};
+DEVI MdRow md_row(const MdK &a, int d, int k, int r) {
+    MdRow w;
+    const int u0 = d - a.V + 1 > 0 ? d - a.V + 1 : 0;
+    const int u1 = d < a.U - 1 ? d : a.U - 1;
+    w.live = r < (u1 - u0 + 1) * a.B;
+    if (!w.live) r = 0;
+    const int i = r / a.B, b = r - i * a.B;
+    w.up = u0 + i; w.vp = d - w.up;
+    const int u = (k & 1) ? a.U - 1 - w.up : w.up, v = (k & 2) ? a.V - 1 - w.vp : w.vp;
+    w.cp = ((long)u * a.V + v) * a.B + b;
+    w.ck = (((long)k * a.U + w.up) * a.V + w.vp) * a.B + b;
+    w.on = w.live && a.mask[w.cp] != 0;
+    return w;
 }
-__host__ DEVI long diag_threads(int U, int V, int B, int H, int d) {
+__host__ DEVI int md_blocks(int U, int V, int B, int H, int d) {
     const int u0 = d - V + 1 > 0 ? d - V + 1 : 0;
     const int u1 = d < U - 1 ? d : U - 1;
-    return 4L * (u1 - u0 + 1) * B * H;
+    const int nrows = (u1 - u0 + 1) * B;
+    return 4 * ((H + MT_J - 1) / MT_J) * ((nrows + MT_ROWS - 1) / MT_ROWS);
 }
 DEVI long slot(const MdK &a, int up, int vp, int b) { return ((long)(up + 1) * (a.V + 1) + vp + 1) * a.B + b; }
 
-__global__ void md_fwd_diag_kernel(MdK a, int d) {
-    const long n = diag_threads(a.U, a.V, a.B, a.H, d);
+__global__ void __launch_bounds__(256) md_fwd_diag_kernel(MdK a, int d) {
+    __shared__ float Rs[2][MT_MCF][5][MT_J];
+    __shared__ float Hs[2][MT_ROWS][MT_MCF + 1];   // predecessor h chunk of the block's rows (u, v)
+    __shared__ long rowpred[2][MT_ROWS];           // h index of each row's predecessors (-1: none)
     const int H = a.H, G = 5 * H, Hp = a.Hp;
     const long VB = (long)a.V * a.B;
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
-        int k, up, vp, b, j;
-        long cp, ck;
-        diag_cell(a, d, e, k, up, vp, b, j, cp, ck);
-        const float *hu = up > 0 ? a.hf + (ck - VB) * H : nullptr;
-        const float *hv = vp > 0 ? a.hf + (ck - a.B) * H : nullptr;
-        const float cu = up > 0 ? a.c[(ck - VB) * H + j] : 0.f;
-        const float cv = vp > 0 ? a.c[(ck - a.B) * H + j] : 0.f;
+    const int u0 = d - a.V + 1 > 0 ? d - a.V + 1 : 0;
+    const int u1 = d < a.U - 1 ? d : a.U - 1;
+    const int nrg = ((u1 - u0 + 1) * a.B + MT_ROWS - 1) / MT_ROWS, njt = (H + MT_J - 1) / MT_J;
+    int bid = blockIdx.x;
+    const int rg = bid % nrg; bid /= nrg;
+    const int jt = bid % njt, k = bid / njt;
+    const int jj = threadIdx.x & 31, rl = threadIdx.x >> 5, j = jt * MT_J + jj;
+    const bool jok = j < H;
+    const float *Ru = a.theta + k * a.P1 + (long)a.D * G, *Rv = Ru + (long)H * G;
+    MdRow rw[MT_RPT];
+    float acc[MT_RPT][5];
+#pragma unroll
+    for (int t = 0; t < MT_RPT; ++t) {
+        rw[t] = md_row(a, d, k, rg * MT_ROWS + rl + MT_RL * t);
+        const float *zc = a.z + rw[t].cp * 20 * Hp + (long)k * 5 * Hp;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[t][q] = (rw[t].on && jok) ? zc[q * Hp + j] : 0.f;
+        if (jj == 0) {  // row rl + 8t of the block
+            rowpred[0][rl + MT_RL * t] = (rw[t].on && rw[t].up > 0) ? (rw[t].ck - VB) * H : -1;
+            rowpred[1][rl + MT_RL * t] = (rw[t].on && rw[t].vp > 0) ? (rw[t].ck - a.B) * H : -1;
+        }
+    }
+    for (int m0 = 0; m0 < H; m0 += MT_MCF) {
+        __syncthreads();
+        // all copies of the chunk in flight at once (cp.async, zero-filled out of range): a load ->
+        // store loop serializes ~20 L2 round trips per thread (measured: half the stall samples)
+        for (int e = threadIdx.x; e < 2 * MT_MCF * 5 * MT_J; e += blockDim.x) {
+            const int jx = e % MT_J, q = (e / MT_J) % 5, mm = (e / (5 * MT_J)) % MT_MCF, w = e / (MT_MCF * 5 * MT_J);
+            const int m = m0 + mm, jg = jt * MT_J + jx;
+            const bool ok = m < H && jg < H;
+            cp_async4_zfill(smem_u32(&Rs[w][mm][q][jx]), ok ? (w ? Rv : Ru) + (long)m * G + q * H + jg : Ru, ok ? 4 : 0);
+        }
+        for (int e = threadIdx.x; e < 2 * MT_ROWS * MT_MCF; e += blockDim.x) {  // coalesced per row
+            const int mm = e % MT_MCF, rr = (e / MT_MCF) % MT_ROWS, w = e / (MT_ROWS * MT_MCF);
+            const long src = rowpred[w][rr];
+            const bool ok = src >= 0 && m0 + mm < H;
+            cp_async4_zfill(smem_u32(&Hs[w][rr][mm]), ok ? a.hf + src + m0 + mm : a.hf, ok ? 4 : 0);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        const int mlen = H - m0 < MT_MCF ? H - m0 : MT_MCF;
+#pragma unroll
+        for (int t = 0; t < MT_RPT; ++t) {
+            if (!rw[t].on) continue;  // warp-uniform
+            const int rr = rl + MT_RL * t;
+            for (int mm = 0; mm < mlen; ++mm) {
+                const float hu = Hs[0][rr][mm], hv = Hs[1][rr][mm];
+#pragma unroll
+                for (int q = 0; q < 5; ++q)
+                    acc[t][q] = fmaf(hv, Rs[1][mm][q][jj], fmaf(hu, Rs[0][mm][q][jj], acc[t][q]));
+            }
+        }
+    }
+    const long prow = (long)(a.U + 1) * (a.V + 1) * a.B;
+#pragma unroll
+    for (int t = 0; t < MT_RPT; ++t) {
+        const MdRow &w = rw[t];
+        if (!w.live || !jok) continue;
+        const long ck = w.ck;
+        const int b = (int)(w.cp % a.B);
+        const float cu = w.up > 0 ? a.c[(ck - VB) * H + j] : 0.f;
+        const float cv = w.vp > 0 ? a.c[(ck - a.B) * H + j] : 0.f;
         float *ac = a.act + ck * G;
         float h = 0.f, cn;
-        if (!a.mask[cp]) {
-            cn = up > 0 ? cu : cv;  // carried (0 when neither predecessor exists)
+        if (!w.on) {
+            cn = w.up > 0 ? cu : cv;  // carried (0 when neither predecessor exists)
 #pragma unroll
             for (int q = 0; q < 5; ++q) ac[q * H + j] = 0.f;
-        } else {
-            const float *Ru = a.theta + k * a.P1 + (long)a.D * G, *Rv = Ru + (long)H * G;
-            const float *zc = a.z + cp * 20 * Hp + (long)k * 5 * Hp;
-            float g5[5];
-#pragma unroll
-            for (int q = 0; q < 5; ++q) g5[q] = zc[q * Hp + j];
-            if (hu)
-                for (int m = 0; m < H; ++m) {
-                    const float hm = hu[m];
-#pragma unroll
-                    for (int q = 0; q < 5; ++q) g5[q] = fmaf(hm, __ldg(Ru + (long)m * G + q * H + j), g5[q]);
-                }
-            if (hv)
-                for (int m = 0; m < H; ++m) {
-                    const float hm = hv[m];
-#pragma unroll
-                    for (int q = 0; q < 5; ++q) g5[q] = fmaf(hm, __ldg(Rv + (long)m * G + q * H + j), g5[q]);
-                }
-            if (!a.stable) {  // [i, fu, fv, g, o]
-                const float gi = msg(g5[0]), fu = msg(g5[1]), fv = msg(g5[2]), gg = mth(g5[3]), go = msg(g5[4]);
-                cn = fu * cu + fv * cv + gi * gg;
-                h = go * mth(cn);
-                ac[j] = gi; ac[H + j] = fu; ac[2 * H + j] = fv; ac[3 * H + j] = gg; ac[4 * H + j] = go;
-            } else {          // [i, f, g, o, lambda]
-                const float gi = msg(g5[0]), f = msg(g5[1]), gg = mth(g5[2]), go = msg(g5[3]), lam = msg(g5[4]);
-                cn = f * (lam * cu + (1.f - lam) * cv) + gi * gg;
-                h = go * mth(cn);
-                ac[j] = gi; ac[H + j] = f; ac[2 * H + j] = gg; ac[3 * H + j] = go; ac[4 * H + j] = lam;
-            }
+        } else if (!a.stable) {  // [i, fu, fv, g, o]
+            const float gi = msg(acc[t][0]), fu = msg(acc[t][1]), fv = msg(acc[t][2]), gg = mth(acc[t][3]),
+                        go = msg(acc[t][4]);
+            cn = fu * cu + fv * cv + gi * gg;
+            h = go * mth(cn);
+            ac[j] = gi; ac[H + j] = fu; ac[2 * H + j] = fv; ac[3 * H + j] = gg; ac[4 * H + j] = go;
+        } else {                 // [i, f, g, o, lambda]
+            const float gi = msg(acc[t][0]), f = msg(acc[t][1]), gg = mth(acc[t][2]), go = msg(acc[t][3]),
+                        lam = msg(acc[t][4]);
+            cn = f * (lam * cu + (1.f - lam) * cv) + gi * gg;
+            h = go * mth(cn);
+            ac[j] = gi; ac[H + j] = f; ac[2 * H + j] = gg; ac[3 * H + j] = go; ac[4 * H + j] = lam;
         }
         a.c[ck * H + j] = cn;
         a.hf[ck * H + j] = h;
-        const long prow = (long)(a.U + 1) * (a.V + 1) * a.B;
-        a.h16[((long)k * prow + slot(a, up, vp, b)) * Hp + j] = __float2half_rn(h);
-        a.y[cp * 4 * H + (long)k * H + j] = h;
+        a.h16[((long)k * prow + slot(a, w.up, w.vp, b)) * Hp + j] = __float2half_rn(h);
+        a.y[w.cp * 4 * H + (long)k * H + j] = h;
     }
 }
 
-__global__ void md_bwd_diag_kernel(MdK a, int d) {
-    const long n = diag_threads(a.U, a.V, a.B, a.H, d);
+__global__ void __launch_bounds__(256) md_bwd_diag_kernel(MdK a, int d) {
+    __shared__ float Rs[2][MT_MC][MT_J];
+    __shared__ float Ds[2][MT_ROWS][MT_MC + 1];  // successor dA chunk of the block's rows (u, v)
+    __shared__ long rowsucc[2][MT_ROWS];          // dA index of each row's successors (-1: none)
     const int H = a.H, G = 5 * H, Hp = a.Hp;
     const long VB = (long)a.V * a.B;
     const long prow = (long)(a.U + 1) * (a.V + 1) * a.B;
     const float scale = (float)(1 << DA_SHIFT);
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
-        int k, up, vp, b, j;
-        long cp, ck;
-        diag_cell(a, d, e, k, up, vp, b, j, cp, ck);
-        const bool su = up + 1 < a.U, sv = vp + 1 < a.V;
-        float dc = (su ? a.dcu[(ck + VB) * H + j] : 0.f) + (sv ? a.dcv[(ck + a.B) * H + j] : 0.f);
+    const int u0 = d - a.V + 1 > 0 ? d - a.V + 1 : 0;
+    const int u1 = d < a.U - 1 ? d : a.U - 1;
+    const int nrg = ((u1 - u0 + 1) * a.B + MT_ROWS - 1) / MT_ROWS, njt = (H + MT_J - 1) / MT_J;
+    int bid = blockIdx.x;
+    const int rg = bid % nrg; bid /= nrg;
+    const int jt = bid % njt, k = bid / njt;
+    const int jj = threadIdx.x & 31, rl = threadIdx.x >> 5, j = jt * MT_J + jj;
+    const bool jok = j < H;
+    const float *RuT = a.rt + (long)k * 2 * G * H, *RvT = RuT + (long)G * H;
+    MdRow rw[MT_RPT];
+    float dh[MT_RPT];
+#pragma unroll
+    for (int t = 0; t < MT_RPT; ++t) {
+        rw[t] = md_row(a, d, k, rg * MT_ROWS + rl + MT_RL * t);
+        dh[t] = (rw[t].on && jok) ? a.dy[rw[t].cp * 4 * H + (long)k * H + j] : 0.f;
+        if (jj == 0) {
+            rowsucc[0][rl + MT_RL * t] = (rw[t].on && rw[t].up + 1 < a.U) ? (rw[t].ck + VB) * G : -1;
+            rowsucc[1][rl + MT_RL * t] = (rw[t].on && rw[t].vp + 1 < a.V) ? (rw[t].ck + a.B) * G : -1;
+        }
+    }
+    // dh += dA(u'+1, v') Ru^T + dA(u', v'+1) Rv^T
+    for (int n0 = 0; n0 < G; n0 += MT_MC) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 2 * MT_MC * MT_J; e += blockDim.x) {
+            const int jx = e % MT_J, nn = (e / MT_J) % MT_MC, w = e / (MT_MC * MT_J);
+            const int n = n0 + nn, jg = jt * MT_J + jx;
+            const bool ok = n < G && jg < H;
+            cp_async4_zfill(smem_u32(&Rs[w][nn][jx]), ok ? (w ? RvT : RuT) + (long)n * H + jg : RuT, ok ? 4 : 0);
+        }
+        for (int e = threadIdx.x; e < 2 * MT_ROWS * MT_MC; e += blockDim.x) {
+            const int nn = e % MT_MC, rr = (e / MT_MC) % MT_ROWS, w = e / (MT_ROWS * MT_MC);
+            const long src = rowsucc[w][rr];
+            const bool ok = src >= 0 && n0 + nn < G;
+            cp_async4_zfill(smem_u32(&Ds[w][rr][nn]), ok ? a.daf + src + n0 + nn : a.daf, ok ? 4 : 0);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        const int nlen = G - n0 < MT_MC ? G - n0 : MT_MC;
+#pragma unroll
+        for (int t = 0; t < MT_RPT; ++t) {
+            if (!rw[t].on) continue;  // warp-uniform
+            const int rr = rl + MT_RL * t;
+            for (int nn = 0; nn < nlen; ++nn)
+                dh[t] = fmaf(Ds[1][rr][nn], Rs[1][nn][jj], fmaf(Ds[0][rr][nn], Rs[0][nn][jj], dh[t]));
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < MT_RPT; ++t) {
+        const MdRow &w = rw[t];
+        if (!w.live || !jok) continue;
+        const long ck = w.ck, cp = w.cp;
+        const int b = (int)(cp % a.B);
+        const bool su = w.up + 1 < a.U, sv = w.vp + 1 < a.V;
+        const float dc = (su ? a.dcu[(ck + VB) * H + j] : 0.f) + (sv ? a.dcv[(ck + a.B) * H + j] : 0.f);
         float *df = a.daf + ck * G;
-        __half *d16 = a.da16 + ((long)k * prow + slot(a, up, vp, b)) * 5 * Hp;
+        __half *d16 = a.da16 + ((long)k * prow + slot(a, w.up, w.vp, b)) * 5 * Hp;
         __half *dp = a.dap + cp * 20 * Hp + (long)k * 5 * Hp;
-        if (!a.mask[cp]) {
+        if (!w.on) {
 #pragma unroll
             for (int q = 0; q < 5; ++q) {
                 df[q * H + j] = 0.f;
                 d16[q * Hp + j] = __float2half_rn(0.f);
                 dp[q * Hp + j] = __float2half_rn(0.f);
             }
-            a.dcu[ck * H + j] = up > 0 ? dc : 0.f;  // the carried c came from the u-predecessor ...
-            a.dcv[ck * H + j] = (up == 0 && vp > 0) ? dc : 0.f;  // ... else from the v-predecessor
+            a.dcu[ck * H + j] = w.up > 0 ? dc : 0.f;                 // the carried c came from the
+            a.dcv[ck * H + j] = (w.up == 0 && w.vp > 0) ? dc : 0.f;  // u-, else the v-predecessor
             continue;
-        }
-        float dh = a.dy[cp * 4 * H + (long)k * H + j];
-        const float *RuT = a.rt + (long)k * 2 * G * H, *RvT = RuT + (long)G * H;
-        if (su) {
-            const float *ds = a.daf + (ck + VB) * G;
-            for (int q = 0; q < G; ++q) dh = fmaf(ds[q], __ldg(RuT + (long)q * H + j), dh);
-        }
-        if (sv) {
-            const float *ds = a.daf + (ck + a.B) * G;
-            for (int q = 0; q < G; ++q) dh = fmaf(ds[q], __ldg(RvT + (long)q * H + j), dh);
         }
         const float *ac = a.act + ck * G;
         const float c = a.c[ck * H + j];
-        const float cu = up > 0 ? a.c[(ck - VB) * H + j] : 0.f;
-        const float cv = vp > 0 ? a.c[(ck - a.B) * H + j] : 0.f;
+        const float cu = w.up > 0 ? a.c[(ck - VB) * H + j] : 0.f;
+        const float cv = w.vp > 0 ? a.c[(ck - a.B) * H + j] : 0.f;
         const float tc = mth(c);
         float da[5];
         if (!a.stable) {
             const float gi = ac[j], fu = ac[H + j], fv = ac[2 * H + j], gg = ac[3 * H + j], go = ac[4 * H + j];
-            const float dct = dc + dh * go * (1.f - tc * tc);
+            const float dct = dc + dh[t] * go * (1.f - tc * tc);
             da[0] = dct * gg * gi * (1.f - gi);
             da[1] = dct * cu * fu * (1.f - fu);
             da[2] = dct * cv * fv * (1.f - fv);
             da[3] = dct * gi * (1.f - gg * gg);
-            da[4] = dh * tc * go * (1.f - go);
+            da[4] = dh[t] * tc * go * (1.f - go);
             a.dcu[ck * H + j] = dct * fu;
             a.dcv[ck * H + j] = dct * fv;
         } else {
             const float gi = ac[j], f = ac[H + j], gg = ac[2 * H + j], go = ac[3 * H + j], lam = ac[4 * H + j];
-            const float dct = dc + dh * go * (1.f - tc * tc);
+            const float dct = dc + dh[t] * go * (1.f - tc * tc);
             const float m = lam * cu + (1.f - lam) * cv;
             da[0] = dct * gg * gi * (1.f - gi);
             da[1] = dct * m * f * (1.f - f);
             da[2] = dct * gi * (1.f - gg * gg);
-            da[3] = dh * tc * go * (1.f - go);
+            da[3] = dh[t] * tc * go * (1.f - go);
             da[4] = dct * f * (cu - cv) * lam * (1.f - lam);
             a.dcu[ck * H + j] = dct * f * lam;
             a.dcv[ck * H + j] = dct * f * (1.f - lam);
@@ -195,9 +287,9 @@ __global__ void md_bwd_diag_kernel(MdK a, int d) {
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
             df[q * H + j] = da[q];
-            const __half s = __float2half_rn(da[q] * scale);
-            d16[q * Hp + j] = s;
-            dp[q * Hp + j] = s;
+            const __half sv16 = __float2half_rn(da[q] * scale);
+            d16[q * Hp + j] = sv16;
+            dp[q * Hp + j] = sv16;
         }
     }
 }
@@ -353,7 +445,7 @@ int md_forward(const MdGeo &g, const float *theta, const float *x, const uint8_t
     if (gemm_f16({x16lo, g.Dp, 0}, {w16, g.Dp, 0}, gz2, 0, st)) return -5;
     for (int d = 0; d < g.U + g.V - 1; ++d) {
         ProfScope ps(PROF_REC_FWD, st);
-        md_fwd_diag_kernel<<<grid1(diag_threads(g.U, g.V, g.B, g.H, d)), 256, 0, st>>>(a, d);
+        md_fwd_diag_kernel<<<md_blocks(g.U, g.V, g.B, g.H, d), 256, 0, st>>>(a, d);
         note_launch();
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
@@ -378,7 +470,7 @@ int md_backward(const MdGeo &g, const float *theta, const float *x, const uint8_
     if (cudaMemsetAsync(ws + w.dap, 0, (size_t)g.cells * 20 * g.Hp * 2, st) != cudaSuccess) return -5;
     for (int d = g.U + g.V - 2; d >= 0; --d) {
         ProfScope ps(PROF_REC_BWD, st);
-        md_bwd_diag_kernel<<<grid1(diag_threads(g.U, g.V, g.B, g.H, d)), 256, 0, st>>>(a, d);
+        md_bwd_diag_kernel<<<md_blocks(g.U, g.V, g.B, g.H, d), 256, 0, st>>>(a, d);
         note_launch();
     }
     if (cudaGetLastError() != cudaSuccess) return -5;
