@@ -7,7 +7,7 @@ import sysconfig
 HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 ROOT = os.path.dirname(PKG)
-SOURCES = ["api.cu", "gemm.cu", "lstm_rec.cu", "rec_step.cu", "mdlstm.cu", "ops.cu", "optim.cu", "dp.cu", "prof.cu"]
+SOURCES = ["api.cu", "gemm.cu", "lstm_rec.cu", "rec_step.cu", "mdlstm.cu", "graph.cu", "ops.cu", "optim.cu", "dp.cu", "prof.cu"]
 OUT = os.path.join(PKG, "libblstm.so")
 
 

@@ -12,6 +12,7 @@
 // pairing is a fixed row shift of a zero-bordered [(U+1) x (V+1) x B] grid), db = column sums.
 #include "common.cuh"
 #include "gemm.h"
+#include "graph.h"
 #include "lstm_rec.h"
 #include "mdlstm.h"
 #include "ops.h"
@@ -443,12 +444,16 @@ int md_forward(const MdGeo &g, const float *theta, const float *x, const uint8_t
     gz2.beta = 1; gz2.bias = nullptr;
     if (gemm_f16({x16, g.Dp, 0}, {w16lo, g.Dp, 0}, gz2, 0, st)) return -5;
     if (gemm_f16({x16lo, g.Dp, 0}, {w16, g.Dp, 0}, gz2, 0, st)) return -5;
-    for (int d = 0; d < g.U + g.V - 1; ++d) {
-        ProfScope ps(PROF_REC_FWD, st);
-        md_fwd_diag_kernel<<<md_blocks(g.U, g.V, g.B, g.H, d), 256, 0, st>>>(a, d);
-        note_launch();
-    }
-    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+    // the U+V-1 wavefront launches, captured once into a CUDA graph (graph.h) and replayed
+    const std::vector<uint64_t> key{3, (uint64_t)g.U, (uint64_t)g.V, (uint64_t)g.B, (uint64_t)g.D, (uint64_t)g.H,
+                                    (uint64_t)g.stable, u64(theta), u64(mask), u64(y), u64(ws), u64(res)};
+    return graph_run(key, PROF_REC_FWD, st, {(const void *)md_fwd_diag_kernel}, [&](cudaStream_t s0) -> int {
+        for (int d = 0; d < g.U + g.V - 1; ++d) {
+            md_fwd_diag_kernel<<<md_blocks(g.U, g.V, g.B, g.H, d), 256, 0, s0>>>(a, d);
+            note_launch();
+        }
+        return cudaGetLastError() == cudaSuccess ? 0 : -5;
+    });
 }
 
 int md_backward(const MdGeo &g, const float *theta, const float *x, const uint8_t *mask, const float *dy, float *dx,
@@ -468,12 +473,16 @@ int md_backward(const MdGeo &g, const float *theta, const float *x, const uint8_
     if (cast_x_f16(x, g.D, g.D, x16, g.Dp, g.cells, st)) return -5;
     if (cudaMemsetAsync(ws + w.da16, 0, (size_t)4 * g.prow * 5 * g.Hp * 2, st) != cudaSuccess) return -5;
     if (cudaMemsetAsync(ws + w.dap, 0, (size_t)g.cells * 20 * g.Hp * 2, st) != cudaSuccess) return -5;
-    for (int d = g.U + g.V - 2; d >= 0; --d) {
-        ProfScope ps(PROF_REC_BWD, st);
-        md_bwd_diag_kernel<<<md_blocks(g.U, g.V, g.B, g.H, d), 256, 0, st>>>(a, d);
-        note_launch();
-    }
-    if (cudaGetLastError() != cudaSuccess) return -5;
+    const std::vector<uint64_t> key{4, (uint64_t)g.U, (uint64_t)g.V, (uint64_t)g.B, (uint64_t)g.D, (uint64_t)g.H,
+                                    (uint64_t)g.stable, u64(theta), u64(mask), u64(dy), u64(ws), u64(res)};
+    if (graph_run(key, PROF_REC_BWD, st, {(const void *)md_bwd_diag_kernel}, [&](cudaStream_t s0) -> int {
+            for (int d = g.U + g.V - 2; d >= 0; --d) {
+                md_bwd_diag_kernel<<<md_blocks(g.U, g.V, g.B, g.H, d), 256, 0, s0>>>(a, d);
+                note_launch();
+            }
+            return cudaGetLastError() == cudaSuccess ? 0 : -5;
+        }))
+        return -5;
     const __half *dap = (const __half *)(ws + w.dap);
     float *gsk = (float *)(ws + w.gsk);
     if (dx) {  // dX = dA W_all^T (the four directions sum in the contraction)

@@ -13,10 +13,8 @@
 #include "gemm.h"
 #include "lstm_rec.h"
 #include "prof.h"
+#include "graph.h"
 #include "rec_step.h"
-
-#include <map>
-#include <vector>
 
 namespace blstm {
 
@@ -120,100 +118,29 @@ int grid_of(long n) {
 size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * B * 4 * Hq * 4; }
 size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)3 * 2 * B * Hq * 4; }
 
-// ---------------------------------------------------------------------------------------------
-// The T-step loop of a layer is captured once into a CUDA graph (keyed by every pointer and size
-// it bakes in) and replayed: a loop of ~3T small launches is otherwise bound by the host's launch
-// rate.  Inside the graph the two directions' per-step GEMMs are parallel branches.
-// ---------------------------------------------------------------------------------------------
-namespace {
-
-struct GraphEntry {
-    cudaGraphExec_t exec;
-    long launches;
-};
-std::map<std::vector<uint64_t>, GraphEntry> g_graphs;
-cudaStream_t g_side = nullptr, g_cap = nullptr;  // capture streams (never the caller's: it may be legacy)
-cudaEvent_t g_fork = nullptr, g_join = nullptr;
-
-int side_init() {
-    if (g_side) return 0;
-    if (cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking) != cudaSuccess) return -5;
-    if (cudaStreamCreateWithFlags(&g_cap, cudaStreamNonBlocking) != cudaSuccess) return -5;
-    if (cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess) return -5;
-    if (cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming) != cudaSuccess) return -5;
-    return 0;
-}
-
-// fork: work on g_side may start once everything issued so far on st has; join: st waits for g_side
-void fork_side(cudaStream_t st) {
-    cudaEventRecord(g_fork, st);
-    cudaStreamWaitEvent(g_side, g_fork, 0);
-}
-void join_side(cudaStream_t st) {
-    cudaEventRecord(g_join, g_side);
-    cudaStreamWaitEvent(st, g_join, 0);
-}
-
-template <typename Body>
-int run_graph(const std::vector<uint64_t> &key, int cat, cudaStream_t st, Body body) {
-    auto it = g_graphs.find(key);
-    if (it == g_graphs.end()) {
-        // load every kernel the body launches first: a lazy module load synchronizes the context,
-        // which a capturing stream does not allow
-        if (gemm_prepare() || side_init()) return -5;
-        cudaFuncAttributes fa;
-        if (cudaFuncGetAttributes(&fa, step_fwd_gate_kernel) != cudaSuccess) return -5;
-        if (cudaFuncGetAttributes(&fa, step_bwd_gate_kernel) != cudaSuccess) return -5;
-        const long n0 = launch_count();
-        // recorded on a stream of our own (capture is not allowed on the legacy default stream);
-        // the graph is then launched on the caller's stream
-        if (cudaStreamBeginCapture(g_cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return -5;
-        prof_suspend(1);
-        const int rc = body(g_cap);
-        prof_suspend(0);
-        cudaGraph_t graph = nullptr;
-        const cudaError_t e = cudaStreamEndCapture(g_cap, &graph);
-        const long nl = launch_count() - n0;
-        note_launch((int)-nl);  // counted when the graph runs, not when it is recorded
-        if (rc || e != cudaSuccess || !graph) {
-            if (graph) cudaGraphDestroy(graph);
-            return -5;
-        }
-        GraphEntry en{nullptr, nl};
-        const cudaError_t ei = cudaGraphInstantiate(&en.exec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (ei != cudaSuccess) return -5;
-        it = g_graphs.emplace(key, en).first;
-    }
-    ProfScope ps(cat, st);
-    if (cudaGraphLaunch(it->second.exec, st) != cudaSuccess) return -5;
-    note_launch((int)it->second.launches);
-    return 0;
-}
-
-uint64_t u64(const void *p) { return (uint64_t)(uintptr_t)p; }
-
-}  // namespace
+// The T-step loop of a layer is captured once into a CUDA graph (graph.h) and replayed: a loop of
+// ~3T small launches is otherwise bound by the host's launch rate.  Inside the graph the two
+// directions' per-step GEMMs are parallel branches.
 
 int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
     const int Hq = p.Hq, B = p.B, T = p.T;
     const std::vector<uint64_t> key{1, (uint64_t)T, (uint64_t)B, (uint64_t)p.H, (uint64_t)Hq, u64(p.Z), u64(p.mask),
                                     u64(p.RT16), u64(p.P), u64(p.C), (uint64_t)p.ldc, (uint64_t)p.c_doff, u64(p.y),
                                     (uint64_t)p.ldy, (uint64_t)p.y_doff, u64(p.y16), u64(p.gates), u64(p.hist)};
-    return run_graph(key, PROF_REC_FWD, st, [&](cudaStream_t s0) -> int {
+    return graph_run(key, PROF_REC_FWD, st, {(const void *)step_fwd_gate_kernel}, [&](cudaStream_t s0) -> int {
         for (int s = 0; s < T; ++s) {
             if (s > 0) {
-                fork_side(s0);
+                graph_fork(s0);
                 for (int d = 0; d < 2; ++d) {
                     const int dir = d == 0 ? 1 : -1;
                     const int t = d == 0 ? s : T - 1 - s;
                     const __half *hprev = p.hist + ((long)d * (T + 1) + t + (dir < 0)) * B * Hq;
                     GemmParams g{B, 4 * Hq, Hq, p.P + (size_t)d * B * 4 * Hq, 4L * Hq, 1.f, 0, nullptr, 0, 0};
                     g.bn = 128;
-                    if (gemm_f16({hprev, Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 0}, g, 0, d ? g_side : s0))
+                    if (gemm_f16({hprev, Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 0}, g, 0, d ? graph_side() : s0))
                         return -5;
                 }
-                join_side(s0);
+                graph_join(s0);
             }
             step_fwd_gate_kernel<<<grid_of(2L * B * Hq), 256, 0, s0>>>(p, s);
             note_launch();
@@ -230,13 +157,13 @@ int rec_step_bwd(const RecStepBwd &p, cudaStream_t st) {
                                     u64(p.C), (uint64_t)p.ldc, (uint64_t)p.c_doff, u64(p.gates), u64(p.dy),
                                     (uint64_t)p.lddy, (uint64_t)p.dy_doff, u64(p.dA), u64(p.dhR), u64(p.dhc),
                                     u64(p.dcc), u64(p.splitk_ws), (uint64_t)p.splitk_elems};
-    return run_graph(key, PROF_REC_BWD, st, [&](cudaStream_t s0) -> int {
+    return graph_run(key, PROF_REC_BWD, st, {(const void *)step_bwd_gate_kernel}, [&](cudaStream_t s0) -> int {
         for (int s = 0; s < T; ++s) {
             step_bwd_gate_kernel<<<grid_of(2L * B * Hq), 256, 0, s0>>>(p, s);
             note_launch();
             if (cudaGetLastError() != cudaSuccess) return -5;
             if (s + 1 == T) break;
-            fork_side(s0);
+            graph_fork(s0);
             for (int d = 0; d < 2; ++d) {
                 const int t = d == 0 ? T - 1 - s : s;
                 const __half *dA = p.dA + ((size_t)t * B) * 8 * Hq + (size_t)d * 4 * Hq;
@@ -245,10 +172,10 @@ int rec_step_bwd(const RecStepBwd &p, cudaStream_t st) {
                 // each direction its own half of the split-K scratch (the branches run concurrently)
                 g.splitk_ws = p.splitk_ws + (size_t)d * (p.splitk_elems / 2);
                 g.splitk_elems = p.splitk_elems / 2;
-                if (gemm_f16({dA, 8L * Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 1}, g, 0, d ? g_side : s0))
+                if (gemm_f16({dA, 8L * Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 1}, g, 0, d ? graph_side() : s0))
                     return -5;
             }
-            join_side(s0);
+            graph_join(s0);
         }
         return 0;
     });

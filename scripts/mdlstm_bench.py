@@ -59,8 +59,8 @@ def run(U, V, B, D, H, K=20):
     rec_flop = cells * 4 * 2 * 5 * H * H * 2  # per pass: 2 predecessors x 5H x H FMAs = 2 flop each
     out = dict(U=U, V=V, B=B, D=D, H=H, diagonals=U + V - 1, ms_fwd_bwd=round(ms, 3),
                cells_per_s=round(cells / (ms * 1e-3)), wavefront_fwd_ms=round(fw[0], 3), wavefront_bwd_ms=round(bw[0], 3),
-               gemm_ms=round(gm[0], 3), us_per_diagonal_fwd=round(1e3 * fw[0] / fw[1], 2),
-               us_per_diagonal_bwd=round(1e3 * bw[0] / bw[1], 2),
+               gemm_ms=round(gm[0], 3), us_per_diagonal_fwd=round(1e3 * fw[0] / (U + V - 1), 2),
+               us_per_diagonal_bwd=round(1e3 * bw[0] / (U + V - 1), 2),
                roofline={"bound": "alu (fp32 FMA)", "achieved_tflops_fwd": round(rec_flop / (fw[0] * 1e-3) / 1e12, 2),
                          "achieved_tflops_bwd": round(rec_flop / (bw[0] * 1e-3) / 1e12, 2),
                          "peak_tflops": round(PEAK_FP32, 1),
