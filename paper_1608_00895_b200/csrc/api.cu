@@ -702,7 +702,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             q.dy = p.dy; q.lddy = p.lddy; q.dy_doff = p.dy_doff;
             q.dA = dA;
             float *sb = (float *)(ws + w.stepB);
-            q.dhR = sb; q.dhc = sb + 2L * g.B * Hq; q.dcc = sb + 4L * g.B * Hq;
+            q.dhR = sb; q.dhc = sb + 16L * g.B * Hq; q.dcc = sb + 18L * g.B * Hq;  // (rec_step: 2 x SB = 16 partials)
             q.splitk_ws = (float *)(ws + w.gsk); q.splitk_elems = GSK_ELEMS;
             TRY(rec_step_bwd(q, st), "rec_step_bwd");
             if (cudaMemsetAsync(dbp, 0, (size_t)8 * Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");

@@ -441,6 +441,14 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
     // split K when the output tiles leave at least half of the allowed CTAs idle
     const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
     const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+    if (p.partials > 0) {  // fixed split, partials left for the consumer (no reduction launch)
+        if (!p.splitk_ws || p.natB || p.flags || p.beta || p.bias || (long)p.partials * p.M * p.N > p.splitk_elems)
+            return -3;
+        GemmParams q = p;
+        q.C = p.splitk_ws; q.ldc = p.N; q.ksplit = p.partials; q.split_stride = (long)p.M * p.N;
+        cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, q, max_ctas, st) : launch_gemm<128>(ta, tb, q, max_ctas, st);
+        return e == cudaSuccess ? 0 : -5;
+    }
     int S = 1;
     if (p.splitk_ws && !p.natB && !p.flags && tiles * 2 <= max_ctas && num_kb >= 32) {
         S = max_ctas / tiles;

@@ -39,6 +39,10 @@ struct GemmParams {
     int ksplit = 1;          // set by gemm_f16
     long split_stride = 0;   // set by gemm_f16: C offset of split s (elements)
     int bn = 0;              // N tile: 0 = gemm_bn(N); 128 forces the narrow tile (more CTAs for small M)
+    // > 0: split K exactly this many ways and leave the fp32 partials in splitk_ws (split s at
+    // s * M * N, row-major [M][N]) for the consumer to sum -- no reduction launch (alpha applies
+    // to each partial; beta / bias unsupported)
+    int partials = 0;
 };
 
 constexpr int GEMM_BM_ROWS = 128;           // M tile

@@ -18,6 +18,11 @@
 
 namespace blstm {
 
+// per-step GEMMs split K this many ways into fp32 partials, summed (fixed order) by the gate kernel
+// that consumes them: 4x / 8x the CTAs of the unsplit GEMM and no reduction launch
+constexpr int SF = 2;  // forward  h R^T: K = Hq (a multiple of 256); 2 x 2 directions x 32 tiles <= 148 SMs
+constexpr int SB = 8;  // BPTT     dA R:  K = 4Hq
+
 namespace {
 
 DEVI float sg(float z) { return __fdividef(1.f, 1.f + __expf(-z)); }
@@ -45,8 +50,11 @@ __global__ void step_fwd_gate_kernel(RecStepFwd p, int s) {
             const float4 z = reinterpret_cast<const float4 *>(p.Z + r * 8 * Hq + (long)d * 4 * Hq)[u];
             float4 a = z;
             if (s > 0) {
-                const float4 q = reinterpret_cast<const float4 *>(p.P + ((long)d * B + b) * 4 * Hq)[u];
-                a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
+#pragma unroll
+                for (int k = 0; k < SF; ++k) {
+                    const float4 q = reinterpret_cast<const float4 *>(p.P + (((long)d * SF + k) * B + b) * 4 * Hq)[u];
+                    a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
+                }
             }
             act = make_float4(sg(a.x), sg(a.y), th(a.z), sg(a.w));
             c = act.y * c_prev + act.x * act.z;
@@ -78,7 +86,13 @@ __global__ void step_bwd_gate_kernel(RecStepBwd p, int s) {
         float dh_in = 0.f, dc = 0.f;
         if (s > 0) {
             const long rp = r + (long)dir * B;       // the frame processed at step s-1
-            dh_in = p.mask[rp] ? p.dhR[sidx] : p.dhc[sidx];
+            if (p.mask[rp]) {
+                const long pb = (long)d * SB * B * Hq + (long)b * Hq + u;
+#pragma unroll
+                for (int k = 0; k < SB; ++k) dh_in += p.dhR[pb + (long)k * B * Hq];
+            } else {
+                dh_in = p.dhc[sidx];
+            }
             dc = p.dcc[sidx];
         }
         __half2 *dap = reinterpret_cast<__half2 *>(p.dA + r * 8 * Hq + (long)d * 4 * Hq + 4 * u);
@@ -115,8 +129,8 @@ int grid_of(long n) {
 
 }  // namespace
 
-size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * B * 4 * Hq * 4; }
-size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)3 * 2 * B * Hq * 4; }
+size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * SF * B * 4 * Hq * 4; }
+size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)(2 * SB + 4) * B * Hq * 4; }
 
 // The T-step loop of a layer is captured once into a CUDA graph (graph.h) and replayed: a loop of
 // ~3T small launches is otherwise bound by the host's launch rate.  Inside the graph the two
@@ -135,8 +149,11 @@ int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
                     const int dir = d == 0 ? 1 : -1;
                     const int t = d == 0 ? s : T - 1 - s;
                     const __half *hprev = p.hist + ((long)d * (T + 1) + t + (dir < 0)) * B * Hq;
-                    GemmParams g{B, 4 * Hq, Hq, p.P + (size_t)d * B * 4 * Hq, 4L * Hq, 1.f, 0, nullptr, 0, 0};
+                    GemmParams g{B, 4 * Hq, Hq, nullptr, 4L * Hq, 1.f, 0, nullptr, 0, 0};
                     g.bn = 128;
+                    g.partials = SF;
+                    g.splitk_ws = p.P + (size_t)d * SF * B * 4 * Hq;
+                    g.splitk_elems = (long)SF * B * 4 * Hq;
                     if (gemm_f16({hprev, Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 0}, g, 0, d ? graph_side() : s0))
                         return -5;
                 }
@@ -167,11 +184,11 @@ int rec_step_bwd(const RecStepBwd &p, cudaStream_t st) {
             for (int d = 0; d < 2; ++d) {
                 const int t = d == 0 ? T - 1 - s : s;
                 const __half *dA = p.dA + ((size_t)t * B) * 8 * Hq + (size_t)d * 4 * Hq;
-                GemmParams g{B, Hq, 4 * Hq, p.dhR + (size_t)d * B * Hq, (long)Hq, alpha, 0, nullptr, 0, 0};
+                GemmParams g{B, Hq, 4 * Hq, nullptr, (long)Hq, alpha, 0, nullptr, 0, 0};
                 g.bn = 128;
-                // each direction its own half of the split-K scratch (the branches run concurrently)
-                g.splitk_ws = p.splitk_ws + (size_t)d * (p.splitk_elems / 2);
-                g.splitk_elems = p.splitk_elems / 2;
+                g.partials = SB;
+                g.splitk_ws = p.dhR + (size_t)d * SB * B * Hq;
+                g.splitk_elems = (long)SB * B * Hq;
                 if (gemm_f16({dA, 8L * Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 1}, g, 0, d ? graph_side() : s0))
                     return -5;
             }

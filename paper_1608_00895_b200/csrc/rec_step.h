@@ -17,7 +17,7 @@ struct RecStepFwd {
     const float *Z;          // [T*B][8Hq] row-major, column d*4Hq + 4u + gamma, bias included
     const uint8_t *mask;     // [T*B]
     const __half *RT16;      // [2][4Hq][Hq] (R^T per direction, gate-interleaved rows)
-    float *P;                // [2][B][4Hq] scratch: this step's h_{t-1} R^T
+    float *P;                // [2][SF][B][4Hq] scratch: this step's h_{t-1} R^T as split-K partials
     float *C;                // cell state after frame t: C[d*c_doff + r*ldc + u]
     long ldc, c_doff;
     float *y;                // [T*B][ldy] (+ d*y_doff), u < H; nullable
@@ -37,7 +37,7 @@ struct RecStepBwd {
     const float *dy;         // [T*B][lddy] (+ d*dy_doff), u < H
     long lddy, dy_doff;
     __half *dA;              // [T*B][8Hq], scaled by 2^DA_SHIFT
-    float *dhR;              // [2][B][Hq] scratch: dA_t R of the previous step
+    float *dhR;              // [2][SB][B][Hq] scratch: dA_t R of the previous step (split-K partials)
     float *dhc, *dcc;        // [2][B][Hq] carried dh (masked frames) and dc
     float *splitk_ws;        // split-K scratch of the per-step GEMM
     long splitk_elems;
