@@ -233,7 +233,79 @@ constexpr int CE_THREADS = 256;  // 8 warps, one frame (row) per warp
 // one warp per frame: coalesced 128-byte reads of the logits row (re-reads hit L1), warp-shuffle
 // max / argmax (ties: lowest index) and sum, 16-byte fp16 stores of dlogits.  Per row:
 //   loss = lse - logit[label],  err = argmax != label,  dlog = (softmax - onehot) * scale
+template <int CE_CHUNKS>
 __global__ void __launch_bounds__(CE_THREADS) ce_head_kernel(const float *__restrict__ logits, long ldl, int K, int Kp,
+                                                             const uint8_t *__restrict__ mask,
+                                                             const int32_t *__restrict__ labels, float scale,
+                                                             __half *__restrict__ dlog16, double *__restrict__ rowloss,
+                                                             int32_t *__restrict__ rowerr, long rows) {
+    const long r = (long)blockIdx.x * (CE_THREADS / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    __half *drow = dlog16 + r * Kp;
+    if (!mask[r]) {
+        for (int k = lane * 8; k < Kp; k += 256) *reinterpret_cast<uint4 *>(drow + k) = make_uint4(0, 0, 0, 0);
+        if (lane == 0) { rowloss[r] = 0.0; rowerr[r] = 0; }
+        return;
+    }
+    // the row is read once into registers: lane owns columns [256c + 8 lane, +8) of chunk c
+    // (float4 loads; every warp access is 1 KB contiguous), exp is evaluated once per logit
+    const float *lrow = logits + r * ldl;
+    float v[CE_CHUNKS][8];
+    float mv = -INFINITY;
+    int mi = 0x7fffffff;
+#pragma unroll
+    for (int c = 0; c < CE_CHUNKS; ++c) {
+        const int k0 = 256 * c + 8 * lane;
+        if (k0 < Kp) {
+            const float4 a = *reinterpret_cast<const float4 *>(lrow + k0);
+            const float4 b = *reinterpret_cast<const float4 *>(lrow + k0 + 4);
+            v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
+            v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (k0 + u >= K) v[c][u] = -INFINITY;
+            if (v[c][u] > mv) { mv = v[c][u]; mi = k0 + u; }  // ascending k per lane: first max = lowest index
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, mv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
+        if (ov > mv || (ov == mv && oi < mi)) { mv = ov; mi = oi; }
+    }
+    float se = 0.f;
+#pragma unroll
+    for (int c = 0; c < CE_CHUNKS; ++c)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            v[c][u] = __expf(v[c][u] - mv);  // exp(-inf) = 0 past K
+            se += v[c][u];
+        }
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const float lse = mv + __logf(se), inv = 1.f / se;
+    const int lab = labels[r];
+#pragma unroll
+    for (int c = 0; c < CE_CHUNKS; ++c) {
+        const int k0 = 256 * c + 8 * lane;
+        if (k0 >= Kp) continue;
+        uint32_t hv[4];
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+            const bool l0 = k0 + u == lab, l1 = k0 + u + 1 == lab;
+            const float p0 = v[c][u] * inv - (l0 ? 1.f : 0.f), p1 = v[c][u + 1] * inv - (l1 ? 1.f : 0.f);
+            __half2 h2 = __floats2half2_rn(p0 * scale, p1 * scale);
+            hv[u / 2] = *reinterpret_cast<uint32_t *>(&h2);
+        }
+        *reinterpret_cast<uint4 *>(drow + k0) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+    }
+    if (lane == 0) {
+        rowloss[r] = (double)lse - (double)lrow[lab];
+        rowerr[r] = mi != lab;
+    }
+}
+// generic width (Kp > 2048): three passes over the row
+__global__ void __launch_bounds__(CE_THREADS) ce_head_any_kernel(const float *__restrict__ logits, long ldl, int K, int Kp,
                                                              const uint8_t *__restrict__ mask,
                                                              const int32_t *__restrict__ labels, float scale,
                                                              __half *__restrict__ dlog16, double *__restrict__ rowloss,
@@ -286,8 +358,16 @@ int ce_head(const float *logits, long ldl, int K, int Kp, const uint8_t *mask, c
     ProfScope ps_(PROF_OTHER, st);
     if (rows <= 0) return 0;
     const long blocks = (rows + CE_THREADS / 32 - 1) / (CE_THREADS / 32);
-    ce_head_kernel<<<(unsigned)blocks, CE_THREADS, 0, st>>>(logits, ldl, K, Kp, mask, labels, scale, dlog16, rowloss,
-                                                            rowerr, rows);
+    const int ch = (Kp + 255) / 256;
+#define CE_CASE(C)                                                                                             \
+    if (ch <= C)                                                                                               \
+        ce_head_kernel<C><<<(unsigned)blocks, CE_THREADS, 0, st>>>(logits, ldl, K, Kp, mask, labels, scale, dlog16, \
+                                                                   rowloss, rowerr, rows);                     \
+    else
+    CE_CASE(1) CE_CASE(2) CE_CASE(4) CE_CASE(8)
+    ce_head_any_kernel<<<(unsigned)blocks, CE_THREADS, 0, st>>>(logits, ldl, K, Kp, mask, labels, scale, dlog16,
+                                                                rowloss, rowerr, rows);
+#undef CE_CASE
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
