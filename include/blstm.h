@@ -235,6 +235,24 @@ int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_desc *layout, 
                      float *state, size_t n, int zero_grad, void *workspace, size_t workspace_bytes,
                      void *stream);
 
+/*
+ * One whole training step: blstm_stack_fwd_bwd, then the update rule opt (blstm_opt_update
+ * semantics with the stack's layout: L2 on weights only, optional global norm constraint) applied
+ * to theta, grad set to 0 afterwards (the update "fused into the allreduce
+ * epilogue").  Each gradient bucket (one per layer, one for the head) is updated on s_side as soon
+ * as it is final -- after its scatters and, with comm, its allreduce -- overlapping the BPTT of the
+ * layers below; with opt->max_norm > 0 (the norm needs every gradient) one update runs at the end.
+ *   theta [P] DEVICE, updated in place; grad [P] DEVICE (+= then consumed: 0 on return)
+ *   opt_state: blstm_opt_state_floats(opt->rule, P) DEVICE floats (NULL if 0)
+ * Other arguments as blstm_stack_fwd_bwd.  The result equals blstm_stack_fwd_bwd followed by
+ * blstm_opt_update(opt, d, ..., zero_grad = 1) bit for bit.
+ */
+int blstm_stack_train_step(const blstm_stack_desc *d, float *theta, float *grad, const float *x, const uint8_t *mask,
+                           const int32_t *labels, const float *dy_top, double *loss_sum, int32_t *frame_errors,
+                           dp_comm *comm, const blstm_opt_params *opt, float *opt_state, void *workspace,
+                           size_t workspace_bytes, void *s_main, void *s_side);
+
+
 /* ------------------------------------------------------------------------ */
 /* Data parallelism over NCCL (§4.1).                      */
 /* ------------------------------------------------------------------------ */

@@ -68,6 +68,8 @@ _SIGS = {
     "blstm_param_offsets": (_sz, [ctypes.POINTER(StackDesc), ctypes.POINTER(ctypes.c_size_t)]),
     "blstm_stack_workspace_bytes": (_sz, [ctypes.POINTER(StackDesc)]),
     "blstm_stack_fwd_bwd": (_i, [ctypes.POINTER(StackDesc)] + [_vp] * 10 + [_sz, _vp, _vp]),
+    "blstm_stack_train_step": (_i, [ctypes.POINTER(StackDesc)] + [_vp] * 9 + [ctypes.POINTER(OptParams), _vp, _vp,
+                                                                             _sz, _vp, _vp]),
     "blstm_stack_fwd": (_i, [ctypes.POINTER(StackDesc)] + [_vp] * 6 + [_sz, _vp]),
     "sgd_update": (_i, [_vp, _vp, _sz, ctypes.c_float, _i, _vp]),
     "blstm_opt_state_floats": (_sz, [_i, _sz]),
@@ -229,6 +231,15 @@ def blstm_stack_fwd_bwd(desc, theta, grad, x, mask, labels, dy_top, loss_sum, fr
         ctypes.byref(desc), _p(theta), _p(grad), _p(x), _p(mask), _p(labels), _p(dy_top), _p(loss_sum),
         _p(frame_errors), comm, _p(workspace), workspace.numel() * workspace.element_size(), sm,
         _stream(s_side) if s_side is not None else sm))
+
+
+def blstm_stack_train_step(desc, theta, grad, x, mask, labels, dy_top, loss_sum, frame_errors, comm, opt: "OptParams",
+                           opt_state, workspace, s_main=None, s_side=None):
+    sm = _stream(s_main)
+    _check("blstm_stack_train_step", lib().blstm_stack_train_step(
+        ctypes.byref(desc), _p(theta), _p(grad), _p(x), _p(mask), _p(labels), _p(dy_top), _p(loss_sum),
+        _p(frame_errors), comm, ctypes.byref(opt), _p(opt_state), _p(workspace),
+        workspace.numel() * workspace.element_size(), sm, _stream(s_side) if s_side is not None else sm))
 
 
 def blstm_stack_fwd(desc, theta, x, mask, Y, C, workspace, stream=None):

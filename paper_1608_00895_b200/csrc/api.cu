@@ -304,7 +304,7 @@ struct StackGeo {
 };
 struct StackWS {
     size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, gsk,
-        stepF, stepB, cs2, total;
+        stepF, stepB, cs2, optp, total;
     size_t maxDn;
     std::vector<size_t> y16, w16, rt16, bq, gates, C, hist;
 };
@@ -387,6 +387,7 @@ static StackWS stack_ws(const StackGeo &g) {
     w.stepF = c.take(g.step ? rec_step_fwd_scratch_bytes(g.B, Hq) : 0);
     w.stepB = c.take(g.step ? rec_step_bwd_scratch_bytes(g.B, Hq) : 0);
     w.cs2 = c.take(g.step ? colsum_scratch_bytes(TB, 8 * Hq) : 0);
+    w.optp = c.take(sizeof(double) * (size_t)opt_norm_partials());  // norm partials of a fused update
     w.total = c.off;
     return w;
 }
@@ -538,11 +539,17 @@ extern "C" int blstm_stack_fwd(const blstm_stack_desc *d, const float *theta, co
 
 int dp_allreduce_grads_impl(dp_comm *c, float *grad, size_t n, cudaStream_t st);
 
-extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta, float *grad, const float *x,
-                                   const uint8_t *mask, const int32_t *labels, const float *dy_top, double *loss_sum,
-                                   int32_t *frame_errors, dp_comm *comm, void *workspace, size_t workspace_bytes,
-                                   void *s_main, void *s_side) {
-    (void)s_side;
+static int opt_range(const blstm_opt_params *p, const blstm_stack_desc *layout, float *theta, float *grad,
+                     float *state, size_t n, size_t lo, size_t hi, int zero_grad, double *partial, cudaStream_t st);
+static int opt_check(const blstm_opt_params *p, float *theta, float *grad, float *state, size_t n);
+
+// forward + BPTT (+ the update rule opt, when given: per bucket on the side stream as soon as the
+// bucket is final -- after its scatters and its allreduce -- or, with the global norm constraint,
+// once over everything at the end)
+static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float *grad, const float *x,
+                           const uint8_t *mask, const int32_t *labels, const float *dy_top, double *loss_sum,
+                           int32_t *frame_errors, dp_comm *comm, const blstm_opt_params *opt, float *opt_state,
+                           void *workspace, size_t workspace_bytes, void *s_main, void *s_side) {
     StackGeo g;
     if (int rc = stack_geo(d, g)) return rc;
     const StackWS w = stack_ws(g);
@@ -572,6 +579,7 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
     cudaStream_t side = (s_side && s_side != s_main && !no_side) ? (cudaStream_t)s_side : st;
     const bool overlap = side != st;
     const int rec_ctas = 2 * g.pl.G * g.pl.NC;
+    const bool bucket_update = opt && !(opt->max_norm > 0.0);
     // per-layer BPTT start counters (zeroed with the Z flags by stack_forward)
     uint32_t *bstarted = (uint32_t *)(ws + w.zflags) + (zflag_words(g) - g.L);
     // Side-stream work that overlaps BPTT(l) must not take SMs before BPTT(l)'s clusters are all
@@ -639,6 +647,9 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         if (comm) {  // sync-mode exchange of this bucket (the head), overlapping the BPTT below
             if (int rc = dp_allreduce_grads_impl(comm, grad + offs[6 * g.L], nparam - offs[6 * g.L], side)) return rc;
         }
+        if (bucket_update)  // the head's parameters are final: update them now (NEXT-3, fused)
+            if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, offs[6 * g.L], nparam, 1, nullptr, side))
+                return rc;
         return 0;
     };
     auto side_layer = [&](int l) -> int {  // dW, dR, db of layer l (inputs: dA / dbpart of its parity)
@@ -669,10 +680,13 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
             TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, side), "scatter dR");
             TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.step ? 1 : g.pl.G, dd, side), "scatter db");
         }
+        const size_t end = l + 1 < g.L ? offs[6 * (l + 1)] : offs[6 * g.L];
         if (comm) {  // sync-mode exchange of layer l's bucket (§4.1), overlapping BPTT
-            const size_t end = l + 1 < g.L ? offs[6 * (l + 1)] : offs[6 * g.L];
             if (int rc = dp_allreduce_grads_impl(comm, grad + offs[6 * l], end - offs[6 * l], side)) return rc;
         }
+        if (bucket_update)  // layer l's parameters are final: update them while BPTT continues below
+            if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, offs[6 * l], end, 1, nullptr, side))
+                return rc;
         if (overlap) cudaEventRecord(evs[g.L + 2 + l], side);
         return 0;
     };
@@ -728,7 +742,31 @@ extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta
         cudaEventRecord(evs[g.L], side);
         cudaStreamWaitEvent(st, evs[g.L], 0);
     }
+    if (opt && !bucket_update)  // the global norm constraint needs every gradient: one update at the end
+        if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, 0, nparam, 1, (double *)(ws + w.optp), st))
+            return rc;
     return 0;
+}
+
+extern "C" int blstm_stack_fwd_bwd(const blstm_stack_desc *d, const float *theta, float *grad, const float *x,
+                                   const uint8_t *mask, const int32_t *labels, const float *dy_top, double *loss_sum,
+                                   int32_t *frame_errors, dp_comm *comm, void *workspace, size_t workspace_bytes,
+                                   void *s_main, void *s_side) {
+    return stack_step_impl(d, theta, grad, x, mask, labels, dy_top, loss_sum, frame_errors, comm, nullptr, nullptr,
+                           workspace, workspace_bytes, s_main, s_side);
+}
+
+extern "C" int blstm_stack_train_step(const blstm_stack_desc *d, float *theta, float *grad, const float *x,
+                                      const uint8_t *mask, const int32_t *labels, const float *dy_top, double *loss_sum,
+                                      int32_t *frame_errors, dp_comm *comm, const blstm_opt_params *opt,
+                                      float *opt_state, void *workspace, size_t workspace_bytes, void *s_main,
+                                      void *s_side) {
+    const size_t n = blstm_param_count(d);
+    if (n == 0) return fail(BLSTM_ERR_ARG, "blstm_stack_train_step: bad descriptor");
+    if (int rc = opt_check(opt, theta, grad, opt_state, n)) return rc;
+    if (d->L > 31) return fail(BLSTM_ERR_UNSUPPORTED, "update with L=%d > 31", d->L);
+    return stack_step_impl(d, theta, grad, x, mask, labels, dy_top, loss_sum, frame_errors, comm, opt, opt_state,
+                           workspace, workspace_bytes, s_main, s_side);
 }
 
 extern "C" int sgd_update(float *theta, float *grad, size_t n, float lr, int zero_grad, void *stream) {
@@ -752,45 +790,32 @@ extern "C" size_t blstm_opt_state_floats(int rule, size_t n) {
 }
 extern "C" size_t blstm_opt_workspace_bytes(size_t) { return sizeof(double) * (size_t)opt_norm_partials(); }
 
-extern "C" int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_desc *layout, float *theta, float *grad,
-                                float *state, size_t n, int zero_grad, void *workspace, size_t workspace_bytes,
-                                void *stream) {
-    if (!p || !theta || !grad) return fail(BLSTM_ERR_ARG, "blstm_opt_update: null params / theta / grad");
-    if (p->rule < BLSTM_OPT_SGD || p->rule > BLSTM_OPT_ADAM) return fail(BLSTM_ERR_ARG, "unknown rule %d", p->rule);
-    if (p->rule == BLSTM_OPT_ADAM && p->step < 1) return fail(BLSTM_ERR_ARG, "ADAM needs step >= 1");
-    const size_t ns = blstm_opt_state_floats(p->rule, n);
-    if (ns && !state) return fail(BLSTM_ERR_ARG, "rule %d needs %zu floats of state", p->rule, ns);
-    if (!al16(theta) || !al16(grad) || (ns && !al16(state)))
-        return fail(BLSTM_ERR_ALIGN, "theta / grad / state must be 16-byte aligned");
-    if (p->max_norm > 0.0) {
-        if (!workspace || !al16(workspace)) return fail(BLSTM_ERR_ALIGN, "norm constraint needs an aligned workspace");
-        if (workspace_bytes < blstm_opt_workspace_bytes(n))
-            return fail(BLSTM_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, blstm_opt_workspace_bytes(n));
-    }
+// One update over [lo, hi) of an n-entry vector (state slot s0 at state + i, s1 at state + n4 + i);
+// the layout's bias ranges are rebased to lo (a boundary before lo still counts: the pairing of
+// [start, end) boundaries is what marks an index as a bias entry).  lo must be a multiple of 4.
+static int opt_range(const blstm_opt_params *p, const blstm_stack_desc *layout, float *theta, float *grad,
+                     float *state, size_t n, size_t lo, size_t hi, int zero_grad, double *partial, cudaStream_t st) {
     OptBiasTable tab;
     tab.nb = 0;
     for (int k = 0; k < OPT_MAX_BOUNDS; ++k) tab.bnd[k] = 0x7fffffffffffffffL;
     if (layout) {
-        if (layout->L > 31) return fail(BLSTM_ERR_UNSUPPORTED, "layout with L=%d > 31", layout->L);
-        const size_t np = blstm_param_count(layout);
-        if (np == 0 || np != n) return fail(BLSTM_ERR_ARG, "n=%zu != blstm_param_count(layout)=%zu", n, np);
         std::vector<size_t> offs(6 * layout->L + 2);
         param_layout(layout, offs.data());
         const long h4 = 4L * layout->H;
         for (int l = 0; l < layout->L; ++l)
             for (int dd = 0; dd < 2; ++dd) {
-                const long b0 = (long)offs[6 * l + 3 * dd + 2];
+                const long b0 = (long)offs[6 * l + 3 * dd + 2] - (long)lo;
                 tab.bnd[tab.nb++] = b0;
                 tab.bnd[tab.nb++] = b0 + h4;
             }
         if (layout->K > 0) {
-            tab.bnd[tab.nb++] = (long)offs[6 * layout->L + 1];
-            tab.bnd[tab.nb++] = (long)offs[6 * layout->L + 1] + layout->K;
+            tab.bnd[tab.nb++] = (long)offs[6 * layout->L + 1] - (long)lo;
+            tab.bnd[tab.nb++] = (long)offs[6 * layout->L + 1] + layout->K - (long)lo;
         }
     }
-    const size_t n4 = rup4(n);
-    float *s0 = ns ? state : nullptr;
-    float *s1 = ns > n4 ? state + n4 : nullptr;
+    const size_t ns = blstm_opt_state_floats(p->rule, n), n4 = rup4(n);
+    float *s0 = ns ? state + lo : nullptr;
+    float *s1 = ns > n4 ? state + n4 + lo : nullptr;
     OptArgs a{(float)p->lr, (float)p->mu, (float)p->rho, (float)p->beta1, (float)p->beta2, (float)p->eps,
               (float)p->l2, (float)p->max_norm, (float)(1.0 - p->rho), (float)(1.0 - p->beta1),
               (float)(1.0 - p->beta2), 1.f, 1.f};
@@ -798,10 +823,38 @@ extern "C" int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_des
         a.c1 = (float)(1.0 / (1.0 - pow(p->beta1, (double)p->step)));
         a.c2 = (float)(1.0 / (1.0 - pow(p->beta2, (double)p->step)));
     }
-    if (n == 0) return 0;
-    TRY(opt_update(p->rule, theta, grad, s0, s1, (long)n, a, p->max_norm, tab, (double *)workspace, zero_grad,
-                   (cudaStream_t)stream), "opt_update");
+    if (hi <= lo) return 0;
+    TRY(opt_update(p->rule, theta + lo, grad + lo, s0, s1, (long)(hi - lo), a, p->max_norm, tab, partial, zero_grad, st),
+        "opt_update");
     return 0;
+}
+
+static int opt_check(const blstm_opt_params *p, float *theta, float *grad, float *state, size_t n) {
+    if (!p || !theta || !grad) return fail(BLSTM_ERR_ARG, "update: null params / theta / grad");
+    if (p->rule < BLSTM_OPT_SGD || p->rule > BLSTM_OPT_ADAM) return fail(BLSTM_ERR_ARG, "unknown rule %d", p->rule);
+    if (p->rule == BLSTM_OPT_ADAM && p->step < 1) return fail(BLSTM_ERR_ARG, "ADAM needs step >= 1");
+    const size_t ns = blstm_opt_state_floats(p->rule, n);
+    if (ns && !state) return fail(BLSTM_ERR_ARG, "rule %d needs %zu floats of state", p->rule, ns);
+    if (!al16(theta) || !al16(grad) || (ns && !al16(state)))
+        return fail(BLSTM_ERR_ALIGN, "theta / grad / state must be 16-byte aligned");
+    return 0;
+}
+
+extern "C" int blstm_opt_update(const blstm_opt_params *p, const blstm_stack_desc *layout, float *theta, float *grad,
+                                float *state, size_t n, int zero_grad, void *workspace, size_t workspace_bytes,
+                                void *stream) {
+    if (int rc = opt_check(p, theta, grad, state, n)) return rc;
+    if (p->max_norm > 0.0) {
+        if (!workspace || !al16(workspace)) return fail(BLSTM_ERR_ALIGN, "norm constraint needs an aligned workspace");
+        if (workspace_bytes < blstm_opt_workspace_bytes(n))
+            return fail(BLSTM_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, blstm_opt_workspace_bytes(n));
+    }
+    if (layout) {
+        if (layout->L > 31) return fail(BLSTM_ERR_UNSUPPORTED, "layout with L=%d > 31", layout->L);
+        const size_t np = blstm_param_count(layout);
+        if (np == 0 || np != n) return fail(BLSTM_ERR_ARG, "n=%zu != blstm_param_count(layout)=%zu", n, np);
+    }
+    return opt_range(p, layout, theta, grad, state, n, 0, n, zero_grad, (double *)workspace, (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------------------

@@ -148,7 +148,7 @@ class StackTrainer:
 
     def __init__(self, cfg, params, batch, device, lr: float = 1e-5, comm=None, world: int = 1,
                  sched: Optional[DPSchedule] = None, opt: Optional[dict] = None, dropout: float = 0.0,
-                 dropout_seed: int = 0):
+                 dropout_seed: int = 0, fused: bool = True):
         """opt: None = plain SGD (sgd_update); else the update rule of blstm_opt_update, e.g.
         {"rule": "adam", "lr": 1e-3, "l2": 1e-4, "max_norm": 10.0} (§4.3)."""
         import torch
@@ -172,12 +172,15 @@ class StackTrainer:
         self.set_batch(batch)
         self.steps_done = 0
         self.opt = dict(opt) if opt is not None else None
+        # fused: blstm_stack_train_step updates each gradient bucket on the side stream as soon as it
+        # is final (plain SGD = rule "sgd", the same arithmetic as sgd_update); else fwd_bwd + update
+        self.fused = fused
+        self.opt_state, self.opt_steps = None, 0
         if self.opt is not None:
             ns = blstm.blstm_opt_state_floats(self.opt["rule"], self.theta.numel())
             self.opt_state = torch.zeros(max(ns, 4), dtype=torch.float32, device=device) if ns else None
             self.opt_ws = torch.empty(blstm.blstm_opt_workspace_bytes(self.theta.numel()), dtype=torch.uint8,
                                       device=device)
-            self.opt_steps = 0
 
     def set_batch(self, batch):
         t = self.torch
@@ -204,6 +207,11 @@ class StackTrainer:
         self.blstm.blstm_opt_update(P, self.desc, theta, grad, self.opt_state, True, self.opt_ws)
 
     def step(self):
+        if self.fused:
+            self._fused_step()
+            self.steps_done += 1
+            return
+
         class _NoSum(Collective):  # the sum already happened inside blstm_stack_fwd_bwd
             def __init__(s, inner): s.inner = inner
             def sum_(s, t): pass
@@ -212,6 +220,20 @@ class StackTrainer:
                     s.inner.mean_(t)
         dp_step(self.theta, self.grad, self._grad, self._update, _NoSum(self.coll), self.sched, self.steps_done)
         self.steps_done += 1
+
+    def _fused_step(self):
+        """dp_step's schedule with the update inside the library step (blstm_stack_train_step)."""
+        if self.dropout > 0:
+            self.desc.dropout_seed = (self.dropout_seed + self.steps_done) & 0xFFFFFFFF
+        self.opt_steps += 1
+        P = (self.blstm.opt_params("sgd", self.lr) if self.opt is None
+             else self.blstm.opt_params(step=self.opt_steps, **self.opt))
+        comm = self.comm if (self.comm is not None and self.sched.grads_summed()) else None
+        self.blstm.blstm_stack_train_step(self.desc, self.theta, self.grad, self.x, self.mask, self.labels,
+                                          self.dy_top, self.loss, self.ferr, comm, P, self.opt_state, self.ws,
+                                          s_side=self.side)
+        if self.sched.average_after(self.steps_done) and self.coll is not None:
+            self.coll.mean_(self.theta)
 
 
 def dp_comm_from_torch(rank: int, world: int):

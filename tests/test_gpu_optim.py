@@ -153,3 +153,25 @@ def test_trainer_adam_with_l2_and_clip_runs():
             assert float((tr.theta - th0).abs().max()) <= 1e-3 * (1 + 1e-5) + ulp
     assert all(np.isfinite(losses))
     assert losses[-1] < losses[0]  # the same batch: the loss goes down
+
+
+@pytest.mark.parametrize("opt", [None, {"rule": "adam", "lr": 1e-3, "l2": 1e-4},
+                                 {"rule": "momentum", "lr": 1e-5, "max_norm": 5.0}])
+def test_fused_train_step_equals_separate_update(opt):
+    """blstm_stack_train_step (update per gradient bucket on the side stream; with the norm
+    constraint one update at the end) gives bit for bit the step of blstm_stack_fwd_bwd followed
+    by blstm_opt_update / sgd_update."""
+    from paper_1608_00895_b200 import synth
+    from paper_1608_00895_b200.train import StackTrainer
+    cfg, params, batch = synth.make_workload(synth.CONFIGS["C3"], B=16)
+    dev = torch.device("cuda:0")
+    a = StackTrainer(cfg, params, batch, dev, lr=1e-5, opt=opt, fused=True, dropout=0.1, dropout_seed=3)
+    b = StackTrainer(cfg, params, batch, dev, lr=1e-5, opt=opt, fused=False, dropout=0.1, dropout_seed=3)
+    for _ in range(3):
+        a.step()
+        b.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.theta, b.theta)
+    assert torch.count_nonzero(a.grad).item() == 0
+    if opt is not None and a.opt_state is not None:
+        assert torch.equal(a.opt_state, b.opt_state)
