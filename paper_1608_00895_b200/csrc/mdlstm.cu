@@ -295,6 +295,120 @@ __global__ void __launch_bounds__(256) md_bwd_diag_kernel(MdK a, int d) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent forward wavefront (one launch per pass): block (direction k, unit tile jt, lane g) keeps its
+// tile of the recurrent weights in shared memory for the whole pass and processes row groups
+// g, g + NG, ... of every anti-diagonal; a grid barrier (monotonic counter, release / acquire)
+// separates the diagonals.  State written by other blocks is read with L1-bypassing loads.  Launched
+// cooperatively (all blocks co-resident, else the launch fails and the per-diagonal kernels run).
+// ---------------------------------------------------------------------------------------------
+DEVI void grid_barrier(uint32_t *count, uint32_t target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        red_release_gpu_add(count, 1u);
+        while (ld_acquire_gpu(count) < target) __nanosleep(64);
+    }
+    __syncthreads();
+}
+DEVI int md_nrows(const MdK &a, int d) {
+    const int u0 = d - a.V + 1 > 0 ? d - a.V + 1 : 0;
+    const int u1 = d < a.U - 1 ? d : a.U - 1;
+    return (u1 - u0 + 1) * a.B;
+}
+
+__global__ void __launch_bounds__(256) md_fwd_persist_kernel(MdK a, uint32_t *bar, int NG) {
+    extern __shared__ float dsm[];
+    __shared__ long rowpred[2][MT_ROWS];
+    const int H = a.H, G = 5 * H, Hp = a.Hp, njt = (H + MT_J - 1) / MT_J, HS = H + 1;
+    const long VB = (long)a.V * a.B;
+    const long prow = (long)(a.U + 1) * (a.V + 1) * a.B;
+    float *Rs = dsm;                   // [2][H][5][32]: Ru, Rv columns of the unit tile
+    float *Hs = Rs + 2 * H * 5 * MT_J; // [2][MT_ROWS][H+1]: predecessor h of the block's rows
+    int bid = blockIdx.x;
+    const int g = bid % NG; bid /= NG;
+    const int jt = bid % njt, k = bid / njt;
+    const int jj = threadIdx.x & 31, rl = threadIdx.x >> 5, j = jt * MT_J + jj;
+    const bool jok = j < H;
+    const float *Ru = a.theta + k * a.P1 + (long)a.D * G, *Rv = Ru + (long)H * G;
+    for (int e = threadIdx.x; e < 2 * H * 5 * MT_J; e += blockDim.x) {
+        const int jx = e % MT_J, q = (e / MT_J) % 5, m = (e / (5 * MT_J)) % H, w = e / (H * 5 * MT_J);
+        const int jg = jt * MT_J + jx;
+        Rs[e] = jg < H ? (w ? Rv : Ru)[(long)m * G + q * H + jg] : 0.f;
+    }
+    const int ND = a.U + a.V - 1;
+    for (int d = 0; d < ND; ++d) {
+        const int nrg = (md_nrows(a, d) + MT_ROWS - 1) / MT_ROWS;
+        for (int rg = g; rg < nrg; rg += NG) {
+            MdRow rw[MT_RPT];
+            float acc[MT_RPT][5];
+#pragma unroll
+            for (int t = 0; t < MT_RPT; ++t) {
+                rw[t] = md_row(a, d, k, rg * MT_ROWS + rl + MT_RL * t);
+                const float *zc = a.z + rw[t].cp * 20 * Hp + (long)k * 5 * Hp;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) acc[t][q] = (rw[t].on && jok) ? zc[q * Hp + j] : 0.f;
+                if (jj == 0) {
+                    rowpred[0][rl + MT_RL * t] = (rw[t].on && rw[t].up > 0) ? (rw[t].ck - VB) * H : -1;
+                    rowpred[1][rl + MT_RL * t] = (rw[t].on && rw[t].vp > 0) ? (rw[t].ck - a.B) * H : -1;
+                }
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < 2 * MT_ROWS * H; e += blockDim.x) {
+                const int m = e % H, rr = (e / H) % MT_ROWS, w = e / (MT_ROWS * H);
+                const long src = rowpred[w][rr];
+                Hs[(w * MT_ROWS + rr) * HS + m] = src >= 0 ? __ldcg(a.hf + src + m) : 0.f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int t = 0; t < MT_RPT; ++t) {
+                if (!rw[t].on) continue;  // warp-uniform
+                const float *hu = Hs + (rl + MT_RL * t) * HS, *hv = Hs + (MT_ROWS + rl + MT_RL * t) * HS;
+                for (int m = 0; m < H; ++m) {
+                    const float u = hu[m], v = hv[m];
+                    const float *r0 = Rs + (m * 5) * MT_J + jj, *r1 = Rs + ((H + m) * 5) * MT_J + jj;
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) acc[t][q] = fmaf(v, r1[q * MT_J], fmaf(u, r0[q * MT_J], acc[t][q]));
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < MT_RPT; ++t) {
+                const MdRow &w = rw[t];
+                if (!w.live || !jok) continue;
+                const long ck = w.ck;
+                const int b = (int)(w.cp % a.B);
+                const float cu = w.up > 0 ? __ldcg(a.c + (ck - VB) * H + j) : 0.f;
+                const float cv = w.vp > 0 ? __ldcg(a.c + (ck - a.B) * H + j) : 0.f;
+                float *ac = a.act + ck * G;
+                float h = 0.f, cn;
+                if (!w.on) {
+                    cn = w.up > 0 ? cu : cv;
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) ac[q * H + j] = 0.f;
+                } else if (!a.stable) {
+                    const float gi = msg(acc[t][0]), fu = msg(acc[t][1]), fv = msg(acc[t][2]), gg = mth(acc[t][3]),
+                                go = msg(acc[t][4]);
+                    cn = fu * cu + fv * cv + gi * gg;
+                    h = go * mth(cn);
+                    ac[j] = gi; ac[H + j] = fu; ac[2 * H + j] = fv; ac[3 * H + j] = gg; ac[4 * H + j] = go;
+                } else {
+                    const float gi = msg(acc[t][0]), f = msg(acc[t][1]), gg = mth(acc[t][2]), go = msg(acc[t][3]),
+                                lam = msg(acc[t][4]);
+                    cn = f * (lam * cu + (1.f - lam) * cv) + gi * gg;
+                    h = go * mth(cn);
+                    ac[j] = gi; ac[H + j] = f; ac[2 * H + j] = gg; ac[3 * H + j] = go; ac[4 * H + j] = lam;
+                }
+                a.c[ck * H + j] = cn;
+                a.hf[ck * H + j] = h;
+                a.h16[((long)k * prow + slot(a, w.up, w.vp, b)) * Hp + j] = __float2half_rn(h);
+                a.y[w.cp * 4 * H + (long)k * H + j] = h;
+            }
+            __syncthreads();  // rowpred / Hs reused by the next row group
+        }
+        if (d + 1 < ND) grid_barrier(bar, (uint32_t)(d + 1) * gridDim.x);
+    }
+}
+
 // W16 [20Hp][Dp]: row k*5Hp + q*Hp + j <- W_k[f][q*H + j] as hi + lo fp16 parts (w16lo may be
 // null); bq [20Hp] <- b_k
 __global__ void md_pack_kernel(const float *theta, long P1, int D, int H, int Hp, int Dp, __half *w16, __half *w16lo,
@@ -395,6 +509,7 @@ MdWS md_ws(const MdGeo &g) {
     w.gsk = take((size_t)(8L << 20) * 4);
     w.da16 = take((size_t)4 * g.prow * 5 * g.Hp * 2);
     w.dxs = take(cells * g.Dp * 4);
+    w.bar = take(256);
     w.total = o;
     size_t r = 0;
     auto rtake = [&](size_t b) { size_t q = r; r += al(b); return q; };
@@ -418,6 +533,45 @@ static MdK md_args(const MdGeo &g, const float *theta, const uint8_t *mask, uint
     a.daf = (float *)(ws + w.daf); a.dcu = (float *)(ws + w.dcu); a.dcv = (float *)(ws + w.dcv);
     a.da16 = (__half *)(ws + w.da16); a.dap = (__half *)(ws + w.dap);
     return a;
+}
+
+// Persistent forward wavefront launch: 0 = done, 1 = not possible here (per-diagonal path instead),
+// < 0 error.  BLSTM_MD_PERSIST=0 forces the per-diagonal path.  (A persistent backward -- the R^T
+// tile plus the successors' dA staged per row group -- measured slower than the per-diagonal
+// kernels: 17.2 vs 11.1 ms at H = 64, one block per SM.)
+static int md_persist(bool fwd, MdK &a, const MdGeo &g, uint32_t *bar, cudaStream_t st) {
+    if (!fwd) return 1;
+    const bool env_off = getenv("BLSTM_MD_PERSIST") && atoi(getenv("BLSTM_MD_PERSIST")) == 0;
+    if (env_off) return 1;
+    const int H = g.H, G = 5 * H;
+    const size_t smem = fwd ? (size_t)(2 * H * 5 * MT_J + 2 * MT_ROWS * (H + 1)) * 4
+                            : (size_t)(2 * G * MT_J + 2 * MT_ROWS * (G + 1)) * 4;
+    if (smem > 200 * 1024) return 1;
+    const void *fn = (const void *)md_fwd_persist_kernel;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        return 1;
+    }
+    const int njt = (H + MT_J - 1) / MT_J;
+    const int maxrows = (g.U < g.V ? g.U : g.V) * g.B;
+    const int maxrg = (maxrows + MT_ROWS - 1) / MT_ROWS;
+    int NG = num_sms() * per_sm / (4 * njt);
+    if (NG > maxrg) NG = maxrg;
+    if (NG < 1) return 1;
+    if (cudaMemsetAsync(bar, 0, sizeof(uint32_t), st) != cudaSuccess) return -5;
+    void *args[] = {(void *)&a, (void *)&bar, (void *)&NG};
+    ProfScope ps(fwd ? PROF_REC_FWD : PROF_REC_BWD, st);
+    if (cudaLaunchCooperativeKernel(fn, dim3(4 * njt * NG), dim3(256), args, smem, st) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
+    note_launch();
+    return 0;
 }
 
 int md_forward(const MdGeo &g, const float *theta, const float *x, const uint8_t *mask, float *y, uint8_t *ws,
@@ -444,6 +598,10 @@ int md_forward(const MdGeo &g, const float *theta, const float *x, const uint8_t
     gz2.beta = 1; gz2.bias = nullptr;
     if (gemm_f16({x16, g.Dp, 0}, {w16lo, g.Dp, 0}, gz2, 0, st)) return -5;
     if (gemm_f16({x16lo, g.Dp, 0}, {w16, g.Dp, 0}, gz2, 0, st)) return -5;
+    {
+        const int rc = md_persist(true, a, g, (uint32_t *)(ws + w.bar), st);
+        if (rc <= 0) return rc;
+    }
     // the U+V-1 wavefront launches, captured once into a CUDA graph (graph.h) and replayed
     const std::vector<uint64_t> key{3, (uint64_t)g.U, (uint64_t)g.V, (uint64_t)g.B, (uint64_t)g.D, (uint64_t)g.H,
                                     (uint64_t)g.stable, u64(theta), u64(mask), u64(y), u64(ws), u64(res)};
@@ -473,9 +631,11 @@ int md_backward(const MdGeo &g, const float *theta, const float *x, const uint8_
     if (cast_x_f16(x, g.D, g.D, x16, g.Dp, g.cells, st)) return -5;
     if (cudaMemsetAsync(ws + w.da16, 0, (size_t)4 * g.prow * 5 * g.Hp * 2, st) != cudaSuccess) return -5;
     if (cudaMemsetAsync(ws + w.dap, 0, (size_t)g.cells * 20 * g.Hp * 2, st) != cudaSuccess) return -5;
+    const int prc = md_persist(false, a, g, (uint32_t *)(ws + w.bar), st);
+    if (prc < 0) return prc;
     const std::vector<uint64_t> key{4, (uint64_t)g.U, (uint64_t)g.V, (uint64_t)g.B, (uint64_t)g.D, (uint64_t)g.H,
                                     (uint64_t)g.stable, u64(theta), u64(mask), u64(dy), u64(ws), u64(res)};
-    if (graph_run(key, PROF_REC_BWD, st, {(const void *)md_bwd_diag_kernel}, [&](cudaStream_t s0) -> int {
+    if (prc == 1 && graph_run(key, PROF_REC_BWD, st, {(const void *)md_bwd_diag_kernel}, [&](cudaStream_t s0) -> int {
             for (int d = g.U + g.V - 2; d >= 0; --d) {
                 md_bwd_diag_kernel<<<md_blocks(g.U, g.V, g.B, g.H, d), 256, 0, s0>>>(a, d);
                 note_launch();

@@ -16,7 +16,7 @@ struct MdGeo {
 };
 
 struct MdWS {  // carved from the caller's workspace / reserve
-    size_t x16, x16lo, w16, w16lo, z, hf, cs, dap, rt, dcu, dcv, daf, gW, gR, gb, gsk, dxs, total;  // workspace
+    size_t x16, x16lo, w16, w16lo, z, hf, cs, dap, rt, dcu, dcv, daf, gW, gR, gb, gsk, dxs, bar, total;  // workspace
     size_t da16;                                                                   // (workspace)
     size_t act, c, h16, rtotal;                                                    // reserve
 };
