@@ -68,15 +68,16 @@ struct LayerGeo {
     int T, B, D, H, Hq, Dp;
     long TB;
     RecPlan pl;
+    bool step = false;  // beyond the persistent kernels' capacity: step-launched recurrence (§5.7)
 };
 // split-K scratch of the weight-gradient GEMMs (GemmParams::splitk_ws): 32 MB
 constexpr long GSK_ELEMS = 8L << 20;
 
 struct FwdWS {
-    size_t x16, w16, rt16, bq, Z, maskN, cnt, total;
+    size_t x16, w16, rt16, bq, Z, maskN, cnt, stepF, total;
 };
 struct BwdWS {
-    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cpk, dypk, gsk, cnt, total;
+    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cpk, dypk, gsk, cnt, stepB, cs2, total;
 };
 struct Reserve {
     size_t gates, hist, total;
@@ -94,9 +95,10 @@ static int layer_geo(const lstm_desc *d, LayerGeo &g) {
     g.pl = rec_plan(d->T, d->B, d->H, 1, num_sms());
     g.Hq = g.pl.Hq;
     g.Dp = rup(d->D, 64);
-    if (!rec_supported(g.pl, d->H))
-        return fail(BLSTM_ERR_UNSUPPORTED, "H=%d B=%d exceeds the recurrence kernels' on-chip capacity (Hq=%d N=%d)",
-                    d->H, d->B, g.pl.Hq, g.pl.N);
+    const bool force_step = getenv("BLSTM_FORCE_STEP") && atoi(getenv("BLSTM_FORCE_STEP")) != 0;
+    g.step = force_step || !rec_supported(g.pl, d->H);
+    if (g.step && (long)g.B * 4 * g.Hq * 2 > GSK_ELEMS)
+        return fail(BLSTM_ERR_UNSUPPORTED, "H=%d B=%d: no recurrence path for this size", d->H, d->B);
     return 0;
 }
 static FwdWS fwd_ws(const LayerGeo &g) {
@@ -106,9 +108,10 @@ static FwdWS fwd_ws(const LayerGeo &g) {
     w.w16 = c.take((size_t)g.Dp * 4 * g.Hq * 2);
     w.rt16 = c.take((size_t)4 * g.Hq * g.Hq * 2);
     w.bq = c.take((size_t)4 * g.Hq * 4);
-    w.Z = c.take(rec_native_elems(g.pl, g.T) * 4);
+    w.Z = c.take(g.step ? (size_t)g.TB * 4 * g.Hq * 4 : rec_native_elems(g.pl, g.T) * 4);
     w.maskN = c.take(rec_mask_bytes(g.pl, g.T));
     w.cnt = c.take(256);
+    w.stepF = c.take(g.step ? rec_step_fwd_scratch_bytes(g.B, g.Hq) : 0);
     w.total = c.off;
     return w;
 }
@@ -131,13 +134,15 @@ static BwdWS bwd_ws(const LayerGeo &g) {
     w.dypk = c.take((size_t)g.TB * g.Hq * 4);
     w.gsk = c.take((size_t)GSK_ELEMS * 4);
     w.cnt = c.take(256);
+    w.stepB = c.take(g.step ? rec_step_bwd_scratch_bytes(g.B, g.Hq) : 0);
+    w.cs2 = c.take(g.step ? colsum_scratch_bytes(g.TB, 4 * g.Hq) : 0);
     w.total = c.off;
     return w;
 }
 static Reserve reserve_of(const LayerGeo &g) {
     Carve c;
     Reserve r;
-    r.gates = c.take(rec_native_elems(g.pl, g.T) * 2);
+    r.gates = c.take(g.step ? (size_t)g.TB * 4 * g.Hq * 2 : rec_native_elems(g.pl, g.T) * 2);
     r.hist = c.take((size_t)(g.T + 1) * g.B * g.Hq * 2);
     r.total = c.off;
     return r;
@@ -192,10 +197,23 @@ extern "C" int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     TRY(pack_rt(R, nullptr, g.H, g.Hq, 1, rt16, st), "pack_rt");
     TRY(pack_bias(b, nullptr, g.H, g.Hq, 1, bq, st), "pack_bias");
     GemmParams gp{(int)g.TB, 4 * g.Hq, g.Dp, Z, 4L * g.Hq, 1.f, 0, bq, 0, 0};
-    set_native(gp, g.pl, g.B);  // Z in the recurrence kernels' CTA-native layout
+    if (!g.step) set_native(gp, g.pl, g.B);  // Z in the recurrence kernels' CTA-native layout
     TRY(gemm_f16({x16, g.Dp, 0}, {w16, 4L * g.Hq, 1}, gp, 0, st), "gemm Z");
     __half *hist = (__half *)(res + rv.hist);
     TRY(init_hist(hist, h0, g.T, g.B, g.H, g.Hq, 1, d->direction, st), "init_hist");
+    if (g.step) {  // one launch group per time step (rec_step.h)
+        RecStepFwd q{};
+        q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = g.Hq; q.ndir = 1; q.dir0 = d->direction;
+        q.Z = Z; q.mask = mask; q.RT16 = rt16;
+        q.P = (float *)(ws + w.stepF);
+        q.C = c; q.ldc = g.H; q.c_doff = 0;
+        q.y = y; q.ldy = d->ldy; q.y_doff = 0;
+        q.gates = (__half *)(res + rv.gates);
+        q.hist = hist;
+        q.h0 = h0; q.c0 = c0; q.hT = hT; q.cT = cT;
+        TRY(rec_step_fwd(q, st), "rec_step_fwd");
+        return 0;
+    }
     uint8_t *maskN = ws + w.maskN;
     TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
     RecParams p = base_params(g, 1, d->direction, mask);
@@ -241,6 +259,22 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     TRY(cast_x_f16(x, d->ldx, g.D, x16, g.Dp, g.TB, st), "cast_x");
     TRY(pack_w(W, nullptr, g.D, g.H, g.Hq, 1, g.Dp, 0, w16, st), "pack_w");
     TRY(pack_rt(R, nullptr, g.H, g.Hq, 1, rt16, st), "pack_rt");
+    if (g.step) {  // one launch group per time step (rec_step.h); db = column sums of dA
+        RecStepBwd q{};
+        q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = g.Hq; q.ndir = 1; q.dir0 = d->direction;
+        q.mask = mask; q.RT16 = rt16;
+        q.C = c; q.ldc = g.H; q.c_doff = 0;
+        q.gates = (const __half *)(res + rv.gates);
+        q.dy = dy; q.lddy = d->ldy; q.dy_doff = 0;
+        q.dA = dA;
+        float *sb = (float *)(ws + w.stepB);
+        q.dhR = sb; q.dhc = sb + 16L * g.B * g.Hq; q.dcc = sb + 18L * g.B * g.Hq;  // (rec_step: 2 x SB partials)
+        q.c0 = c0; q.dhT = dhT; q.dcT = dcT; q.dh0 = dh0; q.dc0 = dc0;
+        TRY(rec_step_bwd(q, st), "rec_step_bwd");
+        if (cudaMemsetAsync(dbp, 0, (size_t)4 * g.Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
+        TRY(colsum_f16_add(dA, g.TB, 4 * g.Hq, 4L * g.Hq, 1.f / (float)(1 << DA_SHIFT), dbp, (float *)(ws + w.cs2), st),
+            "db colsum");
+    } else {
     uint8_t *maskN = ws + w.maskN;
     TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
     RecParams p = base_params(g, 1, d->direction, mask);
@@ -266,6 +300,7 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     p.dh0 = dh0; p.dc0 = dc0;
     p.counters = (uint32_t *)(ws + w.cnt);
     TRY(lstm_rec_bwd(p, rt16, st), "lstm_rec_bwd");
+    }
     const float a = 1.f / (float)(1 << DA_SHIFT);
     if (want_dx) {
         GemmParams gp{(int)g.TB, g.Dp, 4 * g.Hq, dX, g.Dp, a, 0, nullptr, 0, 0};
@@ -285,7 +320,7 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     }
     TRY(scatter_w(dW, g.D, g.H, g.Hq, dWT, g.Dp, 0, 0, st), "scatter dW");
     TRY(scatter_r(dR, g.H, g.Hq, dRT, st), "scatter dR");
-    TRY(scatter_b(db, g.H, g.Hq, dbp, g.pl.G, 0, st), "scatter db");
+    TRY(scatter_b(db, g.H, g.Hq, dbp, g.step ? 1 : g.pl.G, 0, st), "scatter db");
     return 0;
 }
 
@@ -475,7 +510,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
             __half *hist = (__half *)(ws + w.hist[l]);
             TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
             RecStepFwd q{};
-            q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = Hq;
+            q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = Hq; q.ndir = 2; q.dir0 = 1;
             q.Z = Z; q.mask = mask; q.RT16 = (const __half *)(ws + w.rt16[l]);
             q.P = (float *)(ws + w.stepF);
             if (Cout) { q.C = Cout + (size_t)l * 2 * g.TB * g.H; q.ldc = g.H; q.c_doff = g.TB * g.H; }
@@ -709,7 +744,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         p.started = overlap ? bstarted + l : nullptr;
         if (g.step) {  // one launch group per time step (rec_step.h); db = column sums of dA
             RecStepBwd q{};
-            q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = Hq;
+            q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = Hq; q.ndir = 2; q.dir0 = 1;
             q.mask = mask; q.RT16 = (const __half *)(ws + w.rt16[l]);
             q.C = p.C; q.ldc = p.ldc; q.c_doff = p.c_doff;
             q.gates = p.gates;

@@ -30,26 +30,29 @@ DEVI float th(float z) { return 2.f * sg(2.f * z) - 1.f; }
 
 // thread per (d, b, u), u < Hq
 __global__ void step_fwd_gate_kernel(RecStepFwd p, int s) {
-    const int Hq = p.Hq, B = p.B, T = p.T;
-    const long n = 2L * B * Hq;
+    const int Hq = p.Hq, B = p.B, T = p.T, G4 = p.ndir * 4 * Hq;
+    const long n = (long)p.ndir * B * Hq;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
         const int u = (int)(e % Hq);
         const long db = e / Hq;
         const int b = (int)(db % B), d = (int)(db / B);
-        const int dir = d == 0 ? 1 : -1;
-        const int t = d == 0 ? s : T - 1 - s;
+        const int dir = d == 0 ? p.dir0 : -1;
+        const int t = dir > 0 ? s : T - 1 - s;
         const long r = (long)t * B + b;
         const bool valid = p.mask[r] != 0 && u < p.H;
         const int slot_prev = t + (dir < 0), slot_next = slot_prev + dir;
-        const __half *hp = p.hist + (((long)d * (T + 1) + slot_prev) * B + b) * Hq + u;
         __half *hn = p.hist + (((long)d * (T + 1) + slot_next) * B + b) * Hq + u;
-        const float c_prev = s == 0 ? 0.f : p.C[d * p.c_doff + (r - (long)dir * B) * p.ldc + u];
-        float c = c_prev, h = __half2float(*hp);
+        const float c_prev = s == 0 ? ((p.c0 && u < p.H) ? p.c0[((long)d * B + b) * p.H + u] : 0.f)
+                                    : p.C[d * p.c_doff + (r - (long)dir * B) * p.ldc + u];
+        // the fp32 state carried across masked frames (the history holds it in fp16 only)
+        float *hc = p.P + (size_t)2 * SF * B * 4 * Hq + db * Hq + u;
+        const float h_prev = s == 0 ? ((p.h0 && u < p.H) ? p.h0[((long)d * B + b) * p.H + u] : 0.f) : *hc;
+        float c = c_prev, h = h_prev;
         float4 act = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid) {
-            const float4 z = reinterpret_cast<const float4 *>(p.Z + r * 8 * Hq + (long)d * 4 * Hq)[u];
+            const float4 z = reinterpret_cast<const float4 *>(p.Z + r * G4 + (long)d * 4 * Hq)[u];
             float4 a = z;
-            if (s > 0) {
+            {  // h_{t-1} R^T (at s = 0 from the h0 slot of the history, 0 when there is no h0)
 #pragma unroll
                 for (int k = 0; k < SF; ++k) {
                     const float4 q = reinterpret_cast<const float4 *>(p.P + (((long)d * SF + k) * B + b) * 4 * Hq)[u];
@@ -61,29 +64,38 @@ __global__ void step_fwd_gate_kernel(RecStepFwd p, int s) {
             h = act.w * th(c);
         }
         if (u < p.H) p.C[d * p.c_doff + r * p.ldc + u] = c;
-        *hn = valid ? __float2half_rn(h) : *hp;
+        *hc = h;
+        *hn = __float2half_rn(h);
+        if (s == T - 1 && u < p.H) {  // state after the whole scan
+            if (p.hT) p.hT[((long)d * B + b) * p.H + u] = h;
+            if (p.cT) p.cT[((long)d * B + b) * p.H + u] = c;
+        }
         if (p.y && u < p.H) p.y[r * p.ldy + d * p.y_doff + u] = valid ? h : 0.f;
         if (p.y16) p.y16[r * 2 * Hq + (long)d * Hq + u] = __float2half_rn(valid ? h : 0.f);
-        __half2 *gp = reinterpret_cast<__half2 *>(p.gates + r * 8 * Hq + (long)d * 4 * Hq + 4 * u);
+        __half2 *gp = reinterpret_cast<__half2 *>(p.gates + r * G4 + (long)d * 4 * Hq + 4 * u);
         gp[0] = __floats2half2_rn(act.x, act.y);
         gp[1] = __floats2half2_rn(act.z, act.w);
     }
 }
 
 __global__ void step_bwd_gate_kernel(RecStepBwd p, int s) {
-    const int Hq = p.Hq, B = p.B, T = p.T;
+    const int Hq = p.Hq, B = p.B, T = p.T, G4 = p.ndir * 4 * Hq;
     const float scale = (float)(1 << DA_SHIFT);
-    const long n = 2L * B * Hq;
+    const long n = (long)p.ndir * B * Hq;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
         const int u = (int)(e % Hq);
         const long db = e / Hq;
         const int b = (int)(db % B), d = (int)(db / B);
-        const int dir = d == 0 ? 1 : -1;
-        const int t = d == 0 ? T - 1 - s : s;       // this step's frame (reverse of the forward scan)
+        const int dir = d == 0 ? p.dir0 : -1;
+        const int t = dir > 0 ? T - 1 - s : s;       // this step's frame (reverse of the forward scan)
         const long r = (long)t * B + b;
-        const long sidx = db * Hq + u;               // [2][B][Hq] state index
+        const long sidx = db * Hq + u;               // [ndir][B][Hq] state index
         const bool valid = p.mask[r] != 0 && u < p.H;
         float dh_in = 0.f, dc = 0.f;
+        if (s == 0 && u < p.H) {  // gradients at the end of the scan
+            if (p.dhT) dh_in = p.dhT[((long)d * B + b) * p.H + u];
+            if (p.dcT) dc = p.dcT[((long)d * B + b) * p.H + u];
+        }
         if (s > 0) {
             const long rp = r + (long)dir * B;       // the frame processed at step s-1
             if (p.mask[rp]) {
@@ -95,20 +107,21 @@ __global__ void step_bwd_gate_kernel(RecStepBwd p, int s) {
             }
             dc = p.dcc[sidx];
         }
-        __half2 *dap = reinterpret_cast<__half2 *>(p.dA + r * 8 * Hq + (long)d * 4 * Hq + 4 * u);
+        __half2 *dap = reinterpret_cast<__half2 *>(p.dA + r * G4 + (long)d * 4 * Hq + 4 * u);
         if (!valid) {
             dap[0] = __floats2half2_rn(0.f, 0.f);
             dap[1] = __floats2half2_rn(0.f, 0.f);
             p.dhc[sidx] = dh_in;                     // pass through; dc unchanged
-            if (s == 0) p.dcc[sidx] = 0.f;
+            if (s == 0) p.dcc[sidx] = dc;
             continue;
         }
-        const __half2 *gp = reinterpret_cast<const __half2 *>(p.gates + r * 8 * Hq + (long)d * 4 * Hq + 4 * u);
+        const __half2 *gp = reinterpret_cast<const __half2 *>(p.gates + r * G4 + (long)d * 4 * Hq + 4 * u);
         const float2 g01 = __half22float2(gp[0]), g23 = __half22float2(gp[1]);
         const float gi = g01.x, gf = g01.y, gg = g23.x, go = g23.y;
         const float c = p.C[d * p.c_doff + r * p.ldc + u];
         const int tp = t - dir;                      // the frame before t in the forward scan
-        const float c_prev = (tp >= 0 && tp < T) ? p.C[d * p.c_doff + ((long)tp * B + b) * p.ldc + u] : 0.f;
+        const float c_prev = (tp >= 0 && tp < T) ? p.C[d * p.c_doff + ((long)tp * B + b) * p.ldc + u]
+                                                 : (p.c0 ? p.c0[((long)d * B + b) * p.H + u] : 0.f);
         const float dH = dh_in + p.dy[r * p.lddy + d * p.dy_doff + u];
         const float tc = th(c);
         const float dct = dc + dH * go * (1.f - tc * tc);
@@ -122,6 +135,33 @@ __global__ void step_bwd_gate_kernel(RecStepBwd p, int s) {
     }
 }
 
+// dh0 / dc0 after the last BPTT step: dh = dA R of the last processed frame (its partials) where
+// that frame was valid, else the carried dh; dc = the carried dc
+__global__ void step_bwd_final_kernel(RecStepBwd p) {
+    const int Hq = p.Hq, B = p.B, T = p.T;
+    const long n = (long)p.ndir * B * p.H;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int u = (int)(e % p.H);
+        const long db = e / p.H;
+        const int b = (int)(db % B), d = (int)(db / B);
+        const int dir = d == 0 ? p.dir0 : -1;
+        const int t = dir > 0 ? 0 : T - 1;  // the frame processed last
+        const long sidx = db * Hq + u;
+        if (p.dh0) {
+            float v = 0.f;
+            if (p.mask[(long)t * B + b]) {
+                const long pb = (long)d * SB * B * Hq + (long)b * Hq + u;
+#pragma unroll
+                for (int k = 0; k < SB; ++k) v += p.dhR[pb + (long)k * B * Hq];
+            } else {
+                v = p.dhc[sidx];
+            }
+            p.dh0[e] = v;
+        }
+        if (p.dc0) p.dc0[e] = p.dcc[sidx];
+    }
+}
+
 int grid_of(long n) {
     long g = (n + 255) / 256;
     return (int)(g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g));
@@ -129,7 +169,7 @@ int grid_of(long n) {
 
 }  // namespace
 
-size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * SF * B * 4 * Hq * 4; }
+size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * SF * B * 4 * Hq * 4 + (size_t)2 * B * Hq * 4; }
 size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)(2 * SB + 4) * B * Hq * 4; }
 
 // The T-step loop of a layer is captured once into a CUDA graph (graph.h) and replayed: a loop of
@@ -138,16 +178,17 @@ size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)(2 * SB + 4) *
 
 int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
     const int Hq = p.Hq, B = p.B, T = p.T;
-    const std::vector<uint64_t> key{1, (uint64_t)T, (uint64_t)B, (uint64_t)p.H, (uint64_t)Hq, u64(p.Z), u64(p.mask),
+    const std::vector<uint64_t> key{1, (uint64_t)T, (uint64_t)B, (uint64_t)p.H, (uint64_t)Hq, (uint64_t)p.ndir,
+                                    (uint64_t)(p.dir0 + 2), u64(p.h0), u64(p.c0), u64(p.hT), u64(p.cT), u64(p.Z), u64(p.mask),
                                     u64(p.RT16), u64(p.P), u64(p.C), (uint64_t)p.ldc, (uint64_t)p.c_doff, u64(p.y),
                                     (uint64_t)p.ldy, (uint64_t)p.y_doff, u64(p.y16), u64(p.gates), u64(p.hist)};
     return graph_run(key, PROF_REC_FWD, st, {(const void *)step_fwd_gate_kernel}, [&](cudaStream_t s0) -> int {
         for (int s = 0; s < T; ++s) {
-            if (s > 0) {
+            {
                 graph_fork(s0);
-                for (int d = 0; d < 2; ++d) {
-                    const int dir = d == 0 ? 1 : -1;
-                    const int t = d == 0 ? s : T - 1 - s;
+                for (int d = 0; d < p.ndir; ++d) {
+                    const int dir = d == 0 ? p.dir0 : -1;
+                    const int t = dir > 0 ? s : T - 1 - s;
                     const __half *hprev = p.hist + ((long)d * (T + 1) + t + (dir < 0)) * B * Hq;
                     GemmParams g{B, 4 * Hq, Hq, nullptr, 4L * Hq, 1.f, 0, nullptr, 0, 0};
                     g.bn = 128;
@@ -159,7 +200,7 @@ int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
                 }
                 graph_join(s0);
             }
-            step_fwd_gate_kernel<<<grid_of(2L * B * Hq), 256, 0, s0>>>(p, s);
+            step_fwd_gate_kernel<<<grid_of((long)p.ndir * B * Hq), 256, 0, s0>>>(p, s);
             note_launch();
             if (cudaGetLastError() != cudaSuccess) return -5;
         }
@@ -170,31 +211,40 @@ int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
 int rec_step_bwd(const RecStepBwd &p, cudaStream_t st) {
     const int Hq = p.Hq, B = p.B, T = p.T;
     const float alpha = 1.f / (float)(1 << DA_SHIFT);
-    const std::vector<uint64_t> key{2, (uint64_t)T, (uint64_t)B, (uint64_t)p.H, (uint64_t)Hq, u64(p.mask), u64(p.RT16),
+    const std::vector<uint64_t> key{2, (uint64_t)T, (uint64_t)B, (uint64_t)p.H, (uint64_t)Hq, (uint64_t)p.ndir,
+                                    (uint64_t)(p.dir0 + 2), u64(p.c0), u64(p.dhT), u64(p.dcT), u64(p.dh0),
+                                    u64(p.dc0), u64(p.mask), u64(p.RT16),
                                     u64(p.C), (uint64_t)p.ldc, (uint64_t)p.c_doff, u64(p.gates), u64(p.dy),
                                     (uint64_t)p.lddy, (uint64_t)p.dy_doff, u64(p.dA), u64(p.dhR), u64(p.dhc),
                                     u64(p.dcc), u64(p.splitk_ws), (uint64_t)p.splitk_elems};
-    return graph_run(key, PROF_REC_BWD, st, {(const void *)step_bwd_gate_kernel}, [&](cudaStream_t s0) -> int {
+    return graph_run(key, PROF_REC_BWD, st, {(const void *)step_bwd_gate_kernel, (const void *)step_bwd_final_kernel},
+                     [&](cudaStream_t s0) -> int {
         for (int s = 0; s < T; ++s) {
-            step_bwd_gate_kernel<<<grid_of(2L * B * Hq), 256, 0, s0>>>(p, s);
+            step_bwd_gate_kernel<<<grid_of((long)p.ndir * B * Hq), 256, 0, s0>>>(p, s);
             note_launch();
             if (cudaGetLastError() != cudaSuccess) return -5;
-            if (s + 1 == T) break;
+            if (s + 1 == T && !p.dh0) break;  // (dh0 needs the last frame's dA R)
             graph_fork(s0);
-            for (int d = 0; d < 2; ++d) {
-                const int t = d == 0 ? T - 1 - s : s;
-                const __half *dA = p.dA + ((size_t)t * B) * 8 * Hq + (size_t)d * 4 * Hq;
+            for (int d = 0; d < p.ndir; ++d) {
+                const int dir = d == 0 ? p.dir0 : -1;
+                const int t = dir > 0 ? T - 1 - s : s;
+                const __half *dA = p.dA + ((size_t)t * B) * p.ndir * 4 * Hq + (size_t)d * 4 * Hq;
                 GemmParams g{B, Hq, 4 * Hq, nullptr, (long)Hq, alpha, 0, nullptr, 0, 0};
                 g.bn = 128;
                 g.partials = SB;
                 g.splitk_ws = p.dhR + (size_t)d * SB * B * Hq;
                 g.splitk_elems = (long)SB * B * Hq;
-                if (gemm_f16({dA, 8L * Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 1}, g, 0, d ? graph_side() : s0))
+                if (gemm_f16({dA, (long)p.ndir * 4 * Hq, 0}, {p.RT16 + (size_t)d * 4 * Hq * Hq, Hq, 1}, g, 0,
+                             d ? graph_side() : s0))
                     return -5;
             }
             graph_join(s0);
         }
-        return 0;
+        if (p.dh0 || p.dc0) {
+            step_bwd_final_kernel<<<grid_of((long)p.ndir * B * p.H), 256, 0, s0>>>(p);
+            note_launch();
+        }
+        return cudaGetLastError() == cudaSuccess ? 0 : -5;
     });
 }
 

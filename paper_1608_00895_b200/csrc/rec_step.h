@@ -14,21 +14,26 @@ namespace blstm {
 
 struct RecStepFwd {
     int T, B, H, Hq;
-    const float *Z;          // [T*B][8Hq] row-major, column d*4Hq + 4u + gamma, bias included
+    int ndir, dir0;          // directions (1 or 2); scan direction of index 0 (index 1 is always -1)
+    const float *Z;          // [T*B][ndir*4Hq] row-major, column d*4Hq + 4u + gamma, bias included
     const uint8_t *mask;     // [T*B]
     const __half *RT16;      // [2][4Hq][Hq] (R^T per direction, gate-interleaved rows)
-    float *P;                // [2][SF][B][4Hq] scratch: this step's h_{t-1} R^T as split-K partials
+    float *P;                // [2][SF][B][4Hq] scratch: this step's h_{t-1} R^T as split-K partials,
+                             // followed by [2][B][Hq]: the fp32 h carried across masked frames
     float *C;                // cell state after frame t: C[d*c_doff + r*ldc + u]
     long ldc, c_doff;
     float *y;                // [T*B][ldy] (+ d*y_doff), u < H; nullable
     long ldy, y_doff;
     __half *y16;             // [T*B][2Hq] (+ d*Hq); nullable
-    __half *gates;           // [T*B][8Hq] fp16 activations (i, f, g, o at 4u + gamma)
-    __half *hist;            // [2][T+1][B][Hq]: h before frame t at slot t + (dir < 0); slot 0 / T = h0
+    __half *gates;           // [T*B][ndir*4Hq] fp16 activations (i, f, g, o at 4u + gamma)
+    __half *hist;            // [ndir][T+1][B][Hq]: h before frame t at slot t + (dir < 0); slot 0 / T = h0
+    const float *h0, *c0;    // [ndir][B][H] or nullptr (0)
+    float *hT, *cT;          // [ndir][B][H] state after the scan, or nullptr
 };
 
 struct RecStepBwd {
     int T, B, H, Hq;
+    int ndir, dir0;
     const uint8_t *mask;
     const __half *RT16;      // [2][4Hq][Hq]
     const float *C;          // as written by the forward (ldc = Hq, c_doff = T*B*Hq)
@@ -36,7 +41,10 @@ struct RecStepBwd {
     const __half *gates;     // [T*B][8Hq]
     const float *dy;         // [T*B][lddy] (+ d*dy_doff), u < H
     long lddy, dy_doff;
-    __half *dA;              // [T*B][8Hq], scaled by 2^DA_SHIFT
+    __half *dA;              // [T*B][ndir*4Hq], scaled by 2^DA_SHIFT
+    const float *c0;         // [ndir][B][H] or nullptr
+    const float *dhT, *dcT;  // [ndir][B][H] gradients at the end of the scan, or nullptr
+    float *dh0, *dc0;        // [ndir][B][H] gradients w.r.t. h0 / c0 (overwritten), or nullptr
     float *dhR;              // [2][SB][B][Hq] scratch: dA_t R of the previous step (split-K partials)
     float *dhc, *dcc;        // [2][B][Hq] carried dh (masked frames) and dc
     float *splitk_ws;        // split-K scratch of the per-step GEMM

@@ -78,3 +78,31 @@ def test_forced_step_close_to_persistent():
     assert abs(a["loss"] - b["loss"]) / abs(a["loss"]) < 1e-4
     errs = grad_errors(a["grad"], b["grad"], L, D, H, K)
     assert max(errs.values()) < GRAD_TOL, errs
+
+
+@pytest.mark.parametrize("direction", [1, -1])
+def test_single_layer_h1024(direction):
+    """lstm_fwd / lstm_bwd beyond the persistent kernels' capacity (H = 1024) through the
+    step-launched path, with h0 / c0 and the end-of-scan gradients dhT / dcT, against the oracle
+    (y, c, hT, cT, dx, dW, dR, db, dh0, dc0)."""
+    from tests.gpu_util import compare_layer, oracle_layer, run_layer
+    case = synth.random_small_case(11, T=5, B=3, D=24, H=1024, lengths=np.array([5, 3, 0]))
+    s = 1.0 / np.sqrt(1024)
+    case["W"] = (case["W"] * s).astype(np.float32)
+    case["R"] = (case["R"] * s).astype(np.float32)
+    case["dy"] = (case["dy"] * case["mask"][..., None]).astype(np.float32)
+    got = run_layer(case, direction, ldx_pad=3, ldy_pad=5)
+    ref = oracle_layer(case, direction)
+    compare_layer(got, ref, f"H=1024 dir={direction}")
+    assert np.allclose(got["hT"][2], case["h0"][2], atol=1e-6)  # all-masked sequence carries h0
+
+
+def test_forced_step_single_layer(force_step):
+    from tests.gpu_util import compare_layer, oracle_layer, run_layer
+    case = synth.random_small_case(12, T=9, B=5, D=7, H=70)
+    s = 1.0 / np.sqrt(70)  # the paper-sized init scale of the layer tests (test_gpu_parity.py)
+    case["W"] = (case["W"] * s).astype(np.float32)
+    case["R"] = (case["R"] * s).astype(np.float32)
+    case["dy"] = (case["dy"] * case["mask"][..., None]).astype(np.float32)
+    for direction in (1, -1):
+        compare_layer(run_layer(case, direction), oracle_layer(case, direction), f"forced dir={direction}")
