@@ -52,7 +52,7 @@ __global__ void step_fwd_gate_kernel(RecStepFwd p, int s) {
         if (valid) {
             const float4 z = reinterpret_cast<const float4 *>(p.Z + r * G4 + (long)d * 4 * Hq)[u];
             float4 a = z;
-            {  // h_{t-1} R^T (at s = 0 from the h0 slot of the history, 0 when there is no h0)
+            if (s > 0 || p.h0) {  // h_{t-1} R^T (at s = 0 from the h0 slot of the history)
 #pragma unroll
                 for (int k = 0; k < SF; ++k) {
                     const float4 q = reinterpret_cast<const float4 *>(p.P + (((long)d * SF + k) * B + b) * 4 * Hq)[u];
@@ -184,7 +184,7 @@ int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
                                     (uint64_t)p.ldy, (uint64_t)p.y_doff, u64(p.y16), u64(p.gates), u64(p.hist)};
     return graph_run(key, PROF_REC_FWD, st, {(const void *)step_fwd_gate_kernel}, [&](cudaStream_t s0) -> int {
         for (int s = 0; s < T; ++s) {
-            {
+            if (s > 0 || p.h0) {  // (no h0: h_{-1} = 0, nothing to multiply)
                 graph_fork(s0);
                 for (int d = 0; d < p.ndir; ++d) {
                     const int dir = d == 0 ? p.dir0 : -1;
