@@ -628,7 +628,10 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         TRY(wait_count(bstarted + l, (uint32_t)rec_ctas, side), "wait_count");
         return 0;
     };
-    const int side_ctas = overlap ? (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8) : 0;
+    // persistent recurrence: the side GEMMs get the SMs its clusters leave free.  Step-launched
+    // recurrence (no resident clusters): a share of the GPU, so the per-step kernels keep SMs too
+    static const int step_side = getenv("BLSTM_STEP_SIDE_CTAS") ? atoi(getenv("BLSTM_STEP_SIDE_CTAS")) : 74;
+    const int side_ctas = !overlap ? 0 : g.step ? step_side : (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8);
     // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused)
     static thread_local std::vector<cudaEvent_t> evs;
