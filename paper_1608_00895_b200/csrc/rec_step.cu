@@ -31,11 +31,10 @@ DEVI float th(float z) { return 2.f * sg(2.f * z) - 1.f; }
 // thread per (d, b, u), u < Hq
 __global__ void step_fwd_gate_kernel(RecStepFwd p, int s) {
     const int Hq = p.Hq, B = p.B, T = p.T, G4 = p.ndir * 4 * Hq;
-    const long n = (long)p.ndir * B * Hq;
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
-        const int u = (int)(e % Hq);
-        const long db = e / Hq;
-        const int b = (int)(db % B), d = (int)(db / B);
+    // grid: x over units, y over (direction, batch row): no 64-bit index division
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int db = blockIdx.y, b = db % B, d = db / B;
+    if (u < Hq) {
         const int dir = d == 0 ? p.dir0 : -1;
         const int t = dir > 0 ? s : T - 1 - s;
         const long r = (long)t * B + b;
@@ -81,11 +80,9 @@ __global__ void step_fwd_gate_kernel(RecStepFwd p, int s) {
 __global__ void step_bwd_gate_kernel(RecStepBwd p, int s) {
     const int Hq = p.Hq, B = p.B, T = p.T, G4 = p.ndir * 4 * Hq;
     const float scale = (float)(1 << DA_SHIFT);
-    const long n = (long)p.ndir * B * Hq;
-    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
-        const int u = (int)(e % Hq);
-        const long db = e / Hq;
-        const int b = (int)(db % B), d = (int)(db / B);
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int db = blockIdx.y, b = db % B, d = db / B;
+    if (u < Hq) {
         const int dir = d == 0 ? p.dir0 : -1;
         const int t = dir > 0 ? T - 1 - s : s;       // this step's frame (reverse of the forward scan)
         const long r = (long)t * B + b;
@@ -113,7 +110,7 @@ __global__ void step_bwd_gate_kernel(RecStepBwd p, int s) {
             dap[1] = __floats2half2_rn(0.f, 0.f);
             p.dhc[sidx] = dh_in;                     // pass through; dc unchanged
             if (s == 0) p.dcc[sidx] = dc;
-            continue;
+            return;
         }
         const __half2 *gp = reinterpret_cast<const __half2 *>(p.gates + r * G4 + (long)d * 4 * Hq + 4 * u);
         const float2 g01 = __half22float2(gp[0]), g23 = __half22float2(gp[1]);
@@ -200,7 +197,7 @@ int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
                 }
                 graph_join(s0);
             }
-            step_fwd_gate_kernel<<<grid_of((long)p.ndir * B * Hq), 256, 0, s0>>>(p, s);
+            step_fwd_gate_kernel<<<dim3((Hq + 255) / 256, p.ndir * B), 256, 0, s0>>>(p, s);
             note_launch();
             if (cudaGetLastError() != cudaSuccess) return -5;
         }
@@ -220,7 +217,7 @@ int rec_step_bwd(const RecStepBwd &p, cudaStream_t st) {
     return graph_run(key, PROF_REC_BWD, st, {(const void *)step_bwd_gate_kernel, (const void *)step_bwd_final_kernel},
                      [&](cudaStream_t s0) -> int {
         for (int s = 0; s < T; ++s) {
-            step_bwd_gate_kernel<<<grid_of((long)p.ndir * B * Hq), 256, 0, s0>>>(p, s);
+            step_bwd_gate_kernel<<<dim3((Hq + 255) / 256, p.ndir * B), 256, 0, s0>>>(p, s);
             note_launch();
             if (cudaGetLastError() != cudaSuccess) return -5;
             if (s + 1 == T && !p.dh0) break;  // (dh0 needs the last frame's dA R)
