@@ -85,7 +85,11 @@ def kernel_roofline(cat, total_ms, launches, cfg, V, peaks, steps):
             fl -= z_flops_per_frame(cfg)
         a = V * fl * steps / (total_ms / 1e3) / 1e12
         return {"bound": "tensor", "achieved": a, "peak": peaks["tf"], "unit": "TFLOP/s", "frac": a / peaks["tf"],
-                "note": "aggregate over the step's GEMM launches (several shapes)"}
+                "note": "aggregate over the step's GEMM launches (several shapes); the weight-gradient GEMMs "
+                        "run on a side stream capped at the SMs the recurrence clusters leave free (52 of 148 at "
+                        "C3) and the Z GEMMs beside the forward recurrence (inside its timed scope), so this "
+                        "understates the kernel: alone on the GPU the big GEMMs run at 1.2-1.25 PFLOP/s "
+                        "(DESIGN.md 5.1)"}
     flops = 2 * V * 8 * H * H
     bytes_ = 2 * V * 40 * H
     a_tf = flops / per_launch_s / 1e12
