@@ -40,6 +40,8 @@ def _case(U, V, B, D, H, seed, irregular=False):
     (6, 4, 2, 9, 5, True, False),
     (8, 9, 4, 3, 24, False, True),
     (3, 11, 2, 40, 32, True, True),
+    (4, 6, 2, 8, 100, False, True),   # 4 unit tiles in the persistent forward (141 KB of shared memory)
+    (3, 4, 2, 8, 200, True, False),   # R tile beyond 200 KB: the per-diagonal forward
 ])
 def test_mdlstm_matches_oracle(U, V, B, D, H, stable, irregular):
     dev = torch.device("cuda:0")
