@@ -61,7 +61,7 @@ DEVI void tile_coords(int tile, int num_m, int num_n, const GemmParams &p, int &
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_f16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    GemmParams p) {
+                    const __grid_constant__ CUtensorMap tmA2, GemmParams p) {
     using Cfg = GemmCfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -78,11 +78,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
     // split-K: work item = (split, tile); split s covers k-blocks [s*kbs, min(num_kb, (s+1)*kbs))
     const int kbs = (num_kb + p.ksplit - 1) / p.ksplit;
-    const int num_items = num_tiles * p.ksplit;
+    const int per_batch = num_tiles * p.ksplit;
+    const int num_items = per_batch * p.nbatch;
 
     if (warp == 0 && lane_id() == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        if (p.nbatch > 1) tma_prefetch_desc(&tmA2);
         for (int s = 0; s < Cfg::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -101,6 +103,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (p.pdl_chain) {  // (gemm.h) the previous kernel of the chain completed and is visible from here
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -108,11 +114,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
-                const int split = item / num_tiles, tile = item - split * num_tiles;
+                const int bt = item / per_batch, bi = item - bt * per_batch;
+                const int split = bi / num_tiles, tile = bi - split * num_tiles;
                 int mt, nt;
                 tile_coords<BN>(tile, num_m, num_n, p, mt, nt);
                 const int m0 = mt * GEMM_BM, n0 = nt * BN;
                 const int kb1 = min(num_kb, (split + 1) * kbs);
+                const CUtensorMap *mA = bt ? &tmA2 : &tmA;
+                const int boff = bt * (int)p.b_boff;  // along B's outer dimension
                 for (int kb = split * kbs; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
@@ -120,16 +129,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
                     const int k0 = kb * GEMM_BK;
                     if (!p.a_mn) {
-                        tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+                        tma_load_2d(sa, mA, &full[stage], k0, m0);
                     } else {
-                        tma_load_2d(sa, &tmA, &full[stage], m0, k0);
-                        tma_load_2d(sa + 8192, &tmA, &full[stage], m0 + 64, k0);
+                        tma_load_2d(sa, mA, &full[stage], m0, k0);
+                        tma_load_2d(sa + 8192, mA, &full[stage], m0 + 64, k0);
                     }
                     if (!p.b_mn) {
-                        tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+                        tma_load_2d(sb, &tmB, &full[stage], k0, n0 + boff);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+                        for (int j = 0; j < BN / 64; ++j)
+                            tma_load_2d(sb + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0 + boff);
                     }
                     if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -144,7 +154,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
-            const int split = item / num_tiles;
+            const int split = (item % per_batch) / num_tiles;
             const int kb0 = split * kbs, kb1 = min(num_kb, (split + 1) * kbs);
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
@@ -186,11 +196,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float4 *stg4 = reinterpret_cast<float4 *>(sbias + 2 * BN) + (warp - 2) * 128;
         const int lane = lane_id();
         for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
-            const int split = item / num_tiles, tile = item - split * num_tiles;
+            const int bt = item / per_batch, bi = item - bt * per_batch;
+            const int split = bi / num_tiles, tile = bi - split * num_tiles;
             int mt, nt;
             tile_coords<BN>(tile, num_m, num_n, p, mt, nt);
             const int m0 = mt * GEMM_BM, n0 = nt * BN;
-            float *Cbase = p.C + split * p.split_stride;
+            float *Cbase = p.C + bt * p.c_bstride + split * p.split_stride;
             // this tile's bias slice -> shared memory while the MMAs run (a global load per
             // element in the store loop stalled the epilogue on L2 latency)
             for (int k = et; k < BN; k += 32 * GEMM_EPI_WARPS)
@@ -380,17 +391,17 @@ int gemm_prepare() {
 }
 
 template <int BN>
-static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, const GemmParams &p, int max_ctas,
-                               cudaStream_t st) {
+static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &ta2,
+                               const GemmParams &p, int max_ctas, cudaStream_t st) {
     using Cfg = GemmCfg<BN>;
     if (cudaError_t e = gemm_setup<BN>()) return e;
-    const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN) * p.ksplit;
+    const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN) * p.ksplit * p.nbatch;
     int grid = tiles < max_ctas ? tiles : max_ctas;
     if (grid < 1) grid = 1;
     ProfScope ps(PROF_GEMM, st, p.M, p.N, p.K);
     note_launch();
-    if (!p.pdl) {
-        gemm_f16_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, p);
+    if (!p.pdl && !p.pdl_chain) {
+        gemm_f16_kernel<BN><<<grid, GEMM_THREADS, Cfg::SMEM_BYTES, st>>>(ta, tb, ta2, p);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
@@ -403,7 +414,7 @@ static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, con
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_f16_kernel<BN>, ta, tb, p);
+    return cudaLaunchKernelEx(&cfg, gemm_f16_kernel<BN>, ta, tb, ta2, p);
 }
 
 // split-K reduction: C = alpha * sum_s part[s] (+C) (+bias), in fixed order
@@ -429,13 +440,28 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
     if (p.M <= 0 || p.N <= 0) return 0;
     if (p.K <= 0) return -3;  // callers never ask for an empty contraction
     const int BN = p.bn == 128 ? 128 : gemm_bn(p.N);
-    CUtensorMap ta, tb;
+    // two products in one launch (gemm.h a2): partials mode only; batch 1's B lies b_boff rows
+    // (K-major: along N, MN-major: along K) after batch 0's, which must be whole tiles / k-blocks so
+    // no tile of batch 0 reads batch 1's data in place of the zero fill
+    p.nbatch = p.a2 ? 2 : 1;
+    if (p.a2 && (p.partials <= 0 || p.b_boff <= 0 || p.c_bstride < (long)p.partials * p.M * p.N ||
+                 (B.mn_major ? p.K % GEMM_BK : p.N % BN) || p.b_boff < (B.mn_major ? p.K : p.N)))
+        return -3;
+    const long bext = p.a2 ? p.b_boff : 0;  // extra extent of B's outer dimension
+    CUtensorMap ta, tb, ta2;
     int rc;
     if (!A.mn_major) rc = make_tmap_f16(&ta, A.ptr, p.K, p.M, A.ld, GEMM_BM);
     else rc = make_tmap_f16(&ta, A.ptr, p.M, p.K, A.ld, GEMM_BK);
     if (rc) return rc;
-    if (!B.mn_major) rc = make_tmap_f16(&tb, B.ptr, p.K, p.N, B.ld, BN);
-    else rc = make_tmap_f16(&tb, B.ptr, p.N, p.K, B.ld, GEMM_BK);
+    if (p.a2) {
+        if (!A.mn_major) rc = make_tmap_f16(&ta2, p.a2, p.K, p.M, A.ld, GEMM_BM);
+        else rc = make_tmap_f16(&ta2, p.a2, p.M, p.K, A.ld, GEMM_BK);
+        if (rc) return rc;
+    } else {
+        ta2 = ta;
+    }
+    if (!B.mn_major) rc = make_tmap_f16(&tb, B.ptr, p.K, p.N + bext, B.ld, BN);
+    else rc = make_tmap_f16(&tb, B.ptr, p.N, p.K + bext, B.ld, GEMM_BK);
     if (rc) return rc;
     if (max_ctas <= 0) max_ctas = num_sms();
     // split K when the output tiles leave at least half of the allowed CTAs idle
@@ -446,7 +472,8 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
             return -3;
         GemmParams q = p;
         q.C = p.splitk_ws; q.ldc = p.N; q.ksplit = p.partials; q.split_stride = (long)p.M * p.N;
-        cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, q, max_ctas, st) : launch_gemm<128>(ta, tb, q, max_ctas, st);
+        cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, ta2, q, max_ctas, st)
+                                  : launch_gemm<128>(ta, tb, ta2, q, max_ctas, st);
         return e == cudaSuccess ? 0 : -5;
     }
     int S = 1;
@@ -462,7 +489,8 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
         q.C = p.splitk_ws; q.ldc = p.N; q.alpha = 1.f; q.beta = 0; q.bias = nullptr;
         q.ksplit = S; q.split_stride = (long)p.M * p.N;
     }
-    cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, q, max_ctas, st) : launch_gemm<128>(ta, tb, q, max_ctas, st);
+    cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, ta2, q, max_ctas, st)
+                              : launch_gemm<128>(ta, tb, ta2, q, max_ctas, st);
     if (e != cudaSuccess) return -5;
     if (S > 1) {
         const long n = (long)p.M * p.N;

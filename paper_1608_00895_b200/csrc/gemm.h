@@ -43,6 +43,18 @@ struct GemmParams {
     // s * M * N, row-major [M][N]) for the consumer to sum -- no reduction launch (alpha applies
     // to each partial; beta / bias unsupported)
     int partials = 0;
+    // != nullptr: a second, independent product in the same launch (the two directions of a
+    // step-launched recurrence step): batch 1 takes its A operand from a2 (same shape and ld as A),
+    // its B rows / columns at b_boff further along B's outer dimension (B's tensor map spans both),
+    // and writes C at c_bstride elements further
+    const void *a2 = nullptr;
+    long b_boff = 0, c_bstride = 0;
+    int nbatch = 1;          // set by gemm_f16
+    // 1: programmatic dependent launch in a chain of dependent kernels (rec_step.cu): the prologue
+    // overlaps the previous kernel's tail; every thread waits (griddepcontrol.wait) for the
+    // previous grid's completion before any load of its outputs or any store, then lets the next
+    // kernel of the chain launch
+    int pdl_chain = 0;
 };
 
 constexpr int GEMM_BM_ROWS = 128;           // M tile
