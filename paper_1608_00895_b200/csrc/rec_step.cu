@@ -206,6 +206,342 @@ int grid_of(long n) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------------------
+// Persistent forward (Hq <= 1024, B <= 128): the step chain above pays two launches and two grid
+// completions per step.  Here one cooperative launch runs the whole scan.  Thread-block clusters of
+// two CTAs, one cluster per (direction d, 128-column gate tile nt); cluster rank kh holds the K half
+// [kh Hq/2, (kh+1) Hq/2) of the tile's R^T rows in shared memory for the whole scan (TMA, once).
+// Per step s:
+//   1. the TMA warp waits until every CTA of direction d published h_{s-1} (a per-direction counter,
+//      release / acquire at gpu scope), then streams its K half of h_{t-1} (the history slot, the
+//      MMA A operand, M = 128 batch rows) through a PF_S-stage ring;
+//   2. one warp issues the tcgen05 MMAs: D[128 rows x 128 gate columns] = h_{t-1} R^T (K half);
+//   3. the pair exchanges half of D through distributed shared memory: CTA kh finalizes gate columns
+//      [64 kh, 64 kh + 64) of the tile (its 16 units) for all 128 rows and receives the partner's
+//      partial sums for them, so all 8 warps finalize (8 cells per thread);
+//   4. a = Z + P_0 + P_1 (the step chain's order), gates, cell update and mask as in
+//      step_fwd_gate_kernel, with c and the fp32 h carried in registers; h_t -> the history (the
+//      next step's A operand);
+//   5. arrive on the direction's counter, then store C, y, y16 and the gates (off the critical path:
+//      the counter's release covers only the history stores).
+// ---------------------------------------------------------------------------------------------
+constexpr int PF_THREADS = 256;
+constexpr int PF_S = 4;                  // h ring stages (16 KB each: 128 rows x 64 K)
+constexpr uint32_t PF_CHUNK = 16384;
+constexpr uint32_t PF_RECV = 64 * 128 * 4;  // the partner's partial sums of this CTA's 64 columns
+static size_t pf_smem(int Hq) { return (size_t)(Hq / 2 / 64) * PF_CHUNK + PF_S * PF_CHUNK + PF_RECV + 1024 + 256; }
+
+__global__ void __launch_bounds__(PF_THREADS, 1)
+    step_fwd_persist_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmR,
+                            RecStepFwd p, uint32_t *cnt, unsigned long long *trace) {
+#ifdef BLSTM_TRACE
+#define PTR(k) \
+    if (tr) tr[(size_t)s * 16 + (k)] = (unsigned long long)clock64()
+    unsigned long long *tr = (blockIdx.x == 0 && threadIdx.x == 0) ? trace : nullptr;
+#else
+#define PTR(k)
+#endif
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int Hq = p.Hq, B = p.B, T = p.T, H = p.H, G4 = p.ndir * 4 * Hq;
+    const int KC = Hq / 2 / 64;                   // 64-wide K chunks of the half
+    uint8_t *Rs = smem;                           // [KC][128 rows][128 B] SW128
+    uint8_t *ring = Rs + KC * PF_CHUNK;           // [PF_S][128 rows][128 B] SW128
+    float4 *recv = reinterpret_cast<float4 *>(ring + PF_S * PF_CHUNK);  // [16 float4 columns][128 rows]
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + PF_S * PF_CHUNK + PF_RECV);
+    uint64_t *empty = full + PF_S;
+    uint64_t *mma_done = empty + PF_S;
+    uint64_t *rbar = mma_done + 1;
+    uint64_t *xbar = rbar + 1;  // the partner's partial sums landed (st.async complete_tx)
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(xbar + 1);
+
+    const int kh = (int)cluster_ctarank();        // K half (cluster rank)
+    const int tile = blockIdx.x >> 1;
+    const int NT = 4 * Hq / 128;
+    const int d = tile / NT, nt = tile - d * NT;
+    const int dir = d == 0 ? p.dir0 : -1;
+    const int w = warp_uniform(warp_id()), l = lane_id(), q = w & 3, ch = w >> 2;
+    const int m = 32 * q + l;                     // batch row (TMEM lane) this thread reads
+    // this thread finalizes row m, tile columns [64 kh + 32 ch, +32) = 8 units from u0, and sends
+    // the partner its partial sums of columns [64 (1 - kh) + 32 ch, +32)
+    const int u0 = nt * 32 + 16 * kh + 8 * ch;
+    uint32_t *cnt_d = cnt + 32 * d;
+    const uint32_t cpd = 2 * NT;                  // CTAs per direction
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < PF_S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(mma_done, 1);
+        mbar_init(rbar, 1);
+        mbar_init(xbar, 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmH);
+        tma_prefetch_desc(&tmR);
+    }
+    if (w == 1) {
+        tmem_alloc(tslot, 128);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    if (threadIdx.x == 0) {  // the tile's R^T rows, this CTA's K half: resident for the whole scan
+        mbar_arrive_expect_tx(rbar, KC * PF_CHUNK);
+        for (int kc = 0; kc < KC; ++kc)
+            tma_load_2d(Rs + kc * PF_CHUNK, &tmR, rbar, kh * (Hq / 2) + kc * 64, d * 4 * Hq + nt * 128);
+    }
+    mbar_wait(rbar, 0);
+    cluster_sync();  // the partner's barriers are initialised before any remote store
+
+    // state of the 8 cells this thread finalizes (row m, units u0..u0+7)
+    float c_st[8], h_st[8];
+    const bool row_ok = m < B;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int u = u0 + i;
+        c_st[i] = (row_ok && p.c0 && u < H) ? p.c0[((long)d * B + m) * H + u] : 0.f;
+        h_st[i] = (row_ok && p.h0 && u < H) ? p.h0[((long)d * B + m) * H + u] : 0.f;
+    }
+    const bool cvec = (p.ldc & 3) == 0 && (p.c_doff & 3) == 0 && ((uintptr_t)p.C & 15) == 0 && u0 + 8 <= H;
+    const bool yvec = p.y && (p.ldy & 3) == 0 && (p.y_doff & 3) == 0 && ((uintptr_t)p.y & 15) == 0 && u0 + 8 <= H;
+    const uint32_t idesc = idesc_f16(128, 128, 0, 0);
+    const uint32_t partner_recv = mapa_shared(smem_u32(recv), (uint32_t)(kh ^ 1));
+    const uint32_t partner_xbar = mapa_shared(smem_u32(xbar), (uint32_t)(kh ^ 1));
+    int stage = 0;
+    uint32_t phase = 0, mph = 0, xph = 0;
+    for (int s = 0; s < T; ++s) {
+        const int t = dir > 0 ? s : T - 1 - s;
+        const long r = (long)t * B + m;
+        const bool need_mma = s > 0 || p.h0 != nullptr;
+        const int slot_prev = t + (dir < 0);
+        PTR(0);
+        // Z and the mask of this step (produced before the launch): in flight during the MMA
+        float z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = 0.f;
+        bool valid_row = false;
+        if (row_ok) {
+            valid_row = p.mask[r] != 0;
+            const float4 *zp = reinterpret_cast<const float4 *>(p.Z + r * G4 + (long)d * 4 * Hq + 4 * u0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 v = zp[j];
+                z[4 * j] = v.x; z[4 * j + 1] = v.y; z[4 * j + 2] = v.z; z[4 * j + 3] = v.w;
+            }
+        }
+        float acc[32];
+        if (need_mma) {
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(xbar, PF_RECV);  // this step's partial sums
+            if (w == 0) {
+                if (elect_one()) {  // h_{t-1}: wait for the direction's step s-1, then stream it
+                    PTR(1);
+                    if (s > 0) spin_until_geq(cnt_d, (uint32_t)s * cpd);
+                    PTR(2);
+                    fence_proxy_async_global();
+                    const int row0 = (d * (T + 1) + slot_prev) * B;
+                    int st2 = stage;
+                    uint32_t ph2 = phase;
+                    for (int kc = 0; kc < KC; ++kc) {
+                        mbar_wait(&empty[st2], ph2 ^ 1);
+                        mbar_arrive_expect_tx(&full[st2], PF_CHUNK);
+                        tma_load_2d(ring + st2 * PF_CHUNK, &tmH, &full[st2], kh * (Hq / 2) + kc * 64, row0);
+                        if (++st2 == PF_S) { st2 = 0; ph2 ^= 1; }
+                    }
+                    PTR(3);
+                }
+                __syncwarp();
+            } else if (w == 1) {
+                int st2 = stage;
+                uint32_t ph2 = phase;
+                for (int kc = 0; kc < KC; ++kc) {
+                    mbar_wait(&full[st2], ph2);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(ring + st2 * PF_CHUNK), sb = smem_u32(Rs + kc * PF_CHUNK);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        mma_f16_ss_w(tmem, sdesc_sw128(sa + kk * 32, 16, 1024), sdesc_sw128(sb + kk * 32, 16, 1024), idesc,
+                                     (kc | kk) != 0);
+                    mma_commit_w(&empty[st2]);
+                    __syncwarp();
+                    if (++st2 == PF_S) { st2 = 0; ph2 ^= 1; }
+                }
+                mma_commit_w(mma_done);
+                __syncwarp();
+            }
+            {  // ring position after this step (identical in every thread)
+                const int adv = stage + KC;
+                phase ^= (uint32_t)((adv / PF_S) & 1);
+                stage = adv % PF_S;
+            }
+            mbar_wait(mma_done, mph);
+            PTR(4);
+            mph ^= 1;
+            tc_fence_after();
+            const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16);
+            {  // the partner's columns of row m: partial sums -> its receive buffer
+                float v[32];
+                tmem_ld16(ta + 64 * (kh ^ 1) + 32 * ch, *reinterpret_cast<float(*)[16]>(&v[0]));
+                tmem_ld16(ta + 64 * (kh ^ 1) + 32 * ch + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
+                tmem_ld16(ta + 64 * kh + 32 * ch, *reinterpret_cast<float(*)[16]>(&acc[0]));
+                tmem_ld16(ta + 64 * kh + 32 * ch + 16, *reinterpret_cast<float(*)[16]>(&acc[16]));
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    st_async_v4(partner_recv + (uint32_t)(((ch * 8 + j) * 128 + m) * 16), v[4 * j], v[4 * j + 1],
+                                v[4 * j + 2], v[4 * j + 3], partner_xbar);
+            }
+            PTR(5);
+            mbar_wait(xbar, xph);  // the partner's partial sums of this CTA's columns have landed
+            xph ^= 1;
+            PTR(6);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+        }
+        // a = (Z + P_0) + P_1: the step chain's summation order (P_k = K half k)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float4 o = need_mma ? recv[(ch * 8 + j) * 128 + m] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float p0 = kh == 0 ? acc[4 * j + e] : ov[e], p1 = kh == 0 ? ov[e] : acc[4 * j + e];
+                acc[4 * j + e] = (z[4 * j + e] + p0) + p1;
+            }
+        }
+        float yv[8];
+        __half ga[32];
+        if (row_ok) {
+            __half hh[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const bool valid = valid_row && u0 + i < H;
+                float ai = 0.f, af = 0.f, ag = 0.f, ao = 0.f;
+                if (valid) {
+                    ai = sg(acc[4 * i]); af = sg(acc[4 * i + 1]); ag = th(acc[4 * i + 2]); ao = sg(acc[4 * i + 3]);
+                    const float cn = af * c_st[i] + ai * ag;
+                    c_st[i] = cn;
+                    h_st[i] = ao * th(cn);
+                }
+                hh[i] = __float2half_rn(h_st[i]);
+                yv[i] = valid ? h_st[i] : 0.f;
+                ga[4 * i] = __float2half_rn(ai); ga[4 * i + 1] = __float2half_rn(af);
+                ga[4 * i + 2] = __float2half_rn(ag); ga[4 * i + 3] = __float2half_rn(ao);
+            }
+            // h_t -> the history slot the next step's TMA reads
+            *reinterpret_cast<uint4 *>(p.hist + (((long)d * (T + 1) + slot_prev + dir) * B + m) * Hq + u0) =
+                *reinterpret_cast<const uint4 *>(hh);
+        }
+        // publish h_t of this CTA's columns to the direction: the CTA barrier orders every thread's
+        // history store before thread 0's release (cumulative), which the next step's acquire pairs with
+        PTR(7);
+        tc_fence_before();
+        __syncthreads();
+        PTR(8);
+        if (threadIdx.x == 0) red_release_gpu_add(cnt_d, 1u);
+        PTR(9);
+        if (row_ok) {  // the step's other outputs: read only after the launch completes
+            uint4 *gp = reinterpret_cast<uint4 *>(p.gates + r * G4 + (long)d * 4 * Hq + 4 * u0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) gp[j] = *reinterpret_cast<const uint4 *>(&ga[8 * j]);
+            if (p.y16) {
+                __half yh[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) yh[i] = __float2half_rn(yv[i]);
+                *reinterpret_cast<uint4 *>(p.y16 + r * 2 * Hq + (long)d * Hq + u0) = *reinterpret_cast<const uint4 *>(yh);
+            }
+            float *cp = p.C + d * p.c_doff + r * p.ldc + u0;
+            if (cvec) {
+                reinterpret_cast<float4 *>(cp)[0] = make_float4(c_st[0], c_st[1], c_st[2], c_st[3]);
+                reinterpret_cast<float4 *>(cp)[1] = make_float4(c_st[4], c_st[5], c_st[6], c_st[7]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (u0 + i < H) cp[i] = c_st[i];
+            }
+            if (p.y) {
+                float *yq = p.y + r * p.ldy + d * p.y_doff + u0;
+                if (yvec) {
+                    reinterpret_cast<float4 *>(yq)[0] = make_float4(yv[0], yv[1], yv[2], yv[3]);
+                    reinterpret_cast<float4 *>(yq)[1] = make_float4(yv[4], yv[5], yv[6], yv[7]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (u0 + i < H) yq[i] = yv[i];
+                }
+            }
+        }
+    }
+    if (row_ok) {  // state after the whole scan
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int u = u0 + i;
+            if (u < H) {
+                if (p.hT) p.hT[((long)d * B + m) * H + u] = h_st[i];
+                if (p.cT) p.cT[((long)d * B + m) * H + u] = c_st[i];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // no remote store into this CTA's shared memory is outstanding
+    if (w == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 128);
+    }
+}
+
+// 1: launched; 0: not used (the caller runs the step chain); < 0: error.  Used where it applies
+// (B <= 128, Hq <= 1024, all CTAs co-resident); BLSTM_STEP_PERSIST=0 turns it off, =1 forces it
+// (then an inapplicable size or a failed launch is an error instead of the fallback).
+static int rec_step_fwd_persist(const RecStepFwd &p, cudaStream_t st) {
+    const char *e = getenv("BLSTM_STEP_PERSIST");
+    if (e && e[0] == '0') return 0;
+    const bool force = e && e[0] == '1';
+    const int no = force ? -6 : 0;
+    const int Hq = p.Hq;
+    if (p.B > 128 || Hq > 1024 || Hq % 128 || p.T < 1) return no;
+    const int ctas = p.ndir * 2 * (4 * Hq / 128);
+    if (ctas > num_sms()) return no;
+    const size_t smem = pf_smem(Hq);
+    if (cudaFuncSetAttribute(step_fwd_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return force ? -5 : 0;
+    }
+    CUtensorMap tmH, tmR;
+    if (make_tmap_f16(&tmH, p.hist, Hq, (uint64_t)p.ndir * (p.T + 1) * p.B, Hq, 128)) return -5;
+    if (make_tmap_f16(&tmR, p.RT16, Hq, (uint64_t)p.ndir * 4 * Hq, Hq, 128)) return -5;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(PF_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, step_fwd_persist_kernel, &cfg) != cudaSuccess ||
+        nclusters < ctas / 2) {
+        cudaGetLastError();
+        return no;
+    }
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(p.P);  // the partials scratch is unused here
+    if (cudaMemsetAsync(cnt, 0, 64 * sizeof(uint32_t), st) != cudaSuccess) return -5;
+    ProfScope ps(PROF_REC_FWD, st);
+    note_launch();
+    return cudaLaunchKernelEx(&cfg, step_fwd_persist_kernel, tmH, tmR, p, cnt, rec_trace_fwd()) == cudaSuccess ? 1 : -5;
+}
+
 size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * SF * B * 4 * Hq * 4 + (size_t)2 * B * Hq * 4; }
 size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)(2 * SB + 4) * B * Hq * 4; }
 
@@ -214,6 +550,7 @@ size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)(2 * SB + 4) *
 // directions' per-step GEMMs are parallel branches.
 
 int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
+    if (const int rc = rec_step_fwd_persist(p, st)) return rc < 0 ? rc : 0;
     const int Hq = p.Hq, B = p.B, T = p.T;
     const bool pdl = step_pdl();
     const std::vector<uint64_t> key{1, (uint64_t)T, (uint64_t)B, (uint64_t)p.H, (uint64_t)Hq, (uint64_t)p.ndir,

@@ -28,6 +28,9 @@ FWD = [(0, None), (11, "wait own half of h"), (1, "wait partner relay"), (2, "MM
 BWD = [(0, None), (1, "issue next-step loads"), (2, "wait P + gather"), (8, "wait inputs + smem reads"), (9, "dA math + smem"),
        (3, "fences + __syncthreads"), (10, "MMA issue + dA stores"), (4, "MMA wait"),
        (11, "TMEM ld"), (6, "P staging"), (7, "bulk_wait + __syncthreads"), (5, "send P + loads")]
+# the persistent forward of the step-launched path (rec_step.cu, BLSTM_STEP_PERSIST=1)
+PFWD = [(0, None), (1, "Z loads issued"), (2, "grid barrier wait"), (3, "TMA issue"), (4, "MMA wait"),
+        (5, "TMEM ld + send"), (6, "cluster sync"), (7, "gate math + stores"), (8, "__syncthreads"), (9, "arrive")]
 
 
 def report(name, tr, seq):
@@ -59,6 +62,9 @@ def main():
     blstm.blstm_debug_set_trace(None, None)
     f = tf.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
     b = tb.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
+    if os.environ.get("BLSTM_STEP_PERSIST") == "1":
+        report("forward (persistent step path)", f, PFWD)
+        return
     report("forward", f, FWD)
     # backward rows are indexed by s descending; use processing order
     report("backward", b[::-1], BWD)

@@ -106,3 +106,36 @@ def test_forced_step_single_layer(force_step):
     case["dy"] = (case["dy"] * case["mask"][..., None]).astype(np.float32)
     for direction in (1, -1):
         compare_layer(run_layer(case, direction), oracle_layer(case, direction), f"forced dir={direction}")
+
+
+@pytest.mark.parametrize("H,force", [(1024, False), (300, True)])
+def test_persistent_forward_close_to_chain(H, force):
+    """The persistent forward of the step path (B <= 128, Hq <= 1024; rec_step.cu) against the
+    launched chain it replaces (BLSTM_STEP_PERSIST=1 forced vs =0): the same two K-half partial
+    sums in the same order, but separately compiled gate math (FMA contraction may differ), so the
+    outputs agree to rounding, not bit for bit."""
+    L, D, K, T = 2, 40, 13, 7
+    lengths = [7, 6, 2, 7, 1]
+    params = synth.stack_params(L, D, H, K)
+    batch = synth.speech_batch(T, len(lengths), D, K, np.array(lengths), seed=1006)
+    theta = oracle.pack_params(params, L, D, H, K)
+    out = {}
+    if force:
+        os.environ["BLSTM_FORCE_STEP"] = "1"
+    try:
+        for mode in ("0", "1"):
+            os.environ["BLSTM_STEP_PERSIST"] = mode
+            st = Stack(L, D, H, K, T, len(lengths))
+            out[mode] = (st.forward(theta, batch), st.step(theta, batch, side_stream=True))
+    finally:
+        os.environ.pop("BLSTM_STEP_PERSIST", None)
+        os.environ.pop("BLSTM_FORCE_STEP", None)
+    (Y0, C0), g0 = out["0"]
+    (Y1, C1), g1 = out["1"]
+    for l in range(L):
+        assert norm_rel(Y1[l], Y0[l]) < OUT_TOL
+        for d in range(2):
+            assert norm_rel(C1[l, d], C0[l, d]) < OUT_TOL
+    assert abs(g1["loss"] - g0["loss"]) / abs(g0["loss"]) < 1e-4
+    errs = grad_errors(g1["grad"], g0["grad"], L, D, H, K)
+    assert max(errs.values()) < GRAD_TOL, errs
