@@ -312,26 +312,47 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const uint32_t partner_xbar = mapa_shared(smem_u32(xbar), (uint32_t)(kh ^ 1));
     int stage = 0;
     uint32_t phase = 0, mph = 0, xph = 0;
+    // a step's outputs other than the history (read only after the launch completes)
+    float yv[8];
+    __half ga[32];
+    long r_pend = -1;
+    auto store_outputs = [&](long rr) {
+        uint4 *gp = reinterpret_cast<uint4 *>(p.gates + rr * G4 + (long)d * 4 * Hq + 4 * u0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) gp[j] = *reinterpret_cast<const uint4 *>(&ga[8 * j]);
+        if (p.y16) {
+            __half yh[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) yh[i] = __float2half_rn(yv[i]);
+            *reinterpret_cast<uint4 *>(p.y16 + rr * 2 * Hq + (long)d * Hq + u0) = *reinterpret_cast<const uint4 *>(yh);
+        }
+        float *cp = p.C + d * p.c_doff + rr * p.ldc + u0;
+        if (cvec) {
+            reinterpret_cast<float4 *>(cp)[0] = make_float4(c_st[0], c_st[1], c_st[2], c_st[3]);
+            reinterpret_cast<float4 *>(cp)[1] = make_float4(c_st[4], c_st[5], c_st[6], c_st[7]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (u0 + i < H) cp[i] = c_st[i];
+        }
+        if (p.y) {
+            float *yq = p.y + rr * p.ldy + d * p.y_doff + u0;
+            if (yvec) {
+                reinterpret_cast<float4 *>(yq)[0] = make_float4(yv[0], yv[1], yv[2], yv[3]);
+                reinterpret_cast<float4 *>(yq)[1] = make_float4(yv[4], yv[5], yv[6], yv[7]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (u0 + i < H) yq[i] = yv[i];
+            }
+        }
+    };
     for (int s = 0; s < T; ++s) {
         const int t = dir > 0 ? s : T - 1 - s;
         const long r = (long)t * B + m;
         const bool need_mma = s > 0 || p.h0 != nullptr;
         const int slot_prev = t + (dir < 0);
         PTR(0);
-        // Z and the mask of this step (produced before the launch): in flight during the MMA
-        float z[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) z[i] = 0.f;
-        bool valid_row = false;
-        if (row_ok) {
-            valid_row = p.mask[r] != 0;
-            const float4 *zp = reinterpret_cast<const float4 *>(p.Z + r * G4 + (long)d * 4 * Hq + 4 * u0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float4 v = zp[j];
-                z[4 * j] = v.x; z[4 * j + 1] = v.y; z[4 * j + 2] = v.z; z[4 * j + 3] = v.w;
-            }
-        }
         float acc[32];
         if (need_mma) {
             if (threadIdx.x == 0) mbar_arrive_expect_tx(xbar, PF_RECV);  // this step's partial sums
@@ -376,6 +397,25 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
                 phase ^= (uint32_t)((adv / PF_S) & 1);
                 stage = adv % PF_S;
             }
+        }
+        // the previous step's other outputs, deferred to here: off the TMA / MMA warps' path to this
+        // step's loads, overlapping the MMAs
+        if (r_pend >= 0) store_outputs(r_pend);
+        // Z and the mask of this step (produced before the launch): in flight during the MMA
+        float z[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[i] = 0.f;
+        bool valid_row = false;
+        if (row_ok) {
+            valid_row = p.mask[r] != 0;
+            const float4 *zp = reinterpret_cast<const float4 *>(p.Z + r * G4 + (long)d * 4 * Hq + 4 * u0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 v = zp[j];
+                z[4 * j] = v.x; z[4 * j + 1] = v.y; z[4 * j + 2] = v.z; z[4 * j + 3] = v.w;
+            }
+        }
+        if (need_mma) {
             mbar_wait(mma_done, mph);
             PTR(4);
             mph ^= 1;
@@ -412,8 +452,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
                 acc[4 * j + e] = (z[4 * j + e] + p0) + p1;
             }
         }
-        float yv[8];
-        __half ga[32];
         if (row_ok) {
             __half hh[8];
 #pragma unroll
@@ -443,38 +481,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         PTR(8);
         if (threadIdx.x == 0) red_release_gpu_add(cnt_d, 1u);
         PTR(9);
-        if (row_ok) {  // the step's other outputs: read only after the launch completes
-            uint4 *gp = reinterpret_cast<uint4 *>(p.gates + r * G4 + (long)d * 4 * Hq + 4 * u0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) gp[j] = *reinterpret_cast<const uint4 *>(&ga[8 * j]);
-            if (p.y16) {
-                __half yh[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) yh[i] = __float2half_rn(yv[i]);
-                *reinterpret_cast<uint4 *>(p.y16 + r * 2 * Hq + (long)d * Hq + u0) = *reinterpret_cast<const uint4 *>(yh);
-            }
-            float *cp = p.C + d * p.c_doff + r * p.ldc + u0;
-            if (cvec) {
-                reinterpret_cast<float4 *>(cp)[0] = make_float4(c_st[0], c_st[1], c_st[2], c_st[3]);
-                reinterpret_cast<float4 *>(cp)[1] = make_float4(c_st[4], c_st[5], c_st[6], c_st[7]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (u0 + i < H) cp[i] = c_st[i];
-            }
-            if (p.y) {
-                float *yq = p.y + r * p.ldy + d * p.y_doff + u0;
-                if (yvec) {
-                    reinterpret_cast<float4 *>(yq)[0] = make_float4(yv[0], yv[1], yv[2], yv[3]);
-                    reinterpret_cast<float4 *>(yq)[1] = make_float4(yv[4], yv[5], yv[6], yv[7]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        if (u0 + i < H) yq[i] = yv[i];
-                }
-            }
-        }
+        r_pend = row_ok ? r : -1;  // its other outputs: stored during the next step
     }
+    if (r_pend >= 0) store_outputs(r_pend);
     if (row_ok) {  // state after the whole scan
 #pragma unroll
         for (int i = 0; i < 8; ++i) {

@@ -62,7 +62,7 @@ def main():
     blstm.blstm_debug_set_trace(None, None)
     f = tf.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
     b = tb.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
-    if os.environ.get("BLSTM_STEP_PERSIST") == "1":
+    if cfg.H > 512 and os.environ.get("BLSTM_STEP_PERSIST") != "0":  # the step path (H beyond the cluster kernels)
         report("forward (persistent step path)", f, PFWD)
         return
     report("forward", f, FWD)
