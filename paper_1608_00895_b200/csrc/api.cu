@@ -268,7 +268,9 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
         q.dy = dy; q.lddy = d->ldy; q.dy_doff = 0;
         q.dA = dA;
         float *sb = (float *)(ws + w.stepB);
-        q.dhR = sb; q.dhc = sb + 16L * g.B * g.Hq; q.dcc = sb + 18L * g.B * g.Hq;  // (rec_step: 2 x SB partials)
+        q.dhR = sb;
+        q.dhc = sb + rec_step_bwd_partial_floats(g.B, g.Hq);
+        q.dcc = q.dhc + 2L * g.B * g.Hq;
         q.c0 = c0; q.dhT = dhT; q.dcT = dcT; q.dh0 = dh0; q.dc0 = dc0;
         TRY(rec_step_bwd(q, st), "rec_step_bwd");
         if (cudaMemsetAsync(dbp, 0, (size_t)4 * g.Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
@@ -629,8 +631,9 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         return 0;
     };
     // persistent recurrence: the side GEMMs get the SMs its clusters leave free.  Step-launched
-    // recurrence (no resident clusters): a share of the GPU, so the per-step kernels keep SMs too
-    static const int step_side = getenv("BLSTM_STEP_SIDE_CTAS") ? atoi(getenv("BLSTM_STEP_SIDE_CTAS")) : 74;
+    // recurrence (no resident clusters): a share of the GPU sized so that it and the per-step BPTT
+    // GEMM (64 CTAs, rec_step.cu SB) run in one wave (C5 sweep: 64 best of 40..74)
+    static const int step_side = getenv("BLSTM_STEP_SIDE_CTAS") ? atoi(getenv("BLSTM_STEP_SIDE_CTAS")) : 64;
     const int side_ctas = !overlap ? 0 : g.step ? step_side : (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8);
     // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused)
@@ -754,7 +757,9 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
             q.dy = p.dy; q.lddy = p.lddy; q.dy_doff = p.dy_doff;
             q.dA = dA;
             float *sb = (float *)(ws + w.stepB);
-            q.dhR = sb; q.dhc = sb + 16L * g.B * Hq; q.dcc = sb + 18L * g.B * Hq;  // (rec_step: 2 x SB = 16 partials)
+            q.dhR = sb;
+            q.dhc = sb + rec_step_bwd_partial_floats(g.B, Hq);
+            q.dcc = q.dhc + 2L * g.B * Hq;
             q.splitk_ws = (float *)(ws + w.gsk); q.splitk_elems = GSK_ELEMS;
             TRY(rec_step_bwd(q, st), "rec_step_bwd");
             if (cudaMemsetAsync(dbp, 0, (size_t)8 * Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");

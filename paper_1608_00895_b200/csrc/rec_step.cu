@@ -21,7 +21,7 @@ namespace blstm {
 // per-step GEMMs split K this many ways into fp32 partials, summed (fixed order) by the gate kernel
 // that consumes them: 4x / 8x the CTAs of the unsplit GEMM and no reduction launch
 constexpr int SF = 2;  // forward  h R^T: K = Hq (a multiple of 256); 2 x 2 directions x 32 tiles <= 148 SMs
-constexpr int SB = 8;  // BPTT     dA R:  K = 4Hq
+constexpr int SB = 4;  // BPTT     dA R:  K = 4Hq; 2 dirs x 8 tiles x 4 = 64 CTAs beside the side GEMMs (BLSTM_STEP_SIDE_CTAS)
 
 namespace {
 
@@ -552,7 +552,8 @@ static int rec_step_fwd_persist(const RecStepFwd &p, cudaStream_t st) {
 }
 
 size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * SF * B * 4 * Hq * 4 + (size_t)2 * B * Hq * 4; }
-size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (size_t)(2 * SB + 4) * B * Hq * 4; }
+size_t rec_step_bwd_partial_floats(int B, int Hq) { return (size_t)2 * SB * B * Hq; }
+size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (rec_step_bwd_partial_floats(B, Hq) + (size_t)4 * B * Hq) * 4; }
 
 // The T-step loop of a layer is captured once into a CUDA graph (graph.h) and replayed: a loop of
 // ~3T small launches is otherwise bound by the host's launch rate.  Inside the graph the two

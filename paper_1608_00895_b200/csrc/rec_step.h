@@ -46,6 +46,7 @@ struct RecStepBwd {
     const float *dhT, *dcT;  // [ndir][B][H] gradients at the end of the scan, or nullptr
     float *dh0, *dc0;        // [ndir][B][H] gradients w.r.t. h0 / c0 (overwritten), or nullptr
     float *dhR;              // [2][SB][B][Hq] scratch: dA_t R of the previous step (split-K partials)
+                             // (layout of the scratch: rec_step_bwd_partial_floats)
     float *dhc, *dcc;        // [2][B][Hq] carried dh (masked frames) and dc
     float *splitk_ws;        // split-K scratch of the per-step GEMM
     long splitk_elems;
@@ -53,6 +54,9 @@ struct RecStepBwd {
 
 size_t rec_step_fwd_scratch_bytes(int B, int Hq);
 size_t rec_step_bwd_scratch_bytes(int B, int Hq);
+// floats of the dA R partials at the start of the BPTT scratch ([2][SB][B][Hq]); dhc and dcc
+// ([2][B][Hq] each) follow
+size_t rec_step_bwd_partial_floats(int B, int Hq);
 int rec_step_fwd(const RecStepFwd &p, cudaStream_t st);
 int rec_step_bwd(const RecStepBwd &p, cudaStream_t st);
 
