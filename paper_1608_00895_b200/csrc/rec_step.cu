@@ -546,9 +546,19 @@ static int rec_step_fwd_persist(const RecStepFwd &p, cudaStream_t st) {
     }
     uint32_t *cnt = reinterpret_cast<uint32_t *>(p.P);  // the partials scratch is unused here
     if (cudaMemsetAsync(cnt, 0, 64 * sizeof(uint32_t), st) != cudaSuccess) return -5;
-    ProfScope ps(PROF_REC_FWD, st);
+    // a cooperative cluster launch can be refused (e.g. under a profiler that replays kernels):
+    // then the launched chain runs instead, unless forced
+    bool ok;
+    {
+        ProfScope ps(PROF_REC_FWD, st);
+        ok = cudaLaunchKernelEx(&cfg, step_fwd_persist_kernel, tmH, tmR, p, cnt, rec_trace_fwd()) == cudaSuccess;
+    }
+    if (!ok) {
+        cudaGetLastError();
+        return force ? -5 : 0;
+    }
     note_launch();
-    return cudaLaunchKernelEx(&cfg, step_fwd_persist_kernel, tmH, tmR, p, cnt, rec_trace_fwd()) == cudaSuccess ? 1 : -5;
+    return 1;
 }
 
 size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * SF * B * 4 * Hq * 4 + (size_t)2 * B * Hq * 4; }
