@@ -14,35 +14,20 @@ struct GraphEntry {
     long launches;
 };
 std::map<std::vector<uint64_t>, GraphEntry> g_graphs;
-cudaStream_t g_side = nullptr, g_cap = nullptr;
-cudaEvent_t g_fork = nullptr, g_join = nullptr;
+cudaStream_t g_cap = nullptr;  // the capture stream
 
-int side_init() {
-    if (g_side) return 0;
-    if (cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking) != cudaSuccess) return -5;
-    if (cudaStreamCreateWithFlags(&g_cap, cudaStreamNonBlocking) != cudaSuccess) return -5;
-    if (cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess) return -5;
-    if (cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming) != cudaSuccess) return -5;
-    return 0;
+int cap_init() {
+    if (g_cap) return 0;
+    return cudaStreamCreateWithFlags(&g_cap, cudaStreamNonBlocking) == cudaSuccess ? 0 : -5;
 }
 
 }  // namespace
-
-cudaStream_t graph_side() { return g_side; }
-void graph_fork(cudaStream_t st) {
-    cudaEventRecord(g_fork, st);
-    cudaStreamWaitEvent(g_side, g_fork, 0);
-}
-void graph_join(cudaStream_t st) {
-    cudaEventRecord(g_join, g_side);
-    cudaStreamWaitEvent(st, g_join, 0);
-}
 
 int graph_run(const std::vector<uint64_t> &key, int cat, cudaStream_t st, std::initializer_list<const void *> kernels,
               const std::function<int(cudaStream_t)> &body) {
     auto it = g_graphs.find(key);
     if (it == g_graphs.end()) {
-        if (gemm_prepare() || side_init()) return -5;
+        if (gemm_prepare() || cap_init()) return -5;
         cudaFuncAttributes fa;
         for (const void *k : kernels)
             if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return -5;

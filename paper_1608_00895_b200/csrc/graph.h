@@ -18,10 +18,6 @@ namespace blstm {
 // replay is one launch scope of category cat (prof.h).
 int graph_run(const std::vector<uint64_t> &key, int cat, cudaStream_t st, std::initializer_list<const void *> kernels,
               const std::function<int(cudaStream_t)> &body);
-// inside a body: a second capture stream, and fork / join of it with the body's stream
-cudaStream_t graph_side();
-void graph_fork(cudaStream_t s0);
-void graph_join(cudaStream_t s0);
 inline uint64_t u64(const void *p) { return (uint64_t)(uintptr_t)p; }
 
 }  // namespace blstm
