@@ -636,10 +636,12 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     static const int step_side = getenv("BLSTM_STEP_SIDE_CTAS") ? atoi(getenv("BLSTM_STEP_SIDE_CTAS")) : 64;
     const int side_ctas = !overlap ? 0 : g.step ? step_side : (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8);
     // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
-    // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused)
+    // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
+    // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch)
     static thread_local std::vector<cudaEvent_t> evs;
-    if (overlap && evs.size() < 2 * (size_t)g.L + 2) {
-        while (evs.size() < 2 * (size_t)g.L + 2) {
+    const int GSK_FREE = 2 * g.L + 2;
+    if (overlap && evs.size() < 2 * (size_t)g.L + 3) {
+        while (evs.size() < 2 * (size_t)g.L + 3) {
             cudaEvent_t e;
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "event");
             evs.push_back(e);
@@ -683,6 +685,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
         gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
         TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
+        if (overlap) cudaEventRecord(evs[GSK_FREE], side);
         TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
         TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
         if (comm) {  // sync-mode exchange of this bucket (the head), overlapping the BPTT below
@@ -693,42 +696,46 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
                 return rc;
         return 0;
     };
-    auto side_layer = [&](int l) -> int {  // dW, dR, db of layer l (inputs: dA / dbpart of its parity)
+    // ss: the side stream, or (layer 0, which follows the last BPTT) s_main, which is idle then
+    auto side_layer = [&](int l, cudaStream_t ss) -> int {  // dW, dR, db of layer l (its parity's dA / dbpart)
         const int par = l & 1;
         const __half *dA = (__half *)(ws + w.dA) + (size_t)par * g.TB * 8 * Hq;
         float *dWT = (float *)(ws + w.dWT) + (size_t)par * 8 * Hq * w.maxDn;
         float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
         const float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
-        if (overlap) cudaStreamWaitEvent(side, evs[l], 0);
+        if (overlap && ss == side) cudaStreamWaitEvent(side, evs[l], 0);
         if (l > 0)  // overlaps BPTT(l-1)
             if (int rc = side_guard(l - 1)) return rc;
+        // on s_main: the split-K scratch is shared with the side stream's GEMMs (the last layer's)
+        if (overlap && ss != side) cudaStreamWaitEvent(ss, evs[GSK_FREE], 0);
         const __half *X = l == 0 ? (const __half *)(ws + w.x16) : (const __half *)(ws + w.y16[l - 1]);
         // the last layer's weight gradients run after all BPTT work: every SM is free then
         const int wctas = l == 0 ? 0 : side_ctas;
         GemmParams gw{8 * Hq, g.Dn[l], (int)g.TB, dWT, g.Dn[l], a, 0, nullptr, 0, 0};
         gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
-        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, wctas, side), "gemm dW");
+        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, wctas, ss), "gemm dW");
         const __half *hist = (const __half *)(ws + w.hist[l]);
         for (int dd = 0; dd < 2; ++dd) {
             const __half *hprev = hist + ((long)dd * (g.T + 1) + dd) * g.B * Hq;
             GemmParams gr{4 * Hq, Hq, (int)g.TB, dRT + (size_t)dd * 4 * Hq * Hq, Hq, a, 0, nullptr, 0, 0};
             gr.splitk_ws = (float *)(ws + w.gsk); gr.splitk_elems = GSK_ELEMS;
-            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, wctas, side), "gemm dR");
+            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, wctas, ss), "gemm dR");
         }
+        if (overlap && ss == side) cudaEventRecord(evs[GSK_FREE], side);
         for (int dd = 0; dd < 2; ++dd) {
             const int e = 6 * l + 3 * dd;
-            TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], side), "scatter dW");
-            TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, side), "scatter dR");
-            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.step ? 1 : g.pl.G, dd, side), "scatter db");
+            TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], ss), "scatter dW");
+            TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, ss), "scatter dR");
+            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.step ? 1 : g.pl.G, dd, ss), "scatter db");
         }
         const size_t end = l + 1 < g.L ? offs[6 * (l + 1)] : offs[6 * g.L];
         if (comm) {  // sync-mode exchange of layer l's bucket (§4.1), overlapping BPTT
-            if (int rc = dp_allreduce_grads_impl(comm, grad + offs[6 * l], end - offs[6 * l], side)) return rc;
+            if (int rc = dp_allreduce_grads_impl(comm, grad + offs[6 * l], end - offs[6 * l], ss)) return rc;
         }
         if (bucket_update)  // layer l's parameters are final: update them while BPTT continues below
-            if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, offs[6 * l], end, 1, nullptr, side))
+            if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, offs[6 * l], end, 1, nullptr, ss))
                 return rc;
-        if (overlap) cudaEventRecord(evs[g.L + 2 + l], side);
+        if (overlap) cudaEventRecord(evs[g.L + 2 + l], ss);
         return 0;
     };
     int cur = 0;
@@ -769,7 +776,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
             TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
         }
         // the gradient work this BPTT overlaps, enqueued after it
-        if (int rc = (l == g.L - 1) ? side_head() : side_layer(l + 1)) return rc;
+        if (int rc = (l == g.L - 1) ? side_head() : side_layer(l + 1, side)) return rc;
         const __half *w16 = (const __half *)(ws + w.w16[l]);
         if (l > 0) {  // critical path: gradient of the layer below's output
             GemmParams gx{(int)g.TB, g.Dn[l], 8 * Hq, dY[1 - cur], 2L * Hq, a, 0, nullptr, 0, 0};
@@ -780,7 +787,10 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         if (overlap) cudaEventRecord(evs[l], st);
         cur = 1 - cur;
     }
-    if (int rc = side_layer(0)) return rc;
+    // layer 0's gradient work follows the last BPTT: on s_main it starts while the side stream
+    // finishes layer 1's scatters and update (with NCCL, on the side stream: one stream issues the
+    // collectives, in bucket order)
+    if (int rc = side_layer(0, (overlap && !comm) ? st : side)) return rc;
     if (overlap) {  // s_main's view: all gradient work of this call is complete
         cudaEventRecord(evs[g.L], side);
         cudaStreamWaitEvent(st, evs[g.L], 0);
