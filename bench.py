@@ -140,7 +140,10 @@ def measured_peaks():
 # clocks during the timed region
 # ----------------------------------------------------------------------------
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampled every 50 ms from before the warm-up; stop(t0, t1) keeps the samples taken
+    inside the timed region's wall-clock window [t0, t1] (a C3 region is ~70 ms), widened by 0.25 s
+    on each side only if none fell inside (then "window": "widened")."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -154,25 +157,36 @@ class ClockSampler:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
         if self.proc is None:
             return None
+        time.sleep(0.1)  # the sample after the region's end
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        rows = []
+        import datetime
+        stamped = []
         for line in open(self.path):
             parts = [s.strip() for s in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
+            if len(parts) >= 10:
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    ts = None
+                stamped.append((ts, parts[1:]))
         os.unlink(self.path)
+        window = "timed region"
+        rows = [r for ts, r in stamped if t0 is None or (ts is not None and t0 <= ts <= t1)]
+        if not rows and t0 is not None:
+            window = "widened"
+            rows = [r for ts, r in stamped if ts is not None and t0 - 0.25 <= ts <= t1 + 0.25]
         if not rows:
             return None
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -185,7 +199,7 @@ class ClockSampler:
                     reasons.add(n)
         loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "reasons": sorted(reasons), "samples": len(rows), "window": window}
 
 
 # ----------------------------------------------------------------------------
@@ -290,29 +304,30 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return t.item()
 
+    clocks = ClockSampler(local)  # sampling from before the warm-up: running by the timed region
+    clocks.start()
     for _ in range(args.warmup):
         tr.step()
     barrier()
 
     # ---------------- device-resident timed region ----------------
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
     n0 = blstm.blstm_launch_count()
     blstm.blstm_profile_enable(True)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    w0 = time.time()
     e0.record(st)
     for _ in range(args.steps):
         tr.step()
     e1.record(st)
     barrier()
+    w1 = time.time()
     t_local = e0.elapsed_time(e1) / 1e3
     launches = blstm.blstm_launch_count() - n0
     prof = {c: blstm.blstm_profile_read(c) for c in (blstm.PROF_REC_FWD, blstm.PROF_REC_BWD, blstm.PROF_GEMM)}
     blstm.blstm_profile_enable(False)
-    clk = clocks.stop()
+    clk = clocks.stop(w0, w1)
     t_max = max_over_ranks(t_local)
     frames = sum_over_ranks(tr.valid_frames * args.steps)
     value = frames / t_max

@@ -477,12 +477,28 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     const int Hq = g.Hq;
     __half *x16 = (__half *)(ws + w.x16);
     TRY(cast_x_f16(x, g.D, g.D, x16, g.Dp0, g.TB, st, drop ? g.dr : Dropout{0, 0, 0, 1.f}), "cast_x");
-    for (int l = 0; l < g.L; ++l) {
-        const float *Wf = theta + offs[6 * l], *Rf = theta + offs[6 * l + 1], *bf = theta + offs[6 * l + 2];
-        const float *Wb = theta + offs[6 * l + 3], *Rb = theta + offs[6 * l + 4], *bb = theta + offs[6 * l + 5];
-        TRY(pack_w(Wf, Wb, g.Drows[l], g.H, Hq, 2, g.Dn[l], g.rowmode[l], (__half *)(ws + w.w16[l]), st), "pack_w");
-        TRY(pack_rt(Rf, Rb, g.H, Hq, 2, (__half *)(ws + w.rt16[l]), st), "pack_rt");
-        TRY(pack_bias(bf, bb, g.H, Hq, 2, (float *)(ws + w.bq[l]), st), "pack_bias");
+    if (g.L <= PACK_MAXL) {  // the operand copies of every layer: three launches
+        PackLayers pk{};
+        pk.L = g.L; pk.H = g.H; pk.Hq = Hq;
+        for (int l = 0; l < g.L; ++l) {
+            for (int dd = 0; dd < 2; ++dd) {
+                pk.W[l][dd] = theta + offs[6 * l + 3 * dd];
+                pk.R[l][dd] = theta + offs[6 * l + 3 * dd + 1];
+                pk.b[l][dd] = theta + offs[6 * l + 3 * dd + 2];
+            }
+            pk.Drows[l] = g.Drows[l]; pk.Dn[l] = g.Dn[l]; pk.rowmode[l] = g.rowmode[l];
+            pk.W16[l] = (__half *)(ws + w.w16[l]); pk.RT16[l] = (__half *)(ws + w.rt16[l]);
+            pk.bq[l] = (float *)(ws + w.bq[l]);
+        }
+        TRY(pack_layers(pk, st), "pack_layers");
+    } else {
+        for (int l = 0; l < g.L; ++l) {
+            const float *Wf = theta + offs[6 * l], *Rf = theta + offs[6 * l + 1], *bf = theta + offs[6 * l + 2];
+            const float *Wb = theta + offs[6 * l + 3], *Rb = theta + offs[6 * l + 4], *bb = theta + offs[6 * l + 5];
+            TRY(pack_w(Wf, Wb, g.Drows[l], g.H, Hq, 2, g.Dn[l], g.rowmode[l], (__half *)(ws + w.w16[l]), st), "pack_w");
+            TRY(pack_rt(Rf, Rb, g.H, Hq, 2, (__half *)(ws + w.rt16[l]), st), "pack_rt");
+            TRY(pack_bias(bf, bb, g.H, Hq, 2, (float *)(ws + w.bq[l]), st), "pack_bias");
+        }
     }
     float *Z = (float *)(ws + w.Z);
     uint8_t *maskN = ws + w.maskN;  // shared by every layer, forward and BPTT

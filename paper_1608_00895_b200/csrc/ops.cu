@@ -186,6 +186,68 @@ int pack_bias(const float *b0, const float *b1, int H, int Hq, int ndir, float *
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
+// --- every layer's pack_w / pack_rt / pack_bias in one launch each (the step's preamble was
+// 3L launch-bound kernels of a few us each) ------------------------------------------------------
+__global__ void pack_w_all_kernel(PackLayers a) {
+    const int r = blockIdx.y, l = blockIdx.z >> 1, d = blockIdx.z & 1;
+    if (r >= a.Dn[l]) return;
+    const int H = a.H, Hq = a.Hq;
+    const int sr = src_row(r, a.Drows[l], H, Hq, a.rowmode[l]);
+    const float *W = a.W[l][d];
+    __half *out = a.W16[l] + (long)r * 2 * 4 * Hq + (long)d * 4 * Hq;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < Hq; j += gridDim.x * blockDim.x) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (sr >= 0 && j < H) {
+#pragma unroll
+            for (int gam = 0; gam < 4; ++gam) v[gam] = W[(long)sr * 4 * H + gam * H + j];
+        }
+        __half2 lo = __floats2half2_rn(v[0], v[1]), hi = __floats2half2_rn(v[2], v[3]);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t *>(&lo);
+        pk.y = *reinterpret_cast<uint32_t *>(&hi);
+        *reinterpret_cast<uint2 *>(out + 4 * j) = pk;
+    }
+}
+__global__ void __launch_bounds__(256) pack_rt_all_kernel(PackLayers a) {
+    __shared__ float tile[4][32][33];
+    const int H = a.H, Hq = a.Hq;
+    const int k0 = blockIdx.x * 32, j0 = blockIdx.y * 32, l = blockIdx.z >> 1, d = blockIdx.z & 1;
+    const float *R = a.R[l][d];
+    __half *RT16 = a.RT16[l];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int kk = ty; kk < 32; kk += 8) {
+        const int k = k0 + kk, j = j0 + tx;
+#pragma unroll
+        for (int gam = 0; gam < 4; ++gam)
+            tile[gam][kk][tx] = (k < H && j < H) ? R[(long)k * 4 * H + gam * H + j] : 0.f;
+    }
+    __syncthreads();
+    for (int rr = ty; rr < 128; rr += 8) {
+        const int jj = rr >> 2, gam = rr & 3;
+        RT16[((long)d * 4 * Hq + 4 * (j0 + jj) + gam) * Hq + k0 + tx] = __float2half_rn(tile[gam][tx][jj]);
+    }
+}
+__global__ void pack_bias_all_kernel(PackLayers a) {
+    const int Hq = a.Hq, H = a.H, per = 2 * 4 * Hq;
+    const long n = (long)a.L * per;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int l = (int)(e / per), i = (int)(e - (long)l * per);
+        const int d = i / (4 * Hq), qq = i - d * 4 * Hq, j = qq >> 2, gam = qq & 3;
+        a.bq[l][i] = j < H ? a.b[l][d][gam * H + j] : 0.f;
+    }
+}
+int pack_layers(const PackLayers &a, cudaStream_t st) {
+    if (a.L < 1 || a.L > PACK_MAXL) return -3;
+    ProfScope ps_(PROF_OTHER, st);
+    int maxDn = 0;
+    for (int l = 0; l < a.L; ++l) maxDn = a.Dn[l] > maxDn ? a.Dn[l] : maxDn;
+    pack_w_all_kernel<<<dim3((a.Hq + 255) / 256, maxDn, 2 * a.L), 256, 0, st>>>(a);
+    pack_rt_all_kernel<<<dim3(a.Hq / 32, a.Hq / 32, 2 * a.L), 256, 0, st>>>(a);
+    pack_bias_all_kernel<<<grid_for((long)a.L * 8 * a.Hq), 256, 0, st>>>(a);
+    note_launch(3);
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 // --- head weights: W_out [2H, K] -> Wo16 [2Hq, Kp] (rows = padded [fwd | bwd] halves) --------
 __global__ void pack_wout_kernel(const float *__restrict__ Wo, const float *__restrict__ bo, int H, int Hq, int K,
                                  int Kp, __half *__restrict__ Wo16, float *__restrict__ boq) {

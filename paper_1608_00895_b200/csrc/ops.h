@@ -26,6 +26,17 @@ int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir,
            cudaStream_t st);
 int pack_rt(const float *R0, const float *R1, int H, int Hq, int ndir, __half *RT16, cudaStream_t st);
 int pack_bias(const float *b0, const float *b1, int H, int Hq, int ndir, float *bq, cudaStream_t st);
+// every layer of a bidirectional stack at once (pack_w, pack_rt, pack_bias of each layer, both
+// directions): three launches
+constexpr int PACK_MAXL = 16;
+struct PackLayers {
+    int L, H, Hq;
+    const float *W[PACK_MAXL][2], *R[PACK_MAXL][2], *b[PACK_MAXL][2];
+    int Drows[PACK_MAXL], Dn[PACK_MAXL], rowmode[PACK_MAXL];
+    __half *W16[PACK_MAXL], *RT16[PACK_MAXL];
+    float *bq[PACK_MAXL];
+};
+int pack_layers(const PackLayers &a, cudaStream_t st);
 int pack_wout(const float *Wo, const float *bo, int H, int Hq, int K, int Kp, __half *Wo16, float *boq,
               cudaStream_t st);
 int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int ndir, int dir0, cudaStream_t st);
