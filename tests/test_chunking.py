@@ -59,3 +59,22 @@ def test_make_batches():
     assert data.make_batches(chunks, 2, seed=7) == bs
     assert sorted((c.seq, c.start) for b in bs for c in b) == sorted((c.seq, c.start) for c in chunks)
     assert data.chunk_frames(bs) == 5          # conservation
+
+
+def test_gather_chunks_golden():
+    """Pin of oracle.chunking.gather_chunks (an off-by-one in seq_offset or a label written at
+    padding fails): the hand-written batch of tests/golden/chunk_gather.txt."""
+    rows = [list(map(float, ln.split())) for ln in open(os.path.join(os.path.dirname(__file__), "golden",
+                                                                    "chunk_gather.txt"))
+            if ln.strip() and not ln.startswith("#")]
+    T, B, D = 4, 5, 2
+    exp = np.array(rows)[:, 1:].reshape(T, B, 4)
+    frames = np.array([[f + 1, -(f + 1)] for f in range(8)], np.float32)
+    flabels = np.arange(10, 18, dtype=np.int32)
+    seq_offset = [0, 5, 8]
+    chunks = [(s, a, n) for s, L in enumerate((5, 3)) for a, n in ref.chunk_starts(L, 4, 2)]
+    assert chunks == [(0, 0, 4), (0, 2, 3), (0, 4, 1), (1, 0, 3), (1, 2, 1)]
+    x, mask, labels = ref.gather_chunks(frames, flabels, seq_offset, chunks, T)
+    assert np.array_equal(x, exp[..., :D].astype(np.float32))
+    assert np.array_equal(mask, exp[..., 2].astype(np.uint8))
+    assert np.array_equal(labels, exp[..., 3].astype(np.int32))

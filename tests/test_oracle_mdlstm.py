@@ -177,3 +177,45 @@ def test_four_directions_are_flipped_runs():
     f = oracle.mdlstm_fwd(x[::-1, ::-1].copy(), mask, *params[3], False)
     assert np.allclose(y[..., 3 * H:], f["h"][::-1, ::-1], rtol=0, atol=1e-14)
     assert np.allclose(y[..., :H], oracle.mdlstm_fwd(x, mask, *params[0], False)["h"], rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("stable", [False, True])
+def test_multidir_bwd_central_fd(stable):
+    """Pin of oracle.mdlstm_multidir_bwd (the flips of dy into each direction's frame and of dx
+    back out, and the sum of dx over directions): central finite differences of
+    L = sum(y * dy) through all four directions, for dx and every direction's
+    (W, Ru, Rv, b), on a non-square grid with an irregular mask so that a wrong flip fails."""
+    g = np.random.default_rng(8)
+    U, V, B, D, H = 3, 2, 2, 2, 2
+    params = [_params(g, D, H) for _ in range(4)]
+    x = g.standard_normal((U, V, B, D))
+    mask = np.ones((U, V, B)); mask[2, 1, 0] = 0; mask[2, :, 1] = 0; mask[1, 1, 1] = 0
+    dy = g.standard_normal((U, V, B, 4 * H))
+
+    def loss(x=x, params=params):
+        y, _ = oracle.mdlstm_multidir(x, mask, params, stable)
+        return np.sum(y * dy)
+    _, fwds = oracle.mdlstm_multidir(x, mask, params, stable)
+    dx, grads = oracle.mdlstm_multidir_bwd(x, mask, params, fwds, dy, stable)
+    eps = 1e-5
+
+    def rel(fd, an):
+        return np.max(np.abs(fd - an) / np.maximum(1e-7, np.abs(fd) + np.abs(an)))
+    fd = np.zeros_like(x)
+    for i in np.ndindex(x.shape):
+        p = x.copy(); p[i] += eps
+        m = x.copy(); m[i] -= eps
+        fd[i] = (loss(x=p) - loss(x=m)) / (2 * eps)
+    worst = rel(fd, dx)
+    assert np.any(dx != 0)
+    for k in range(4):
+        for q in range(4):
+            base = params[k][q]
+            fd = np.zeros_like(base)
+            for i in np.ndindex(base.shape):
+                pp = [list(t) for t in params]; pm = [list(t) for t in params]
+                a = base.copy(); a[i] += eps; pp[k][q] = a
+                a = base.copy(); a[i] -= eps; pm[k][q] = a
+                fd[i] = (loss(params=pp) - loss(params=pm)) / (2 * eps)
+            worst = max(worst, rel(fd, grads[k][q]))
+    assert worst <= 1e-5, worst
