@@ -374,10 +374,20 @@ static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
     }
     return 0;
 }
-// Z GEMM -> recurrence completion counters: [L][2 directions][M-tiles]
-// Z GEMM completion counters [L][2][M tiles], then one BPTT "CTAs started" counter per layer
+// Z GEMM completion counters [L][2 directions][M tiles], then one BPTT "CTAs started" counter per
+// layer, then two start-arbitration words per layer (forward recurrence vs its Z GEMM, common.cuh)
 static size_t zflag_words(const StackGeo &g) {
-    return (size_t)g.L * 2 * ((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS) + g.L;
+    return (size_t)g.L * 2 * ((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS) + 3 * g.L;
+}
+// true when something may serialize kernels or withhold SMs from a concurrent launch: a profiler
+// or sanitizer injected into the process (ncu, compute-sanitizer: CUDA_INJECTION64_PATH),
+// CUDA_LAUNCH_BLOCKING=1, or an MPS SM cap.  The Z-GEMM overlap is then not attempted at all
+// (the start arbitration would also keep it correct, after a 20 ms wait per layer).
+static bool serialized_env() {
+    const char *inj = getenv("CUDA_INJECTION64_PATH");
+    const char *lb = getenv("CUDA_LAUNCH_BLOCKING");
+    const char *mps = getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE");
+    return (inj && *inj) || (lb && atoi(lb) != 0) || (mps && *mps);
 }
 static StackWS stack_ws(const StackGeo &g) {
     Carve c;
@@ -514,7 +524,9 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     // BLSTM_OVERLAP=0 disables it: profilers that serialize or replay kernels one at a time (ncu)
     // would otherwise leave the recurrence waiting for a GEMM that cannot run beside it.
     const int side_ctas = num_sms() - 2 * g.pl.G * g.pl.NC;
-    static const bool overlap_env = !(getenv("BLSTM_OVERLAP") && atoi(getenv("BLSTM_OVERLAP")) == 0);
+    // BLSTM_OVERLAP=0: never; =2: even in a serialized environment (tests of the arbitration)
+    static const int overlap_mode = getenv("BLSTM_OVERLAP") ? atoi(getenv("BLSTM_OVERLAP")) : 1;
+    static const bool overlap_env = overlap_mode == 2 || (overlap_mode != 0 && !serialized_env());
     const bool overlap = overlap_env && side_ctas >= 8 && !g.step;
     if (overlap && gemm_prepare()) return fail(BLSTM_ERR_CUDA, "gemm_prepare");
     for (int l = 0; l < g.L; ++l) {
@@ -558,14 +570,27 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         else { p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq; }
         p.gates = (__half *)(ws + w.gates[l]); p.ldg = 8L * Hq;
         p.hist = hist;
-        p.counters = (uint32_t *)(ws + w.cnt);        if (overlap) {  // the pair is timed as one forward-recurrence scope (prof_suspend)
+        p.counters = (uint32_t *)(ws + w.cnt);
+        if (overlap) {  // the three launches are timed as one forward-recurrence scope (prof_suspend)
+            // start arbitration (common.cuh): the recurrence goes ahead only once every GEMM CTA is
+            // resident; otherwise it exits and the conditional re-launch after the GEMM runs it
+            static const int arb_mode = getenv("BLSTM_ARB") ? atoi(getenv("BLSTM_ARB")) : 3;  // A/B: bit 0 arb, bit 1 rerun
+            uint32_t *arb = zflags + zflag_words(g) - 2 * g.L + 2 * l;
+            gp.arb = (arb_mode & 1) ? arb : nullptr;
+            p.arb = (arb_mode & 1) ? arb : nullptr;
+            p.arb_target = (uint32_t)gemm_grid((int)g.TB, 8 * Hq, 0, side_ctas);
+            RecParams p2 = p;
+            p2.arb = nullptr;
+            p2.rerun = arb;
             ProfScope ps(PROF_REC_FWD, st);
             prof_suspend(1);
             const int rc1 = lstm_rec_fwd(p, (const __half *)(ws + w.rt16[l]), st);
             const int rc2 = rc1 ? 0 : gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gp, side_ctas, st);
+            const int rc3 = (rc1 || rc2 || !(arb_mode & 2)) ? 0 : lstm_rec_fwd(p2, (const __half *)(ws + w.rt16[l]), st);
             prof_suspend(0);
             TRY(rc1, "lstm_rec_fwd");
             TRY(rc2, "gemm Z");
+            TRY(rc3, "lstm_rec_fwd (conditional re-launch)");
         } else {
             TRY(lstm_rec_fwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_fwd");
         }
@@ -634,7 +659,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     const int rec_ctas = 2 * g.pl.G * g.pl.NC;
     const bool bucket_update = opt && !(opt->max_norm > 0.0);
     // per-layer BPTT start counters (zeroed with the Z flags by stack_forward)
-    uint32_t *bstarted = (uint32_t *)(ws + w.zflags) + (zflag_words(g) - g.L);
+    uint32_t *bstarted = (uint32_t *)(ws + w.zflags) + (zflag_words(g) - 3 * g.L);
     // Side-stream work that overlaps BPTT(l) must not take SMs before BPTT(l)'s clusters are all
     // placed: GEMM CTAs dispatched first spread over every GPC, no GPC keeps 16 free SMs and the
     // BPTT waits for the whole GEMM (measured: 0.98 instead of 0.63 ms per layer).  Both become

@@ -463,4 +463,33 @@ DEVI void red_release_gpu_add(uint32_t *p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Start arbitration between a persistent consumer and the concurrent producer it spins on (the
+// forward recurrence and its Z GEMM, launched as a programmatic dependent: PDL lets the GEMM start
+// early but does not guarantee it -- a profiler that serializes kernels, CUDA_LAUNCH_BLOCKING, an
+// MPS SM cap or a co-tenant can keep it off the GPU until the consumer exits).  Two words per
+// launch pair, zeroed before it: arb[0] counts resident producer CTAs (each adds 1 at entry),
+// arb[1] is the decision, set once by compare-and-swap: ARB_GO by a consumer CTA that saw every
+// producer CTA resident (count == target), ARB_ABORT by one that waited ARB_TIMEOUT_NS without
+// seeing it.  Every consumer CTA follows the one decision: an aborted consumer exits at once and
+// a conditional re-launch after the producer does the work (api.cu stack_forward).
+// (A compare-and-swap loop on a single word by the 52 producer CTAs cost ~20 us per launch.)
+// ---------------------------------------------------------------------------
+constexpr uint32_t ARB_GO = 1u, ARB_ABORT = 2u;
+constexpr uint64_t ARB_TIMEOUT_NS = 20ull * 1000 * 1000;
+DEVI void arb_checkin(uint32_t *arb) { red_release_gpu_add(arb, 1u); }  // producer CTA, one thread
+DEVI bool arb_decide(uint32_t *arb, uint32_t target) {  // consumer CTA, one thread: true = go
+    const uint64_t t0 = globaltimer_ns();
+    for (;;) {
+        uint32_t d = ld_acquire_gpu(arb + 1);
+        if (d == 0) {
+            if (ld_acquire_gpu(arb) >= target) d = atomicCAS(arb + 1, 0u, ARB_GO);
+            else if (globaltimer_ns() - t0 > ARB_TIMEOUT_NS) d = atomicCAS(arb + 1, 0u, ARB_ABORT);
+            else { __nanosleep(128); continue; }
+            if (d == 0) d = ld_acquire_gpu(arb + 1);  // our CAS won: re-read the word we wrote
+        }
+        return d == ARB_GO;
+    }
+}
+
 }  // namespace blstm

@@ -95,6 +95,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         fence_mbar_init();
     }
+    if (p.arb) {  // resident (common.cuh); the conditional re-launch of the recurrence may launch
+        if (threadIdx.x == 64) arb_checkin(p.arb);
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
     if (warp == 1) {
         tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
         tmem_relinquish();
@@ -430,6 +434,13 @@ __global__ void splitk_reduce_kernel(const float *__restrict__ part, int S, long
         float *dst = C + m * ldc + c;
         *dst = beta ? *dst + v : v;
     }
+}
+
+int gemm_grid(int M, int N, int bn, int max_ctas) {
+    const int BN = bn == 128 ? 128 : gemm_bn(N);
+    if (max_ctas <= 0) max_ctas = num_sms();
+    const int tiles = ((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN);
+    return tiles < max_ctas ? (tiles < 1 ? 1 : tiles) : max_ctas;
 }
 
 // C = alpha * op(A) op(B)^T (+C) (+bias).  Returns 0 / negative error.

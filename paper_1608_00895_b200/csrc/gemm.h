@@ -31,6 +31,9 @@ struct GemmParams {
     // launch as a programmatic dependent of the previous kernel in the stream (which triggers it
     // once all its CTAs are resident: lstm_rec_fwd), so the GEMM runs beside it on the free SMs
     int pdl = 0;
+    // != nullptr (with pdl): the start-arbitration word shared with the recurrence (common.cuh
+    // arb_checkin); every CTA checks in at entry
+    uint32_t *arb = nullptr;
     // != nullptr: split-K scratch (fp32, splitk_elems floats).  GEMMs with few output tiles and a long
     // K (the weight gradients, K = T*B) split K over idle SMs; partial tiles land in the scratch and
     // a fixed-order reduction writes C (deterministic).
@@ -60,6 +63,8 @@ struct GemmParams {
 constexpr int GEMM_BM_ROWS = 128;           // M tile
 inline int gemm_bn(int N) { return N > 128 ? 256 : 128; }  // N tile chosen by gemm_f16
 
+// CTAs of a launch of gemm_f16 without split-K (e.g. the flagged Z GEMM): the arbitration target
+int gemm_grid(int M, int N, int bn, int max_ctas);
 int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &p, int max_ctas, cudaStream_t st);
 // load + configure the GEMM kernels now: with lazy module loading the first launch of a kernel
 // synchronizes the context, which must not happen while a recurrence waits on that GEMM (pdl)

@@ -169,6 +169,13 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     uint64_t *bars = (uint64_t *)(smem + fwd_region0(Hq, N));
     uint32_t *tslot = (uint32_t *)(bars + 8);
 
+    // the conditional re-launch after an aborted start (RecParams::rerun), a programmatic dependent
+    // of the Z GEMM: wait for the GEMM grid (and through its own wait, the primary recurrence) to
+    // complete, then a uniform early exit unless the primary aborted
+    if (p.rerun) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (*(volatile const uint32_t *)(p.rerun + 1) != ARB_ABORT) return;
+    }
     // this CTA is resident: a programmatically dependent launch (the concurrent Z GEMM, gemm.h pdl)
     // may start on the SMs left free once every CTA of this grid got here
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -284,11 +291,25 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             zfront += dir;
         }
     };
-    if (zf && threadIdx.x == ZPOLL && T > 0) {
-        z_wait(dir > 0 ? 0 : T - 1);
-        if (T > 1) z_wait(dir > 0 ? 1 : T - 2);
+    uint32_t *go = tslot + 1;  // the start arbitration's decision (RecParams::arb), CTA-wide
+    if (threadIdx.x == ZPOLL) {
+        const bool ok = p.arb ? arb_decide(p.arb, p.arb_target) : true;
+        *go = ok ? 1u : 0u;
+        if (ok && zf && T > 0) {
+            z_wait(dir > 0 ? 0 : T - 1);
+            if (T > 1) z_wait(dir > 0 ? 1 : T - 2);
+        }
     }
     cluster_sync();  // every CTA done with its R staging before peers write into hbuf / stg
+    if (*go == 0) {  // the Z GEMM never became resident: the re-launch after it does the layer
+        tc_fence_before();
+        __syncthreads();
+        if (w == 0) {
+            tc_fence_after();
+            tmem_dealloc2(tmem, TCOLS);
+        }
+        return;
+    }
 
     float c_st[NMQ], h_st[NMQ];
 #pragma unroll
@@ -965,7 +986,7 @@ RecPlan rec_plan(int T, int B, int H, int ndir, int sms) {
     return pl;
 }
 
-static size_t fwd_smem(const RecPlan &pl) { return fwd_region0(pl.Hq, pl.N) + 1024 + 64; }
+static size_t fwd_smem(const RecPlan &pl) { return fwd_region0(pl.Hq, pl.N) + 1024 + 128; }
 // per-step input rings of the BPTT kernel (see IN_SLOT / cring there)
 static size_t bwd_in_bytes(int N) { return 2 * ((size_t)N * 128 + 512 * (N / 4) * 2 + 1024) + 3 * (size_t)N * 128; }
 static size_t bwd_smem(const RecPlan &pl) {
@@ -987,7 +1008,8 @@ size_t rec_P_bytes(const RecPlan &pl) {
 }
 
 template <typename Kern, typename... Args>
-static cudaError_t launch_cluster(Kern kern, int grid, int cluster, size_t smem, cudaStream_t st, Args... args) {
+static cudaError_t launch_cluster_ex(Kern kern, int grid, int cluster, size_t smem, cudaStream_t st, bool pdl,
+                                     Args... args) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (cluster > 8) {
@@ -999,14 +1021,20 @@ static cudaError_t launch_cluster(Kern kern, int grid, int cluster, size_t smem,
     cfg.blockDim = dim3(REC_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cluster;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+template <typename Kern, typename... Args>
+static cudaError_t launch_cluster(Kern kern, int grid, int cluster, size_t smem, cudaStream_t st, Args... args) {
+    return launch_cluster_ex(kern, grid, cluster, smem, st, false, args...);
 }
 
 static unsigned long long *g_trace_fwd = nullptr, *g_trace_bwd = nullptr;
@@ -1029,9 +1057,9 @@ int lstm_rec_fwd(const RecParams &p_in, const __half *RT16, cudaStream_t st) {
     note_launch();
     cudaError_t e;
     switch (p.N) {
-        case 16: e = launch_cluster(lstm_rec_fwd_kernel<1>, grid, p.NC, smem, st, tmR, p); break;
-        case 32: e = launch_cluster(lstm_rec_fwd_kernel<2>, grid, p.NC, smem, st, tmR, p); break;
-        case 64: e = launch_cluster(lstm_rec_fwd_kernel<4>, grid, p.NC, smem, st, tmR, p); break;
+        case 16: e = launch_cluster_ex(lstm_rec_fwd_kernel<1>, grid, p.NC, smem, st, p.rerun != nullptr, tmR, p); break;
+        case 32: e = launch_cluster_ex(lstm_rec_fwd_kernel<2>, grid, p.NC, smem, st, p.rerun != nullptr, tmR, p); break;
+        case 64: e = launch_cluster_ex(lstm_rec_fwd_kernel<4>, grid, p.NC, smem, st, p.rerun != nullptr, tmR, p); break;
         default: return -6;
     }
     return e == cudaSuccess ? 0 : -5;

@@ -54,6 +54,13 @@ struct RecParams {
     // != nullptr (BPTT): each CTA adds 1 at entry, so a side-stream kernel can hold back work
     // that would otherwise take SMs before every recurrence cluster is placed (wait_count)
     uint32_t *started;
+    // forward overlapped with its Z GEMM (common.cuh arb_decide): != nullptr in the primary launch,
+    // which goes ahead only once all arb_target GEMM CTAs are resident and otherwise exits at once;
+    // rerun != nullptr (a second launch, a programmatic dependent of the GEMM): wait for the GEMM
+    // grid, then exit unless that word carries the abort bit, else run the layer (Z complete)
+    uint32_t *arb;
+    uint32_t arb_target;
+    const uint32_t *rerun;
     unsigned long long *trace;   // debug: per-step phase timestamps of CTA 0 / thread 0, or nullptr
 };
 
