@@ -251,6 +251,25 @@ def run_reference(args, cfg):
 # ----------------------------------------------------------------------------
 # the CUDA path
 # ----------------------------------------------------------------------------
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a launcher: re-run this script under torchrun with N ranks on
+    this node (127.0.0.1), the launch the driver uses.  Fails loudly when the node has fewer than N
+    GPUs rather than timing fewer."""
+    import socket
+    if args.impl == "cuda":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} requested but this node has {have} GPU(s)")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -267,6 +286,11 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = synth.CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)  # one process per GPU (the driver's torchrun launch, done here)
+    _, _, world = rank_env()
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     if args.impl == "reference":
         return run_reference(args, cfg)
 

@@ -267,6 +267,15 @@ int dp_allreduce_grads(dp_comm *c, float *grad, size_t n, void *stream);
 int dp_average_params(dp_comm *c, float *theta, size_t n, void *stream);
 int dp_comm_destroy(dp_comm *c);
 /*
+ * The sync-mode exchange buckets of blstm_stack_fwd_bwd / blstm_stack_train_step (host-only,
+ * no device work): [lo[i], hi[i]) of theta's layout, in the order the step issues the bucket
+ * allreduces (and, in blstm_stack_train_step, the bucket updates): the head (K > 0) first,
+ * then layer L-1 down to layer 0, each as soon as its gradients are final.
+ * The buckets partition [0, blstm_param_count).  lo, hi: HOST arrays of max_buckets >= L + 1
+ * entries.  Returns the bucket count, or BLSTM_ERR_ARG.
+ */
+int blstm_dp_buckets(const blstm_stack_desc *d, size_t *lo, size_t *hi, int max_buckets);
+/*
  * N replicas resident on ONE device (a single-GPU simulation of N workers, SURVEY.md §8(f)
  * NEXT-1): x_r <- scale * sum_{q<n} x_q for every r < n, summed in replica order 0..n-1 in
  * fp32, so all replicas receive identical bits.  scale = 1/n is the paper's parameter

@@ -81,6 +81,8 @@ _SIGS = {
     "dp_allreduce_grads": (_i, [_vp, _vp, _sz, _vp]),
     "dp_average_params": (_i, [_vp, _vp, _sz, _vp]),
     "dp_comm_destroy": (_i, [_vp]),
+    "blstm_dp_buckets": (_i, [ctypes.POINTER(StackDesc), ctypes.POINTER(ctypes.c_size_t),
+                              ctypes.POINTER(ctypes.c_size_t), _i]),
     "mdlstm_param_count": (_sz, [ctypes.POINTER(MdDesc)]),
     "mdlstm_workspace_bytes": (_sz, [ctypes.POINTER(MdDesc)]),
     "mdlstm_reserve_bytes": (_sz, [ctypes.POINTER(MdDesc)]),
@@ -289,6 +291,16 @@ def dp_comm_init(nranks: int, rank: int, uid: bytes):
 
 def dp_allreduce_grads(comm, grad, stream=None):
     _check("dp_allreduce_grads", lib().dp_allreduce_grads(comm, _p(grad), grad.numel(), _stream(stream)))
+
+
+def blstm_dp_buckets(desc: StackDesc):
+    """[(lo, hi)] of the step's exchange buckets, in issue order (host-only)."""
+    n = desc.L + 1
+    lo, hi = (ctypes.c_size_t * n)(), (ctypes.c_size_t * n)()
+    k = lib().blstm_dp_buckets(ctypes.byref(desc), lo, hi, n)
+    if k < 0:
+        raise BlstmError("blstm_dp_buckets", k, last_error())
+    return [(int(lo[i]), int(hi[i])) for i in range(k)]
 
 
 def dp_average_params(comm, theta, stream=None):

@@ -462,6 +462,27 @@ static size_t param_layout(const blstm_stack_desc *d, size_t *offs) {
     return o;
 }
 
+// The sync-mode exchange buckets of one step, in the order stack_step_impl issues them: the head
+// [offs[6L], P) first (when K > 0), then layer L-1 down to layer 0, layer l = [offs[6l], next).
+// They partition [0, P).  Returns the bucket count (<= L + 1).
+static int dp_buckets(const blstm_stack_desc *d, size_t *lo, size_t *hi) {
+    std::vector<size_t> offs(6 * d->L + 2);
+    const size_t n = param_layout(d, offs.data());
+    int k = 0;
+    if (d->K > 0) { lo[k] = offs[6 * d->L]; hi[k] = n; ++k; }
+    for (int l = d->L - 1; l >= 0; --l) {
+        lo[k] = offs[6 * l];
+        hi[k] = l + 1 < d->L ? offs[6 * (l + 1)] : offs[6 * d->L];
+        ++k;
+    }
+    return k;
+}
+extern "C" int blstm_dp_buckets(const blstm_stack_desc *d, size_t *lo, size_t *hi, int max_buckets) {
+    if (!d || d->L < 1 || d->H < 1 || d->D < 1 || d->K < 0 || !lo || !hi) return fail(BLSTM_ERR_ARG, "bad argument");
+    if (max_buckets < d->L + (d->K > 0 ? 1 : 0)) return fail(BLSTM_ERR_ARG, "need room for %d buckets", d->L + 1);
+    return dp_buckets(d, lo, hi);
+}
+
 extern "C" size_t blstm_param_count(const blstm_stack_desc *d) {
     if (!d || d->L < 1 || d->H < 1 || d->D < 1 || d->K < 0) return 0;
     return param_layout(d, nullptr);
@@ -658,6 +679,10 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     const bool overlap = side != st;
     const int rec_ctas = 2 * g.pl.G * g.pl.NC;
     const bool bucket_update = opt && !(opt->max_norm > 0.0);
+    // exchange / update buckets (dp_buckets): index 0 = head (K > 0), then layers L-1 .. 0
+    std::vector<size_t> blo(g.L + 1), bhi(g.L + 1);
+    dp_buckets(d, blo.data(), bhi.data());
+    const int bhead = g.K > 0 ? 1 : 0;
     // per-layer BPTT start counters (zeroed with the Z flags by stack_forward)
     uint32_t *bstarted = (uint32_t *)(ws + w.zflags) + (zflag_words(g) - 3 * g.L);
     // Side-stream work that overlaps BPTT(l) must not take SMs before BPTT(l)'s clusters are all
@@ -730,10 +755,10 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
         TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
         if (comm) {  // sync-mode exchange of this bucket (the head), overlapping the BPTT below
-            if (int rc = dp_allreduce_grads_impl(comm, grad + offs[6 * g.L], nparam - offs[6 * g.L], side)) return rc;
+            if (int rc = dp_allreduce_grads_impl(comm, grad + blo[0], bhi[0] - blo[0], side)) return rc;
         }
         if (bucket_update)  // the head's parameters are final: update them now (NEXT-3, fused)
-            if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, offs[6 * g.L], nparam, 1, nullptr, side))
+            if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, blo[0], bhi[0], 1, nullptr, side))
                 return rc;
         return 0;
     };
@@ -769,12 +794,12 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
             TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, ss), "scatter dR");
             TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.step ? 1 : g.pl.G, dd, ss), "scatter db");
         }
-        const size_t end = l + 1 < g.L ? offs[6 * (l + 1)] : offs[6 * g.L];
+        const size_t b0 = blo[bhead + g.L - 1 - l], b1 = bhi[bhead + g.L - 1 - l];  // layer l's bucket
         if (comm) {  // sync-mode exchange of layer l's bucket (§4.1), overlapping BPTT
-            if (int rc = dp_allreduce_grads_impl(comm, grad + offs[6 * l], end - offs[6 * l], ss)) return rc;
+            if (int rc = dp_allreduce_grads_impl(comm, grad + b0, b1 - b0, ss)) return rc;
         }
         if (bucket_update)  // layer l's parameters are final: update them while BPTT continues below
-            if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, offs[6 * l], end, 1, nullptr, ss))
+            if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, b0, b1, 1, nullptr, ss))
                 return rc;
         if (overlap) cudaEventRecord(evs[g.L + 2 + l], ss);
         return 0;

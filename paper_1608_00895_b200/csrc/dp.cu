@@ -12,6 +12,8 @@
 
 #include "blstm.h"
 
+// A 1-rank communicator runs the same NCCL calls (an in-place copy; the average divides by 1):
+// the path is exercised by a one-GPU test bit for bit against comm = NULL.
 struct dp_comm {
     ncclComm_t comm;
     int nranks, rank;
@@ -53,7 +55,6 @@ extern "C" int dp_comm_init(int nranks, int rank, const unsigned char id[128], d
 
 int dp_allreduce_grads_impl(dp_comm *c, float *grad, size_t n, cudaStream_t st) {
     if (!c || !grad) return BLSTM_ERR_ARG;
-    if (c->nranks == 1) return 0;
     ncclResult_t r = ncclAllReduce(grad, grad, n, ncclFloat32, ncclSum, c->comm, st);
     return r == ncclSuccess ? 0 : nccl_fail(r, "ncclAllReduce(sum)");
 }
@@ -64,7 +65,6 @@ extern "C" int dp_allreduce_grads(dp_comm *c, float *grad, size_t n, void *strea
 
 extern "C" int dp_average_params(dp_comm *c, float *theta, size_t n, void *stream) {
     if (!c || !theta) return BLSTM_ERR_ARG;
-    if (c->nranks == 1) return 0;
     ncclResult_t r = ncclAllReduce(theta, theta, n, ncclFloat32, ncclAvg, c->comm, (cudaStream_t)stream);
     return r == ncclSuccess ? 0 : nccl_fail(r, "ncclAllReduce(avg)");
 }

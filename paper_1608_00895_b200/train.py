@@ -67,13 +67,11 @@ class NcclCollective(Collective):
 
     def sum_(self, t):
         from . import blstm
-        if self.world > 1:
-            blstm.dp_allreduce_grads(self.comm, t)
+        blstm.dp_allreduce_grads(self.comm, t)
 
     def mean_(self, t):
         from . import blstm
-        if self.world > 1:
-            blstm.dp_average_params(self.comm, t)
+        blstm.dp_average_params(self.comm, t)
 
 
 @dataclass
@@ -104,6 +102,20 @@ def dp_step(theta, grad, compute_grad: Callable[[object, object], None], update:
         coll.sum_(grad)
     update(theta, grad)
     if sched.average_after(step_index):
+        coll.mean_(theta)
+
+
+def fused_dp_step(step_fn: Callable[[bool], None], theta, coll: Optional[Collective], sched: DPSchedule,
+                  step_index: int):
+    """The schedule of one rank's step with the update inside the library step
+    (blstm_stack_train_step; StackTrainer's default path).
+
+    step_fn(sum_grads) runs fwd + BPTT + update of this rank; with sum_grads the gradient is
+    SUMmed over ranks inside the step, bucket by bucket in blstm_dp_buckets order, before each
+    bucket's update (sync mode).  In avg(K) mode the step is local and the parameters are
+    averaged after every K-th step."""
+    step_fn(sched.grads_summed())
+    if sched.average_after(step_index) and coll is not None:
         coll.mean_(theta)
 
 
@@ -222,18 +234,19 @@ class StackTrainer:
         self.steps_done += 1
 
     def _fused_step(self):
-        """dp_step's schedule with the update inside the library step (blstm_stack_train_step)."""
+        """fused_dp_step's schedule with the update inside the library step (blstm_stack_train_step)."""
         if self.dropout > 0:
             self.desc.dropout_seed = (self.dropout_seed + self.steps_done) & 0xFFFFFFFF
         self.opt_steps += 1
         P = (self.blstm.opt_params("sgd", self.lr) if self.opt is None
              else self.blstm.opt_params(step=self.opt_steps, **self.opt))
-        comm = self.comm if (self.comm is not None and self.sched.grads_summed()) else None
-        self.blstm.blstm_stack_train_step(self.desc, self.theta, self.grad, self.x, self.mask, self.labels,
-                                          self.dy_top, self.loss, self.ferr, comm, P, self.opt_state, self.ws,
-                                          s_side=self.side)
-        if self.sched.average_after(self.steps_done) and self.coll is not None:
-            self.coll.mean_(self.theta)
+
+        def step_fn(sum_grads):
+            comm = self.comm if (self.comm is not None and sum_grads) else None
+            self.blstm.blstm_stack_train_step(self.desc, self.theta, self.grad, self.x, self.mask, self.labels,
+                                              self.dy_top, self.loss, self.ferr, comm, P, self.opt_state, self.ws,
+                                              s_side=self.side)
+        fused_dp_step(step_fn, self.theta, self.coll, self.sched, self.steps_done)
 
 
 def dp_comm_from_torch(rank: int, world: int):
