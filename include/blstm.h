@@ -12,7 +12,10 @@
  *     (§5: "time ... as first, the batch index as second and
  *     the layer output size as third dimension").  Floating tensors are fp32.
  *   - The mask is the paper's index tensor: uint8 [T, B], 1 = real
- *     frame, 0 = padding.  Any 0/1 pattern is accepted (nonzero reads as 1).  At
+ *     frame, 0 = padding.  Any 0/1 pattern is accepted.  An entry outside {0,1}
+ *     is detected on device and reported lazily: the first call
+ *     after the kernel that saw it has completed returns BLSTM_ERR_ARG (or
+ *     blstm_check_errors() does); that launch read it as 1.  At
  *     a masked frame the LSTM state (h, c) is carried unchanged, the output is 0
  *     and the backward pass emits zero gate gradient (R2/R4).
  *   - LSTM variant (paper silent, R1): no peepholes, gate blocks
@@ -60,6 +63,10 @@ typedef enum {
 const char *blstm_last_error(void);
 /* ABI version (major*100 + minor). */
 int blstm_version(void);
+/* Errors detected by kernels of completed earlier calls (a mask entry outside {0,1}): returns
+   BLSTM_ERR_ARG once per detection and clears it, else BLSTM_OK.  Synchronize the stream first to
+   see the calls issued on it. */
+int blstm_check_errors(void);
 
 /* ------------------------------------------------------------------------ */
 /* One LSTM layer, one direction: PAPER.md §4.2 P:232-236.                   */

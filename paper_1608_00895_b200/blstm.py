@@ -60,6 +60,7 @@ _i = ctypes.c_int
 _SIGS = {
     "blstm_last_error": (ctypes.c_char_p, []),
     "blstm_version": (_i, []),
+    "blstm_check_errors": (_i, []),
     "lstm_workspace_bytes": (_sz, [ctypes.POINTER(LstmDesc)]),
     "lstm_reserve_bytes": (_sz, [ctypes.POINTER(LstmDesc)]),
     "lstm_fwd": (_i, [ctypes.POINTER(LstmDesc)] + [_vp] * 13 + [_sz, _vp]),
@@ -145,6 +146,11 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def blstm_check_errors():
+    """Raises BlstmError if a kernel of a completed earlier call saw a mask entry outside {0,1}."""
+    _check("blstm_check_errors", lib().blstm_check_errors())
 
 
 def last_error() -> str:

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <vector>
 
 #include "blstm.h"
@@ -41,6 +42,13 @@ static int fail(int code, const char *fmt, ...) {
 extern "C" const char *blstm_last_error(void) { return g_err; }
 int blstm_set_error(int code, const char *msg) { return fail(code, "%s", msg); }
 extern "C" int blstm_version(void) { return 100; }
+
+// blstm.h: a mask entry outside {0,1} is detected on device (pack_mask / check_mask) and reported
+// lazily: by the first API call after the kernel that saw it has completed, or by blstm_check_errors.
+static int mask_pending() {
+    return mask_flag_take() ? fail(BLSTM_ERR_ARG, "a mask entry outside {0,1} was passed to an earlier call") : 0;
+}
+extern "C" int blstm_check_errors(void) { return mask_pending(); }
 
 static inline size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 struct Carve {
@@ -173,6 +181,7 @@ static RecParams base_params(const LayerGeo &g, int ndir, int dir0, const uint8_
 extern "C" int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask, const float *W, const float *R,
                         const float *b, const float *h0, const float *c0, float *y, float *c, float *hT, float *cT,
                         void *reserve, void *workspace, size_t workspace_bytes, void *stream) {
+    if (int rc = mask_pending()) return rc;
     LayerGeo g;
     if (int rc = layer_geo(d, g)) return rc;
     if (!x || !mask || !W || !R || !b || !y || !c || !reserve || !workspace)
@@ -211,6 +220,7 @@ extern "C" int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask,
         q.gates = (__half *)(res + rv.gates);
         q.hist = hist;
         q.h0 = h0; q.c0 = c0; q.hT = hT; q.cT = cT;
+        TRY(check_mask(mask, g.TB, st), "check_mask");
         TRY(rec_step_fwd(q, st), "rec_step_fwd");
         return 0;
     }
@@ -234,6 +244,7 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
                         const float *dhT, const float *dcT, float *dx, float *dW, float *dR, float *db, float *dh0,
                         float *dc0, void *workspace, size_t workspace_bytes, void *stream) {
     (void)h0;  // h0 enters through the saved history (reserve)
+    if (int rc = mask_pending()) return rc;
     LayerGeo g;
     if (int rc = layer_geo(d, g)) return rc;
     const bool want_dx = !(d->flags & BLSTM_NO_DX);
@@ -272,6 +283,7 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
         q.dhc = sb + rec_step_bwd_partial_floats(g.B, g.Hq);
         q.dcc = q.dhc + 2L * g.B * g.Hq;
         q.c0 = c0; q.dhT = dhT; q.dcT = dcT; q.dh0 = dh0; q.dc0 = dc0;
+        TRY(check_mask(mask, g.TB, st), "check_mask");
         TRY(rec_step_bwd(q, st), "rec_step_bwd");
         if (cudaMemsetAsync(dbp, 0, (size_t)4 * g.Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
         TRY(colsum_f16_add(dA, g.TB, 4 * g.Hq, 4L * g.Hq, 1.f / (float)(1 << DA_SHIFT), dbp, (float *)(ws + w.cs2), st),
@@ -534,6 +546,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     float *Z = (float *)(ws + w.Z);
     uint8_t *maskN = ws + w.maskN;  // shared by every layer, forward and BPTT
     if (!g.step) TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
+    else TRY(check_mask(mask, g.TB, st), "check_mask");
     const int num_m = (int)((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS);
     uint32_t *zflags = (uint32_t *)(ws + w.zflags);
     if (cudaMemsetAsync(zflags, 0, zflag_words(g) * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset zflags");
@@ -629,6 +642,7 @@ static int check_stack_ptrs(const StackWS &w, const float *theta, const float *x
 
 extern "C" int blstm_stack_fwd(const blstm_stack_desc *d, const float *theta, const float *x, const uint8_t *mask,
                                float *Y, float *C, void *workspace, size_t workspace_bytes, void *stream) {
+    if (int rc = mask_pending()) return rc;
     StackGeo g;
     if (int rc = stack_geo(d, g)) return rc;
     const StackWS w = stack_ws(g);
@@ -649,6 +663,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
                            const uint8_t *mask, const int32_t *labels, const float *dy_top, double *loss_sum,
                            int32_t *frame_errors, dp_comm *comm, const blstm_opt_params *opt, float *opt_state,
                            void *workspace, size_t workspace_bytes, void *s_main, void *s_side) {
+    if (int rc = mask_pending()) return rc;
     StackGeo g;
     if (int rc = stack_geo(d, g)) return rc;
     const StackWS w = stack_ws(g);
@@ -704,7 +719,11 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
     // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch)
-    static thread_local std::vector<cudaEvent_t> evs;
+    // (per thread and per device: an event may only be recorded on a stream of its own device)
+    static thread_local std::map<int, std::vector<cudaEvent_t>> evs_by_dev;
+    int cur_dev = 0;
+    if (cudaGetDevice(&cur_dev) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "cudaGetDevice");
+    std::vector<cudaEvent_t> &evs = evs_by_dev[cur_dev];
     const int GSK_FREE = 2 * g.L + 2;
     if (overlap && evs.size() < 2 * (size_t)g.L + 3) {
         while (evs.size() < 2 * (size_t)g.L + 3) {
@@ -714,8 +733,8 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         }
     }
     if (overlap && g.K == 0) {  // the side stream may start only after everything issued so far on s_main
-        cudaEventRecord(evs[g.L + 1], st);
-        cudaStreamWaitEvent(side, evs[g.L + 1], 0);
+        TRY((int)cudaEventRecord(evs[g.L + 1], st), "cudaEventRecord");
+        TRY((int)cudaStreamWaitEvent(side, evs[g.L + 1], 0), "cudaStreamWaitEvent");
     }
     if (g.K > 0) {
         __half *wo16 = (__half *)(ws + w.wo16), *dlog = (__half *)(ws + w.dlog16);
@@ -731,7 +750,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         TRY(gemm_f16({dlog, g.Kp, 0}, {wo16, g.Kp, 0}, gd, 0, st), "gemm dY_top");
         if (g.dr.on) TRY(dropout_f32(dY[0], g.TB, g.H, Hq, g.L, g.dr, st), "dropout dY_top");
         // the head's parameter gradients are off the critical path too: side stream (side_head)
-        if (overlap) cudaEventRecord(evs[g.L + 1], st);
+        if (overlap) TRY((int)cudaEventRecord(evs[g.L + 1], st), "cudaEventRecord");
     } else {
         TRY(pad_halves(dy_top, g.H, Hq, g.TB, dY[0], st), "pad dy_top");
         if (cudaMemsetAsync(loss_sum, 0, sizeof(double), st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
@@ -746,12 +765,12 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         if (g.K == 0) return 0;
         __half *dlog = (__half *)(ws + w.dlog16);
         float *dWoT = (float *)(ws + w.dWoT);
-        if (overlap) cudaStreamWaitEvent(side, evs[g.L + 1], 0);
+        if (overlap) TRY((int)cudaStreamWaitEvent(side, evs[g.L + 1], 0), "cudaStreamWaitEvent");
         if (int rc = side_guard(g.L - 1)) return rc;
         GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
         gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
         TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
-        if (overlap) cudaEventRecord(evs[GSK_FREE], side);
+        if (overlap) TRY((int)cudaEventRecord(evs[GSK_FREE], side), "cudaEventRecord");
         TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
         TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
         if (comm) {  // sync-mode exchange of this bucket (the head), overlapping the BPTT below
@@ -769,11 +788,11 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         float *dWT = (float *)(ws + w.dWT) + (size_t)par * 8 * Hq * w.maxDn;
         float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
         const float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
-        if (overlap && ss == side) cudaStreamWaitEvent(side, evs[l], 0);
+        if (overlap && ss == side) TRY((int)cudaStreamWaitEvent(side, evs[l], 0), "cudaStreamWaitEvent");
         if (l > 0)  // overlaps BPTT(l-1)
             if (int rc = side_guard(l - 1)) return rc;
         // on s_main: the split-K scratch is shared with the side stream's GEMMs (the last layer's)
-        if (overlap && ss != side) cudaStreamWaitEvent(ss, evs[GSK_FREE], 0);
+        if (overlap && ss != side) TRY((int)cudaStreamWaitEvent(ss, evs[GSK_FREE], 0), "cudaStreamWaitEvent");
         const __half *X = l == 0 ? (const __half *)(ws + w.x16) : (const __half *)(ws + w.y16[l - 1]);
         // the last layer's weight gradients run after all BPTT work: every SM is free then
         const int wctas = l == 0 ? 0 : side_ctas;
@@ -787,7 +806,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
             gr.splitk_ws = (float *)(ws + w.gsk); gr.splitk_elems = GSK_ELEMS;
             TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, wctas, ss), "gemm dR");
         }
-        if (overlap && ss == side) cudaEventRecord(evs[GSK_FREE], side);
+        if (overlap && ss == side) TRY((int)cudaEventRecord(evs[GSK_FREE], side), "cudaEventRecord");
         for (int dd = 0; dd < 2; ++dd) {
             const int e = 6 * l + 3 * dd;
             TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], ss), "scatter dW");
@@ -801,7 +820,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         if (bucket_update)  // layer l's parameters are final: update them while BPTT continues below
             if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, b0, b1, 1, nullptr, ss))
                 return rc;
-        if (overlap) cudaEventRecord(evs[g.L + 2 + l], ss);
+        if (overlap) TRY((int)cudaEventRecord(evs[g.L + 2 + l], ss), "cudaEventRecord");
         return 0;
     };
     int cur = 0;
@@ -810,7 +829,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         __half *dA = (__half *)(ws + w.dA) + (size_t)par * g.TB * 8 * Hq;
         float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
         // layer l+2 used the same parity buffers: its side-stream GEMMs must be done reading them
-        if (overlap && l + 2 < g.L) cudaStreamWaitEvent(st, evs[g.L + 2 + l + 2], 0);
+        if (overlap && l + 2 < g.L) TRY((int)cudaStreamWaitEvent(st, evs[g.L + 2 + l + 2], 0), "cudaStreamWaitEvent");
         RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
         p.maskN = (const uint8_t *)(ws + w.maskN);  // packed by stack_forward
         p.C = (float *)(ws + w.C[l]); p.ldc = Hq; p.c_doff = g.TB * Hq;
@@ -850,7 +869,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
             // gradient of the undropped output of layer l-1 (site l)
             if (g.dr.on) TRY(dropout_f32(dY[1 - cur], g.TB, g.H, Hq, l, g.dr, st), "dropout dX");
         }
-        if (overlap) cudaEventRecord(evs[l], st);
+        if (overlap) TRY((int)cudaEventRecord(evs[l], st), "cudaEventRecord");
         cur = 1 - cur;
     }
     // layer 0's gradient work follows the last BPTT: on s_main it starts while the side stream
@@ -858,8 +877,8 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     // collectives, in bucket order)
     if (int rc = side_layer(0, (overlap && !comm) ? st : side)) return rc;
     if (overlap) {  // s_main's view: all gradient work of this call is complete
-        cudaEventRecord(evs[g.L], side);
-        cudaStreamWaitEvent(st, evs[g.L], 0);
+        TRY((int)cudaEventRecord(evs[g.L], side), "cudaEventRecord");
+        TRY((int)cudaStreamWaitEvent(st, evs[g.L], 0), "cudaStreamWaitEvent");
     }
     if (opt && !bucket_update)  // the global norm constraint needs every gradient: one update at the end
         if (int rc = opt_range(opt, d, (float *)theta, grad, opt_state, nparam, 0, nparam, 1, (double *)(ws + w.optp), st))

@@ -106,8 +106,10 @@ DEVI void xpose4(const float (&a)[4], float (&b)[4], int gam) {
     b[0] = v0; b[1] = v1; b[2] = v2; b[3] = v3;
 }
 
-// Gate nonlinearities in fp32 with the hardware exp2 (relative error ~1e-7, far inside the
-// fp16-operand budget; R9): sigmoid(z) = 1/(1+e^-z), tanh(z) = 2 sigmoid(2z) - 1.
+// Gate nonlinearities in fp32 with the hardware exp2 (R9): sigmoid(z) = 1/(1+e^-z) has
+// ~1e-7 relative error; tanh(z) = 2 sigmoid(2z) - 1 has ~1e-7 ABSOLUTE error (so up to ~1e-3
+// relative near |z| ~ 1e-4, where tanh itself is tiny).  Both are far inside the normwise fp16-operand
+// budget, which is what R10 measures.
 DEVI float sigm_f(float z) { return __fdividef(1.f, 1.f + __expf(-z)); }
 DEVI float tanh_f(float z) { return 2.f * sigm_f(2.f * z) - 1.f; }
 // activation of gate row gam (tanh for g, sigmoid otherwise) without lane divergence

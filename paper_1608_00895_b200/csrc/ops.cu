@@ -4,6 +4,7 @@
 // P:253-254), deterministic reductions, gradient scatter-add back to the flat
 // theta layout, and SGD (§4.3).  All grid-stride, coalesced on the
 // large side of each mapping.
+#include <algorithm>
 #include "common.cuh"
 #include "ops.h"
 #include "prof.h"
@@ -562,21 +563,64 @@ int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, 
 }
 
 // --- dy_top [rows, 2H] -> dY [rows, 2Hq] (padded halves) ------------------------------------
+// --- mask validation (blstm.h: an entry outside {0,1} -> BLSTM_ERR_ARG, read back lazily) ------
+// One flag per process in mapped pinned host memory: kernels that read the caller's mask OR 1 into
+// it on a bad byte; the host reads it at the next API call (mask_flag_take), after the kernel ran.
+static unsigned *g_mask_flag = nullptr;
+unsigned *mask_flag() {
+    if (!g_mask_flag) {
+        void *p = nullptr;
+        if (cudaHostAlloc(&p, 16, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+        *(volatile unsigned *)p = 0;
+        g_mask_flag = (unsigned *)p;
+    }
+    return g_mask_flag;
+}
+int mask_flag_take() {
+    if (!g_mask_flag || *(volatile unsigned *)g_mask_flag == 0) return 0;
+    *(volatile unsigned *)g_mask_flag = 0;
+    return 1;
+}
+
 __global__ void pack_mask_kernel(const uint8_t *__restrict__ mask, int T, int B, int G, int Bg, int N,
-                                 uint8_t *__restrict__ maskN) {
+                                 uint8_t *__restrict__ maskN, unsigned *err) {
     const long n = (long)T * G * N;
+    bool bad = false;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
         const long tg = i / N;
         const int c = (int)(i - tg * N), g = (int)(tg % G);
         const long t = tg / G;
         const int b = g * Bg + c;
-        maskN[i] = (c < Bg && b < B) ? mask[t * B + b] : 0;
+        const uint8_t v = (c < Bg && b < B) ? mask[t * B + b] : 0;
+        bad |= v > 1;
+        maskN[i] = v;
     }
+    if (bad && err) *(volatile unsigned *)err = 1u;
 }
 int pack_mask(const uint8_t *mask, int T, int B, int G, int Bg, int N, uint8_t *maskN, cudaStream_t st) {
     ProfScope ps_(PROF_OTHER, st);
     if (T == 0) return 0;
-    pack_mask_kernel<<<grid_for((long)T * G * N), 256, 0, st>>>(mask, T, B, G, Bg, N, maskN);
+    pack_mask_kernel<<<grid_for((long)T * G * N), 256, 0, st>>>(mask, T, B, G, Bg, N, maskN, mask_flag());
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
+__global__ void check_mask_kernel(const uint8_t *__restrict__ mask, long n, unsigned *err) {
+    bool bad = false;
+    const long n16 = n / 16;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n16; i += (long)gridDim.x * blockDim.x) {
+        const uint4 v = __ldg((const uint4 *)mask + i);
+        bad |= ((v.x | v.y | v.z | v.w) & 0xFEFEFEFEu) != 0;
+    }
+    for (long i = n16 * 16 + blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+        bad |= mask[i] > 1;
+    if (bad && err) *(volatile unsigned *)err = 1u;
+}
+int check_mask(const uint8_t *mask, long n, cudaStream_t st) {
+    ProfScope ps_(PROF_OTHER, st);
+    if (n <= 0) return 0;
+    const long work = (n + 15) / 16;
+    check_mask_kernel<<<(unsigned)std::min<long>((work + 255) / 256, 148 * 4), 256, 0, st>>>(mask, n, mask_flag());
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }

@@ -54,6 +54,10 @@ int scatter_wout(float *gWo, int H, int Hq, int K, const float *dWoT, long ldw, 
 // recurrence kernels' mask rows: maskN[(t*G + g)*N + n] = mask[t*B + g*Bg + n] for n < Bg,
 // g*Bg + n < B, else 0 (one N-byte row per step and batch group, bulk-copyable)
 int pack_mask(const uint8_t *mask, int T, int B, int G, int Bg, int N, uint8_t *maskN, cudaStream_t st);
+// mask entries outside {0,1}: pack_mask and check_mask set a process-wide flag (mapped host memory);
+// mask_flag_take() returns 1 (and clears it) if a kernel that has completed saw one
+int check_mask(const uint8_t *mask, long n, cudaStream_t st);
+int mask_flag_take();
 // dst[r*ldd + j] = src[r*lds + j] for j < cols (a row-strided copy into an aligned buffer)
 int copy_rows(const float *src, long lds, long rows, int cols, float *dst, long ldd, cudaStream_t st);
 int pad_halves(const float *src, int H, int Hq, long rows, float *dst, cudaStream_t st);

@@ -2,6 +2,9 @@
 and compare with the fp64 oracle.  Tolerances (BASELINE.json north_star, DESIGN.md
 R10): outputs and cell states normwise max|g-r|/max|r| <= 1e-3; gradients
 relative L2 <= 1e-2."""
+import json
+import os
+
 import numpy as np
 import torch
 
@@ -10,6 +13,19 @@ from paper_1608_00895_b200 import blstm
 
 OUT_TOL = 1e-3
 GRAD_TOL = 1e-2
+
+
+def record(case, errs, **extra):
+    """Append one parity record (per-tensor error magnitudes) as a JSON line to $BLSTM_PARITY_LOG,
+    when set.  The committed summaries under profiles/ (r02_parity_*.jsonl) come from this."""
+    path = os.environ.get("BLSTM_PARITY_LOG")
+    if not path:
+        return
+    rec = {"case": case, "errors": {(k if isinstance(k, str) else "/".join(map(str, k))): float(v)
+                                    for k, v in errs.items()}}
+    rec.update(extra)
+    with open(path, "a") as f:
+        f.write(json.dumps(rec) + "\n")
 
 
 def dev():
@@ -85,6 +101,7 @@ def oracle_layer(case, direction=1, with_state=True):
 def compare_layer(got, ref, label=""):
     errs = {k: norm_rel(got[k], ref[k]) for k in ("y", "c", "hT", "cT")}
     errs.update({k: l2_rel(got[k], ref[k]) for k in ("dx", "dW", "dR", "db", "dh0", "dc0")})
+    record(label, errs, metric={"y,c,hT,cT": "normwise", "rest": "rel-L2"})
     for k in ("y", "c", "hT", "cT"):
         assert errs[k] <= OUT_TOL, (label, k, errs)
     for k in ("dx", "dW", "dR", "db", "dh0", "dc0"):

@@ -20,7 +20,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU box
 
 import oracle  # noqa: E402
 from paper_1608_00895_b200 import synth  # noqa: E402
-from tests.gpu_util import GRAD_TOL, OUT_TOL, Stack, grad_errors, norm_rel  # noqa: E402
+from tests.gpu_util import GRAD_TOL, OUT_TOL, Stack, grad_errors, norm_rel, record  # noqa: E402
 
 SAMPLE = [5, 60]  # two chunks of the C3 batch (one full-length, one partial)
 
@@ -43,15 +43,17 @@ def test_c3_forward_sampled_chunks(c3):
     Y, C = st.forward(theta, batch)
     sub = _sub(batch, SAMPLE)
     ref = oracle.blstm_step(theta, sub.x, sub.mask, cfg.L, cfg.H, cfg.K, labels=sub.labels, want_states=True)
-    worst = 0.0
+    errs = {}
     for l in range(cfg.L):
         for d in range(2):
             y = Y[l][:, SAMPLE, d * cfg.H:(d + 1) * cfg.H]
             yr = ref["Ys"][l][..., d * cfg.H:(d + 1) * cfg.H]
-            e = max(norm_rel(y, yr), norm_rel(C[l, d][:, SAMPLE], ref["Cs"][l, d]))
-            worst = max(worst, e)
-            assert e <= OUT_TOL, (l, d, e)
+            errs[f"y[{l}][{d}]"] = norm_rel(y, yr)
+            errs[f"c[{l}][{d}]"] = norm_rel(C[l, d][:, SAMPLE], ref["Cs"][l, d])
+    record("C3 forward, full batch, chunks %s" % SAMPLE, errs, metric="normwise")
+    worst = max(errs.values())
     print(f"C3 forward, worst normwise error over layers/directions: {worst:.2e}")
+    assert worst <= OUT_TOL, errs
 
 
 def test_c3_training_step_masked_to_sample(c3):
@@ -66,5 +68,8 @@ def test_c3_training_step_masked_to_sample(c3):
     assert abs(got["loss"] - ref["loss"]) / abs(ref["loss"]) <= OUT_TOL
     assert got["frame_errors"] == ref["frame_errors"] or abs(got["frame_errors"] - ref["frame_errors"]) <= 2
     errs = grad_errors(got["grad"], ref["grad"], cfg.L, cfg.D, cfg.H, cfg.K)
+    record("C3 step masked to chunks %s" % SAMPLE, errs, metric="rel-L2",
+           loss_rel=abs(got["loss"] - ref["loss"]) / abs(ref["loss"]),
+           frame_errors=[got["frame_errors"], ref["frame_errors"]])
     print("C3 masked-sample step, worst gradient rel-L2:", max(errs.values()))
     assert max(errs.values()) <= GRAD_TOL, errs

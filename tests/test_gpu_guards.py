@@ -173,3 +173,41 @@ def test_mdlstm_reads_no_stale_workspace():
         out.append((y.cpu(), dx.cpu(), grad.cpu()))
     for a, b in zip(*out):
         assert torch.all(torch.isfinite(b)) and torch.equal(a, b)
+
+
+@pytest.mark.parametrize("force_step", [False, True])
+def test_mask_entry_outside_01_is_reported(force_step):
+    """blstm.h / SURVEY §8(b): a mask entry outside {0,1} -> BLSTM_ERR_ARG, detected on device and
+    reported by the next call (or blstm_check_errors) once the kernel that saw it has completed."""
+    if force_step:
+        os.environ["BLSTM_FORCE_STEP"] = "1"
+    try:
+        L, D, H, K, T, B = 1, 8, 32, 5, 6, 3
+        params = synth.stack_params(L, D, H, K)
+        batch = synth.speech_batch(T, B, D, K, np.array([6, 4, 2]), seed=1000)
+        theta = torch.tensor(oracle.pack_params(params, L, D, H, K), dtype=torch.float32, device="cuda:0")
+        desc = blstm.stack_desc(L, D, H, K, T, B)
+        ws = torch.empty(blstm.blstm_stack_workspace_bytes(desc), dtype=torch.uint8, device="cuda:0")
+        x = torch.tensor(batch.x, device="cuda:0")
+        Y = torch.zeros((L, T, B, 2 * H), device="cuda:0")
+        C = torch.zeros((L, 2, T, B, H), device="cuda:0")
+        good = torch.tensor(batch.mask, device="cuda:0")
+        blstm.blstm_stack_fwd(desc, theta, x, good, Y, C, ws)
+        torch.cuda.synchronize()
+        blstm.blstm_check_errors()  # clean so far
+        bad = good.clone()
+        bad[1, 0] = 2
+        blstm.blstm_stack_fwd(desc, theta, x, bad, Y, C, ws)  # the error is found on device ...
+        torch.cuda.synchronize()
+        with pytest.raises(blstm.BlstmError) as e:  # ... and reported by the next call
+            blstm.blstm_stack_fwd(desc, theta, x, good, Y, C, ws)
+        assert e.value.code == -1 and "outside {0,1}" in str(e.value)
+        blstm.blstm_stack_fwd(desc, theta, x, good, Y, C, ws)  # reported once, then clear
+        torch.cuda.synchronize()
+        blstm.blstm_check_errors()
+        blstm.blstm_stack_fwd(desc, theta, x, bad, Y, C, ws)
+        torch.cuda.synchronize()
+        with pytest.raises(blstm.BlstmError):
+            blstm.blstm_check_errors()
+    finally:
+        os.environ.pop("BLSTM_FORCE_STEP", None)
