@@ -283,6 +283,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dropout", type=float, default=0.0, help="input dropout of every layer (NEXT-4); 0 = off")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "fp16x2w"],
+                    help="tensor-core operand precision (blstm.h BLSTM_PREC_*)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = synth.CONFIGS[args.config]
@@ -308,7 +310,8 @@ def main():
     cfg, params, batch = synth.make_workload(cfg, rank)
     tr = StackTrainer(cfg, params, batch, dev, lr=args.lr, comm=comm, world=world,
                       sched=DPSchedule(args.dp_mode, args.avg_k if args.dp_mode == "avg" else 1),
-                      dropout=args.dropout, dropout_seed=7 + 1000 * rank)
+                      dropout=args.dropout, dropout_seed=7 + 1000 * rank,
+                      precision={"fp16": 0, "fp16x2w": 1}[args.precision])
 
     def barrier():
         torch.cuda.synchronize()
@@ -404,7 +407,8 @@ def main():
         "vs_baseline": None, "dtype": "f16 MMA operands / f32 accumulate+state", "data": "synthetic",
         "config": dict(workload_desc(cfg, world), valid_frames_per_gpu=V, dp_mode=args.dp_mode,
                        **({"avg_k": args.avg_k} if args.dp_mode == "avg" else {}),
-                       **({"input_dropout": args.dropout} if args.dropout > 0 else {})),
+                       **({"input_dropout": args.dropout} if args.dropout > 0 else {}),
+                       precision=args.precision),
         "roofline": roof,
         "kernel_ms_per_step": {cats[c]: prof[c][0] / args.steps for c in prof},
         "roofline_by_kernel": {cats[c]: kernel_roofline(c, prof[c][0], prof[c][1], cfg, tr.valid_frames, peaks, args.steps)

@@ -72,7 +72,15 @@ int blstm_check_errors(void);
 /* One LSTM layer, one direction: PAPER.md §4.2 P:232-236.                   */
 /* ------------------------------------------------------------------------ */
 enum { BLSTM_NO_DX = 4, BLSTM_ACCUM_DX = 2 };
-enum { BLSTM_PREC_FP16 = 0 };
+/* Precision of the tensor-core operands (R9; SURVEY §8(c) precision table):
+ *   BLSTM_PREC_FP16    fp16 operands (round to nearest), fp32 accumulation and state (default);
+ *   BLSTM_PREC_FP16X2W the input projection Z = x W + b (the a1 GEMM) with W split into
+ *                      W_hi = fp16(W) and W_lo = fp16(W - W_hi), Z = x W_hi + x W_lo in one GEMM over
+ *                      a doubled K: removes W's rounding, the dominant error term at small D
+ *                      (measured in profiles/r02_parity_*.jsonl); everything else as FP16.
+ * Other values (a 3-term split, TF32) return BLSTM_ERR_UNSUPPORTED: the remaining error is the
+ * recurrent h R product, whose split would triple the MMAs on the serial chain. */
+enum { BLSTM_PREC_FP16 = 0, BLSTM_PREC_FP16X2W = 1 };
 
 typedef struct {
     int T, B, D, H;   /* frames, batch, input width, hidden units; T >= 0, B, D, H >= 1 */
@@ -81,7 +89,7 @@ typedef struct {
     int ldx, ldy;     /* row strides (elements) of x/dx and of y/dy; ldx >= D, ldy >= H.  A BLSTM
                          direction writes its half of [T,B,2H] with ldy = 2H. */
     int flags;        /* BLSTM_NO_DX / BLSTM_ACCUM_DX (lstm_bwd only) */
-    int precision;    /* BLSTM_PREC_FP16 */
+    int precision;    /* BLSTM_PREC_FP16 or BLSTM_PREC_FP16X2W */
 } lstm_desc;
 
 /* Scratch bytes for one lstm_fwd / lstm_bwd call. */
@@ -127,7 +135,7 @@ typedef struct {
     int K;        /* classes of the softmax-CE head; 0 = no head, dy_top drives BPTT */
     int T, B;     /* frames, batch (chunks) */
     int flags;    /* reserved, 0 */
-    int precision;/* BLSTM_PREC_FP16 */
+    int precision;/* BLSTM_PREC_FP16 or BLSTM_PREC_FP16X2W */
     /* Input dropout of blstm_stack_fwd_bwd ("dropout on the layer inputs of any
      * layer"; R20): 0 <= dropout < 1 is the drop probability of every element of every
      * layer's input and of the head's input; dropout_seed selects the masks (a counter-based draw

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libblstm.so")
 BLSTM_NO_DX = 4
 BLSTM_ACCUM_DX = 2
 BLSTM_PREC_FP16 = 0
+BLSTM_PREC_FP16X2W = 1  # the input projection with W split hi + lo (blstm.h)
 
 _lib = None
 

@@ -77,7 +77,16 @@ struct LayerGeo {
     long TB;
     RecPlan pl;
     bool step = false;  // beyond the persistent kernels' capacity: step-launched recurrence (§5.7)
+    int x2w = 0;        // BLSTM_PREC_FP16X2W: the input projection with W split hi + lo (R9)
 };
+// precision modes (blstm.h): FP16, or FP16X2W (the a1 GEMM reads [W_hi; W_lo] along a doubled K)
+static int precision_x2w(int prec, int *x2w) {
+    if (prec == BLSTM_PREC_FP16 || prec == BLSTM_PREC_FP16X2W) {
+        *x2w = prec == BLSTM_PREC_FP16X2W;
+        return 0;
+    }
+    return fail(BLSTM_ERR_UNSUPPORTED, "precision %d not supported (FP16 = 0, FP16X2W = 1; DESIGN.md R9)", prec);
+}
 // split-K scratch of the weight-gradient GEMMs (GemmParams::splitk_ws): 32 MB
 constexpr long GSK_ELEMS = 8L << 20;
 
@@ -97,7 +106,7 @@ static int layer_geo(const lstm_desc *d, LayerGeo &g) {
         return fail(BLSTM_ERR_SHAPE, "need T>=0, B>=1, D>=1, H>=1 (got T=%d B=%d D=%d H=%d)", d->T, d->B, d->D, d->H);
     if (d->direction != 1 && d->direction != -1) return fail(BLSTM_ERR_ARG, "direction must be +1 or -1");
     if (d->ldx < d->D || d->ldy < d->H) return fail(BLSTM_ERR_SHAPE, "need ldx >= D and ldy >= H");
-    if (d->precision != BLSTM_PREC_FP16) return fail(BLSTM_ERR_UNSUPPORTED, "precision %d not supported", d->precision);
+    if (int rc = precision_x2w(d->precision, &g.x2w)) return rc;
     g.T = d->T; g.B = d->B; g.D = d->D; g.H = d->H;
     g.TB = (long)d->T * d->B;
     g.pl = rec_plan(d->T, d->B, d->H, 1, num_sms());
@@ -113,7 +122,7 @@ static FwdWS fwd_ws(const LayerGeo &g) {
     Carve c;
     FwdWS w;
     w.x16 = c.take((size_t)g.TB * g.Dp * 2);
-    w.w16 = c.take((size_t)g.Dp * 4 * g.Hq * 2);
+    w.w16 = c.take((size_t)(g.x2w ? 2 : 1) * g.Dp * 4 * g.Hq * 2);
     w.rt16 = c.take((size_t)4 * g.Hq * g.Hq * 2);
     w.bq = c.take((size_t)4 * g.Hq * 4);
     w.Z = c.take(g.step ? (size_t)g.TB * 4 * g.Hq * 4 : rec_native_elems(g.pl, g.T) * 4);
@@ -127,7 +136,7 @@ static BwdWS bwd_ws(const LayerGeo &g) {
     Carve c;
     BwdWS w;
     w.x16 = c.take((size_t)g.TB * g.Dp * 2);
-    w.w16 = c.take((size_t)g.Dp * 4 * g.Hq * 2);
+    w.w16 = c.take((size_t)(g.x2w ? 2 : 1) * g.Dp * 4 * g.Hq * 2);
     w.rt16 = c.take((size_t)4 * g.Hq * g.Hq * 2);
     w.dA = c.take((size_t)g.TB * 4 * g.Hq * 2);
     w.dX = c.take((size_t)g.TB * g.Dp * 4);
@@ -202,10 +211,11 @@ extern "C" int lstm_fwd(const lstm_desc *d, const float *x, const uint8_t *mask,
     __half *x16 = (__half *)(ws + w.x16), *w16 = (__half *)(ws + w.w16), *rt16 = (__half *)(ws + w.rt16);
     float *bq = (float *)(ws + w.bq), *Z = (float *)(ws + w.Z);
     TRY(cast_x_f16(x, d->ldx, g.D, x16, g.Dp, g.TB, st), "cast_x");
-    TRY(pack_w(W, nullptr, g.D, g.H, g.Hq, 1, g.Dp, 0, w16, st), "pack_w");
+    TRY(pack_w(W, nullptr, g.D, g.H, g.Hq, 1, g.Dp, 0, w16, st, g.x2w ? g.Dp : 0), "pack_w");
     TRY(pack_rt(R, nullptr, g.H, g.Hq, 1, rt16, st), "pack_rt");
     TRY(pack_bias(b, nullptr, g.H, g.Hq, 1, bq, st), "pack_bias");
-    GemmParams gp{(int)g.TB, 4 * g.Hq, g.Dp, Z, 4L * g.Hq, 1.f, 0, bq, 0, 0};
+    GemmParams gp{(int)g.TB, 4 * g.Hq, (g.x2w ? 2 : 1) * g.Dp, Z, 4L * g.Hq, 1.f, 0, bq, 0, 0};
+    gp.a_kwrap = g.x2w ? g.Dp / GEMM_BK_ELEMS : 0;
     if (!g.step) set_native(gp, g.pl, g.B);  // Z in the recurrence kernels' CTA-native layout
     TRY(gemm_f16({x16, g.Dp, 0}, {w16, 4L * g.Hq, 1}, gp, 0, st), "gemm Z");
     __half *hist = (__half *)(res + rv.hist);
@@ -350,6 +360,7 @@ struct StackGeo {
     // beyond the persistent kernels' on-chip capacity (e.g. H = 1024): step-launched recurrence
     // (rec_step.h); BLSTM_FORCE_STEP=1 selects it for any size (tests)
     bool step = false;
+    int x2w = 0;  // BLSTM_PREC_FP16X2W (LayerGeo::x2w)
 };
 struct StackWS {
     size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, gsk,
@@ -362,7 +373,7 @@ static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
     if (!d) return fail(BLSTM_ERR_ARG, "null blstm_stack_desc");
     if (d->L < 1 || d->D < 1 || d->H < 1 || d->K < 0 || d->T < 1 || d->B < 1)
         return fail(BLSTM_ERR_SHAPE, "need L,D,H,T,B >= 1 and K >= 0");
-    if (d->precision != BLSTM_PREC_FP16) return fail(BLSTM_ERR_UNSUPPORTED, "precision %d not supported", d->precision);
+    if (int rc = precision_x2w(d->precision, &g.x2w)) return rc;
     g.L = d->L; g.D = d->D; g.H = d->H; g.K = d->K; g.T = d->T; g.B = d->B;
     g.TB = (long)d->T * d->B;
     g.pl = rec_plan(d->T, d->B, d->H, 2, num_sms());
@@ -411,7 +422,7 @@ static StackWS stack_ws(const StackGeo &g) {
     w.x16 = c.take((size_t)TB * g.Dp0 * 2);
     for (int l = 0; l < g.L; ++l) {
         w.y16.push_back(c.take((size_t)TB * 2 * Hq * 2));
-        w.w16.push_back(c.take((size_t)g.Dn[l] * 8 * Hq * 2));
+        w.w16.push_back(c.take((size_t)(g.x2w ? 2 : 1) * g.Dn[l] * 8 * Hq * 2));
         w.rt16.push_back(c.take((size_t)2 * 4 * Hq * Hq * 2));
         w.bq.push_back(c.take((size_t)8 * Hq * 4));
         const size_t ge = g.step ? (size_t)TB * 8 * Hq : rec_native_elems(g.pl, g.T);
@@ -530,6 +541,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
                 pk.b[l][dd] = theta + offs[6 * l + 3 * dd + 2];
             }
             pk.Drows[l] = g.Drows[l]; pk.Dn[l] = g.Dn[l]; pk.rowmode[l] = g.rowmode[l];
+            pk.lo_rows[l] = g.x2w ? g.Dn[l] : 0;
             pk.W16[l] = (__half *)(ws + w.w16[l]); pk.RT16[l] = (__half *)(ws + w.rt16[l]);
             pk.bq[l] = (float *)(ws + w.bq[l]);
         }
@@ -538,7 +550,8 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         for (int l = 0; l < g.L; ++l) {
             const float *Wf = theta + offs[6 * l], *Rf = theta + offs[6 * l + 1], *bf = theta + offs[6 * l + 2];
             const float *Wb = theta + offs[6 * l + 3], *Rb = theta + offs[6 * l + 4], *bb = theta + offs[6 * l + 5];
-            TRY(pack_w(Wf, Wb, g.Drows[l], g.H, Hq, 2, g.Dn[l], g.rowmode[l], (__half *)(ws + w.w16[l]), st), "pack_w");
+            TRY(pack_w(Wf, Wb, g.Drows[l], g.H, Hq, 2, g.Dn[l], g.rowmode[l], (__half *)(ws + w.w16[l]), st,
+                       g.x2w ? g.Dn[l] : 0), "pack_w");
             TRY(pack_rt(Rf, Rb, g.H, Hq, 2, (__half *)(ws + w.rt16[l]), st), "pack_rt");
             TRY(pack_bias(bf, bb, g.H, Hq, 2, (float *)(ws + w.bq[l]), st), "pack_bias");
         }
@@ -569,7 +582,8 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
         const long lda = l == 0 ? g.Dp0 : 2L * Hq;
         if (g.step) {  // row-major Z, then one launch pair per time step (rec_step.h)
-            GemmParams gz{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
+            GemmParams gz{(int)g.TB, 8 * Hq, (g.x2w ? 2 : 1) * g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
+            gz.a_kwrap = g.x2w ? g.Dn[l] / GEMM_BK_ELEMS : 0;
             TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gz, 0, st), "gemm Z");
             __half *hist = (__half *)(ws + w.hist[l]);
             TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
@@ -586,7 +600,8 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
             TRY(rec_step_fwd(q, st), "rec_step_fwd");
             continue;
         }
-        GemmParams gp{(int)g.TB, 8 * Hq, g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
+        GemmParams gp{(int)g.TB, 8 * Hq, (g.x2w ? 2 : 1) * g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
+        gp.a_kwrap = g.x2w ? g.Dn[l] / GEMM_BK_ELEMS : 0;
         set_native(gp, g.pl, g.B);  // Z in the recurrence kernels' CTA-native layout
         gp.flags = zflags + (size_t)l * 2 * num_m;
         gp.flag_desc = 2;  // direction 1 (backward) reads time steps in descending order

@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
                     const int k0 = kb * GEMM_BK;
                     if (!p.a_mn) {
-                        tma_load_2d(sa, mA, &full[stage], k0, m0);
+                        const int ka = p.a_kwrap ? (kb % p.a_kwrap) * GEMM_BK : k0;
+                        tma_load_2d(sa, mA, &full[stage], ka, m0);
                     } else {
                         tma_load_2d(sa, mA, &full[stage], m0, k0);
                         tma_load_2d(sa + 8192, mA, &full[stage], m0 + 64, k0);
@@ -459,9 +460,11 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
                  (B.mn_major ? p.K % GEMM_BK : p.N % BN) || p.b_boff < (B.mn_major ? p.K : p.N)))
         return -3;
     const long bext = p.a2 ? p.b_boff : 0;  // extra extent of B's outer dimension
+    if (p.a_kwrap && (A.mn_major || p.a2 || p.K % (p.a_kwrap * GEMM_BK))) return -3;
+    const long ka_ext = p.a_kwrap ? (long)p.a_kwrap * GEMM_BK : p.K;  // A's K extent (zero fill beyond ld)
     CUtensorMap ta, tb, ta2;
     int rc;
-    if (!A.mn_major) rc = make_tmap_f16(&ta, A.ptr, p.K, p.M, A.ld, GEMM_BM);
+    if (!A.mn_major) rc = make_tmap_f16(&ta, A.ptr, ka_ext < A.ld ? ka_ext : A.ld, p.M, A.ld, GEMM_BM);
     else rc = make_tmap_f16(&ta, A.ptr, p.M, p.K, A.ld, GEMM_BK);
     if (rc) return rc;
     if (p.a2) {

@@ -58,9 +58,14 @@ struct GemmParams {
     // previous grid's completion before any load of its outputs or any store, then lets the next
     // kernel of the chain launch
     int pdl_chain = 0;
+    // > 0 (K-major A, single product): A is read with its K index wrapped modulo a_kwrap k-blocks
+    // (a_kwrap * 64 elements), so one launch computes A.[B_0; B_1; ...] over K = nseg * a_kwrap * 64
+    // with B's segments stacked along K -- BLSTM_PREC_FP16X2W's Z = X W_hi + X W_lo (R9)
+    int a_kwrap = 0;
 };
 
 constexpr int GEMM_BM_ROWS = 128;           // M tile
+constexpr int GEMM_BK_ELEMS = 64;           // K block (a_kwrap unit)
 inline int gemm_bn(int N) { return N > 128 ? 256 : 128; }  // N tile chosen by gemm_f16
 
 // CTAs of a launch of gemm_f16 without split-K (e.g. the flagged Z GEMM): the arbitration target

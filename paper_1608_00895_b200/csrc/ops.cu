@@ -113,30 +113,44 @@ DEVI int src_row(int r, int Drows, int H, int Hq, int rowmode) {
 // --- W_d [Drows, 4H] -> W16 [Dn, ndir*4Hq] with column 4j+gamma (+ d*4Hq) ------------------
 // one thread per (row, direction, unit j): the four gate reads are each coalesced across the warp
 // (consecutive j), the four fp16 results one 8-byte store
+// split_w (BLSTM_PREC_FP16X2W, R9): four fp32 gate values -> fp16 hi (round to nearest) and
+// lo = fp16(v - hi), so hi + lo carries ~22 bits of v
+DEVI void store_w4(__half *out, const float v[4], __half *out_lo) {
+    __half2 a = __floats2half2_rn(v[0], v[1]), b = __floats2half2_rn(v[2], v[3]);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t *>(&a);
+    pk.y = *reinterpret_cast<uint32_t *>(&b);
+    *reinterpret_cast<uint2 *>(out) = pk;
+    if (out_lo) {
+        const float2 fa = __half22float2(a), fb = __half22float2(b);
+        __half2 la = __floats2half2_rn(v[0] - fa.x, v[1] - fa.y), lb = __floats2half2_rn(v[2] - fb.x, v[3] - fb.y);
+        pk.x = *reinterpret_cast<uint32_t *>(&la);
+        pk.y = *reinterpret_cast<uint32_t *>(&lb);
+        *reinterpret_cast<uint2 *>(out_lo) = pk;
+    }
+}
+
 __global__ void pack_w_kernel(const float *__restrict__ W0, const float *__restrict__ W1, int Drows, int H, int Hq,
-                              int ndir, int Dn, int rowmode, __half *__restrict__ W16) {
+                              int ndir, int Dn, int rowmode, __half *__restrict__ W16, int lo_rows) {
     const int r = blockIdx.y, d = blockIdx.z;
     const int sr = src_row(r, Drows, H, Hq, rowmode);
     const float *W = d == 0 ? W0 : W1;
     __half *out = W16 + (long)r * ndir * 4 * Hq + (long)d * 4 * Hq;
+    __half *out_lo = lo_rows ? out + (long)lo_rows * ndir * 4 * Hq : nullptr;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < Hq; j += gridDim.x * blockDim.x) {
         float v[4] = {0.f, 0.f, 0.f, 0.f};
         if (sr >= 0 && j < H) {
 #pragma unroll
             for (int gam = 0; gam < 4; ++gam) v[gam] = W[(long)sr * 4 * H + gam * H + j];
         }
-        __half2 lo = __floats2half2_rn(v[0], v[1]), hi = __floats2half2_rn(v[2], v[3]);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t *>(&lo);
-        pk.y = *reinterpret_cast<uint32_t *>(&hi);
-        *reinterpret_cast<uint2 *>(out + 4 * j) = pk;
+        store_w4(out + 4 * j, v, out_lo ? out_lo + 4 * j : nullptr);
     }
 }
 int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir, int Dn, int rowmode, __half *W16,
-           cudaStream_t st) {
+           cudaStream_t st, int lo_rows) {
     ProfScope ps_(PROF_OTHER, st);
     dim3 grid((Hq + 255) / 256, Dn, ndir);
-    pack_w_kernel<<<grid, 256, 0, st>>>(W0, W1, Drows, H, Hq, ndir, Dn, rowmode, W16);
+    pack_w_kernel<<<grid, 256, 0, st>>>(W0, W1, Drows, H, Hq, ndir, Dn, rowmode, W16, lo_rows);
     note_launch();
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
@@ -196,17 +210,14 @@ __global__ void pack_w_all_kernel(PackLayers a) {
     const int sr = src_row(r, a.Drows[l], H, Hq, a.rowmode[l]);
     const float *W = a.W[l][d];
     __half *out = a.W16[l] + (long)r * 2 * 4 * Hq + (long)d * 4 * Hq;
+    __half *out_lo = a.lo_rows[l] ? out + (long)a.lo_rows[l] * 2 * 4 * Hq : nullptr;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < Hq; j += gridDim.x * blockDim.x) {
         float v[4] = {0.f, 0.f, 0.f, 0.f};
         if (sr >= 0 && j < H) {
 #pragma unroll
             for (int gam = 0; gam < 4; ++gam) v[gam] = W[(long)sr * 4 * H + gam * H + j];
         }
-        __half2 lo = __floats2half2_rn(v[0], v[1]), hi = __floats2half2_rn(v[2], v[3]);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t *>(&lo);
-        pk.y = *reinterpret_cast<uint32_t *>(&hi);
-        *reinterpret_cast<uint2 *>(out + 4 * j) = pk;
+        store_w4(out + 4 * j, v, out_lo ? out_lo + 4 * j : nullptr);
     }
 }
 __global__ void __launch_bounds__(256) pack_rt_all_kernel(PackLayers a) {

@@ -22,8 +22,10 @@ int dropout_f16(__half *y, long rows, int H, int Hq, int site, const Dropout &dr
 int dropout_f32(float *y, long rows, int H, int Hq, int site, const Dropout &dr, cudaStream_t st);
 // rowmode 0: input rows are W rows (rows >= Drows are padding); 1: input rows are the padded
 // [fwd (Hq) | bwd (Hq)] halves of the layer below (row half*Hq + jj <-> W row half*H + jj).
+// lo_rows > 0 (BLSTM_PREC_FP16X2W): also write lo = fp16(W - hi) at row r + lo_rows (W16 then has
+// 2 * lo_rows rows: [W_hi; W_lo] stacked along K)
 int pack_w(const float *W0, const float *W1, int Drows, int H, int Hq, int ndir, int Dn, int rowmode, __half *W16,
-           cudaStream_t st);
+           cudaStream_t st, int lo_rows = 0);
 int pack_rt(const float *R0, const float *R1, int H, int Hq, int ndir, __half *RT16, cudaStream_t st);
 int pack_bias(const float *b0, const float *b1, int H, int Hq, int ndir, float *bq, cudaStream_t st);
 // every layer of a bidirectional stack at once (pack_w, pack_rt, pack_bias of each layer, both
@@ -33,6 +35,7 @@ struct PackLayers {
     int L, H, Hq;
     const float *W[PACK_MAXL][2], *R[PACK_MAXL][2], *b[PACK_MAXL][2];
     int Drows[PACK_MAXL], Dn[PACK_MAXL], rowmode[PACK_MAXL];
+    int lo_rows[PACK_MAXL];  // > 0: W_lo rows at that offset (pack_w)
     __half *W16[PACK_MAXL], *RT16[PACK_MAXL];
     float *bq[PACK_MAXL];
 };

@@ -160,7 +160,7 @@ class StackTrainer:
 
     def __init__(self, cfg, params, batch, device, lr: float = 1e-5, comm=None, world: int = 1,
                  sched: Optional[DPSchedule] = None, opt: Optional[dict] = None, dropout: float = 0.0,
-                 dropout_seed: int = 0, fused: bool = True):
+                 dropout_seed: int = 0, fused: bool = True, precision: int = 0):
         """opt: None = plain SGD (sgd_update); else the update rule of blstm_opt_update, e.g.
         {"rule": "adam", "lr": 1e-3, "l2": 1e-4, "max_norm": 10.0} (§4.3)."""
         import torch
@@ -170,7 +170,7 @@ class StackTrainer:
         # input dropout: a fresh mask seed per step (dropout_seed + step index)
         self.dropout, self.dropout_seed = dropout, dropout_seed
         self.desc = blstm.stack_desc(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B, dropout=dropout,
-                                     dropout_seed=dropout_seed)
+                                     dropout_seed=dropout_seed, precision=precision)
         self.theta = torch.tensor(theta_from_params(params, self.desc), device=device)
         self.grad = torch.zeros_like(self.theta)
         self.ws = torch.empty(blstm.blstm_stack_workspace_bytes(self.desc), dtype=torch.uint8, device=device)

@@ -53,7 +53,7 @@ def l2_rel(g, r):
     return float(np.linalg.norm(g - r) / den) if den > 0 else float(np.linalg.norm(g))
 
 
-def run_layer(case, direction=1, with_state=True, ldx_pad=0, ldy_pad=0):
+def run_layer(case, direction=1, with_state=True, ldx_pad=0, ldy_pad=0, precision=0):
     """lstm_fwd + lstm_bwd through the ABI; returns numpy fp64 results."""
     x = case["x"].astype(np.float32)
     T, B, D = x.shape
@@ -61,7 +61,7 @@ def run_layer(case, direction=1, with_state=True, ldx_pad=0, ldy_pad=0):
     ldx, ldy = D + ldx_pad, H + ldy_pad
     xp = np.zeros((T, B, ldx), np.float32)
     xp[..., :D] = x
-    desc = blstm.lstm_desc(T, B, D, H, direction, ldx=ldx, ldy=ldy)
+    desc = blstm.lstm_desc(T, B, D, H, direction, ldx=ldx, ldy=ldy, precision=precision)
     ws = torch.zeros(blstm.lstm_workspace_bytes(desc), dtype=torch.uint8, device=dev())
     res = torch.zeros(blstm.lstm_reserve_bytes(desc), dtype=torch.uint8, device=dev())
     gx = T_(xp)
@@ -112,9 +112,9 @@ def compare_layer(got, ref, label=""):
 class Stack:
     """Device buffers + one call of blstm_stack_fwd_bwd / blstm_stack_fwd."""
 
-    def __init__(self, L, D, H, K, T, B, dropout=0.0, seed=0):
+    def __init__(self, L, D, H, K, T, B, dropout=0.0, seed=0, precision=0):
         self.L, self.D, self.H, self.K, self.T, self.B = L, D, H, K, T, B
-        self.desc = blstm.stack_desc(L, D, H, K, T, B, dropout=dropout, dropout_seed=seed)
+        self.desc = blstm.stack_desc(L, D, H, K, T, B, dropout=dropout, dropout_seed=seed, precision=precision)
         self.n, self.offs = blstm.blstm_param_offsets(self.desc)
         self.ws = torch.empty(blstm.blstm_stack_workspace_bytes(self.desc), dtype=torch.uint8, device=dev())
 

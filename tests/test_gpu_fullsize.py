@@ -37,9 +37,10 @@ def _sub(batch, idx):
                        labels=np.ascontiguousarray(batch.labels[:, idx]))
 
 
-def test_c3_forward_sampled_chunks(c3):
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp16", "fp16x2w"])
+def test_c3_forward_sampled_chunks(c3, precision):
     cfg, theta, batch = c3
-    st = Stack(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B)
+    st = Stack(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B, precision=precision)
     Y, C = st.forward(theta, batch)
     sub = _sub(batch, SAMPLE)
     ref = oracle.blstm_step(theta, sub.x, sub.mask, cfg.L, cfg.H, cfg.K, labels=sub.labels, want_states=True)
@@ -50,25 +51,26 @@ def test_c3_forward_sampled_chunks(c3):
             yr = ref["Ys"][l][..., d * cfg.H:(d + 1) * cfg.H]
             errs[f"y[{l}][{d}]"] = norm_rel(y, yr)
             errs[f"c[{l}][{d}]"] = norm_rel(C[l, d][:, SAMPLE], ref["Cs"][l, d])
-    record("C3 forward, full batch, chunks %s" % SAMPLE, errs, metric="normwise")
+    record("C3 forward, full batch, chunks %s, precision %d" % (SAMPLE, precision), errs, metric="normwise")
     worst = max(errs.values())
     print(f"C3 forward, worst normwise error over layers/directions: {worst:.2e}")
     assert worst <= OUT_TOL, errs
 
 
-def test_c3_training_step_masked_to_sample(c3):
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp16", "fp16x2w"])
+def test_c3_training_step_masked_to_sample(c3, precision):
     cfg, theta, batch = c3
     keep = np.zeros(cfg.B, bool)
     keep[SAMPLE] = True
     masked = synth.Batch(x=batch.x.copy(), mask=(batch.mask * keep[None, :]).astype(np.uint8),
                          labels=batch.labels.copy())
-    got = Stack(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B).step(theta, masked, side_stream=True)
+    got = Stack(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B, precision=precision).step(theta, masked, side_stream=True)
     sub = _sub(batch, SAMPLE)
     ref = oracle.blstm_step(theta, sub.x, sub.mask, cfg.L, cfg.H, cfg.K, labels=sub.labels)
     assert abs(got["loss"] - ref["loss"]) / abs(ref["loss"]) <= OUT_TOL
     assert got["frame_errors"] == ref["frame_errors"] or abs(got["frame_errors"] - ref["frame_errors"]) <= 2
     errs = grad_errors(got["grad"], ref["grad"], cfg.L, cfg.D, cfg.H, cfg.K)
-    record("C3 step masked to chunks %s" % SAMPLE, errs, metric="rel-L2",
+    record("C3 step masked to chunks %s, precision %d" % (SAMPLE, precision), errs, metric="rel-L2",
            loss_rel=abs(got["loss"] - ref["loss"]) / abs(ref["loss"]),
            frame_errors=[got["frame_errors"], ref["frame_errors"]])
     print("C3 masked-sample step, worst gradient rel-L2:", max(errs.values()))

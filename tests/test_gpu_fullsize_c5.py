@@ -38,9 +38,10 @@ def c5():
     return cfg, theta, batch, cols, [int(lens[c]) for c in cols], ref
 
 
-def test_c5_forward_longest_and_shortest_sequence(c5):
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp16", "fp16x2w"])
+def test_c5_forward_longest_and_shortest_sequence(c5, precision):
     cfg, theta, batch, cols, lens, ref = c5
-    Y, C = Stack(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B).forward(theta, batch)
+    Y, C = Stack(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B, precision=precision).forward(theta, batch)
     errs = {}
     for l in range(cfg.L):
         for d in range(2):
@@ -50,21 +51,22 @@ def test_c5_forward_longest_and_shortest_sequence(c5):
                 errs[f"y[{l}][{d}] T={n}"] = norm_rel(y, yr)
                 errs[f"c[{l}][{d}] T={n}"] = norm_rel(C[l, d][:n, [col]], ref["Cs"][l, d][:n, [j]])
             assert np.all(Y[l][lens[1]:, cols[1]] == 0)  # masked frames output 0
-    record("C5 forward, full batch, sequences T=%s" % lens, errs, metric="normwise")
+    record("C5 forward, full batch, sequences T=%s, precision %d" % (lens, precision), errs, metric="normwise")
     worst = max(errs.values())
     print(f"C5 forward, worst normwise error: {worst:.2e} (margin {OUT_TOL / worst:.2f}x)")
     assert worst <= OUT_TOL, errs
 
 
-def test_c5_training_step_masked_to_sample(c5):
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp16", "fp16x2w"])
+def test_c5_training_step_masked_to_sample(c5, precision):
     cfg, theta, batch, cols, lens, ref = c5
     keep = np.zeros(cfg.B, bool)
     keep[cols] = True
     masked = synth.Batch(x=batch.x.copy(), mask=(batch.mask * keep[None, :]).astype(np.uint8), labels=batch.labels.copy())
-    got = Stack(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B).step(theta, masked, side_stream=True)
+    got = Stack(cfg.L, cfg.D, cfg.H, cfg.K, cfg.T, cfg.B, precision=precision).step(theta, masked, side_stream=True)
     loss_rel = abs(got["loss"] - ref["loss"]) / abs(ref["loss"])
     errs = grad_errors(got["grad"], ref["grad"], cfg.L, cfg.D, cfg.H, cfg.K)
-    record("C5 step masked to sequences T=%s" % lens, errs, metric="rel-L2", loss_rel=loss_rel,
+    record("C5 step masked to sequences T=%s, precision %d" % (lens, precision), errs, metric="rel-L2", loss_rel=loss_rel,
            frame_errors=[got["frame_errors"], ref["frame_errors"]])
     print("C5 masked-sample step, worst gradient rel-L2:", max(errs.values()), "loss rel", loss_rel)
     assert loss_rel <= OUT_TOL

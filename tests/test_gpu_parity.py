@@ -110,9 +110,11 @@ def test_layer_all_masked_column_and_empty_frames():
         assert np.all(got["y"][:, 1] == 0) and np.all(got["dx"][:, 1] == 0)
 
 
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp16", "fp16x2w"])
 @pytest.mark.parametrize("direction", [1, -1])
-def test_layer_c2(direction):
-    """Config C2 (BASELINE.json configs[1]) per direction: H=500, D=40, B=32, T=500, masked."""
+def test_layer_c2(direction, precision):
+    """Config C2 (BASELINE.json configs[1]) per direction: H=500, D=40, B=32, T=500, masked; in both
+    precision modes (blstm.h BLSTM_PREC_*)."""
     cfg, params, batch = synth.make_workload(synth.CONFIGS["C2"])
     p = params.layers[0][0 if direction > 0 else 1]
     H = cfg.H
@@ -120,10 +122,10 @@ def test_layer_c2(direction):
     case = dict(x=batch.x, mask=batch.mask, W=p.W, R=p.R, b=p.b, h0=np.zeros((cfg.B, H), np.float32),
                 c0=np.zeros((cfg.B, H), np.float32), dy=np.ascontiguousarray(dy),
                 dhT=np.zeros((cfg.B, H), np.float32), dcT=np.zeros((cfg.B, H), np.float32))
-    got = run_layer(case, direction, with_state=False)
+    got = run_layer(case, direction, with_state=False, precision=precision)
     ref = oracle_layer(case, direction, with_state=False)
-    errs = compare_layer(got, ref, f"C2 dir={direction}")
-    print("C2 errors", direction, errs)
+    errs = compare_layer(got, ref, f"C2 dir={direction} precision={precision}")
+    print("C2 errors", direction, precision, errs)
 
 
 def test_layer_deterministic():
