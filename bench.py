@@ -102,25 +102,114 @@ def kernel_roofline(cat, total_ms, launches, cfg, V, peaks, steps):
             "alt": {"bound": "hbm", "achieved": a_gb, "peak": peaks["gbs"], "unit": "GB/s", "frac": f_gb}}
 
 
-def ncu_traffic(kernel_prefix):
-    """DRAM bytes (read + write) per launch of a kernel, from the newest committed ncu summary
-    (profiles/r*_ncu_v*.json, one `ncu --set full` capture; scripts/ncu_summarize.py), or None."""
+def ncu_traffic(kernel_prefix, config):
+    """DRAM bytes (read + write) per launch of a kernel category, averaged over the launches of one
+    `ncu --set full` capture of ONE training step of this config (scripts/ncu_step.py, summarised by
+    scripts/ncu_summarize.py --config into profiles/r*_ncu_*.json), newest round first; None when no
+    capture of this config exists."""
     import glob
     import re
-    files = glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_v*.json"))
-    key = lambda f: tuple(int(x) for x in re.findall(r"r(\d+)_ncu_v(\d+)", os.path.basename(f))[0])  # noqa: E731
-    for f in sorted(files, key=key, reverse=True):
+    files = glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_*.json"))
+    rnd = lambda f: int(re.findall(r"r(\d+)_", os.path.basename(f))[0])  # noqa: E731
+    for f in sorted(files, key=lambda f: (rnd(f), os.path.getmtime(f)), reverse=True):
         try:
             with open(f) as fh:
-                caps = json.load(fh).get("full_captures", {})
+                j = json.load(fh)
         except Exception:
             continue
-        for rep, ks in caps.items():
-            for k in ks:
-                if k["kernel"].startswith(kernel_prefix) and k.get("dram_read_unit") == "Mbyte":
-                    return {"bytes": (k["dram_read"] + k["dram_write"]) * 1e6,
-                            "source": f"{os.path.relpath(f, ROOT)} ({os.path.basename(rep)}, {k['kernel']})"}
+        if j.get("config") != config:
+            continue
+        for rep, ks in j.get("full_captures", {}).items():
+            sel = [k for k in ks if k["kernel"].startswith(kernel_prefix) and "dram_read" in k]
+            if not sel:
+                continue
+            scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = sum(k["dram_read"] * scale.get(k.get("dram_read_unit"), 1e6) +
+                      k["dram_write"] * scale.get(k.get("dram_write_unit"), 1e6) for k in sel)
+            return {"bytes": tot / len(sel), "launches": len(sel),
+                    "source": f"{os.path.relpath(f, ROOT)} ({os.path.basename(rep)}: {len(sel)} x {kernel_prefix})"}
     return None
+
+
+def gemm_shapes(cfg):
+    """(M, N, K) of every dense contraction of one training step as stack_step_impl launches them,
+    in the kernels' padded layouts (Hq = H rounded up to 256; Dn = D rounded up to 64
+    for layer 0, 2Hq above; Kp = K rounded up to 64)."""
+    rup = lambda a, b: (a + b - 1) // b * b  # noqa: E731
+    Hq = rup(cfg.H, 256)
+    TB = cfg.T * cfg.B
+    Kp = rup(cfg.K, 64) if cfg.K else 0
+    sh = []
+    for l in range(cfg.L):
+        Dn = rup(cfg.D, 64) if l == 0 else 2 * Hq
+        sh += [(TB, 8 * Hq, Dn), (8 * Hq, Dn, TB), (4 * Hq, Hq, TB), (4 * Hq, Hq, TB)]  # Z, dW^T, dR^T x 2
+        if l > 0:
+            sh.append((TB, Dn, 8 * Hq))  # dX
+    if cfg.K:
+        sh += [(TB, cfg.K, 2 * Hq), (TB, 2 * Hq, Kp), (cfg.K, 2 * Hq, TB)]  # logits, dY_top, dW_out^T
+    return sh
+
+
+def gemm_alg_bytes(cfg):
+    """algorithmic bytes of the step's GEMMs: fp16 A and B read once, fp32 C written once"""
+    return sum(2 * (M * K + N * K) + 4 * M * N for M, N, K in gemm_shapes(cfg))
+
+
+def step_floor(config):
+    """the per-timestep floor terms measured by scripts/step_floor.cu + scripts/dsmem_bench.cu
+    (profiles/r02_step_floor.json), or None"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_step_floor.json")) as f:
+            j = json.load(f)
+        return j.get(config)
+    except Exception:
+        return None
+
+
+def alg_bytes_per_frame(cfg):
+    """sum_l 2*4*(3 D_l + 13 H) + head 4*(4H + 2K)"""
+    b = sum(2 * 4 * (3 * (cfg.D if l == 0 else 2 * cfg.H) + 13 * cfg.H) for l in range(cfg.L))
+    if cfg.K:
+        b += 4 * (4 * cfg.H + 2 * cfg.K)
+    return b
+
+
+def crit_flops_per_frame(cfg):
+    """dense contractions on the dependency chain: Z of every layer, dX of layers
+    >= 1, and the head's logits and dY"""
+    f = z_flops_per_frame(cfg) + sum(2 * 8 * 2 * cfg.H * cfg.H for l in range(1, cfg.L))
+    if cfg.K:
+        f += 2 * 2 * (2 * cfg.H) * cfg.K
+    return f
+
+
+def step_roofline(cfg, V, peaks, t_measured_ms):
+    """T_roof = max(T_tc, T_hbm, T_crit), T_crit = F_crit / P_tc + N_steps * t_floor,
+    t_floor = max(t_mma + t_epi + t_xchg, bytes_step / BW) per direction pair and step; roofline
+    fraction = T_roof / T_measured."""
+    P, BW = peaks["tf"] * 1e12, peaks["gbs"] * 1e9
+    t_tc = V * alg_flops_per_frame(cfg) / P * 1e3
+    t_hbm = V * alg_bytes_per_frame(cfg) / BW * 1e3
+    t_gemm_crit = V * crit_flops_per_frame(cfg) / P * 1e3
+    fl = step_floor(cfg.name)
+    out = {"T_tc_ms": t_tc, "T_hbm_ms": t_hbm, "F_crit_over_P_tc_ms": t_gemm_crit, "T_measured_ms": t_measured_ms}
+    if fl:
+        bytes_step = 2 * (V / cfg.T) * 40 * cfg.H  # both directions' recurrence bytes per step (DESIGN.md 5.2)
+        t_hbm_step = bytes_step / BW * 1e9
+        tf_ = max(fl["t_mma_ns"] + fl["t_epi_fwd_ns"] + fl["t_xchg_ns"], t_hbm_step)
+        tb_ = max(fl["t_mma_ns"] + fl["t_epi_bwd_ns"] + fl["t_xchg_ns"], t_hbm_step)
+        n_steps = cfg.L * cfg.T
+        t_crit = t_gemm_crit + n_steps * (tf_ + tb_) / 1e6
+        t_roof = max(t_tc, t_hbm, t_crit)
+        out.update({"t_floor_fwd_ns": tf_, "t_floor_bwd_ns": tb_, "hbm_ns_per_step": t_hbm_step,
+                    "serial_steps": 2 * n_steps, "T_crit_ms": t_crit, "T_roof_ms": t_roof,
+                    "frac": t_roof / t_measured_ms, "floor_terms": fl,
+                    "bound": "latency (T_crit)" if t_roof == t_crit else ("tensor" if t_roof == t_tc else "hbm")})
+    else:
+        t_roof = max(t_tc, t_hbm, t_gemm_crit)
+        out.update({"T_roof_ms": t_roof, "frac": t_roof / t_measured_ms, "T_crit_ms": None,
+                    "note": f"no measured step floor for {cfg.name}: T_roof without the serial-step term"})
+    return out
 
 
 def measured_peaks():
@@ -205,7 +294,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 # the oracle, timed on the host cores (cpu_baseline / --impl reference)
 # ----------------------------------------------------------------------------
-def time_oracle(cfg, budget_s: float, rank: int = 0):
+def time_oracle(cfg, budget_s: float, rank: int = 0, single_thread: bool = False):
     """frames/s of the fp64 oracle on a bounded sample (b chunks) of the same workload."""
     import oracle
     _, params, batch = synth.make_workload(cfg, rank)
@@ -225,10 +314,32 @@ def time_oracle(cfg, budget_s: float, rank: int = 0):
     dt, _ = run(b, 8)                          # calibration: cost per frame-step
     T = int(np.clip(budget_s / max(dt / 8, 1e-6), 8, cfg.T))
     dt, fr = run(b, T)
-    return {"value": fr / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"one training step (fwd+BPTT+SGD, fp64) of {cfg.name} restricted to {b} of its "
-                      f"{cfg.B} chunks and their first {T} of {cfg.T} frames ({fr} valid frames) in "
-                      f"{dt:.1f} s; OpenMP over batch rows / output rows"}
+    res = {"value": fr / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+           "sample": f"one training step (fwd+BPTT+SGD, fp64) of {cfg.name} restricted to {b} of its "
+                     f"{cfg.B} chunks and their first {T} of {cfg.T} frames ({fr} valid frames) in "
+                     f"{dt:.1f} s; OpenMP over batch rows / output rows"}
+    if single_thread and cores > 1:  # the same oracle on one host thread (OMP_NUM_THREADS=1 equivalent)
+        lib = oracle.lib()
+        lib.omp_set_num_threads(1)
+        try:
+            d1, _ = run(1, 8)
+            T1 = int(np.clip(0.35 * budget_s / max(d1 / 8, 1e-6), 8, cfg.T))
+            d1, f1 = run(1, T1)
+        finally:
+            lib.omp_set_num_threads(cores)
+        res["single_thread"] = {"value": f1 / d1, "unit": UNIT, "cores": 1,
+                                "sample": f"1 chunk, its first {T1} frames ({f1} valid frames) in {d1:.1f} s"}
+    return res
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args, cfg):
@@ -389,17 +500,22 @@ def main():
     cats = {0: "lstm_rec_fwd", 1: "lstm_rec_bwd", 2: "gemm_f16 (all GEMMs)"}
     dom = max(prof, key=lambda c: prof[c][0])
     roof = kernel_roofline(dom, prof[dom][0], prof[dom][1], cfg, tr.valid_frames, peaks, args.steps)
-    tr_ncu = ncu_traffic({0: "lstm_rec_fwd_kernel", 1: "lstm_rec_bwd_kernel"}.get(dom, "-"))
+    kprefix = {0: "step_fwd" if cfg.H > 512 else "lstm_rec_fwd_kernel",
+               1: "step_bwd" if cfg.H > 512 else "lstm_rec_bwd_kernel", 2: "gemm_f16_kernel"}[dom]
+    tr_ncu = ncu_traffic(kprefix, cfg.name)
+    n_gemm = len(gemm_shapes(cfg))
+    alg_launch = (roof["achieved"] * 1e9 * prof[dom][0] / max(prof[dom][1], 1) / 1e3 if roof["unit"] == "GB/s"
+                  else gemm_alg_bytes(cfg) / n_gemm if dom == 2 else 2 * tr.valid_frames * 40 * cfg.H)
     roof.update({"kernel": cats[dom], "traffic": tr_ncu["bytes"] if tr_ncu else None,
                  "traffic_unit": "bytes/launch (dram read + write)",
                  "traffic_source": tr_ncu["source"] if tr_ncu else None,
-                 "algorithmic_bytes_per_launch": (roof["achieved"] * 1e9 * prof[dom][0] / max(prof[dom][1], 1) / 1e3
-                                                  if roof["unit"] == "GB/s" else None),
+                 "algorithmic_bytes_per_launch": alg_launch,
                  "launch_ms": prof[dom][0] / max(prof[dom][1], 1),
                  "share_of_step": prof[dom][0] / (t_local * 1e3),
                  "peak_source": peaks["source"], "peak_note": peaks["note"]})
     step_ms = t_max / args.steps * 1e3
     V = tr.valid_frames
+    roof["step"] = step_roofline(cfg, V, peaks, step_ms)
     t_tc = V * alg_flops_per_frame(cfg) / (peaks["tf"] * 1e12) * 1e3
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -421,7 +537,7 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = time_oracle(cfg, 15.0)
+            line["cpu_baseline"] = time_oracle(cfg, 15.0, single_thread=True)
         except Exception as e:  # the oracle is a reported baseline, never the product path
             line["cpu_baseline"] = {"error": str(e)}
     print(json.dumps(line), flush=True)

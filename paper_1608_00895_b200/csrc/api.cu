@@ -361,12 +361,13 @@ struct StackGeo {
     // (rec_step.h); BLSTM_FORCE_STEP=1 selects it for any size (tests)
     bool step = false;
     int x2w = 0;  // BLSTM_PREC_FP16X2W (LayerGeo::x2w)
+    int dbs = 0;  // db partial groups per direction and parity in the dbp buffer
 };
 struct StackWS {
     size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, gsk,
         stepF, stepB, cs2, optp, total;
     size_t maxDn;
-    std::vector<size_t> y16, w16, rt16, bq, gates, C, hist;
+    std::vector<size_t> y16, w16, rt16, bq, gates, C, hist, r16;
 };
 
 static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
@@ -389,6 +390,7 @@ static int stack_geo(const blstm_stack_desc *d, StackGeo &g) {
     g.dr.thr = (uint32_t)floor((double)d->dropout * 4294967296.0);
     g.dr.seed = d->dropout_seed;
     g.dr.scale = (float)(1.0 / (1.0 - (double)d->dropout));
+    g.dbs = g.step ? (g.pl.G > rec_step_bwd_db_groups() ? g.pl.G : rec_step_bwd_db_groups()) : g.pl.G;
     g.Dn.resize(g.L); g.Drows.resize(g.L); g.rowmode.resize(g.L);
     for (int l = 0; l < g.L; ++l) {
         g.Dn[l] = l == 0 ? g.Dp0 : 2 * g.Hq;
@@ -429,6 +431,8 @@ static StackWS stack_ws(const StackGeo &g) {
         w.gates.push_back(c.take(ge * 2));
         w.C.push_back(c.take((size_t)2 * TB * Hq * 4));
         w.hist.push_back(c.take((size_t)2 * (g.T + 1) * g.B * Hq * 2));
+        // step mode: R in pack_w's K-major layout [Hq][8Hq] (the persistent BPTT's A operand)
+        w.r16.push_back(c.take(g.step ? (size_t)Hq * 8 * Hq * 2 : 0));
     }
     const size_t zn = g.step ? (size_t)TB * 8 * Hq : rec_native_elems(g.pl, g.T), zl = (size_t)TB * g.Kp;  // Z / logits
     w.Z = c.take((zn > zl ? zn : zl) * 4);
@@ -442,7 +446,7 @@ static StackWS stack_ws(const StackGeo &g) {
     w.dY1 = c.take((size_t)TB * 2 * Hq * 4);
     w.dWT = c.take((size_t)2 * 8 * Hq * maxDn * 4);
     w.dRT = c.take((size_t)2 * 2 * 4 * Hq * Hq * 4);
-    w.dbp = c.take((size_t)2 * 2 * g.pl.G * 4 * Hq * 4);
+    w.dbp = c.take((size_t)2 * 2 * g.dbs * 4 * Hq * 4);
     w.P = c.take(rec_P_bytes(g.pl));
     w.cnt = c.take(256);
     w.wo16 = c.take((size_t)2 * Hq * (g.Kp ? g.Kp : 64) * 2);
@@ -721,16 +725,22 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     // ready when the same main-stream kernel completes, so the order is a race; a one-CTA kernel
     // on the side stream waits for BPTT(l)'s CTAs to check in first.
     static const bool no_guard = getenv("BLSTM_NO_GUARD") && atoi(getenv("BLSTM_NO_GUARD")) != 0;  // A/B
+    // step mode: the persistent BPTT (rec_step.cu) when it applies, else the launched chain
+    const int step_bwd_ctas = g.step ? rec_step_bwd_persist_ctas(g.B, g.Hq, 2) : 0;
+    std::vector<char> bwd_persist(g.L, 0);
+    std::vector<int> db_groups(g.L, g.step ? 1 : g.pl.G);
     auto side_guard = [&](int l) -> int {
-        if (!overlap || no_guard || g.step) return 0;  // (step mode: no persistent BPTT to place)
-        TRY(wait_count(bstarted + l, (uint32_t)rec_ctas, side), "wait_count");
+        if (!overlap || no_guard || (g.step && !bwd_persist[l])) return 0;  // (chain: nothing resident to place)
+        TRY(wait_count(bstarted + l, (uint32_t)(g.step ? step_bwd_ctas : rec_ctas), side), "wait_count");
         return 0;
     };
     // persistent recurrence: the side GEMMs get the SMs its clusters leave free.  Step-launched
     // recurrence (no resident clusters): a share of the GPU sized so that it and the per-step BPTT
     // GEMM (64 CTAs, rec_step.cu SB) run in one wave (C5 sweep: 64 best of 40..74)
     static const int step_side = getenv("BLSTM_STEP_SIDE_CTAS") ? atoi(getenv("BLSTM_STEP_SIDE_CTAS")) : 64;
-    const int side_ctas = !overlap ? 0 : g.step ? step_side : (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8);
+    static const bool step_side_env = getenv("BLSTM_STEP_SIDE_CTAS") != nullptr;
+    const int step_share = (step_bwd_ctas && !step_side_env) ? num_sms() - step_bwd_ctas : step_side;
+    const int side_ctas = !overlap ? 0 : g.step ? step_share : (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8);
     // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
     // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch)
@@ -747,6 +757,10 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
             evs.push_back(e);
         }
     }
+    if (step_bwd_ctas)  // R of every layer in pack_w's K-major layout: the persistent BPTT's A operand
+        for (int l = 0; l < g.L; ++l)
+            TRY(pack_w(theta + offs[6 * l + 1], theta + offs[6 * l + 4], g.H, g.H, Hq, 2, Hq, 0,
+                       (__half *)(ws + w.r16[l]), st), "pack_w R16");
     if (overlap && g.K == 0) {  // the side stream may start only after everything issued so far on s_main
         TRY((int)cudaEventRecord(evs[g.L + 1], st), "cudaEventRecord");
         TRY((int)cudaStreamWaitEvent(side, evs[g.L + 1], 0), "cudaStreamWaitEvent");
@@ -802,7 +816,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         const __half *dA = (__half *)(ws + w.dA) + (size_t)par * g.TB * 8 * Hq;
         float *dWT = (float *)(ws + w.dWT) + (size_t)par * 8 * Hq * w.maxDn;
         float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
-        const float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
+        const float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.dbs * 4 * Hq;
         if (overlap && ss == side) TRY((int)cudaStreamWaitEvent(side, evs[l], 0), "cudaStreamWaitEvent");
         if (l > 0)  // overlaps BPTT(l-1)
             if (int rc = side_guard(l - 1)) return rc;
@@ -826,7 +840,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
             const int e = 6 * l + 3 * dd;
             TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], ss), "scatter dW");
             TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, ss), "scatter dR");
-            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, g.step ? 1 : g.pl.G, dd, ss), "scatter db");
+            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, db_groups[l], dd, ss), "scatter db");
         }
         const size_t b0 = blo[bhead + g.L - 1 - l], b1 = bhi[bhead + g.L - 1 - l];  // layer l's bucket
         if (comm) {  // sync-mode exchange of layer l's bucket (§4.1), overlapping BPTT
@@ -842,7 +856,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     for (int l = g.L - 1; l >= 0; --l) {
         const int par = l & 1;
         __half *dA = (__half *)(ws + w.dA) + (size_t)par * g.TB * 8 * Hq;
-        float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.pl.G * 4 * Hq;
+        float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.dbs * 4 * Hq;
         // layer l+2 used the same parity buffers: its side-stream GEMMs must be done reading them
         if (overlap && l + 2 < g.L) TRY((int)cudaStreamWaitEvent(st, evs[g.L + 2 + l + 2], 0), "cudaStreamWaitEvent");
         RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
@@ -868,10 +882,18 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
             q.dhc = sb + rec_step_bwd_partial_floats(g.B, Hq);
             q.dcc = q.dhc + 2L * g.B * Hq;
             q.splitk_ws = (float *)(ws + w.gsk); q.splitk_elems = GSK_ELEMS;
-            TRY(rec_step_bwd(q, st), "rec_step_bwd");
-            if (cudaMemsetAsync(dbp, 0, (size_t)8 * Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
-            TRY(colsum_f16_add(dA, g.TB, 8 * Hq, 8L * Hq, 1.f / (float)(1 << DA_SHIFT), dbp, (float *)(ws + w.cs2), st),
-                "db colsum");
+            q.R16 = (const __half *)(ws + w.r16[l]);
+            q.dbpart = dbp;  // the persistent BPTT's db partials ([2][8][4Hq], dbs >= 8)
+            q.started = p.started;
+            const int rc = rec_step_bwd(q, st);
+            if (rc < 0) TRY(rc, "rec_step_bwd");
+            bwd_persist[l] = rc == 1;
+            db_groups[l] = rc == 1 ? rec_step_bwd_db_groups() : 1;
+            if (rc == 0) {  // the step chain: db = column sums of dA ([2][1][4Hq])
+                if (cudaMemsetAsync(dbp, 0, (size_t)8 * Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
+                TRY(colsum_f16_add(dA, g.TB, 8 * Hq, 8L * Hq, 1.f / (float)(1 << DA_SHIFT), dbp, (float *)(ws + w.cs2), st),
+                    "db colsum");
+            }
         } else {
             TRY(lstm_rec_bwd(p, (const __half *)(ws + w.rt16[l]), st), "lstm_rec_bwd");
         }

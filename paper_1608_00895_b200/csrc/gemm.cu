@@ -490,12 +490,19 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
                                   : launch_gemm<128>(ta, tb, ta2, q, max_ctas, st);
         return e == cudaSuccess ? 0 : -5;
     }
+    // split K when it shortens the launch: the estimate is the waves of (split, tile) work items over
+    // the allowed CTAs, each 1/S of a full-K tile, plus the fixed-order reduction's HBM pass over
+    // the S partial tiles (e.g. dR^T at C3: 32 tiles on the 52 SMs the recurrence leaves -> S = 3)
     int S = 1;
-    if (p.splitk_ws && !p.natB && !p.flags && tiles * 2 <= max_ctas && num_kb >= 32) {
-        S = max_ctas / tiles;
-        if (S > num_kb / 16) S = num_kb / 16;  // >= 16 k-blocks per split
-        if (S > 8) S = 8;
-        while (S > 1 && (long)S * p.M * p.N > p.splitk_elems) --S;
+    if (p.splitk_ws && !p.natB && !p.flags && num_kb >= 32) {
+        const double t_tile = 2.0 * GEMM_BM * BN * (double)p.K / 9.0e12;   // one full-K tile on one SM (s)
+        const double mn_bytes = 8.0 * (double)p.M * p.N;                    // a partial written + read (fp32)
+        double best = (double)((tiles + max_ctas - 1) / max_ctas) * t_tile;
+        for (int s = 2; s <= 8; ++s) {
+            if (num_kb / s < 16 || (long)s * p.M * p.N > p.splitk_elems) break;  // >= 16 k-blocks per split
+            const double est = (double)((tiles * s + max_ctas - 1) / max_ctas) * t_tile / s + s * mn_bytes / 5.0e12;
+            if (est < 0.97 * best) { best = est; S = s; }
+        }
         if (S > 1) S = (num_kb + (num_kb + S - 1) / S - 1) / ((num_kb + S - 1) / S);  // no empty split
     }
     GemmParams q = p;

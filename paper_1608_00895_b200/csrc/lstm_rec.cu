@@ -1041,6 +1041,7 @@ static cudaError_t launch_cluster(Kern kern, int grid, int cluster, size_t smem,
 
 static unsigned long long *g_trace_fwd = nullptr, *g_trace_bwd = nullptr;
 unsigned long long *rec_trace_fwd() { return g_trace_fwd; }
+unsigned long long *rec_trace_bwd() { return g_trace_bwd; }
 void rec_set_trace(unsigned long long *fwd, unsigned long long *bwd) {
     g_trace_fwd = fwd;
     g_trace_bwd = bwd;

@@ -66,7 +66,8 @@ struct RecParams {
 
 // debug hook: per-step phase timestamps (globaltimer ns, 8 per step) of the next launches
 void rec_set_trace(unsigned long long *fwd, unsigned long long *bwd);
-unsigned long long *rec_trace_fwd();  // the forward trace buffer (nullptr unless set)
+unsigned long long *rec_trace_fwd();
+unsigned long long *rec_trace_bwd();  // the forward trace buffer (nullptr unless set)
 
 // CTA-native layout of Z and of the saved gate activations (one time step = one block per
 // (direction, batch group, CTA)): element (t, d, g, c, column block cb, gate row r, i) at

@@ -561,6 +561,438 @@ static int rec_step_fwd_persist(const RecStepFwd &p, cudaStream_t st) {
     return 1;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent BPTT (Hq in {512, 1024}, B <= 128): the mirror of the persistent forward, with the
+// recurrent weights resident on chip for the whole reverse scan and no launch per time step
+// (north_star: "the mirrored BPTT kernel").
+//   dh_{t'}[b, k] = sum_n dA_t[b, n] R[k, n]   (k: hidden unit, n: gate column 4u + gamma)
+// Thread-block clusters of PB_KS = 4 CTAs, one cluster per (direction d, 128-unit tile ut); cluster
+// rank ks holds the K-split n in [ks Hq, (ks+1) Hq) of the tile's R rows as the tcgen05 A operand
+// (M = 128 units): the first PB_TK columns in TMEM (A-from-TMEM MMAs), the rest in shared memory
+// (SW128, TMA once).  2 * (Hq / 128) * 4 CTAs: 64 at C5, which leaves the other SMs to the
+// weight-gradient GEMMs of the layer above (side stream).
+// Per step s (frame t; the reverse of the forward scan):
+//   1. the TMA warp waits until the unit tiles whose gate columns form this CTA's K-split have
+//      published dA of step s-1 (per-(direction, tile) counters, release / acquire at gpu scope),
+//      then streams dA_{s-1}[128 batch rows][K-split] (the B operand, N = batch) through a ring;
+//   2. one warp issues the MMAs: D[128 units x 128 batch] (fp32, TMEM) = R[tile, K-split] dA^T;
+//   3. reduce-scatter of D over the cluster through distributed shared memory: rank j owns batch
+//      columns [32 j, 32 j + 32) and receives the other three ranks' partial sums of them
+//      (st.async, complete_tx on its mbarrier); dh = P_0 + P_1 + P_2 + P_3 (fixed order);
+//   4. the gate gradients of frame t as in step_bwd_gate_kernel (dH, dc~, dA, dc; masked frames
+//      pass dh and dc through, R4), dA -> HBM (scaled fp16, the next step's B operand and the
+//      weight-gradient GEMMs' input), db accumulated in registers;
+//   5. arrive on the tile's counter.
+// After the last step, with dh0 requested, one more MMA + reduction gives dh0.
+// ---------------------------------------------------------------------------------------------
+constexpr int PB_THREADS = 256;
+constexpr int PB_KS = 4;                 // K-splits = cluster size
+constexpr int PB_S = 7;                  // dA ring stages (16 KB: 128 batch rows x 64 gate columns)
+constexpr int PB_TK = 768;               // K columns of the A operand held in TMEM (384 columns)
+constexpr uint32_t PB_CHUNK = 16384;
+constexpr uint32_t PB_RECV = (PB_KS - 1) * 32 * 128 * 2;  // three ranks' partial sums of 32 batch columns,
+                                                          // fp16 (x2: double-buffered by step parity)
+constexpr uint32_t PB_DCOL = 384;        // TMEM column of D [128 lanes x 128 batch columns]
+constexpr int PB_DBG = 2 * PB_KS;        // db partial groups per direction (rank x column half)
+static int pb_tk(int Hq) { return Hq < PB_TK ? Hq : PB_TK; }
+static size_t pb_smem(int Hq) {
+    return (size_t)((Hq - pb_tk(Hq)) / 64) * PB_CHUNK + PB_S * PB_CHUNK + 2 * PB_RECV + 1024 + 256;
+}
+
+__global__ void __launch_bounds__(PB_THREADS, 1)
+    step_bwd_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmR,
+                            RecStepBwd p, const __half *__restrict__ R16, uint32_t *cnt, float *dbpart,
+                            unsigned long long *trace) {
+#ifdef BLSTM_TRACE
+#define PTB(k) \
+    if (trb) trb[(size_t)s * 16 + (k)] = (unsigned long long)clock64()
+    unsigned long long *trb = (blockIdx.x == 0 && threadIdx.x == 0) ? trace : nullptr;
+#else
+#define PTB(k)
+#endif
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int Hq = p.Hq, B = p.B, T = p.T, H = p.H, G4 = p.ndir * 4 * Hq;
+    const int TK = Hq < PB_TK ? Hq : PB_TK;      // K in TMEM
+    const int KCT = TK / 64, KC = Hq / 64;        // 64-wide K chunks: in TMEM, in total
+    uint8_t *Rs = smem;                           // [KC - KCT][128 rows][128 B] SW128 (K-major A)
+    uint8_t *ring = Rs + (KC - KCT) * PB_CHUNK;   // [PB_S][128 batch rows][128 B] SW128 (K-major B)
+    uint4 *recv = reinterpret_cast<uint4 *>(ring + PB_S * PB_CHUNK);  // [2 parity][3 slots][4 col groups][128 units][8 fp16]
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + PB_S * PB_CHUNK + 2 * PB_RECV);
+    uint64_t *empty = full + PB_S;
+    uint64_t *mma_done = empty + PB_S;
+    uint64_t *rbar = mma_done + 1;
+    uint64_t *xbar = rbar + 1;                    // [2 parity]
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(xbar + 2);
+
+    const int ks = (int)cluster_ctarank();
+    const int NUT = Hq / 128;
+    const int cl = blockIdx.x / PB_KS;
+    const int d = cl / NUT, ut = cl - d * NUT;
+    const int dir = d == 0 ? p.dir0 : -1;
+    const int w = warp_uniform(warp_id()), l = lane_id(), q = w & 3, ch = w >> 2;
+    const int m = 32 * q + l;                     // unit row of the tile (TMEM lane)
+    const int u = ut * 128 + m;                   // hidden unit
+    const int b0 = 32 * ks + 16 * ch;             // this thread's 16 batch columns (owner role)
+    // the unit tiles whose gate columns [ks Hq, (ks+1) Hq) this CTA's K-split covers
+    const int tlo = ks * Hq / 4 / 128, thi = ((ks + 1) * Hq / 4 - 1) / 128;
+    uint32_t *cnt_d = cnt + 16 * d;
+    const float scale = (float)(1 << DA_SHIFT), alpha = 1.f / scale;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < PB_S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(mma_done, 1);
+        mbar_init(rbar, 1);
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmA);
+        if (KC > KCT) tma_prefetch_desc(&tmR);
+    }
+    if (w == 1) {
+        tmem_alloc(tslot, 512);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    if (p.started && threadIdx.x == 0) red_release_gpu_add(p.started, 1u);  // placed (side-stream guard)
+    const int col0 = d * 4 * Hq + ks * Hq;        // first gate column of the K-split in R16 / dA
+    if (threadIdx.x == 0 && KC > KCT) {            // the K-split's columns beyond TK: shared memory
+        mbar_arrive_expect_tx(rbar, (KC - KCT) * PB_CHUNK);
+        for (int kc = KCT; kc < KC; ++kc) tma_load_2d(Rs + (kc - KCT) * PB_CHUNK, &tmR, rbar, col0 + kc * 64, ut * 128);
+    }
+    {   // the first TK columns -> TMEM columns [0, TK/2) (two fp16 per 32-bit column, lane = unit row);
+        // warps w and w + 4 share lane quarter q and split the columns
+        const __half *row = R16 + (size_t)(ut * 128 + m) * (2 * 4 * Hq) + col0;
+        const int half = TK / 2;                  // fp16 per warp group
+        const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+        for (int c0 = ch * half; c0 < ch * half + half; c0 += 32) {
+            uint32_t v[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint4 x = *reinterpret_cast<const uint4 *>(row + c0 + 8 * j);
+                v[4 * j] = x.x; v[4 * j + 1] = x.y; v[4 * j + 2] = x.z; v[4 * j + 3] = x.w;
+            }
+            tmem_st16(tq + (uint32_t)(c0 / 2), v);
+        }
+        tmem_st_wait();
+    }
+    if (KC > KCT) mbar_wait(rbar, 0);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // every rank's barriers are initialised before any remote store
+    tc_fence_after();
+
+    const uint32_t idesc = idesc_f16(128, 128, 0, 0);
+    const uint32_t dq = tmem + ((uint32_t)(32 * q) << 16) + PB_DCOL;
+    // The reduction's receive buffer and its mbarrier are double-buffered by step parity.  Rank j
+    // sends its step-s partial sums (buffer s & 1) only after it received every other rank's step-(s-1)
+    // sums, each sent after that rank had consumed its step-(s-2) buffer (same parity) and re-armed
+    // its barrier: the all-to-all exchange itself orders the reuse, no cluster barrier per step.
+    if (threadIdx.x == 0) {  // steps 1 and 2 (parities 1 and 0)
+        mbar_arrive_expect_tx(&xbar[1], PB_RECV);
+        mbar_arrive_expect_tx(&xbar[0], PB_RECV);
+    }
+
+    // per-cell state of the 16 cells (unit u, batch b0 + i) this thread owns
+    float dc[16], dhc[16], db[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int b = b0 + i;
+        const bool ok = b < B && u < H;
+        dc[i] = (ok && p.dcT) ? p.dcT[((long)d * B + b) * H + u] : 0.f;
+        dhc[i] = (ok && p.dhT) ? p.dhT[((long)d * B + b) * H + u] : 0.f;
+    }
+    int stage = 0;
+    uint32_t phase = 0, mph = 0, xph[2] = {0, 0};
+    uint32_t mprev = 0;  // mask bits (cell i) of the frame of the previous step
+    const int S_END = T + (p.dh0 ? 1 : 0);        // step T: dh0 only
+    for (int s = 0; s < S_END; ++s) {
+        const bool last = s == T;
+        const int t = dir > 0 ? T - 1 - s : s;   // this step's frame (unused when last)
+        const int tp = dir > 0 ? T - s : s - 1;  // the frame of step s-1
+        const bool need_mma = s > 0;
+        PTB(0);
+        float dh[16];
+        PTB(1);
+        if (need_mma) {
+            if (w == 0) {
+                if (elect_one()) {  // dA of step s-1 (frame tp), this CTA's K-split of it
+                    for (int tt = tlo; tt <= thi; ++tt) spin_until_geq(cnt_d + tt, (uint32_t)s * PB_KS);
+                    PTB(2);
+                    fence_proxy_async_global();
+                    int st2 = stage;
+                    uint32_t ph2 = phase;
+                    for (int kc = 0; kc < KC; ++kc) {
+                        mbar_wait(&empty[st2], ph2 ^ 1);
+                        mbar_arrive_expect_tx(&full[st2], PB_CHUNK);
+                        tma_load_2d(ring + st2 * PB_CHUNK, &tmA, &full[st2], col0 + kc * 64, tp * B);
+                        if (++st2 == PB_S) { st2 = 0; ph2 ^= 1; }
+                    }
+                    PTB(3);
+                }
+                __syncwarp();
+            } else if (w == 1) {
+                int st2 = stage;
+                uint32_t ph2 = phase;
+                for (int kc = 0; kc < KC; ++kc) {
+                    mbar_wait(&full[st2], ph2);
+                    tc_fence_after();
+                    const uint32_t sb = smem_u32(ring + st2 * PB_CHUNK);
+                    if (kc < KCT) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_f16_ts_w(tmem + PB_DCOL, tmem + (uint32_t)(kc * 32 + kk * 8),
+                                         sdesc_sw128(sb + kk * 32, 16, 1024), idesc, (kc | kk) != 0);
+                    } else {
+                        const uint32_t sa = smem_u32(Rs + (kc - KCT) * PB_CHUNK);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_f16_ss_w(tmem + PB_DCOL, sdesc_sw128(sa + kk * 32, 16, 1024),
+                                         sdesc_sw128(sb + kk * 32, 16, 1024), idesc, 1);
+                    }
+                    mma_commit_w(&empty[st2]);
+                    __syncwarp();
+                    if (++st2 == PB_S) { st2 = 0; ph2 ^= 1; }
+                }
+                mma_commit_w(mma_done);
+                __syncwarp();
+            }
+            {
+                const int adv = stage + KC;
+                phase ^= (uint32_t)((adv / PB_S) & 1);
+                stage = adv % PB_S;
+            }
+        }
+        // saved state of this step's frame (produced before the launch), loaded while the MMAs run:
+        // issued after the TMA / MMA warps' role work (a load that stalls those warps would stall
+        // the chain), all independent (no load feeds an address or a branch), kept packed (gates as
+        // fp16 pairs) so the 16 cells' state fits in registers; cells beyond B read row B - 1
+        uint2 gq[16];
+        float cc[16], cp[16], dy[16];
+        uint32_t mbits = 0;
+        if (!last) {
+            const int tpf = t - dir;              // the frame before t in the forward scan
+            const bool tpf_in = tpf >= 0 && tpf < T;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int b = min(b0 + i, B - 1);
+                const long r = (long)t * B + b;
+                mbits |= (p.mask[r] != 0 && b0 + i < B) ? (1u << i) : 0u;
+                gq[i] = *reinterpret_cast<const uint2 *>(p.gates + r * G4 + (long)d * 4 * Hq + 4 * u);
+                cc[i] = p.C[d * p.c_doff + r * p.ldc + u];
+                cp[i] = tpf_in ? p.C[d * p.c_doff + ((long)tpf * B + b) * p.ldc + u]
+                               : (p.c0 && u < H ? p.c0[((long)d * B + b) * H + u] : 0.f);
+                dy[i] = p.dy[r * p.lddy + d * p.dy_doff + u];
+            }
+        }
+        if (need_mma) {
+            mbar_wait(mma_done, mph);
+            PTB(4);
+            mph ^= 1;
+            tc_fence_after();
+            // reduce-scatter: columns [64 ch, 64 ch + 64) of row m belong to ranks 2ch and 2ch + 1
+            const int par = s & 1;
+            const uint32_t pofs = (uint32_t)par * PB_RECV;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+                const int j = 2 * ch + jj;
+                if (j == ks) continue;
+                const uint32_t slot = (uint32_t)(ks < j ? ks : ks - 1);
+                const uint32_t rbase = mapa_shared(smem_u32(recv), (uint32_t)j) + pofs;
+                const uint32_t rbar = mapa_shared(smem_u32(&xbar[par]), (uint32_t)j);
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {  // 16 columns at a time (registers), as fp16
+                    float v[16];
+                    tmem_ld16(dq + 32 * j + 16 * hh, v);
+                    tmem_ld_wait();
+                    uint32_t hv[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        __half2 h2 = __floats2half2_rn(v[2 * e], v[2 * e + 1]);
+                        hv[e] = *reinterpret_cast<uint32_t *>(&h2);
+                    }
+#pragma unroll
+                    for (int cg = 0; cg < 2; ++cg)
+                        st_async_v4u(rbase + (uint32_t)(((slot * 4 + 2 * hh + cg) * 128 + m) * 16), hv[4 * cg],
+                                     hv[4 * cg + 1], hv[4 * cg + 2], hv[4 * cg + 3], rbar);
+                }
+            }
+            float own[16];
+            tmem_ld16(dq + b0, own);
+            tmem_ld_wait();
+            PTB(5);
+            mbar_wait(&xbar[par], xph[par]);  // the three other ranks' partial sums of this CTA's columns
+            PTB(6);
+            xph[par] ^= 1;
+            const uint4 *rv = recv + par * (PB_RECV / 16);
+            // dh = P_0 + P_1 + P_2 + P_3 (rank order; the other ranks' partials as fp16), unscaled
+            float pr[PB_KS - 1][16];
+#pragma unroll
+            for (int sl = 0; sl < PB_KS - 1; ++sl)
+#pragma unroll
+                for (int cg = 0; cg < 2; ++cg) {
+                    const uint4 x = rv[(sl * 4 + 2 * ch + cg) * 128 + m];
+                    const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&xw[e]));
+                        pr[sl][8 * cg + 2 * e] = f.x;
+                        pr[sl][8 * cg + 2 * e + 1] = f.y;
+                    }
+                }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                float a = 0.f;
+#pragma unroll
+                for (int j = 0; j < PB_KS; ++j) {  // rank j's partial: own, or slot j (j < ks) / j - 1 (j > ks)
+                    const float lo = pr[j < PB_KS - 1 ? j : PB_KS - 2][i], hi = pr[j > 0 ? j - 1 : 0][i];
+                    const float v = j == ks ? own[i] : (j < ks ? lo : hi);
+                    a = j == 0 ? v : a + v;
+                }
+                dh[i] = a * alpha;
+            }
+            tc_fence_before();
+            // buffer par is reused at step s + 2: its barrier is re-armed by thread 0 after the CTA
+            // barrier at the end of this step (every thread has read the buffer by then)
+        }
+        PTB(7);
+        if (last) {  // dh0 / dc0: the gradient w.r.t. the state before the scan
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int b = b0 + i;
+                if (b >= B || u >= H) continue;
+                p.dh0[((long)d * B + b) * H + u] = ((mprev >> i) & 1u) ? dh[i] : dhc[i];
+                if (p.dc0) p.dc0[((long)d * B + b) * H + u] = dc[i];
+            }
+            break;
+        }
+        // gate gradients of frame t
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int b = b0 + i;
+            if (b >= B) continue;
+            float dh_in = dhc[i];
+            if (need_mma && ((mprev >> i) & 1u)) dh_in = dh[i];
+            __half2 *dap = reinterpret_cast<__half2 *>(p.dA + ((long)t * B + b) * G4 + (long)d * 4 * Hq + 4 * u);
+            if (!((mbits >> i) & 1u) || u >= H) {
+                dap[0] = __floats2half2_rn(0.f, 0.f);
+                dap[1] = __floats2half2_rn(0.f, 0.f);
+                dhc[i] = dh_in;  // pass through; dc unchanged
+                continue;
+            }
+            const float2 g01 = __half22float2(*reinterpret_cast<const __half2 *>(&gq[i].x));
+            const float2 g23 = __half22float2(*reinterpret_cast<const __half2 *>(&gq[i].y));
+            const float gi = g01.x, gf = g01.y, gg = g23.x, go = g23.y;
+            const float dH = dh_in + dy[i];
+            const float tc = th(cc[i]);
+            const float dct = dc[i] + dH * go * (1.f - tc * tc);
+            const float da_i = dct * gg * gi * (1.f - gi);
+            const float da_f = dct * cp[i] * gf * (1.f - gf);
+            const float da_g = dct * gi * (1.f - gg * gg);
+            const float da_o = dH * tc * go * (1.f - go);
+            dap[0] = __floats2half2_rn(da_i * scale, da_f * scale);
+            dap[1] = __floats2half2_rn(da_g * scale, da_o * scale);
+            db[0] += da_i; db[1] += da_f; db[2] += da_g; db[3] += da_o;
+            dc[i] = dct * gf;
+            dhc[i] = dh_in;
+        }
+        // publish dA_t of this tile: the CTA barrier orders every thread's stores before thread 0's
+        // release (cumulative), which the consumers' acquire pairs with
+        mprev = mbits;
+        PTB(8);
+        tc_fence_before();
+        __syncthreads();
+        PTB(9);
+        if (threadIdx.x == 0) {
+            red_release_gpu_add(cnt_d + ut, 1u);
+            if (need_mma) mbar_arrive_expect_tx(&xbar[s & 1], PB_RECV);  // for step s + 2
+        }
+    }
+    if (dbpart) {  // db partials: [d][rank * 2 + column half][4Hq] (0 for padding units)
+        float *dp = dbpart + ((long)d * PB_DBG + ks * 2 + ch) * 4 * Hq + 4 * u;
+        dp[0] = db[0]; dp[1] = db[1]; dp[2] = db[2]; dp[3] = db[3];
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // no remote store into this CTA's shared memory is outstanding
+    if (w == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// 1: the persistent BPTT ran (db partials, PB_DBG groups per direction, written to p.dbpart when
+// given); 0: not used (the caller runs the step chain); < 0: error.  BLSTM_STEP_PERSIST_BWD=0 turns it
+// off, =1 forces it.
+static int rec_step_bwd_persist(const RecStepBwd &p, cudaStream_t st) {
+    const char *e = getenv("BLSTM_STEP_PERSIST_BWD");
+    if (e && e[0] == '0') return 0;
+    const bool force = e && e[0] == '1';
+    const int no = force ? -6 : 0;
+    const int Hq = p.Hq;
+    if (p.B > 128 || (Hq != 512 && Hq != 1024) || p.T < 1 || p.ndir != 2 || !p.R16) return no;
+    const int ctas = p.ndir * (Hq / 128) * PB_KS;
+    if (ctas > num_sms()) return no;
+    const size_t smem = pb_smem(Hq);
+    if (cudaFuncSetAttribute(step_bwd_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return force ? -5 : 0;
+    }
+    CUtensorMap tmA, tmR;
+    if (make_tmap_f16(&tmA, p.dA, (uint64_t)p.ndir * 4 * Hq, (uint64_t)p.T * p.B, (uint64_t)p.ndir * 4 * Hq, 128))
+        return -5;
+    if (make_tmap_f16(&tmR, p.R16, (uint64_t)2 * 4 * Hq, (uint64_t)Hq, (uint64_t)2 * 4 * Hq, 128)) return -5;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(PB_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = PB_KS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, step_bwd_persist_kernel, &cfg) != cudaSuccess ||
+        nclusters < ctas / PB_KS) {
+        cudaGetLastError();
+        return no;
+    }
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(p.dhR);  // the chain's partials scratch is unused here
+    if (cudaMemsetAsync(cnt, 0, 32 * sizeof(uint32_t), st) != cudaSuccess) return -5;
+    bool ok;
+    {
+        ProfScope ps(PROF_REC_BWD, st);
+        ok = cudaLaunchKernelEx(&cfg, step_bwd_persist_kernel, tmA, tmR, p, p.R16, cnt, p.dbpart, rec_trace_bwd()) ==
+             cudaSuccess;
+    }
+    if (!ok) {
+        cudaGetLastError();
+        return force ? -5 : 0;
+    }
+    note_launch();
+    return 1;
+}
+int rec_step_bwd_db_groups() { return PB_DBG; }
+int rec_step_bwd_persist_ctas(int B, int Hq, int ndir) {
+    const char *e = getenv("BLSTM_STEP_PERSIST_BWD");
+    if (e && e[0] == '0') return 0;
+    if (B > 128 || (Hq != 512 && Hq != 1024) || ndir != 2) return 0;
+    const int ctas = ndir * (Hq / 128) * PB_KS;
+    return ctas <= num_sms() ? ctas : 0;
+}
+
 size_t rec_step_fwd_scratch_bytes(int B, int Hq) { return (size_t)2 * SF * B * 4 * Hq * 4 + (size_t)2 * B * Hq * 4; }
 size_t rec_step_bwd_partial_floats(int B, int Hq) { return (size_t)2 * SB * B * Hq; }
 size_t rec_step_bwd_scratch_bytes(int B, int Hq) { return (rec_step_bwd_partial_floats(B, Hq) + (size_t)4 * B * Hq) * 4; }
@@ -612,6 +1044,7 @@ int rec_step_fwd(const RecStepFwd &p, cudaStream_t st) {
 }
 
 int rec_step_bwd(const RecStepBwd &p, cudaStream_t st) {
+    if (const int rc = rec_step_bwd_persist(p, st)) return rc;
     const int Hq = p.Hq, B = p.B, T = p.T;
     const float alpha = 1.f / (float)(1 << DA_SHIFT);
     const bool pdl = step_pdl();

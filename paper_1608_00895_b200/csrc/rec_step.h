@@ -50,6 +50,13 @@ struct RecStepBwd {
     float *dhc, *dcc;        // [2][B][Hq] carried dh (masked frames) and dc
     float *splitk_ws;        // split-K scratch of the per-step GEMM
     long splitk_elems;
+    // the persistent BPTT (rec_step.cu step_bwd_persist_kernel) also needs: R in the K-major layout
+    // of pack_w ([Hq][2 * 4Hq]: R16[k][d 4Hq + 4u + gamma] = R_d[k][gamma H + u]; nullptr: chain only),
+    // the db partials output ([ndir][rec_step_bwd_db_groups()][4Hq]; nullptr: not written) and an
+    // optional "CTAs placed" counter (side-stream guard)
+    const __half *R16;
+    float *dbpart;
+    uint32_t *started;
 };
 
 size_t rec_step_fwd_scratch_bytes(int B, int Hq);
@@ -58,6 +65,11 @@ size_t rec_step_bwd_scratch_bytes(int B, int Hq);
 // ([2][B][Hq] each) follow
 size_t rec_step_bwd_partial_floats(int B, int Hq);
 int rec_step_fwd(const RecStepFwd &p, cudaStream_t st);
+// 0: the step chain ran (db: column sums of dA are the caller's); 1: the persistent BPTT ran and wrote
+// p.dbpart (rec_step_bwd_db_groups() partial groups per direction); < 0: error
 int rec_step_bwd(const RecStepBwd &p, cudaStream_t st);
+int rec_step_bwd_db_groups();
+// CTAs of the persistent BPTT for this shape, 0 when it does not apply (then the chain runs)
+int rec_step_bwd_persist_ctas(int B, int Hq, int ndir);
 
 }  // namespace blstm

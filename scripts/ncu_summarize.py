@@ -2,7 +2,10 @@
 training step, serialised / cold-cache, so compare SHARES) and key counters of the
 --set full captures (duration, DRAM bytes, tensor-pipe / SM throughput, occupancy).
 
-usage: python scripts/ncu_summarize.py <launches.csv> <steps_in_run> <out_prefix> [rep.ncu-rep ...]
+usage: python scripts/ncu_summarize.py <launches.csv|-> <steps_in_run> <out_prefix> [--config C3] [rep.ncu-rep ...]
+
+--config tags the summary with the workload it was captured on: bench.py takes roofline.traffic only
+from a summary of its own config (profiles/r*_ncu_*.json with "config" == its config).
 """
 import csv
 import io
@@ -69,17 +72,24 @@ def rep_summary(path):
 
 
 def main():
-    launches, steps, prefix = sys.argv[1], int(sys.argv[2]), sys.argv[3]
-    agg = launch_list(launches, steps)
-    total = sum(v[0] for v in agg.values())
+    argv = sys.argv[1:]
+    config = None
+    if "--config" in argv:
+        i = argv.index("--config")
+        config = argv[i + 1]
+        del argv[i:i + 2]
+    launches, steps, prefix = argv[0], int(argv[1]), argv[2]
+    agg = launch_list(launches, steps) if launches != "-" else {}
+    total = sum(v[0] for v in agg.values()) or 1.0
     ours = {k: v for k, v in agg.items() if not k.startswith("at::") and "at::" not in k}
     summary = {"source": launches, "note": "ncu --metrics gpu__time_duration.sum --clock-control none; serialised, "
                                           "cold-cache per-launch times: compare shares, not absolutes",
                "kernels": {k: {"us_total": v[0], "launches": v[1], "share_of_listed": v[0] / total}
                            for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])},
                "ours_us_total": sum(v[0] for v in ours.values()), "all_us_total": total}
+    summary["config"] = config
     reps = {}
-    for rp in sys.argv[4:]:
+    for rp in argv[3:]:
         reps[rp] = rep_summary(rp)
     summary["full_captures"] = reps
     json.dump(summary, open(prefix + ".json", "w"), indent=1)

@@ -31,6 +31,10 @@ BWD = [(0, None), (1, "issue next-step loads"), (2, "wait P + gather"), (8, "wai
 # the persistent forward of the step-launched path (rec_step.cu, BLSTM_STEP_PERSIST=1)
 PFWD = [(0, None), (1, "Z loads issued"), (2, "grid barrier wait"), (3, "TMA issue"), (4, "MMA wait"),
         (5, "TMEM ld + send"), (6, "cluster sync"), (7, "gate math + stores"), (8, "__syncthreads"), (9, "arrive")]
+# the persistent BPTT of the step path (rec_step.cu step_bwd_persist_kernel), CTA 0 thread 0 (the TMA lane)
+PBWD = [(0, None), (1, "state loads issued"), (2, "counter wait"), (3, "TMA issue"), (4, "MMA wait"),
+        (5, "TMEM ld + sends"), (6, "recv wait"), (7, "dh sum + arrive"), (8, "gate math + dA stores"),
+        (9, "__syncthreads")]
 
 
 def report(name, tr, seq):
@@ -64,6 +68,8 @@ def main():
     b = tb.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
     if cfg.H > 512 and os.environ.get("BLSTM_STEP_PERSIST") != "0":  # the step path (H beyond the cluster kernels)
         report("forward (persistent step path)", f, PFWD)
+        if os.environ.get("BLSTM_STEP_PERSIST_BWD") != "0":
+            report("backward (persistent step path)", b, PBWD)  # rows in processing order (s)
         return
     report("forward", f, FWD)
     # backward rows are indexed by s descending; use processing order

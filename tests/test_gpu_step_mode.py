@@ -139,3 +139,67 @@ def test_persistent_forward_close_to_chain(H, force):
     assert abs(g1["loss"] - g0["loss"]) / abs(g0["loss"]) < 1e-4
     errs = grad_errors(g1["grad"], g0["grad"], L, D, H, K)
     assert max(errs.values()) < GRAD_TOL, errs
+
+
+# ---------------------------------------------------------------------------------------------
+# the persistent BPTT of the step path (rec_step.cu step_bwd_persist_kernel): R resident in TMEM +
+# shared memory across 4-CTA clusters, no launch per time step
+# ---------------------------------------------------------------------------------------------
+def _launches_of_step(st, theta, batch):
+    from paper_1608_00895_b200 import blstm
+    n0 = blstm.blstm_launch_count()
+    out = st.step(theta, batch, side_stream=True)
+    return out, blstm.blstm_launch_count() - n0
+
+
+@pytest.mark.parametrize("H,force", [(1024, False), (300, True)])
+def test_persistent_bptt_matches_oracle(H, force):
+    """Hq = 1024 (TMEM + shared-memory A operand) and Hq = 512 (TMEM only), ragged lengths with an
+    empty sequence, B not a multiple of the 32-column ownership blocks."""
+    if force:
+        os.environ["BLSTM_FORCE_STEP"] = "1"
+    try:
+        rng = np.random.default_rng(3)
+        T, B = 17, 37
+        lengths = rng.integers(1, T + 1, size=B)
+        lengths[0], lengths[5] = T, 0
+        L, D, K = 2, 40, 13
+        params = synth.stack_params(L, D, H, K)
+        batch = synth.speech_batch(T, B, D, K, lengths, seed=1006)
+        theta = oracle.pack_params(params, L, D, H, K)
+        got, n = _launches_of_step(Stack(L, D, H, K, T, B), theta, batch)
+        assert n < 2 * L * T, f"{n} launches: the per-step chain ran, not the persistent BPTT"
+        ref = oracle.blstm_step(theta, batch.x, batch.mask, L, H, K, labels=batch.labels)
+        assert abs(got["loss"] - ref["loss"]) / abs(ref["loss"]) < OUT_TOL
+        errs = grad_errors(got["grad"], ref["grad"], L, D, H, K)
+        assert max(errs.values()) < GRAD_TOL, errs
+    finally:
+        os.environ.pop("BLSTM_FORCE_STEP", None)
+
+
+@pytest.mark.parametrize("H,B,force", [(1024, 128, False), (1024, 100, False), (300, 128, True)])
+def test_persistent_bptt_close_to_chain(H, B, force):
+    """Full 128-column batch (every owner block busy) over 40 steps: the persistent BPTT and the
+    launched chain compute the same gradients up to rounding order (fp32 sums of fp16 products)."""
+    if force:
+        os.environ["BLSTM_FORCE_STEP"] = "1"
+    try:
+        T, L, D, K = 40, 2, 40, 11
+        rng = np.random.default_rng(4)
+        lengths = rng.integers(1, T + 1, size=B)
+        lengths[0] = T
+        params = synth.stack_params(L, D, H, K)
+        batch = synth.speech_batch(T, B, D, K, lengths, seed=1007)
+        theta = oracle.pack_params(params, L, D, H, K)
+        a, na = _launches_of_step(Stack(L, D, H, K, T, B), theta, batch)
+        os.environ["BLSTM_STEP_PERSIST_BWD"] = "0"
+        try:
+            b, nb = _launches_of_step(Stack(L, D, H, K, T, B), theta, batch)
+        finally:
+            del os.environ["BLSTM_STEP_PERSIST_BWD"]
+        assert na < nb - L * T, (na, nb)
+        assert abs(a["loss"] - b["loss"]) <= 1e-6 * abs(b["loss"])
+        errs = grad_errors(a["grad"], b["grad"], L, D, H, K)
+        assert max(errs.values()) < 2e-3, errs
+    finally:
+        os.environ.pop("BLSTM_FORCE_STEP", None)
