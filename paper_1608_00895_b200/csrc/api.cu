@@ -408,11 +408,22 @@ static size_t zflag_words(const StackGeo &g) {
 // or sanitizer injected into the process (ncu, compute-sanitizer: CUDA_INJECTION64_PATH),
 // CUDA_LAUNCH_BLOCKING=1, or an MPS SM cap.  The Z-GEMM overlap is then not attempted at all
 // (the start arbitration would also keep it correct, after a 20 ms wait per layer).
+static bool tool_injected() {  // a profiler / sanitizer library mapped into this process
+    FILE *f = fopen("/proc/self/maps", "r");
+    if (!f) return false;
+    char line[1024];
+    bool hit = false;
+    while (!hit && fgets(line, sizeof line, f))
+        hit = strstr(line, "Injection") || strstr(line, "nsight-compute") || strstr(line, "libsanitizer") ||
+              strstr(line, "compute-sanitizer");
+    fclose(f);
+    return hit;
+}
 static bool serialized_env() {
     const char *inj = getenv("CUDA_INJECTION64_PATH");
     const char *lb = getenv("CUDA_LAUNCH_BLOCKING");
     const char *mps = getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE");
-    return (inj && *inj) || (lb && atoi(lb) != 0) || (mps && *mps);
+    return (inj && *inj) || (lb && atoi(lb) != 0) || (mps && *mps) || tool_injected();
 }
 static StackWS stack_ws(const StackGeo &g) {
     Carve c;
