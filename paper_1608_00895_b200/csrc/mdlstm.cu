@@ -49,7 +49,14 @@ struct MdK {  // kernel arguments
     float *dcu, *dcv;        // [4][U][V][B][H]: dc this cell passes to its u- / v-predecessor
     __half *da16;            // [4][prow][5Hp]
     __half *dap;             // [cells][20Hp]
+    unsigned long long *trace;  // debug (BLSTM_TRACE builds): per-diagonal phase clocks of CTA 0
 };
+#ifdef BLSTM_TRACE
+#define WTRACE(s, k) \
+    if (trace) trace[(size_t)(s) * 16 + (k)] = (unsigned long long)clock64()
+#else
+#define WTRACE(s, k)
+#endif
 
 // Tile decomposition of one anti-diagonal: block = (direction k, 32-unit tile, group of 32 rows),
 // row = (cell on the diagonal, image); warp w of the block owns rows w, w+8, w+16, w+24 of its group
@@ -409,6 +416,582 @@ __global__ void __launch_bounds__(256) md_fwd_persist_kernel(MdK a, uint32_t *ba
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Tensor-core wavefront: one persistent CTA per (direction k,
+// image b).  Cells of different images or directions never depend on each other, so a CTA walks
+// all U+V-1 anti-diagonals of its image alone -- no grid barrier, the previous diagonal's state
+// stays in shared memory.  The recurrent weights are resident in TMEM as the tcgen05 A operand,
+// split hi + lo (fp16 each), and every contraction is the 3-term product A_hi B_hi + A_lo B_hi +
+// A_hi B_lo (operand error ~2^-22: the 2-D recurrence compounds errors along paths of up to U+V
+// cells and |c| grows with u+v, so one fp16 pass is not accurate enough).
+// Forward, diagonal d: Q = [Ru^T; Rv^T] . H_{d-1}^T  (M = 10 Hp gate rows in up to 5 tiles, N = the
+//   <= 32 cells of diagonal d-1, K = Hp); cell (u', v') takes column (u'-1) of the Ru half and
+//   column u' of the Rv half (its two predecessors on d-1), adds Z, and runs the gates and cell.
+// Backward, diagonal d (reverse): P = [Ru; Rv] . dA_{d+1}^T  (M = 2 Hp, K = 5 Hp split over four
+//   issuing warps into four accumulators, N = cells of d+1); dh of (u', v') = dy + P_u column of
+//   its u-successor (u'+1) + P_v column of its v-successor (u').
+// Requires Hp <= 64 and min(U, V) <= 32 (md_wave_ok); else the per-diagonal CUDA-core kernels run.
+// ---------------------------------------------------------------------------------------------
+constexpr int WV_N = 32;         // MMA N: cells of one diagonal (min(U, V) <= 32)
+constexpr int WV_THREADS = 512;  // 16 warps: thread = (unit pair jp = tid % 32, cell slot tid / 32)
+constexpr int WV_KW = 4;         // backward: K-split issuing warps / accumulators
+
+// element (n, k) of a [WV_N x K] K-major no-swizzle B operand: core matrices of 8 n x 8 k (128 B),
+// the WV_N / 8 of one K group contiguous, K groups WV_LBO bytes apart.  The 16-byte pad per K group
+// keeps the epilogue's stores conflict-free: a warp writes one n and 64 consecutive k, i.e. 8 K
+// groups, which would otherwise all start on the same bank (8-way conflicts).
+constexpr int WV_LBO = WV_N * 16 + 16;
+constexpr int WV_LBOH = WV_LBO / 2;  // in halves
+DEVI int wv_bidx(int n, int k) { return (k >> 3) * WV_LBOH + n * 8 + (k & 7); }
+__host__ DEVI int wv_bsize(int K) { return K / 8 * WV_LBOH; }  // halves of one B part
+DEVI uint32_t pack_h2(__half lo16, __half hi16) {
+    return (uint32_t)__half_as_ushort(lo16) | ((uint32_t)__half_as_ushort(hi16) << 16);
+}
+DEVI void split_h(float x, __half &hi, __half &lo) {
+    hi = __float2half_rn(x);
+    lo = __float2half_rn(x - __half2float(hi));
+}
+__host__ DEVI int wv_u0(int d, int V) { return d - V + 1 > 0 ? d - V + 1 : 0; }
+__host__ DEVI int wv_u1(int d, int U) { return d < U - 1 ? d : U - 1; }
+
+// per-cell constants of one diagonal (int32 offsets; md_wave_ok bounds them)
+struct WvCell {
+    int ck;    // direction-frame cell index ((k U + u') V + v') B + b
+    int cp;    // physical cell index (u V + v) B + b
+    int slot;  // row of the zero-bordered [(U+1)(V+1)B] direction-frame grid (h16 / da16)
+    int flags; // bit 0 mask, 1 has u-pred, 2 has v-pred, 3 has u-succ, 4 has v-succ
+};
+DEVI WvCell wv_cell(const MdK &a, int k, int b, int d, int i) {
+    const int up = wv_u0(d, a.V) + i, vp = d - up;
+    const int u = (k & 1) ? a.U - 1 - up : up, v = (k & 2) ? a.V - 1 - vp : vp;
+    WvCell c;
+    c.ck = ((k * a.U + up) * a.V + vp) * a.B + b;
+    c.cp = (u * a.V + v) * a.B + b;
+    c.slot = ((up + 1) * (a.V + 1) + vp + 1) * a.B + b;
+    c.flags = (a.mask[c.cp] != 0) | (up > 0) << 1 | (vp > 0) << 2 | (up + 1 < a.U) << 3 | (vp + 1 < a.V) << 4;
+    return c;
+}
+
+// A operand rows -> TMEM (hi at column col_hi, lo at col_lo; ncol 32-bit columns = 2 ncol K values
+// per row).  row_val(r, kk) gives the fp32 value; warp w writes lanes 32 (w & 3) .. of tile mt for
+// the 8-column blocks with (block % 4) == (w >> 2).
+template <typename F>
+DEVI void wv_load_a(uint32_t tmem, int mt, uint32_t col_hi, uint32_t col_lo, int ncol, F row_val) {
+    const int w = warp_id(), l = lane_id(), q = w & 3;
+    const int r = mt * 128 + 32 * q + l;
+    for (int c0 = 8 * (w >> 2); c0 < ncol; c0 += 32) {
+        uint32_t vh[8], vl[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int kk = 2 * (c0 + i);
+            __half h0, l0, h1, l1;
+            split_h(row_val(r, kk), h0, l0);
+            split_h(row_val(r, kk + 1), h1, l1);
+            vh[i] = pack_h2(h0, h1);
+            vl[i] = pack_h2(l0, l1);
+        }
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+        tmem_st8(lane_base + col_hi + c0, vh);
+        tmem_st8(lane_base + col_lo + c0, vl);
+    }
+}
+// 32 lanes x 8 columns load
+DEVI void tmem_ld8f(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+// issue the three split products D (+)= A_hi B_hi + A_lo B_hi + A_hi B_lo over K steps [ks0, ks1)
+DEVI void wv_mma3(uint32_t dt, uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl, int ks0, int ks1, uint32_t idesc) {
+    // descriptor of K step ks = that of step 0 + ks * 2 * WV_LBO bytes in the 14-bit address field
+    // (shared-memory addresses < 256 KB: no carry out of the field)
+    const uint64_t dh0 = sdesc_noswz(bh, WV_LBO, 128), dl0 = sdesc_noswz(bl, WV_LBO, 128);
+    constexpr uint64_t DKS = 2 * WV_LBO / 16;
+    for (int ks = ks0; ks < ks1; ++ks) mma_f16_ts_w(dt, ah + ks * 8, dh0 + ks * DKS, idesc, ks > ks0);
+    for (int ks = ks0; ks < ks1; ++ks) mma_f16_ts_w(dt, al + ks * 8, dh0 + ks * DKS, idesc, 1);
+    for (int ks = ks0; ks < ks1; ++ks) mma_f16_ts_w(dt, ah + ks * 8, dl0 + ks * DKS, idesc, 1);
+}
+
+__global__ void __launch_bounds__(WV_THREADS, 1) md_wave_fwd_kernel(MdK a) {
+    extern __shared__ uint8_t wv_smem[];
+    uint8_t *sm = (uint8_t *)(((uintptr_t)wv_smem + 1023) & ~(uintptr_t)1023);
+    const int Hp = a.Hp, H = a.H, G5 = 5 * Hp, R10 = 10 * Hp, U = a.U, V = a.V, B = a.B;
+    const int k = blockIdx.x / B, b = blockIdx.x - k * B;
+    const int Mt = (R10 + 127) / 128;
+    float *Zs = (float *)sm;                       // [2][WV_N][5Hp]  Z of the cells of a diagonal
+    float *stg = Zs + 2 * WV_N * G5;               // [WV_N][10Hp]    Q^T (column-major staging)
+    __half *Bh = (__half *)(stg + WV_N * R10);     // [Hp/8][WV_N][8] (+pad) h of the previous diagonal, hi
+    __half *Bl = Bh + wv_bsize(Hp);                //                  and lo parts
+    float *cst = (float *)(Bl + wv_bsize(Hp));     // [2][WV_N][Hp]   c of the previous / this diagonal
+    WvCell *tab = (WvCell *)(cst + 2 * WV_N * Hp); // [2][WV_N]       cells of diagonals d, d+1
+    uint64_t *bars = (uint64_t *)(tab + 2 * WV_N); // [0] mma, [1..2] Z landed
+    uint32_t *tslot = (uint32_t *)(bars + 4);
+    const int w = warp_id(), l = lane_id(), tid = threadIdx.x;
+    const int prow = (U + 1) * (V + 1) * B;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], Mt);
+        mbar_init(&bars[1], 1);
+        mbar_init(&bars[2], 1);
+        fence_mbar_init();
+    }
+    if (w == 0) {
+        tmem_alloc(tslot, 512);
+        tmem_relinquish();
+    }
+    for (int e = tid; e < wv_bsize(Hp); e += WV_THREADS) reinterpret_cast<uint32_t *>(Bh)[e] = 0u;  // Bh + Bl
+    if (tid < WV_N && tid <= wv_u1(0, U) - wv_u0(0, V)) tab[tid] = wv_cell(a, k, b, 0, tid);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    // TMEM columns: A_hi tile mt at [mt Hp/2, ...), A_lo at Mt Hp/2 + mt Hp/2, D tile mt at Mt Hp + 32 mt
+    const uint32_t colAl = Mt * Hp / 2, colD = Mt * Hp;
+    const float *Ru = a.theta + k * a.P1 + (long)a.D * 5 * H, *Rv = Ru + (long)H * 5 * H;
+    for (int mt = 0; mt < Mt; ++mt)  // row r = wv 5Hp + q Hp + jj: gate column q H + jj of R_wv; K = unit
+        wv_load_a(tmem, mt, mt * Hp / 2, colAl + mt * Hp / 2, Hp / 2, [&](int r, int kk) -> float {
+            const int wv = r / G5, n = r - wv * G5, q = n / Hp, jj = n - q * Hp;
+            return (r < R10 && jj < H && kk < H) ? (wv ? Rv : Ru)[(long)kk * 5 * H + q * H + jj] : 0.f;
+        });
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    const int ND = U + V - 1;
+    auto issue_z = [&](int d, int sl) {  // warp 15: lane i copies cell i's Z row (5Hp fp32)
+        const int u0 = wv_u0(d, V), n = wv_u1(d, U) - u0 + 1;
+        if (l == 0) mbar_arrive_expect_tx(&bars[1 + sl], (uint32_t)(n * G5 * 4));
+        __syncwarp();
+        if (l < n) {
+            const int up = u0 + l, vp = d - up;
+            const int u = (k & 1) ? U - 1 - up : up, v = (k & 2) ? V - 1 - vp : vp;
+            const long cp = ((long)u * V + v) * B + b;
+            bulk_g2s(smem_u32(Zs + (sl * WV_N + l) * G5), a.z + cp * 20 * Hp + (long)k * G5, (uint32_t)(G5 * 4),
+                     &bars[1 + sl]);
+        }
+    };
+    if (w == 15) issue_z(0, 0);
+    const int j = 2 * (tid & 31), cs = tid >> 5;  // epilogue: units j, j+1 of cells cs, cs + 16
+    const bool j0 = j < H, j1 = j + 1 < H, hodd = H & 1;
+    const uint32_t idesc = idesc_f16(128, WV_N, 0, 0);
+    uint32_t mph = 0;
+#ifdef BLSTM_TRACE
+    unsigned long long *trace = (blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
+#endif
+    for (int d = 0; d < ND; ++d) {
+        const int sl = d & 1;
+        WTRACE(d, 0);
+        const int u0 = wv_u0(d, V), n = wv_u1(d, U) - u0 + 1;
+        const int pu0 = d > 0 ? wv_u0(d - 1, V) : 0;
+        if (d > 0 && w < Mt) {  // Q tile w = A_w . H_{d-1}^T, three products
+            tc_fence_after();
+            wv_mma3(tmem + colD + 32 * w, tmem + w * Hp / 2, tmem + colAl + w * Hp / 2, smem_u32(Bh), smem_u32(Bl), 0,
+                    Hp / 16, idesc);
+            mma_commit_w(&bars[0]);
+        }
+        WTRACE(d, 1);
+        if (w == 15 && d + 1 < ND) {
+            issue_z(d + 1, sl ^ 1);  // its slot was last read at d-1
+            const int n1 = wv_u1(d + 1, U) - wv_u0(d + 1, V) + 1;
+            if (l < n1) tab[(sl ^ 1) * WV_N + l] = wv_cell(a, k, b, d + 1, l);  // read after the next barriers
+        }
+        WTRACE(d, 2);
+        // one warp waits for Z and the MMAs (spinning warps would take issue slots from the MMA
+        // issue); the CTA barrier then releases the rest (hardware-blocking, no polling)
+        if (w == Mt) {
+            mbar_wait(&bars[1 + sl], (d >> 1) & 1);
+            if (d > 0) mbar_wait(&bars[0], mph);
+        }
+        if (d > 0) mph ^= 1;
+        WTRACE(d, 3);
+        __syncthreads();
+        WTRACE(d, 4);
+        if (d > 0) {
+            tc_fence_after();
+            const int q = w & 3, cb = 8 * (w >> 2);
+            float v[5][8];  // all tiles' loads in flight, one wait
+#pragma unroll
+            for (int mt = 0; mt < 5; ++mt)
+                if (mt < Mt) tmem_ld8f(tmem + ((uint32_t)(32 * q) << 16) + colD + 32 * mt + cb, v[mt]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int mt = 0; mt < 5; ++mt) {
+                const int row = mt * 128 + 32 * q + l;
+                if (mt < Mt && row < R10) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) stg[(cb + c) * R10 + row] = v[mt][c];
+                }
+            }
+        }
+        WTRACE(d, 5);
+        tc_fence_before();
+        __syncthreads();
+        WTRACE(d, 6);
+        const float *cprev = cst + (sl ^ 1) * WV_N * Hp;
+        float *ccur = cst + sl * WV_N * Hp;
+        const float *zs = Zs + sl * WV_N * G5;
+        const WvCell *tb = tab + sl * WV_N;
+        if (j < Hp) {
+            for (int i = cs; i < n; i += 16) {
+                const WvCell ce = tb[i];
+                const int up = u0 + i;
+                const bool hasu = ce.flags & 2, hasv = ce.flags & 4, on = ce.flags & 1;
+                const int mu = up - 1 - pu0, mv = up - pu0;
+                const float2 cu = hasu ? *reinterpret_cast<const float2 *>(cprev + mu * Hp + j) : make_float2(0.f, 0.f);
+                const float2 cv = hasv ? *reinterpret_cast<const float2 *>(cprev + mv * Hp + j) : make_float2(0.f, 0.f);
+                float2 g[5], h = make_float2(0.f, 0.f), cn;
+                if (on) {
+                    float2 pre[5];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) {
+                        float2 s = *reinterpret_cast<const float2 *>(zs + i * G5 + q * Hp + j);
+                        if (hasu) {
+                            const float2 t = *reinterpret_cast<const float2 *>(stg + mu * R10 + q * Hp + j);
+                            s.x += t.x; s.y += t.y;
+                        }
+                        if (hasv) {
+                            const float2 t = *reinterpret_cast<const float2 *>(stg + mv * R10 + G5 + q * Hp + j);
+                            s.x += t.x; s.y += t.y;
+                        }
+                        pre[q] = s;
+                    }
+                    if (!a.stable) {  // [i, fu, fv, g, o]
+#pragma unroll
+                        for (int q = 0; q < 5; ++q)
+                            g[q] = q == 3 ? make_float2(mth(pre[q].x), mth(pre[q].y)) : make_float2(msg(pre[q].x), msg(pre[q].y));
+                        cn.x = g[1].x * cu.x + g[2].x * cv.x + g[0].x * g[3].x;
+                        cn.y = g[1].y * cu.y + g[2].y * cv.y + g[0].y * g[3].y;
+                        h = make_float2(g[4].x * mth(cn.x), g[4].y * mth(cn.y));
+                    } else {          // [i, f, g, o, lambda]
+#pragma unroll
+                        for (int q = 0; q < 5; ++q)
+                            g[q] = q == 2 ? make_float2(mth(pre[q].x), mth(pre[q].y)) : make_float2(msg(pre[q].x), msg(pre[q].y));
+                        cn.x = g[1].x * (g[4].x * cu.x + (1.f - g[4].x) * cv.x) + g[0].x * g[2].x;
+                        cn.y = g[1].y * (g[4].y * cu.y + (1.f - g[4].y) * cv.y) + g[0].y * g[2].y;
+                        h = make_float2(g[3].x * mth(cn.x), g[3].y * mth(cn.y));
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) g[q] = make_float2(0.f, 0.f);
+                    cn = hasu ? cu : cv;  // masked: c carried (0 without predecessors), h = 0
+                }
+                if (!j0) { h.x = 0.f; cn.x = 0.f; }  // padding units stay 0 (B operand K padding)
+                if (!j1) { h.y = 0.f; cn.y = 0.f; }
+                *reinterpret_cast<float2 *>(ccur + i * Hp + j) = cn;
+                __half hx, lx, hy, ly;
+                split_h(h.x, hx, lx);
+                split_h(h.y, hy, ly);
+                *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, j)) = pack_h2(hx, hy);
+                *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, j)) = pack_h2(lx, ly);
+                if (j0) {  // saved state (Hp-strided rows: pairs stay 8-byte aligned) and the outputs
+                    float *ac = a.act + (long)ce.ck * G5 + j;
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) *reinterpret_cast<float2 *>(ac + q * Hp) = g[q];
+                    *reinterpret_cast<float2 *>(a.c + (long)ce.ck * Hp + j) = cn;
+                    *reinterpret_cast<__half2 *>(a.h16 + ((long)k * prow + ce.slot) * Hp + j) = __floats2half2_rn(h.x, h.y);
+                    float *yp = a.y + (long)ce.cp * 4 * H + k * H + j;
+                    if (!hodd && j1) {
+                        *reinterpret_cast<float2 *>(yp) = h;
+                    } else {
+                        yp[0] = h.x;
+                        if (j1) yp[1] = h.y;
+                    }
+                }
+            }
+        }
+        WTRACE(d, 7);
+        fence_async_smem();  // B written by the generic proxy, read by the next MMAs
+        tc_fence_before();
+        __syncthreads();
+        WTRACE(d, 8);
+    }
+    if (w == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+__global__ void __launch_bounds__(WV_THREADS, 1) md_wave_bwd_kernel(MdK a) {
+    extern __shared__ uint8_t wv_smem[];
+    uint8_t *sm = (uint8_t *)(((uintptr_t)wv_smem + 1023) & ~(uintptr_t)1023);
+    const int Hp = a.Hp, H = a.H, G5 = 5 * Hp, R2 = 2 * Hp, U = a.U, V = a.V, B = a.B;
+    const int k = blockIdx.x / B, b = blockIdx.x - k * B;
+    float *stg = (float *)sm;                      // [WV_N][2Hp]   P^T (column-major staging), x 2^DA_SHIFT
+    __half *Bh = (__half *)(stg + WV_N * R2);      // [5Hp/8][WV_N][8] (+pad) dA x 2^DA_SHIFT of diagonal d+1, hi
+    __half *Bl = Bh + wv_bsize(G5);                //                   and lo parts
+    float *acts = (float *)(Bl + wv_bsize(G5));    // [2][WV_N][5Hp] saved gate activations of a diagonal
+    float *cr = acts + 2 * WV_N * G5;              // [3][WV_N][Hp]  c of diagonals d, d-1 (ring by d % 3)
+    float *dcu = cr + 3 * WV_N * Hp;               // [2][WV_N][Hp]  dc passed to the u- / v-predecessor
+    float *dcv = dcu + 2 * WV_N * Hp;
+    float *dys = dcv + 2 * WV_N * Hp;              // [2][WV_N][Hp]  dy of a diagonal's cells
+    WvCell *tab = (WvCell *)(dys + 2 * WV_N * Hp); // [2][WV_N]
+    uint64_t *bars = (uint64_t *)(tab + 2 * WV_N); // [0] mma, [1..2] inputs landed
+    uint32_t *tslot = (uint32_t *)(bars + 4);
+    const int w = warp_id(), l = lane_id(), tid = threadIdx.x;
+    const int prow = (U + 1) * (V + 1) * B;
+    const float scale = (float)(1 << DA_SHIFT), unscale = 1.f / scale;
+    const int KS = G5 / 16;  // K steps of the contraction
+
+    if (tid == 0) {
+        mbar_init(&bars[0], WV_KW);
+        mbar_init(&bars[1], 1);
+        mbar_init(&bars[2], 1);
+        fence_mbar_init();
+    }
+    if (w == 0) {
+        tmem_alloc(tslot, 512);
+        tmem_relinquish();
+    }
+    for (int e = tid; e < wv_bsize(G5); e += WV_THREADS) reinterpret_cast<uint32_t *>(Bh)[e] = 0u;  // Bh + Bl
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    // TMEM: A_hi [0, 5Hp/2), A_lo [5Hp/2, 5Hp), accumulator a at 5Hp + 32 a
+    const uint32_t colAl = G5 / 2, colD = G5;
+    const float *Ru = a.theta + k * a.P1 + (long)a.D * 5 * H, *Rv = Ru + (long)H * 5 * H;
+    // row r = wv Hp + unit; K index q Hp + jj = gate column q H + jj of that unit's R_wv row
+    wv_load_a(tmem, 0, 0, colAl, G5 / 2, [&](int r, int kk) -> float {
+        const int wv = r / Hp, rr = r - wv * Hp, q = kk / Hp, jj = kk - q * Hp;
+        return (r < R2 && rr < H && jj < H) ? (wv ? Rv : Ru)[(long)rr * 5 * H + q * H + jj] : 0.f;
+    });
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    const int ND = U + V - 1;
+    const bool hodd = H & 1, dy_bulk = ((H * 4) & 15) == 0;  // dy rows by bulk copy when 16-byte sized
+    // inputs of diagonal d2 (warp 15, lane i = cell i): the saved activations, dy and the cell table
+    // of its cells, c of diagonal d2-1 (the predecessors); c of d2 itself came with d2+1 (with_c for
+    // the first)
+    auto issue_in = [&](int d2, bool with_c) {
+        const int sl = d2 & 1;
+        const int u0 = wv_u0(d2, V), n = wv_u1(d2, U) - u0 + 1;
+        const int np = d2 >= 1 ? wv_u1(d2 - 1, U) - wv_u0(d2 - 1, V) + 1 : 0;
+        WvCell ce{};
+        if (l < n) ce = wv_cell(a, k, b, d2, l);
+        uint32_t bytes = (uint32_t)(n * G5 * 4 + np * Hp * 4 + (with_c ? n * Hp * 4 : 0) + (dy_bulk ? n * H * 4 : 0));
+        if (l == 0) mbar_arrive_expect_tx(&bars[1 + sl], bytes);
+        __syncwarp();
+        if (l < n) {
+            tab[sl * WV_N + l] = ce;
+            bulk_g2s(smem_u32(acts + (sl * WV_N + l) * G5), a.act + (long)ce.ck * G5, (uint32_t)(G5 * 4), &bars[1 + sl]);
+            if (with_c)
+                bulk_g2s(smem_u32(cr + ((d2 % 3) * WV_N + l) * Hp), a.c + (long)ce.ck * Hp, (uint32_t)(Hp * 4), &bars[1 + sl]);
+            const float *dyp = a.dy + (long)ce.cp * 4 * H + k * H;
+            float *dyd = dys + (sl * WV_N + l) * Hp;
+            if (dy_bulk)
+                bulk_g2s(smem_u32(dyd), dyp, (uint32_t)(H * 4), &bars[1 + sl]);
+            else
+                for (int e = 0; e < H; ++e) dyd[e] = dyp[e];  // (rare: H * 4 not a multiple of 16)
+        }
+        if (l < np) {
+            const int up = wv_u0(d2 - 1, V) + l;
+            const int ckp = ((k * U + up) * V + (d2 - 1 - up)) * B + b;
+            bulk_g2s(smem_u32(cr + (((d2 + 2) % 3) * WV_N + l) * Hp), a.c + (long)ckp * Hp, (uint32_t)(Hp * 4),
+                     &bars[1 + sl]);
+        }
+    };
+    if (w == 15) issue_in(ND - 1, true);
+    const int j = 2 * (tid & 31), cs = tid >> 5;
+    const bool j0 = j < H, j1 = j + 1 < H;
+    const uint32_t idesc = idesc_f16(128, WV_N, 0, 0);
+    uint32_t mph = 0, iph = 0;
+    const int ks0 = (w * KS) / WV_KW, ks1 = ((w + 1) * KS) / WV_KW;  // this warp's K range (w < WV_KW)
+#ifdef BLSTM_TRACE
+    unsigned long long *trace = (blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
+#endif
+    for (int d = ND - 1; d >= 0; --d) {
+        const int sl = d & 1;
+        WTRACE(ND - 1 - d, 0);
+        const int u0 = wv_u0(d, V), n = wv_u1(d, U) - u0 + 1;
+        const bool has_succ = d + 1 < ND;
+        const int su0 = has_succ ? wv_u0(d + 1, V) : 0, pu0 = d > 0 ? wv_u0(d - 1, V) : 0;
+        if (has_succ && w < WV_KW) {  // P_w = A[:, K range w] . dA_{d+1}[:, K range w]^T, three products
+            tc_fence_after();
+            wv_mma3(tmem + colD + 32 * w, tmem, tmem + colAl, smem_u32(Bh), smem_u32(Bl), ks0, ks1, idesc);
+            mma_commit_w(&bars[0]);
+        }
+        WTRACE(ND - 1 - d, 1);
+        if (w == 15 && d >= 1) issue_in(d - 1, false);  // its slots were last read at d+1
+        WTRACE(ND - 1 - d, 2);
+        if (w == WV_KW) {  // one warp waits (see the forward), the CTA barrier releases the rest
+            mbar_wait(&bars[1 + sl], (iph >> sl) & 1);
+            if (has_succ) mbar_wait(&bars[0], mph);
+        }
+        iph ^= 1u << sl;
+        if (has_succ) mph ^= 1;
+        WTRACE(ND - 1 - d, 3);
+        __syncthreads();
+        WTRACE(ND - 1 - d, 4);
+        if (has_succ) {
+            tc_fence_after();
+            const int q = w & 3, cb = 8 * (w >> 2);
+            float x[WV_KW][8], v[8];  // KS = 5Hp/16 >= 5: every K range is non-empty
+#pragma unroll
+            for (int aa = 0; aa < WV_KW; ++aa) tmem_ld8f(tmem + ((uint32_t)(32 * q) << 16) + colD + 32 * aa + cb, x[aa]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = (x[0][c] + x[1][c]) + (x[2][c] + x[3][c]);
+            const int row = 32 * q + l;
+            if (row < R2) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) stg[(cb + c) * R2 + row] = v[c];
+            }
+        }
+        WTRACE(ND - 1 - d, 5);
+        tc_fence_before();
+        __syncthreads();
+        WTRACE(ND - 1 - d, 6);
+        const float *ac_s = acts + sl * WV_N * G5, *c_s = cr + (d % 3) * WV_N * Hp;
+        const float *cp_s = cr + ((d + 2) % 3) * WV_N * Hp;  // c of diagonal d-1
+        const float *dcu_p = dcu + (sl ^ 1) * WV_N * Hp, *dcv_p = dcv + (sl ^ 1) * WV_N * Hp;
+        float *dcu_c = dcu + sl * WV_N * Hp, *dcv_c = dcv + sl * WV_N * Hp;
+        const float *dy_s = dys + sl * WV_N * Hp;
+        const WvCell *tb = tab + sl * WV_N;
+        if (j < Hp) {
+            for (int i = cs; i < n; i += 16) {
+                const WvCell ce = tb[i];
+                const int up = u0 + i;
+                const bool su = ce.flags & 8, sv = ce.flags & 16, on = ce.flags & 1;
+                float2 da[5], ou = make_float2(0.f, 0.f), ov = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < 5; ++q) da[q] = make_float2(0.f, 0.f);
+                const int iu = up + 1 - su0, iv = up - su0;  // successor columns on d+1
+                float2 dc = make_float2(0.f, 0.f);
+                if (su) {
+                    const float2 t = *reinterpret_cast<const float2 *>(dcu_p + iu * Hp + j);
+                    dc.x += t.x; dc.y += t.y;
+                }
+                if (sv) {
+                    const float2 t = *reinterpret_cast<const float2 *>(dcv_p + iv * Hp + j);
+                    dc.x += t.x; dc.y += t.y;
+                }
+                if (!on) {
+                    if (ce.flags & 2) ou = dc;                       // the carried c came from the u-,
+                    else if (ce.flags & 4) ov = dc;                  // else the v-predecessor
+                } else {
+                    float2 dh = *reinterpret_cast<const float2 *>(dy_s + i * Hp + j);  // (.y unused past H)
+                    if (su) {
+                        const float2 t = *reinterpret_cast<const float2 *>(stg + iu * R2 + j);
+                        dh.x += t.x * unscale; dh.y += t.y * unscale;
+                    }
+                    if (sv) {
+                        const float2 t = *reinterpret_cast<const float2 *>(stg + iv * R2 + Hp + j);
+                        dh.x += t.x * unscale; dh.y += t.y * unscale;
+                    }
+                    const float *acl = ac_s + i * G5 + j;
+                    const float2 c = *reinterpret_cast<const float2 *>(c_s + i * Hp + j);
+                    const float2 cu = (ce.flags & 2) ? *reinterpret_cast<const float2 *>(cp_s + (up - 1 - pu0) * Hp + j)
+                                                     : make_float2(0.f, 0.f);
+                    const float2 cv = (ce.flags & 4) ? *reinterpret_cast<const float2 *>(cp_s + (up - pu0) * Hp + j)
+                                                     : make_float2(0.f, 0.f);
+                    float2 A[5];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) A[q] = *reinterpret_cast<const float2 *>(acl + q * Hp);
+                    auto cellg = [&](float dhv, float dcv_, float cc, float cuu, float cvv, const float *g, float *o,
+                                     float &ouu, float &ovv) {
+                        const float tc = mth(cc);
+                        const float dct = dcv_ + dhv * (a.stable ? g[3] : g[4]) * (1.f - tc * tc);
+                        if (!a.stable) {  // [i, fu, fv, g, o]
+                            o[0] = dct * g[3] * g[0] * (1.f - g[0]);
+                            o[1] = dct * cuu * g[1] * (1.f - g[1]);
+                            o[2] = dct * cvv * g[2] * (1.f - g[2]);
+                            o[3] = dct * g[0] * (1.f - g[3] * g[3]);
+                            o[4] = dhv * tc * g[4] * (1.f - g[4]);
+                            ouu = dct * g[1];
+                            ovv = dct * g[2];
+                        } else {          // [i, f, g, o, lambda]
+                            const float m = g[4] * cuu + (1.f - g[4]) * cvv;
+                            o[0] = dct * g[2] * g[0] * (1.f - g[0]);
+                            o[1] = dct * m * g[1] * (1.f - g[1]);
+                            o[2] = dct * g[0] * (1.f - g[2] * g[2]);
+                            o[3] = dhv * tc * g[3] * (1.f - g[3]);
+                            o[4] = dct * g[1] * (cuu - cvv) * g[4] * (1.f - g[4]);
+                            ouu = dct * g[1] * g[4];
+                            ovv = dct * g[1] * (1.f - g[4]);
+                        }
+                    };
+                    float gx[5], gy[5], ox[5], oy[5];
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) { gx[q] = A[q].x; gy[q] = A[q].y; }
+                    cellg(dh.x, dc.x, c.x, cu.x, cv.x, gx, ox, ou.x, ov.x);
+                    cellg(dh.y, dc.y, c.y, cu.y, cv.y, gy, oy, ou.y, ov.y);
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) da[q] = make_float2(ox[q], oy[q]);
+                    if (!j0) { ou.x = ov.x = 0.f; }
+                    if (!j1) { ou.y = ov.y = 0.f; }
+                }
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    if (!j0) da[q].x = 0.f;
+                    if (!j1) da[q].y = 0.f;
+                }
+                *reinterpret_cast<float2 *>(dcu_c + i * Hp + j) = ou;
+                *reinterpret_cast<float2 *>(dcv_c + i * Hp + j) = ov;
+                __half2 *dpp = reinterpret_cast<__half2 *>(a.dap + (long)ce.cp * 20 * Hp + k * G5 + j);
+                __half2 *d16 = reinterpret_cast<__half2 *>(a.da16 + ((long)k * prow + ce.slot) * G5 + j);
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    __half hx, lx, hy, ly;
+                    split_h(da[q].x * scale, hx, lx);
+                    split_h(da[q].y * scale, hy, ly);
+                    *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, q * Hp + j)) = pack_h2(hx, hy);
+                    *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, q * Hp + j)) = pack_h2(lx, ly);
+                    if (j0) {
+                        dpp[q * Hp / 2] = __halves2half2(hx, hy);
+                        d16[q * Hp / 2] = __halves2half2(hx, hy);
+                    }
+                }
+            }
+        }
+        WTRACE(ND - 1 - d, 7);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        WTRACE(ND - 1 - d, 8);
+    }
+    if (w == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+size_t wv_fwd_smem(int Hp) {
+    return 1024 + (size_t)(2 * WV_N * 5 * Hp + WV_N * 10 * Hp + 2 * WV_N * Hp) * 4 + (size_t)2 * wv_bsize(Hp) * 2 +
+           2 * WV_N * sizeof(WvCell) + 64;
+}
+size_t wv_bwd_smem(int Hp) {
+    return 1024 + (size_t)(WV_N * 2 * Hp + 2 * WV_N * 5 * Hp + 3 * WV_N * Hp + 6 * WV_N * Hp) * 4 +
+           (size_t)2 * wv_bsize(5 * Hp) * 2 + 2 * WV_N * sizeof(WvCell) + 64;
+}
+// the tensor-core wavefront applies (BLSTM_MD_WAVE=0: never)
+bool md_wave_ok(const MdGeo &g) {
+    const bool off = getenv("BLSTM_MD_WAVE") && atoi(getenv("BLSTM_MD_WAVE")) == 0;  // read per call (tests A/B)
+    if (off) return false;
+    const int mn = g.U < g.V ? g.U : g.V;
+    // int32 cell offsets (WvCell) and grid rows
+    const bool fits32 = g.cells * 20 * g.Hp < (1L << 31) && 4 * g.prow * 5 * g.Hp < (1L << 31);
+    return fits32 && g.Hp <= 64 && mn <= WV_N && wv_fwd_smem(g.Hp) <= 227 * 1024 && wv_bwd_smem(g.Hp) <= 227 * 1024;
+}
+int md_wave_launch(bool fwd, const MdGeo &g, const MdK &a, cudaStream_t st) {
+    const void *fn = fwd ? (const void *)md_wave_fwd_kernel : (const void *)md_wave_bwd_kernel;
+    const size_t smem = fwd ? wv_fwd_smem(g.Hp) : wv_bwd_smem(g.Hp);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -5;
+    ProfScope ps(fwd ? PROF_REC_FWD : PROF_REC_BWD, st);
+    if (fwd)
+        md_wave_fwd_kernel<<<4 * g.B, WV_THREADS, smem, st>>>(a);
+    else
+        md_wave_bwd_kernel<<<4 * g.B, WV_THREADS, smem, st>>>(a);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 // W16 [20Hp][Dp]: row k*5Hp + q*Hp + j <- W_k[f][q*H + j] as hi + lo fp16 parts (w16lo may be
 // null); bq [20Hp] <- b_k
 __global__ void md_pack_kernel(const float *theta, long P1, int D, int H, int Hp, int Dp, __half *w16, __half *w16lo,
@@ -513,8 +1096,8 @@ MdWS md_ws(const MdGeo &g) {
     w.total = o;
     size_t r = 0;
     auto rtake = [&](size_t b) { size_t q = r; r += al(b); return q; };
-    w.act = rtake(st * 5 * g.H * 4);
-    w.c = rtake(st * g.H * 4);
+    w.act = rtake(st * 5 * g.Hp * 4);  // row stride 5H (per-diagonal kernels) or 5Hp (wavefront)
+    w.c = rtake(st * g.Hp * 4);
     w.h16 = rtake((size_t)4 * g.prow * g.Hp * 2);
     w.rtotal = r;
     return w;
@@ -532,6 +1115,7 @@ static MdK md_args(const MdGeo &g, const float *theta, const uint8_t *mask, uint
     a.rt = (const float *)(ws + w.rt);
     a.daf = (float *)(ws + w.daf); a.dcu = (float *)(ws + w.dcu); a.dcv = (float *)(ws + w.dcv);
     a.da16 = (__half *)(ws + w.da16); a.dap = (__half *)(ws + w.dap);
+    a.trace = nullptr;
     return a;
 }
 
@@ -598,6 +1182,8 @@ int md_forward(const MdGeo &g, const float *theta, const float *x, const uint8_t
     gz2.beta = 1; gz2.bias = nullptr;
     if (gemm_f16({x16, g.Dp, 0}, {w16lo, g.Dp, 0}, gz2, 0, st)) return -5;
     if (gemm_f16({x16lo, g.Dp, 0}, {w16, g.Dp, 0}, gz2, 0, st)) return -5;
+    a.trace = rec_trace_fwd();
+    if (md_wave_ok(g)) return md_wave_launch(true, g, a, st);
     {
         const int rc = md_persist(true, a, g, (uint32_t *)(ws + w.bar), st);
         if (rc <= 0) return rc;
@@ -621,17 +1207,23 @@ int md_backward(const MdGeo &g, const float *theta, const float *x, const uint8_
     a.dy = dy;
     const float alpha = 1.f / (float)(1 << DA_SHIFT);
     __half *x16 = (__half *)(ws + w.x16), *w16 = (__half *)(ws + w.w16);
+    const bool wave = md_wave_ok(g);
     {
         ProfScope ps(PROF_OTHER, st);
         md_pack_kernel<<<grid1(20L * g.Hp * g.Dp), 256, 0, st>>>(theta, a.P1, g.D, g.H, g.Hp, g.Dp, w16, nullptr,
                                                                  (float *)(ws + w.gb));
-        md_pack_rt_kernel<<<grid1(8L * 5 * g.H * g.H), 256, 0, st>>>(theta, a.P1, g.D, g.H, (float *)(ws + w.rt));
-        note_launch(2);
+        note_launch();
+        if (!wave) {
+            md_pack_rt_kernel<<<grid1(8L * 5 * g.H * g.H), 256, 0, st>>>(theta, a.P1, g.D, g.H, (float *)(ws + w.rt));
+            note_launch();
+        }
     }
     if (cast_x_f16(x, g.D, g.D, x16, g.Dp, g.cells, st)) return -5;
     if (cudaMemsetAsync(ws + w.da16, 0, (size_t)4 * g.prow * 5 * g.Hp * 2, st) != cudaSuccess) return -5;
     if (cudaMemsetAsync(ws + w.dap, 0, (size_t)g.cells * 20 * g.Hp * 2, st) != cudaSuccess) return -5;
-    const int prc = md_persist(false, a, g, (uint32_t *)(ws + w.bar), st);
+    a.trace = rec_trace_bwd();
+    if (wave && md_wave_launch(false, g, a, st)) return -5;
+    const int prc = wave ? 0 : md_persist(false, a, g, (uint32_t *)(ws + w.bar), st);
     if (prc < 0) return prc;
     const std::vector<uint64_t> key{4, (uint64_t)g.U, (uint64_t)g.V, (uint64_t)g.B, (uint64_t)g.D, (uint64_t)g.H,
                                     (uint64_t)g.stable, u64(theta), u64(mask), u64(dy), u64(ws), u64(res)};

@@ -3,10 +3,12 @@ U x V = 32 x 256 grid (text-line height x width after patching), B = 16 images, 
 channels, H units per direction (32 and 64), four directions, two-forget cell, full masks.
 
 Reported per forward+backward call: device time (CUDA events), grid cells per second, and the
-wavefront kernels' time (library launch events, categories rec_fwd / rec_bwd) against the
-FP32 CUDA-core roofline: the recurrent contraction is 2 x 5H x H FMAs per (cell, direction) in
-the forward and the same in the backward's dh; peak = 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz
-= 74.4 TFLOP/s."""
+wavefront kernels' time (library launch events, categories rec_fwd / rec_bwd).  The recurrent
+contraction is 2 x 5H x H multiply-adds per (cell, direction) in the forward and the same in the
+backward's dh.  Two paths (BLSTM_MD_WAVE=1 default / 0): the tensor-core wavefront (one CTA per
+(direction, image), 3-term split fp16 products on tcgen05; latency-bound: the per-diagonal chain of
+MMA -> TMEM -> gates -> next B operand inside one SM) and the CUDA-core per-diagonal kernels (fp32
+FMA; FP32 peak = 148 SMs x 128 lanes x 2 x 1.965 GHz = 74.4 TFLOP/s)."""
 import json
 import os
 import sys
@@ -27,6 +29,10 @@ def run(U, V, B, D, H, K=20):
     n, wsb, rsb = blstm.mdlstm_sizes(desc)
     g = torch.Generator(device=dev).manual_seed(0)
     th = 0.2 * torch.randn(n, device=dev, generator=g)
+    P1 = n // 4  # per direction: W [D,5H], Ru, Rv [H,5H], b [5H]; forget-gate biases -1.5 (fu + fv < 1:
+    for k in range(4):  # the two-forget cell stays finite over 287 diagonals)
+        o = k * P1 + D * 5 * H + 2 * H * 5 * H
+        th[o + H:o + 3 * H] -= 1.5
     x = torch.randn((U, V, B, D), device=dev, generator=g)
     m = torch.ones((U, V, B), dtype=torch.uint8, device=dev)
     dy = torch.randn((U, V, B, 4 * H), device=dev, generator=g)
@@ -57,7 +63,8 @@ def run(U, V, B, D, H, K=20):
     blstm.blstm_profile_enable(0)
     cells = U * V * B
     rec_flop = cells * 4 * 2 * 5 * H * H * 2  # per pass: 2 predecessors x 5H x H FMAs = 2 flop each
-    out = dict(U=U, V=V, B=B, D=D, H=H, diagonals=U + V - 1, ms_fwd_bwd=round(ms, 3),
+    out = dict(path="wavefront (tcgen05)" if os.environ.get("BLSTM_MD_WAVE", "1") != "0" else "per-diagonal (CUDA cores)",
+               U=U, V=V, B=B, D=D, H=H, diagonals=U + V - 1, ms_fwd_bwd=round(ms, 3),
                cells_per_s=round(cells / (ms * 1e-3)), wavefront_fwd_ms=round(fw[0], 3), wavefront_bwd_ms=round(bw[0], 3),
                gemm_ms=round(gm[0], 3), us_per_diagonal_fwd=round(1e3 * fw[0] / (U + V - 1), 2),
                us_per_diagonal_bwd=round(1e3 * bw[0] / (U + V - 1), 2),
@@ -70,5 +77,7 @@ def run(U, V, B, D, H, K=20):
 
 
 if __name__ == "__main__":
-    for H in (32, 64):
-        run(32, 256, 16, 16, H)
+    for wave in ("1", "0"):
+        os.environ["BLSTM_MD_WAVE"] = wave
+        for H in (32, 64):
+            run(32, 256, 16, 16, H)
