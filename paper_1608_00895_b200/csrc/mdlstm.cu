@@ -447,6 +447,14 @@ __host__ DEVI int wv_bsize(int K) { return K / 8 * WV_LBOH; }  // halves of one 
 DEVI uint32_t pack_h2(__half lo16, __half hi16) {
     return (uint32_t)__half_as_ushort(lo16) | ((uint32_t)__half_as_ushort(hi16) << 16);
 }
+// two values at once: packed conversions (one cvt.rn.f16x2.f32 per pair instead of two scalar ones)
+DEVI void split_h2(float x, float y, uint32_t &hi, uint32_t &lo) {
+    const __half2 h = __floats2half2_rn(x, y);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(x - hf.x, y - hf.y);
+    hi = *reinterpret_cast<const uint32_t *>(&h);
+    lo = *reinterpret_cast<const uint32_t *>(&l);
+}
 DEVI void split_h(float x, __half &hi, __half &lo) {
     hi = __float2half_rn(x);
     lo = __float2half_rn(x - __half2float(hi));
@@ -682,11 +690,10 @@ __global__ void __launch_bounds__(WV_THREADS, 1) md_wave_fwd_kernel(MdK a) {
                 if (!j0) { h.x = 0.f; cn.x = 0.f; }  // padding units stay 0 (B operand K padding)
                 if (!j1) { h.y = 0.f; cn.y = 0.f; }
                 *reinterpret_cast<float2 *>(ccur + i * Hp + j) = cn;
-                __half hx, lx, hy, ly;
-                split_h(h.x, hx, lx);
-                split_h(h.y, hy, ly);
-                *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, j)) = pack_h2(hx, hy);
-                *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, j)) = pack_h2(lx, ly);
+                uint32_t hh, hl;
+                split_h2(h.x, h.y, hh, hl);
+                *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, j)) = hh;
+                *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, j)) = hl;
                 if (j0) {  // saved state (Hp-strided rows: pairs stay 8-byte aligned) and the outputs
                     float *ac = a.act + (long)ce.ck * G5 + j;
 #pragma unroll
@@ -765,7 +772,7 @@ __global__ void __launch_bounds__(WV_THREADS, 1) md_wave_bwd_kernel(MdK a) {
     tc_fence_after();
 
     const int ND = U + V - 1;
-    const bool hodd = H & 1, dy_bulk = ((H * 4) & 15) == 0;  // dy rows by bulk copy when 16-byte sized
+    const bool dy_bulk = ((H * 4) & 15) == 0;  // dy rows by bulk copy when 16-byte sized
     // inputs of diagonal d2 (warp 15, lane i = cell i): the saved activations, dy and the cell table
     // of its cells, c of diagonal d2-1 (the predecessors); c of d2 itself came with d2+1 (with_c for
     // the first)
@@ -938,14 +945,13 @@ __global__ void __launch_bounds__(WV_THREADS, 1) md_wave_bwd_kernel(MdK a) {
                 __half2 *d16 = reinterpret_cast<__half2 *>(a.da16 + ((long)k * prow + ce.slot) * G5 + j);
 #pragma unroll
                 for (int q = 0; q < 5; ++q) {
-                    __half hx, lx, hy, ly;
-                    split_h(da[q].x * scale, hx, lx);
-                    split_h(da[q].y * scale, hy, ly);
-                    *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, q * Hp + j)) = pack_h2(hx, hy);
-                    *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, q * Hp + j)) = pack_h2(lx, ly);
+                    uint32_t hh, hl;
+                    split_h2(da[q].x * scale, da[q].y * scale, hh, hl);
+                    *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, q * Hp + j)) = hh;
+                    *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, q * Hp + j)) = hl;
                     if (j0) {
-                        dpp[q * Hp / 2] = __halves2half2(hx, hy);
-                        d16[q * Hp / 2] = __halves2half2(hx, hy);
+                        reinterpret_cast<uint32_t *>(dpp)[q * Hp / 2] = hh;
+                        reinterpret_cast<uint32_t *>(d16)[q * Hp / 2] = hh;
                     }
                 }
             }
@@ -1008,16 +1014,35 @@ __global__ void md_pack_kernel(const float *theta, long P1, int D, int H, int Hp
         if (f == 0) bq[row] = ok ? theta[k * P1 + (long)D * 5 * H + 2L * H * 5 * H + q * H + j] : 0.f;
     }
 }
-// x [cells][D] -> hi / lo fp16 parts [cells][Dp] (zero padded)
-__global__ void md_split_x_kernel(const float *x, int D, int Dp, long cells, __half *hi, __half *lo) {
+// the split-precision projection as ONE GEMM over a tripled K (Z written once):
+//   xcat [cells][3Dp] = [x_hi | x_hi | x_lo],  wcat [20Hp][3Dp] = [W_hi | W_lo | W_hi]
+//   Z = xcat wcat^T = x_hi W_hi + x_hi W_lo + x_lo W_hi  (zero padded past D)
+__global__ void md_split_x_kernel(const float *x, int D, int Dp, long cells, __half *xcat) {
     const long n = cells * Dp;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
         const long r = e / Dp;
         const int f = (int)(e - r * Dp);
         const float v = f < D ? x[r * D + f] : 0.f;
         const __half h = __float2half_rn(v);
-        hi[e] = h;
-        lo[e] = __float2half_rn(v - __half2float(h));
+        __half *row = xcat + r * 3 * Dp;
+        row[f] = h;
+        row[Dp + f] = h;
+        row[2 * Dp + f] = __float2half_rn(v - __half2float(h));
+    }
+}
+__global__ void md_pack_cat_kernel(const float *theta, long P1, int D, int H, int Hp, int Dp, __half *wcat, float *bq) {
+    const long n = 20L * Hp * Dp;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const int f = (int)(e % Dp);
+        const int row = (int)(e / Dp), k = row / (5 * Hp), q = (row / Hp) % 5, j = row % Hp;
+        const bool ok = j < H;
+        const float v = (ok && f < D) ? theta[k * P1 + (long)f * 5 * H + q * H + j] : 0.f;
+        const __half hi = __float2half_rn(v);
+        __half *r = wcat + (long)row * 3 * Dp;
+        r[f] = hi;
+        r[Dp + f] = __float2half_rn(v - __half2float(hi));
+        r[2 * Dp + f] = hi;
+        if (f == 0) bq[row] = ok ? theta[k * P1 + (long)D * 5 * H + 2L * H * 5 * H + q * H + j] : 0.f;
     }
 }
 // rt [4][2][5H][H] <- Ru_k^T, Rv_k^T
@@ -1075,9 +1100,9 @@ MdWS md_ws(const MdGeo &g) {
     auto take = [&](size_t b) { size_t r = o; o += al(b); return r; };
     const size_t cells = g.cells, st = 4 * cells;  // direction-frame elements per unit
     w.x16 = take(cells * g.Dp * 2);
-    w.x16lo = take(cells * g.Dp * 2);
+    w.x16lo = take(cells * 3 * g.Dp * 2);          // forward: xcat [cells][3Dp]
     w.w16 = take((size_t)20 * g.Hp * g.Dp * 2);
-    w.w16lo = take((size_t)20 * g.Hp * g.Dp * 2);
+    w.w16lo = take((size_t)20 * g.Hp * 3 * g.Dp * 2);  // forward: wcat [20Hp][3Dp]
     w.z = take(cells * 20 * g.Hp * 4);
     w.hf = take(st * g.H * 4);
     w.gb = take((size_t)20 * g.Hp * 4);  // bias vector in the forward, db in the backward
@@ -1163,25 +1188,20 @@ int md_forward(const MdGeo &g, const float *theta, const float *x, const uint8_t
     const MdWS w = md_ws(g);
     MdK a = md_args(g, theta, mask, ws, res);
     a.y = y;
-    __half *x16 = (__half *)(ws + w.x16), *w16 = (__half *)(ws + w.w16);
-    __half *x16lo = (__half *)(ws + w.x16lo), *w16lo = (__half *)(ws + w.w16lo);
+    __half *xcat = (__half *)(ws + w.x16lo), *wcat = (__half *)(ws + w.w16lo);
     float *bq = (float *)(ws + w.gb);
     {
         ProfScope ps(PROF_OTHER, st);
-        md_pack_kernel<<<grid1(20L * g.Hp * g.Dp), 256, 0, st>>>(theta, a.P1, g.D, g.H, g.Hp, g.Dp, w16, w16lo, bq);
-        md_split_x_kernel<<<grid1(g.cells * g.Dp), 256, 0, st>>>(x, g.D, g.Dp, g.cells, x16, x16lo);
+        md_pack_cat_kernel<<<grid1(20L * g.Hp * g.Dp), 256, 0, st>>>(theta, a.P1, g.D, g.H, g.Hp, g.Dp, wcat, bq);
+        md_split_x_kernel<<<grid1(g.cells * g.Dp), 256, 0, st>>>(x, g.D, g.Dp, g.cells, xcat);
         note_launch(2);
     }
     if (cudaMemsetAsync(res + w.h16, 0, (size_t)4 * g.prow * g.Hp * 2, st) != cudaSuccess) return -5;
     // Z = x W + b in split precision: x_hi W_hi + x_hi W_lo + x_lo W_hi (fp16 tensor-core operands,
     // fp32 accumulate; operand error ~2^-22 instead of 2^-11: the 2-D recurrence compounds the input
-    // error along paths of up to U+V cells)
-    GemmParams gz{(int)g.cells, 20 * g.Hp, g.Dp, (float *)(ws + w.z), 20L * g.Hp, 1.f, 0, bq, 0, 0};
-    if (gemm_f16({x16, g.Dp, 0}, {w16, g.Dp, 0}, gz, 0, st)) return -5;
-    GemmParams gz2 = gz;
-    gz2.beta = 1; gz2.bias = nullptr;
-    if (gemm_f16({x16, g.Dp, 0}, {w16lo, g.Dp, 0}, gz2, 0, st)) return -5;
-    if (gemm_f16({x16lo, g.Dp, 0}, {w16, g.Dp, 0}, gz2, 0, st)) return -5;
+    // error along paths of up to U+V cells), one GEMM over K = 3 Dp
+    GemmParams gz{(int)g.cells, 20 * g.Hp, 3 * g.Dp, (float *)(ws + w.z), 20L * g.Hp, 1.f, 0, bq, 0, 0};
+    if (gemm_f16({xcat, 3L * g.Dp, 0}, {wcat, 3L * g.Dp, 0}, gz, 0, st)) return -5;
     a.trace = rec_trace_fwd();
     if (md_wave_ok(g)) return md_wave_launch(true, g, a, st);
     {
