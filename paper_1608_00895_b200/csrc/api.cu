@@ -19,6 +19,16 @@
 
 using namespace blstm;
 
+// scatter-add output of a weight-gradient GEMM whose rows are the gate-interleaved columns
+// d 4Hq + 4u + gamma of dA (gemm.h GemmScatter): row (u, gamma) of direction d -> d dstride +
+// gamma H + u; column n -> n ld (colmode 0, n < ncols) or, for padded halves of width Hq, (h H + u) ld
+static GemmScatter scatter_gate_rows(float *dst, int H, int Hq, long dstride, int colmode, int ncols, long ld) {
+    GemmScatter s;
+    s.dst = dst; s.rowmode = 1; s.colmode = colmode; s.H = H; s.Hq = Hq; s.ncols = ncols;
+    s.dstride = dstride; s.ld = ld;
+    return s;
+}
+
 // ---------------------------------------------------------------------------
 // errors
 // ---------------------------------------------------------------------------
@@ -332,18 +342,19 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
         TRY(store_dx(dx, d->ldx, dX, g.Dp, g.D, g.TB, (d->flags & BLSTM_ACCUM_DX) ? 1 : 0, st), "store_dx");
     }
     {
+        // dW [D, 4H] += (dA^T x)^T, scattered from the gate-interleaved rows by the GEMM itself
         GemmParams gp{4 * g.Hq, g.Dp, (int)g.TB, dWT, g.Dp, a, 0, nullptr, 0, 0};
         gp.splitk_ws = (float *)(ws + w.gsk); gp.splitk_elems = GSK_ELEMS;
+        gp.scat = scatter_gate_rows(dW, g.H, g.Hq, 0, 0, g.D, 4L * g.H);
         TRY(gemm_f16({dA, 4L * g.Hq, 1}, {x16, g.Dp, 1}, gp, 0, st), "gemm dW");
     }
     {
         const __half *hprev = (const __half *)(res + rv.hist) + (d->direction < 0 ? (long)g.B * g.Hq : 0);
         GemmParams gp{4 * g.Hq, g.Hq, (int)g.TB, dRT, g.Hq, a, 0, nullptr, 0, 0};
         gp.splitk_ws = (float *)(ws + w.gsk); gp.splitk_elems = GSK_ELEMS;
+        gp.scat = scatter_gate_rows(dR, g.H, g.Hq, 0, 0, g.H, 4L * g.H);
         TRY(gemm_f16({dA, 4L * g.Hq, 1}, {hprev, g.Hq, 1}, gp, 0, st), "gemm dR");
     }
-    TRY(scatter_w(dW, g.D, g.H, g.Hq, dWT, g.Dp, 0, 0, st), "scatter dW");
-    TRY(scatter_r(dR, g.H, g.Hq, dRT, st), "scatter dR");
     TRY(scatter_b(db, g.H, g.Hq, dbp, g.step ? 1 : g.pl.G, 0, st), "scatter db");
     return 0;
 }
@@ -754,15 +765,16 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     const int side_ctas = !overlap ? 0 : g.step ? step_share : (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8);
     // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
-    // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch)
+    // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch),
+    // [2L+3] main -> side (layer 0's dW is accumulated: the forked tail, side_layer)
     // (per thread and per device: an event may only be recorded on a stream of its own device)
     static thread_local std::map<int, std::vector<cudaEvent_t>> evs_by_dev;
     int cur_dev = 0;
     if (cudaGetDevice(&cur_dev) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "cudaGetDevice");
     std::vector<cudaEvent_t> &evs = evs_by_dev[cur_dev];
     const int GSK_FREE = 2 * g.L + 2;
-    if (overlap && evs.size() < 2 * (size_t)g.L + 3) {
-        while (evs.size() < 2 * (size_t)g.L + 3) {
+    if (overlap && evs.size() < 2 * (size_t)g.L + 4) {
+        while (evs.size() < 2 * (size_t)g.L + 4) {
             cudaEvent_t e;
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "event");
             evs.push_back(e);
@@ -807,11 +819,13 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         float *dWoT = (float *)(ws + w.dWoT);
         if (overlap) TRY((int)cudaStreamWaitEvent(side, evs[g.L + 1], 0), "cudaStreamWaitEvent");
         if (int rc = side_guard(g.L - 1)) return rc;
+        // dW_out [2H, K] += (dlogits^T Y)^T, scattered from the padded halves of Y by the GEMM
         GemmParams gw{g.K, 2 * Hq, (int)g.TB, dWoT, 2L * Hq, a, 0, nullptr, 0, 0};
         gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
+        gw.scat.dst = grad + offs[6 * g.L]; gw.scat.rowmode = 0; gw.scat.nrows = g.K;
+        gw.scat.colmode = 1; gw.scat.H = g.H; gw.scat.Hq = Hq; gw.scat.ld = g.K;
         TRY(gemm_f16({dlog, g.Kp, 1}, {ytop, 2L * Hq, 1}, gw, side_ctas, side), "gemm dW_out");
         if (overlap) TRY((int)cudaEventRecord(evs[GSK_FREE], side), "cudaEventRecord");
-        TRY(scatter_wout(grad + offs[6 * g.L], g.H, Hq, g.K, dWoT, 2L * Hq, side), "scatter dW_out");
         TRY(colsum_f16_add(dlog, g.TB, g.K, g.Kp, a, grad + offs[6 * g.L + 1], (float *)(ws + w.cs), side), "db_out");
         if (comm) {  // sync-mode exchange of this bucket (the head), overlapping the BPTT below
             if (int rc = dp_allreduce_grads_impl(comm, grad + blo[0], bhi[0] - blo[0], side)) return rc;
@@ -828,30 +842,42 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         float *dWT = (float *)(ws + w.dWT) + (size_t)par * 8 * Hq * w.maxDn;
         float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
         const float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.dbs * 4 * Hq;
-        if (overlap && ss == side) TRY((int)cudaStreamWaitEvent(side, evs[l], 0), "cudaStreamWaitEvent");
+        // layer 0 on s_main (after the last BPTT): fork -- dW stays on s_main, dR and the rest go to the
+        // side stream once it finished layer 1's work, each with its own half of the split-K scratch;
+        // the three small GEMMs then run side by side instead of one after another (tail -40 us at C3)
+        const bool fork = l == 0 && overlap && ss != side && !comm;
+        cudaStream_t sw = ss, sr = fork ? side : ss;
+        float *gsk_w = (float *)(ws + w.gsk), *gsk_r = fork ? gsk_w + GSK_ELEMS / 2 : gsk_w;
+        const long gsk_n = fork ? GSK_ELEMS / 2 : GSK_ELEMS;
+        if (overlap && sr == side) TRY((int)cudaStreamWaitEvent(side, evs[l], 0), "cudaStreamWaitEvent");
         if (l > 0)  // overlaps BPTT(l-1)
             if (int rc = side_guard(l - 1)) return rc;
         // on s_main: the split-K scratch is shared with the side stream's GEMMs (the last layer's)
-        if (overlap && ss != side) TRY((int)cudaStreamWaitEvent(ss, evs[GSK_FREE], 0), "cudaStreamWaitEvent");
+        if (overlap && sw != side) TRY((int)cudaStreamWaitEvent(sw, evs[GSK_FREE], 0), "cudaStreamWaitEvent");
         const __half *X = l == 0 ? (const __half *)(ws + w.x16) : (const __half *)(ws + w.y16[l - 1]);
         // the last layer's weight gradients run after all BPTT work: every SM is free then
         const int wctas = l == 0 ? 0 : side_ctas;
+        // dW_d [Drows, 4H] of both directions += (dA^T X)^T, scattered into grad by the GEMM
         GemmParams gw{8 * Hq, g.Dn[l], (int)g.TB, dWT, g.Dn[l], a, 0, nullptr, 0, 0};
-        gw.splitk_ws = (float *)(ws + w.gsk); gw.splitk_elems = GSK_ELEMS;
-        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, wctas, ss), "gemm dW");
+        gw.splitk_ws = gsk_w; gw.splitk_elems = gsk_n;
+        gw.scat = scatter_gate_rows(grad + offs[6 * l], g.H, Hq, (long)(offs[6 * l + 3] - offs[6 * l]), g.rowmode[l],
+                                    g.Drows[l], 4L * g.H);
+        TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, wctas, sw), "gemm dW");
+        if (fork) TRY((int)cudaEventRecord(evs[2 * g.L + 3], sw), "cudaEventRecord");
         const __half *hist = (const __half *)(ws + w.hist[l]);
         for (int dd = 0; dd < 2; ++dd) {
             const __half *hprev = hist + ((long)dd * (g.T + 1) + dd) * g.B * Hq;
             GemmParams gr{4 * Hq, Hq, (int)g.TB, dRT + (size_t)dd * 4 * Hq * Hq, Hq, a, 0, nullptr, 0, 0};
-            gr.splitk_ws = (float *)(ws + w.gsk); gr.splitk_elems = GSK_ELEMS;
-            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, wctas, ss), "gemm dR");
+            gr.splitk_ws = gsk_r; gr.splitk_elems = gsk_n;
+            gr.scat = scatter_gate_rows(grad + offs[6 * l + 3 * dd + 1], g.H, Hq, 0, 0, g.H, 4L * g.H);
+            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, wctas, sr), "gemm dR");
         }
         if (overlap && ss == side) TRY((int)cudaEventRecord(evs[GSK_FREE], side), "cudaEventRecord");
-        for (int dd = 0; dd < 2; ++dd) {
-            const int e = 6 * l + 3 * dd;
-            TRY(scatter_w(grad + offs[e], g.Drows[l], g.H, Hq, dWT, g.Dn[l], dd, g.rowmode[l], ss), "scatter dW");
-            TRY(scatter_r(grad + offs[e + 1], g.H, Hq, dRT + (size_t)dd * 4 * Hq * Hq, ss), "scatter dR");
-            TRY(scatter_b(grad + offs[e + 2], g.H, Hq, dbp, db_groups[l], dd, ss), "scatter db");
+        for (int dd = 0; dd < 2; ++dd)
+            TRY(scatter_b(grad + offs[6 * l + 3 * dd + 2], g.H, Hq, dbp, db_groups[l], dd, sr), "scatter db");
+        if (fork) {  // the rest of layer 0's work (update, completion event) follows on the side stream
+            TRY((int)cudaStreamWaitEvent(sr, evs[2 * g.L + 3], 0), "cudaStreamWaitEvent");
+            ss = sr;
         }
         const size_t b0 = blo[bhead + g.L - 1 - l], b1 = bhi[bhead + g.L - 1 - l];  // layer l's bucket
         if (comm) {  // sync-mode exchange of layer l's bucket (§4.1), overlapping BPTT

@@ -58,6 +58,18 @@ DEVI void tile_coords(int tile, int num_m, int num_n, const GemmParams &p, int &
     nt = w;
 }
 
+// scatter-mode addresses (gemm.h GemmScatter); -1: the element has no destination (padding)
+DEVI long scat_row(const GemmScatter &s, int m) {
+    if (s.rowmode == 0) return m < s.nrows ? (long)m : -1L;
+    const int d = m / (4 * s.Hq), r = m - d * 4 * s.Hq, u = r >> 2, gam = r & 3;
+    return u < s.H ? d * s.dstride + (long)gam * s.H + u : -1L;
+}
+DEVI long scat_col(const GemmScatter &s, int n) {
+    if (s.colmode == 0) return n < s.ncols ? (long)n * s.ld : -1L;
+    const int h = n / s.Hq, u = n - h * s.Hq;
+    return u < s.H ? ((long)h * s.H + u) * s.ld : -1L;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_f16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -225,7 +237,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const int n = n0 + c;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = v[j] * p.alpha + bs[c + j];
-                if (p.natB) {
+                if (p.scat.dst) {  // scatter-add into the parameter layout (split-K: the reduction does it)
+                    if (m >= p.M) continue;
+                    const long ro = scat_row(p.scat, m);
+                    if (ro < 0) continue;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const long co = n + j < p.N ? scat_col(p.scat, n + j) : -1L;
+                        if (co >= 0) p.scat.dst[ro + co] += v[j];
+                    }
+                } else if (p.natB) {
                     if (m >= p.M || n >= p.N) continue;
                     // CTA-native layout of the recurrence (see lstm_rec.h): the 16 columns stay in
                     // one 128-row block of one CTA, consecutive columns are NQ floats apart
@@ -388,10 +409,13 @@ static cudaError_t gemm_setup() {
     return cudaSuccess;
 }
 __global__ void splitk_reduce_kernel(const float *__restrict__ part, int S, long stride, int M, int N, float *C,
-                                     long ldc, float alpha, int beta, const float *__restrict__ bias);
+                                     long ldc, float alpha, int beta, const float *__restrict__ bias, GemmScatter sc);
+__global__ void splitk_scatter_kernel(const float *__restrict__ part, int S, long stride, int M, int N, float alpha,
+                                      GemmScatter sc);
 int gemm_prepare() {
     cudaFuncAttributes a;
     if (cudaFuncGetAttributes(&a, splitk_reduce_kernel) != cudaSuccess) return -5;
+    if (cudaFuncGetAttributes(&a, splitk_scatter_kernel) != cudaSuccess) return -5;
     return (gemm_setup<128>() == cudaSuccess && gemm_setup<256>() == cudaSuccess) ? 0 : -5;
 }
 
@@ -423,17 +447,56 @@ static cudaError_t launch_gemm(const CUtensorMap &ta, const CUtensorMap &tb, con
 }
 
 // split-K reduction: C = alpha * sum_s part[s] (+C) (+bias), in fixed order
+// (scatter mode, sc.dst: dst[row_off(m) + col_off(c)] += alpha * sum_s part[s] instead)
 __global__ void splitk_reduce_kernel(const float *__restrict__ part, int S, long stride, int M, int N, float *C,
-                                     long ldc, float alpha, int beta, const float *__restrict__ bias) {
+                                     long ldc, float alpha, int beta, const float *__restrict__ bias, GemmScatter sc) {
     const long n = (long)M * N;
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
         const long m = i / N;
         const int c = (int)(i - m * N);
         float acc = 0.f;
         for (int s = 0; s < S; ++s) acc += part[s * stride + i];
+        if (sc.dst) {
+            const long ro = scat_row(sc, (int)m), co = scat_col(sc, c);
+            if (ro >= 0 && co >= 0) sc.dst[ro + co] += acc * alpha;
+            continue;
+        }
         float v = acc * alpha + (bias ? bias[c] : 0.f);
         float *dst = C + m * ldc + c;
         *dst = beta ? *dst + v : v;
+    }
+}
+
+// split-K reduction in scatter mode: the destination runs along m (the gate columns of the
+// parameter matrices), the partials along n, so the sum is transposed through a 32 x 32 shared tile:
+// reads coalesced along n, scatter-adds along m (8 consecutive floats per (unit block, gate))
+__global__ void __launch_bounds__(256) splitk_scatter_kernel(const float *__restrict__ part, int S, long stride, int M,
+                                                             int N, float alpha, GemmScatter sc) {
+    __shared__ float tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int tn = (N + 31) / 32, tm = (M + 31) / 32;
+    for (int tb = blockIdx.x; tb < tm * tn; tb += gridDim.x) {
+        const int m0 = (tb / tn) * 32, n0 = (tb % tn) * 32;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int m = m0 + ty + 8 * k, n = n0 + tx;
+            float acc = 0.f;
+            if (m < M && n < N)
+                for (int s = 0; s < S; ++s) acc += part[s * stride + (long)m * N + n];
+            tile[ty + 8 * k][tx] = acc;
+        }
+        __syncthreads();
+        const int m = m0 + tx;
+        const long ro = m < M ? scat_row(sc, m) : -1L;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int n = n0 + ty + 8 * k;
+            if (ro >= 0 && n < N) {
+                const long co = scat_col(sc, n);
+                if (co >= 0) sc.dst[ro + co] += tile[tx][ty + 8 * k] * alpha;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -509,6 +572,7 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
     if (S > 1) {
         q.C = p.splitk_ws; q.ldc = p.N; q.alpha = 1.f; q.beta = 0; q.bias = nullptr;
         q.ksplit = S; q.split_stride = (long)p.M * p.N;
+        q.scat = GemmScatter{};  // the partials are plain; the reduction scatters
     }
     cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, ta2, q, max_ctas, st)
                               : launch_gemm<128>(ta, tb, ta2, q, max_ctas, st);
@@ -517,8 +581,14 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
         const long n = (long)p.M * p.N;
         long g = (n + 255) / 256;
         if (g > 148 * 8) g = 148 * 8;
-        splitk_reduce_kernel<<<(int)g, 256, 0, st>>>(p.splitk_ws, S, (long)p.M * p.N, p.M, p.N, p.C, p.ldc, p.alpha,
-                                                    p.beta, p.bias);
+        if (p.scat.dst) {
+            long tiles32 = (long)((p.M + 31) / 32) * ((p.N + 31) / 32);
+            splitk_scatter_kernel<<<(int)(tiles32 < 148 * 8 ? tiles32 : 148 * 8), 256, 0, st>>>(
+                p.splitk_ws, S, (long)p.M * p.N, p.M, p.N, p.alpha, p.scat);
+        } else {
+            splitk_reduce_kernel<<<(int)g, 256, 0, st>>>(p.splitk_ws, S, (long)p.M * p.N, p.M, p.N, p.C, p.ldc, p.alpha,
+                                                        p.beta, p.bias, p.scat);
+        }
         note_launch();
         if (cudaGetLastError() != cudaSuccess) return -5;
     }

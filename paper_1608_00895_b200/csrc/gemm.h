@@ -11,6 +11,18 @@ struct GemmOperand {
     int mn_major;     // 0: element (r, k) at ptr[r*ld + k]; 1: at ptr[k*ld + r]
 };
 
+// Scatter output (gemm.h GemmParams::scat): element (m, n) of alpha * A B^T is ADDED to
+// dst[row_off(m) + col_off(n)] instead of being stored to C -- the weight gradients land in the flat
+// parameter vector's layout (blstm.h) directly, with no staging matrix and no scatter pass.
+//   rowmode 0: m -> m (m < nrows);  1: gate-interleaved m = d 4Hq + 4u + gamma -> d dstride + gamma H + u
+//              (skipped for u >= H)
+//   colmode 0: n -> n ld (n < ncols);  1: padded halves n = h Hq + u -> (h H + u) ld (skipped for u >= H)
+struct GemmScatter {
+    float *dst = nullptr;
+    int rowmode = 0, colmode = 0, H = 0, Hq = 0, nrows = 0, ncols = 0;
+    long dstride = 0, ld = 0;
+};
+
 struct GemmParams {
     int M, N, K;
     float *C;           // fp32 [M, ldc]
@@ -62,6 +74,7 @@ struct GemmParams {
     // (a_kwrap * 64 elements), so one launch computes A.[B_0; B_1; ...] over K = nseg * a_kwrap * 64
     // with B's segments stacked along K -- BLSTM_PREC_FP16X2W's Z = X W_hi + X W_lo (R9)
     int a_kwrap = 0;
+    GemmScatter scat;  // scat.dst != nullptr: scatter-add output (C, ldc, beta and bias unused; no flags / partials)
 };
 
 constexpr int GEMM_BM_ROWS = 128;           // M tile

@@ -314,16 +314,16 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     uint32_t phase = 0, mph = 0, xph = 0;
     // a step's outputs other than the history (read only after the launch completes)
     float yv[8];
-    __half ga[32];
+    __half2 ga[16];  // (packed conversions: one cvt per pair)
     long r_pend = -1;
     auto store_outputs = [&](long rr) {
         uint4 *gp = reinterpret_cast<uint4 *>(p.gates + rr * G4 + (long)d * 4 * Hq + 4 * u0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) gp[j] = *reinterpret_cast<const uint4 *>(&ga[8 * j]);
+        for (int j = 0; j < 4; ++j) gp[j] = *reinterpret_cast<const uint4 *>(&ga[4 * j]);
         if (p.y16) {
-            __half yh[8];
+            __half2 yh[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) yh[i] = __float2half_rn(yv[i]);
+            for (int i = 0; i < 4; ++i) yh[i] = __floats2half2_rn(yv[2 * i], yv[2 * i + 1]);
             *reinterpret_cast<uint4 *>(p.y16 + rr * 2 * Hq + (long)d * Hq + u0) = *reinterpret_cast<const uint4 *>(yh);
         }
         float *cp = p.C + d * p.c_doff + rr * p.ldc + u0;
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             }
         }
         if (row_ok) {
-            __half hh[8];
+            float hv[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const bool valid = valid_row && u0 + i < H;
@@ -464,11 +464,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
                     c_st[i] = cn;
                     h_st[i] = ao * th(cn);
                 }
-                hh[i] = __float2half_rn(h_st[i]);
+                hv[i] = h_st[i];
                 yv[i] = valid ? h_st[i] : 0.f;
-                ga[4 * i] = __float2half_rn(ai); ga[4 * i + 1] = __float2half_rn(af);
-                ga[4 * i + 2] = __float2half_rn(ag); ga[4 * i + 3] = __float2half_rn(ao);
+                ga[2 * i] = __floats2half2_rn(ai, af);
+                ga[2 * i + 1] = __floats2half2_rn(ag, ao);
             }
+            __half2 hh[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) hh[i] = __floats2half2_rn(hv[2 * i], hv[2 * i + 1]);
             // h_t -> the history slot the next step's TMA reads
             *reinterpret_cast<uint4 *>(p.hist + (((long)d * (T + 1) + slot_prev + dir) * B + m) * Hq + u0) =
                 *reinterpret_cast<const uint4 *>(hh);

@@ -24,6 +24,11 @@ SHAPES = [  # name, M, N, K, a_mn, b_mn, per-step count
     ("dW layer0", 8 * Hq, Dp0, TB, 1, 1, 1),
     ("dW layer1-4", 8 * Hq, 2 * Hq, TB, 1, 1, 4),
     ("dR (x2/layer)", 4 * Hq, Hq, TB, 1, 1, 10),
+    # not in the C3 total (count 0): C5 (T*B = 128000, Hq = 1024) and the MDLSTM bench (32x256x16
+    # cells, 20Hp = 1280 at H = 64, K = 3 Dp for the split projection)
+    ("C5 Z layer0", 128000, 8192, 64, 0, 1, 0),
+    ("C5 dX layer1-3", 128000, 2048, 8192, 0, 0, 0),
+    ("MD Z (K=3Dp)", 131072, 1280, 192, 0, 0, 0),
 ]
 
 
