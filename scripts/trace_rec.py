@@ -53,8 +53,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
     ap.add_argument("--mhz", type=float, default=1965.0)
+    ap.add_argument("--B", type=int, default=None, help="batch override (e.g. C3 at B=40: N=16 per cluster)")
     args = ap.parse_args()
-    cfg, params, batch = synth.make_workload(synth.CONFIGS[args.config])
+    cfg, params, batch = synth.make_workload(synth.CONFIGS[args.config], B=args.B)
     dev = torch.device("cuda:0")
     tr = StackTrainer(cfg, params, batch, dev)
     tr.step()
