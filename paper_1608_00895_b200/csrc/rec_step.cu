@@ -225,7 +225,13 @@ int grid_of(long n) {
 //   5. arrive on the direction's counter, then store C, y, y16 and the gates (off the critical path:
 //      the counter's release covers only the history stores).
 // ---------------------------------------------------------------------------------------------
-constexpr int PF_THREADS = 256;
+#ifndef BLSTM_PF_THREADS
+#define BLSTM_PF_THREADS 256  // 512 (4 units per thread) measured slower: C5 forward 33.4 vs 31.3 ms
+#endif
+constexpr int PF_THREADS = BLSTM_PF_THREADS;  // 256 or 512
+constexpr int PF_CH = PF_THREADS / 128;       // column chunks per TMEM lane quarter
+constexpr int PF_CW = 64 / PF_CH;             // tile columns a thread finalizes (32 or 16)
+constexpr int PF_UPT = PF_CW / 4;             // units a thread finalizes (8 or 4)
 constexpr int PF_S = 4;                  // h ring stages (16 KB each: 128 rows x 64 K)
 constexpr uint32_t PF_CHUNK = 16384;
 constexpr uint32_t PF_RECV = 64 * 128 * 4;  // the partner's partial sums of this CTA's 64 columns
@@ -262,9 +268,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const int dir = d == 0 ? p.dir0 : -1;
     const int w = warp_uniform(warp_id()), l = lane_id(), q = w & 3, ch = w >> 2;
     const int m = 32 * q + l;                     // batch row (TMEM lane) this thread reads
-    // this thread finalizes row m, tile columns [64 kh + 32 ch, +32) = 8 units from u0, and sends
-    // the partner its partial sums of columns [64 (1 - kh) + 32 ch, +32)
-    const int u0 = nt * 32 + 16 * kh + 8 * ch;
+    // this thread finalizes row m, tile columns [64 kh + CW ch, +CW) = UPT units from u0, and sends
+    // the partner its partial sums of columns [64 (1 - kh) + CW ch, +CW)
+    constexpr int CW = PF_CW, UPT = PF_UPT;
+    const int u0 = nt * 32 + 16 * kh + UPT * ch;
     uint32_t *cnt_d = cnt + 32 * d;
     const uint32_t cpd = 2 * NT;                  // CTAs per direction
 
@@ -296,53 +303,57 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     mbar_wait(rbar, 0);
     cluster_sync();  // the partner's barriers are initialised before any remote store
 
-    // state of the 8 cells this thread finalizes (row m, units u0..u0+7)
-    float c_st[8], h_st[8];
+    // state of the UPT cells this thread finalizes (row m, units u0..u0+UPT-1)
+    float c_st[UPT], h_st[UPT];
     const bool row_ok = m < B;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < UPT; ++i) {
         const int u = u0 + i;
         c_st[i] = (row_ok && p.c0 && u < H) ? p.c0[((long)d * B + m) * H + u] : 0.f;
         h_st[i] = (row_ok && p.h0 && u < H) ? p.h0[((long)d * B + m) * H + u] : 0.f;
     }
-    const bool cvec = (p.ldc & 3) == 0 && (p.c_doff & 3) == 0 && ((uintptr_t)p.C & 15) == 0 && u0 + 8 <= H;
-    const bool yvec = p.y && (p.ldy & 3) == 0 && (p.y_doff & 3) == 0 && ((uintptr_t)p.y & 15) == 0 && u0 + 8 <= H;
+    const bool cvec = (p.ldc & 3) == 0 && (p.c_doff & 3) == 0 && ((uintptr_t)p.C & 15) == 0 && u0 + UPT <= H;
+    const bool yvec = p.y && (p.ldy & 3) == 0 && (p.y_doff & 3) == 0 && ((uintptr_t)p.y & 15) == 0 && u0 + UPT <= H;
     const uint32_t idesc = idesc_f16(128, 128, 0, 0);
     const uint32_t partner_recv = mapa_shared(smem_u32(recv), (uint32_t)(kh ^ 1));
     const uint32_t partner_xbar = mapa_shared(smem_u32(xbar), (uint32_t)(kh ^ 1));
     int stage = 0;
     uint32_t phase = 0, mph = 0, xph = 0;
     // a step's outputs other than the history (read only after the launch completes)
-    float yv[8];
-    __half2 ga[16];  // (packed conversions: one cvt per pair)
+    float yv[UPT];
+    __half2 ga[2 * UPT];  // (packed conversions: one cvt per pair)
     long r_pend = -1;
     auto store_outputs = [&](long rr) {
         uint4 *gp = reinterpret_cast<uint4 *>(p.gates + rr * G4 + (long)d * 4 * Hq + 4 * u0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) gp[j] = *reinterpret_cast<const uint4 *>(&ga[4 * j]);
+        for (int j = 0; j < UPT / 2; ++j) gp[j] = *reinterpret_cast<const uint4 *>(&ga[4 * j]);
         if (p.y16) {
-            __half2 yh[4];
+            __half2 yh[UPT / 2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) yh[i] = __floats2half2_rn(yv[2 * i], yv[2 * i + 1]);
-            *reinterpret_cast<uint4 *>(p.y16 + rr * 2 * Hq + (long)d * Hq + u0) = *reinterpret_cast<const uint4 *>(yh);
+            for (int i = 0; i < UPT / 2; ++i) yh[i] = __floats2half2_rn(yv[2 * i], yv[2 * i + 1]);
+            __half *yd = p.y16 + rr * 2 * Hq + (long)d * Hq + u0;
+            if constexpr (UPT == 8) *reinterpret_cast<uint4 *>(yd) = *reinterpret_cast<const uint4 *>(yh);
+            else *reinterpret_cast<uint2 *>(yd) = *reinterpret_cast<const uint2 *>(yh);
         }
         float *cp = p.C + d * p.c_doff + rr * p.ldc + u0;
         if (cvec) {
-            reinterpret_cast<float4 *>(cp)[0] = make_float4(c_st[0], c_st[1], c_st[2], c_st[3]);
-            reinterpret_cast<float4 *>(cp)[1] = make_float4(c_st[4], c_st[5], c_st[6], c_st[7]);
+#pragma unroll
+            for (int v = 0; v < UPT / 4; ++v)
+                reinterpret_cast<float4 *>(cp)[v] = make_float4(c_st[4 * v], c_st[4 * v + 1], c_st[4 * v + 2], c_st[4 * v + 3]);
         } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < UPT; ++i)
                 if (u0 + i < H) cp[i] = c_st[i];
         }
         if (p.y) {
             float *yq = p.y + rr * p.ldy + d * p.y_doff + u0;
             if (yvec) {
-                reinterpret_cast<float4 *>(yq)[0] = make_float4(yv[0], yv[1], yv[2], yv[3]);
-                reinterpret_cast<float4 *>(yq)[1] = make_float4(yv[4], yv[5], yv[6], yv[7]);
+#pragma unroll
+                for (int v = 0; v < UPT / 4; ++v)
+                    reinterpret_cast<float4 *>(yq)[v] = make_float4(yv[4 * v], yv[4 * v + 1], yv[4 * v + 2], yv[4 * v + 3]);
             } else {
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < UPT; ++i)
                     if (u0 + i < H) yq[i] = yv[i];
             }
         }
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         const bool need_mma = s > 0 || p.h0 != nullptr;
         const int slot_prev = t + (dir < 0);
         PTR(0);
-        float acc[32];
+        float acc[CW];
         if (need_mma) {
             if (threadIdx.x == 0) mbar_arrive_expect_tx(xbar, PF_RECV);  // this step's partial sums
             if (w == 0) {
@@ -402,15 +413,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         // step's loads, overlapping the MMAs
         if (r_pend >= 0) store_outputs(r_pend);
         // Z and the mask of this step (produced before the launch): in flight during the MMA
-        float z[32];
+        float z[CW];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) z[i] = 0.f;
+        for (int i = 0; i < CW; ++i) z[i] = 0.f;
         bool valid_row = false;
         if (row_ok) {
             valid_row = p.mask[r] != 0;
             const float4 *zp = reinterpret_cast<const float4 *>(p.Z + r * G4 + (long)d * 4 * Hq + 4 * u0);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < CW / 4; ++j) {
                 const float4 v = zp[j];
                 z[4 * j] = v.x; z[4 * j + 1] = v.y; z[4 * j + 2] = v.z; z[4 * j + 3] = v.w;
             }
@@ -422,15 +433,16 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             tc_fence_after();
             const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16);
             {  // the partner's columns of row m: partial sums -> its receive buffer
-                float v[32];
-                tmem_ld16(ta + 64 * (kh ^ 1) + 32 * ch, *reinterpret_cast<float(*)[16]>(&v[0]));
-                tmem_ld16(ta + 64 * (kh ^ 1) + 32 * ch + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
-                tmem_ld16(ta + 64 * kh + 32 * ch, *reinterpret_cast<float(*)[16]>(&acc[0]));
-                tmem_ld16(ta + 64 * kh + 32 * ch + 16, *reinterpret_cast<float(*)[16]>(&acc[16]));
+                float v[CW];
+#pragma unroll
+                for (int k16 = 0; k16 < CW / 16; ++k16) {
+                    tmem_ld16(ta + 64 * (kh ^ 1) + CW * ch + 16 * k16, *reinterpret_cast<float(*)[16]>(&v[16 * k16]));
+                    tmem_ld16(ta + 64 * kh + CW * ch + 16 * k16, *reinterpret_cast<float(*)[16]>(&acc[16 * k16]));
+                }
                 tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    st_async_v4(partner_recv + (uint32_t)(((ch * 8 + j) * 128 + m) * 16), v[4 * j], v[4 * j + 1],
+                for (int j = 0; j < CW / 4; ++j)
+                    st_async_v4(partner_recv + (uint32_t)(((ch * (CW / 4) + j) * 128 + m) * 16), v[4 * j], v[4 * j + 1],
                                 v[4 * j + 2], v[4 * j + 3], partner_xbar);
             }
             PTR(5);
@@ -439,12 +451,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             PTR(6);
         } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+            for (int i = 0; i < CW; ++i) acc[i] = 0.f;
         }
         // a = (Z + P_0) + P_1: the step chain's summation order (P_k = K half k)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float4 o = need_mma ? recv[(ch * 8 + j) * 128 + m] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < CW / 4; ++j) {
+            const float4 o = need_mma ? recv[(ch * (CW / 4) + j) * 128 + m] : make_float4(0.f, 0.f, 0.f, 0.f);
             const float ov[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -453,9 +465,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             }
         }
         if (row_ok) {
-            float hv[8];
+            float hv[UPT];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < UPT; ++i) {
                 const bool valid = valid_row && u0 + i < H;
                 float ai = 0.f, af = 0.f, ag = 0.f, ao = 0.f;
                 if (valid) {
@@ -469,12 +481,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
                 ga[2 * i] = __floats2half2_rn(ai, af);
                 ga[2 * i + 1] = __floats2half2_rn(ag, ao);
             }
-            __half2 hh[4];
+            __half2 hh[UPT / 2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) hh[i] = __floats2half2_rn(hv[2 * i], hv[2 * i + 1]);
+            for (int i = 0; i < UPT / 2; ++i) hh[i] = __floats2half2_rn(hv[2 * i], hv[2 * i + 1]);
             // h_t -> the history slot the next step's TMA reads
-            *reinterpret_cast<uint4 *>(p.hist + (((long)d * (T + 1) + slot_prev + dir) * B + m) * Hq + u0) =
-                *reinterpret_cast<const uint4 *>(hh);
+            __half *hd = p.hist + (((long)d * (T + 1) + slot_prev + dir) * B + m) * Hq + u0;
+            if constexpr (UPT == 8) *reinterpret_cast<uint4 *>(hd) = *reinterpret_cast<const uint4 *>(hh);
+            else *reinterpret_cast<uint2 *>(hd) = *reinterpret_cast<const uint2 *>(hh);
         }
         // publish h_t of this CTA's columns to the direction: the CTA barrier orders every thread's
         // history store before thread 0's release (cumulative), which the next step's acquire pairs with
@@ -489,7 +502,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     if (r_pend >= 0) store_outputs(r_pend);
     if (row_ok) {  // state after the whole scan
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < UPT; ++i) {
             const int u = u0 + i;
             if (u < H) {
                 if (p.hT) p.hT[((long)d * B + m) * H + u] = h_st[i];
