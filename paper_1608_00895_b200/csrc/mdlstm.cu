@@ -976,6 +976,518 @@ size_t wv_bwd_smem(int Hp) {
     return 1024 + (size_t)(WV_N * 2 * Hp + 2 * WV_N * 5 * Hp + 3 * WV_N * Hp + 6 * WV_N * Hp) * 4 +
            (size_t)2 * wv_bsize(5 * Hp) * 2 + 2 * WV_N * sizeof(WvCell) + 64;
 }
+// ---------------------------------------------------------------------------------------------
+// CTA-pair wavefront (round 2): a cluster of 2 CTAs per (direction k, image b); rank r owns the
+// units [r Hh, (r+1) Hh), Hh = Hp / 2, so each SM does half of a diagonal's gate math (the single-
+// CTA kernels above are bound by that epilogue) and 128 instead of 64 SMs work.
+//   Forward: rank r's A operand holds the gate rows of its own units (M = 10 Hh, <= 3 tiles), K = all
+//   Hp units of h_{d-1}; after its epilogue each rank writes h_d of its units (hi / lo) into its own
+//   B operand and, by st.async with complete_tx, into the partner's (double-buffered by diagonal
+//   parity: the partner may finish diagonal d+1 while this rank's MMA still reads diagonal d-1).
+//   Backward: K split -- rank r's A operand is [Ru; Rv] (all 2 Hp rows) restricted to the gate columns
+//   of its own units, its B operand its own dA_{d+1}; the partial P rows of the partner's units go
+//   to the partner by st.async (8 KB at Hp = 64), and each rank sums the two partials of its own rows
+//   in fixed order (rank 0's + rank 1's: deterministic).
+// Applies for Hp in {32, 64} (md_wave_pair).
+// ---------------------------------------------------------------------------------------------
+DEVI void st_async_b32(uint32_t dst_cluster, uint32_t v, uint32_t mbar_cluster) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst_cluster), "r"(v),
+                 "r"(mbar_cluster)
+                 : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wave2_fwd_kernel(MdK a) {
+    extern __shared__ uint8_t wv_smem[];
+    uint8_t *sm = (uint8_t *)(((uintptr_t)wv_smem + 1023) & ~(uintptr_t)1023);
+    const int Hp = a.Hp, Hh = Hp / 2, H = a.H, G5 = 5 * Hp, R10 = 10 * Hh, U = a.U, V = a.V, B = a.B;
+    const int r = (int)cluster_ctarank();
+    const int kbi = blockIdx.x >> 1, k = kbi / B, b = kbi - k * B;
+    const int Mt = (R10 + 127) / 128;
+    const int BS = wv_bsize(Hp);
+    float *Zs = (float *)sm;                        // [2][WV_N][5Hp]
+    float *stg = Zs + 2 * WV_N * G5;                // [WV_N][10Hh]   Q^T rows of the own units
+    __half *Bb = (__half *)(stg + WV_N * R10);      // [2 parity][2 part][BS]  h of a diagonal (all units)
+    float *cst = (float *)(Bb + 4 * BS);            // [2][WV_N][Hh]  c of the own units
+    WvCell *tab = (WvCell *)(cst + 2 * WV_N * Hh);  // [2][WV_N]
+    uint64_t *bars = (uint64_t *)(tab + 2 * WV_N);  // [0] mma, [1..2] Z landed, [3..4] partner's h half landed
+    uint32_t *tslot = (uint32_t *)(bars + 5);
+    const int w = warp_id(), l = lane_id(), tid = threadIdx.x;
+    const int prow = (U + 1) * (V + 1) * B;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], Mt);
+        for (int i = 1; i < 5; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    if (w == 0) {
+        tmem_alloc(tslot, 512);
+        tmem_relinquish();
+    }
+    for (int e = tid; e < 2 * BS; e += WV_THREADS) reinterpret_cast<uint32_t *>(Bb)[e] = 0u;  // 4 B halves
+    if (tid < WV_N && tid <= wv_u1(0, U) - wv_u0(0, V)) tab[tid] = wv_cell(a, k, b, 0, tid);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t colAl = Mt * Hp / 2, colD = Mt * Hp;
+    const float *Ru = a.theta + k * a.P1 + (long)a.D * 5 * H, *Rv = Ru + (long)H * 5 * H;
+    for (int mt = 0; mt < Mt; ++mt)  // row = wv 5Hh + q Hh + jj': gate column q H + (r Hh + jj') of R_wv
+        wv_load_a(tmem, mt, mt * Hp / 2, colAl + mt * Hp / 2, Hp / 2, [&](int row, int kk) -> float {
+            const int wv = row / (5 * Hh), n = row - wv * 5 * Hh, q = n / Hh, jj = r * Hh + (n - q * Hh);
+            return (row < R10 && jj < H && kk < H) ? (wv ? Rv : Ru)[(long)kk * 5 * H + q * H + jj] : 0.f;
+        });
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    cluster_sync();  // the partner's barriers are initialised before any remote store
+
+    const int ND = U + V - 1;
+    auto issue_z = [&](int d, int sl) {  // warp 15: lane i copies cell i's Z row (5Hp fp32)
+        const int u0 = wv_u0(d, V), n = wv_u1(d, U) - u0 + 1;
+        if (l == 0) mbar_arrive_expect_tx(&bars[1 + sl], (uint32_t)(n * G5 * 4));
+        __syncwarp();
+        if (l < n) {
+            const int up = u0 + l, vp = d - up;
+            const int u = (k & 1) ? U - 1 - up : up, v = (k & 2) ? V - 1 - vp : vp;
+            const long cp = ((long)u * V + v) * B + b;
+            bulk_g2s(smem_u32(Zs + (sl * WV_N + l) * G5), a.z + cp * 20 * Hp + (long)k * G5, (uint32_t)(G5 * 4),
+                     &bars[1 + sl]);
+        }
+    };
+    if (w == 15) issue_z(0, 0);
+    // epilogue: unit pair pi (own units jl = 2 pi, 2 pi + 1; global j = r Hh + jl), cell ic
+    const int pi = tid & 15, ic = tid >> 4, jl = 2 * pi, j = r * Hh + jl;
+    const bool act_t = jl < Hh, j0 = j < H, j1 = j + 1 < H, hodd = H & 1;
+    const uint32_t idesc = idesc_f16(128, WV_N, 0, 0);
+    const uint32_t bb_addr = smem_u32(Bb), peer_bb = mapa_shared(bb_addr, (uint32_t)(r ^ 1));
+    const uint32_t peer_x = mapa_shared(smem_u32(&bars[3]), (uint32_t)(r ^ 1));
+    uint32_t mph = 0;
+#ifdef BLSTM_TRACE
+    unsigned long long *trace = (blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
+#endif
+    for (int d = 0; d < ND; ++d) {
+        const int sl = d & 1;
+        WTRACE(d, 0);
+        const int u0 = wv_u0(d, V), n = wv_u1(d, U) - u0 + 1;
+        const int pu0 = d > 0 ? wv_u0(d - 1, V) : 0;
+        if (d > 0 && w < Mt) {  // h_{d-1}: the own half (CTA barrier below) and the partner's half landed
+            mbar_wait_cluster(&bars[3 + (sl ^ 1)], ((d - 1) >> 1) & 1);
+            tc_fence_after();
+            const uint32_t bh = bb_addr + (uint32_t)((sl ^ 1) * 2) * BS * 2;
+            wv_mma3(tmem + colD + 32 * w, tmem + w * Hp / 2, tmem + colAl + w * Hp / 2, bh, bh + BS * 2, 0, Hp / 16,
+                    idesc);
+            mma_commit_w(&bars[0]);
+        }
+        WTRACE(d, 1);
+        if (w == 15 && d + 1 < ND) {
+            issue_z(d + 1, sl ^ 1);
+            const int n1 = wv_u1(d + 1, U) - wv_u0(d + 1, V) + 1;
+            if (l < n1) tab[(sl ^ 1) * WV_N + l] = wv_cell(a, k, b, d + 1, l);
+        }
+        // the partner's h_d: n cells x Hh units x (hi, lo) fp16
+        if (w == 14 && l == 0) mbar_arrive_expect_tx(&bars[3 + sl], (uint32_t)(n * Hh * 4));
+        WTRACE(d, 2);
+        if (w == Mt) {
+            mbar_wait(&bars[1 + sl], (d >> 1) & 1);
+            if (d > 0) mbar_wait(&bars[0], mph);
+        }
+        if (d > 0) mph ^= 1;
+        WTRACE(d, 3);
+        __syncthreads();
+        WTRACE(d, 4);
+        if (d > 0) {
+            tc_fence_after();
+            const int q = w & 3, cb = 8 * (w >> 2);
+            float v[3][8];
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt)
+                if (mt < Mt) tmem_ld8f(tmem + ((uint32_t)(32 * q) << 16) + colD + 32 * mt + cb, v[mt]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int mt = 0; mt < 3; ++mt) {
+                const int row = mt * 128 + 32 * q + l;
+                if (mt < Mt && row < R10) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) stg[(cb + c) * R10 + row] = v[mt][c];
+                }
+            }
+        }
+        WTRACE(d, 5);
+        tc_fence_before();
+        __syncthreads();
+        WTRACE(d, 6);
+        const float *cprev = cst + (sl ^ 1) * WV_N * Hh;
+        float *ccur = cst + sl * WV_N * Hh;
+        const float *zs = Zs + sl * WV_N * G5;
+        if (act_t && ic < n) {
+            const int i = ic;
+            const WvCell ce = tab[sl * WV_N + i];
+            const int up = u0 + i;
+            const bool hasu = ce.flags & 2, hasv = ce.flags & 4, on = ce.flags & 1;
+            const int mu = up - 1 - pu0, mv = up - pu0;
+            const float2 cu = hasu ? *reinterpret_cast<const float2 *>(cprev + mu * Hh + jl) : make_float2(0.f, 0.f);
+            const float2 cv = hasv ? *reinterpret_cast<const float2 *>(cprev + mv * Hh + jl) : make_float2(0.f, 0.f);
+            float2 g[5], h = make_float2(0.f, 0.f), cn;
+            if (on) {
+                float2 pre[5];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    float2 s2 = *reinterpret_cast<const float2 *>(zs + i * G5 + q * Hp + j);
+                    if (hasu) {
+                        const float2 t2 = *reinterpret_cast<const float2 *>(stg + mu * R10 + q * Hh + jl);
+                        s2.x += t2.x; s2.y += t2.y;
+                    }
+                    if (hasv) {
+                        const float2 t2 = *reinterpret_cast<const float2 *>(stg + mv * R10 + 5 * Hh + q * Hh + jl);
+                        s2.x += t2.x; s2.y += t2.y;
+                    }
+                    pre[q] = s2;
+                }
+                if (!a.stable) {  // [i, fu, fv, g, o]
+#pragma unroll
+                    for (int q = 0; q < 5; ++q)
+                        g[q] = q == 3 ? make_float2(mth(pre[q].x), mth(pre[q].y)) : make_float2(msg(pre[q].x), msg(pre[q].y));
+                    cn.x = g[1].x * cu.x + g[2].x * cv.x + g[0].x * g[3].x;
+                    cn.y = g[1].y * cu.y + g[2].y * cv.y + g[0].y * g[3].y;
+                    h = make_float2(g[4].x * mth(cn.x), g[4].y * mth(cn.y));
+                } else {          // [i, f, g, o, lambda]
+#pragma unroll
+                    for (int q = 0; q < 5; ++q)
+                        g[q] = q == 2 ? make_float2(mth(pre[q].x), mth(pre[q].y)) : make_float2(msg(pre[q].x), msg(pre[q].y));
+                    cn.x = g[1].x * (g[4].x * cu.x + (1.f - g[4].x) * cv.x) + g[0].x * g[2].x;
+                    cn.y = g[1].y * (g[4].y * cu.y + (1.f - g[4].y) * cv.y) + g[0].y * g[2].y;
+                    h = make_float2(g[3].x * mth(cn.x), g[3].y * mth(cn.y));
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 5; ++q) g[q] = make_float2(0.f, 0.f);
+                cn = hasu ? cu : cv;
+            }
+            if (!j0) { h.x = 0.f; cn.x = 0.f; }
+            if (!j1) { h.y = 0.f; cn.y = 0.f; }
+            *reinterpret_cast<float2 *>(ccur + i * Hh + jl) = cn;
+            uint32_t hh, hl;
+            split_h2(h.x, h.y, hh, hl);
+            const uint32_t off = (uint32_t)((sl * 2) * BS + wv_bidx(i, j)) * 2;  // bytes, part hi
+            *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(Bb) + off) = hh;
+            *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(Bb) + off + BS * 2) = hl;
+            st_async_b32(peer_bb + off, hh, peer_x + 8 * sl);
+            st_async_b32(peer_bb + off + BS * 2, hl, peer_x + 8 * sl);
+            if (j0) {
+                float *ac = a.act + (long)ce.ck * G5 + j;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) *reinterpret_cast<float2 *>(ac + q * Hp) = g[q];
+                *reinterpret_cast<float2 *>(a.c + (long)ce.ck * Hp + j) = cn;
+                *reinterpret_cast<__half2 *>(a.h16 + ((long)k * prow + ce.slot) * Hp + j) = __floats2half2_rn(h.x, h.y);
+                float *yp = a.y + (long)ce.cp * 4 * H + k * H + j;
+                if (!hodd && j1) {
+                    *reinterpret_cast<float2 *>(yp) = h;
+                } else {
+                    yp[0] = h.x;
+                    if (j1) yp[1] = h.y;
+                }
+            }
+        }
+        WTRACE(d, 7);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        WTRACE(d, 8);
+    }
+    // the partner's h of the last diagonal (never read) has landed: no remote store is outstanding
+    if (tid == 0) mbar_wait_cluster(&bars[3 + ((ND - 1) & 1)], ((ND - 1) >> 1) & 1);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (w == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wave2_bwd_kernel(MdK a) {
+    extern __shared__ uint8_t wv_smem[];
+    uint8_t *sm = (uint8_t *)(((uintptr_t)wv_smem + 1023) & ~(uintptr_t)1023);
+    const int Hp = a.Hp, Hh = Hp / 2, H = a.H, G5 = 5 * Hp, K5 = 5 * Hh, R2 = 2 * Hh, U = a.U, V = a.V, B = a.B;
+    const int r = (int)cluster_ctarank();
+    const int kbi = blockIdx.x >> 1, k = kbi / B, b = kbi - k * B;
+    const int BS = wv_bsize(K5);
+    float *stg = (float *)sm;                       // [WV_N][2Hh]  this rank's partial P of its own rows (x 2^DA_SHIFT)
+    float *rcv = stg + WV_N * R2;                   // [2 par][WV_N][2Hh]  the partner's partial of them
+    __half *Bh = (__half *)(rcv + 2 * WV_N * R2);   // [5Hh/8][WV_N][8] (+pad): own dA of diagonal d+1, hi
+    __half *Bl = Bh + BS;                           //                         and lo parts
+    float *acts = (float *)(Bl + BS);               // [2][WV_N][5Hp]
+    float *cr = acts + 2 * WV_N * G5;               // [3][WV_N][Hp]
+    float *dcu = cr + 3 * WV_N * Hp;                // [2][WV_N][Hh]  (own units)
+    float *dcv = dcu + 2 * WV_N * Hh;
+    float *dys = dcv + 2 * WV_N * Hh;               // [2][WV_N][Hp]
+    WvCell *tab = (WvCell *)(dys + 2 * WV_N * Hp);  // [2][WV_N]
+    uint64_t *bars = (uint64_t *)(tab + 2 * WV_N);  // [0] mma, [1..2] inputs landed, [3..4] partner's partial landed
+    uint32_t *tslot = (uint32_t *)(bars + 5);
+    const int w = warp_id(), l = lane_id(), tid = threadIdx.x;
+    const int prow = (U + 1) * (V + 1) * B;
+    const float scale = (float)(1 << DA_SHIFT), unscale = 1.f / scale;
+    const int KS = K5 / 16;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], WV_KW);
+        for (int i = 1; i < 5; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    if (w == 0) {
+        tmem_alloc(tslot, 512);
+        tmem_relinquish();
+    }
+    for (int e = tid; e < BS; e += WV_THREADS) reinterpret_cast<uint32_t *>(Bh)[e] = 0u;  // Bh + Bl
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t colAl = K5 / 2, colD = K5;
+    const float *Ru = a.theta + k * a.P1 + (long)a.D * 5 * H, *Rv = Ru + (long)H * 5 * H;
+    // row = wv Hp + unit; K index q Hh + jj' = gate column q H + (r Hh + jj') of that unit's R_wv row
+    wv_load_a(tmem, 0, 0, colAl, K5 / 2, [&](int row, int kk) -> float {
+        const int wv = row / Hp, rr = row - wv * Hp, q = kk / Hh, jj = r * Hh + (kk - q * Hh);
+        return (row < 2 * Hp && rr < H && jj < H) ? (wv ? Rv : Ru)[(long)rr * 5 * H + q * H + jj] : 0.f;
+    });
+    tmem_st_wait();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    cluster_sync();
+
+    const int ND = U + V - 1;
+    const bool dy_bulk = ((H * 4) & 15) == 0;
+    auto issue_in = [&](int d2, bool with_c) {  // as md_wave_bwd_kernel
+        const int sl = d2 & 1;
+        const int u0 = wv_u0(d2, V), n = wv_u1(d2, U) - u0 + 1;
+        const int np = d2 >= 1 ? wv_u1(d2 - 1, U) - wv_u0(d2 - 1, V) + 1 : 0;
+        WvCell ce{};
+        if (l < n) ce = wv_cell(a, k, b, d2, l);
+        uint32_t bytes = (uint32_t)(n * G5 * 4 + np * Hp * 4 + (with_c ? n * Hp * 4 : 0) + (dy_bulk ? n * H * 4 : 0));
+        if (l == 0) mbar_arrive_expect_tx(&bars[1 + sl], bytes);
+        __syncwarp();
+        if (l < n) {
+            tab[sl * WV_N + l] = ce;
+            bulk_g2s(smem_u32(acts + (sl * WV_N + l) * G5), a.act + (long)ce.ck * G5, (uint32_t)(G5 * 4), &bars[1 + sl]);
+            if (with_c)
+                bulk_g2s(smem_u32(cr + ((d2 % 3) * WV_N + l) * Hp), a.c + (long)ce.ck * Hp, (uint32_t)(Hp * 4), &bars[1 + sl]);
+            const float *dyp = a.dy + (long)ce.cp * 4 * H + k * H;
+            float *dyd = dys + (sl * WV_N + l) * Hp;
+            if (dy_bulk)
+                bulk_g2s(smem_u32(dyd), dyp, (uint32_t)(H * 4), &bars[1 + sl]);
+            else
+                for (int e = 0; e < H; ++e) dyd[e] = dyp[e];
+        }
+        if (l < np) {
+            const int up = wv_u0(d2 - 1, V) + l;
+            const int ckp = ((k * U + up) * V + (d2 - 1 - up)) * B + b;
+            bulk_g2s(smem_u32(cr + (((d2 + 2) % 3) * WV_N + l) * Hp), a.c + (long)ckp * Hp, (uint32_t)(Hp * 4),
+                     &bars[1 + sl]);
+        }
+    };
+    if (w == 15) issue_in(ND - 1, true);
+    const int pi = tid & 15, ic = tid >> 4, jl = 2 * pi, j = r * Hh + jl;
+    const bool act_t = jl < Hh, j0 = j < H, j1 = j + 1 < H;
+    const uint32_t idesc = idesc_f16(128, WV_N, 0, 0);
+    const uint32_t peer_rcv = mapa_shared(smem_u32(rcv), (uint32_t)(r ^ 1));
+    const uint32_t peer_x = mapa_shared(smem_u32(&bars[3]), (uint32_t)(r ^ 1));
+    uint32_t mph = 0, iph = 0;
+    const int ks0 = (w * KS) / WV_KW, ks1 = ((w + 1) * KS) / WV_KW;
+#ifdef BLSTM_TRACE
+    unsigned long long *trace = (blockIdx.x == 0 && tid == 0) ? a.trace : nullptr;
+#endif
+    for (int d = ND - 1; d >= 0; --d) {
+        const int sl = d & 1;
+        WTRACE(ND - 1 - d, 0);
+        const int u0 = wv_u0(d, V), n = wv_u1(d, U) - u0 + 1;
+        const bool has_succ = d + 1 < ND;
+        const int su0 = has_succ ? wv_u0(d + 1, V) : 0, pu0 = d > 0 ? wv_u0(d - 1, V) : 0;
+        if (has_succ && w < WV_KW) {  // partial P_w over this rank's K range part w
+            tc_fence_after();
+            wv_mma3(tmem + colD + 32 * w, tmem, tmem + colAl, smem_u32(Bh), smem_u32(Bl), ks0, ks1, idesc);
+            mma_commit_w(&bars[0]);
+        }
+        WTRACE(ND - 1 - d, 1);
+        if (w == 15 && d >= 1) issue_in(d - 1, false);
+        if (has_succ && w == 14 && l == 0) mbar_arrive_expect_tx(&bars[3 + sl], (uint32_t)(WV_N * R2 * 4));
+        WTRACE(ND - 1 - d, 2);
+        if (w == WV_KW) {
+            mbar_wait(&bars[1 + sl], (iph >> sl) & 1);
+            if (has_succ) mbar_wait(&bars[0], mph);
+        }
+        iph ^= 1u << sl;
+        if (has_succ) mph ^= 1;
+        WTRACE(ND - 1 - d, 3);
+        __syncthreads();
+        WTRACE(ND - 1 - d, 4);
+        if (has_succ) {  // the partial's rows: own units -> stg, the partner's -> its receive buffer
+            tc_fence_after();
+            const int q = w & 3, cb = 8 * (w >> 2);
+            float x[WV_KW][8], v[8];
+#pragma unroll
+            for (int aa = 0; aa < WV_KW; ++aa) tmem_ld8f(tmem + ((uint32_t)(32 * q) << 16) + colD + 32 * aa + cb, x[aa]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = (x[0][c] + x[1][c]) + (x[2][c] + x[3][c]);
+            const int row = 32 * q + l;
+            if (row < 2 * Hp) {
+                const int wv = row / Hp, unit = row - wv * Hp, owner = unit / Hh;
+                const int lr = wv * Hh + (unit - owner * Hh);  // row among the owner's 2Hh
+                if (owner == r) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) stg[(cb + c) * R2 + lr] = v[c];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        st_async_b32(peer_rcv + (uint32_t)(((sl * WV_N + cb + c) * R2 + lr) * 4), __float_as_uint(v[c]),
+                                     peer_x + 8 * sl);
+                }
+            }
+        }
+        WTRACE(ND - 1 - d, 5);
+        if (has_succ && w == WV_KW) mbar_wait_cluster(&bars[3 + sl], ((ND - 2 - d) >> 1) & 1);
+        tc_fence_before();
+        __syncthreads();
+        WTRACE(ND - 1 - d, 6);
+        const float *ac_s = acts + sl * WV_N * G5, *c_s = cr + (d % 3) * WV_N * Hp;
+        const float *cp_s = cr + ((d + 2) % 3) * WV_N * Hp;
+        const float *dcu_p = dcu + (sl ^ 1) * WV_N * Hh, *dcv_p = dcv + (sl ^ 1) * WV_N * Hh;
+        float *dcu_c = dcu + sl * WV_N * Hh, *dcv_c = dcv + sl * WV_N * Hh;
+        const float *dy_s = dys + sl * WV_N * Hp;
+        const float *rv = rcv + sl * WV_N * R2;
+        if (act_t && ic < n) {
+            const int i = ic;
+            const WvCell ce = tab[sl * WV_N + i];
+            const int up = u0 + i;
+            const bool su = ce.flags & 8, sv = ce.flags & 16, on = ce.flags & 1;
+            float2 da[5], ou = make_float2(0.f, 0.f), ov = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) da[q] = make_float2(0.f, 0.f);
+            const int iu = up + 1 - su0, iv = up - su0;
+            float2 dc = make_float2(0.f, 0.f);
+            if (su) {
+                const float2 t = *reinterpret_cast<const float2 *>(dcu_p + iu * Hh + jl);
+                dc.x += t.x; dc.y += t.y;
+            }
+            if (sv) {
+                const float2 t = *reinterpret_cast<const float2 *>(dcv_p + iv * Hh + jl);
+                dc.x += t.x; dc.y += t.y;
+            }
+            // P of an own row = rank 0's partial + rank 1's partial (fixed order on both ranks)
+            auto prow2 = [&](int col, int lr) -> float2 {
+                const float2 mine = *reinterpret_cast<const float2 *>(stg + col * R2 + lr);
+                const float2 peer = *reinterpret_cast<const float2 *>(rv + col * R2 + lr);
+                return r == 0 ? make_float2(mine.x + peer.x, mine.y + peer.y) : make_float2(peer.x + mine.x, peer.y + mine.y);
+            };
+            if (!on) {
+                if (ce.flags & 2) ou = dc;
+                else if (ce.flags & 4) ov = dc;
+            } else {
+                float2 dh = *reinterpret_cast<const float2 *>(dy_s + i * Hp + j);
+                if (su) {
+                    const float2 t = prow2(iu, jl);
+                    dh.x += t.x * unscale; dh.y += t.y * unscale;
+                }
+                if (sv) {
+                    const float2 t = prow2(iv, Hh + jl);
+                    dh.x += t.x * unscale; dh.y += t.y * unscale;
+                }
+                const float *acl = ac_s + i * G5 + j;
+                const float2 c = *reinterpret_cast<const float2 *>(c_s + i * Hp + j);
+                const float2 cu = (ce.flags & 2) ? *reinterpret_cast<const float2 *>(cp_s + (up - 1 - pu0) * Hp + j)
+                                                 : make_float2(0.f, 0.f);
+                const float2 cv = (ce.flags & 4) ? *reinterpret_cast<const float2 *>(cp_s + (up - pu0) * Hp + j)
+                                                 : make_float2(0.f, 0.f);
+                float gx[5], gy[5], ox[5], oy[5];
+#pragma unroll
+                for (int q = 0; q < 5; ++q) {
+                    const float2 t = *reinterpret_cast<const float2 *>(acl + q * Hp);
+                    gx[q] = t.x; gy[q] = t.y;
+                }
+                auto cellg = [&](float dhv, float dcv_, float cc, float cuu, float cvv, const float *g, float *o,
+                                 float &ouu, float &ovv) {
+                    const float tc = mth(cc);
+                    const float dct = dcv_ + dhv * (a.stable ? g[3] : g[4]) * (1.f - tc * tc);
+                    if (!a.stable) {
+                        o[0] = dct * g[3] * g[0] * (1.f - g[0]);
+                        o[1] = dct * cuu * g[1] * (1.f - g[1]);
+                        o[2] = dct * cvv * g[2] * (1.f - g[2]);
+                        o[3] = dct * g[0] * (1.f - g[3] * g[3]);
+                        o[4] = dhv * tc * g[4] * (1.f - g[4]);
+                        ouu = dct * g[1];
+                        ovv = dct * g[2];
+                    } else {
+                        const float m = g[4] * cuu + (1.f - g[4]) * cvv;
+                        o[0] = dct * g[2] * g[0] * (1.f - g[0]);
+                        o[1] = dct * m * g[1] * (1.f - g[1]);
+                        o[2] = dct * g[0] * (1.f - g[2] * g[2]);
+                        o[3] = dhv * tc * g[3] * (1.f - g[3]);
+                        o[4] = dct * g[1] * (cuu - cvv) * g[4] * (1.f - g[4]);
+                        ouu = dct * g[1] * g[4];
+                        ovv = dct * g[1] * (1.f - g[4]);
+                    }
+                };
+                cellg(dh.x, dc.x, c.x, cu.x, cv.x, gx, ox, ou.x, ov.x);
+                cellg(dh.y, dc.y, c.y, cu.y, cv.y, gy, oy, ou.y, ov.y);
+#pragma unroll
+                for (int q = 0; q < 5; ++q) da[q] = make_float2(ox[q], oy[q]);
+                if (!j0) { ou.x = ov.x = 0.f; }
+                if (!j1) { ou.y = ov.y = 0.f; }
+            }
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                if (!j0) da[q].x = 0.f;
+                if (!j1) da[q].y = 0.f;
+            }
+            *reinterpret_cast<float2 *>(dcu_c + i * Hh + jl) = ou;
+            *reinterpret_cast<float2 *>(dcv_c + i * Hh + jl) = ov;
+            uint32_t *dpp = reinterpret_cast<uint32_t *>(a.dap + (long)ce.cp * 20 * Hp + k * G5 + j);
+            uint32_t *d16 = reinterpret_cast<uint32_t *>(a.da16 + ((long)k * prow + ce.slot) * G5 + j);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                uint32_t hh, hl;
+                split_h2(da[q].x * scale, da[q].y * scale, hh, hl);
+                *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, q * Hh + jl)) = hh;
+                *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, q * Hh + jl)) = hl;
+                if (j0) {
+                    dpp[q * Hp / 2] = hh;
+                    d16[q * Hp / 2] = hh;
+                }
+            }
+        }
+        WTRACE(ND - 1 - d, 7);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        WTRACE(ND - 1 - d, 8);
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (w == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+size_t wv2_fwd_smem(int Hp) {
+    const int Hh = Hp / 2;
+    return 1024 + (size_t)(2 * WV_N * 5 * Hp + WV_N * 10 * Hh + 2 * WV_N * Hh) * 4 + (size_t)4 * wv_bsize(Hp) * 2 +
+           2 * WV_N * sizeof(WvCell) + 64;
+}
+size_t wv2_bwd_smem(int Hp) {
+    const int Hh = Hp / 2;
+    return 1024 + (size_t)(3 * WV_N * 2 * Hh + 2 * WV_N * 5 * Hp + 3 * WV_N * Hp + 4 * WV_N * Hh + 2 * WV_N * Hp) * 4 +
+           (size_t)2 * wv_bsize(5 * Hh) * 2 + 2 * WV_N * sizeof(WvCell) + 64;
+}
+// the CTA-pair wavefront applies (Hp in {32, 64}: K groups of the half split stay whole; BLSTM_MD_PAIR=0: never)
+bool md_wave_pair(const MdGeo &g) {
+    const bool off = getenv("BLSTM_MD_PAIR") && atoi(getenv("BLSTM_MD_PAIR")) == 0;
+    return !off && (g.Hp == 32 || g.Hp == 64) && wv2_fwd_smem(g.Hp) <= 227 * 1024 && wv2_bwd_smem(g.Hp) <= 227 * 1024;
+}
+
 // the tensor-core wavefront applies (BLSTM_MD_WAVE=0: never)
 bool md_wave_ok(const MdGeo &g) {
     const bool off = getenv("BLSTM_MD_WAVE") && atoi(getenv("BLSTM_MD_WAVE")) == 0;  // read per call (tests A/B)
@@ -986,6 +1498,18 @@ bool md_wave_ok(const MdGeo &g) {
     return fits32 && g.Hp <= 64 && mn <= WV_N && wv_fwd_smem(g.Hp) <= 227 * 1024 && wv_bwd_smem(g.Hp) <= 227 * 1024;
 }
 int md_wave_launch(bool fwd, const MdGeo &g, const MdK &a, cudaStream_t st) {
+    if (md_wave_pair(g)) {  // clusters of 2 CTAs per (direction, image)
+        const void *fn = fwd ? (const void *)md_wave2_fwd_kernel : (const void *)md_wave2_bwd_kernel;
+        const size_t smem = fwd ? wv2_fwd_smem(g.Hp) : wv2_bwd_smem(g.Hp);
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -5;
+        ProfScope ps(fwd ? PROF_REC_FWD : PROF_REC_BWD, st);
+        if (fwd)
+            md_wave2_fwd_kernel<<<8 * g.B, WV_THREADS, smem, st>>>(a);
+        else
+            md_wave2_bwd_kernel<<<8 * g.B, WV_THREADS, smem, st>>>(a);
+        note_launch();
+        return cudaGetLastError() == cudaSuccess ? 0 : -5;
+    }
     const void *fn = fwd ? (const void *)md_wave_fwd_kernel : (const void *)md_wave_bwd_kernel;
     const size_t smem = fwd ? wv_fwd_smem(g.Hp) : wv_bwd_smem(g.Hp);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -5;

@@ -63,7 +63,10 @@ def run(U, V, B, D, H, K=20):
     blstm.blstm_profile_enable(0)
     cells = U * V * B
     rec_flop = cells * 4 * 2 * 5 * H * H * 2  # per pass: 2 predecessors x 5H x H FMAs = 2 flop each
-    out = dict(path="wavefront (tcgen05)" if os.environ.get("BLSTM_MD_WAVE", "1") != "0" else "per-diagonal (CUDA cores)",
+    path = "per-diagonal (CUDA cores)" if os.environ.get("BLSTM_MD_WAVE", "1") == "0" else (
+        "wavefront (tcgen05, one CTA per direction x image)" if os.environ.get("BLSTM_MD_PAIR", "1") == "0"
+        else "wavefront (tcgen05, CTA pair per direction x image)")
+    out = dict(path=path,
                U=U, V=V, B=B, D=D, H=H, diagonals=U + V - 1, ms_fwd_bwd=round(ms, 3),
                cells_per_s=round(cells / (ms * 1e-3)), wavefront_fwd_ms=round(fw[0], 3), wavefront_bwd_ms=round(bw[0], 3),
                gemm_ms=round(gm[0], 3), us_per_diagonal_fwd=round(1e3 * fw[0] / (U + V - 1), 2),
@@ -77,7 +80,8 @@ def run(U, V, B, D, H, K=20):
 
 
 if __name__ == "__main__":
-    for wave in ("1", "0"):
+    for wave, pair in (("1", "1"), ("1", "0"), ("0", "0")):
         os.environ["BLSTM_MD_WAVE"] = wave
+        os.environ["BLSTM_MD_PAIR"] = pair
         for H in (32, 64):
             run(32, 256, 16, 16, H)

@@ -79,7 +79,7 @@ def _check(params, theta, x, mask, dy, y, dx, g, stable, tag=""):
     return ey, errs
 
 
-@pytest.mark.parametrize("wave", ["1", "0"])
+@pytest.mark.parametrize("wave", ["1", "single", "0"])
 @pytest.mark.parametrize("U,V,B,D,H,stable,irregular", [
     (5, 7, 3, 6, 16, False, False),
     (6, 4, 2, 9, 5, True, False),
@@ -91,9 +91,11 @@ def _check(params, theta, x, mask, dy, y, dx, g, stable, tag=""):
     (3, 4, 2, 8, 200, True, False),   # R tile beyond 200 KB: the per-diagonal forward
 ])
 def test_mdlstm_matches_oracle(U, V, B, D, H, stable, irregular, wave, monkeypatch):
-    """wave=1: the tensor-core wavefront where it applies (Hp <= 64, min(U, V) <= 32), else the
-    CUDA-core kernels; wave=0 forces the CUDA-core kernels."""
-    monkeypatch.setenv("BLSTM_MD_WAVE", wave)
+    """wave=1: the tensor-core wavefront where it applies (Hp <= 64, min(U, V) <= 32; CTA pairs for
+    Hp in {32, 64}), else the CUDA-core kernels; single: the one-CTA tensor-core wavefront
+    (BLSTM_MD_PAIR=0); wave=0 forces the CUDA-core kernels."""
+    monkeypatch.setenv("BLSTM_MD_WAVE", "0" if wave == "0" else "1")
+    monkeypatch.setenv("BLSTM_MD_PAIR", "0" if wave == "single" else "1")
     _check(*_run(U, V, B, D, H, stable, irregular), stable, f"{U}x{V} B={B} H={H} wave={wave}")
 
 
@@ -104,6 +106,19 @@ def test_mdlstm_bench_grid(H, stable, scale, fbias):
     tensor-core wavefront, every output and gradient against the fp64 oracle.  Parameters are
     well conditioned on this grid (_case: the two-forget cell with fu + fv < 1)."""
     _check(*_run(32, 256, 2, 16, H, stable, True, seed=77, scale=scale, fbias=fbias), stable, f"32x256 H={H}")
+
+
+@pytest.mark.parametrize("H,stable", [(64, False), (32, True)])
+def test_mdlstm_pair_close_to_single(H, stable, monkeypatch):
+    """The CTA-pair wavefront (units split over a cluster of 2, h halves / partial P exchanged over
+    DSMEM) and the one-CTA wavefront agree to ~fp32 rounding on the 32 x 256 grid."""
+    outs = []
+    for pair in ("1", "0"):
+        monkeypatch.setenv("BLSTM_MD_PAIR", pair)
+        outs.append(_run(32, 256, 2, 16, H, stable, True, seed=9, scale=0.25, fbias=-1.5)[5:])
+    (y1, dx1, g1), (y0, dx0, g0) = outs
+    assert norm_rel(y1, y0) < 2e-5, norm_rel(y1, y0)
+    assert l2_rel(dx1, dx0) < 1e-4 and l2_rel(g1, g0) < 1e-4, (l2_rel(dx1, dx0), l2_rel(g1, g0))
 
 
 def test_mdlstm_wave_close_to_cuda_cores(monkeypatch):
