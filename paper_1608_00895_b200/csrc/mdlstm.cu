@@ -990,6 +990,7 @@ size_t wv_bwd_smem(int Hp) {
 //   in fixed order (rank 0's + rank 1's: deterministic).
 // Applies for Hp in {32, 64} (md_wave_pair).
 // ---------------------------------------------------------------------------------------------
+DEVI void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 DEVI void st_async_b32(uint32_t dst_cluster, uint32_t v, uint32_t mbar_cluster) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst_cluster), "r"(v),
                  "r"(mbar_cluster)
@@ -1009,14 +1010,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
     __half *Bb = (__half *)(stg + WV_N * R10);      // [2 parity][2 part][BS]  h of a diagonal (all units)
     float *cst = (float *)(Bb + 4 * BS);            // [2][WV_N][Hh]  c of the own units
     WvCell *tab = (WvCell *)(cst + 2 * WV_N * Hh);  // [2][WV_N]
-    uint64_t *bars = (uint64_t *)(tab + 2 * WV_N);  // [0] mma, [1..2] Z landed, [3..4] partner's h half landed
-    uint32_t *tslot = (uint32_t *)(bars + 5);
+    // [0] mma, [1..2] Z landed, [3..4] partner's h half landed, [5..6] slot free (consumers -> producer)
+    uint64_t *bars = (uint64_t *)(tab + 2 * WV_N);
+    uint32_t *tslot = (uint32_t *)(bars + 7);
     const int w = warp_id(), l = lane_id(), tid = threadIdx.x;
     const int prow = (U + 1) * (V + 1) * B;
 
     if (tid == 0) {
         mbar_init(&bars[0], Mt);
-        for (int i = 1; i < 5; ++i) mbar_init(&bars[i], 1);
+        for (int i = 1; i < 7; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     if (w == 0) {
@@ -1024,7 +1026,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
         tmem_relinquish();
     }
     for (int e = tid; e < 2 * BS; e += WV_THREADS) reinterpret_cast<uint32_t *>(Bb)[e] = 0u;  // 4 B halves
-    if (tid < WV_N && tid <= wv_u1(0, U) - wv_u0(0, V)) tab[tid] = wv_cell(a, k, b, 0, tid);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -1055,10 +1056,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
                      &bars[1 + sl]);
         }
     };
-    if (w == 15) issue_z(0, 0);
-    // epilogue: unit pair pi (own units jl = 2 pi, 2 pi + 1; global j = r Hh + jl), cell ic
-    const int pi = tid & 15, ic = tid >> 4, jl = 2 * pi, j = r * Hh + jl;
-    const bool act_t = jl < Hh, j0 = j < H, j1 = j + 1 < H, hodd = H & 1;
+    // warp 15 is the producer: Z rows and the cell table of diagonal d2 into slot d2 & 1 as soon as the
+    // consumers (warps 0-14, named barrier 1) released it after diagonal d2 - 2 -- the ~32 bulk copies
+    // a diagonal needs cost ~1 us of issue and stay off the consumers' per-diagonal chain
+    if (w == 15) {
+        for (int d2 = 0; d2 < ND; ++d2) {
+            const int sl2 = d2 & 1;
+            if (d2 >= 2) mbar_wait(&bars[5 + sl2], ((d2 - 2) >> 1) & 1);
+            const int n2 = wv_u1(d2, U) - wv_u0(d2, V) + 1;
+            if (l < n2) tab[sl2 * WV_N + l] = wv_cell(a, k, b, d2, l);
+            __syncwarp();  // the table is written before lane 0's arrive (release) in issue_z
+            issue_z(d2, sl2);
+        }
+    } else {
+    // epilogue work item (unit pair pi: own units jl = 2 pi, 2 pi + 1, global j = r Hh + jl; cell ic)
+    const bool hodd = H & 1;
     const uint32_t idesc = idesc_f16(128, WV_N, 0, 0);
     const uint32_t bb_addr = smem_u32(Bb), peer_bb = mapa_shared(bb_addr, (uint32_t)(r ^ 1));
     const uint32_t peer_x = mapa_shared(smem_u32(&bars[3]), (uint32_t)(r ^ 1));
@@ -1080,47 +1092,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
             mma_commit_w(&bars[0]);
         }
         WTRACE(d, 1);
-        if (w == 15 && d + 1 < ND) {
-            issue_z(d + 1, sl ^ 1);
-            const int n1 = wv_u1(d + 1, U) - wv_u0(d + 1, V) + 1;
-            if (l < n1) tab[(sl ^ 1) * WV_N + l] = wv_cell(a, k, b, d + 1, l);
-        }
         // the partner's h_d: n cells x Hh units x (hi, lo) fp16
         if (w == 14 && l == 0) mbar_arrive_expect_tx(&bars[3 + sl], (uint32_t)(n * Hh * 4));
         WTRACE(d, 2);
-        if (w == Mt) {
+        if (w == 0) {  // (after its MMA issue; thread 0's trace then shows the waits)
             mbar_wait(&bars[1 + sl], (d >> 1) & 1);
             if (d > 0) mbar_wait(&bars[0], mph);
         }
         if (d > 0) mph ^= 1;
         WTRACE(d, 3);
-        __syncthreads();
+        named_bar(1, WV_THREADS - 32);
         WTRACE(d, 4);
         if (d > 0) {
             tc_fence_after();
-            const int q = w & 3, cb = 8 * (w >> 2);
-            float v[3][8];
+            // lane quarter q = w & 3 (the warp's TMEM lanes); 8-column blocks: warp 11 also takes the
+            // producer warp's block 3 (a 17th warp measured slower: 96 registers, spills)
+            const int q = w & 3;
+            for (int cbi = w >> 2; cbi < 4; cbi += (w == 11 ? 1 : 4)) {
+                const int cb = 8 * cbi;
+                float v[3][8];
 #pragma unroll
-            for (int mt = 0; mt < 3; ++mt)
-                if (mt < Mt) tmem_ld8f(tmem + ((uint32_t)(32 * q) << 16) + colD + 32 * mt + cb, v[mt]);
-            tmem_ld_wait();
+                for (int mt = 0; mt < 3; ++mt)
+                    if (mt < Mt) tmem_ld8f(tmem + ((uint32_t)(32 * q) << 16) + colD + 32 * mt + cb, v[mt]);
+                tmem_ld_wait();
 #pragma unroll
-            for (int mt = 0; mt < 3; ++mt) {
-                const int row = mt * 128 + 32 * q + l;
-                if (mt < Mt && row < R10) {
+                for (int mt = 0; mt < 3; ++mt) {
+                    const int row = mt * 128 + 32 * q + l;
+                    if (mt < Mt && row < R10) {
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) stg[(cb + c) * R10 + row] = v[mt][c];
+                        for (int c = 0; c < 8; ++c) stg[(cb + c) * R10 + row] = v[mt][c];
+                    }
                 }
             }
         }
         WTRACE(d, 5);
         tc_fence_before();
-        __syncthreads();
+        named_bar(1, WV_THREADS - 32);
         WTRACE(d, 6);
         const float *cprev = cst + (sl ^ 1) * WV_N * Hh;
         float *ccur = cst + sl * WV_N * Hh;
         const float *zs = Zs + sl * WV_N * G5;
-        if (act_t && ic < n) {
+        for (int item = tid; item < 16 * WV_N; item += WV_THREADS - 32) {
+            const int pi = item & 15, ic = item >> 4, jl = 2 * pi, j = r * Hh + jl;
+            const bool j0 = j < H, j1 = j + 1 < H;
+            if (jl >= Hh || ic >= n) continue;
             const int i = ic;
             const WvCell ce = tab[sl * WV_N + i];
             const int up = u0 + i;
@@ -1192,11 +1207,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
         WTRACE(d, 7);
         fence_async_smem();
         tc_fence_before();
-        __syncthreads();
+        named_bar(1, WV_THREADS - 32);
+        if (tid == 0) mbar_arrive(&bars[5 + sl]);  // slot sl (Z, cell table of diagonal d) free
         WTRACE(d, 8);
     }
     // the partner's h of the last diagonal (never read) has landed: no remote store is outstanding
     if (tid == 0) mbar_wait_cluster(&bars[3 + ((ND - 1) & 1)], ((ND - 1) >> 1) & 1);
+    }  // consumers
     tc_fence_before();
     __syncthreads();
     cluster_sync();
@@ -1223,8 +1240,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
     float *dcv = dcu + 2 * WV_N * Hh;
     float *dys = dcv + 2 * WV_N * Hh;               // [2][WV_N][Hp]
     WvCell *tab = (WvCell *)(dys + 2 * WV_N * Hp);  // [2][WV_N]
-    uint64_t *bars = (uint64_t *)(tab + 2 * WV_N);  // [0] mma, [1..2] inputs landed, [3..4] partner's partial landed
-    uint32_t *tslot = (uint32_t *)(bars + 5);
+    // [0] mma, [1..2] inputs landed, [3..4] partner's partial landed, [5..6] slot free (consumers -> producer)
+    uint64_t *bars = (uint64_t *)(tab + 2 * WV_N);
+    uint32_t *tslot = (uint32_t *)(bars + 7);
     const int w = warp_id(), l = lane_id(), tid = threadIdx.x;
     const int prow = (U + 1) * (V + 1) * B;
     const float scale = (float)(1 << DA_SHIFT), unscale = 1.f / scale;
@@ -1232,7 +1250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
 
     if (tid == 0) {
         mbar_init(&bars[0], WV_KW);
-        for (int i = 1; i < 5; ++i) mbar_init(&bars[i], 1);
+        for (int i = 1; i < 7; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     if (w == 0) {
@@ -1265,20 +1283,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
         const int np = d2 >= 1 ? wv_u1(d2 - 1, U) - wv_u0(d2 - 1, V) + 1 : 0;
         WvCell ce{};
         if (l < n) ce = wv_cell(a, k, b, d2, l);
+        const float *dyp = a.dy + (long)ce.cp * 4 * H + k * H;
+        float *dyd = dys + (sl * WV_N + l) * Hp;
+        if (l < n) {  // generic writes first: lane 0's arrive (release) below publishes them
+            tab[sl * WV_N + l] = ce;
+            if (!dy_bulk)
+                for (int e = 0; e < H; ++e) dyd[e] = dyp[e];  // (rare: H * 4 not a multiple of 16)
+        }
+        __syncwarp();
         uint32_t bytes = (uint32_t)(n * G5 * 4 + np * Hp * 4 + (with_c ? n * Hp * 4 : 0) + (dy_bulk ? n * H * 4 : 0));
         if (l == 0) mbar_arrive_expect_tx(&bars[1 + sl], bytes);
         __syncwarp();
         if (l < n) {
-            tab[sl * WV_N + l] = ce;
             bulk_g2s(smem_u32(acts + (sl * WV_N + l) * G5), a.act + (long)ce.ck * G5, (uint32_t)(G5 * 4), &bars[1 + sl]);
             if (with_c)
                 bulk_g2s(smem_u32(cr + ((d2 % 3) * WV_N + l) * Hp), a.c + (long)ce.ck * Hp, (uint32_t)(Hp * 4), &bars[1 + sl]);
-            const float *dyp = a.dy + (long)ce.cp * 4 * H + k * H;
-            float *dyd = dys + (sl * WV_N + l) * Hp;
-            if (dy_bulk)
-                bulk_g2s(smem_u32(dyd), dyp, (uint32_t)(H * 4), &bars[1 + sl]);
-            else
-                for (int e = 0; e < H; ++e) dyd[e] = dyp[e];
+            if (dy_bulk) bulk_g2s(smem_u32(dyd), dyp, (uint32_t)(H * 4), &bars[1 + sl]);
         }
         if (l < np) {
             const int up = wv_u0(d2 - 1, V) + l;
@@ -1287,9 +1307,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
                      &bars[1 + sl]);
         }
     };
-    if (w == 15) issue_in(ND - 1, true);
-    const int pi = tid & 15, ic = tid >> 4, jl = 2 * pi, j = r * Hh + jl;
-    const bool act_t = jl < Hh, j0 = j < H, j1 = j + 1 < H;
+    // warp 15 is the producer (see md_wave2_fwd_kernel): the inputs of diagonal d2 into slot d2 & 1
+    // once the consumers released it after diagonal d2 + 2
+    if (w == 15) {
+        for (int d2 = ND - 1; d2 >= 0; --d2) {
+            if (d2 + 2 <= ND - 1) mbar_wait(&bars[5 + (d2 & 1)], ((ND - 3 - d2) >> 1) & 1);
+            issue_in(d2, d2 == ND - 1);
+        }
+    } else {
     const uint32_t idesc = idesc_f16(128, WV_N, 0, 0);
     const uint32_t peer_rcv = mapa_shared(smem_u32(rcv), (uint32_t)(r ^ 1));
     const uint32_t peer_x = mapa_shared(smem_u32(&bars[3]), (uint32_t)(r ^ 1));
@@ -1310,21 +1335,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
             mma_commit_w(&bars[0]);
         }
         WTRACE(ND - 1 - d, 1);
-        if (w == 15 && d >= 1) issue_in(d - 1, false);
         if (has_succ && w == 14 && l == 0) mbar_arrive_expect_tx(&bars[3 + sl], (uint32_t)(WV_N * R2 * 4));
         WTRACE(ND - 1 - d, 2);
-        if (w == WV_KW) {
+        if (w == 0) {  // (after its MMA issue; thread 0's trace then shows the waits)
             mbar_wait(&bars[1 + sl], (iph >> sl) & 1);
             if (has_succ) mbar_wait(&bars[0], mph);
         }
         iph ^= 1u << sl;
         if (has_succ) mph ^= 1;
         WTRACE(ND - 1 - d, 3);
-        __syncthreads();
+        named_bar(1, WV_THREADS - 32);
         WTRACE(ND - 1 - d, 4);
         if (has_succ) {  // the partial's rows: own units -> stg, the partner's -> its receive buffer
-            tc_fence_after();
-            const int q = w & 3, cb = 8 * (w >> 2);
+          tc_fence_after();
+          const int q = w & 3;
+          for (int cbi = w >> 2; cbi < 4; cbi += (w == 11 ? 1 : 4)) {
+            const int cb = 8 * cbi;
             float x[WV_KW][8], v[8];
 #pragma unroll
             for (int aa = 0; aa < WV_KW; ++aa) tmem_ld8f(tmem + ((uint32_t)(32 * q) << 16) + colD + 32 * aa + cb, x[aa]);
@@ -1345,11 +1371,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
                                      peer_x + 8 * sl);
                 }
             }
+          }
         }
         WTRACE(ND - 1 - d, 5);
-        if (has_succ && w == WV_KW) mbar_wait_cluster(&bars[3 + sl], ((ND - 2 - d) >> 1) & 1);
+        if (has_succ && w == 0) mbar_wait_cluster(&bars[3 + sl], ((ND - 2 - d) >> 1) & 1);
+        WTRACE(ND - 1 - d, 9);
         tc_fence_before();
-        __syncthreads();
+        named_bar(1, WV_THREADS - 32);
         WTRACE(ND - 1 - d, 6);
         const float *ac_s = acts + sl * WV_N * G5, *c_s = cr + (d % 3) * WV_N * Hp;
         const float *cp_s = cr + ((d + 2) % 3) * WV_N * Hp;
@@ -1357,7 +1385,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
         float *dcu_c = dcu + sl * WV_N * Hh, *dcv_c = dcv + sl * WV_N * Hh;
         const float *dy_s = dys + sl * WV_N * Hp;
         const float *rv = rcv + sl * WV_N * R2;
-        if (act_t && ic < n) {
+        for (int item = tid; item < 16 * WV_N; item += WV_THREADS - 32) {
+            const int pi = item & 15, ic = item >> 4, jl = 2 * pi, j = r * Hh + jl;
+            const bool j0 = j < H, j1 = j + 1 < H;
+            if (jl >= Hh || ic >= n) continue;
             const int i = ic;
             const WvCell ce = tab[sl * WV_N + i];
             const int up = u0 + i;
@@ -1460,9 +1491,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
         WTRACE(ND - 1 - d, 7);
         fence_async_smem();
         tc_fence_before();
-        __syncthreads();
+        named_bar(1, WV_THREADS - 32);
+        if (tid == 0) mbar_arrive(&bars[5 + sl]);  // slot sl (inputs of diagonal d) free
         WTRACE(ND - 1 - d, 8);
     }
+    }  // consumers
     tc_fence_before();
     __syncthreads();
     cluster_sync();

@@ -11,6 +11,10 @@ FWD = [(0, None), (1, "MMA issue"), (2, "Z prefetch + mask loads"), (3, "(waitin
        (5, "TMEM ld -> staging"), (6, "__syncthreads"), (7, "gates + cell + stores"), (8, "fence + __syncthreads")]
 BWD = [(0, None), (1, "MMA issue"), (2, "input prefetch + dy loads"), (3, "(waiting warp: inputs + MMA)"), (4, "__syncthreads"),
        (5, "TMEM ld -> staging"), (6, "__syncthreads"), (7, "gate gradients + stores"), (8, "fence + __syncthreads")]
+# the CTA-pair backward (BLSTM_MD_PAIR=1, Hp in {32, 64}): slot 9 = after the partner's partial landed
+BWD2 = [(0, None), (1, "MMA issue"), (2, "input prefetch"), (3, "wait inputs + MMA"), (4, "__syncthreads"),
+        (5, "TMEM ld -> own stg / partner st.async"), (9, "wait partner's partial"), (6, "__syncthreads"),
+        (7, "gate gradients + stores"), (8, "fence + __syncthreads")]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--H", type=int, default=64)
@@ -44,4 +48,4 @@ f = tf.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
 b = tb.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
 print(f"U={U} V={V} B={B} H={H}")
 report("wavefront forward (per diagonal)", f, FWD)
-report("wavefront backward (per diagonal)", b, BWD)
+report("wavefront backward (per diagonal)", b, BWD2 if os.environ.get("BLSTM_MD_PAIR", "1") != "0" and H in (32, 64) else BWD)
