@@ -229,6 +229,9 @@ int grid_of(long n) {
 #define BLSTM_PF_THREADS 256  // 512 (4 units per thread) measured slower: C5 forward 33.4 vs 31.3 ms
 #endif
 constexpr int PF_THREADS = BLSTM_PF_THREADS;  // 256 or 512
+#ifndef BLSTM_PTRACE_CTA
+#define BLSTM_PTRACE_CTA 0  // the persistent step kernels' traced CTA (-1: the last, i.e. direction 1)
+#endif
 constexpr int PF_CH = PF_THREADS / 128;       // column chunks per TMEM lane quarter
 constexpr int PF_CW = 64 / PF_CH;             // tile columns a thread finalizes (32 or 16)
 constexpr int PF_UPT = PF_CW / 4;             // units a thread finalizes (8 or 4)
@@ -243,7 +246,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 #ifdef BLSTM_TRACE
 #define PTR(k) \
     if (tr) tr[(size_t)s * 16 + (k)] = (unsigned long long)clock64()
-    unsigned long long *tr = (blockIdx.x == 0 && threadIdx.x == 0) ? trace : nullptr;
+    unsigned long long *tr = (blockIdx.x == (BLSTM_PTRACE_CTA < 0 ? gridDim.x - 1 : BLSTM_PTRACE_CTA) && threadIdx.x == 0)
+                                 ? trace : nullptr;
+    if (tr) tr[15] = (unsigned long long)clock64();  // kernel entry (slot 15 of step 0)
+    if (tr) tr[14] = globaltimer_ns();                // (slot 14: entry / exit in globaltimer ns)
 #else
 #define PTR(k)
 #endif
@@ -513,6 +519,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // no remote store into this CTA's shared memory is outstanding
+#ifdef BLSTM_TRACE
+    if (tr) tr[(size_t)(T - 1) * 16 + 14] = globaltimer_ns();
+#endif
     if (w == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, 128);

@@ -68,6 +68,9 @@ def main():
     f = tf.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
     b = tb.cpu().numpy().astype(np.float64) * 1e3 / args.mhz
     if cfg.H > 512 and os.environ.get("BLSTM_STEP_PERSIST") != "0":  # the step path (H beyond the cluster kernels)
+        print(f"forward kernel entry -> exit (globaltimer): {(tf.cpu().numpy()[-1, 14] - tf.cpu().numpy()[0, 14]) / 1e3:.1f} us")
+        print(f"forward kernel prologue (entry -> step 0): {f[0, 0] - f[0, 15]:.0f} ns; "
+              f"scan (step 0 -> end of the last step): {(f[-1, 9] - f[0, 0]) / 1e3:.1f} us")
         report("forward (persistent step path)", f, PFWD)
         if os.environ.get("BLSTM_STEP_PERSIST_BWD") != "0":
             report("backward (persistent step path)", b, PBWD)  # rows in processing order (s)
