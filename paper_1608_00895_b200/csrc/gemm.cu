@@ -561,7 +561,7 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
         const double t_tile = 2.0 * GEMM_BM * BN * (double)p.K / 9.0e12;   // one full-K tile on one SM (s)
         const double mn_bytes = 8.0 * (double)p.M * p.N;                    // a partial written + read (fp32)
         double best = (double)((tiles + max_ctas - 1) / max_ctas) * t_tile;
-        for (int s = 2; s <= 8; ++s) {
+        for (int s = 2; s <= 64; ++s) {  // (few-tile GEMMs over a very long K: the MDLSTM dR, 3 tiles x K = 132k)
             if (num_kb / s < 16 || (long)s * p.M * p.N > p.splitk_elems) break;  // >= 16 k-blocks per split
             const double est = (double)((tiles * s + max_ctas - 1) / max_ctas) * t_tile / s + s * mn_bytes / 5.0e12;
             if (est < 0.97 * best) { best = est; S = s; }

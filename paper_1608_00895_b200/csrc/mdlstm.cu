@@ -694,12 +694,13 @@ __global__ void __launch_bounds__(WV_THREADS, 1) md_wave_fwd_kernel(MdK a) {
                 split_h2(h.x, h.y, hh, hl);
                 *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, j)) = hh;
                 *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, j)) = hl;
+                // the dR GEMMs' operand, every unit (padding: 0), so only its border rows need zeroing
+                *reinterpret_cast<__half2 *>(a.h16 + ((long)k * prow + ce.slot) * Hp + j) = __floats2half2_rn(h.x, h.y);
                 if (j0) {  // saved state (Hp-strided rows: pairs stay 8-byte aligned) and the outputs
                     float *ac = a.act + (long)ce.ck * G5 + j;
 #pragma unroll
                     for (int q = 0; q < 5; ++q) *reinterpret_cast<float2 *>(ac + q * Hp) = g[q];
                     *reinterpret_cast<float2 *>(a.c + (long)ce.ck * Hp + j) = cn;
-                    *reinterpret_cast<__half2 *>(a.h16 + ((long)k * prow + ce.slot) * Hp + j) = __floats2half2_rn(h.x, h.y);
                     float *yp = a.y + (long)ce.cp * 4 * H + k * H + j;
                     if (!hodd && j1) {
                         *reinterpret_cast<float2 *>(yp) = h;
@@ -949,10 +950,8 @@ __global__ void __launch_bounds__(WV_THREADS, 1) md_wave_bwd_kernel(MdK a) {
                     split_h2(da[q].x * scale, da[q].y * scale, hh, hl);
                     *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, q * Hp + j)) = hh;
                     *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, q * Hp + j)) = hl;
-                    if (j0) {
-                        reinterpret_cast<uint32_t *>(dpp)[q * Hp / 2] = hh;
-                        reinterpret_cast<uint32_t *>(d16)[q * Hp / 2] = hh;
-                    }
+                    reinterpret_cast<uint32_t *>(dpp)[q * Hp / 2] = hh;  // (padding units: zeros)
+                    reinterpret_cast<uint32_t *>(d16)[q * Hp / 2] = hh;
                 }
             }
         }
@@ -1189,12 +1188,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
             *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(Bb) + off + BS * 2) = hl;
             st_async_b32(peer_bb + off, hh, peer_x + 8 * sl);
             st_async_b32(peer_bb + off + BS * 2, hl, peer_x + 8 * sl);
+            *reinterpret_cast<__half2 *>(a.h16 + ((long)k * prow + ce.slot) * Hp + j) = __floats2half2_rn(h.x, h.y);
             if (j0) {
                 float *ac = a.act + (long)ce.ck * G5 + j;
 #pragma unroll
                 for (int q = 0; q < 5; ++q) *reinterpret_cast<float2 *>(ac + q * Hp) = g[q];
                 *reinterpret_cast<float2 *>(a.c + (long)ce.ck * Hp + j) = cn;
-                *reinterpret_cast<__half2 *>(a.h16 + ((long)k * prow + ce.slot) * Hp + j) = __floats2half2_rn(h.x, h.y);
                 float *yp = a.y + (long)ce.cp * 4 * H + k * H + j;
                 if (!hodd && j1) {
                     *reinterpret_cast<float2 *>(yp) = h;
@@ -1482,10 +1481,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
                 split_h2(da[q].x * scale, da[q].y * scale, hh, hl);
                 *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, q * Hh + jl)) = hh;
                 *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, q * Hh + jl)) = hl;
-                if (j0) {
-                    dpp[q * Hp / 2] = hh;
-                    d16[q * Hp / 2] = hh;
-                }
+                dpp[q * Hp / 2] = hh;  // (padding units: zeros)
+                d16[q * Hp / 2] = hh;
             }
         }
         WTRACE(ND - 1 - d, 7);
@@ -1613,9 +1610,29 @@ __global__ void md_pack_rt_kernel(const float *theta, long P1, int D, int H, flo
         rt[e] = theta[k * P1 + (long)D * G + (long)w * H * G + (long)j * G + q];
     }
 }
-// grad W_k[f][q*H + j] += gW[k*5Hp + q*Hp + j][f]; Ru, Rv from gR [4][2][5Hp][Hp]; b from gb [20Hp]
+// zero the border rows (u' = -1 or v' = -1) of a zero-bordered [4][(U+1)(V+1)B][width] fp16 grid
+// (h16, da16): the tensor-core wavefront writes every interior row, so no full memset is needed
+__global__ void md_zero_border_kernel(__half *grid, int U, int V, int B, int width) {
+    const long per = (long)(V + 1 + U) * B, prow = (long)(U + 1) * (V + 1) * B;
+    const long n = 4 * per * (width / 2);
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x) {
+        const long row = e / (width / 2);
+        const int col = (int)(e - row * (width / 2)) * 2;
+        const int k = (int)(row / per);
+        const long br = row - k * per;
+        // border row br: the first (V+1) B rows (u' = -1), then rows ((up+1)(V+1)) B + b (v' = -1)
+        const long slot = br < (long)(V + 1) * B ? br : ((br / B - (V + 1) + 1) * (long)(V + 1)) * B + br % B;
+        *reinterpret_cast<__half2 *>(grid + (k * prow + slot) * width + col) = __floats2half2_rn(0.f, 0.f);
+    }
+}
+// x16 [cells][Dp] column D <- 1: the dW GEMM's column D is then db = the column sums of dA (D < Dp)
+__global__ void md_ones_col_kernel(__half *x16, long cells, int Dp, int D) {
+    for (long r = blockIdx.x * (long)blockDim.x + threadIdx.x; r < cells; r += (long)gridDim.x * blockDim.x)
+        x16[r * Dp + D] = __float2half_rn(1.f);
+}
+// grad W_k[f][q*H + j] += gW[k*5Hp + q*Hp + j][f]; Ru, Rv from gR [4][2][5Hp][Hp]; b from gb[row * gbs]
 __global__ void md_scatter_kernel(float *grad, long P1, int D, int H, int Hp, int Dp, const float *gW, const float *gR,
-                                  const float *gb) {
+                                  const float *gb, int gbs) {
     const int G = 5 * H;
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < 4 * P1; e += (long)gridDim.x * blockDim.x) {
         const int k = (int)(e / P1);
@@ -1632,7 +1649,7 @@ __global__ void md_scatter_kernel(float *grad, long P1, int D, int H, int Hp, in
             v = gR[(((long)k * 2 + w) * 5 * Hp + q * Hp + j) * Hp + m];
         } else {
             const int n = (int)(o - (long)D * G - 2L * H * G), q = n / H, j = n % H;
-            v = gb[(long)k * 5 * Hp + q * Hp + j];
+            v = gb[((long)k * 5 * Hp + q * Hp + j) * gbs];
         }
         grad[e] += v;
     }
@@ -1753,7 +1770,14 @@ int md_forward(const MdGeo &g, const float *theta, const float *x, const uint8_t
         md_split_x_kernel<<<grid1(g.cells * g.Dp), 256, 0, st>>>(x, g.D, g.Dp, g.cells, xcat);
         note_launch(2);
     }
-    if (cudaMemsetAsync(res + w.h16, 0, (size_t)4 * g.prow * g.Hp * 2, st) != cudaSuccess) return -5;
+    if (md_wave_ok(g)) {  // the wavefront writes every interior row (all Hp units): zero the borders only
+        ProfScope ps(PROF_OTHER, st);
+        md_zero_border_kernel<<<grid1(4L * (g.U + g.V + 1) * g.B * g.Hp / 2), 256, 0, st>>>(
+            (__half *)(res + w.h16), g.U, g.V, g.B, g.Hp);
+        note_launch();
+    } else if (cudaMemsetAsync(res + w.h16, 0, (size_t)4 * g.prow * g.Hp * 2, st) != cudaSuccess) {
+        return -5;
+    }
     // Z = x W + b in split precision: x_hi W_hi + x_hi W_lo + x_lo W_hi (fp16 tensor-core operands,
     // fp32 accumulate; operand error ~2^-22 instead of 2^-11: the 2-D recurrence compounds the input
     // error along paths of up to U+V cells), one GEMM over K = 3 Dp
@@ -1796,8 +1820,21 @@ int md_backward(const MdGeo &g, const float *theta, const float *x, const uint8_
         }
     }
     if (cast_x_f16(x, g.D, g.D, x16, g.Dp, g.cells, st)) return -5;
-    if (cudaMemsetAsync(ws + w.da16, 0, (size_t)4 * g.prow * 5 * g.Hp * 2, st) != cudaSuccess) return -5;
-    if (cudaMemsetAsync(ws + w.dap, 0, (size_t)g.cells * 20 * g.Hp * 2, st) != cudaSuccess) return -5;
+    const bool ones = g.D < g.Dp;  // db through the dW GEMM (a column of ones in x), else column sums
+    if (ones) {
+        ProfScope ps(PROF_OTHER, st);
+        md_ones_col_kernel<<<grid1(g.cells), 256, 0, st>>>(x16, g.cells, g.Dp, g.D);
+        note_launch();
+    }
+    if (wave) {  // every interior row and every unit of dap / da16 is written: zero da16's borders only
+        ProfScope ps(PROF_OTHER, st);
+        md_zero_border_kernel<<<grid1(4L * (g.U + g.V + 1) * g.B * 5 * g.Hp / 2), 256, 0, st>>>(
+            (__half *)(ws + w.da16), g.U, g.V, g.B, 5 * g.Hp);
+        note_launch();
+    } else {
+        if (cudaMemsetAsync(ws + w.da16, 0, (size_t)4 * g.prow * 5 * g.Hp * 2, st) != cudaSuccess) return -5;
+        if (cudaMemsetAsync(ws + w.dap, 0, (size_t)g.cells * 20 * g.Hp * 2, st) != cudaSuccess) return -5;
+    }
     a.trace = rec_trace_bwd();
     if (wave && md_wave_launch(false, g, a, st)) return -5;
     const int prc = wave ? 0 : md_persist(false, a, g, (uint32_t *)(ws + w.bar), st);
@@ -1835,13 +1872,16 @@ int md_backward(const MdGeo &g, const float *theta, const float *x, const uint8_
             gr.splitk_ws = gsk; gr.splitk_elems = 8L << 20;
             if (gemm_f16({A, 5L * g.Hp, 1}, {Hb, g.Hp, 1}, gr, 0, st)) return -5;
         }
-    if (cudaMemsetAsync(ws + w.gb, 0, (size_t)20 * g.Hp * 4, st) != cudaSuccess) return -5;
-    if (colsum_f16_add(dap, g.cells, 20 * g.Hp, 20L * g.Hp, alpha, (float *)(ws + w.gb), (float *)(ws + w.cs), st))
-        return -5;
+    if (!ones) {
+        if (cudaMemsetAsync(ws + w.gb, 0, (size_t)20 * g.Hp * 4, st) != cudaSuccess) return -5;
+        if (colsum_f16_add(dap, g.cells, 20 * g.Hp, 20L * g.Hp, alpha, (float *)(ws + w.gb), (float *)(ws + w.cs), st))
+            return -5;
+    }
     {
         ProfScope ps(PROF_OTHER, st);
+        const float *gb = ones ? (const float *)(ws + w.gW) + g.D : (const float *)(ws + w.gb);
         md_scatter_kernel<<<grid1(4 * a.P1), 256, 0, st>>>(grad, a.P1, g.D, g.H, g.Hp, g.Dp, (const float *)(ws + w.gW),
-                                                           (const float *)(ws + w.gR), (const float *)(ws + w.gb));
+                                                           (const float *)(ws + w.gR), gb, ones ? g.Dp : 1);
         note_launch();
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
