@@ -846,7 +846,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         if (pr == 0 && w < 4) {  // even CTA: warp-collective issue of tile w / KP, K part w % KP
             // the partner's dA half has landed here, and the partner's own B operand is complete
             mbar_wait_cluster(&bars[4], k_done & 1);
+            TRACE(12);
             mbar_wait_cluster(&bars[5], k_done & 1);
+            TRACE(13);
             if (threadIdx.x == 0 && k_done + 1 < T) mbar_arrive_expect_tx(&bars[4], DA_TX);
             tc_fence_after();
             const int mt = w / KP, kp = w % KP, kpn = 16 / KP;  // K steps of 16 per part

@@ -26,7 +26,8 @@ FWD = [(0, None), (11, "wait own half of h"), (1, "wait partner relay"), (2, "MM
        (8, "TMEM ld"), (9, "gate activations"), (10, "cell update + staging"), (7, "proxy fence"),
        (4, "bulk_wait + __syncthreads"), (5, "send h + arm"), (6, "Z prefetch")]
 BWD = [(0, None), (1, "issue next-step loads"), (2, "wait P + gather"), (8, "wait inputs + smem reads"), (9, "dA math + smem"),
-       (3, "fences + __syncthreads"), (10, "MMA issue + dA stores"), (4, "MMA wait"),
+       (3, "fences + __syncthreads"), (12, "wait partner's dA half"), (13, "wait partner's B complete"),
+       (10, "MMA issue + dA stores"), (4, "MMA wait"),
        (11, "TMEM ld"), (6, "P staging"), (7, "bulk_wait + __syncthreads"), (5, "send P + loads")]
 # the persistent forward of the step-launched path (rec_step.cu, BLSTM_STEP_PERSIST=1)
 PFWD = [(0, None), (1, "Z loads issued"), (2, "grid barrier wait"), (3, "TMA issue"), (4, "MMA wait"),
