@@ -34,8 +34,8 @@ struct GemmCfg {
     static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
     static constexpr int B_BYTES = BN * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + 2 * BN * 4 /*bias*/ +
-                                      GEMM_EPI_WARPS * 2048 /*store staging*/;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                                      GEMM_EPI_WARPS * 4096 /*store staging*/;
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -204,14 +204,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int row_in_tile = q * 32 + lane_id();
         int acc = 0;
         uint32_t acc_phase = 0;
-        float *sbias = reinterpret_cast<float *>(tmem_slot + 4);  // [2][BN], one per accumulator
         const int et = threadIdx.x - 64;                           // 0..255 over the epilogue warps
         const int chalf = (warp - 2) / 4;                          // column half of this warp
-        // row-major stores go through a per-warp [32 rows][16 cols] staging tile (float4 index
-        // XOR-swizzled by row) so each store instruction writes 8 rows x 64 contiguous bytes; direct
-        // per-lane row stores touched 32 rows x 16 B (half sectors), which bound the output-heavy GEMMs
-        float4 *stg4 = reinterpret_cast<float4 *>(sbias + 2 * BN) + (warp - 2) * 128;
+        // row-major stores go through a per-warp [32 rows][32 cols] staging tile (float4 index
+        // XOR-swizzled by row), so each store instruction writes 4 rows x 128 contiguous bytes (whole
+        // lines); two TMEM loads are in flight per wait, and the bias comes from warp-uniform L1
+        // loads issued before that wait (no per-tile barrier to stage it)
+        float4 *stg4 = reinterpret_cast<float4 *>(tmem_slot + 4) + (warp - 2) * 256;
         const int lane = lane_id();
+        (void)et;
         for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
             const int bt = item / per_batch, bi = item - bt * per_batch;
             const int split = bi / num_tiles, tile = bi - split * num_tiles;
@@ -219,36 +220,46 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tile_coords<BN>(tile, num_m, num_n, p, mt, nt);
             const int m0 = mt * GEMM_BM, n0 = nt * BN;
             float *Cbase = p.C + bt * p.c_bstride + split * p.split_stride;
-            // this tile's bias slice -> shared memory while the MMAs run (a global load per
-            // element in the store loop stalled the epilogue on L2 latency)
-            for (int k = et; k < BN; k += 32 * GEMM_EPI_WARPS)
-                sbias[acc * BN + k] = (p.bias && n0 + k < p.N) ? p.bias[n0 + k] : 0.f;
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * GEMM_EPI_WARPS) : "memory");
-            const float *bs = sbias + acc * BN;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int m = m0 + row_in_tile;
             float *crow = Cbase + (size_t)m * p.ldc;
 #pragma unroll 1
-            for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 16) {
-                float v[16];
-                tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
-                tmem_ld_wait();
+            for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
+                float v[32];
+                const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c;
+                tmem_ld16(ta, *reinterpret_cast<float(*)[16]>(&v[0]));
+                tmem_ld16(ta + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
                 const int n = n0 + c;
+                float bv[32];
+                if (p.bias && n + 32 <= p.N && ((uintptr_t)(p.bias + n) & 15) == 0) {  // warp-uniform: broadcast
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = v[j] * p.alpha + bs[c + j];
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 b4 = __ldg(reinterpret_cast<const float4 *>(p.bias + n + j));
+                        bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+                    }
+                } else if (p.bias) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) bv[j] = n + j < p.N ? __ldg(p.bias + n + j) : 0.f;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) bv[j] = 0.f;
+                }
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = v[j] * p.alpha + bv[j];
                 if (p.scat.dst) {  // scatter-add into the parameter layout (split-K: the reduction does it)
                     if (m >= p.M) continue;
                     const long ro = scat_row(p.scat, m);
                     if (ro < 0) continue;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
+                    for (int j = 0; j < 32; ++j) {
                         const long co = n + j < p.N ? scat_col(p.scat, n + j) : -1L;
                         if (co >= 0) p.scat.dst[ro + co] += v[j];
                     }
                 } else if (p.natB) {
                     if (m >= p.M || n >= p.N) continue;
-                    // CTA-native layout of the recurrence (see lstm_rec.h): the 16 columns stay in
+                    // CTA-native layout of the recurrence (see lstm_rec.h): the 32 columns stay in
                     // one 128-row block of one CTA, consecutive columns are NQ floats apart
                     const long t = m / p.natB, b = m - t * p.natB;
                     const int g = (int)(b / p.natBg), nn = (int)(b - (long)g * p.natBg);
@@ -259,17 +270,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     const long cn = ((long)d * p.natG * p.natNC + (rr >> 7)) * blk + (long)(rr & 127) * p.natNQ;
                     float *base = p.C + rm + cn;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
+                    for (int j = 0; j < 32; ++j)
                         if (n + j < p.N) base[(long)j * p.natNQ] = v[j];
                 } else if ((p.ldc & 3) == 0 && ((uintptr_t)Cbase & 15) == 0) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        stg4[lane * 4 + (k ^ (lane & 3))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                    for (int k = 0; k < 8; ++k)
+                        stg4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
                     __syncwarp();
 #pragma unroll
-                    for (int it = 0; it < 4; ++it) {
-                        const int r = 8 * it + (lane >> 2), k = lane & 3;
-                        float4 o = stg4[r * 4 + (k ^ (r & 3))];
+                    for (int it = 0; it < 8; ++it) {
+                        const int r = 4 * it + (lane >> 3), k = lane & 7;
+                        float4 o = stg4[r * 8 + (k ^ (r & 7))];
                         const int mm = m0 + 32 * q + r, nn = n + 4 * k;
                         if (mm < p.M && nn < p.N) {
                             float *dst = Cbase + (size_t)mm * p.ldc + nn;
@@ -287,9 +298,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     }
                     __syncwarp();
                 } else if (m < p.M && n < p.N) {
-                    if (n + 16 <= p.N && (p.ldc & 3) == 0) {
+                    if (n + 32 <= p.N && (p.ldc & 3) == 0) {
 #pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
+                        for (int j = 0; j < 32; j += 4) {
                             float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                             float4 *dst = reinterpret_cast<float4 *>(crow + n + j);
                             if (p.beta) {
@@ -300,7 +311,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
+                        for (int j = 0; j < 32; ++j)
                             if (n + j < p.N) crow[n + j] = p.beta ? crow[n + j] + v[j] : v[j];
                     }
                 }
