@@ -1069,7 +1069,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
         }
     } else {
     // epilogue work item (unit pair pi: own units jl = 2 pi, 2 pi + 1, global j = r Hh + jl; cell ic)
-    const bool hodd = H & 1;
     const uint32_t idesc = idesc_f16(128, WV_N, 0, 0);
     const uint32_t bb_addr = smem_u32(Bb), peer_bb = mapa_shared(bb_addr, (uint32_t)(r ^ 1));
     const uint32_t peer_x = mapa_shared(smem_u32(&bars[3]), (uint32_t)(r ^ 1));
@@ -1131,75 +1130,84 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
         const float *cprev = cst + (sl ^ 1) * WV_N * Hh;
         float *ccur = cst + sl * WV_N * Hh;
         const float *zs = Zs + sl * WV_N * G5;
-        for (int item = tid; item < 16 * WV_N; item += WV_THREADS - 32) {
-            const int pi = item & 15, ic = item >> 4, jl = 2 * pi, j = r * Hh + jl;
-            const bool j0 = j < H, j1 = j + 1 < H;
-            if (jl >= Hh || ic >= n) continue;
+        // epilogue work item = (4 own units jl = 4 qi .. 4 qi + 3, global j = r Hh + jl; cell ic): 256
+        // items at Hh = 32, at most one per consumer thread (with 2-unit items, 32 threads took two)
+        for (int item = tid; item < (Hh / 4) * WV_N; item += WV_THREADS - 32) {
+            const int qi = item % (Hh / 4), ic = item / (Hh / 4), jl = 4 * qi, j = r * Hh + jl;
+            if (ic >= n) continue;
             const int i = ic;
             const WvCell ce = tab[sl * WV_N + i];
             const int up = u0 + i;
             const bool hasu = ce.flags & 2, hasv = ce.flags & 4, on = ce.flags & 1;
             const int mu = up - 1 - pu0, mv = up - pu0;
-            const float2 cu = hasu ? *reinterpret_cast<const float2 *>(cprev + mu * Hh + jl) : make_float2(0.f, 0.f);
-            const float2 cv = hasv ? *reinterpret_cast<const float2 *>(cprev + mv * Hh + jl) : make_float2(0.f, 0.f);
-            float2 g[5], h = make_float2(0.f, 0.f), cn;
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 cu4 = hasu ? *reinterpret_cast<const float4 *>(cprev + mu * Hh + jl) : z4;
+            const float4 cv4 = hasv ? *reinterpret_cast<const float4 *>(cprev + mv * Hh + jl) : z4;
+            const float cu[4] = {cu4.x, cu4.y, cu4.z, cu4.w}, cv[4] = {cv4.x, cv4.y, cv4.z, cv4.w};
+            float g[5][4], h[4], cn[4];
             if (on) {
-                float2 pre[5];
+                float pre[5][4];
 #pragma unroll
                 for (int q = 0; q < 5; ++q) {
-                    float2 s2 = *reinterpret_cast<const float2 *>(zs + i * G5 + q * Hp + j);
+                    float4 s4 = *reinterpret_cast<const float4 *>(zs + i * G5 + q * Hp + j);
                     if (hasu) {
-                        const float2 t2 = *reinterpret_cast<const float2 *>(stg + mu * R10 + q * Hh + jl);
-                        s2.x += t2.x; s2.y += t2.y;
+                        const float4 t4 = *reinterpret_cast<const float4 *>(stg + mu * R10 + q * Hh + jl);
+                        s4.x += t4.x; s4.y += t4.y; s4.z += t4.z; s4.w += t4.w;
                     }
                     if (hasv) {
-                        const float2 t2 = *reinterpret_cast<const float2 *>(stg + mv * R10 + 5 * Hh + q * Hh + jl);
-                        s2.x += t2.x; s2.y += t2.y;
+                        const float4 t4 = *reinterpret_cast<const float4 *>(stg + mv * R10 + 5 * Hh + q * Hh + jl);
+                        s4.x += t4.x; s4.y += t4.y; s4.z += t4.z; s4.w += t4.w;
                     }
-                    pre[q] = s2;
+                    pre[q][0] = s4.x; pre[q][1] = s4.y; pre[q][2] = s4.z; pre[q][3] = s4.w;
                 }
-                if (!a.stable) {  // [i, fu, fv, g, o]
 #pragma unroll
-                    for (int q = 0; q < 5; ++q)
-                        g[q] = q == 3 ? make_float2(mth(pre[q].x), mth(pre[q].y)) : make_float2(msg(pre[q].x), msg(pre[q].y));
-                    cn.x = g[1].x * cu.x + g[2].x * cv.x + g[0].x * g[3].x;
-                    cn.y = g[1].y * cu.y + g[2].y * cv.y + g[0].y * g[3].y;
-                    h = make_float2(g[4].x * mth(cn.x), g[4].y * mth(cn.y));
-                } else {          // [i, f, g, o, lambda]
+                for (int e = 0; e < 4; ++e) {
+                    if (!a.stable) {  // [i, fu, fv, g, o]
 #pragma unroll
-                    for (int q = 0; q < 5; ++q)
-                        g[q] = q == 2 ? make_float2(mth(pre[q].x), mth(pre[q].y)) : make_float2(msg(pre[q].x), msg(pre[q].y));
-                    cn.x = g[1].x * (g[4].x * cu.x + (1.f - g[4].x) * cv.x) + g[0].x * g[2].x;
-                    cn.y = g[1].y * (g[4].y * cu.y + (1.f - g[4].y) * cv.y) + g[0].y * g[2].y;
-                    h = make_float2(g[3].x * mth(cn.x), g[3].y * mth(cn.y));
+                        for (int q = 0; q < 5; ++q) g[q][e] = q == 3 ? mth(pre[q][e]) : msg(pre[q][e]);
+                        cn[e] = g[1][e] * cu[e] + g[2][e] * cv[e] + g[0][e] * g[3][e];
+                        h[e] = g[4][e] * mth(cn[e]);
+                    } else {          // [i, f, g, o, lambda]
+#pragma unroll
+                        for (int q = 0; q < 5; ++q) g[q][e] = q == 2 ? mth(pre[q][e]) : msg(pre[q][e]);
+                        cn[e] = g[1][e] * (g[4][e] * cu[e] + (1.f - g[4][e]) * cv[e]) + g[0][e] * g[2][e];
+                        h[e] = g[3][e] * mth(cn[e]);
+                    }
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < 5; ++q) g[q] = make_float2(0.f, 0.f);
-                cn = hasu ? cu : cv;
+                for (int e = 0; e < 4; ++e) {
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) g[q][e] = 0.f;
+                    h[e] = 0.f;
+                    cn[e] = hasu ? cu[e] : cv[e];  // masked: c carried (0 without predecessors), h = 0
+                }
             }
-            if (!j0) { h.x = 0.f; cn.x = 0.f; }
-            if (!j1) { h.y = 0.f; cn.y = 0.f; }
-            *reinterpret_cast<float2 *>(ccur + i * Hh + jl) = cn;
-            uint32_t hh, hl;
-            split_h2(h.x, h.y, hh, hl);
-            const uint32_t off = (uint32_t)((sl * 2) * BS + wv_bidx(i, j)) * 2;  // bytes, part hi
-            *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(Bb) + off) = hh;
-            *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(Bb) + off + BS * 2) = hl;
-            st_async_b32(peer_bb + off, hh, peer_x + 8 * sl);
-            st_async_b32(peer_bb + off + BS * 2, hl, peer_x + 8 * sl);
-            *reinterpret_cast<__half2 *>(a.h16 + ((long)k * prow + ce.slot) * Hp + j) = __floats2half2_rn(h.x, h.y);
-            if (j0) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (j + e >= H) { h[e] = 0.f; cn[e] = 0.f; }  // padding units stay 0 (B operand K padding)
+            *reinterpret_cast<float4 *>(ccur + i * Hh + jl) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+            uint32_t hh0, hl0, hh1, hl1;
+            split_h2(h[0], h[1], hh0, hl0);
+            split_h2(h[2], h[3], hh1, hl1);
+            const uint32_t off = (uint32_t)((sl * 2) * BS + wv_bidx(i, j)) * 2;  // bytes, part hi (8-byte aligned)
+            *reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(Bb) + off) = make_uint2(hh0, hh1);
+            *reinterpret_cast<uint2 *>(reinterpret_cast<uint8_t *>(Bb) + off + BS * 2) = make_uint2(hl0, hl1);
+            st_async_v2u(peer_bb + off, hh0, hh1, peer_x + 8 * sl);
+            st_async_v2u(peer_bb + off + BS * 2, hl0, hl1, peer_x + 8 * sl);
+            *reinterpret_cast<uint2 *>(a.h16 + ((long)k * prow + ce.slot) * Hp + j) = make_uint2(hh0, hh1);
+            if (j < H) {
                 float *ac = a.act + (long)ce.ck * G5 + j;
 #pragma unroll
-                for (int q = 0; q < 5; ++q) *reinterpret_cast<float2 *>(ac + q * Hp) = g[q];
-                *reinterpret_cast<float2 *>(a.c + (long)ce.ck * Hp + j) = cn;
+                for (int q = 0; q < 5; ++q) *reinterpret_cast<float4 *>(ac + q * Hp) = make_float4(g[q][0], g[q][1], g[q][2], g[q][3]);
+                *reinterpret_cast<float4 *>(a.c + (long)ce.ck * Hp + j) = make_float4(cn[0], cn[1], cn[2], cn[3]);
                 float *yp = a.y + (long)ce.cp * 4 * H + k * H + j;
-                if (!hodd && j1) {
-                    *reinterpret_cast<float2 *>(yp) = h;
+                if ((H & 3) == 0) {
+                    *reinterpret_cast<float4 *>(yp) = make_float4(h[0], h[1], h[2], h[3]);
                 } else {
-                    yp[0] = h.x;
-                    if (j1) yp[1] = h.y;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (j + e < H) yp[e] = h[e];
                 }
             }
         }
@@ -1384,105 +1392,106 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WV_THREADS, 1) md_wa
         float *dcu_c = dcu + sl * WV_N * Hh, *dcv_c = dcv + sl * WV_N * Hh;
         const float *dy_s = dys + sl * WV_N * Hp;
         const float *rv = rcv + sl * WV_N * R2;
-        for (int item = tid; item < 16 * WV_N; item += WV_THREADS - 32) {
-            const int pi = item & 15, ic = item >> 4, jl = 2 * pi, j = r * Hh + jl;
-            const bool j0 = j < H, j1 = j + 1 < H;
-            if (jl >= Hh || ic >= n) continue;
+        // work item = (4 own units jl = 4 qi .., global j = r Hh + jl; cell ic): at most one per thread
+        for (int item = tid; item < (Hh / 4) * WV_N; item += WV_THREADS - 32) {
+            const int qi = item % (Hh / 4), ic = item / (Hh / 4), jl = 4 * qi, j = r * Hh + jl;
+            if (ic >= n) continue;
             const int i = ic;
             const WvCell ce = tab[sl * WV_N + i];
             const int up = u0 + i;
             const bool su = ce.flags & 8, sv = ce.flags & 16, on = ce.flags & 1;
-            float2 da[5], ou = make_float2(0.f, 0.f), ov = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int q = 0; q < 5; ++q) da[q] = make_float2(0.f, 0.f);
             const int iu = up + 1 - su0, iv = up - su0;
-            float2 dc = make_float2(0.f, 0.f);
-            if (su) {
-                const float2 t = *reinterpret_cast<const float2 *>(dcu_p + iu * Hh + jl);
-                dc.x += t.x; dc.y += t.y;
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            auto ld4 = [](const float *q) { return *reinterpret_cast<const float4 *>(q); };
+            auto arr = [](float4 v, float (&o)[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; };
+            float dc[4], dcu4[4], dcv4[4];
+            arr(su ? ld4(dcu_p + iu * Hh + jl) : z4, dcu4);
+            arr(sv ? ld4(dcv_p + iv * Hh + jl) : z4, dcv4);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dc[e] = dcu4[e] + dcv4[e];
+            float da[5][4], ou[4], ov[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                ou[e] = ov[e] = 0.f;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) da[q][e] = 0.f;
             }
-            if (sv) {
-                const float2 t = *reinterpret_cast<const float2 *>(dcv_p + iv * Hh + jl);
-                dc.x += t.x; dc.y += t.y;
-            }
-            // P of an own row = rank 0's partial + rank 1's partial (fixed order on both ranks)
-            auto prow2 = [&](int col, int lr) -> float2 {
-                const float2 mine = *reinterpret_cast<const float2 *>(stg + col * R2 + lr);
-                const float2 peer = *reinterpret_cast<const float2 *>(rv + col * R2 + lr);
-                return r == 0 ? make_float2(mine.x + peer.x, mine.y + peer.y) : make_float2(peer.x + mine.x, peer.y + mine.y);
-            };
             if (!on) {
-                if (ce.flags & 2) ou = dc;
-                else if (ce.flags & 4) ov = dc;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (ce.flags & 2) ou[e] = dc[e];       // the carried c came from the u-,
+                    else if (ce.flags & 4) ov[e] = dc[e];  // else the v-predecessor
+                }
             } else {
-                float2 dh = *reinterpret_cast<const float2 *>(dy_s + i * Hp + j);
-                if (su) {
-                    const float2 t = prow2(iu, jl);
-                    dh.x += t.x * unscale; dh.y += t.y * unscale;
-                }
-                if (sv) {
-                    const float2 t = prow2(iv, Hh + jl);
-                    dh.x += t.x * unscale; dh.y += t.y * unscale;
-                }
-                const float *acl = ac_s + i * G5 + j;
-                const float2 c = *reinterpret_cast<const float2 *>(c_s + i * Hp + j);
-                const float2 cu = (ce.flags & 2) ? *reinterpret_cast<const float2 *>(cp_s + (up - 1 - pu0) * Hp + j)
-                                                 : make_float2(0.f, 0.f);
-                const float2 cv = (ce.flags & 4) ? *reinterpret_cast<const float2 *>(cp_s + (up - pu0) * Hp + j)
-                                                 : make_float2(0.f, 0.f);
-                float gx[5], gy[5], ox[5], oy[5];
-#pragma unroll
-                for (int q = 0; q < 5; ++q) {
-                    const float2 t = *reinterpret_cast<const float2 *>(acl + q * Hp);
-                    gx[q] = t.x; gy[q] = t.y;
-                }
-                auto cellg = [&](float dhv, float dcv_, float cc, float cuu, float cvv, const float *g, float *o,
-                                 float &ouu, float &ovv) {
-                    const float tc = mth(cc);
-                    const float dct = dcv_ + dhv * (a.stable ? g[3] : g[4]) * (1.f - tc * tc);
-                    if (!a.stable) {
-                        o[0] = dct * g[3] * g[0] * (1.f - g[0]);
-                        o[1] = dct * cuu * g[1] * (1.f - g[1]);
-                        o[2] = dct * cvv * g[2] * (1.f - g[2]);
-                        o[3] = dct * g[0] * (1.f - g[3] * g[3]);
-                        o[4] = dhv * tc * g[4] * (1.f - g[4]);
-                        ouu = dct * g[1];
-                        ovv = dct * g[2];
-                    } else {
-                        const float m = g[4] * cuu + (1.f - g[4]) * cvv;
-                        o[0] = dct * g[2] * g[0] * (1.f - g[0]);
-                        o[1] = dct * m * g[1] * (1.f - g[1]);
-                        o[2] = dct * g[0] * (1.f - g[2] * g[2]);
-                        o[3] = dhv * tc * g[3] * (1.f - g[3]);
-                        o[4] = dct * g[1] * (cuu - cvv) * g[4] * (1.f - g[4]);
-                        ouu = dct * g[1] * g[4];
-                        ovv = dct * g[1] * (1.f - g[4]);
-                    }
+                // P of an own row = rank 0's partial + rank 1's partial (fixed order on both ranks)
+                auto prow4 = [&](int col, int lr, float (&o)[4]) {
+                    const float4 mine = ld4(stg + col * R2 + lr), peer = ld4(rv + col * R2 + lr);
+                    if (r == 0) arr(make_float4(mine.x + peer.x, mine.y + peer.y, mine.z + peer.z, mine.w + peer.w), o);
+                    else arr(make_float4(peer.x + mine.x, peer.y + mine.y, peer.z + mine.z, peer.w + mine.w), o);
                 };
-                cellg(dh.x, dc.x, c.x, cu.x, cv.x, gx, ox, ou.x, ov.x);
-                cellg(dh.y, dc.y, c.y, cu.y, cv.y, gy, oy, ou.y, ov.y);
+                float dh[4], pu[4], pv[4], c[4], cu[4], cv[4];
+                arr(ld4(dy_s + i * Hp + j), dh);
+                if (su) prow4(iu, jl, pu);
+                if (sv) prow4(iv, Hh + jl, pv);
 #pragma unroll
-                for (int q = 0; q < 5; ++q) da[q] = make_float2(ox[q], oy[q]);
-                if (!j0) { ou.x = ov.x = 0.f; }
-                if (!j1) { ou.y = ov.y = 0.f; }
+                for (int e = 0; e < 4; ++e) {
+                    if (su) dh[e] += pu[e] * unscale;
+                    if (sv) dh[e] += pv[e] * unscale;
+                }
+                arr(ld4(c_s + i * Hp + j), c);
+                arr((ce.flags & 2) ? ld4(cp_s + (up - 1 - pu0) * Hp + j) : z4, cu);
+                arr((ce.flags & 4) ? ld4(cp_s + (up - pu0) * Hp + j) : z4, cv);
+                float gq[5][4];
+                const float *acl = ac_s + i * G5 + j;
+#pragma unroll
+                for (int q = 0; q < 5; ++q) arr(ld4(acl + q * Hp), gq[q]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float tc = mth(c[e]);
+                    if (!a.stable) {  // [i, fu, fv, g, o]
+                        const float gi = gq[0][e], fu = gq[1][e], fv = gq[2][e], gg = gq[3][e], go = gq[4][e];
+                        const float dct = dc[e] + dh[e] * go * (1.f - tc * tc);
+                        da[0][e] = dct * gg * gi * (1.f - gi);
+                        da[1][e] = dct * cu[e] * fu * (1.f - fu);
+                        da[2][e] = dct * cv[e] * fv * (1.f - fv);
+                        da[3][e] = dct * gi * (1.f - gg * gg);
+                        da[4][e] = dh[e] * tc * go * (1.f - go);
+                        ou[e] = dct * fu;
+                        ov[e] = dct * fv;
+                    } else {          // [i, f, g, o, lambda]
+                        const float gi = gq[0][e], f = gq[1][e], gg = gq[2][e], go = gq[3][e], lam = gq[4][e];
+                        const float dct = dc[e] + dh[e] * go * (1.f - tc * tc);
+                        const float m = lam * cu[e] + (1.f - lam) * cv[e];
+                        da[0][e] = dct * gg * gi * (1.f - gi);
+                        da[1][e] = dct * m * f * (1.f - f);
+                        da[2][e] = dct * gi * (1.f - gg * gg);
+                        da[3][e] = dh[e] * tc * go * (1.f - go);
+                        da[4][e] = dct * f * (cu[e] - cv[e]) * lam * (1.f - lam);
+                        ou[e] = dct * f * lam;
+                        ov[e] = dct * f * (1.f - lam);
+                    }
+                }
             }
 #pragma unroll
-            for (int q = 0; q < 5; ++q) {
-                if (!j0) da[q].x = 0.f;
-                if (!j1) da[q].y = 0.f;
-            }
-            *reinterpret_cast<float2 *>(dcu_c + i * Hh + jl) = ou;
-            *reinterpret_cast<float2 *>(dcv_c + i * Hh + jl) = ov;
-            uint32_t *dpp = reinterpret_cast<uint32_t *>(a.dap + (long)ce.cp * 20 * Hp + k * G5 + j);
-            uint32_t *d16 = reinterpret_cast<uint32_t *>(a.da16 + ((long)k * prow + ce.slot) * G5 + j);
+            for (int e = 0; e < 4; ++e)
+                if (j + e >= H) {  // padding units: zeros
+                    ou[e] = ov[e] = 0.f;
+#pragma unroll
+                    for (int q = 0; q < 5; ++q) da[q][e] = 0.f;
+                }
+            *reinterpret_cast<float4 *>(dcu_c + i * Hh + jl) = make_float4(ou[0], ou[1], ou[2], ou[3]);
+            *reinterpret_cast<float4 *>(dcv_c + i * Hh + jl) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+            uint2 *dpp = reinterpret_cast<uint2 *>(a.dap + (long)ce.cp * 20 * Hp + k * G5 + j);
+            uint2 *d16 = reinterpret_cast<uint2 *>(a.da16 + ((long)k * prow + ce.slot) * G5 + j);
 #pragma unroll
             for (int q = 0; q < 5; ++q) {
-                uint32_t hh, hl;
-                split_h2(da[q].x * scale, da[q].y * scale, hh, hl);
-                *reinterpret_cast<uint32_t *>(Bh + wv_bidx(i, q * Hh + jl)) = hh;
-                *reinterpret_cast<uint32_t *>(Bl + wv_bidx(i, q * Hh + jl)) = hl;
-                dpp[q * Hp / 2] = hh;  // (padding units: zeros)
-                d16[q * Hp / 2] = hh;
+                uint32_t hh0, hl0, hh1, hl1;
+                split_h2(da[q][0] * scale, da[q][1] * scale, hh0, hl0);
+                split_h2(da[q][2] * scale, da[q][3] * scale, hh1, hl1);
+                *reinterpret_cast<uint2 *>(Bh + wv_bidx(i, q * Hh + jl)) = make_uint2(hh0, hh1);
+                *reinterpret_cast<uint2 *>(Bl + wv_bidx(i, q * Hh + jl)) = make_uint2(hl0, hl1);
+                dpp[q * Hp / 4] = make_uint2(hh0, hh1);  // (padding units: zeros)
+                d16[q * Hp / 4] = make_uint2(hh0, hh1);
             }
         }
         WTRACE(ND - 1 - d, 7);
