@@ -755,6 +755,9 @@ __global__ void __launch_bounds__(PB_THREADS, 1)
                     uint32_t ph2 = phase;
                     for (int kc = 0; kc < KC; ++kc) {
                         mbar_wait(&empty[st2], ph2 ^ 1);
+#ifdef BLSTM_TRACE
+                        if (p.exp == 1) { mbar_arrive(&full[st2]); if (++st2 == PB_S) { st2 = 0; ph2 ^= 1; } continue; }
+#endif
                         mbar_arrive_expect_tx(&full[st2], PB_CHUNK);
                         tma_load_2d(ring + st2 * PB_CHUNK, &tmA, &full[st2], col0 + kc * 64, tp * B);
                         if (++st2 == PB_S) { st2 = 0; ph2 ^= 1; }
@@ -769,6 +772,10 @@ __global__ void __launch_bounds__(PB_THREADS, 1)
                     mbar_wait(&full[st2], ph2);
                     tc_fence_after();
                     const uint32_t sb = smem_u32(ring + st2 * PB_CHUNK);
+#ifdef BLSTM_TRACE
+                    if (p.exp == 2) {
+                    } else
+#endif
                     if (kc < KCT) {
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
@@ -996,10 +1003,14 @@ static int rec_step_bwd_persist(const RecStepBwd &p, cudaStream_t st) {
     }
     uint32_t *cnt = reinterpret_cast<uint32_t *>(p.dhR);  // the chain's partials scratch is unused here
     if (cudaMemsetAsync(cnt, 0, 32 * sizeof(uint32_t), st) != cudaSuccess) return -5;
+    RecStepBwd q = p;
+#ifdef BLSTM_TRACE
+    if (getenv("BLSTM_PB_EXP")) q.exp = atoi(getenv("BLSTM_PB_EXP"));  // timing isolation
+#endif
     bool ok;
     {
         ProfScope ps(PROF_REC_BWD, st);
-        ok = cudaLaunchKernelEx(&cfg, step_bwd_persist_kernel, tmA, tmR, p, p.R16, cnt, p.dbpart, rec_trace_bwd()) ==
+        ok = cudaLaunchKernelEx(&cfg, step_bwd_persist_kernel, tmA, tmR, q, p.R16, cnt, p.dbpart, rec_trace_bwd()) ==
              cudaSuccess;
     }
     if (!ok) {

@@ -57,6 +57,7 @@ struct RecStepBwd {
     const __half *R16;
     float *dbpart;
     uint32_t *started;
+    int exp;  // trace builds only (BLSTM_PB_EXP): 1 = MMAs without the dA loads, 2 = loads without MMAs
 };
 
 size_t rec_step_fwd_scratch_bytes(int B, int Hq);
