@@ -911,27 +911,25 @@ __global__ void __launch_bounds__(PB_THREADS, 1)
             if (b >= B) continue;
             float dh_in = dhc[i];
             if (need_mma && ((mprev >> i) & 1u)) dh_in = dh[i];
-            __half2 *dap = reinterpret_cast<__half2 *>(p.dA + ((long)t * B + b) * G4 + (long)d * 4 * Hq + 4 * u);
-            if (!((mbits >> i) & 1u) || u >= H) {
-                dap[0] = __floats2half2_rn(0.f, 0.f);
-                dap[1] = __floats2half2_rn(0.f, 0.f);
-                dhc[i] = dh_in;  // pass through; dc unchanged
-                continue;
-            }
+            // masked frame or padding unit: dA = 0, dh passes through, dc unchanged (R4).  Branch-free,
+            // selects on `valid` (the unselected arithmetic may see the padding's values), and one
+            // 8-byte store of the four fp16 gate gradients per cell
+            const bool valid = ((mbits >> i) & 1u) && u < H;
             const float2 g01 = __half22float2(*reinterpret_cast<const __half2 *>(&gq[i].x));
             const float2 g23 = __half22float2(*reinterpret_cast<const __half2 *>(&gq[i].y));
             const float gi = g01.x, gf = g01.y, gg = g23.x, go = g23.y;
             const float dH = dh_in + dy[i];
             const float tc = th(cc[i]);
             const float dct = dc[i] + dH * go * (1.f - tc * tc);
-            const float da_i = dct * gg * gi * (1.f - gi);
-            const float da_f = dct * cp[i] * gf * (1.f - gf);
-            const float da_g = dct * gi * (1.f - gg * gg);
-            const float da_o = dH * tc * go * (1.f - go);
-            dap[0] = __floats2half2_rn(da_i * scale, da_f * scale);
-            dap[1] = __floats2half2_rn(da_g * scale, da_o * scale);
+            const float da_i = valid ? dct * gg * gi * (1.f - gi) : 0.f;
+            const float da_f = valid ? dct * cp[i] * gf * (1.f - gf) : 0.f;
+            const float da_g = valid ? dct * gi * (1.f - gg * gg) : 0.f;
+            const float da_o = valid ? dH * tc * go * (1.f - go) : 0.f;
+            __half2 h01 = __floats2half2_rn(da_i * scale, da_f * scale), h23 = __floats2half2_rn(da_g * scale, da_o * scale);
+            *reinterpret_cast<uint2 *>(p.dA + ((long)t * B + b) * G4 + (long)d * 4 * Hq + 4 * u) =
+                make_uint2(*reinterpret_cast<uint32_t *>(&h01), *reinterpret_cast<uint32_t *>(&h23));
             db[0] += da_i; db[1] += da_f; db[2] += da_g; db[3] += da_o;
-            dc[i] = dct * gf;
+            dc[i] = valid ? dct * gf : dc[i];
             dhc[i] = dh_in;
         }
         // publish dA_t of this tile: the CTA barrier orders every thread's stores before thread 0's
