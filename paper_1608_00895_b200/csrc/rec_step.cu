@@ -748,12 +748,19 @@ __global__ void __launch_bounds__(PB_THREADS, 1)
         if (need_mma) {
             if (w == 0) {
                 if (elect_one()) {  // dA of step s-1 (frame tp), this CTA's K-split of it
-                    for (int tt = tlo; tt <= thi; ++tt) spin_until_geq(cnt_d + tt, (uint32_t)s * PB_KS);
-                    PTB(2);
-                    fence_proxy_async_global();
+                    // per source tile: a chunk's loads wait only for the tile that owns its columns,
+                    // so the first tile's chunks stream (and their MMAs run) while the last publishes
+                    int waited = tlo - 1;
                     int st2 = stage;
                     uint32_t ph2 = phase;
                     for (int kc = 0; kc < KC; ++kc) {
+                        const int tt = (ks * Hq + kc * 64) / 512;  // unit tile of gate columns col0 + kc*64
+                        if (tt > waited) {
+                            spin_until_geq(cnt_d + tt, (uint32_t)s * PB_KS);
+                            fence_proxy_async_global();
+                            waited = tt;
+                            if (tt == tlo) PTB(2);
+                        }
                         mbar_wait(&empty[st2], ph2 ^ 1);
 #ifdef BLSTM_TRACE
                         if (p.exp == 1) { mbar_arrive(&full[st2]); if (++st2 == PB_S) { st2 = 0; ph2 ^= 1; } continue; }
