@@ -104,7 +104,7 @@ struct FwdWS {
     size_t x16, w16, rt16, bq, Z, maskN, cnt, stepF, total;
 };
 struct BwdWS {
-    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cpk, dypk, gsk, cnt, stepB, cs2, total;
+    size_t x16, w16, rt16, dA, dX, dWT, dRT, dbp, P, maskN, cpk, dypk, gsk, cnt, stepB, cs2, r16, total;
 };
 struct Reserve {
     size_t gates, hist, total;
@@ -163,6 +163,8 @@ static BwdWS bwd_ws(const LayerGeo &g) {
     w.cnt = c.take(256);
     w.stepB = c.take(g.step ? rec_step_bwd_scratch_bytes(g.B, g.Hq) : 0);
     w.cs2 = c.take(g.step ? colsum_scratch_bytes(g.TB, 4 * g.Hq) : 0);
+    // step mode: R in pack_w's K-major layout, the persistent BPTT's A operand (rec_step.h R16)
+    w.r16 = c.take(g.step && rec_step_bwd_persist_ctas(g.B, g.Hq, 1) ? (size_t)4 * g.Hq * g.Hq * 2 : 0);
     w.total = c.off;
     return w;
 }
@@ -303,8 +305,13 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
         q.dhc = sb + rec_step_bwd_partial_floats(g.B, g.Hq);
         q.dcc = q.dhc + 2L * g.B * g.Hq;
         q.c0 = c0; q.dhT = dhT; q.dcT = dcT; q.dh0 = dh0; q.dc0 = dc0;
+        if (rec_step_bwd_persist_ctas(g.B, g.Hq, 1)) {  // the persistent BPTT (no launch per time step)
+            __half *r16 = (__half *)(ws + w.r16);
+            TRY(pack_w(R, nullptr, g.H, g.H, g.Hq, 1, g.Hq, 0, r16, st), "pack_w R16");
+            q.R16 = r16;
+        }
         TRY(check_mask(mask, g.TB, st), "check_mask");
-        TRY(rec_step_bwd(q, st), "rec_step_bwd");
+        if (const int rc = rec_step_bwd(q, st); rc < 0) TRY(rc, "rec_step_bwd");  // 1: the persistent BPTT ran
         if (cudaMemsetAsync(dbp, 0, (size_t)4 * g.Hq * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset");
         TRY(colsum_f16_add(dA, g.TB, 4 * g.Hq, 4L * g.Hq, 1.f / (float)(1 << DA_SHIFT), dbp, (float *)(ws + w.cs2), st),
             "db colsum");

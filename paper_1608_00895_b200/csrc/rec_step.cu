@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(PB_THREADS, 1)
     }
     {   // the first TK columns -> TMEM columns [0, TK/2) (two fp16 per 32-bit column, lane = unit row);
         // warps w and w + 4 share lane quarter q and split the columns
-        const __half *row = R16 + (size_t)(ut * 128 + m) * (2 * 4 * Hq) + col0;
+        const __half *row = R16 + (size_t)(ut * 128 + m) * (p.ndir * 4 * Hq) + col0;
         const int half = TK / 2;                  // fp16 per warp group
         const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
         for (int c0 = ch * half; c0 < ch * half + half; c0 += 32) {
@@ -824,10 +824,12 @@ __global__ void __launch_bounds__(PB_THREADS, 1)
                 const long r = (long)t * B + b;
                 mbits |= (p.mask[r] != 0 && b0 + i < B) ? (1u << i) : 0u;
                 gq[i] = *reinterpret_cast<const uint2 *>(p.gates + r * G4 + (long)d * 4 * Hq + 4 * u);
-                cc[i] = p.C[d * p.c_doff + r * p.ldc + u];
-                cp[i] = tpf_in ? p.C[d * p.c_doff + ((long)tpf * B + b) * p.ldc + u]
-                               : (p.c0 && u < H ? p.c0[((long)d * B + b) * H + u] : 0.f);
-                dy[i] = p.dy[r * p.lddy + d * p.dy_doff + u];
+                // (padding units u >= H read nothing: the caller's rows may be exactly H wide)
+                cc[i] = u < H ? p.C[d * p.c_doff + r * p.ldc + u] : 0.f;
+                cp[i] = u >= H ? 0.f
+                        : tpf_in ? p.C[d * p.c_doff + ((long)tpf * B + b) * p.ldc + u]
+                                 : (p.c0 ? p.c0[((long)d * B + b) * H + u] : 0.f);
+                dy[i] = u < H ? p.dy[r * p.lddy + d * p.dy_doff + u] : 0.f;
             }
         }
         if (need_mma) {
@@ -973,7 +975,7 @@ static int rec_step_bwd_persist(const RecStepBwd &p, cudaStream_t st) {
     const bool force = e && e[0] == '1';
     const int no = force ? -6 : 0;
     const int Hq = p.Hq;
-    if (p.B > 128 || (Hq != 512 && Hq != 1024) || p.T < 1 || p.ndir != 2 || !p.R16) return no;
+    if (p.B > 128 || (Hq != 512 && Hq != 1024) || p.T < 1 || p.ndir < 1 || p.ndir > 2 || !p.R16) return no;
     const int ctas = p.ndir * (Hq / 128) * PB_KS;
     if (ctas > num_sms()) return no;
     const size_t smem = pb_smem(Hq);
@@ -985,7 +987,7 @@ static int rec_step_bwd_persist(const RecStepBwd &p, cudaStream_t st) {
     CUtensorMap tmA, tmR;
     if (make_tmap_f16(&tmA, p.dA, (uint64_t)p.ndir * 4 * Hq, (uint64_t)p.T * p.B, (uint64_t)p.ndir * 4 * Hq, 128))
         return -5;
-    if (make_tmap_f16(&tmR, p.R16, (uint64_t)2 * 4 * Hq, (uint64_t)Hq, (uint64_t)2 * 4 * Hq, 128)) return -5;
+    if (make_tmap_f16(&tmR, p.R16, (uint64_t)p.ndir * 4 * Hq, (uint64_t)Hq, (uint64_t)p.ndir * 4 * Hq, 128)) return -5;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ctas);
     cfg.blockDim = dim3(PB_THREADS);
@@ -1029,7 +1031,7 @@ int rec_step_bwd_db_groups() { return PB_DBG; }
 int rec_step_bwd_persist_ctas(int B, int Hq, int ndir) {
     const char *e = getenv("BLSTM_STEP_PERSIST_BWD");
     if (e && e[0] == '0') return 0;
-    if (B > 128 || (Hq != 512 && Hq != 1024) || ndir != 2) return 0;
+    if (B > 128 || (Hq != 512 && Hq != 1024) || ndir < 1 || ndir > 2) return 0;
     const int ctas = ndir * (Hq / 128) * PB_KS;
     return ctas <= num_sms() ? ctas : 0;
 }

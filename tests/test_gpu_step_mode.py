@@ -97,6 +97,29 @@ def test_single_layer_h1024(direction):
     assert np.allclose(got["hT"][2], case["h0"][2], atol=1e-6)  # all-masked sequence carries h0
 
 
+@pytest.mark.parametrize("direction", [1, -1])
+def test_single_layer_persistent_bptt(direction):
+    """lstm_bwd at H = 1024 (one direction) through the persistent BPTT (rec_step.cu, ndir = 1): no
+    launch per time step, ragged lengths with an empty sequence, row pitches wider than H, against
+    the oracle."""
+    from paper_1608_00895_b200 import blstm
+    from tests.gpu_util import compare_layer, oracle_layer, run_layer
+    T = 40
+    rng = np.random.default_rng(13)
+    lengths = rng.integers(1, T + 1, size=37)
+    lengths[0], lengths[3] = T, 0
+    case = synth.random_small_case(13, T=T, B=37, D=24, H=1024, lengths=lengths)
+    s = 1.0 / np.sqrt(1024)
+    case["W"] = (case["W"] * s).astype(np.float32)
+    case["R"] = (case["R"] * s).astype(np.float32)
+    case["dy"] = (case["dy"] * case["mask"][..., None]).astype(np.float32)
+    n0 = blstm.blstm_launch_count()
+    got = run_layer(case, direction, ldx_pad=3, ldy_pad=5)
+    n = blstm.blstm_launch_count() - n0
+    assert n < T, f"{n} launches for T = {T}: a per-step chain ran"
+    compare_layer(got, oracle_layer(case, direction), f"persistent BPTT H=1024 dir={direction}")
+
+
 def test_forced_step_single_layer(force_step):
     from tests.gpu_util import compare_layer, oracle_layer, run_layer
     case = synth.random_small_case(12, T=9, B=5, D=7, H=70)
