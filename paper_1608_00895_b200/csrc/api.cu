@@ -609,6 +609,14 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     static const bool overlap_env = overlap_mode == 2 || (overlap_mode != 0 && !serialized_env());
     const bool overlap = overlap_env && side_ctas >= 8 && !g.step;
     if (overlap && gemm_prepare()) return fail(BLSTM_ERR_CUDA, "gemm_prepare");
+    {  // every layer's h0 slots (zero), once: no launch between the layers' recurrences
+        for (int l0 = 0; l0 < g.L; l0 += PACK_MAXL) {
+            HistLayers hl{};
+            const int n = g.L - l0 < PACK_MAXL ? g.L - l0 : PACK_MAXL;
+            for (int l = 0; l < n; ++l) hl.hist[l] = (__half *)(ws + w.hist[l0 + l]);
+            TRY(init_hist_layers(hl, n, g.T, g.B, Hq, st), "init_hist_layers");
+        }
+    }
     for (int l = 0; l < g.L; ++l) {
         if (drop && l > 0)  // layer l's input = layer l-1's output, dropped in place (site l)
             TRY(dropout_f16((__half *)(ws + w.y16[l - 1]), g.TB, g.H, Hq, l, g.dr, st), "dropout");
@@ -619,7 +627,6 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
             gz.a_kwrap = g.x2w ? g.Dn[l] / GEMM_BK_ELEMS : 0;
             TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gz, 0, st), "gemm Z");
             __half *hist = (__half *)(ws + w.hist[l]);
-            TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
             RecStepFwd q{};
             q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = Hq; q.ndir = 2; q.dir0 = 1;
             q.Z = Z; q.mask = mask; q.RT16 = (const __half *)(ws + w.rt16[l]);
@@ -641,7 +648,6 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         gp.pdl = overlap;
         if (!overlap) TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gp, 0, st), "gemm Z");
         __half *hist = (__half *)(ws + w.hist[l]);
-        TRY(init_hist(hist, nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
         RecParams p = base_params(LayerGeo{g.T, g.B, g.D, g.H, Hq, 0, g.TB, g.pl}, 2, 1, mask);
         p.maskN = maskN;
         p.Z = Z; p.ldz = 8L * Hq;

@@ -300,6 +300,28 @@ int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int nd
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
+// every layer's initial history slots (zero h0) in one launch: grid.y = layer
+__global__ void init_hist_layers_kernel(HistLayers hl, int T, int B, int Hq) {
+    __half *hist = hl.hist[blockIdx.y];
+    const long n = 2L * B * Hq;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+        const int d = (int)(i / ((long)B * Hq));
+        const long rem = i - (long)d * B * Hq;
+        const int slot = d == 0 ? 0 : T;
+        hist[((long)d * (T + 1) + slot) * B * Hq + rem] = __float2half_rn(0.f);
+    }
+}
+int init_hist_layers(const HistLayers &hl, int L, int T, int B, int Hq, cudaStream_t st) {
+    if (L < 1 || L > PACK_MAXL) return -3;
+    ProfScope ps_(PROF_OTHER, st);
+    const long n = 2L * B * Hq;
+    long g = (n + 255) / 256;
+    if (g > 148) g = 148;
+    init_hist_layers_kernel<<<dim3((unsigned)g, (unsigned)L), 256, 0, st>>>(hl, T, B, Hq);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 // --- softmax cross-entropy over one frame per CTA ------------------------------------------
 // logits [rows, ldl] fp32 (K valid columns); writes dlog16 [rows, Kp] = 2^shift (softmax - onehot)
 // at valid frames (0 elsewhere), rowloss (double) and rowerr (argmax != label, lowest index on ties).

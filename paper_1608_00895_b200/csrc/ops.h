@@ -31,6 +31,10 @@ int pack_bias(const float *b0, const float *b1, int H, int Hq, int ndir, float *
 // every layer of a bidirectional stack at once (pack_w, pack_rt, pack_bias of each layer, both
 // directions): three launches
 constexpr int PACK_MAXL = 16;
+struct HistLayers {
+    __half *hist[PACK_MAXL];
+};
+int init_hist_layers(const HistLayers &hl, int L, int T, int B, int Hq, cudaStream_t st);
 struct PackLayers {
     int L, H, Hq;
     const float *W[PACK_MAXL][2], *R[PACK_MAXL][2], *b[PACK_MAXL][2];
@@ -43,6 +47,7 @@ int pack_layers(const PackLayers &a, cudaStream_t st);
 int pack_wout(const float *Wo, const float *bo, int H, int Hq, int K, int Kp, __half *Wo16, float *boq,
               cudaStream_t st);
 int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int ndir, int dir0, cudaStream_t st);
+// the zero initial-state slots of every layer's bidirectional history (stack, no h0): one launch
 int ce_head(const float *logits, long ldl, int K, int Kp, const uint8_t *mask, const int32_t *labels, float scale,
             __half *dlog16, double *rowloss, int32_t *rowerr, long rows, cudaStream_t st);
 int reduce_loss(const double *rowloss, const int32_t *rowerr, long rows, double *loss, int32_t *ferr,
