@@ -730,6 +730,36 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     uint8_t *ws = (uint8_t *)workspace;
     std::vector<size_t> offs(6 * g.L + 2);
     const size_t nparam = param_layout(d, offs.data());
+    // BLSTM_NO_SIDE=1: run the off-critical-path work on s_main too (experiments)
+    static const bool no_side = getenv("BLSTM_NO_SIDE") && atoi(getenv("BLSTM_NO_SIDE")) != 0;
+    cudaStream_t side = (s_side && s_side != s_main && !no_side) ? (cudaStream_t)s_side : st;
+    const bool overlap = side != st;
+    // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
+    // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
+    // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch),
+    // [2L+3] main -> side (layer 0's dW is accumulated: the forked tail, side_layer),
+    // [2L+4] main -> side (start of the call), [2L+5] side -> main (the head's operand pack done),
+    // [2L+6] main -> side (ce_head done: the loss reduction runs on the side stream)
+    // (per thread and per device: an event may only be recorded on a stream of its own device)
+    static thread_local std::map<int, std::vector<cudaEvent_t>> evs_by_dev;
+    int cur_dev = 0;
+    if (cudaGetDevice(&cur_dev) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "cudaGetDevice");
+    std::vector<cudaEvent_t> &evs = evs_by_dev[cur_dev];
+    const int GSK_FREE = 2 * g.L + 2;
+    if (overlap && evs.size() < 2 * (size_t)g.L + 7) {
+        while (evs.size() < 2 * (size_t)g.L + 7) {
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "event");
+            evs.push_back(e);
+        }
+    }
+    if (overlap && g.K > 0) {  // the head's operand pack beside the forward (it is needed after it)
+        TRY((int)cudaEventRecord(evs[2 * g.L + 4], st), "cudaEventRecord");
+        TRY((int)cudaStreamWaitEvent(side, evs[2 * g.L + 4], 0), "cudaStreamWaitEvent");
+        TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, g.Hq, g.K, g.Kp, (__half *)(ws + w.wo16),
+                      (float *)(ws + w.boq), side), "pack_wout");
+        TRY((int)cudaEventRecord(evs[2 * g.L + 5], side), "cudaEventRecord");
+    }
     if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st, true)) return rc;
     if (g.dr.on && g.K > 0)  // the head's input (site L)
         TRY(dropout_f16((__half *)(ws + w.y16[g.L - 1]), g.TB, g.H, g.Hq, g.L, g.dr, st), "dropout");
@@ -742,10 +772,6 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     // needs them after BPTT of layer l): with a side stream they run on the SMs the recurrence
     // clusters leave free, overlapping BPTT of layer l-1.  Their inputs (dA, dbpart) and scratch
     // are double-buffered by layer parity.
-    // BLSTM_NO_SIDE=1: run the off-critical-path work on s_main too (experiments)
-    static const bool no_side = getenv("BLSTM_NO_SIDE") && atoi(getenv("BLSTM_NO_SIDE")) != 0;
-    cudaStream_t side = (s_side && s_side != s_main && !no_side) ? (cudaStream_t)s_side : st;
-    const bool overlap = side != st;
     const int rec_ctas = 2 * g.pl.G * g.pl.NC;
     const bool bucket_update = opt && !(opt->max_norm > 0.0);
     // exchange / update buckets (dp_buckets): index 0 = head (K > 0), then layers L-1 .. 0
@@ -776,23 +802,6 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     static const bool step_side_env = getenv("BLSTM_STEP_SIDE_CTAS") != nullptr;
     const int step_share = (step_bwd_ctas && !step_side_env) ? num_sms() - step_bwd_ctas : step_side;
     const int side_ctas = !overlap ? 0 : g.step ? step_share : (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8);
-    // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
-    // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
-    // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch),
-    // [2L+3] main -> side (layer 0's dW is accumulated: the forked tail, side_layer)
-    // (per thread and per device: an event may only be recorded on a stream of its own device)
-    static thread_local std::map<int, std::vector<cudaEvent_t>> evs_by_dev;
-    int cur_dev = 0;
-    if (cudaGetDevice(&cur_dev) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "cudaGetDevice");
-    std::vector<cudaEvent_t> &evs = evs_by_dev[cur_dev];
-    const int GSK_FREE = 2 * g.L + 2;
-    if (overlap && evs.size() < 2 * (size_t)g.L + 4) {
-        while (evs.size() < 2 * (size_t)g.L + 4) {
-            cudaEvent_t e;
-            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "event");
-            evs.push_back(e);
-        }
-    }
     if (step_bwd_ctas)  // R of every layer in pack_w's K-major layout: the persistent BPTT's A operand
         for (int l = 0; l < g.L; ++l)
             TRY(pack_w(theta + offs[6 * l + 1], theta + offs[6 * l + 4], g.H, g.H, Hq, 2, Hq, 0,
@@ -804,13 +813,19 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     if (g.K > 0) {
         __half *wo16 = (__half *)(ws + w.wo16), *dlog = (__half *)(ws + w.dlog16);
         float *boq = (float *)(ws + w.boq), *logits = (float *)(ws + w.Z);
-        TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, Hq, g.K, g.Kp, wo16, boq, st), "pack_wout");
+        if (overlap) TRY((int)cudaStreamWaitEvent(st, evs[2 * g.L + 5], 0), "cudaStreamWaitEvent");
+        else TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, Hq, g.K, g.Kp, wo16, boq, st), "pack_wout");
         GemmParams gl{(int)g.TB, g.K, 2 * Hq, logits, g.Kp, 1.f, 0, boq, 0, 0};
         TRY(gemm_f16({ytop, 2L * Hq, 0}, {wo16, g.Kp, 1}, gl, 0, st), "gemm logits");
         TRY(ce_head(logits, g.Kp, g.K, g.Kp, mask, labels, (float)(1 << DA_SHIFT), dlog, (double *)(ws + w.rowloss),
                     (int32_t *)(ws + w.rowerr), g.TB, st), "ce_head");
-        TRY(reduce_loss((double *)(ws + w.rowloss), (int32_t *)(ws + w.rowerr), g.TB, loss_sum, frame_errors, st),
-            "reduce_loss");
+        // the loss and frame-error sums are read only after the call: side stream
+        if (overlap) {
+            TRY((int)cudaEventRecord(evs[2 * g.L + 6], st), "cudaEventRecord");
+            TRY((int)cudaStreamWaitEvent(side, evs[2 * g.L + 6], 0), "cudaStreamWaitEvent");
+        }
+        TRY(reduce_loss((double *)(ws + w.rowloss), (int32_t *)(ws + w.rowerr), g.TB, loss_sum, frame_errors,
+                        overlap ? side : st), "reduce_loss");
         GemmParams gd{(int)g.TB, 2 * Hq, g.Kp, dY[0], 2L * Hq, a, 0, nullptr, 0, 0};
         TRY(gemm_f16({dlog, g.Kp, 0}, {wo16, g.Kp, 0}, gd, 0, st), "gemm dY_top");
         if (g.dr.on) TRY(dropout_f32(dY[0], g.TB, g.H, Hq, g.L, g.dr, st), "dropout dY_top");
