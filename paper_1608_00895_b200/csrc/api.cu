@@ -555,30 +555,44 @@ extern "C" size_t blstm_stack_workspace_bytes(const blstm_stack_desc *d) {
 
 // forward of the whole stack; Yout [L,T,B,2H] / Cout [L,2,T,B,H] optional (parity view).
 // train: apply the input dropout of g.dr (sites 0..L-1 on the layer inputs, site L on the head's)
+// side / packed (train step): the operand packs of layers 1..L-1 run on `side` beside this
+// preamble and layer 0 (recorded on `packed`; layer 1 waits for it)
 static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const StackWS &w, uint8_t *ws,
                          const float *theta, const float *x, const uint8_t *mask, float *Yout, float *Cout,
-                         cudaStream_t st, bool train = false) {
+                         cudaStream_t st, bool train = false, cudaStream_t side = nullptr, cudaEvent_t packed = nullptr) {
     const bool drop = train && g.dr.on;
     std::vector<size_t> offs(6 * g.L + 2);
     param_layout(d, offs.data());
     const int Hq = g.Hq;
     __half *x16 = (__half *)(ws + w.x16);
     TRY(cast_x_f16(x, g.D, g.D, x16, g.Dp0, g.TB, st, drop ? g.dr : Dropout{0, 0, 0, 1.f}), "cast_x");
-    if (g.L <= PACK_MAXL) {  // the operand copies of every layer: three launches
-        PackLayers pk{};
-        pk.L = g.L; pk.H = g.H; pk.Hq = Hq;
-        for (int l = 0; l < g.L; ++l) {
-            for (int dd = 0; dd < 2; ++dd) {
-                pk.W[l][dd] = theta + offs[6 * l + 3 * dd];
-                pk.R[l][dd] = theta + offs[6 * l + 3 * dd + 1];
-                pk.b[l][dd] = theta + offs[6 * l + 3 * dd + 2];
+    const bool split_pack = side && side != st && packed && g.L > 1;
+    if (g.L <= PACK_MAXL) {  // the operand copies of every layer: three launches (or layer 0 here and
+                             // layers 1..L-1 on the side stream)
+        auto pack_range = [&](int l0, int l1, cudaStream_t s) -> int {
+            PackLayers pk{};
+            pk.L = l1 - l0; pk.H = g.H; pk.Hq = Hq;
+            for (int l = l0; l < l1; ++l) {
+                const int i = l - l0;
+                for (int dd = 0; dd < 2; ++dd) {
+                    pk.W[i][dd] = theta + offs[6 * l + 3 * dd];
+                    pk.R[i][dd] = theta + offs[6 * l + 3 * dd + 1];
+                    pk.b[i][dd] = theta + offs[6 * l + 3 * dd + 2];
+                }
+                pk.Drows[i] = g.Drows[l]; pk.Dn[i] = g.Dn[l]; pk.rowmode[i] = g.rowmode[l];
+                pk.lo_rows[i] = g.x2w ? g.Dn[l] : 0;
+                pk.W16[i] = (__half *)(ws + w.w16[l]); pk.RT16[i] = (__half *)(ws + w.rt16[l]);
+                pk.bq[i] = (float *)(ws + w.bq[l]);
             }
-            pk.Drows[l] = g.Drows[l]; pk.Dn[l] = g.Dn[l]; pk.rowmode[l] = g.rowmode[l];
-            pk.lo_rows[l] = g.x2w ? g.Dn[l] : 0;
-            pk.W16[l] = (__half *)(ws + w.w16[l]); pk.RT16[l] = (__half *)(ws + w.rt16[l]);
-            pk.bq[l] = (float *)(ws + w.bq[l]);
+            return pack_layers(pk, s);
+        };
+        if (split_pack) {
+            TRY(pack_range(1, g.L, side), "pack_layers (side)");
+            TRY((int)cudaEventRecord(packed, side), "cudaEventRecord");
+            TRY(pack_range(0, 1, st), "pack_layers");
+        } else {
+            TRY(pack_range(0, g.L, st), "pack_layers");
         }
-        TRY(pack_layers(pk, st), "pack_layers");
     } else {
         for (int l = 0; l < g.L; ++l) {
             const float *Wf = theta + offs[6 * l], *Rf = theta + offs[6 * l + 1], *bf = theta + offs[6 * l + 2];
@@ -618,6 +632,8 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         }
     }
     for (int l = 0; l < g.L; ++l) {
+        if (l == 1 && split_pack && g.L <= PACK_MAXL)  // layers 1..L-1's operand copies (side stream)
+            TRY((int)cudaStreamWaitEvent(st, packed, 0), "cudaStreamWaitEvent");
         if (drop && l > 0)  // layer l's input = layer l-1's output, dropped in place (site l)
             TRY(dropout_f16((__half *)(ws + w.y16[l - 1]), g.TB, g.H, Hq, l, g.dr, st), "dropout");
         const __half *A = l == 0 ? x16 : (const __half *)(ws + w.y16[l - 1]);
@@ -739,28 +755,33 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch),
     // [2L+3] main -> side (layer 0's dW is accumulated: the forked tail, side_layer),
     // [2L+4] main -> side (start of the call), [2L+5] side -> main (the head's operand pack done),
-    // [2L+6] main -> side (ce_head done: the loss reduction runs on the side stream)
+    // [2L+6] main -> side (ce_head done: the loss reduction runs on the side stream),
+    // [2L+7] side -> main (the operand packs of layers 1..L-1 done, stack_forward)
     // (per thread and per device: an event may only be recorded on a stream of its own device)
     static thread_local std::map<int, std::vector<cudaEvent_t>> evs_by_dev;
     int cur_dev = 0;
     if (cudaGetDevice(&cur_dev) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "cudaGetDevice");
     std::vector<cudaEvent_t> &evs = evs_by_dev[cur_dev];
     const int GSK_FREE = 2 * g.L + 2;
-    if (overlap && evs.size() < 2 * (size_t)g.L + 7) {
-        while (evs.size() < 2 * (size_t)g.L + 7) {
+    if (overlap && evs.size() < 2 * (size_t)g.L + 8) {
+        while (evs.size() < 2 * (size_t)g.L + 8) {
             cudaEvent_t e;
             if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "event");
             evs.push_back(e);
         }
     }
-    if (overlap && g.K > 0) {  // the head's operand pack beside the forward (it is needed after it)
+    if (overlap) {  // the side stream starts behind everything issued so far on s_main
         TRY((int)cudaEventRecord(evs[2 * g.L + 4], st), "cudaEventRecord");
         TRY((int)cudaStreamWaitEvent(side, evs[2 * g.L + 4], 0), "cudaStreamWaitEvent");
+    }
+    if (overlap && g.K > 0) {  // the head's operand pack beside the forward (it is needed after it)
         TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, g.Hq, g.K, g.Kp, (__half *)(ws + w.wo16),
                       (float *)(ws + w.boq), side), "pack_wout");
         TRY((int)cudaEventRecord(evs[2 * g.L + 5], side), "cudaEventRecord");
     }
-    if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st, true)) return rc;
+    if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st, true, overlap ? side : nullptr,
+                               overlap ? evs[2 * g.L + 7] : nullptr))
+        return rc;
     if (g.dr.on && g.K > 0)  // the head's input (site L)
         TRY(dropout_f16((__half *)(ws + w.y16[g.L - 1]), g.TB, g.H, g.Hq, g.L, g.dr, st), "dropout");
 
