@@ -753,7 +753,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     // events: [l] main -> side (dA of layer l ready), [L] side -> main (all done), [L+1] start,
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
     // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch),
-    // [2L+3] main -> side (layer 0's dW is accumulated: the forked tail, side_layer),
+    // [2L+3] main -> side (layer 0's dW and direction-1 dR are accumulated: the forked tail, side_layer),
     // [2L+4] main -> side (start of the call), [2L+5] side -> main (the head's operand pack done),
     // [2L+6] main -> side (ce_head done: the loss reduction runs on the side stream),
     // [2L+7] side -> main (the operand packs of layers 1..L-1 done, stack_forward)
@@ -891,9 +891,10 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         float *dWT = (float *)(ws + w.dWT) + (size_t)par * 8 * Hq * w.maxDn;
         float *dRT = (float *)(ws + w.dRT) + (size_t)par * 2 * 4 * Hq * Hq;
         const float *dbp = (float *)(ws + w.dbp) + (size_t)par * 2 * g.dbs * 4 * Hq;
-        // layer 0 on s_main (after the last BPTT): fork -- dW stays on s_main, dR and the rest go to the
-        // side stream once it finished layer 1's work, each with its own half of the split-K scratch;
-        // the three small GEMMs then run side by side instead of one after another (tail -40 us at C3)
+        // layer 0 on s_main (after the last BPTT): fork -- dW and then direction 1's dR stay on s_main,
+        // direction 0's dR and the rest go to the side stream once it finished layer 1's work, each
+        // stream with its own half of the split-K scratch; the three small GEMMs then run side by side
+        // instead of one after another
         const bool fork = l == 0 && overlap && ss != side && !comm;
         cudaStream_t sw = ss, sr = fork ? side : ss;
         float *gsk_w = (float *)(ws + w.gsk), *gsk_r = fork ? gsk_w + GSK_ELEMS / 2 : gsk_w;
@@ -912,15 +913,18 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         gw.scat = scatter_gate_rows(grad + offs[6 * l], g.H, Hq, (long)(offs[6 * l + 3] - offs[6 * l]), g.rowmode[l],
                                     g.Drows[l], 4L * g.H);
         TRY(gemm_f16({dA, 8L * Hq, 1}, {X, (long)g.Dn[l], 1}, gw, wctas, sw), "gemm dW");
-        if (fork) TRY((int)cudaEventRecord(evs[2 * g.L + 3], sw), "cudaEventRecord");
         const __half *hist = (const __half *)(ws + w.hist[l]);
         for (int dd = 0; dd < 2; ++dd) {
+            // forked tail: direction 1's dR follows dW on s_main (its half of the scratch), beside
+            // direction 0's on the side stream
+            const bool on_w = fork && dd == 1;
             const __half *hprev = hist + ((long)dd * (g.T + 1) + dd) * g.B * Hq;
             GemmParams gr{4 * Hq, Hq, (int)g.TB, dRT + (size_t)dd * 4 * Hq * Hq, Hq, a, 0, nullptr, 0, 0};
-            gr.splitk_ws = gsk_r; gr.splitk_elems = gsk_n;
+            gr.splitk_ws = on_w ? gsk_w : gsk_r; gr.splitk_elems = gsk_n;
             gr.scat = scatter_gate_rows(grad + offs[6 * l + 3 * dd + 1], g.H, Hq, 0, 0, g.H, 4L * g.H);
-            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, wctas, sr), "gemm dR");
+            TRY(gemm_f16({dA + (size_t)dd * 4 * Hq, 8L * Hq, 1}, {hprev, Hq, 1}, gr, wctas, on_w ? sw : sr), "gemm dR");
         }
+        if (fork) TRY((int)cudaEventRecord(evs[2 * g.L + 3], sw), "cudaEventRecord");
         if (overlap && ss == side) TRY((int)cudaEventRecord(evs[GSK_FREE], side), "cudaEventRecord");
         for (int dd = 0; dd < 2; ++dd)
             TRY(scatter_b(grad + offs[6 * l + 3 * dd + 2], g.H, Hq, dbp, db_groups[l], dd, sr), "scatter db");
