@@ -555,45 +555,70 @@ extern "C" size_t blstm_stack_workspace_bytes(const blstm_stack_desc *d) {
 
 // forward of the whole stack; Yout [L,T,B,2H] / Cout [L,2,T,B,H] optional (parity view).
 // train: apply the input dropout of g.dr (sites 0..L-1 on the layer inputs, site L on the head's)
-// side / packed (train step): the operand packs of layers 1..L-1 run on `side` beside this
-// preamble and layer 0 (recorded on `packed`; layer 1 waits for it)
+// side / packed (train step): the operand packs of layers 1..L-1 run on `side`
+// beside layer 0 (recorded on `packed`; layer 1 waits for it); pack_head: the CE head's operands
+// are packed in the preamble launch too
 static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const StackWS &w, uint8_t *ws,
                          const float *theta, const float *x, const uint8_t *mask, float *Yout, float *Cout,
-                         cudaStream_t st, bool train = false, cudaStream_t side = nullptr, cudaEvent_t packed = nullptr) {
+                         cudaStream_t st, bool train = false, cudaStream_t side = nullptr, cudaEvent_t packed = nullptr,
+                         bool pack_head = false) {
     const bool drop = train && g.dr.on;
     std::vector<size_t> offs(6 * g.L + 2);
     param_layout(d, offs.data());
     const int Hq = g.Hq;
     __half *x16 = (__half *)(ws + w.x16);
-    TRY(cast_x_f16(x, g.D, g.D, x16, g.Dp0, g.TB, st, drop ? g.dr : Dropout{0, 0, 0, 1.f}), "cast_x");
-    const bool split_pack = side && side != st && packed && g.L > 1;
-    if (g.L <= PACK_MAXL) {  // the operand copies of every layer: three launches (or layer 0 here and
-                             // layers 1..L-1 on the side stream)
-        auto pack_range = [&](int l0, int l1, cudaStream_t s) -> int {
-            PackLayers pk{};
-            pk.L = l1 - l0; pk.H = g.H; pk.Hq = Hq;
-            for (int l = l0; l < l1; ++l) {
-                const int i = l - l0;
-                for (int dd = 0; dd < 2; ++dd) {
-                    pk.W[i][dd] = theta + offs[6 * l + 3 * dd];
-                    pk.R[i][dd] = theta + offs[6 * l + 3 * dd + 1];
-                    pk.b[i][dd] = theta + offs[6 * l + 3 * dd + 2];
-                }
-                pk.Drows[i] = g.Drows[l]; pk.Dn[i] = g.Dn[l]; pk.rowmode[i] = g.rowmode[l];
-                pk.lo_rows[i] = g.x2w ? g.Dn[l] : 0;
-                pk.W16[i] = (__half *)(ws + w.w16[l]); pk.RT16[i] = (__half *)(ws + w.rt16[l]);
-                pk.bq[i] = (float *)(ws + w.bq[l]);
+    // layers 1..L-1's packs on the side stream beside layer 0 (C3: 7.17 vs 7.21 ms per step with every
+    // pack in the preamble launch); BLSTM_PREP_SPLIT=0: all in the preamble launch
+    static const bool prep_split = !(getenv("BLSTM_PREP_SPLIT") && atoi(getenv("BLSTM_PREP_SPLIT")) == 0);
+    // (not in step mode: there the side packs would slow layer 0's HBM-bound Z GEMM, which runs alone)
+    const bool split_pack = prep_split && !g.step && side && side != st && packed && g.L > 1 && g.L <= PACK_MAXL;
+    auto pack_range = [&](int l0, int l1, PackLayers &pk) {
+        pk.L = l1 - l0; pk.H = g.H; pk.Hq = Hq;
+        for (int l = l0; l < l1; ++l) {
+            const int i = l - l0;
+            for (int dd = 0; dd < 2; ++dd) {
+                pk.W[i][dd] = theta + offs[6 * l + 3 * dd];
+                pk.R[i][dd] = theta + offs[6 * l + 3 * dd + 1];
+                pk.b[i][dd] = theta + offs[6 * l + 3 * dd + 2];
             }
-            return pack_layers(pk, s);
-        };
-        if (split_pack) {
-            TRY(pack_range(1, g.L, side), "pack_layers (side)");
-            TRY((int)cudaEventRecord(packed, side), "cudaEventRecord");
-            TRY(pack_range(0, 1, st), "pack_layers");
-        } else {
-            TRY(pack_range(0, g.L, st), "pack_layers");
+            pk.Drows[i] = g.Drows[l]; pk.Dn[i] = g.Dn[l]; pk.rowmode[i] = g.rowmode[l];
+            pk.lo_rows[i] = g.x2w ? g.Dn[l] : 0;
+            pk.W16[i] = (__half *)(ws + w.w16[l]); pk.RT16[i] = (__half *)(ws + w.rt16[l]);
+            pk.bq[i] = (float *)(ws + w.bq[l]);
         }
-    } else {
+    };
+    float *Z = (float *)(ws + w.Z);
+    uint8_t *maskN = ws + w.maskN;  // shared by every layer, forward and BPTT
+    const int num_m = (int)((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS);
+    uint32_t *zflags = (uint32_t *)(ws + w.zflags);
+    // the preamble in one launch (ops.h StackPrep): x16, the operand packs of layer 0 (every layer
+    // without the side stream), the mask, the Z flags and every layer's h0 history slots
+    {
+        StackPrep pr{};
+        pr.x = x; pr.ldx = g.D; pr.D = g.D; pr.x16 = x16; pr.Dp = g.Dp0; pr.rows = g.TB;
+        pr.dr = drop ? g.dr : Dropout{0, 0, 0, 1.f};
+        if (g.L <= PACK_MAXL) pack_range(0, split_pack ? 1 : g.L, pr.pk);
+        pr.pk.H = g.H; pr.pk.Hq = Hq;
+        if (pack_head && g.K > 0) {  // the CE head's operands (pack_wout)
+            pr.Wo = theta + offs[6 * g.L]; pr.bo = theta + offs[6 * g.L + 1]; pr.K = g.K; pr.Kp = g.Kp;
+            pr.Wo16 = (__half *)(ws + w.wo16); pr.boq = (float *)(ws + w.boq);
+        }
+        pr.mask_mode = g.step ? 2 : 1; pr.mask = mask; pr.T = g.T; pr.B = g.B;
+        pr.G = g.pl.G; pr.Bg = g.pl.Bg; pr.N = g.pl.N; pr.maskN = maskN; pr.mask_n = g.TB;
+        pr.zero = zflags; pr.zero_n = (long)zflag_words(g);
+        if (g.L <= PACK_MAXL) {
+            pr.hist_L = g.L; pr.hT = g.T; pr.hB = g.B; pr.hHq = Hq;
+            for (int l = 0; l < g.L; ++l) pr.hl.hist[l] = (__half *)(ws + w.hist[l]);
+        }
+        TRY(stack_prep(pr, st), "stack_prep");
+    }
+    if (split_pack) {  // layers 1..L-1's operand copies on the side stream (after s_main's launch)
+        PackLayers pk{};
+        pack_range(1, g.L, pk);
+        TRY(pack_layers(pk, side), "pack_layers (side)");
+        TRY((int)cudaEventRecord(packed, side), "cudaEventRecord");
+    }
+    if (g.L > PACK_MAXL) {  // (beyond the one-launch tables: per layer)
         for (int l = 0; l < g.L; ++l) {
             const float *Wf = theta + offs[6 * l], *Rf = theta + offs[6 * l + 1], *bf = theta + offs[6 * l + 2];
             const float *Wb = theta + offs[6 * l + 3], *Rb = theta + offs[6 * l + 4], *bb = theta + offs[6 * l + 5];
@@ -601,15 +626,9 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
                        g.x2w ? g.Dn[l] : 0), "pack_w");
             TRY(pack_rt(Rf, Rb, g.H, Hq, 2, (__half *)(ws + w.rt16[l]), st), "pack_rt");
             TRY(pack_bias(bf, bb, g.H, Hq, 2, (float *)(ws + w.bq[l]), st), "pack_bias");
+            TRY(init_hist((__half *)(ws + w.hist[l]), nullptr, g.T, g.B, g.H, Hq, 2, 1, st), "init_hist");
         }
     }
-    float *Z = (float *)(ws + w.Z);
-    uint8_t *maskN = ws + w.maskN;  // shared by every layer, forward and BPTT
-    if (!g.step) TRY(pack_mask(mask, g.T, g.B, g.pl.G, g.pl.Bg, g.pl.N, maskN, st), "pack_mask");
-    else TRY(check_mask(mask, g.TB, st), "check_mask");
-    const int num_m = (int)((g.TB + GEMM_BM_ROWS - 1) / GEMM_BM_ROWS);
-    uint32_t *zflags = (uint32_t *)(ws + w.zflags);
-    if (cudaMemsetAsync(zflags, 0, zflag_words(g) * 4, st) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "memset zflags");
     // Overlap: layer l's recurrence is launched first and, once all its CTAs are resident, triggers
     // the Z GEMM as a programmatic dependent launch on the SMs its clusters leave free; the
     // recurrence waits per M-tile on the GEMM's completion counters.  Only when every GEMM CTA can
@@ -623,16 +642,8 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     static const bool overlap_env = overlap_mode == 2 || (overlap_mode != 0 && !serialized_env());
     const bool overlap = overlap_env && side_ctas >= 8 && !g.step;
     if (overlap && gemm_prepare()) return fail(BLSTM_ERR_CUDA, "gemm_prepare");
-    {  // every layer's h0 slots (zero), once: no launch between the layers' recurrences
-        for (int l0 = 0; l0 < g.L; l0 += PACK_MAXL) {
-            HistLayers hl{};
-            const int n = g.L - l0 < PACK_MAXL ? g.L - l0 : PACK_MAXL;
-            for (int l = 0; l < n; ++l) hl.hist[l] = (__half *)(ws + w.hist[l0 + l]);
-            TRY(init_hist_layers(hl, n, g.T, g.B, Hq, st), "init_hist_layers");
-        }
-    }
     for (int l = 0; l < g.L; ++l) {
-        if (l == 1 && split_pack && g.L <= PACK_MAXL)  // layers 1..L-1's operand copies (side stream)
+        if (l == 1 && split_pack)  // layers 1..L-1's operand copies (side stream)
             TRY((int)cudaStreamWaitEvent(st, packed, 0), "cudaStreamWaitEvent");
         if (drop && l > 0)  // layer l's input = layer l-1's output, dropped in place (site l)
             TRY(dropout_f16((__half *)(ws + w.y16[l - 1]), g.TB, g.H, Hq, l, g.dr, st), "dropout");
@@ -754,7 +765,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
     // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch),
     // [2L+3] main -> side (layer 0's dW and direction-1 dR are accumulated: the forked tail, side_layer),
-    // [2L+4] main -> side (start of the call), [2L+5] side -> main (the head's operand pack done),
+    // [2L+4] main -> side (start of the call), [2L+5] (unused),
     // [2L+6] main -> side (ce_head done: the loss reduction runs on the side stream),
     // [2L+7] side -> main (the operand packs of layers 1..L-1 done, stack_forward)
     // (per thread and per device: an event may only be recorded on a stream of its own device)
@@ -774,13 +785,8 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         TRY((int)cudaEventRecord(evs[2 * g.L + 4], st), "cudaEventRecord");
         TRY((int)cudaStreamWaitEvent(side, evs[2 * g.L + 4], 0), "cudaStreamWaitEvent");
     }
-    if (overlap && g.K > 0) {  // the head's operand pack beside the forward (it is needed after it)
-        TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, g.Hq, g.K, g.Kp, (__half *)(ws + w.wo16),
-                      (float *)(ws + w.boq), side), "pack_wout");
-        TRY((int)cudaEventRecord(evs[2 * g.L + 5], side), "cudaEventRecord");
-    }
     if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st, true, overlap ? side : nullptr,
-                               overlap ? evs[2 * g.L + 7] : nullptr))
+                               overlap ? evs[2 * g.L + 7] : nullptr, true))
         return rc;
     if (g.dr.on && g.K > 0)  // the head's input (site L)
         TRY(dropout_f16((__half *)(ws + w.y16[g.L - 1]), g.TB, g.H, g.Hq, g.L, g.dr, st), "dropout");
@@ -834,8 +840,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     if (g.K > 0) {
         __half *wo16 = (__half *)(ws + w.wo16), *dlog = (__half *)(ws + w.dlog16);
         float *boq = (float *)(ws + w.boq), *logits = (float *)(ws + w.Z);
-        if (overlap) TRY((int)cudaStreamWaitEvent(st, evs[2 * g.L + 5], 0), "cudaStreamWaitEvent");
-        else TRY(pack_wout(theta + offs[6 * g.L], theta + offs[6 * g.L + 1], g.H, Hq, g.K, g.Kp, wo16, boq, st), "pack_wout");
+        (void)wo16; (void)boq;  // packed by the preamble launch (stack_forward)
         GemmParams gl{(int)g.TB, g.K, 2 * Hq, logits, g.Kp, 1.f, 0, boq, 0, 0};
         TRY(gemm_f16({ytop, 2L * Hq, 0}, {wo16, g.Kp, 1}, gl, 0, st), "gemm logits");
         TRY(ce_head(logits, g.Kp, g.K, g.Kp, mask, labels, (float)(1 << DA_SHIFT), dlog, (double *)(ws + w.rowloss),

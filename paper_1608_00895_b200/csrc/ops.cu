@@ -300,28 +300,6 @@ int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int nd
     return cudaGetLastError() == cudaSuccess ? 0 : -5;
 }
 
-// every layer's initial history slots (zero h0) in one launch: grid.y = layer
-__global__ void init_hist_layers_kernel(HistLayers hl, int T, int B, int Hq) {
-    __half *hist = hl.hist[blockIdx.y];
-    const long n = 2L * B * Hq;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-        const int d = (int)(i / ((long)B * Hq));
-        const long rem = i - (long)d * B * Hq;
-        const int slot = d == 0 ? 0 : T;
-        hist[((long)d * (T + 1) + slot) * B * Hq + rem] = __float2half_rn(0.f);
-    }
-}
-int init_hist_layers(const HistLayers &hl, int L, int T, int B, int Hq, cudaStream_t st) {
-    if (L < 1 || L > PACK_MAXL) return -3;
-    ProfScope ps_(PROF_OTHER, st);
-    const long n = 2L * B * Hq;
-    long g = (n + 255) / 256;
-    if (g > 148) g = 148;
-    init_hist_layers_kernel<<<dim3((unsigned)g, (unsigned)L), 256, 0, st>>>(hl, T, B, Hq);
-    note_launch();
-    return cudaGetLastError() == cudaSuccess ? 0 : -5;
-}
-
 // --- softmax cross-entropy over one frame per CTA ------------------------------------------
 // logits [rows, ldl] fp32 (K valid columns); writes dlog16 [rows, Kp] = 2^shift (softmax - onehot)
 // at valid frames (0 elsewhere), rowloss (double) and rowerr (argmax != label, lowest index on ties).
@@ -609,6 +587,158 @@ unsigned *mask_flag() {
     }
     return g_mask_flag;
 }
+// --- the stack step's preamble in one launch (ops.h StackPrep) -----------------------------
+// Each job is the body of its single-purpose kernel above with (blockIdx, gridDim) replaced by the
+// job-local block index and block count.
+__global__ void __launch_bounds__(256) stack_prep_kernel(StackPrep p) {
+    __shared__ float tile[4][32][33];  // pack_rt's transpose tile
+    int b = blockIdx.x;
+    const long t = threadIdx.x, nt = blockDim.x;
+    if (b < p.nb[0]) {  // cast_x_kernel
+        const long n = p.rows * p.Dp, stride = (long)p.nb[0] * nt;
+        for (long i = b * nt + t; i < n; i += stride) {
+            const long r = i / p.Dp;
+            const int k = (int)(i - r * p.Dp);
+            float v = k < p.D ? p.x[r * p.ldx + k] : 0.f;
+            if (p.dr.on && k < p.D) v = drop_keep(p.dr.seed, 0, (unsigned long long)r * p.D + k, p.dr.thr) ? v * p.dr.scale : 0.f;
+            p.x16[i] = __float2half_rn(v);
+        }
+        return;
+    }
+    b -= p.nb[0];
+    const PackLayers &a = p.pk;
+    if (b < p.nb[1]) {  // pack_w_all_kernel: block (bx, r, z) of grid (ceil(Hq/256), maxDn, 2L)
+        const int gx = (a.Hq + 255) / 256;
+        const int bx = b % gx, r = (b / gx) % p.maxDn, z = b / (gx * p.maxDn);
+        const int l = z >> 1, d = z & 1;
+        if (r >= a.Dn[l]) return;
+        const int H = a.H, Hq = a.Hq;
+        const int sr = src_row(r, a.Drows[l], H, Hq, a.rowmode[l]);
+        const float *W = a.W[l][d];
+        __half *out = a.W16[l] + (long)r * 2 * 4 * Hq + (long)d * 4 * Hq;
+        __half *out_lo = a.lo_rows[l] ? out + (long)a.lo_rows[l] * 2 * 4 * Hq : nullptr;
+        for (int j = bx * (int)nt + (int)t; j < Hq; j += gx * (int)nt) {
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+            if (sr >= 0 && j < H) {
+#pragma unroll
+                for (int gam = 0; gam < 4; ++gam) v[gam] = W[(long)sr * 4 * H + gam * H + j];
+            }
+            store_w4(out + 4 * j, v, out_lo ? out_lo + 4 * j : nullptr);
+        }
+        return;
+    }
+    b -= p.nb[1];
+    if (b < p.nb[2]) {  // pack_rt_all_kernel: block (bx, by, z) of grid (Hq/32, Hq/32, 2L)
+        const int H = a.H, Hq = a.Hq, g32 = Hq / 32;
+        const int bx = b % g32, by = (b / g32) % g32, z = b / (g32 * g32);
+        const int k0 = bx * 32, j0 = by * 32, l = z >> 1, d = z & 1;
+        const float *R = a.R[l][d];
+        __half *RT16 = a.RT16[l];
+        const int tx = (int)t & 31, ty = (int)t >> 5;
+        for (int kk = ty; kk < 32; kk += 8) {
+            const int k = k0 + kk, j = j0 + tx;
+#pragma unroll
+            for (int gam = 0; gam < 4; ++gam)
+                tile[gam][kk][tx] = (k < H && j < H) ? R[(long)k * 4 * H + gam * H + j] : 0.f;
+        }
+        __syncthreads();
+        for (int rr = ty; rr < 128; rr += 8) {
+            const int jj = rr >> 2, gam = rr & 3;
+            RT16[((long)d * 4 * Hq + 4 * (j0 + jj) + gam) * Hq + k0 + tx] = __float2half_rn(tile[gam][tx][jj]);
+        }
+        return;
+    }
+    b -= p.nb[2];
+    if (b < p.nb[3]) {  // pack_bias_all_kernel
+        const int Hq = a.Hq, H = a.H, per = 2 * 4 * Hq;
+        const long n = (long)a.L * per, stride = (long)p.nb[3] * nt;
+        for (long e = b * nt + t; e < n; e += stride) {
+            const int l = (int)(e / per), i = (int)(e - (long)l * per);
+            const int d = i / (4 * Hq), qq = i - d * 4 * Hq, j = qq >> 2, gam = qq & 3;
+            a.bq[l][i] = j < H ? a.b[l][d][gam * H + j] : 0.f;
+        }
+        return;
+    }
+    b -= p.nb[3];
+    if (b < p.nb[4]) {  // pack_mask_kernel (mode 1) / check_mask_kernel (mode 2)
+        bool bad = false;
+        const long stride = (long)p.nb[4] * nt;
+        if (p.mask_mode == 1) {
+            const long n = (long)p.T * p.G * p.N;
+            for (long i = b * nt + t; i < n; i += stride) {
+                const long tg = i / p.N;
+                const int c = (int)(i - tg * p.N), g = (int)(tg % p.G);
+                const long tt = tg / p.G;
+                const int bb = g * p.Bg + c;
+                const uint8_t v = (c < p.Bg && bb < p.B) ? p.mask[tt * p.B + bb] : 0;
+                bad |= v > 1;
+                p.maskN[i] = v;
+            }
+        } else {
+            const long n = p.mask_n, n16 = n / 16;
+            for (long i = b * nt + t; i < n16; i += stride) {
+                const uint4 v = __ldg((const uint4 *)p.mask + i);
+                bad |= ((v.x | v.y | v.z | v.w) & 0xFEFEFEFEu) != 0;
+            }
+            for (long i = n16 * 16 + b * nt + t; i < n; i += stride) bad |= p.mask[i] > 1;
+        }
+        if (bad && p.err) *(volatile unsigned *)p.err = 1u;
+        return;
+    }
+    b -= p.nb[4];
+    if (b < p.nb[5]) {  // zero words
+        for (long i = b * nt + t; i < p.zero_n; i += (long)p.nb[5] * nt) p.zero[i] = 0u;
+        return;
+    }
+    b -= p.nb[5];
+    if (b < p.nb[6]) {  // the zero h0 history slots (init_hist_kernel without h0): block (bx, layer)
+        const int per = p.nb[6] / p.hist_L, l = b / per, bx = b - l * per;
+        __half *hist = p.hl.hist[l];
+        const long n = 2L * p.hB * p.hHq;
+        for (long i = bx * nt + t; i < n; i += (long)per * nt) {
+            const int d = (int)(i / ((long)p.hB * p.hHq));
+            const long rem = i - (long)d * p.hB * p.hHq;
+            const int slot = d == 0 ? 0 : p.hT;
+            hist[((long)d * (p.hT + 1) + slot) * p.hB * p.hHq + rem] = __float2half_rn(0.f);
+        }
+        return;
+    }
+    b -= p.nb[6];
+    if (b < p.nb[7]) {  // pack_wout_kernel
+        const int H = p.pk.H, Hq = p.pk.Hq;
+        const long n = (long)2 * Hq * p.Kp;
+        for (long i = b * nt + t; i < n; i += (long)p.nb[7] * nt) {
+            const int r = (int)(i / p.Kp), k = (int)(i - (long)r * p.Kp);
+            const int sr = src_row(r, 2 * H, H, Hq, 1);
+            p.Wo16[i] = __float2half_rn((sr >= 0 && k < p.K) ? p.Wo[(long)sr * p.K + k] : 0.f);
+            if (r == 0) p.boq[k] = k < p.K ? p.bo[k] : 0.f;
+        }
+    }
+}
+int stack_prep(StackPrep &p, cudaStream_t st) {
+    auto cap = [](long work, long lim) { long g = (work + 255) / 256; return (int)(g < 1 ? 1 : (g > lim ? lim : g)); };
+    p.err = mask_flag();
+    p.nb[0] = p.rows * p.Dp > 0 ? cap(p.rows * p.Dp, 148 * 4) : 0;
+    p.maxDn = 0;
+    for (int l = 0; l < p.pk.L; ++l) p.maxDn = p.pk.Dn[l] > p.maxDn ? p.pk.Dn[l] : p.maxDn;
+    p.nb[1] = p.pk.L ? ((p.pk.Hq + 255) / 256) * p.maxDn * 2 * p.pk.L : 0;
+    p.nb[2] = p.pk.L ? (p.pk.Hq / 32) * (p.pk.Hq / 32) * 2 * p.pk.L : 0;
+    p.nb[3] = p.pk.L ? cap((long)p.pk.L * 8 * p.pk.Hq, 148 * 4) : 0;
+    const long mwork = p.mask_mode == 1 ? (long)p.T * p.G * p.N : p.mask_mode == 2 ? (p.mask_n + 15) / 16 : 0;
+    p.nb[4] = mwork > 0 ? cap(mwork, 148 * 4) : 0;
+    p.nb[5] = p.zero_n > 0 ? cap(p.zero_n, 148) : 0;
+    p.nb[6] = p.hist_L > 0 ? p.hist_L * cap(2L * p.hB * p.hHq, 64) : 0;
+    p.nb[7] = p.Wo16 ? cap((long)2 * p.pk.Hq * p.Kp, 148 * 2) : 0;
+    long total = 0;
+    for (int i = 0; i < 8; ++i) total += p.nb[i];
+    if (total == 0) return 0;
+    if (total > 0x7fffffffL || p.hist_L > PACK_MAXL || p.pk.L > PACK_MAXL) return -3;
+    ProfScope ps_(PROF_OTHER, st);
+    stack_prep_kernel<<<(unsigned)total, 256, 0, st>>>(p);
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 int mask_flag_take() {
     if (!g_mask_flag || *(volatile unsigned *)g_mask_flag == 0) return 0;
     *(volatile unsigned *)g_mask_flag = 0;

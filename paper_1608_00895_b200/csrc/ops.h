@@ -34,7 +34,7 @@ constexpr int PACK_MAXL = 16;
 struct HistLayers {
     __half *hist[PACK_MAXL];
 };
-int init_hist_layers(const HistLayers &hl, int L, int T, int B, int Hq, cudaStream_t st);
+
 struct PackLayers {
     int L, H, Hq;
     const float *W[PACK_MAXL][2], *R[PACK_MAXL][2], *b[PACK_MAXL][2];
@@ -44,10 +44,27 @@ struct PackLayers {
     float *bq[PACK_MAXL];
 };
 int pack_layers(const PackLayers &a, cudaStream_t st);
+// The stack step's preamble in ONE launch (it was bound by the host's launch rate: ~7 small
+// launches / memsets of a few us each): x -> x16 (cast_x_f16), the operand packs of layers
+// [0, pk.L) (pack_layers), the mask (mask_mode 1: pack_mask, 2: check_mask), zero words (the Z
+// flags), every layer's zero h0 history slots (init_hist) and the head's operands (pack_wout).
+// Jobs are independent and
+// take disjoint block ranges.
+struct StackPrep {
+    const float *x; long ldx; int D; __half *x16; int Dp; long rows; Dropout dr;
+    PackLayers pk;  // pk.L = 0: no packs
+    int mask_mode; const uint8_t *mask; int T, B, G, Bg, N; uint8_t *maskN; long mask_n;
+    uint32_t *zero; long zero_n;
+    HistLayers hl; int hist_L, hT, hB, hHq;
+    const float *Wo, *bo; int K, Kp; __half *Wo16; float *boq;  // the head's operands (pack_wout); Wo16 = nullptr: none
+    int maxDn;
+    unsigned *err;
+    int nb[8];  // blocks per job: cast, pack_w, pack_rt, pack_bias, mask, zero, hist, head (set by stack_prep)
+};
+int stack_prep(StackPrep &p, cudaStream_t st);
 int pack_wout(const float *Wo, const float *bo, int H, int Hq, int K, int Kp, __half *Wo16, float *boq,
               cudaStream_t st);
 int init_hist(__half *hist, const float *h0, int T, int B, int H, int Hq, int ndir, int dir0, cudaStream_t st);
-// the zero initial-state slots of every layer's bidirectional history (stack, no h0): one launch
 int ce_head(const float *logits, long ldl, int K, int Kp, const uint8_t *mask, const int32_t *labels, float scale,
             __half *dlog16, double *rowloss, int32_t *rowerr, long rows, cudaStream_t st);
 int reduce_loss(const double *rowloss, const int32_t *rowerr, long rows, double *loss, int32_t *ferr,

@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(PB_THREADS, 1)
     const int u = ut * 128 + m;                   // hidden unit
     const int b0 = 32 * ks + 16 * ch;             // this thread's 16 batch columns (owner role)
     // the unit tiles whose gate columns [ks Hq, (ks+1) Hq) this CTA's K-split covers
-    const int tlo = ks * Hq / 4 / 128, thi = ((ks + 1) * Hq / 4 - 1) / 128;
+    const int tlo = ks * Hq / 4 / 128;  // (through ((ks + 1) Hq / 4 - 1) / 128: two tiles at Hq = 1024)
     uint32_t *cnt_d = cnt + 16 * d;
     const float scale = (float)(1 << DA_SHIFT), alpha = 1.f / scale;
 
