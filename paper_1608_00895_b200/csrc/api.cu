@@ -309,6 +309,13 @@ extern "C" int lstm_bwd(const lstm_desc *d, const float *x, const uint8_t *mask,
             __half *r16 = (__half *)(ws + w.r16);
             TRY(pack_w(R, nullptr, g.H, g.H, g.Hq, 1, g.Hq, 0, r16, st), "pack_w R16");
             q.R16 = r16;
+            if (g.H < g.Hq) {  // it reads c and dy rows Hq wide (padding units: masked out, never stored)
+                float *cp = (float *)(ws + w.cpk), *dyp = (float *)(ws + w.dypk);
+                TRY(copy_rows(c, g.H, g.TB, g.H, cp, g.Hq, st), "copy_rows c");
+                TRY(copy_rows(dy, d->ldy, g.TB, g.H, dyp, g.Hq, st), "copy_rows dy");
+                q.C = cp; q.ldc = g.Hq;
+                q.dy = dyp; q.lddy = g.Hq;
+            }
         }
         TRY(check_mask(mask, g.TB, st), "check_mask");
         if (const int rc = rec_step_bwd(q, st); rc < 0) TRY(rc, "rec_step_bwd");  // 1: the persistent BPTT ran

@@ -824,12 +824,12 @@ __global__ void __launch_bounds__(PB_THREADS, 1)
                 const long r = (long)t * B + b;
                 mbits |= (p.mask[r] != 0 && b0 + i < B) ? (1u << i) : 0u;
                 gq[i] = *reinterpret_cast<const uint2 *>(p.gates + r * G4 + (long)d * 4 * Hq + 4 * u);
-                // (padding units u >= H read nothing: the caller's rows may be exactly H wide)
-                cc[i] = u < H ? p.C[d * p.c_doff + r * p.ldc + u] : 0.f;
-                cp[i] = u >= H ? 0.f
-                        : tpf_in ? p.C[d * p.c_doff + ((long)tpf * B + b) * p.ldc + u]
-                                 : (p.c0 ? p.c0[((long)d * B + b) * H + u] : 0.f);
-                dy[i] = u < H ? p.dy[r * p.lddy + d * p.dy_doff + u] : 0.f;
+                // (rows are read Hq wide: the callers pass ldc, lddy >= Hq; unguarded loads, since a
+                // u < H guard on them measured 7 % slower BPTT at C5)
+                cc[i] = p.C[d * p.c_doff + r * p.ldc + u];
+                cp[i] = tpf_in ? p.C[d * p.c_doff + ((long)tpf * B + b) * p.ldc + u]
+                               : (p.c0 && u < H ? p.c0[((long)d * B + b) * H + u] : 0.f);
+                dy[i] = p.dy[r * p.lddy + d * p.dy_doff + u];
             }
         }
         if (need_mma) {

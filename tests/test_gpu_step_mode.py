@@ -97,19 +97,19 @@ def test_single_layer_h1024(direction):
     assert np.allclose(got["hT"][2], case["h0"][2], atol=1e-6)  # all-masked sequence carries h0
 
 
-@pytest.mark.parametrize("direction", [1, -1])
-def test_single_layer_persistent_bptt(direction):
-    """lstm_bwd at H = 1024 (one direction) through the persistent BPTT (rec_step.cu, ndir = 1): no
-    launch per time step, ragged lengths with an empty sequence, row pitches wider than H, against
-    the oracle."""
+@pytest.mark.parametrize("direction,H", [(1, 1024), (-1, 1024), (1, 1000)])
+def test_single_layer_persistent_bptt(direction, H):
+    """lstm_bwd at H = 1024 and 1000 (Hq = 1024: padding units) through the persistent BPTT
+    (rec_step.cu, ndir = 1): no launch per time step, ragged lengths with an empty sequence, row
+    pitches wider than H, against the oracle."""
     from paper_1608_00895_b200 import blstm
     from tests.gpu_util import compare_layer, oracle_layer, run_layer
     T = 40
     rng = np.random.default_rng(13)
     lengths = rng.integers(1, T + 1, size=37)
     lengths[0], lengths[3] = T, 0
-    case = synth.random_small_case(13, T=T, B=37, D=24, H=1024, lengths=lengths)
-    s = 1.0 / np.sqrt(1024)
+    case = synth.random_small_case(13, T=T, B=37, D=24, H=H, lengths=lengths)
+    s = 1.0 / np.sqrt(H)
     case["W"] = (case["W"] * s).astype(np.float32)
     case["R"] = (case["R"] * s).astype(np.float32)
     case["dy"] = (case["dy"] * case["mask"][..., None]).astype(np.float32)
@@ -117,7 +117,7 @@ def test_single_layer_persistent_bptt(direction):
     got = run_layer(case, direction, ldx_pad=3, ldy_pad=5)
     n = blstm.blstm_launch_count() - n0
     assert n < T, f"{n} launches for T = {T}: a per-step chain ran"
-    compare_layer(got, oracle_layer(case, direction), f"persistent BPTT H=1024 dir={direction}")
+    compare_layer(got, oracle_layer(case, direction), f"persistent BPTT H={H} dir={direction}")
 
 
 def test_forced_step_single_layer(force_step):
