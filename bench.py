@@ -448,8 +448,23 @@ def main():
         tr.step()
     barrier()
 
+    # ---------------- untimed profiled pass: every launch category ----------------
+    # Each profiled launch is bracketed by two event records between the stream's kernels (~1.7 us
+    # per launch, ~1 % of a C3 step), so the timed region below brackets only the dominant
+    # category (the roofline's kernel); the others' per-step times come from this pass.
+    n_prof = max(1, min(args.steps, 5))
+    blstm.blstm_profile_select(-1)
+    blstm.blstm_profile_enable(True)
+    for _ in range(n_prof):
+        tr.step()
+    prof_all = {c: blstm.blstm_profile_read(c) for c in (blstm.PROF_REC_FWD, blstm.PROF_REC_BWD, blstm.PROF_GEMM)}
+    blstm.blstm_profile_enable(False)
+    dom = max(prof_all, key=lambda c: prof_all[c][0])
+    barrier()
+
     # ---------------- device-resident timed region ----------------
     n0 = blstm.blstm_launch_count()
+    blstm.blstm_profile_select(1 << dom)
     blstm.blstm_profile_enable(True)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -463,8 +478,11 @@ def main():
     w1 = time.time()
     t_local = e0.elapsed_time(e1) / 1e3
     launches = blstm.blstm_launch_count() - n0
-    prof = {c: blstm.blstm_profile_read(c) for c in (blstm.PROF_REC_FWD, blstm.PROF_REC_BWD, blstm.PROF_GEMM)}
+    # the dominant category live from the timed region; the others scaled from the untimed pass
+    prof = {c: (prof_all[c][0] * args.steps / n_prof, prof_all[c][1] * args.steps // n_prof) for c in prof_all}
+    prof[dom] = blstm.blstm_profile_read(dom)
     blstm.blstm_profile_enable(False)
+    blstm.blstm_profile_select(-1)
     clk = clocks.stop(w0, w1)
     t_max = max_over_ranks(t_local)
     frames = sum_over_ranks(tr.valid_frames * args.steps)
@@ -498,7 +516,6 @@ def main():
 
     peaks = measured_peaks()
     cats = {0: "lstm_rec_fwd", 1: "lstm_rec_bwd", 2: "gemm_f16 (all GEMMs)"}
-    dom = max(prof, key=lambda c: prof[c][0])
     roof = kernel_roofline(dom, prof[dom][0], prof[dom][1], cfg, tr.valid_frames, peaks, args.steps)
     kprefix = {0: "step_fwd" if cfg.H > 512 else "lstm_rec_fwd_kernel",
                1: "step_bwd" if cfg.H > 512 else "lstm_rec_bwd_kernel", 2: "gemm_f16_kernel"}[dom]
@@ -527,6 +544,7 @@ def main():
                        precision=args.precision),
         "roofline": roof,
         "kernel_ms_per_step": {cats[c]: prof[c][0] / args.steps for c in prof},
+        "kernel_ms_source": {"timed_region": cats[dom], "untimed_pass_steps": n_prof},
         "roofline_by_kernel": {cats[c]: kernel_roofline(c, prof[c][0], prof[c][1], cfg, tr.valid_frames, peaks, args.steps)
                                for c in prof},
         "step_tensor_bound_ms": t_tc,

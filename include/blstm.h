@@ -350,6 +350,11 @@ long blstm_launch_count(void);
  * launching stream (records are reset); on = 2: also the helper kernels (category 3, for
  * blstm_profile_timeline; adds two events per helper launch); on == 0: stop. */
 int blstm_profile_enable(int on);
+/* Restrict the recording to the categories whose bit is set in cat_mask (bit c: category c; the
+ * default, and -1, is every category).  Each bracket is two event records between the stream's
+ * kernels (~1.7 us per C3 launch): bench.py times only the dominant category inside its timed
+ * region and the others in an untimed pass.  Returns 0. */
+int blstm_profile_select(int cat_mask);
 /* cat: 0 forward recurrence, 1 BPTT recurrence, 2 GEMM.  Synchronizes the
  * recorded events; returns the summed device time (ms) and launch count. */
 int blstm_profile_read(int cat, double *total_ms, long *launches);

@@ -96,6 +96,7 @@ _SIGS = {
                             ctypes.c_float, _i, _vp, _vp]),
     "blstm_launch_count": (ctypes.c_long, []),
     "blstm_profile_enable": (_i, [_i]),
+    "blstm_profile_select": (_i, [_i]),
     "blstm_profile_read": (_i, [_i, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_long)]),
     "blstm_profile_timeline": (_i, [ctypes.POINTER(ctypes.c_double), _i]),
     "blstm_debug_set_trace": (_i, [_vp, _vp]),
@@ -111,6 +112,11 @@ def blstm_launch_count() -> int:
 def blstm_profile_enable(on):
     """on: False/0 off, True/1 recurrence + GEMM launches, 2 also helper kernels (timeline)."""
     _check("blstm_profile_enable", lib().blstm_profile_enable(int(on)))
+
+
+def blstm_profile_select(cat_mask: int = -1):
+    """Record only the launch categories whose bit is set (-1: all)."""
+    _check("blstm_profile_select", lib().blstm_profile_select(int(cat_mask)))
 
 
 def blstm_profile_read(cat: int):

@@ -20,6 +20,7 @@ static std::vector<ProfRec> g_recs;   // recorded launches since enable
 static std::vector<cudaEvent_t> g_pool;
 static size_t g_pool_used = 0;
 static int g_suspend = 0;
+static int g_cat_mask = -1;  // blstm_profile_select
 
 void prof_suspend(int on) { g_suspend += on ? 1 : -1; }
 
@@ -36,7 +37,7 @@ static cudaEvent_t pool_event() {
 }
 
 int prof_begin(int cat, cudaStream_t st, int a, int b, int c) {
-    if (!g_prof_on || g_suspend > 0 || (cat == PROF_OTHER && g_prof_on < 2)) return -1;
+    if (!g_prof_on || g_suspend > 0 || (cat == PROF_OTHER && g_prof_on < 2) || !((g_cat_mask >> cat) & 1)) return -1;
     ProfRec r{cat, pool_event(), pool_event(), st, a, b, c};
     if (!r.e0 || !r.e1) return -1;
     cudaEventRecord(r.e0, st);
@@ -61,6 +62,10 @@ extern "C" int blstm_profile_enable(int on) {
     return 0;
 }
 
+extern "C" int blstm_profile_select(int cat_mask) {
+    g_cat_mask = cat_mask;
+    return 0;
+}
 extern "C" int blstm_profile_read(int cat, double *total_ms, long *launches) {
     double tot = 0.0;
     long n = 0;
