@@ -390,7 +390,7 @@ struct StackGeo {
 };
 struct StackWS {
     size_t x16, Z, maskN, zflags, dA, dY0, dY1, dWT, dRT, dbp, P, cnt, wo16, boq, dlog16, dWoT, rowloss, rowerr, cs, gsk,
-        stepF, stepB, cs2, optp, total;
+        stepF, stepB, cs2, optp, tsk, total;
     size_t maxDn;
     std::vector<size_t> y16, w16, rt16, bq, gates, C, hist, r16;
 };
@@ -493,6 +493,7 @@ static StackWS stack_ws(const StackGeo &g) {
     w.rowerr = c.take((size_t)TB * 4);
     w.cs = c.take(colsum_scratch_bytes(TB, g.K ? g.K : 1));
     w.gsk = c.take((size_t)GSK_ELEMS * 4);
+    w.tsk = c.take((size_t)gemm_tail_elems() * 4);  // s_main GEMMs' tail-wave partials (gemm.h tail_ws)
     // step mode: per-step scratch and the column-sum scratch of db (dbpart from dA)
     w.stepF = c.take(g.step ? rec_step_fwd_scratch_bytes(g.B, Hq) : 0);
     w.stepB = c.take(g.step ? rec_step_bwd_scratch_bytes(g.B, Hq) : 0);
@@ -658,6 +659,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         const long lda = l == 0 ? g.Dp0 : 2L * Hq;
         if (g.step) {  // row-major Z, then one launch pair per time step (rec_step.h)
             GemmParams gz{(int)g.TB, 8 * Hq, (g.x2w ? 2 : 1) * g.Dn[l], Z, 8L * Hq, 1.f, 0, (const float *)(ws + w.bq[l]), 0, 0};
+            gz.tail_ws = (float *)(ws + w.tsk); gz.tail_elems = gemm_tail_elems();
             gz.a_kwrap = g.x2w ? g.Dn[l] / GEMM_BK_ELEMS : 0;
             TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gz, 0, st), "gemm Z");
             __half *hist = (__half *)(ws + w.hist[l]);
@@ -849,6 +851,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         float *boq = (float *)(ws + w.boq), *logits = (float *)(ws + w.Z);
         (void)wo16; (void)boq;  // packed by the preamble launch (stack_forward)
         GemmParams gl{(int)g.TB, g.K, 2 * Hq, logits, g.Kp, 1.f, 0, boq, 0, 0};
+        gl.tail_ws = (float *)(ws + w.tsk); gl.tail_elems = gemm_tail_elems();
         TRY(gemm_f16({ytop, 2L * Hq, 0}, {wo16, g.Kp, 1}, gl, 0, st), "gemm logits");
         TRY(ce_head(logits, g.Kp, g.K, g.Kp, mask, labels, (float)(1 << DA_SHIFT), dlog, (double *)(ws + w.rowloss),
                     (int32_t *)(ws + w.rowerr), g.TB, st), "ce_head");
@@ -860,6 +863,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         TRY(reduce_loss((double *)(ws + w.rowloss), (int32_t *)(ws + w.rowerr), g.TB, loss_sum, frame_errors,
                         overlap ? side : st), "reduce_loss");
         GemmParams gd{(int)g.TB, 2 * Hq, g.Kp, dY[0], 2L * Hq, a, 0, nullptr, 0, 0};
+        gd.tail_ws = (float *)(ws + w.tsk); gd.tail_elems = gemm_tail_elems();
         TRY(gemm_f16({dlog, g.Kp, 0}, {wo16, g.Kp, 0}, gd, 0, st), "gemm dY_top");
         if (g.dr.on) TRY(dropout_f32(dY[0], g.TB, g.H, Hq, g.L, g.dr, st), "dropout dY_top");
         // the head's parameter gradients are off the critical path too: side stream (side_head)
@@ -1004,6 +1008,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         const __half *w16 = (const __half *)(ws + w.w16[l]);
         if (l > 0) {  // critical path: gradient of the layer below's output
             GemmParams gx{(int)g.TB, g.Dn[l], 8 * Hq, dY[1 - cur], 2L * Hq, a, 0, nullptr, 0, 0};
+            gx.tail_ws = (float *)(ws + w.tsk); gx.tail_elems = gemm_tail_elems();
             TRY(gemm_f16({dA, 8L * Hq, 0}, {w16, 8L * Hq, 0}, gx, 0, st), "gemm dX");
             // gradient of the undropped output of layer l-1 (site l)
             if (g.dr.on) TRY(dropout_f32(dY[1 - cur], g.TB, g.H, Hq, l, g.dr, st), "dropout dX");

@@ -58,6 +58,33 @@ DEVI void tile_coords(int tile, int num_m, int num_n, const GemmParams &p, int &
     nt = w;
 }
 
+// work item -> (batch, split, tile, k-block range, tail partial slot or -1); identical in the
+// producer, MMA and epilogue loops
+struct GemmItem {
+    int bt, split, tile, kb0, kb1, tslot;
+};
+DEVI GemmItem gemm_item(const GemmParams &p, int item, int num_tiles, int per_batch, int kbs, int num_kb) {
+    GemmItem it;
+    if (p.tail_split > 1 && item >= p.full_items) {  // a K-split of a tile of the partial last wave
+        const int ti = item - p.full_items, kbt = (num_kb + p.tail_split - 1) / p.tail_split;
+        it.bt = 0;
+        it.tslot = ti;
+        it.tile = p.full_items + ti / p.tail_split;
+        it.split = ti % p.tail_split;
+        it.kb0 = it.split * kbt;
+        it.kb1 = min(num_kb, it.kb0 + kbt);
+    } else {
+        it.bt = item / per_batch;
+        const int bi = item - it.bt * per_batch;
+        it.split = bi / num_tiles;
+        it.tile = bi - it.split * num_tiles;
+        it.kb0 = it.split * kbs;
+        it.kb1 = min(num_kb, (it.split + 1) * kbs);
+        it.tslot = -1;
+    }
+    return it;
+}
+
 // scatter-mode addresses (gemm.h GemmScatter); -1: the element has no destination (padding)
 DEVI long scat_row(const GemmScatter &s, int m) {
     if (s.rowmode == 0) return m < s.nrows ? (long)m : -1L;
@@ -91,7 +118,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // split-K: work item = (split, tile); split s covers k-blocks [s*kbs, min(num_kb, (s+1)*kbs))
     const int kbs = (num_kb + p.ksplit - 1) / p.ksplit;
     const int per_batch = num_tiles * p.ksplit;
-    const int num_items = per_batch * p.nbatch;
+    const int num_items = p.tail_split > 1 ? p.full_items + (num_tiles - p.full_items) * p.tail_split
+                                           : per_batch * p.nbatch;
 
     if (warp == 0 && lane_id() == 0) {
         tma_prefetch_desc(&tmA);
@@ -130,15 +158,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
-                const int bt = item / per_batch, bi = item - bt * per_batch;
-                const int split = bi / num_tiles, tile = bi - split * num_tiles;
+                const GemmItem itm = gemm_item(p, item, num_tiles, per_batch, kbs, num_kb);
+                const int bt = itm.bt;
                 int mt, nt;
-                tile_coords<BN>(tile, num_m, num_n, p, mt, nt);
+                tile_coords<BN>(itm.tile, num_m, num_n, p, mt, nt);
                 const int m0 = mt * GEMM_BM, n0 = nt * BN;
-                const int kb1 = min(num_kb, (split + 1) * kbs);
                 const CUtensorMap *mA = bt ? &tmA2 : &tmA;
                 const int boff = bt * (int)p.b_boff;  // along B's outer dimension
-                for (int kb = split * kbs; kb < kb1; ++kb) {
+                for (int kb = itm.kb0; kb < itm.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t *sa = smem + stage * Cfg::STAGE_BYTES;
                     uint8_t *sb = sa + Cfg::A_BYTES;
@@ -171,8 +198,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
-            const int split = (item % per_batch) / num_tiles;
-            const int kb0 = split * kbs, kb1 = min(num_kb, (split + 1) * kbs);
+            const GemmItem itm = gemm_item(p, item, num_tiles, per_batch, kbs, num_kb);
+            const int kb0 = itm.kb0, kb1 = itm.kb1;
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
@@ -214,10 +241,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int lane = lane_id();
         (void)et;
         for (int item = blockIdx.x; item < num_items; item += gridDim.x) {
-            const int bt = item / per_batch, bi = item - bt * per_batch;
-            const int split = bi / num_tiles, tile = bi - split * num_tiles;
+            const GemmItem itm = gemm_item(p, item, num_tiles, per_batch, kbs, num_kb);
+            const int bt = itm.bt, split = itm.split, tslot = itm.tslot;
             int mt, nt;
-            tile_coords<BN>(tile, num_m, num_n, p, mt, nt);
+            tile_coords<BN>(itm.tile, num_m, num_n, p, mt, nt);
             const int m0 = mt * GEMM_BM, n0 = nt * BN;
             float *Cbase = p.C + bt * p.c_bstride + split * p.split_stride;
             mbar_wait(&tfull[acc], acc_phase);
@@ -246,6 +273,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     for (int j = 0; j < 32; ++j) bv[j] = 0.f;
                 }
                 tmem_ld_wait();
+                if (tslot >= 0) {  // tail split: the raw partial tile [128][BN] (the reduction finishes it)
+                    float4 *dst = reinterpret_cast<float4 *>(p.tail_ws + (size_t)tslot * GEMM_BM * BN +
+                                                             (size_t)row_in_tile * BN + c);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    continue;
+                }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = v[j] * p.alpha + bv[j];
                 if (p.scat.dst) {  // scatter-add into the parameter layout (split-K: the reduction does it)
@@ -423,6 +457,60 @@ __global__ void splitk_reduce_kernel(const float *__restrict__ part, int S, long
                                      long ldc, float alpha, int beta, const float *__restrict__ bias, GemmScatter sc);
 __global__ void splitk_scatter_kernel(const float *__restrict__ part, int S, long stride, int M, int N, float alpha,
                                       GemmScatter sc);
+// the partial last wave's tiles: sum the tail_split (<= 4) partial tiles in split order, then
+// alpha, bias and beta as the epilogue would.  TAIL_BLK blocks per tile, every load of a thread
+// issued before its first use (a latency-bound loop over 44 blocks cost more than the split saved)
+constexpr int TAIL_BLK = 8;
+template <int BN>
+__global__ void __launch_bounds__(256) gemm_tail_reduce_kernel(GemmParams p, int num_n) {
+    const int tt = blockIdx.x / TAIL_BLK, part_i = blockIdx.x - tt * TAIL_BLK;
+    const int tile = p.full_items + tt, mt = tile / num_n, nt = tile - mt * num_n;
+    const float4 *part = reinterpret_cast<const float4 *>(p.tail_ws + (size_t)tt * p.tail_split * GEMM_BM * BN);
+    constexpr int PER = GEMM_BM * BN / 4 / TAIL_BLK / 256;  // float4 per thread
+    const long sstride = (long)GEMM_BM * BN / 4;
+    float4 acc[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) acc[i] = part[(part_i * PER + i) * 256 + threadIdx.x];
+#pragma unroll
+    for (int sp = 1; sp < 4; ++sp) {
+        if (sp >= p.tail_split) break;
+        float4 b[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) b[i] = part[sp * sstride + (part_i * PER + i) * 256 + threadIdx.x];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            acc[i].x += b[i].x; acc[i].y += b[i].y; acc[i].z += b[i].z; acc[i].w += b[i].w;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e4 = (part_i * PER + i) * 256 + threadIdx.x;
+        const int r = (4 * e4) / BN, c = 4 * e4 - r * BN;
+        const int m = mt * GEMM_BM + r, n = nt * BN + c;
+        if (m >= p.M || n >= p.N) continue;
+        float v[4] = {acc[i].x, acc[i].y, acc[i].z, acc[i].w};
+        float *dst = p.C + (size_t)m * p.ldc + n;
+        if (n + 4 <= p.N && (p.ldc & 3) == 0 && ((uintptr_t)dst & 15) == 0) {
+            float4 o;
+            o.x = v[0] * p.alpha + (p.bias ? p.bias[n] : 0.f);
+            o.y = v[1] * p.alpha + (p.bias ? p.bias[n + 1] : 0.f);
+            o.z = v[2] * p.alpha + (p.bias ? p.bias[n + 2] : 0.f);
+            o.w = v[3] * p.alpha + (p.bias ? p.bias[n + 3] : 0.f);
+            if (p.beta) {
+                const float4 old = *reinterpret_cast<const float4 *>(dst);
+                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+            }
+            *reinterpret_cast<float4 *>(dst) = o;
+        } else {
+            for (int j = 0; j < 4 && n + j < p.N; ++j) {
+                const float x = v[j] * p.alpha + (p.bias ? p.bias[n + j] : 0.f);
+                dst[j] = p.beta ? dst[j] + x : x;
+            }
+        }
+    }
+}
+long gemm_tail_elems() { return 148L * GEMM_BM * 256; }
+
 int gemm_prepare() {
     cudaFuncAttributes a;
     if (cudaFuncGetAttributes(&a, splitk_reduce_kernel) != cudaSuccess) return -5;
@@ -585,9 +673,34 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
         q.ksplit = S; q.split_stride = (long)p.M * p.N;
         q.scat = GemmScatter{};  // the partials are plain; the reduction scatters
     }
+    // tail split (gemm.h tail_ws): the r tiles of a partial last wave, each split St ways over K,
+    // so the wave's idle SMs take a share (BLSTM_GEMM_TAIL=0: off)
+    static const bool tail_env = !(getenv("BLSTM_GEMM_TAIL") && getenv("BLSTM_GEMM_TAIL")[0] == '0');
+    q.tail_split = 0;
+    if (tail_env && S == 1 && p.tail_ws && !p.natB && !p.flags && !p.a2 && !p.scat.dst && !p.pdl && !p.pdl_chain &&
+        !p.arb && p.ksplit <= 1 && tiles > max_ctas) {
+        const int r = tiles % max_ctas;
+        if (r > 0 && 2 * r <= max_ctas) {
+            int St = max_ctas / r < 4 ? max_ctas / r : 4;
+            while (St > 1 && num_kb / St < 8) --St;  // >= 8 k-blocks per split
+            if (St > 1 && (long)r * St * GEMM_BM * BN <= p.tail_elems) {
+                q.tail_split = St;
+                q.full_items = tiles - r;
+            }
+        }
+    }
     cudaError_t e = BN == 256 ? launch_gemm<256>(ta, tb, ta2, q, max_ctas, st)
                               : launch_gemm<128>(ta, tb, ta2, q, max_ctas, st);
     if (e != cudaSuccess) return -5;
+    if (q.tail_split > 1) {
+        const int num_n = (p.N + BN - 1) / BN;
+        ProfScope ps(PROF_GEMM, st, p.M, p.N, p.K);
+        const unsigned nb = (unsigned)(tiles - q.full_items) * TAIL_BLK;
+        if (BN == 256) gemm_tail_reduce_kernel<256><<<nb, 256, 0, st>>>(q, num_n);
+        else gemm_tail_reduce_kernel<128><<<nb, 256, 0, st>>>(q, num_n);
+        note_launch();
+        if (cudaGetLastError() != cudaSuccess) return -5;
+    }
     if (S > 1) {
         const long n = (long)p.M * p.N;
         long g = (n + 255) / 256;

@@ -75,7 +75,16 @@ struct GemmParams {
     // with B's segments stacked along K -- BLSTM_PREC_FP16X2W's Z = X W_hi + X W_lo (R9)
     int a_kwrap = 0;
     GemmScatter scat;  // scat.dst != nullptr: scatter-add output (C, ldc, beta and bias unused; no flags / partials)
+    // != nullptr: a plain GEMM (no split-K, flags, batch, scatter or PDL) whose tiles leave a partial
+    // last wave splits that wave's tiles over K, tail_split ways, into fp32 partial tiles here
+    // (tail_elems floats); a fixed-order reduction then writes them (deterministic).  The idle SMs
+    // of the last wave share its work (e.g. C3's dX: 636 tiles = 4.3 waves on 148 SMs)
+    float *tail_ws = nullptr;
+    long tail_elems = 0;
+    int full_items = 0, tail_split = 0;  // set by gemm_f16
 };
+// floats of a tail_ws that lets every shape use the tail split (one partial tile per SM)
+long gemm_tail_elems();
 
 constexpr int GEMM_BM_ROWS = 128;           // M tile
 constexpr int GEMM_BK_ELEMS = 64;           // K block (a_kwrap unit)
