@@ -683,7 +683,9 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
         if (r > 0 && 2 * r <= max_ctas) {
             int St = max_ctas / r < 4 ? max_ctas / r : 4;
             while (St > 1 && num_kb / St < 8) --St;  // >= 8 k-blocks per split
-            if (St > 1 && (long)r * St * GEMM_BM * BN <= p.tail_elems) {
+            // worth it when the saved (1 - 1/St) of a tile's time beats the reduction launch (~10 us):
+            // a tile of K >= 3072 (C3 dX, ~27 us) yes; the head's K = 1024 / 1536 GEMMs measured no
+            if (St > 1 && num_kb >= 48 && (long)r * St * GEMM_BM * BN <= p.tail_elems) {
                 q.tail_split = St;
                 q.full_items = tiles - r;
             }
