@@ -569,7 +569,7 @@ extern "C" size_t blstm_stack_workspace_bytes(const blstm_stack_desc *d) {
 static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const StackWS &w, uint8_t *ws,
                          const float *theta, const float *x, const uint8_t *mask, float *Yout, float *Cout,
                          cudaStream_t st, bool train = false, cudaStream_t side = nullptr, cudaEvent_t packed = nullptr,
-                         bool pack_head = false) {
+                         bool pack_head = false, cudaEvent_t z0done = nullptr, bool *r16_on_side = nullptr) {
     const bool drop = train && g.dr.on;
     std::vector<size_t> offs(6 * g.L + 2);
     param_layout(d, offs.data());
@@ -578,8 +578,14 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     // layers 1..L-1's packs on the side stream beside layer 0 (C3: 7.17 vs 7.21 ms per step with every
     // pack in the preamble launch); BLSTM_PREP_SPLIT=0: all in the preamble launch
     static const bool prep_split = !(getenv("BLSTM_PREP_SPLIT") && atoi(getenv("BLSTM_PREP_SPLIT")) == 0);
-    // (not in step mode: there the side packs would slow layer 0's HBM-bound Z GEMM, which runs alone)
+    // (step mode: deferred until layer 0's Z GEMM is done -- beside it they slowed that HBM-bound
+    // GEMM -- and with the persistent BPTT's R16 packs of every layer, which then leave the critical
+    // path too: *r16_on_side)
     const bool split_pack = prep_split && !g.step && side && side != st && packed && g.L > 1 && g.L <= PACK_MAXL;
+    const bool step_defer = prep_split && g.step && train && side && side != st && packed && z0done &&
+                            g.L <= PACK_MAXL && (g.L > 1 || r16_on_side);
+    const bool defer_r16 = step_defer && r16_on_side && rec_step_bwd_persist_ctas(g.B, g.Hq, 2) > 0;
+    if (r16_on_side) *r16_on_side = defer_r16;
     auto pack_range = [&](int l0, int l1, PackLayers &pk) {
         pk.L = l1 - l0; pk.H = g.H; pk.Hq = Hq;
         for (int l = l0; l < l1; ++l) {
@@ -605,7 +611,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
         StackPrep pr{};
         pr.x = x; pr.ldx = g.D; pr.D = g.D; pr.x16 = x16; pr.Dp = g.Dp0; pr.rows = g.TB;
         pr.dr = drop ? g.dr : Dropout{0, 0, 0, 1.f};
-        if (g.L <= PACK_MAXL) pack_range(0, split_pack ? 1 : g.L, pr.pk);
+        if (g.L <= PACK_MAXL) pack_range(0, (split_pack || step_defer) ? 1 : g.L, pr.pk);
         pr.pk.H = g.H; pr.pk.Hq = Hq;
         if (pack_head && g.K > 0) {  // the CE head's operands (pack_wout)
             pr.Wo = theta + offs[6 * g.L]; pr.bo = theta + offs[6 * g.L + 1]; pr.K = g.K; pr.Kp = g.Kp;
@@ -651,7 +657,7 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
     const bool overlap = overlap_env && side_ctas >= 8 && !g.step;
     if (overlap && gemm_prepare()) return fail(BLSTM_ERR_CUDA, "gemm_prepare");
     for (int l = 0; l < g.L; ++l) {
-        if (l == 1 && split_pack)  // layers 1..L-1's operand copies (side stream)
+        if (l == 1 && (split_pack || step_defer))  // layers 1..L-1's operand copies (side stream)
             TRY((int)cudaStreamWaitEvent(st, packed, 0), "cudaStreamWaitEvent");
         if (drop && l > 0)  // layer l's input = layer l-1's output, dropped in place (site l)
             TRY(dropout_f16((__half *)(ws + w.y16[l - 1]), g.TB, g.H, Hq, l, g.dr, st), "dropout");
@@ -662,6 +668,20 @@ static int stack_forward(const blstm_stack_desc *d, const StackGeo &g, const Sta
             gz.tail_ws = (float *)(ws + w.tsk); gz.tail_elems = gemm_tail_elems();
             gz.a_kwrap = g.x2w ? g.Dn[l] / GEMM_BK_ELEMS : 0;
             TRY(gemm_f16({A, lda, 0}, {ws + w.w16[l], 8L * Hq, 1}, gz, 0, st), "gemm Z");
+            if (l == 0 && step_defer) {  // the deferred operand packs, beside layer 0's recurrence
+                TRY((int)cudaEventRecord(z0done, st), "cudaEventRecord");
+                TRY((int)cudaStreamWaitEvent(side, z0done, 0), "cudaStreamWaitEvent");
+                if (g.L > 1) {
+                    PackLayers pk{};
+                    pack_range(1, g.L, pk);
+                    TRY(pack_layers(pk, side), "pack_layers (side)");
+                }
+                if (defer_r16)  // R of every layer in pack_w's K-major layout (the persistent BPTT's A)
+                    for (int l2 = 0; l2 < g.L; ++l2)
+                        TRY(pack_w(theta + offs[6 * l2 + 1], theta + offs[6 * l2 + 4], g.H, g.H, Hq, 2, Hq, 0,
+                                   (__half *)(ws + w.r16[l2]), side), "pack_w R16");
+                TRY((int)cudaEventRecord(packed, side), "cudaEventRecord");
+            }
             __half *hist = (__half *)(ws + w.hist[l]);
             RecStepFwd q{};
             q.T = g.T; q.B = g.B; q.H = g.H; q.Hq = Hq; q.ndir = 2; q.dir0 = 1;
@@ -774,7 +794,7 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     // [L+2+l] side -> main (layer l's gradient work done: its parity buffers may be reused),
     // [2L+2] side -> main (the side stream's latest GEMMs are done with the split-K scratch),
     // [2L+3] main -> side (layer 0's dW and direction-1 dR are accumulated: the forked tail, side_layer),
-    // [2L+4] main -> side (start of the call), [2L+5] (unused),
+    // [2L+4] main -> side (start of the call), [2L+5] main -> side (step mode: layer 0's Z GEMM done),
     // [2L+6] main -> side (ce_head done: the loss reduction runs on the side stream),
     // [2L+7] side -> main (the operand packs of layers 1..L-1 done, stack_forward)
     // (per thread and per device: an event may only be recorded on a stream of its own device)
@@ -794,8 +814,10 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
         TRY((int)cudaEventRecord(evs[2 * g.L + 4], st), "cudaEventRecord");
         TRY((int)cudaStreamWaitEvent(side, evs[2 * g.L + 4], 0), "cudaStreamWaitEvent");
     }
+    bool r16_on_side = false;
     if (int rc = stack_forward(d, g, w, ws, theta, x, mask, nullptr, nullptr, st, true, overlap ? side : nullptr,
-                               overlap ? evs[2 * g.L + 7] : nullptr, true))
+                               overlap ? evs[2 * g.L + 7] : nullptr, true, overlap ? evs[2 * g.L + 5] : nullptr,
+                               &r16_on_side))
         return rc;
     if (g.dr.on && g.K > 0)  // the head's input (site L)
         TRY(dropout_f16((__half *)(ws + w.y16[g.L - 1]), g.TB, g.H, g.Hq, g.L, g.dr, st), "dropout");
@@ -838,7 +860,9 @@ static int stack_step_impl(const blstm_stack_desc *d, const float *theta, float 
     static const bool step_side_env = getenv("BLSTM_STEP_SIDE_CTAS") != nullptr;
     const int step_share = (step_bwd_ctas && !step_side_env) ? num_sms() - step_bwd_ctas : step_side;
     const int side_ctas = !overlap ? 0 : g.step ? step_share : (num_sms() - rec_ctas > 8 ? num_sms() - rec_ctas : 8);
-    if (step_bwd_ctas)  // R of every layer in pack_w's K-major layout: the persistent BPTT's A operand
+    if (step_bwd_ctas && r16_on_side)  // packed on the side stream during the forward (stack_forward)
+        TRY((int)cudaStreamWaitEvent(st, evs[2 * g.L + 7], 0), "cudaStreamWaitEvent");
+    else if (step_bwd_ctas)  // R of every layer in pack_w's K-major layout: the persistent BPTT's A operand
         for (int l = 0; l < g.L; ++l)
             TRY(pack_w(theta + offs[6 * l + 1], theta + offs[6 * l + 4], g.H, g.H, Hq, 2, Hq, 0,
                        (__half *)(ws + w.r16[l]), st), "pack_w R16");
