@@ -375,6 +375,231 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2) for plain GEMMs with many tiles: a 2-CTA cluster computes a
+// 256 x 256 tile; CTA r loads its 128 rows of A and its 128 columns of B (B split by N) per
+// k-block, both completing on the even CTA's full barrier (TMA .cta_group::2); the even CTA
+// issues M = 256, N = 256 MMAs that read both CTAs' shared memory and write each CTA's 128 rows
+// of D into its own TMEM; commits are multicast to both CTAs.  Per SM a k-block is 32 KB of
+// operands instead of 48 KB, and the pair MMA keeps the tensor pipe busier (ncu: the single-CTA
+// kernel's TC pipe at 80 % on C5's Z GEMM).  Plain row-major output with alpha / beta / bias only.
+// ---------------------------------------------------------------------------
+constexpr int GP_STAGES = 6;
+constexpr int GP_A_BYTES = GEMM_BM * GEMM_BK * 2;           // 16 KB: this CTA's 128 rows of A
+constexpr int GP_B_BYTES = 128 * GEMM_BK * 2;               // 16 KB: this CTA's 128 columns of B
+constexpr int GP_STAGE_BYTES = GP_A_BYTES + GP_B_BYTES;
+constexpr int GP_SMEM_BYTES = GP_STAGES * GP_STAGE_BYTES + 1024 + 256 + GEMM_EPI_WARPS * 4096;
+
+DEVI void tma_load_2d_pair(void *dst, const CUtensorMap *m, uint32_t bar_cluster, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+DEVI void mma_f16_ss2_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+DEVI void mbar_remote_arrive_release(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_f16_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(smem + GP_STAGES * GP_STAGE_BYTES);
+    uint64_t *empty = full + GP_STAGES;
+    uint64_t *tfull = empty + GP_STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+    constexpr int BN = 256;
+
+    const int warp = warp_id();
+    const int r = (int)cluster_ctarank();
+    const int num_mp = (p.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM);
+    const int num_n = (p.N + BN - 1) / BN;
+    const int num_items = num_mp * num_n;
+    const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+    const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (warp == 0 && lane_id() == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < GP_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * GEMM_EPI_WARPS);  // (the even CTA's: both CTAs' epilogue warps)
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        tmem_alloc2(tmem_slot, 2 * BN);
+        tmem_relinquish2();
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // every barrier of the pair initialised before any remote arrive / complete_tx
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (both CTAs) ----------------
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int item = cl; item < num_items; item += ncl) {
+                const int mp = item / num_n, nt = item - mp * num_n;
+                const int m0 = mp * 2 * GEMM_BM + r * GEMM_BM, n0 = nt * BN + r * 128;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t *sa = smem + stage * GP_STAGE_BYTES;
+                    uint8_t *sb = sa + GP_A_BYTES;
+                    const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);  // the even CTA's barrier
+                    if (r == 0) mbar_arrive_expect_tx(&full[stage], 2 * GP_STAGE_BYTES);
+                    const int k0 = kb * GEMM_BK;
+                    if (!p.a_mn) {
+                        tma_load_2d_pair(sa, &tmA, fb, k0, m0);
+                    } else {
+                        tma_load_2d_pair(sa, &tmA, fb, m0, k0);
+                        tma_load_2d_pair(sa + 8192, &tmA, fb, m0 + 64, k0);
+                    }
+                    if (!p.b_mn) {
+                        tma_load_2d_pair(sb, &tmB, fb, k0, n0);
+                    } else {
+                        tma_load_2d_pair(sb, &tmB, fb, n0, k0);
+                        tma_load_2d_pair(sb + 8192, &tmB, fb, n0 + 64, k0);
+                    }
+                    if (++stage == GP_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (the even CTA) ----------------
+        if (r == 0) {
+            const uint32_t idesc = idesc_f16(2 * GEMM_BM, BN, p.a_mn, p.b_mn);
+            const int a_mn = warp_uniform(p.a_mn), b_mn = warp_uniform(p.b_mn);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int item = cl; item < num_items; item += ncl) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * GP_STAGE_BYTES);
+                    const uint32_t sb = sa + GP_A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
+                        const uint64_t ad = a_mn ? sdesc_sw128(sa + kk * 2048, 8192, 1024) : sdesc_sw128(sa + kk * 32, 16, 1024);
+                        const uint64_t bd = b_mn ? sdesc_sw128(sb + kk * 2048, 8192, 1024) : sdesc_sw128(sb + kk * 32, 16, 1024);
+                        mma_f16_ss2_w(d_tmem, ad, bd, idesc, (kb != 0) | (kk != 0));
+                    }
+                    mma_commit2_w(&empty[stage], (uint16_t)3);
+                    if (kb == num_kb - 1) mma_commit2_w(&tfull[acc], (uint16_t)3);
+                    __syncwarp();
+                    if (++stage == GP_STAGES) { stage = 0; phase ^= 1; }
+                }
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ---------------- epilogue (both CTAs, warps 2..9): this CTA's 128 rows x 256 columns ----------------
+        const int q = warp & 3;
+        const int row_in_tile = q * 32 + lane_id();
+        const int chalf = (warp - 2) / 4;
+        float4 *stg4 = reinterpret_cast<float4 *>(tmem_slot + 4) + (warp - 2) * 256;
+        const int lane = lane_id();
+        const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int item = cl; item < num_items; item += ncl) {
+            const int mp = item / num_n, nt = item - mp * num_n;
+            const int m0 = mp * 2 * GEMM_BM + r * GEMM_BM, n0 = nt * BN;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int m = m0 + row_in_tile;
+            float *crow = p.C + (size_t)m * p.ldc;
+#pragma unroll 1
+            for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
+                float v[32];
+                const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c;
+                tmem_ld16(ta, *reinterpret_cast<float(*)[16]>(&v[0]));
+                tmem_ld16(ta + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
+                const int n = n0 + c;
+                float bv[32];
+                if (p.bias && n + 32 <= p.N && ((uintptr_t)(p.bias + n) & 15) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 b4 = __ldg(reinterpret_cast<const float4 *>(p.bias + n + j));
+                        bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+                    }
+                } else if (p.bias) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) bv[j] = n + j < p.N ? __ldg(p.bias + n + j) : 0.f;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) bv[j] = 0.f;
+                }
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = v[j] * p.alpha + bv[j];
+                if ((p.ldc & 3) == 0 && ((uintptr_t)p.C & 15) == 0) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        stg4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int it = 0; it < 8; ++it) {
+                        const int rr = 4 * it + (lane >> 3), k = lane & 7;
+                        float4 o = stg4[rr * 8 + (k ^ (rr & 7))];
+                        const int mm = m0 + 32 * q + rr, nn = n + 4 * k;
+                        if (mm < p.M && nn < p.N) {
+                            float *dst = p.C + (size_t)mm * p.ldc + nn;
+                            if (nn + 4 <= p.N) {
+                                if (p.beta) {
+                                    const float4 old = *reinterpret_cast<const float4 *>(dst);
+                                    o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+                                }
+                                *reinterpret_cast<float4 *>(dst) = o;
+                            } else {
+                                const float ov[4] = {o.x, o.y, o.z, o.w};
+                                for (int e = 0; e < p.N - nn; ++e) dst[e] = p.beta ? dst[e] + ov[e] : ov[e];
+                            }
+                        }
+                    }
+                    __syncwarp();
+                } else if (m < p.M && n < p.N) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (n + j < p.N) crow[n + j] = p.beta ? crow[n + j] + v[j] : v[j];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_remote_arrive_release(tempty0 + (uint32_t)acc * 8u);  // the even CTA's tempty[acc]
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // no remote arrive / complete_tx / MMA into this CTA is outstanding
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc2(tmem_base, 2 * BN);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -515,6 +740,7 @@ int gemm_prepare() {
     cudaFuncAttributes a;
     if (cudaFuncGetAttributes(&a, splitk_reduce_kernel) != cudaSuccess) return -5;
     if (cudaFuncGetAttributes(&a, splitk_scatter_kernel) != cudaSuccess) return -5;
+    if (cudaFuncGetAttributes(&a, gemm_f16_pair_kernel) != cudaSuccess) return -5;
     return (gemm_setup<128>() == cudaSuccess && gemm_setup<256>() == cudaSuccess) ? 0 : -5;
 }
 
@@ -672,6 +898,33 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
         q.C = p.splitk_ws; q.ldc = p.N; q.alpha = 1.f; q.beta = 0; q.bias = nullptr;
         q.ksplit = S; q.split_stride = (long)p.M * p.N;
         q.scat = GemmScatter{};  // the partials are plain; the reduction scatters
+    }
+    // CTA pairs (gemm_f16_pair_kernel): plain GEMMs with at least a wave of 256 x 256 tiles;
+    // BLSTM_GEMM_PAIR=0: off
+    static const bool pair_env = !(getenv("BLSTM_GEMM_PAIR") && getenv("BLSTM_GEMM_PAIR")[0] == '0');
+    if (pair_env && S == 1 && BN == 256 && !p.natB && !p.flags && !p.a2 && !p.scat.dst && !p.pdl && !p.pdl_chain &&
+        !p.arb && p.partials == 0 && p.a_kwrap == 0 && p.nbatch == 1 && max_ctas >= 2) {
+        const int pair_tiles = ((p.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((p.N + 255) / 256);
+        const int clusters = max_ctas / 2;
+        if (pair_tiles >= clusters) {
+            CUtensorMap tbp;
+            int rc2;
+            if (!B.mn_major) rc2 = make_tmap_f16(&tbp, B.ptr, p.K, p.N, B.ld, 128);
+            else rc2 = make_tmap_f16(&tbp, B.ptr, p.N, p.K, B.ld, GEMM_BK);
+            if (rc2) return rc2;
+            static bool attr_done = false;
+            if (!attr_done) {
+                if (cudaFuncSetAttribute(gemm_f16_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GP_SMEM_BYTES) != cudaSuccess)
+                    return -5;
+                attr_done = true;
+            }
+            const int grid = 2 * (pair_tiles < clusters ? pair_tiles : clusters);
+            ProfScope ps(PROF_GEMM, st, p.M, p.N, p.K);
+            note_launch();
+            gemm_f16_pair_kernel<<<grid, GEMM_THREADS, GP_SMEM_BYTES, st>>>(ta, tbp, p);
+            return cudaGetLastError() == cudaSuccess ? 0 : -5;
+        }
     }
     // tail split (gemm.h tail_ws): the r tiles of a partial last wave, each split St ways over K,
     // so the wave's idle SMs take a share (BLSTM_GEMM_TAIL=0: off)

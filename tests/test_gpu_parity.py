@@ -20,7 +20,9 @@ from tests.gpu_util import (GRAD_TOL, OUT_TOL, Stack, T_, compare_layer, dev, gr
 # ----------------------------------------------------------------------------
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (300, 200, 130), (20250 // 50, 1501, 1024), (64, 40, 8),
-                                   (1000, 2048, 512)])
+                                   (1000, 2048, 512),
+                                   # >= 74 tiles of 256 x 256: the CTA-pair kernel (M and N tails; exact)
+                                   (4000, 1200, 320), (4096, 1280, 256)])
 def test_gemm_tcgen05_matches_torch(a_mn, b_mn, M, N, K):
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N * 3 + K)
     A = torch.randn(M, K, generator=g).half()
