@@ -387,7 +387,8 @@ constexpr int GP_STAGES = 6;
 constexpr int GP_A_BYTES = GEMM_BM * GEMM_BK * 2;           // 16 KB: this CTA's 128 rows of A
 constexpr int GP_B_BYTES = 128 * GEMM_BK * 2;               // 16 KB: this CTA's 128 columns of B
 constexpr int GP_STAGE_BYTES = GP_A_BYTES + GP_B_BYTES;
-constexpr int GP_SMEM_BYTES = GP_STAGES * GP_STAGE_BYTES + 1024 + 256 + GEMM_EPI_WARPS * 4096;
+// [stages][barriers, 1 KB][store staging: 8 warps x 4 KB, 1024-aligned for the SW128 TMA stores]
+constexpr int GP_SMEM_BYTES = GP_STAGES * GP_STAGE_BYTES + 1024 + 1024 + GEMM_EPI_WARPS * 4096;
 
 DEVI void tma_load_2d_pair(void *dst, const CUtensorMap *m, uint32_t bar_cluster, int c0, int c1) {
     asm volatile(
@@ -408,7 +409,8 @@ DEVI void mbar_remote_arrive_release(uint32_t bar_cluster) {
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
-    gemm_f16_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+    gemm_f16_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmC, GemmParams p, int tma_store) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *full = (uint64_t *)(smem + GP_STAGES * GP_STAGE_BYTES);
@@ -517,7 +519,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const int q = warp & 3;
         const int row_in_tile = q * 32 + lane_id();
         const int chalf = (warp - 2) / 4;
-        float4 *stg4 = reinterpret_cast<float4 *>(tmem_slot + 4) + (warp - 2) * 256;
+        // (1024-aligned: the SW128 layout of a [32 rows][32 fp32] box, chunk k of row r at k ^ (r & 7))
+        float4 *stg4 = reinterpret_cast<float4 *>(smem + GP_STAGES * GP_STAGE_BYTES + 1024) + (warp - 2) * 256;
         const int lane = lane_id();
         const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
         int acc = 0;
@@ -553,6 +556,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                 tmem_ld_wait();
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = v[j] * p.alpha + bv[j];
+                if (tma_store) {  // the staged [32 x 32] box leaves by one TMA store (bounds clipped by TMA)
+                    if (lane == 0) bulk_wait_read<0>();  // the previous box has been read out
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        stg4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                reinterpret_cast<uint64_t>(&tmC)),
+                            "r"(n), "r"(m0 + 32 * q), "r"(smem_u32(stg4))
+                            : "memory");
+                        bulk_commit();
+                    }
+                    continue;
+                }
                 if ((p.ldc & 3) == 0 && ((uintptr_t)p.C & 15) == 0) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
@@ -590,6 +611,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
+    if (tma_store && warp >= 2 && lane_id() == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // no remote arrive / complete_tx / MMA into this CTA is outstanding
@@ -920,9 +942,15 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
                 attr_done = true;
             }
             const int grid = 2 * (pair_tiles < clusters ? pair_tiles : clusters);
+            // TMA stores of the output (plain overwrite of a 16-byte-aligned fp32 C; BLSTM_GEMM_TMA_STORE=0: off)
+            static const bool tstore_env = !(getenv("BLSTM_GEMM_TMA_STORE") && getenv("BLSTM_GEMM_TMA_STORE")[0] == '0');
+            CUtensorMap tmc;
+            int tma_store = 0;
+            if (tstore_env && !p.beta && make_tmap_f32_rows(&tmc, p.C, p.N, p.M, p.ldc, 32) == 0) tma_store = 1;
+            else tmc = tbp;  // (unused)
             ProfScope ps(PROF_GEMM, st, p.M, p.N, p.K);
             note_launch();
-            gemm_f16_pair_kernel<<<grid, GEMM_THREADS, GP_SMEM_BYTES, st>>>(ta, tbp, p);
+            gemm_f16_pair_kernel<<<grid, GEMM_THREADS, GP_SMEM_BYTES, st>>>(ta, tbp, tmc, p, tma_store);
             return cudaGetLastError() == cudaSuccess ? 0 : -5;
         }
     }
