@@ -424,8 +424,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     const int r = (int)cluster_ctarank();
     const int num_mp = (p.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM);
     const int num_n = (p.N + BN - 1) / BN;
-    const int num_items = num_mp * num_n;
+    const int num_tiles = num_mp * num_n;
+    const int ks = p.ksplit > 1 ? p.ksplit : 1;  // split-K: item = (split, tile); partials at split * split_stride
+    const int num_items = num_tiles * ks;
     const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+    const int kbs = (num_kb + ks - 1) / ks;
     const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (warp == 0 && lane_id() == 0) {
@@ -457,9 +460,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int item = cl; item < num_items; item += ncl) {
-                const int mp = item / num_n, nt = item - mp * num_n;
+                const int split = item / num_tiles, tile = item - split * num_tiles;
+                const int mp = tile / num_n, nt = tile - mp * num_n;
                 const int m0 = mp * 2 * GEMM_BM + r * GEMM_BM, n0 = nt * BN + r * 128;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                const int kb1 = min(num_kb, (split + 1) * kbs);
+                for (int kb = split * kbs; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t *sa = smem + stage * GP_STAGE_BYTES;
                     uint8_t *sb = sa + GP_A_BYTES;
@@ -492,10 +497,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int item = cl; item < num_items; item += ncl) {
+                const int split = item / num_tiles;
+                const int kb0 = split * kbs, kb1 = min(num_kb, (split + 1) * kbs);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + stage * GP_STAGE_BYTES);
@@ -504,10 +511,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                     for (int kk = 0; kk < GEMM_BK / 16; ++kk) {
                         const uint64_t ad = a_mn ? sdesc_sw128(sa + kk * 2048, 8192, 1024) : sdesc_sw128(sa + kk * 32, 16, 1024);
                         const uint64_t bd = b_mn ? sdesc_sw128(sb + kk * 2048, 8192, 1024) : sdesc_sw128(sb + kk * 32, 16, 1024);
-                        mma_f16_ss2_w(d_tmem, ad, bd, idesc, (kb != 0) | (kk != 0));
+                        mma_f16_ss2_w(d_tmem, ad, bd, idesc, (kb != kb0) | (kk != 0));
                     }
                     mma_commit2_w(&empty[stage], (uint16_t)3);
-                    if (kb == num_kb - 1) mma_commit2_w(&tfull[acc], (uint16_t)3);
+                    if (kb == kb1 - 1) mma_commit2_w(&tfull[acc], (uint16_t)3);
                     __syncwarp();
                     if (++stage == GP_STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -526,12 +533,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int item = cl; item < num_items; item += ncl) {
-            const int mp = item / num_n, nt = item - mp * num_n;
+            const int split = item / num_tiles, tile = item - split * num_tiles;
+            const int mp = tile / num_n, nt = tile - mp * num_n;
             const int m0 = mp * 2 * GEMM_BM + r * GEMM_BM, n0 = nt * BN;
+            float *Cb = p.C + split * p.split_stride;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int m = m0 + row_in_tile;
-            float *crow = p.C + (size_t)m * p.ldc;
+            float *crow = Cb + (size_t)m * p.ldc;
 #pragma unroll 1
             for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
                 float v[32];
@@ -574,7 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                     }
                     continue;
                 }
-                if ((p.ldc & 3) == 0 && ((uintptr_t)p.C & 15) == 0) {
+                if ((p.ldc & 3) == 0 && ((uintptr_t)Cb & 15) == 0) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
                         stg4[lane * 8 + (k ^ (lane & 7))] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
@@ -585,7 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                         float4 o = stg4[rr * 8 + (k ^ (rr & 7))];
                         const int mm = m0 + 32 * q + rr, nn = n + 4 * k;
                         if (mm < p.M && nn < p.N) {
-                            float *dst = p.C + (size_t)mm * p.ldc + nn;
+                            float *dst = Cb + (size_t)mm * p.ldc + nn;
                             if (nn + 4 <= p.N) {
                                 if (p.beta) {
                                     const float4 old = *reinterpret_cast<const float4 *>(dst);
@@ -854,6 +863,23 @@ int gemm_grid(int M, int N, int bn, int max_ctas) {
     return tiles < max_ctas ? (tiles < 1 ? 1 : tiles) : max_ctas;
 }
 
+// the fixed-order reduction of S split-K partials (splitk_ws) into C or the scatter destination
+static int splitk_finish(const GemmParams &p, int S, cudaStream_t st) {
+    const long n = (long)p.M * p.N;
+    long g = (n + 255) / 256;
+    if (g > 148 * 8) g = 148 * 8;
+    if (p.scat.dst) {
+        long tiles32 = (long)((p.M + 31) / 32) * ((p.N + 31) / 32);
+        splitk_scatter_kernel<<<(int)(tiles32 < 148 * 8 ? tiles32 : 148 * 8), 256, 0, st>>>(
+            p.splitk_ws, S, (long)p.M * p.N, p.M, p.N, p.alpha, p.scat);
+    } else {
+        splitk_reduce_kernel<<<(int)g, 256, 0, st>>>(p.splitk_ws, S, (long)p.M * p.N, p.M, p.N, p.C, p.ldc, p.alpha,
+                                                    p.beta, p.bias, p.scat);
+    }
+    note_launch();
+    return cudaGetLastError() == cudaSuccess ? 0 : -5;
+}
+
 // C = alpha * op(A) op(B)^T (+C) (+bias).  Returns 0 / negative error.
 int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, int max_ctas, cudaStream_t st) {
     GemmParams p = pin;
@@ -923,12 +949,13 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
     }
     // CTA pairs (gemm_f16_pair_kernel): plain GEMMs with at least a wave of 256 x 256 tiles;
     // BLSTM_GEMM_PAIR=0: off
+    // (split-K GEMMs too: their partial tiles are plain rows of splitk_ws, reduced below)
     static const bool pair_env = !(getenv("BLSTM_GEMM_PAIR") && getenv("BLSTM_GEMM_PAIR")[0] == '0');
-    if (pair_env && S == 1 && BN == 256 && !p.natB && !p.flags && !p.a2 && !p.scat.dst && !p.pdl && !p.pdl_chain &&
+    if (pair_env && BN == 256 && !p.natB && !p.flags && !p.a2 && (S > 1 || !p.scat.dst) && !p.pdl && !p.pdl_chain &&
         !p.arb && p.partials == 0 && p.a_kwrap == 0 && p.nbatch == 1 && max_ctas >= 2) {
         const int pair_tiles = ((p.M + 2 * GEMM_BM - 1) / (2 * GEMM_BM)) * ((p.N + 255) / 256);
         const int clusters = max_ctas / 2;
-        if (pair_tiles >= clusters) {
+        if ((long)pair_tiles * S >= clusters) {
             CUtensorMap tbp;
             int rc2;
             if (!B.mn_major) rc2 = make_tmap_f16(&tbp, B.ptr, p.K, p.N, B.ld, 128);
@@ -946,12 +973,19 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
             static const bool tstore_env = !(getenv("BLSTM_GEMM_TMA_STORE") && getenv("BLSTM_GEMM_TMA_STORE")[0] == '0');
             CUtensorMap tmc;
             int tma_store = 0;
-            if (tstore_env && !p.beta && make_tmap_f32_rows(&tmc, p.C, p.N, p.M, p.ldc, 32) == 0) tma_store = 1;
+            // (not for split-K partials: rows past M of one split are the next split's rows)
+            if (tstore_env && S == 1 && !q.beta && make_tmap_f32_rows(&tmc, q.C, q.N, q.M, q.ldc, 32) == 0) tma_store = 1;
             else tmc = tbp;  // (unused)
-            ProfScope ps(PROF_GEMM, st, p.M, p.N, p.K);
-            note_launch();
-            gemm_f16_pair_kernel<<<grid, GEMM_THREADS, GP_SMEM_BYTES, st>>>(ta, tbp, tmc, p, tma_store);
-            return cudaGetLastError() == cudaSuccess ? 0 : -5;
+            const int gridp = 2 * ((long)pair_tiles * S < clusters ? pair_tiles * S : clusters);
+            {
+                ProfScope ps(PROF_GEMM, st, p.M, p.N, p.K);
+                note_launch();
+                gemm_f16_pair_kernel<<<gridp, GEMM_THREADS, GP_SMEM_BYTES, st>>>(ta, tbp, tmc, q, tma_store);
+                if (cudaGetLastError() != cudaSuccess) return -5;
+            }
+            (void)grid;
+            if (S == 1) return 0;
+            return splitk_finish(p, S, st);
         }
     }
     // tail split (gemm.h tail_ws): the r tiles of a partial last wave, each split St ways over K,
@@ -984,21 +1018,7 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
         note_launch();
         if (cudaGetLastError() != cudaSuccess) return -5;
     }
-    if (S > 1) {
-        const long n = (long)p.M * p.N;
-        long g = (n + 255) / 256;
-        if (g > 148 * 8) g = 148 * 8;
-        if (p.scat.dst) {
-            long tiles32 = (long)((p.M + 31) / 32) * ((p.N + 31) / 32);
-            splitk_scatter_kernel<<<(int)(tiles32 < 148 * 8 ? tiles32 : 148 * 8), 256, 0, st>>>(
-                p.splitk_ws, S, (long)p.M * p.N, p.M, p.N, p.alpha, p.scat);
-        } else {
-            splitk_reduce_kernel<<<(int)g, 256, 0, st>>>(p.splitk_ws, S, (long)p.M * p.N, p.M, p.N, p.C, p.ldc, p.alpha,
-                                                        p.beta, p.bias, p.scat);
-        }
-        note_launch();
-        if (cudaGetLastError() != cudaSuccess) return -5;
-    }
+    if (S > 1) return splitk_finish(p, S, st);
     return 0;
 }
 
