@@ -697,15 +697,18 @@ int num_sms() {
 
 template <int BN>
 static cudaError_t gemm_setup() {
-    static bool done = false;
-    if (!done) {
+    static bool done[64] = {};  // per device: a function attribute is set per context
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!done[dev]) {
         cudaError_t e = cudaFuncSetAttribute(gemm_f16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              GemmCfg<BN>::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         cudaFuncAttributes a;
         e = cudaFuncGetAttributes(&a, gemm_f16_kernel<BN>);  // forces the (lazy) module load
         if (e != cudaSuccess) return e;
-        done = true;
+        done[dev] = true;
     }
     return cudaSuccess;
 }
@@ -961,12 +964,15 @@ int gemm_f16(const GemmOperand &A, const GemmOperand &B, const GemmParams &pin, 
             if (!B.mn_major) rc2 = make_tmap_f16(&tbp, B.ptr, p.K, p.N, B.ld, 128);
             else rc2 = make_tmap_f16(&tbp, B.ptr, p.N, p.K, B.ld, GEMM_BK);
             if (rc2) return rc2;
-            static bool attr_done = false;
-            if (!attr_done) {
+            static bool attr_done[64] = {};  // per device
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev < 0 || dev >= 64) dev = 0;
+            if (!attr_done[dev]) {
                 if (cudaFuncSetAttribute(gemm_f16_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          GP_SMEM_BYTES) != cudaSuccess)
                     return -5;
-                attr_done = true;
+                attr_done[dev] = true;
             }
             const int grid = 2 * (pair_tiles < clusters ? pair_tiles : clusters);
             // TMA stores of the output (plain overwrite of a 16-byte-aligned fp32 C; BLSTM_GEMM_TMA_STORE=0: off)
