@@ -337,7 +337,9 @@ int mdlstm_bwd(const mdlstm_desc *d, const float *theta, const float *x, const u
 /* ------------------------------------------------------------------------ */
 /* C[m,n] = alpha * sum_k A(m,k) B(n,k) (+ C[m,n] if beta) (+ bias[n]), A and B fp16
  * DEVICE (16-byte aligned, ld a multiple of 8), each K-major (element (r,k) at
- * ptr[r*ld + k], *_mn = 0) or MN-major (at ptr[k*ld + r], *_mn = 1); C fp32. */
+ * ptr[r*ld + k], *_mn = 0) or MN-major (at ptr[k*ld + r], *_mn = 1); C fp32.  The same kernels
+ * the stack runs: split-K over a long K, CTA-pair tiles and tail-wave splits, with a
+ * library-owned scratch per device (288 MB, allocated on the first call). */
 int blstm_gemm_f16(int M, int N, int K, const void *A, long lda, int a_mn, const void *B, long ldb, int b_mn,
                    float *C, long ldc, float alpha, int beta, const float *bias, void *stream);
 

@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <vector>
 
 #include "blstm.h"
@@ -1243,6 +1244,29 @@ extern "C" int blstm_gemm_f16(int M, int N, int K, const void *A, long lda, int 
     if (!A || !B || !C || M < 0 || N < 0 || K < 1) return fail(BLSTM_ERR_ARG, "blstm_gemm_f16: bad argument");
     if (!al16(A) || !al16(B) || (lda & 7) || (ldb & 7)) return fail(BLSTM_ERR_ALIGN, "A/B must be 16-byte aligned, ld % 8 == 0");
     GemmParams gp{M, N, K, C, ldc, alpha, beta, bias, 0, 0};
+    // the same split-K and tail-wave scratch the stack gives its GEMMs (library-owned, per device,
+    // allocated on first use), so the hook times and tests the kernels the stack runs
+    static std::mutex mu;
+    static std::map<int, std::pair<float *, float *>> scratch;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(BLSTM_ERR_CUDA, "cudaGetDevice");
+    std::pair<float *, float *> sc{nullptr, nullptr};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = scratch.find(dev);
+        if (it == scratch.end()) {
+            float *a = nullptr, *b = nullptr;
+            if (cudaMalloc(&a, (size_t)GSK_ELEMS * 4) != cudaSuccess ||
+                cudaMalloc(&b, (size_t)gemm_tail_elems() * 4) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(BLSTM_ERR_CUDA, "blstm_gemm_f16: scratch allocation");
+            }
+            it = scratch.emplace(dev, std::make_pair(a, b)).first;
+        }
+        sc = it->second;
+    }
+    gp.splitk_ws = sc.first; gp.splitk_elems = GSK_ELEMS;
+    gp.tail_ws = sc.second; gp.tail_elems = gemm_tail_elems();
     TRY(gemm_f16({A, lda, a_mn}, {B, ldb, b_mn}, gp, 0, (cudaStream_t)stream), "gemm");
     return 0;
 }

@@ -22,14 +22,18 @@ from tests.gpu_util import (GRAD_TOL, OUT_TOL, Stack, T_, compare_layer, dev, gr
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (300, 200, 130), (20250 // 50, 1501, 1024), (64, 40, 8),
                                    (1000, 2048, 512),
                                    # >= 74 tiles of 256 x 256: the CTA-pair kernel (M and N tails; exact)
-                                   (4000, 1200, 320), (4096, 1280, 256)])
+                                   (4000, 1200, 320), (4096, 1280, 256),
+                                   # long K: split-K on the single-CTA kernel, and on the pair kernel
+                                   (500, 300, 8192), (4096, 1000, 12288)])
 def test_gemm_tcgen05_matches_torch(a_mn, b_mn, M, N, K):
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N * 3 + K)
     A = torch.randn(M, K, generator=g).half()
     Bm = torch.randn(N, K, generator=g).half()
-    ref = A.float() @ Bm.float().T
+    ref = (A.double() @ Bm.double().T).float()  # exact products, fp64 sums
     bias = torch.randn(N, generator=g)
     ref_b = 0.5 * ref + bias
+    # fp32 accumulation over K terms (any order: TMEM, split-K partials): error ~ sqrt(K) ulps
+    tol = 1e-5 * max(1.0, (K / 1024) ** 0.5)
     def padded(X):  # row stride a multiple of 8 elements (TMA: 16-byte strides)
         r, c = X.shape
         buf = torch.zeros(r, (c + 7) // 8 * 8, dtype=X.dtype)
@@ -42,12 +46,12 @@ def test_gemm_tcgen05_matches_torch(a_mn, b_mn, M, N, K):
     blstm.blstm_gemm_f16(Ad, a_mn, Bd, b_mn, C, M, N, K, alpha=0.5, bias=bias.to(dev()))
     torch.cuda.synchronize()
     err = (C.cpu() - ref_b).abs().max().item() / ref_b.abs().max().item()
-    assert err < 1e-5, err
+    assert err < tol, err
     # beta accumulate
     blstm.blstm_gemm_f16(Ad, a_mn, Bd, b_mn, C, M, N, K, alpha=1.0, beta=1)
     torch.cuda.synchronize()
     err2 = (C.cpu() - (ref_b + ref)).abs().max().item() / (ref_b + ref).abs().max().item()
-    assert err2 < 1e-5, err2
+    assert err2 < tol, err2
 
 
 # ----------------------------------------------------------------------------
